@@ -1,0 +1,198 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Compiles the UNMODIFIED reference headers where they lie
+// (/root/reference/proj/include, header-only C++20) into oracle/_ref/libappo_ref.so
+// and exposes the hot-path functions with a C ABI so the tests can
+//   (1) pin the oracle restatement (oracle/appo_oracle.c) against the real
+//       reference, and
+//   (2) generate the golden vectors committed under tests/golden/.
+// bench.py --impl reference also times these functions as the reference CPU
+// path.  No reference source is copied into this repository; this file only
+// includes the headers and forwards arguments.
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "appo/offpolicy.hpp"
+#include "appo/policy.hpp"
+#include "appo/trajstore.hpp"
+
+using namespace appo;
+
+namespace {
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ContractError&) {
+    return 1;
+  } catch (const ConfigError&) {
+    return 2;
+  } catch (const NumericError&) {
+    return 3;
+  } catch (...) {
+    return 4;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+// offpolicy.hpp:139 vtrace
+int ref_vtrace(int T, const double* r, const double* v, double boot, const double* tl,
+               const double* bl, const std::uint8_t* d, double rho_bar, double c_bar, double gamma,
+               double* v_out, double* pg_out, double* rho_out, double* c_out) {
+  return guarded([&] {
+    auto o = vtrace({r, (size_t)T}, {v, (size_t)T}, boot, {tl, (size_t)T}, {bl, (size_t)T},
+                    {d, (size_t)T}, VTraceConfig{rho_bar, c_bar, gamma});
+    std::memcpy(v_out, o.v.data(), sizeof(double) * T);
+    std::memcpy(pg_out, o.pg_adv.data(), sizeof(double) * T);
+    if (rho_out) std::memcpy(rho_out, o.rho.data(), sizeof(double) * T);
+    if (c_out) std::memcpy(c_out, o.c.data(), sizeof(double) * T);
+  });
+}
+
+// Batched [n_traj x T] driver used for CPU-baseline timing; trajectories
+// [lo, hi) only, so the caller can partition across threads.
+int ref_vtrace_range(int lo, int hi, int T, const double* r, const double* v, const double* boot,
+                     const double* tl, const double* bl, const std::uint8_t* d, double rho_bar,
+                     double c_bar, double gamma, double* v_out, double* pg_out) {
+  return guarded([&] {
+    for (int i = lo; i < hi; ++i) {
+      const size_t o = (size_t)i * T;
+      auto out = vtrace({r + o, (size_t)T}, {v + o, (size_t)T}, boot[i], {tl + o, (size_t)T},
+                        {bl + o, (size_t)T}, {d + o, (size_t)T},
+                        VTraceConfig{rho_bar, c_bar, gamma});
+      std::memcpy(v_out + o, out.v.data(), sizeof(double) * T);
+      std::memcpy(pg_out + o, out.pg_adv.data(), sizeof(double) * T);
+    }
+  });
+}
+
+// offpolicy.hpp:182 nstep_returns
+void ref_nstep_returns(int T, const double* r, double boot, const std::uint8_t* d, double gamma,
+                       double* ret) {
+  auto o = nstep_returns({r, (size_t)T}, boot, {d, (size_t)T}, gamma);
+  std::memcpy(ret, o.data(), sizeof(double) * T);
+}
+
+// offpolicy.hpp:195 / :202
+double ref_ppo_objective(double ratio, double adv, double lo, double hi) {
+  ClipConfig c{lo, hi};
+  return ppo_clip_objective(ratio, adv, c);
+}
+double ref_ppo_dratio(double ratio, double adv, double lo, double hi) {
+  ClipConfig c{lo, hi};
+  return ppo_clip_dratio(ratio, adv, c);
+}
+double ref_importance_ratio(double t, double b) { return importance_ratio(t, b); }
+
+// offpolicy.hpp:224 total_loss ; out = policy, value, entropy, total
+int ref_total_loss(int n, const double* ratios, const double* adv, const double* values,
+                   const double* vt, const double* ent, double lo, double hi, double value_coef,
+                   double entropy_coef, double* out4) {
+  return guarded([&] {
+    LossConfig cfg;
+    cfg.clip = ClipConfig{lo, hi};
+    cfg.value_coef = value_coef;
+    cfg.entropy_coef = entropy_coef;
+    auto o = total_loss({ratios, (size_t)n}, {adv, (size_t)n}, {values, (size_t)n},
+                        {vt, (size_t)n}, {ent, (size_t)n}, cfg);
+    out4[0] = o.policy;
+    out4[1] = o.value;
+    out4[2] = o.entropy;
+    out4[3] = o.total;
+  });
+}
+
+// policy.hpp:214 softmax_heads / :262 log_prob_and_entropy, single head {n}
+void ref_softmax(int n, const double* logits, double* probs) {
+  ActionHeadsSpec h;
+  h.sizes = {n};
+  softmax_heads(h, {logits, (size_t)n}, {probs, (size_t)n});
+}
+int ref_log_prob_entropy(int n, const double* logits, int action, double* logp, double* ent) {
+  return guarded([&] {
+    ActionHeadsSpec h;
+    h.sizes = {n};
+    auto [lp, e] = log_prob_and_entropy(h, {logits, (size_t)n}, FactoredAction{action});
+    *logp = lp;
+    *ent = e;
+  });
+}
+
+// policy.hpp:232 sample_action, `count` draws from one mt19937_64(seed)
+void ref_sample_actions(int n, const double* logits, std::uint64_t seed, int count, int* actions,
+                        double* logps) {
+  ActionHeadsSpec h;
+  h.sizes = {n};
+  std::mt19937_64 rng(seed);
+  for (int i = 0; i < count; ++i) {
+    auto [a, lp] = sample_action(h, {logits, (size_t)n}, rng);
+    actions[i] = a[0];
+    logps[i] = lp;
+  }
+}
+
+// policy.hpp:431 optimizer_step on a raw vector (shape-free: a ModelShape
+// whose n_params() equals n is not needed because optimizer_step only uses
+// theta/m/v sizes).
+int ref_optimizer_step(long n, double* theta, double* m, double* v, const double* g, long* t,
+                       double lr, double b1, double b2, double eps, double clip) {
+  return guarded([&] {
+    PolicyParams p;
+    p.theta.assign(theta, theta + n);
+    p.adam.m.assign(m, m + n);
+    p.adam.v.assign(v, v + n);
+    p.adam.t = *t;
+    AdamConfig cfg;
+    cfg.lr = lr;
+    cfg.beta1 = b1;
+    cfg.beta2 = b2;
+    cfg.eps = eps;
+    cfg.grad_clip = clip;
+    optimizer_step(p, {g, (size_t)n}, cfg);
+    std::memcpy(theta, p.theta.data(), sizeof(double) * n);
+    std::memcpy(m, p.adam.m.data(), sizeof(double) * n);
+    std::memcpy(v, p.adam.v.data(), sizeof(double) * n);
+    *t = p.adam.t;
+  });
+}
+
+// trajstore.hpp:62 traj_layout::Offsets (reference f64 element types)
+void ref_slot_offsets(std::uint32_t T, std::uint32_t obs_dim, std::uint32_t hidden_dim,
+                      std::uint32_t n_heads, std::uint64_t* out) {
+  TrajectoryShape s{T, obs_dim, hidden_dim, n_heads};
+  traj_layout::Offsets o(s);
+  const std::size_t v[10] = {o.obs,      o.hidden,   o.actions,  o.rewards,     o.logp,
+                             o.dones,    o.versions, o.boot_obs, o.boot_hidden, o.total};
+  for (int i = 0; i < 10; ++i) out[i] = v[i];
+}
+
+// acceptance.cpp:42-56 / test_offpolicy.cpp:20-34 instance generator,
+// reproduced bit-for-bit by driving the same std distributions from the
+// same engine.  Writes T values per array; `state` carries the engine.
+void* ref_rng_new(std::uint64_t seed) { return new std::mt19937_64(seed); }
+void ref_rng_free(void* p) { delete static_cast<std::mt19937_64*>(p); }
+void ref_random_instance(void* state, int T, double done_prob, double* r, double* v, double* tl,
+                         double* bl, std::uint8_t* d, double* boot) {
+  auto& rng = *static_cast<std::mt19937_64*>(state);
+  std::uniform_real_distribution<double> ur(-1.0, 1.0);
+  std::uniform_real_distribution<double> lp(-2.5, -0.1);
+  std::bernoulli_distribution bd(done_prob);
+  for (int t = 0; t < T; ++t) {
+    r[t] = ur(rng);
+    v[t] = ur(rng);
+    tl[t] = lp(rng);
+    bl[t] = lp(rng);
+    d[t] = bd(rng) ? 1 : 0;
+  }
+  *boot = ur(rng);
+}
+
+std::uint64_t ref_splitmix64(std::uint64_t x) { return splitmix64(x); }
+std::uint64_t ref_derive_seed(std::uint64_t s, std::uint64_t k) { return derive_seed(s, k); }
+std::uint64_t ref_fnv1a64(const void* p, std::size_t n) { return fnv1a64(p, n); }
+
+}  // extern "C"
