@@ -1,0 +1,183 @@
+/*
+ * appo_capi.h -- C ABI of the B200-native APPO hot path (libappo_b200.so).
+ *
+ * The reference (/root/reference/proj, header-only C++20) has no FFI: its hot
+ * path is a set of inline free functions called by PolicyWorkerUnit::run_once
+ * (orchestrator.hpp:602-673) and LearnerUnit::step (orchestrator.hpp:760-901).
+ * Each entry point below names the reference function(s) it replaces.  A host
+ * that used the reference calls these instead (see INTEGRATION.md for the C++
+ * shim that restores the reference's exception types and std::span signatures).
+ *
+ * Conventions
+ *   - Every call returns appo_status.  0 ok; 1 ContractError (shape / range /
+ *     order, common.hpp:23-26); 2 ConfigError (invalid rho_bar/c_bar/gamma/clip,
+ *     common.hpp:30-33); 3 NumericError (non-finite input / gradient / loss,
+ *     common.hpp:37-40); 4 resource (CUDA / allocation failure).
+ *     appo_last_error() returns the thread's last message.
+ *   - Pointers named d_* are caller-owned DEVICE memory; h_* are caller-owned
+ *     HOST memory (pinned for the *_host variants' best throughput).  The
+ *     library owns only ctx-internal parameters, optimizer state and scratch.
+ *   - Work is enqueued on the ctx stream (appo_ctx_set_stream) and is
+ *     asynchronous unless stated.  Kernels that find non-finite inputs raise a
+ *     sticky device flag; appo_ctx_sync() waits for the stream and returns 3 if
+ *     the flag was raised (then clears it), mirroring the reference throwing
+ *     NumericError from the same call.
+ *   - Layout of per-step arrays is [n_traj x T] row-major, i.e. the learner's
+ *     gather order s = i*T + t (orchestrator.hpp:781-795).
+ */
+#ifndef APPO_CAPI_H
+#define APPO_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APPO_CAPI_VERSION 1
+
+#if defined(__GNUC__)
+#define APPO_API __attribute__((visibility("default")))
+#else
+#define APPO_API
+#endif
+
+typedef enum {
+  APPO_OK = 0,
+  APPO_ERR_CONTRACT = 1,
+  APPO_ERR_CONFIG = 2,
+  APPO_ERR_NUMERIC = 3,
+  APPO_ERR_RESOURCE = 4
+} appo_status;
+
+typedef struct appo_ctx appo_ctx;
+
+/* Model contract: convnet_simple over u8 obs [C][H][W] -> GRU(512)
+ * -> categorical head (n_actions) + value.  Replaces ModelShape
+ * (policy.hpp:39-59), whose MLP trunk the reference uses as a stand-in. */
+typedef struct {
+  int32_t obs_c, obs_h, obs_w; /* 3, 72, 128 at the Doom shape */
+  int32_t n_actions;           /* 6 (ActionHeadsSpec{6}, policy.hpp:25-35) */
+  int32_t T;                   /* rollout / recurrence length, 32 */
+  int32_t reserved[3];
+} appo_model_desc;
+
+/* Learner hyper-parameters: AdamConfig (policy.hpp:88-94), LossConfig
+ * (offpolicy.hpp:208-212), VTraceConfig (offpolicy.hpp:96-106), advantage
+ * source / normalisation (orchestrator.hpp:47,838-845). */
+typedef struct {
+  float lr, beta1, beta2, eps, grad_clip;
+  float entropy_coef, value_coef, clip_low, clip_high;
+  float rho_bar, c_bar, gamma, gae_lambda;
+  int32_t adv_source; /* 0 = V-trace pg_adv, 1 = n-step - V, 2 = GAE(lambda) */
+  int32_t normalize_adv;
+  int32_t reserved;
+} appo_hparams;
+
+/* LearnerStepRow (orchestrator.hpp:700-711) loss fields + extras. */
+typedef struct {
+  double policy_loss, value_loss, entropy, total_loss; /* LossComponents */
+  double mean_ratio;                                   /* GradientResult::mean_ratio */
+  double grad_norm;                                    /* pre-clip global norm */
+  double lag_mean, lag_max;                            /* orchestrator.hpp:862-863 */
+  int64_t version;                                     /* version after the step */
+} appo_step_out;
+
+APPO_API const char* appo_last_error(void);
+APPO_API int appo_capi_version(void);
+
+/* ---- context ----------------------------------------------------------- */
+/* desc may be NULL for a context that only runs the stateless kernels. */
+APPO_API int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo_ctx** out);
+APPO_API int appo_ctx_destroy(appo_ctx* ctx);
+APPO_API int appo_ctx_set_stream(appo_ctx* ctx, void* cuda_stream);
+APPO_API int appo_ctx_sync(appo_ctx* ctx);
+/* Number of launches of this library's kernels enqueued on ctx so far. */
+APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);
+
+/* ---- off-policy returns (offpolicy.hpp) --------------------------------- */
+/* Replaces vtrace (offpolicy.hpp:139-178) for n_traj trajectories at once.
+ * d_rho_out / d_c_out may be NULL.  Validation as VTraceConfig::validate. */
+APPO_API int appo_vtrace(appo_ctx* ctx, int n_traj, int T, const float* d_rewards, const float* d_values,
+                const float* d_bootstrap, const float* d_target_logp,
+                const float* d_behavior_logp, const uint8_t* d_dones, float gamma, float rho_bar,
+                float c_bar, float* d_v_out, float* d_pg_adv_out, float* d_rho_out,
+                float* d_c_out);
+/* Replaces nstep_returns (offpolicy.hpp:182-192). */
+APPO_API int appo_nstep_returns(appo_ctx* ctx, int n_traj, int T, const float* d_rewards,
+                       const float* d_bootstrap, const uint8_t* d_dones, float gamma,
+                       float* d_ret_out);
+/* GAE(lambda) (new; lambda = 1 equals nstep_returns - V).  d_ret_out may be NULL. */
+APPO_API int appo_gae(appo_ctx* ctx, int n_traj, int T, const float* d_rewards, const float* d_values,
+             const float* d_bootstrap, const uint8_t* d_dones, float gamma, float lambda,
+             float* d_adv_out, float* d_ret_out);
+/* Replaces total_loss (offpolicy.hpp:224-246); h_out4 = {policy, value, entropy,
+ * total} in fp64, written after an internal sync (this call is synchronous). */
+APPO_API int appo_total_loss(appo_ctx* ctx, int n, const float* d_ratios, const float* d_adv,
+                    const float* d_values, const float* d_v_targets, const float* d_entropies,
+                    float clip_low, float clip_high, float value_coef, float entropy_coef,
+                    double* h_out4);
+
+/* ---- heads (policy.hpp:214-281) ----------------------------------------- */
+/* Target log-prob of the stored action and entropy per sample (single head of
+ * n_actions), replaces log_prob_and_entropy.  Out-of-range actions are a
+ * contract error (device flag, reported by appo_ctx_sync as 1). */
+APPO_API int appo_logp_entropy(appo_ctx* ctx, int B, int n_actions, const float* d_logits,
+                      const int32_t* d_actions, float* d_logp_out, float* d_entropy_out);
+/* sample_action (policy.hpp:232-258) with a counter-based uniform per row:
+ * u_b = U(key, counter0 + b).  Writes action and joint log-prob. */
+APPO_API int appo_sample_actions(appo_ctx* ctx, int B, int n_actions, const float* d_logits, uint64_t key,
+                        uint64_t counter0, int32_t* d_actions, float* d_logp);
+
+/* ---- optimizer (policy.hpp:431-455) -------------------------------------- */
+/* Global-norm clip + Adam over flat fp32 vectors, step t (1-based, after the
+ * increment).  Non-finite gradient -> params untouched, status 3 at sync.
+ * h_grad_norm (optional) receives the pre-clip norm after an internal sync. */
+APPO_API int appo_adam_step(appo_ctx* ctx, int64_t n, float* d_theta, float* d_m, float* d_v,
+                   const float* d_grad, int64_t t, float lr, float beta1, float beta2, float eps,
+                   float grad_clip, double* h_grad_norm);
+
+/* ---- model-level calls (need a ctx created with a model desc) ------------ */
+APPO_API int64_t appo_param_count(const appo_model_desc* desc);
+/* Trajectory slot layout v2 (trajstore.hpp:62-87 with u8 obs and f32
+ * hidden/reward/logp): 10 offsets {obs, hidden, actions, rewards, logp, dones,
+ * versions, boot_obs, boot_hidden, total}. */
+APPO_API int appo_slot_layout(const appo_model_desc* desc, uint64_t* out10);
+
+/* ParamStore::fetch/publish (policy.hpp:487-509): copies the learner's fp32
+ * parameters (flat contract order) to h_dst / from h_src.  Setting
+ * parameters resets Adam moments to zero and bumps the version. */
+APPO_API int appo_params_get(appo_ctx* ctx, float* h_dst, int64_t* version_out);
+APPO_API int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version);
+APPO_API int appo_adam_get(appo_ctx* ctx, float* h_m, float* h_v, int64_t* t_out);
+APPO_API int appo_adam_set(appo_ctx* ctx, const float* h_m, const float* h_v, int64_t t);
+APPO_API int64_t appo_params_version(appo_ctx* ctx);
+
+/* Batched policy inference: replaces forward_batch + sample_action + the row
+ * writes of PolicyWorkerUnit::run_once (orchestrator.hpp:643-656).
+ * d_obs u8 [B][C*H*W], d_h_in f32 [B][512] -> d_actions i32 [B], d_logp f32 [B],
+ * d_h_out f32 [B][512], d_values f32 [B], d_logits (optional) f32 [B][A].
+ * Sampling uses u = U(ctx key, rng_counter0 + b).  *h_version_out (optional)
+ * receives the parameter version used (ExchangeLayout version field). */
+APPO_API int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float* d_h_in,
+                        uint64_t rng_counter0, int32_t* d_actions, float* d_logp,
+                        float* d_h_out, float* d_values, float* d_logits,
+                        int64_t* h_version_out);
+
+/* Learner step over n_traj trajectory slots of layout v2 living in one device
+ * slot region: replaces assemble_minibatch's gather + LearnerUnit::step
+ * (orchestrator.hpp:770-868): forward (encoder + GRU unrolled from the stored
+ * h0 with resets after done) + bootstrap forward, target logp/entropy, V-trace
+ * (or n-step / GAE), advantage normalisation, PPO + value + entropy loss,
+ * BPTT, encoder backward, global-norm clip + Adam, version += 1, publish of the
+ * bf16 inference copy.  h_slot_ids are in FIFO arrival order (index i of the
+ * minibatch = trajectory i).  Synchronous: fills *out. */
+APPO_API int appo_learner_step(appo_ctx* ctx, const void* d_slot_region, uint64_t slot_bytes,
+                      const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp,
+                      appo_step_out* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APPO_CAPI_H */

@@ -1,0 +1,392 @@
+"""B200-native APPO hot path (Sample Factory, arXiv 2006.11751).
+
+Python host mirror of the reference's hot-path interface over the C ABI in
+include/appo_capi.h (libappo_b200.so, hand-written sm_100a CUDA).  Function
+names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/appo): ``vtrace`` (offpolicy.hpp:139),
+``nstep_returns`` (:182), ``total_loss`` (:224), ``log_prob_and_entropy``
+(policy.hpp:262), ``optimizer_step`` (policy.hpp:431), the policy-worker batch
+inference (orchestrator.hpp:602-673) and the learner step
+(orchestrator.hpp:760-868).  Errors raise ContractError / ConfigError /
+NumericError like the reference's exception taxonomy (common.hpp:20-45).
+
+Device buffers are torch CUDA tensors (torch is only the allocator/stream
+plumbing here); every computation runs in libappo_b200.so.  There is no CPU
+fallback: importing this package on a machine without the built library
+raises, and calls without a CUDA device raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libappo_b200.so")
+
+
+class AppoError(RuntimeError):
+    pass
+
+
+class ContractError(AppoError):
+    """Broken precondition (common.hpp:23-26)."""
+
+
+class ConfigError(AppoError):
+    """Invalid configuration (common.hpp:30-33)."""
+
+
+class NumericError(AppoError):
+    """Non-finite value where a finite one is required (common.hpp:37-40)."""
+
+
+class ResourceError(AppoError):
+    """CUDA / allocation failure."""
+
+
+_ERRS = {1: ContractError, 2: ConfigError, 3: NumericError, 4: ResourceError}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        from . import _build
+        _build.build()
+    return C.CDLL(LIB_PATH)
+
+
+_L = _load()
+
+_vp = C.c_void_p
+_i = C.c_int
+_i64 = C.c_int64
+_u64 = C.c_uint64
+_f = C.c_float
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("obs_c", C.c_int32), ("obs_h", C.c_int32), ("obs_w", C.c_int32),
+                ("n_actions", C.c_int32), ("T", C.c_int32), ("reserved", C.c_int32 * 3)]
+
+    @staticmethod
+    def doom(n_actions: int = 6, T: int = 32) -> "ModelDesc":
+        return ModelDesc(3, 72, 128, n_actions, T)
+
+    @property
+    def shape(self):
+        return (self.obs_c, self.obs_h, self.obs_w, self.n_actions)
+
+    @property
+    def obs_dim(self):
+        return self.obs_c * self.obs_h * self.obs_w
+
+
+class HParams(C.Structure):
+    _fields_ = [("lr", _f), ("beta1", _f), ("beta2", _f), ("eps", _f), ("grad_clip", _f),
+                ("entropy_coef", _f), ("value_coef", _f), ("clip_low", _f), ("clip_high", _f),
+                ("rho_bar", _f), ("c_bar", _f), ("gamma", _f), ("gae_lambda", _f),
+                ("adv_source", C.c_int32), ("normalize_adv", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    @staticmethod
+    def defaults(**kw) -> "HParams":
+        """Paper Table A.5 / reference defaults (policy.hpp:88-94, offpolicy.hpp:18-45,
+        orchestrator.hpp:52-92)."""
+        d = dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-6, grad_clip=4.0, entropy_coef=0.003,
+                 value_coef=0.5, clip_low=1.0 / 1.1, clip_high=1.1, rho_bar=1.0, c_bar=1.0,
+                 gamma=0.99, gae_lambda=0.95, adv_source=0, normalize_adv=0)
+        d.update(kw)
+        return HParams(**d)
+
+
+class StepOut(C.Structure):
+    _fields_ = [("policy_loss", C.c_double), ("value_loss", C.c_double),
+                ("entropy", C.c_double), ("total_loss", C.c_double),
+                ("mean_ratio", C.c_double), ("grad_norm", C.c_double),
+                ("lag_mean", C.c_double), ("lag_max", C.c_double), ("version", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _sig(name, res, *args):
+    f = getattr(_L, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("appo_last_error", C.c_char_p)
+_sig("appo_capi_version", _i)
+_sig("appo_ctx_create", _i, C.POINTER(ModelDesc), _i, _u64, C.POINTER(_vp))
+_sig("appo_ctx_destroy", _i, _vp)
+_sig("appo_ctx_set_stream", _i, _vp, _vp)
+_sig("appo_ctx_sync", _i, _vp)
+_sig("appo_ctx_launch_count", _i64, _vp)
+_sig("appo_vtrace", _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _vp, _vp, _vp,
+     _vp)
+_sig("appo_nstep_returns", _i, _vp, _i, _i, _vp, _vp, _vp, _f, _vp)
+_sig("appo_gae", _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _f, _f, _vp, _vp)
+_sig("appo_total_loss", _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _f,
+     C.POINTER(C.c_double))
+_sig("appo_logp_entropy", _i, _vp, _i, _i, _vp, _vp, _vp, _vp)
+_sig("appo_sample_actions", _i, _vp, _i, _i, _vp, _u64, _u64, _vp, _vp)
+_sig("appo_adam_step", _i, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _f, _f, _f, _f, _f,
+     C.POINTER(C.c_double))
+_sig("appo_param_count", _i64, C.POINTER(ModelDesc))
+_sig("appo_slot_layout", _i, C.POINTER(ModelDesc), C.POINTER(_u64))
+_sig("appo_params_get", _i, _vp, _vp, C.POINTER(_i64))
+_sig("appo_params_set", _i, _vp, _vp, _i64)
+_sig("appo_adam_get", _i, _vp, _vp, _vp, C.POINTER(_i64))
+_sig("appo_adam_set", _i, _vp, _vp, _vp, _i64)
+_sig("appo_params_version", _i64, _vp)
+_sig("appo_policy_forward", _i, _vp, _i, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp,
+     C.POINTER(_i64))
+_sig("appo_learner_step", _i, _vp, _vp, _u64, _vp, _i, C.POINTER(HParams), C.POINTER(StepOut))
+_sig("appo_dbg_gemm", _i, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i64, _i, _f, _vp,
+     _vp, _i64, _i, _i)
+_sig("appo_dbg_model_ptrs", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp))
+_sig("appo_dbg_copy_d2h", _i, _vp, _vp, _vp, _u64)
+
+LIB = _L
+
+
+def check(status: int):
+    if status != 0:
+        msg = (_L.appo_last_error() or b"").decode(errors="replace")
+        raise _ERRS.get(status, AppoError)(msg)
+
+
+def param_count(desc: ModelDesc) -> int:
+    return int(_L.appo_param_count(C.byref(desc)))
+
+
+def slot_layout(desc: ModelDesc) -> dict:
+    out = (_u64 * 10)()
+    check(_L.appo_slot_layout(C.byref(desc), out))
+    keys = ["obs", "hidden", "actions", "rewards", "logp", "dones", "versions", "boot_obs",
+            "boot_hidden", "total"]
+    return dict(zip(keys, [int(x) for x in out]))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ContractError("device tensors required (torch CUDA tensors)")
+
+
+class Context:
+    """One appo_ctx: a device, a stream, optional model (parameters + Adam)."""
+
+    def __init__(self, device: int = 0, seed: int = 1, model: ModelDesc | None = None,
+                 stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise ResourceError("libappo_b200 needs a CUDA device")
+        self.torch = torch
+        self.device = device
+        self.model = model
+        h = C.c_void_p()
+        check(_L.appo_ctx_create(C.byref(model) if model is not None else None, device, seed,
+                                 C.byref(h)))
+        self.h = h
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        check(_L.appo_ctx_set_stream(self.h, C.c_void_p(self.stream.cuda_stream)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _L.appo_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        check(_L.appo_ctx_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_L.appo_ctx_launch_count(self.h))
+
+    # ---- off-policy -----------------------------------------------------
+    def vtrace(self, rewards, values, bootstrap, target_logp, behavior_logp, dones, gamma=0.99,
+               rho_bar=1.0, c_bar=1.0, with_weights=False, sync=True):
+        """vtrace (offpolicy.hpp:139-178) over [n_traj, T] tensors."""
+        torch = self.torch
+        _need_cuda(rewards, values, bootstrap, target_logp, behavior_logp, dones)
+        n, T = rewards.shape
+        v = torch.empty_like(rewards)
+        pg = torch.empty_like(rewards)
+        rho = torch.empty_like(rewards) if with_weights else None
+        c = torch.empty_like(rewards) if with_weights else None
+        check(_L.appo_vtrace(self.h, n, T, _ptr(rewards), _ptr(values), _ptr(bootstrap),
+                             _ptr(target_logp), _ptr(behavior_logp), _ptr(dones), gamma, rho_bar,
+                             c_bar, _ptr(v), _ptr(pg), _ptr(rho), _ptr(c)))
+        if sync:
+            self.sync()
+        return (v, pg, rho, c) if with_weights else (v, pg)
+
+    def nstep_returns(self, rewards, bootstrap, dones, gamma, sync=True):
+        _need_cuda(rewards, bootstrap, dones)
+        n, T = rewards.shape
+        ret = self.torch.empty_like(rewards)
+        check(_L.appo_nstep_returns(self.h, n, T, _ptr(rewards), _ptr(bootstrap), _ptr(dones),
+                                    gamma, _ptr(ret)))
+        if sync:
+            self.sync()
+        return ret
+
+    def gae(self, rewards, values, bootstrap, dones, gamma, lam, sync=True):
+        _need_cuda(rewards, values, bootstrap, dones)
+        n, T = rewards.shape
+        adv = self.torch.empty_like(rewards)
+        ret = self.torch.empty_like(rewards)
+        check(_L.appo_gae(self.h, n, T, _ptr(rewards), _ptr(values), _ptr(bootstrap),
+                          _ptr(dones), gamma, lam, _ptr(adv), _ptr(ret)))
+        if sync:
+            self.sync()
+        return adv, ret
+
+    def total_loss(self, ratios, adv, values, v_targets, entropies, clip_low=1 / 1.1,
+                   clip_high=1.1, value_coef=0.5, entropy_coef=0.003):
+        """total_loss (offpolicy.hpp:224-246) -> dict(policy, value, entropy, total)."""
+        _need_cuda(ratios, adv, values, v_targets, entropies)
+        out = (C.c_double * 4)()
+        check(_L.appo_total_loss(self.h, ratios.numel(), _ptr(ratios), _ptr(adv), _ptr(values),
+                                 _ptr(v_targets), _ptr(entropies), clip_low, clip_high,
+                                 value_coef, entropy_coef, out))
+        return dict(policy=out[0], value=out[1], entropy=out[2], total=out[3])
+
+    def log_prob_and_entropy(self, logits, actions, sync=True):
+        _need_cuda(logits, actions)
+        B, A = logits.shape
+        lp = self.torch.empty(B, device=logits.device, dtype=self.torch.float32)
+        en = self.torch.empty_like(lp)
+        check(_L.appo_logp_entropy(self.h, B, A, _ptr(logits), _ptr(actions), _ptr(lp), _ptr(en)))
+        if sync:
+            self.sync()
+        return lp, en
+
+    def sample_actions(self, logits, key, counter0=0, sync=True):
+        _need_cuda(logits)
+        B, A = logits.shape
+        a = self.torch.empty(B, device=logits.device, dtype=self.torch.int32)
+        lp = self.torch.empty(B, device=logits.device, dtype=self.torch.float32)
+        check(_L.appo_sample_actions(self.h, B, A, _ptr(logits), key, counter0, _ptr(a), _ptr(lp)))
+        if sync:
+            self.sync()
+        return a, lp
+
+    def optimizer_step(self, theta, m, v, grad, t, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-6,
+                       grad_clip=4.0):
+        """optimizer_step (policy.hpp:431-455) on flat fp32 tensors; t is the
+        step number after the increment.  Returns the pre-clip gradient norm."""
+        _need_cuda(theta, m, v, grad)
+        norm = C.c_double()
+        check(_L.appo_adam_step(self.h, theta.numel(), _ptr(theta), _ptr(m), _ptr(v), _ptr(grad),
+                                t, lr, beta1, beta2, eps, grad_clip, C.byref(norm)))
+        return norm.value
+
+    # ---- model ------------------------------------------------------------
+    @property
+    def n_params(self) -> int:
+        return param_count(self.model)
+
+    def get_params(self):
+        th = np.zeros(self.n_params, dtype=np.float32)
+        ver = C.c_int64()
+        check(_L.appo_params_get(self.h, th.ctypes.data_as(C.c_void_p), C.byref(ver)))
+        return th, ver.value
+
+    def set_params(self, theta: np.ndarray, version: int = 0):
+        th = np.ascontiguousarray(theta, dtype=np.float32)
+        assert th.size == self.n_params
+        check(_L.appo_params_set(self.h, th.ctypes.data_as(C.c_void_p), version))
+
+    def get_adam(self):
+        m = np.zeros(self.n_params, dtype=np.float32)
+        v = np.zeros(self.n_params, dtype=np.float32)
+        t = C.c_int64()
+        check(_L.appo_adam_get(self.h, m.ctypes.data_as(C.c_void_p),
+                               v.ctypes.data_as(C.c_void_p), C.byref(t)))
+        return m, v, t.value
+
+    def set_adam(self, m, v, t):
+        m = np.ascontiguousarray(m, dtype=np.float32)
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        check(_L.appo_adam_set(self.h, m.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p),
+                               t))
+
+    @property
+    def version(self) -> int:
+        return int(_L.appo_params_version(self.h))
+
+    def policy_forward(self, obs, h_in, rng_counter0=0, want_logits=False, out=None):
+        """Batched inference: obs u8 [B, C*H*W], h_in f32 [B, 512] (CUDA) ->
+        dict(actions, logp, h_out, values[, logits], version)."""
+        torch = self.torch
+        _need_cuda(obs, h_in)
+        B = obs.shape[0]
+        dev = obs.device
+        if out is None:
+            out = dict(actions=torch.empty(B, dtype=torch.int32, device=dev),
+                       logp=torch.empty(B, dtype=torch.float32, device=dev),
+                       h_out=torch.empty(B, 512, dtype=torch.float32, device=dev),
+                       values=torch.empty(B, dtype=torch.float32, device=dev))
+            if want_logits:
+                out["logits"] = torch.empty(B, self.model.n_actions, dtype=torch.float32,
+                                            device=dev)
+        ver = C.c_int64()
+        check(_L.appo_policy_forward(self.h, B, _ptr(obs), _ptr(h_in), rng_counter0,
+                                     _ptr(out["actions"]), _ptr(out["logp"]), _ptr(out["h_out"]),
+                                     _ptr(out["values"]), _ptr(out.get("logits")),
+                                     C.byref(ver)))
+        out["version"] = ver.value
+        return out
+
+    def learner_step(self, region, slot_bytes: int, slot_ids, hp: HParams | None = None):
+        """One APPO learner step over trajectory slots (layout v2) in FIFO order."""
+        _need_cuda(region)
+        ids = np.ascontiguousarray(slot_ids, dtype=np.int32)
+        hp = hp or HParams.defaults()
+        out = StepOut()
+        check(_L.appo_learner_step(self.h, _ptr(region), slot_bytes,
+                                   ids.ctypes.data_as(C.c_void_p), ids.size, C.byref(hp),
+                                   C.byref(out)))
+        return out.as_dict()
+
+    def model_ptrs(self):
+        th, g, pb = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(_L.appo_dbg_model_ptrs(self.h, C.byref(th), C.byref(g), C.byref(pb)))
+        return th.value, g.value, pb.value
+
+    def grad(self) -> np.ndarray:
+        """The last learner step's flat fp32 gradient (pre-clip), for tests."""
+        _, g, _ = self.model_ptrs()
+        out = np.zeros(self.n_params, dtype=np.float32)
+        check(_L.appo_dbg_copy_d2h(self.h, out.ctypes.data_as(C.c_void_p), C.c_void_p(g),
+                                   out.nbytes))
+        return out
+
+    def gemm(self, M, N, K, a, lda, a_mn, b, ldb, b_mn, out, ldo, flags=0, scale=1.0, bias=None,
+             aux=None, ld_aux=0, bn=128, splits=1):
+        """Engine-level GEMM hook (include/appo_internal.h) for tests."""
+        check(_L.appo_dbg_gemm(self.h, M, N, K, _ptr(a), lda, int(a_mn), _ptr(b), ldb, int(b_mn),
+                               _ptr(out), ldo, flags, scale, _ptr(bias), _ptr(aux), ld_aux, bn,
+                               splits))
+
+
+EPI_BIAS, EPI_ELU, EPI_DELU, EPI_BF16, EPI_TRANS, EPI_ACCUM = 1, 2, 4, 8, 16, 32
+
+from .store import TrajectoryStore  # noqa: E402,F401

@@ -1,0 +1,127 @@
+// Shared plumbing for libappo_b200.so: error handling (status codes of
+// include/appo_capi.h mirroring ContractError/ConfigError/NumericError,
+// common.hpp:20-45), the context, and small device helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/appo_capi.h"
+
+namespace appo_b200 {
+
+void set_error(const std::string& msg);
+
+struct Model;  // model.cu
+
+// Device flag slots raised by kernels; read by appo_ctx_sync.
+enum : int { kFlagNumeric = 0, kFlagContract = 1, kNumFlags = 4 };
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t seed = 0;
+  int* d_flags = nullptr;        // [kNumFlags]
+  double* d_red = nullptr;       // reduction workspace (partials), kRedSlots doubles
+  unsigned* d_counter = nullptr; // last-block counters
+  double* h_pinned = nullptr;    // small pinned readback buffer
+  int64_t launches = 0;
+  float* d_ws = nullptr;         // split-K GEMM workspace
+  size_t ws_bytes = 0;
+  int num_sms = 148;
+  bool has_model = false;
+  appo_model_desc desc{};
+  Model* model = nullptr;
+};
+constexpr int kRedSlots = 148 * 8 * 8;
+
+}  // namespace appo_b200
+
+struct appo_ctx : appo_b200::Ctx {};
+
+#define APPO_CUDA_TRY(expr)                                                          \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      appo_b200::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+      return APPO_ERR_RESOURCE;                                                      \
+    }                                                                                \
+  } while (0)
+
+#define APPO_REQUIRE(cond, code, msg)  \
+  do {                                 \
+    if (!(cond)) {                     \
+      appo_b200::set_error(msg);       \
+      return (code);                   \
+    }                                  \
+  } while (0)
+
+// Launch-and-count: every kernel of the library goes through this so
+// appo_ctx_launch_count reports how many of OUR kernels ran.
+#define APPO_LAUNCH(ctx, kernel, grid, block, smem, ...)                        \
+  do {                                                                         \
+    kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);            \
+    (ctx)->launches++;                                                         \
+    cudaError_t _le = cudaGetLastError();                                      \
+    if (_le != cudaSuccess) {                                                  \
+      appo_b200::set_error(std::string("launch " #kernel ": ") +               \
+                           cudaGetErrorString(_le));                           \
+      return APPO_ERR_RESOURCE;                                                \
+    }                                                                          \
+  } while (0)
+
+namespace appo_b200 {
+
+__device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Counter-based uniform in [0,1) (oracle: orc_uniform).
+__device__ __forceinline__ double uniform01(uint64_t key, uint64_t counter) {
+  uint64_t h = splitmix64(key ^ splitmix64(counter));
+  return (double)(h >> 11) * (1.0 / 9007199254740992.0);
+}
+
+inline uint64_t host_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+inline uint64_t host_derive_seed(uint64_t seed, uint64_t stream) {
+  return host_splitmix64(seed ^ host_splitmix64(stream + 1));
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Kernel-side launchers implemented in the .cu files (return appo_status).
+int launch_vtrace(Ctx* c, int n_traj, int T, const float* r, const float* v, const float* boot,
+                  const float* tl, const float* bl, const uint8_t* d, float gamma, float rho_bar,
+                  float c_bar, float* v_out, float* pg_out, float* rho_out, float* c_out);
+int launch_nstep(Ctx* c, int n_traj, int T, const float* r, const float* boot, const uint8_t* d,
+                 float gamma, float* ret);
+int launch_gae(Ctx* c, int n_traj, int T, const float* r, const float* v, const float* boot,
+               const uint8_t* d, float gamma, float lambda, float* adv, float* ret);
+int launch_total_loss(Ctx* c, int n, const float* ratios, const float* adv, const float* values,
+                      const float* vt, const float* ent, float lo, float hi, float vc, float ec,
+                      double* d_out4);
+int launch_logp_entropy(Ctx* c, int B, int A, const float* logits, const int32_t* actions,
+                        float* logp, float* ent);
+int launch_sample(Ctx* c, int B, int A, const float* logits, uint64_t key, uint64_t counter0,
+                  int32_t* actions, float* logp);
+int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
+                float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
+                uint16_t* bf16_copy, float* f32_copy);
+
+}  // namespace appo_b200

@@ -1,0 +1,212 @@
+// C ABI entry points (include/appo_capi.h): context management and the
+// stateless hot-path kernels.  Model-level entry points live in model.cu.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "appo_common.cuh"
+
+namespace appo_b200 {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace appo_b200
+
+using namespace appo_b200;
+
+namespace {
+int check_ctx(appo_ctx* ctx) {
+  if (!ctx) {
+    set_error("null appo_ctx");
+    return APPO_ERR_CONTRACT;
+  }
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    return APPO_ERR_RESOURCE;
+  }
+  return APPO_OK;
+}
+// VTraceConfig::validate (offpolicy.hpp:101-105)
+int validate_vtrace(float gamma, float rho_bar, float c_bar) {
+  if (!(rho_bar >= c_bar && c_bar > 0.0f)) {
+    set_error("vtrace requires rho_bar >= c_bar > 0");
+    return APPO_ERR_CONFIG;
+  }
+  if (!(gamma > 0.0f && gamma <= 1.0f)) {
+    set_error("discount must be in (0,1]");
+    return APPO_ERR_CONFIG;
+  }
+  return APPO_OK;
+}
+}  // namespace
+
+#define CTX_OR_RETURN(ctx)             \
+  do {                                 \
+    int _s = check_ctx(ctx);           \
+    if (_s != APPO_OK) return _s;      \
+  } while (0)
+
+int model_create(appo_b200::Ctx* c);   // model.cu
+void model_destroy(appo_b200::Ctx* c); // model.cu
+
+extern "C" {
+
+const char* appo_last_error(void) { return g_last_error.c_str(); }
+int appo_capi_version(void) { return APPO_CAPI_VERSION; }
+
+int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo_ctx** out) {
+  APPO_REQUIRE(out != nullptr, APPO_ERR_CONTRACT, "appo_ctx_create: null out");
+  int n = 0;
+  APPO_CUDA_TRY(cudaGetDeviceCount(&n));
+  APPO_REQUIRE(device >= 0 && device < n, APPO_ERR_CONTRACT, "appo_ctx_create: bad device");
+  APPO_CUDA_TRY(cudaSetDevice(device));
+  appo_ctx* c = new appo_ctx();
+  c->device = device;
+  c->seed = seed;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (c->num_sms <= 0) c->num_sms = 148;
+  if (cudaMalloc(&c->d_flags, sizeof(int) * kNumFlags) != cudaSuccess ||
+      cudaMalloc(&c->d_red, sizeof(double) * kRedSlots) != cudaSuccess ||
+      cudaMalloc(&c->d_counter, sizeof(unsigned) * 16) != cudaSuccess ||
+      cudaMallocHost(&c->h_pinned, sizeof(double) * 64) != cudaSuccess) {
+    set_error("appo_ctx_create: allocation failed");
+    delete c;
+    return APPO_ERR_RESOURCE;
+  }
+  cudaMemset(c->d_flags, 0, sizeof(int) * kNumFlags);
+  cudaMemset(c->d_counter, 0, sizeof(unsigned) * 16);
+  cudaDeviceSynchronize();
+  if (desc) {
+    c->has_model = true;
+    c->desc = *desc;
+    int st = model_create(c);
+    if (st != APPO_OK) {
+      appo_ctx_destroy(c);
+      return st;
+    }
+  }
+  *out = c;
+  return APPO_OK;
+}
+
+int appo_ctx_destroy(appo_ctx* ctx) {
+  if (!ctx) return APPO_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaDeviceSynchronize();
+  if (ctx->model) model_destroy(ctx);
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_red);
+  cudaFree(ctx->d_counter);
+  cudaFreeHost(ctx->h_pinned);
+  delete ctx;
+  return APPO_OK;
+}
+
+int appo_ctx_set_stream(appo_ctx* ctx, void* stream) {
+  CTX_OR_RETURN(ctx);
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return APPO_OK;
+}
+
+int appo_ctx_sync(appo_ctx* ctx) {
+  CTX_OR_RETURN(ctx);
+  int flags[kNumFlags];
+  APPO_CUDA_TRY(cudaMemcpyAsync(flags, ctx->d_flags, sizeof(flags), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (flags[kFlagNumeric] || flags[kFlagContract]) {
+    APPO_CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(flags), ctx->stream));
+    APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (flags[kFlagContract]) {
+      set_error("contract violation detected on device (action index out of range?)");
+      return APPO_ERR_CONTRACT;
+    }
+    set_error("non-finite value detected on device (NumericError)");
+    return APPO_ERR_NUMERIC;
+  }
+  return APPO_OK;
+}
+
+int64_t appo_ctx_launch_count(appo_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int appo_vtrace(appo_ctx* ctx, int n_traj, int T, const float* r, const float* v,
+                const float* boot, const float* tl, const float* bl, const uint8_t* d,
+                float gamma, float rho_bar, float c_bar, float* v_out, float* pg_out,
+                float* rho_out, float* c_out) {
+  CTX_OR_RETURN(ctx);
+  int st = validate_vtrace(gamma, rho_bar, c_bar);
+  if (st) return st;
+  APPO_REQUIRE(n_traj >= 0 && T >= 0, APPO_ERR_CONTRACT, "vtrace: negative shape");
+  APPO_REQUIRE(n_traj == 0 || T == 0 || (r && v && boot && tl && bl && d && v_out && pg_out),
+               APPO_ERR_CONTRACT, "vtrace: null buffer");
+  return launch_vtrace(ctx, n_traj, T, r, v, boot, tl, bl, d, gamma, rho_bar, c_bar, v_out,
+                       pg_out, rho_out, c_out);
+}
+
+int appo_nstep_returns(appo_ctx* ctx, int n_traj, int T, const float* r, const float* boot,
+                       const uint8_t* d, float gamma, float* ret) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(n_traj >= 0 && T >= 0, APPO_ERR_CONTRACT, "nstep: negative shape");
+  return launch_nstep(ctx, n_traj, T, r, boot, d, gamma, ret);
+}
+
+int appo_gae(appo_ctx* ctx, int n_traj, int T, const float* r, const float* v, const float* boot,
+             const uint8_t* d, float gamma, float lambda, float* adv, float* ret) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(n_traj >= 0 && T >= 0, APPO_ERR_CONTRACT, "gae: negative shape");
+  APPO_REQUIRE(gamma > 0.0f && gamma <= 1.0f, APPO_ERR_CONFIG, "discount must be in (0,1]");
+  APPO_REQUIRE(lambda >= 0.0f && lambda <= 1.0f, APPO_ERR_CONFIG, "gae lambda must be in [0,1]");
+  return launch_gae(ctx, n_traj, T, r, v, boot, d, gamma, lambda, adv, ret);
+}
+
+int appo_total_loss(appo_ctx* ctx, int n, const float* ratios, const float* adv,
+                    const float* values, const float* vt, const float* ent, float lo, float hi,
+                    float vc, float ec, double* h_out4) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(0.0f < lo && lo < 1.0f && 1.0f < hi, APPO_ERR_CONFIG,
+               "ppo clip requires 0 < low < 1 < high");
+  APPO_REQUIRE(n >= 0 && h_out4, APPO_ERR_CONTRACT, "total_loss: bad arguments");
+  double* d_out = ctx->d_red + kRedSlots - 8;
+  int st = launch_total_loss(ctx, n, ratios, adv, values, vt, ent, lo, hi, vc, ec, d_out);
+  if (st) return st;
+  APPO_CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned, d_out, sizeof(double) * 4, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  st = appo_ctx_sync(ctx);
+  std::memcpy(h_out4, ctx->h_pinned, sizeof(double) * 4);
+  return st;
+}
+
+int appo_logp_entropy(appo_ctx* ctx, int B, int A, const float* logits, const int32_t* actions,
+                      float* logp, float* ent) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(B >= 0 && A >= 1 && A <= 64, APPO_ERR_CONTRACT, "logp_entropy: bad shape");
+  return launch_logp_entropy(ctx, B, A, logits, actions, logp, ent);
+}
+
+int appo_sample_actions(appo_ctx* ctx, int B, int A, const float* logits, uint64_t key,
+                        uint64_t counter0, int32_t* actions, float* logp) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(B >= 0 && A >= 1 && A <= 64, APPO_ERR_CONTRACT, "sample: bad shape");
+  return launch_sample(ctx, B, A, logits, key, counter0, actions, logp);
+}
+
+int appo_adam_step(appo_ctx* ctx, int64_t n, float* theta, float* m, float* v, const float* g,
+                   int64_t t, float lr, float b1, float b2, float eps, float clip,
+                   double* h_grad_norm) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(n >= 0 && t >= 1, APPO_ERR_CONTRACT, "adam: n >= 0 and t >= 1 required");
+  double* d_norm = ctx->d_red + kRedSlots - 16;
+  int st = launch_adam(ctx, n, theta, m, v, g, t, lr, b1, b2, eps, clip, d_norm, nullptr, nullptr);
+  if (st) return st;
+  if (h_grad_norm) {
+    APPO_CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned, d_norm, sizeof(double), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    st = appo_ctx_sync(ctx);
+    *h_grad_norm = ctx->h_pinned[0];
+    return st;
+  }
+  return APPO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// Host interface of the tcgen05 GEMM engine (gemm.cu).
+#pragma once
+#include <stdint.h>
+
+#include "appo_common.cuh"
+
+namespace appo_b200 {
+
+enum EpiFlags : int {
+  EPI_BIAS = 1,    // + bias[n]
+  EPI_ELU = 2,     // ELU(x) after scale/bias
+  EPI_DELU = 4,    // x * ELU'(aux[m][n]) where aux is the post-ELU activation (bf16)
+  EPI_BF16 = 8,    // store bf16 (else fp32)
+  EPI_TRANS = 16,  // store D[m][n] at out[n*ldo + m]
+  EPI_ACCUM = 32,  // out += result (fp32 only)
+};
+
+struct Epilogue {
+  int flags = 0;
+  float scale = 1.0f;
+  const float* bias = nullptr;
+  const uint16_t* aux = nullptr;  // bf16 bits
+  int64_t ld_aux = 0;
+  void* out = nullptr;
+  int64_t ldo = 0;
+};
+
+// One GEMM operand in global memory (bf16).
+//   K-major : element (row r, k) at ptr[r*ld + k]   (rows = M for A, N for B)
+//   MN-major: element (row r, k) at ptr[k*ld + r]
+struct Operand {
+  const void* ptr = nullptr;
+  int64_t ld = 0;
+  bool mn_major = false;
+};
+
+// D[M,N] = sum_k A[m,k] B[n,k] with epilogue.  bn in {32,64,128,192,256}
+// (MN-major B needs bn % 64 == 0).  splits > 1 splits K; partial sums go to
+// the ctx's workspace and a reduce kernel applies the epilogue (fp32 only).
+int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
+              const Epilogue& epi, int bn, int splits = 1);
+
+// Workspace management for split-K partials (grown on demand).
+int gemm_workspace(Ctx* c, size_t bytes, float** out);
+
+}  // namespace appo_b200

@@ -1,0 +1,702 @@
+// Model-level orchestration and its C ABI: parameter contract and init,
+// batched policy inference (replaces forward_batch + sample_action,
+// policy.hpp:165-258, in PolicyWorkerUnit::run_once, orchestrator.hpp:602-673)
+// and the learner step (replaces assemble_minibatch's gather +
+// LearnerUnit::step, orchestrator.hpp:760-868).
+//
+// Dense contractions go to the tcgen05 GEMM engine (gemm.cu); everything else
+// to the SIMT kernels of model_kernels.cu.  Activations are NHWC bf16 so each
+// conv layer is one im2col + one GEMM whose [rows][Cout] output IS the next
+// layer's NHWC input, and conv3's output rows flatten (h, w, c) for the FC.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "gemm.cuh"
+#include "model.cuh"
+#include "model_kernels.cuh"
+
+namespace appo_b200 {
+
+static size_t a8(size_t x) { return (x + 7) & ~size_t(7); }
+
+int make_dims(const appo_model_desc& m, Dims* out) {
+  Dims d{};
+  d.C = m.obs_c;
+  d.H = m.obs_h;
+  d.W = m.obs_w;
+  d.A = m.n_actions;
+  d.T = m.T;
+  if (d.C < 1 || d.H < 36 || d.W < 36 || (d.W % 4) != 0 || d.A < 1 || d.A > kMaxActions - 1 ||
+      d.T < 1) {
+    set_error("model desc: need C>=1, H,W>=36, W%4==0, 1<=n_actions<=15, T>=1");
+    return APPO_ERR_CONFIG;
+  }
+  d.H1 = (d.H - 8) / 4 + 1;
+  d.W1 = (d.W - 8) / 4 + 1;
+  d.H2 = (d.H1 - 4) / 2 + 1;
+  d.W2 = (d.W1 - 4) / 2 + 1;
+  d.H3 = (d.H2 - 3) / 2 + 1;
+  d.W3 = (d.W2 - 3) / 2 + 1;
+  d.P1 = d.H1 * d.W1;
+  d.P2 = d.H2 * d.W2;
+  d.P3 = d.H3 * d.W3;
+  d.K1 = d.C * 64;
+  d.F = d.P3 * 128;
+  int64_t o = 0;
+  d.off_c1w = o; o += 32LL * d.K1;
+  d.off_c1b = o; o += 32;
+  d.off_c2w = o; o += 64LL * 16 * 32;
+  d.off_c2b = o; o += 64;
+  d.off_c3w = o; o += 128LL * 9 * 64;
+  d.off_c3b = o; o += 128;
+  d.off_fcw = o; o += (int64_t)kHidden * d.F;
+  d.off_fcb = o; o += kHidden;
+  d.off_wih = o; o += (int64_t)kGates * kHidden;
+  d.off_whh = o; o += (int64_t)kGates * kHidden;
+  d.off_bih = o; o += kGates;
+  d.off_bhh = o; o += kGates;
+  d.off_wpi = o; o += (int64_t)d.A * kHidden;
+  d.off_bpi = o; o += d.A;
+  d.off_wv = o; o += kHidden;
+  d.off_bv = o; o += 1;
+  d.total = o;
+  d.obs_dim = (int64_t)d.C * d.H * d.W;
+  // trajectory slot layout v2 (trajstore.hpp:62-87; u8 obs, f32 hidden/reward/logp)
+  size_t s = 64;
+  const size_t T = d.T, od = d.obs_dim, hd = kHidden;
+  d.slot[0] = s; s += a8(T * od);
+  d.slot[1] = s; s += a8(T * hd * 4);
+  d.slot[2] = s; s += a8(T * 1 * 4);
+  d.slot[3] = s; s += a8(T * 4);
+  d.slot[4] = s; s += a8(T * 4);
+  d.slot[5] = s; s += a8(T);
+  d.slot[6] = s; s += a8(T * 8);
+  d.slot[7] = s; s += a8(od);
+  d.slot[8] = s; s += a8(hd * 4);
+  d.slot[9] = s;
+  *out = d;
+  return APPO_OK;
+}
+
+namespace {
+
+uint16_t host_f2bf(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  const uint32_t r = ((u >> 16) & 1u) + 0x7FFFu;  // round to nearest even
+  return (uint16_t)((u + r) >> 16);
+}
+
+double host_uniform(uint64_t key, uint64_t counter) {
+  const uint64_t h = host_splitmix64(key ^ host_splitmix64(counter));
+  return (double)(h >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Glorot-uniform in the style of init_params (policy.hpp:110-131); gain 1.0
+// trunk/core, 0.01 heads; biases zero.  Same stream as the oracle's
+// orc_model_init so tests can start both from identical parameters.
+void init_params_host(const Dims& d, uint64_t seed, std::vector<float>& th) {
+  th.assign(d.total, 0.0f);
+  const uint64_t k = host_derive_seed(seed, 0xA11CE);
+  auto fill = [&](int64_t off, int64_t rows, int64_t cols, double gain, uint64_t key) {
+    const double a = gain * std::sqrt(6.0 / (double)(rows + cols));
+    for (int64_t i = 0; i < rows * cols; ++i)
+      th[off + i] = (float)((2.0 * host_uniform(key, (uint64_t)i) - 1.0) * a);
+  };
+  fill(d.off_c1w, 32, d.K1, 1.0, k + 1);
+  fill(d.off_c2w, 64, 16 * 32, 1.0, k + 2);
+  fill(d.off_c3w, 128, 9 * 64, 1.0, k + 3);
+  fill(d.off_fcw, kHidden, d.F, 1.0, k + 4);
+  fill(d.off_wih, kGates, kHidden, 1.0, k + 5);
+  fill(d.off_whh, kGates, kHidden, 1.0, k + 6);
+  fill(d.off_wpi, d.A, kHidden, 0.01, k + 7);
+  fill(d.off_wv, 1, kHidden, 0.01, k + 8);
+}
+
+// Arena allocation helper: offsets are 256-byte aligned.
+struct Arena {
+  size_t off = 0;
+  template <class T>
+  size_t take(T** p, size_t count) {
+    const size_t o = off;
+    off += ((count * sizeof(T)) + 255) & ~size_t(255);
+    *p = reinterpret_cast<T*>(o);  // relocated after the single cudaMalloc
+    return o;
+  }
+};
+template <class T>
+void reloc(T*& p, uint8_t* base) {
+  p = reinterpret_cast<T*>(base + reinterpret_cast<size_t>(p));
+}
+
+int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner) {
+  if (R <= s.cap_rows && n_traj <= s.cap_traj) return APPO_OK;
+  const Dims& d = M->d;
+  if (s.col1) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(s.col1);
+    cudaFreeHost(s.h_stats);
+  }
+  s = Scratch{};
+  const int B = learner ? n_traj * d.T : R;
+  const int G = learner ? n_traj : R;  // rows of gh per GEMM
+  Arena a;
+  a.take(&s.col1, (size_t)R * d.P1 * d.K1);
+  a.take(&s.a1, (size_t)R * d.P1 * 32);
+  a.take(&s.col2, (size_t)R * d.P2 * 512);
+  a.take(&s.a2, (size_t)R * d.P2 * 64);
+  a.take(&s.col3, (size_t)R * d.P3 * 576);
+  a.take(&s.a3, (size_t)R * d.F);
+  a.take(&s.x, (size_t)R * kHidden);
+  a.take(&s.gi, (size_t)R * kGates);
+  a.take(&s.gh, (size_t)G * kGates);
+  a.take(&s.hbf, (size_t)R * kHidden);
+  if (learner) {
+    a.take(&s.core, (size_t)R * kHidden);
+    a.take(&s.core_bf, (size_t)R * kHidden);
+    a.take(&s.gates, (size_t)R * 4 * kHidden);
+    a.take(&s.hin, (size_t)R * kHidden);
+    a.take(&s.hcur, (size_t)n_traj * kHidden);
+    a.take(&s.logits, (size_t)R * d.A);
+    a.take(&s.values, (size_t)R);
+    a.take(&s.tlogp, (size_t)B);
+    a.take(&s.ent, (size_t)B);
+    a.take(&s.vt, (size_t)B);
+    a.take(&s.pg, (size_t)B);
+    a.take(&s.adv, (size_t)B);
+    a.take(&s.rew, (size_t)B);
+    a.take(&s.blogp, (size_t)B);
+    a.take(&s.act, (size_t)B);
+    a.take(&s.done, (size_t)B);
+    a.take(&s.ver, (size_t)B);
+    a.take(&s.dlog, (size_t)B * (d.A + 1));
+    a.take(&s.dhead, (size_t)B * 16);
+    a.take(&s.dcore, (size_t)B * kHidden);
+    a.take(&s.dnext, (size_t)n_traj * kHidden);
+    a.take(&s.dgi, (size_t)B * kGates);
+    a.take(&s.dgh, (size_t)B * kGates);
+    a.take(&s.dzfc, (size_t)B * kHidden);
+    a.take(&s.dz3, (size_t)B * d.F);
+    a.take(&s.dz2, (size_t)B * d.P2 * 64);
+    a.take(&s.dz1, (size_t)B * d.P1 * 32);
+    a.take(&s.dcol3, (size_t)B * d.P3 * 576);
+    a.take(&s.dcol2, (size_t)B * d.P2 * 512);
+    a.take(&s.headw, (size_t)16 * kHidden);
+    a.take(&s.colsum_part, (size_t)256 * kGates + 64);
+    a.take(&s.slot_ids, (size_t)n_traj);
+    a.take(&s.stats, (size_t)16);
+  }
+  uint8_t* base = nullptr;
+  if (cudaMalloc(&base, a.off) != cudaSuccess) {
+    set_error("scratch allocation failed (" + std::to_string(a.off >> 20) + " MiB)");
+    s = Scratch{};
+    return APPO_ERR_RESOURCE;
+  }
+  reloc(s.col1, base); reloc(s.a1, base); reloc(s.col2, base); reloc(s.a2, base);
+  reloc(s.col3, base); reloc(s.a3, base); reloc(s.x, base); reloc(s.gi, base);
+  reloc(s.gh, base); reloc(s.hbf, base);
+  if (learner) {
+    reloc(s.core, base); reloc(s.core_bf, base); reloc(s.gates, base); reloc(s.hin, base);
+    reloc(s.hcur, base); reloc(s.logits, base); reloc(s.values, base); reloc(s.tlogp, base);
+    reloc(s.ent, base); reloc(s.vt, base); reloc(s.pg, base); reloc(s.adv, base);
+    reloc(s.rew, base); reloc(s.blogp, base); reloc(s.act, base); reloc(s.done, base);
+    reloc(s.ver, base); reloc(s.dlog, base); reloc(s.dhead, base); reloc(s.dcore, base);
+    reloc(s.dnext, base); reloc(s.dgi, base); reloc(s.dgh, base); reloc(s.dzfc, base);
+    reloc(s.dz3, base); reloc(s.dz2, base); reloc(s.dz1, base); reloc(s.dcol3, base);
+    reloc(s.dcol2, base); reloc(s.headw, base); reloc(s.colsum_part, base);
+    reloc(s.slot_ids, base); reloc(s.stats, base);
+    if (cudaMallocHost(&s.h_stats, sizeof(double) * 16 + sizeof(int32_t) * n_traj) !=
+        cudaSuccess) {
+      cudaFree(base);
+      s = Scratch{};
+      set_error("pinned stats allocation failed");
+      return APPO_ERR_RESOURCE;
+    }
+  } else {
+    cudaMallocHost(&s.h_stats, sizeof(double) * 16);
+  }
+  // col1 is the arena base (first take) -> freeing col1 frees the arena.
+  s.cap_rows = R;
+  s.cap_traj = n_traj;
+  return APPO_OK;
+}
+
+int splits_for(Ctx* c, int M, int N, int bn, int K) {
+  const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  const int nkb = (K + 63) / 64;
+  int sp = (2 * c->num_sms + tiles - 1) / tiles;
+  if (sp > nkb / 2) sp = nkb / 2;  // keep >= 2 k-blocks per split
+  return sp < 1 ? 1 : sp;
+}
+
+#define TRY(x)                    \
+  do {                            \
+    int _st = (x);                \
+    if (_st != APPO_OK) return _st; \
+  } while (0)
+
+// Encoder forward over R images: col1..a3 -> x (bf16 [R][512]) and gi.
+int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, const uint16_t* wb,
+                    const float* pf) {
+  const Dims& d = M->d;
+  TRY(k_im2col_u8(c, src, R, d, s.col1));
+  Epilogue e;
+  // conv1: [R*P1, 32] = col1 [R*P1, K1] . W1[32, K1]^T, x/255 folded into scale
+  e.flags = EPI_BIAS | EPI_ELU | EPI_BF16;
+  e.scale = 1.0f / 255.0f;
+  e.bias = pf + d.off_c1b;
+  e.out = s.a1;
+  e.ldo = 32;
+  TRY(gemm_bf16(c, R * d.P1, 32, d.K1, Operand{s.col1, d.K1, false},
+                Operand{wb + d.off_c1w, d.K1, false}, e, 32));
+  TRY(k_im2col_nhwc(c, s.a1, R, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.col2));
+  e.scale = 1.0f;
+  e.bias = pf + d.off_c2b;
+  e.out = s.a2;
+  e.ldo = 64;
+  TRY(gemm_bf16(c, R * d.P2, 64, 512, Operand{s.col2, 512, false},
+                Operand{wb + d.off_c2w, 512, false}, e, 64));
+  TRY(k_im2col_nhwc(c, s.a2, R, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.col3));
+  e.bias = pf + d.off_c3b;
+  e.out = s.a3;
+  e.ldo = 128;
+  TRY(gemm_bf16(c, R * d.P3, 128, 576, Operand{s.col3, 576, false},
+                Operand{wb + d.off_c3w, 576, false}, e, 128));
+  e.bias = pf + d.off_fcb;
+  e.out = s.x;
+  e.ldo = kHidden;
+  TRY(gemm_bf16(c, R, kHidden, d.F, Operand{s.a3, d.F, false}, Operand{wb + d.off_fcw, d.F, false},
+                e, 128));
+  Epilogue g;
+  g.flags = EPI_BIAS;
+  g.bias = pf + d.off_bih;
+  g.out = s.gi;
+  g.ldo = kGates;
+  TRY(gemm_bf16(c, R, kGates, kHidden, Operand{s.x, kHidden, false},
+                Operand{wb + d.off_wih, kHidden, false}, g, 256));
+  return APPO_OK;
+}
+
+}  // namespace
+
+}  // namespace appo_b200
+
+using namespace appo_b200;
+
+int model_create(Ctx* c) {
+  Model* M = new Model();
+  int st = make_dims(c->desc, &M->d);
+  if (st) {
+    delete M;
+    return st;
+  }
+  c->model = M;
+  const int64_t P = M->d.total;
+  APPO_CUDA_TRY(cudaMalloc(&M->theta, P * 4));
+  APPO_CUDA_TRY(cudaMalloc(&M->m, P * 4));
+  APPO_CUDA_TRY(cudaMalloc(&M->v, P * 4));
+  APPO_CUDA_TRY(cudaMalloc(&M->grad, P * 4));
+  for (int k = 0; k < 2; ++k) {
+    APPO_CUDA_TRY(cudaMalloc(&M->pub_bf16[k], P * 2));
+    APPO_CUDA_TRY(cudaMalloc(&M->pub_f32[k], P * 4));
+  }
+  M->sample_key = host_derive_seed(c->seed, 0x9900);
+  std::vector<float> th;
+  init_params_host(M->d, c->seed, th);
+  return appo_params_set(static_cast<appo_ctx*>(c), th.data(), 0);
+}
+
+void model_destroy(Ctx* c) {
+  Model* M = c->model;
+  if (!M) return;
+  cudaFree(M->theta);
+  cudaFree(M->m);
+  cudaFree(M->v);
+  cudaFree(M->grad);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(M->pub_bf16[k]);
+    cudaFree(M->pub_f32[k]);
+  }
+  for (Scratch* s : {&M->si, &M->sl}) {
+    if (s->col1) cudaFree(s->col1);
+    if (s->h_stats) cudaFreeHost(s->h_stats);
+  }
+  delete M;
+  c->model = nullptr;
+}
+
+#define MODEL_OR_RETURN(ctx)                                                        \
+  do {                                                                              \
+    APPO_REQUIRE((ctx) != nullptr, APPO_ERR_CONTRACT, "null appo_ctx");             \
+    APPO_REQUIRE((ctx)->model != nullptr, APPO_ERR_CONTRACT,                        \
+                 "context was created without a model desc");                       \
+    APPO_CUDA_TRY(cudaSetDevice((ctx)->device));                                    \
+  } while (0)
+
+extern "C" {
+
+int64_t appo_param_count(const appo_model_desc* desc) {
+  if (!desc) return -1;
+  Dims d;
+  if (make_dims(*desc, &d)) return -1;
+  return d.total;
+}
+
+int appo_slot_layout(const appo_model_desc* desc, uint64_t* out10) {
+  APPO_REQUIRE(desc && out10, APPO_ERR_CONTRACT, "slot_layout: null argument");
+  Dims d;
+  int st = make_dims(*desc, &d);
+  if (st) return st;
+  for (int i = 0; i < 10; ++i) out10[i] = d.slot[i];
+  return APPO_OK;
+}
+
+int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  const int64_t P = M->d.total;
+  APPO_REQUIRE(h_src != nullptr, APPO_ERR_CONTRACT, "params_set: null source");
+  std::vector<uint16_t> bf(P);
+  for (int64_t i = 0; i < P; ++i) bf[i] = host_f2bf(h_src[i]);
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(cudaMemcpy(M->theta, h_src, P * 4, cudaMemcpyHostToDevice));
+  APPO_CUDA_TRY(cudaMemset(M->m, 0, P * 4));
+  APPO_CUDA_TRY(cudaMemset(M->v, 0, P * 4));
+  for (int k = 0; k < 2; ++k) {
+    APPO_CUDA_TRY(cudaMemcpy(M->pub_f32[k], h_src, P * 4, cudaMemcpyHostToDevice));
+    APPO_CUDA_TRY(cudaMemcpy(M->pub_bf16[k], bf.data(), P * 2, cudaMemcpyHostToDevice));
+  }
+  M->version = version;
+  M->adam_t = 0;
+  M->published = 0;
+  return APPO_OK;
+}
+
+int appo_params_get(appo_ctx* ctx, float* h_dst, int64_t* version_out) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (h_dst)
+    APPO_CUDA_TRY(cudaMemcpy(h_dst, M->theta, M->d.total * 4, cudaMemcpyDeviceToHost));
+  if (version_out) *version_out = M->version;
+  return APPO_OK;
+}
+
+int appo_adam_get(appo_ctx* ctx, float* h_m, float* h_v, int64_t* t_out) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (h_m) APPO_CUDA_TRY(cudaMemcpy(h_m, M->m, M->d.total * 4, cudaMemcpyDeviceToHost));
+  if (h_v) APPO_CUDA_TRY(cudaMemcpy(h_v, M->v, M->d.total * 4, cudaMemcpyDeviceToHost));
+  if (t_out) *t_out = M->adam_t;
+  return APPO_OK;
+}
+
+int appo_adam_set(appo_ctx* ctx, const float* h_m, const float* h_v, int64_t t) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (h_m) APPO_CUDA_TRY(cudaMemcpy(M->m, h_m, M->d.total * 4, cudaMemcpyHostToDevice));
+  if (h_v) APPO_CUDA_TRY(cudaMemcpy(M->v, h_v, M->d.total * 4, cudaMemcpyHostToDevice));
+  M->adam_t = t;
+  return APPO_OK;
+}
+
+int64_t appo_params_version(appo_ctx* ctx) {
+  return (ctx && ctx->model) ? ctx->model->version : -1;
+}
+
+int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float* d_h_in,
+                        uint64_t rng_counter0, int32_t* d_actions, float* d_logp,
+                        float* d_h_out, float* d_values, float* d_logits,
+                        int64_t* h_version_out) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  const Dims& d = M->d;
+  APPO_REQUIRE(B >= 0, APPO_ERR_CONTRACT, "policy_forward: batch must be >= 0");
+  if (h_version_out) *h_version_out = M->version;
+  if (B == 0) return APPO_OK;
+  APPO_REQUIRE(d_obs && d_h_in && d_actions && d_logp && d_h_out && d_values, APPO_ERR_CONTRACT,
+               "policy_forward: null buffer");
+  APPO_REQUIRE((reinterpret_cast<uintptr_t>(d_obs) & 3) == 0, APPO_ERR_CONTRACT,
+               "policy_forward: obs must be 4-byte aligned");
+  Scratch& s = M->si;
+  TRY(alloc_scratch(ctx, M, s, B, 0, false));
+  const int pub = M->published;
+  const uint16_t* wb = M->pub_bf16[pub];
+  const float* pf = M->pub_f32[pub];
+  ObsSrc src;
+  src.base = d_obs;
+  src.img_stride = d.obs_dim;
+  TRY(encoder_forward(ctx, M, s, src, B, wb, pf));
+  TRY(k_f32_to_bf16(ctx, B, d_h_in, kHidden, s.hbf, kHidden, kHidden));
+  Epilogue g;
+  g.flags = EPI_BIAS;
+  g.bias = pf + d.off_bhh;
+  g.out = s.gh;
+  g.ldo = kGates;
+  TRY(gemm_bf16(ctx, B, kGates, kHidden, Operand{s.hbf, kHidden, false},
+                Operand{wb + d.off_whh, kHidden, false}, g, 256));
+  TRY(k_gru_infer(ctx, B, d.A, s.gi, s.gh, d_h_in, pf + d.off_wpi, pf + d.off_bpi,
+                  pf + d.off_wv, pf + d.off_bv, M->sample_key, rng_counter0, d_h_out, d_actions,
+                  d_logp, d_values, d_logits));
+  return APPO_OK;
+}
+
+int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
+                      const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp,
+                      appo_step_out* out) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  const Dims& d = M->d;
+  APPO_REQUIRE(hp && out && d_region && h_slot_ids && n_traj >= 1, APPO_ERR_CONTRACT,
+               "learner_step: bad arguments");
+  APPO_REQUIRE(slot_bytes >= d.slot[9], APPO_ERR_CONTRACT,
+               "learner_step: slot_bytes smaller than the layout v2 slot");
+  APPO_REQUIRE(n_traj <= 4096, APPO_ERR_CONTRACT, "learner_step: at most 4096 trajectories");
+  // VTraceConfig / ClipConfig validation (offpolicy.hpp:101-122)
+  APPO_REQUIRE(hp->rho_bar >= hp->c_bar && hp->c_bar > 0.0f, APPO_ERR_CONFIG,
+               "vtrace requires rho_bar >= c_bar > 0");
+  APPO_REQUIRE(hp->gamma > 0.0f && hp->gamma <= 1.0f, APPO_ERR_CONFIG,
+               "discount must be in (0,1]");
+  APPO_REQUIRE(0.0f < hp->clip_low && hp->clip_low < 1.0f && 1.0f < hp->clip_high,
+               APPO_ERR_CONFIG, "ppo clip requires 0 < low < 1 < high");
+  APPO_REQUIRE(hp->adv_source >= 0 && hp->adv_source <= 2, APPO_ERR_CONFIG,
+               "adv_source must be 0 (vtrace), 1 (nstep) or 2 (gae)");
+  const int T = d.T;
+  const int B = n_traj * T;
+  const int R = B + n_traj;
+  Scratch& s = M->sl;
+  TRY(alloc_scratch(ctx, M, s, R, n_traj, true));
+  cudaStream_t st = ctx->stream;
+  const int pub = M->published;
+  const uint16_t* wb = M->pub_bf16[pub];
+  const float* th = M->theta;  // fp32 master (== pub_f32[pub])
+  const uint8_t* region = static_cast<const uint8_t*>(d_region);
+
+  int32_t* h_ids = reinterpret_cast<int32_t*>(s.h_stats + 16);
+  std::memcpy(h_ids, h_slot_ids, sizeof(int32_t) * n_traj);
+  APPO_CUDA_TRY(cudaMemcpyAsync(s.slot_ids, h_ids, sizeof(int32_t) * n_traj,
+                                cudaMemcpyHostToDevice, st));
+  SlotOffsets off;
+  std::memcpy(&off, d.slot, sizeof(off));
+  TRY(k_gather_slots(ctx, n_traj, T, region, slot_bytes, s.slot_ids, off, s.act, s.rew, s.blogp,
+                     s.done, s.ver, s.hcur));
+
+  // ---- forward: encoder over all T steps + bootstrap obs ----
+  ObsSrc src;
+  src.base = region;
+  src.slot_ids = s.slot_ids;
+  src.slot_bytes = slot_bytes;
+  src.obs_off = d.slot[0];
+  src.boot_off = d.slot[7];
+  src.T = T;
+  src.n_traj = n_traj;
+  src.obs_dim = d.obs_dim;
+  TRY(encoder_forward(ctx, M, s, src, R, wb, th));
+
+  // ---- GRU unrolled over T steps (+ bootstrap step) ----
+  Epilogue g;
+  g.flags = EPI_BIAS;
+  g.bias = th + d.off_bhh;
+  g.out = s.gh;
+  g.ldo = kGates;
+  for (int t = 0; t <= T; ++t) {
+    TRY(k_stage_h(ctx, n_traj, T, t, s.hcur, s.hin, s.hbf));
+    const uint16_t* a = (t < T) ? s.hbf + (size_t)t * kHidden : s.hbf + (size_t)B * kHidden;
+    const int64_t lda = (t < T) ? (int64_t)T * kHidden : kHidden;
+    TRY(gemm_bf16(ctx, n_traj, kGates, kHidden, Operand{a, lda, false},
+                  Operand{wb + d.off_whh, kHidden, false}, g, 128));
+    TRY(k_gru_train(ctx, n_traj, T, t, s.gi, s.gh, s.done, s.hcur, s.core, s.core_bf, s.gates));
+  }
+  TRY(k_heads_fwd(ctx, R, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
+                  th + d.off_bv, s.logits, s.values));
+
+  // ---- targets: logp/entropy, V-trace, advantages ----
+  TRY(launch_logp_entropy(ctx, B, d.A, s.logits, s.act, s.tlogp, s.ent));
+  TRY(launch_vtrace(ctx, n_traj, T, s.rew, s.values, s.values + B, s.tlogp, s.blogp, s.done,
+                    hp->gamma, hp->rho_bar, hp->c_bar, s.vt, s.pg, nullptr, nullptr));
+  const float* adv = s.pg;
+  if (hp->adv_source == 1 || hp->adv_source == 2) {
+    const float lam = hp->adv_source == 1 ? 1.0f : hp->gae_lambda;
+    TRY(launch_gae(ctx, n_traj, T, s.rew, s.values, s.values + B, s.done, hp->gamma, lam, s.adv,
+                   nullptr));
+    adv = s.adv;
+  } else if (hp->normalize_adv) {
+    APPO_CUDA_TRY(cudaMemcpyAsync(s.adv, s.pg, sizeof(float) * B, cudaMemcpyDeviceToDevice, st));
+    adv = s.adv;
+  }
+  if (hp->normalize_adv) TRY(k_normalize(ctx, B, s.adv));
+
+  // ---- loss and its gradient wrt logits / value ----
+  LossHP lh{hp->clip_low, hp->clip_high, hp->value_coef, hp->entropy_coef};
+  TRY(k_ppo_loss(ctx, B, d.A, s.logits, s.values, s.act, s.blogp, adv, s.vt, lh, s.dlog,
+                 s.dhead, s.stats));
+  TRY(k_lag(ctx, B, s.ver, M->version, s.stats));
+
+  float* G = M->grad;
+  APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
+
+  // ---- heads backward ----
+  TRY(k_heads_bwd(ctx, B, d.A, s.dlog, th + d.off_wpi, th + d.off_wv, s.dcore));
+  {
+    Epilogue e;
+    e.out = s.headw;
+    e.ldo = kHidden;
+    TRY(gemm_bf16(ctx, 16, kHidden, B, Operand{s.dhead, 16, true},
+                  Operand{s.core_bf, kHidden, true}, e, 256,
+                  splits_for(ctx, 16, kHidden, 256, B)));
+    float* bsum = s.colsum_part + 256 * kGates;
+    TRY(k_colsum(ctx, B, d.A + 1, s.dlog, d.A + 1, false, s.colsum_part, bsum, false));
+    TRY(k_head_grad_scatter(ctx, d.A, s.headw, bsum, G + d.off_wpi, G + d.off_bpi, G + d.off_wv,
+                            G + d.off_bv));
+  }
+
+  // ---- BPTT through the GRU ----
+  APPO_CUDA_TRY(cudaMemsetAsync(s.dnext, 0, sizeof(float) * n_traj * kHidden, st));
+  {
+    Epilogue e;
+    e.flags = EPI_ACCUM;
+    e.out = s.dnext;
+    e.ldo = kHidden;
+    for (int t = T - 1; t >= 0; --t) {
+      TRY(k_gru_bwd(ctx, n_traj, T, t, s.dcore, s.done, s.gates, s.hin, s.dnext, s.dgi, s.dgh));
+      if (t == 0) break;  // dh wrt h0 is not needed (h0 is data)
+      TRY(gemm_bf16(ctx, n_traj, kHidden, kGates,
+                    Operand{s.dgh + (size_t)t * kGates, (int64_t)T * kGates, false},
+                    Operand{wb + d.off_whh, kHidden, true}, e, 64, 4));
+    }
+  }
+  {
+    // dW_ih = dgi^T x, dW_hh = dgh^T h_in, biases = column sums
+    Epilogue e;
+    e.out = G + d.off_wih;
+    e.ldo = kHidden;
+    TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgi, kGates, true},
+                  Operand{s.x, kHidden, true}, e, 256, splits_for(ctx, kGates, kHidden, 256, B)));
+    e.out = G + d.off_whh;
+    TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgh, kGates, true},
+                  Operand{s.hbf, kHidden, true}, e, 256, splits_for(ctx, kGates, kHidden, 256, B)));
+    TRY(k_colsum(ctx, B, kGates, s.dgi, kGates, true, s.colsum_part, G + d.off_bih, false));
+    TRY(k_colsum(ctx, B, kGates, s.dgh, kGates, true, s.colsum_part, G + d.off_bhh, false));
+    // dx = dgi . W_ih, times ELU'(fc) -> dz_fc
+    Epilogue x;
+    x.flags = EPI_DELU | EPI_BF16;
+    x.aux = s.x;
+    x.ld_aux = kHidden;
+    x.out = s.dzfc;
+    x.ldo = kHidden;
+    TRY(gemm_bf16(ctx, B, kHidden, kGates, Operand{s.dgi, kGates, false},
+                  Operand{wb + d.off_wih, kHidden, true}, x, 128));
+  }
+  // ---- FC backward ----
+  {
+    Epilogue e;
+    e.out = G + d.off_fcw;
+    e.ldo = d.F;
+    TRY(gemm_bf16(ctx, kHidden, d.F, B, Operand{s.dzfc, kHidden, true},
+                  Operand{s.a3, d.F, true}, e, 256, splits_for(ctx, kHidden, d.F, 256, B)));
+    TRY(k_colsum(ctx, B, kHidden, s.dzfc, kHidden, true, s.colsum_part, G + d.off_fcb, false));
+    Epilogue x;
+    x.flags = EPI_DELU | EPI_BF16;
+    x.aux = s.a3;
+    x.ld_aux = d.F;
+    x.out = s.dz3;
+    x.ldo = d.F;
+    TRY(gemm_bf16(ctx, B, d.F, kHidden, Operand{s.dzfc, kHidden, false},
+                  Operand{wb + d.off_fcw, d.F, true}, x, 128));
+  }
+  // ---- conv3 backward ----
+  {
+    const int M3 = B * d.P3;
+    Epilogue e;
+    e.out = G + d.off_c3w;
+    e.ldo = 576;
+    TRY(gemm_bf16(ctx, 128, 576, M3, Operand{s.dz3, 128, true}, Operand{s.col3, 576, true}, e,
+                  192, splits_for(ctx, 128, 576, 192, M3)));
+    TRY(k_colsum(ctx, M3, 128, s.dz3, 128, true, s.colsum_part, G + d.off_c3b, false));
+    Epilogue x;
+    x.out = s.dcol3;
+    x.ldo = 576;
+    TRY(gemm_bf16(ctx, M3, 576, 128, Operand{s.dz3, 128, false},
+                  Operand{wb + d.off_c3w, 576, true}, x, 192));
+    TRY(k_col2im_delu(ctx, s.dcol3, s.a2, B, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.dz2));
+  }
+  // ---- conv2 backward ----
+  {
+    const int M2 = B * d.P2;
+    Epilogue e;
+    e.out = G + d.off_c2w;
+    e.ldo = 512;
+    TRY(gemm_bf16(ctx, 64, 512, M2, Operand{s.dz2, 64, true}, Operand{s.col2, 512, true}, e, 256,
+                  splits_for(ctx, 64, 512, 256, M2)));
+    TRY(k_colsum(ctx, M2, 64, s.dz2, 64, true, s.colsum_part, G + d.off_c2b, false));
+    Epilogue x;
+    x.out = s.dcol2;
+    x.ldo = 512;
+    TRY(gemm_bf16(ctx, M2, 512, 64, Operand{s.dz2, 64, false},
+                  Operand{wb + d.off_c2w, 512, true}, x, 256));
+    TRY(k_col2im_delu(ctx, s.dcol2, s.a1, B, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.dz1));
+  }
+  // ---- conv1 weight gradient (input is data) ----
+  {
+    const int M1 = B * d.P1;
+    Epilogue e;
+    e.scale = 1.0f / 255.0f;
+    e.out = G + d.off_c1w;
+    e.ldo = d.K1;
+    TRY(gemm_bf16(ctx, 32, d.K1, M1, Operand{s.dz1, 32, true}, Operand{s.col1, d.K1, true}, e,
+                  d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64,
+                  splits_for(ctx, 32, d.K1, d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64, M1)));
+    TRY(k_colsum(ctx, M1, 32, s.dz1, 32, true, s.colsum_part, G + d.off_c1b, false));
+  }
+
+  // ---- global-norm clip + Adam; publish into the other buffer ----
+  const int next = pub ^ 1;
+  M->adam_t += 1;
+  TRY(launch_adam(ctx, d.total, M->theta, M->m, M->v, G, M->adam_t, hp->lr, hp->beta1,
+                  hp->beta2, hp->eps, hp->grad_clip, s.stats + 8, M->pub_bf16[next],
+                  M->pub_f32[next]));
+  APPO_CUDA_TRY(cudaMemcpyAsync(s.h_stats, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost,
+                                st));
+  const int sync_st = appo_ctx_sync(ctx);
+  const double* hs = s.h_stats;
+  out->policy_loss = hs[0];
+  out->value_loss = hs[1];
+  out->entropy = hs[2];
+  out->total_loss = hs[3];
+  out->mean_ratio = hs[4];
+  out->lag_mean = hs[6];
+  out->lag_max = hs[7];
+  out->grad_norm = hs[8];
+  if (sync_st != APPO_OK) {
+    M->adam_t -= 1;  // optimizer_step threw: params untouched (adam kernel checks the flag)
+    out->version = M->version;
+    return sync_st;
+  }
+  M->published = next;
+  M->version += 1;
+  out->version = M->version;
+  return APPO_OK;
+}
+
+}  // extern "C"
+
+#include "../../include/appo_internal.h"
+extern "C" int appo_dbg_model_ptrs(appo_ctx* ctx, float** theta, float** grad, void** pub_bf16) {
+  MODEL_OR_RETURN(ctx);
+  if (theta) *theta = ctx->model->theta;
+  if (grad) *grad = ctx->model->grad;
+  if (pub_bf16) *pub_bf16 = ctx->model->pub_bf16[ctx->model->published];
+  return APPO_OK;
+}
+extern "C" int appo_dbg_copy_d2h(appo_ctx* ctx, void* h_dst, const void* d_src, uint64_t bytes) {
+  APPO_REQUIRE(ctx != nullptr, APPO_ERR_CONTRACT, "null ctx");
+  APPO_CUDA_TRY(cudaSetDevice(ctx->device));
+  APPO_CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return APPO_OK;
+}

@@ -1,0 +1,76 @@
+// Model state owned by a context: convnet_simple + GRU-512 + categorical head
+// (DESIGN.md §2), fp32 master parameters + Adam moments, the double-buffered
+// published copy read by inference (bf16 for GEMM weights, fp32 for the small
+// SIMT-consumed tensors), and activation scratch sized on demand.
+#pragma once
+#include <stdint.h>
+
+#include "appo_common.cuh"
+
+namespace appo_b200 {
+
+constexpr int kHidden = 512;
+constexpr int kGates = 3 * kHidden;
+
+struct Dims {
+  int C, H, W, A, T;
+  int H1, W1, P1, H2, W2, P2, H3, W3, P3;
+  int K1;  // C*64
+  int F;   // P3*128 (flatten)
+  int64_t off_c1w, off_c1b, off_c2w, off_c2b, off_c3w, off_c3b, off_fcw, off_fcb, off_wih,
+      off_whh, off_bih, off_bhh, off_wpi, off_bpi, off_wv, off_bv, total;
+  int64_t obs_dim;
+  uint64_t slot[10];  // layout v2 offsets
+};
+
+int make_dims(const appo_model_desc& d, Dims* out);
+
+// Scratch for a forward / learner pass over R encoder rows.
+struct Scratch {
+  int cap_rows = 0;  // encoder rows (images)
+  int cap_traj = 0;
+  uint16_t *col1 = nullptr, *a1 = nullptr, *col2 = nullptr, *a2 = nullptr, *col3 = nullptr,
+           *a3 = nullptr, *x = nullptr;  // bf16
+  float* gi = nullptr;                   // [R][1536]
+  float* gh = nullptr;                   // [R or n_traj][1536]
+  uint16_t* hbf = nullptr;               // [R][512] bf16 h inputs
+  // learner-only
+  float *core = nullptr, *gates = nullptr, *hin = nullptr, *hcur = nullptr;  // fp32
+  uint16_t* core_bf = nullptr;
+  float *logits = nullptr, *values = nullptr;
+  float *tlogp = nullptr, *ent = nullptr, *vt = nullptr, *pg = nullptr, *adv = nullptr;
+  float *rew = nullptr, *blogp = nullptr;
+  int32_t* act = nullptr;
+  uint8_t* done = nullptr;
+  int64_t* ver = nullptr;
+  float* dlog = nullptr;        // [B][A+1] fp32
+  uint16_t* dhead = nullptr;    // [B][16] bf16
+  float* dcore = nullptr;       // [B][512]
+  float* dnext = nullptr;       // [n_traj][512]
+  uint16_t *dgi = nullptr, *dgh = nullptr;  // [B][1536] bf16
+  uint16_t *dzfc = nullptr, *dz3 = nullptr, *dz2 = nullptr, *dz1 = nullptr;
+  float *dcol3 = nullptr, *dcol2 = nullptr;
+  float* headw = nullptr;       // [16][512]
+  float* colsum_part = nullptr; // partials for bias grads
+  int32_t* slot_ids = nullptr;
+  double* stats = nullptr;      // device stats block
+  double* h_stats = nullptr;    // pinned
+};
+
+struct Model {
+  Dims d;
+  float* theta = nullptr;  // fp32 master [P]
+  float* m = nullptr;
+  float* v = nullptr;
+  float* grad = nullptr;
+  uint16_t* pub_bf16[2] = {nullptr, nullptr};
+  float* pub_f32[2] = {nullptr, nullptr};
+  int published = 0;
+  int64_t version = 0;
+  int64_t adam_t = 0;
+  uint64_t sample_key = 0;
+  Scratch si;  // inference scratch
+  Scratch sl;  // learner scratch
+};
+
+}  // namespace appo_b200

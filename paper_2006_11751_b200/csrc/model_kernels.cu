@@ -1,0 +1,642 @@
+// SIMT kernels around the tcgen05 GEMMs of the model: im2col / col2im(+ELU'),
+// the GRU cell (inference: fused with heads + sampling; training: with saved
+// gates and done-masked recurrence), heads forward/backward, the fused PPO
+// loss, slot gathers, column sums for bias gradients.
+//
+// All of these are HBM/latency-bound elementwise or small-reduction kernels:
+// coalesced along the innermost (channel / hidden) dimension, 16-byte vector
+// accesses where the layout allows it.
+#include <cuda_bf16.h>
+
+#include "model_kernels.cuh"
+
+namespace appo_b200 {
+namespace {
+
+__device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+__device__ __forceinline__ uint16_t f2bf(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+__device__ __forceinline__ const uint8_t* obs_ptr(const ObsSrc& o, int64_t r) {
+  if (!o.slot_ids) return o.base + r * o.img_stride;
+  const int64_t B = (int64_t)o.n_traj * o.T;
+  if (r < B) {
+    const int64_t i = r / o.T, t = r % o.T;
+    return o.base + (uint64_t)o.slot_ids[i] * o.slot_bytes + o.obs_off + t * o.obs_dim;
+  }
+  return o.base + (uint64_t)o.slot_ids[r - B] * o.slot_bytes + o.boot_off;
+}
+
+// conv1 im2col from u8 CHW images: col[r*P1 + y*W1 + x][(c*8 + kh)*8 + kw] = obs[c][4y+kh][4x+kw]
+// (values kept as exact integers 0..255 in bf16; the 1/255 is folded into the
+// GEMM epilogue scale).  One thread = one (row, c, kh): 8 bytes in, 16 B out.
+__global__ void im2col_u8_kernel(ObsSrc src, int64_t R, int C, int H, int W, int H1, int W1,
+                                 uint16_t* __restrict__ col) {
+  const int64_t P1 = (int64_t)H1 * W1;
+  const int64_t total = R * P1 * C * 8;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int ckh = (int)(g % (C * 8));
+    const int64_t row = g / (C * 8);
+    const int64_t r = row / P1;
+    const int p = (int)(row % P1);
+    const int y = p / W1, x = p % W1;
+    const int c = ckh >> 3, kh = ckh & 7;
+    const uint8_t* img = obs_ptr(src, r);
+    const uint8_t* s = img + ((int64_t)c * H + (y * 4 + kh)) * W + x * 4;
+    const uint32_t lo = *reinterpret_cast<const uint32_t*>(s);
+    const uint32_t hi = *reinterpret_cast<const uint32_t*>(s + 4);
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t word = j < 2 ? lo : hi;
+      const int sh = (j & 1) * 16;
+      const float f0 = (float)((word >> sh) & 0xFF);
+      const float f1 = (float)((word >> (sh + 8)) & 0xFF);
+      w[j] = (uint32_t)f2bf(f0) | ((uint32_t)f2bf(f1) << 16);
+    }
+    *reinterpret_cast<uint4*>(col + row * (C * 64) + ckh * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// NHWC im2col: col[r*Po + y*Wo + x][(kh*k + kw)*Cin + ci] = act[r][sy+kh][sx+kw][ci]
+// One thread = 8 channels (16 B).
+__global__ void im2col_nhwc_kernel(const uint16_t* __restrict__ act, int64_t R, int Hi, int Wi,
+                                   int Cin, int k, int s, int Ho, int Wo,
+                                   uint16_t* __restrict__ col) {
+  const int cg = Cin / 8;
+  const int64_t Po = (int64_t)Ho * Wo;
+  const int64_t total = R * Po * k * k * cg;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(g % cg);
+    int64_t rest = g / cg;
+    const int kk = (int)(rest % (k * k));
+    const int64_t row = rest / (k * k);
+    const int64_t r = row / Po;
+    const int p = (int)(row % Po);
+    const int y = p / Wo, x = p % Wo, kh = kk / k, kw = kk % k;
+    const uint4 v = *reinterpret_cast<const uint4*>(
+        act + (((r * Hi) + (y * s + kh)) * Wi + (x * s + kw)) * Cin + c8 * 8);
+    *reinterpret_cast<uint4*>(col + row * (int64_t)(k * k * Cin) + kk * Cin + c8 * 8) = v;
+  }
+}
+
+// Backward of im2col (gather form) fused with ELU': for each input element
+// dz[r][yi][xi][ci] = aprev'(.) * sum_{kh,kw: (yi-kh)%s==0, (xi-kw)%s==0} dcol[row(yo,xo)][(kh*k+kw)*Cin+ci]
+__global__ void col2im_delu_kernel(const float* __restrict__ dcol,
+                                   const uint16_t* __restrict__ aprev, int64_t R, int Hi, int Wi,
+                                   int Cin, int k, int s, int Ho, int Wo,
+                                   uint16_t* __restrict__ dz) {
+  const int64_t total = R * Hi * Wi * Cin;
+  const int K = k * k * Cin;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int ci = (int)(g % Cin);
+    int64_t rest = g / Cin;
+    const int xi = (int)(rest % Wi);
+    rest /= Wi;
+    const int yi = (int)(rest % Hi);
+    const int64_t r = rest / Hi;
+    float acc = 0.0f;
+    for (int kh = yi % s; kh < k; kh += s) {
+      const int yo = (yi - kh) / s;
+      if (yo < 0 || yo >= Ho) continue;
+      for (int kw = xi % s; kw < k; kw += s) {
+        const int xo = (xi - kw) / s;
+        if (xo < 0 || xo >= Wo) continue;
+        acc += dcol[(r * Ho * Wo + (int64_t)yo * Wo + xo) * K + (kh * k + kw) * Cin + ci];
+      }
+    }
+    const float a = bf2f(aprev[g]);
+    dz[g] = f2bf(acc * (a > 0.0f ? 1.0f : a + 1.0f));
+  }
+}
+
+__global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int64_t src_ld,
+                                   uint16_t* __restrict__ dst, int64_t dst_ld, int cols) {
+  const int64_t total = n * cols;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = g / cols;
+    const int c = (int)(g % cols);
+    dst[r * dst_ld + c] = f2bf(src[r * src_ld + c]);
+  }
+}
+
+// GRU cell (PyTorch gate order r, z, n) + heads + sampling for inference.
+// One warp per env; lane owns hidden units j = lane + 32q.
+__global__ void __launch_bounds__(256)
+    gru_infer_kernel(int B, int A, const float* __restrict__ gi, const float* __restrict__ gh,
+                     const float* __restrict__ h_in, const float* __restrict__ wpi,
+                     const float* __restrict__ bpi, const float* __restrict__ wv,
+                     const float* __restrict__ bv, uint64_t key, uint64_t counter0,
+                     float* __restrict__ h_out, int32_t* __restrict__ actions,
+                     float* __restrict__ logp, float* __restrict__ values,
+                     float* __restrict__ logits_out) {
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const float* gib = gi + (int64_t)b * kGates;
+  const float* ghb = gh + (int64_t)b * kGates;
+  float acc[kMaxActions + 1];
+#pragma unroll
+  for (int a = 0; a <= kMaxActions; ++a) acc[a] = 0.0f;
+#pragma unroll 4
+  for (int q = 0; q < kHidden / 32; ++q) {
+    const int j = lane + 32 * q;
+    const float r = sigmoidf_(gib[j] + ghb[j]);
+    const float z = sigmoidf_(gib[kHidden + j] + ghb[kHidden + j]);
+    const float n = tanhf(gib[2 * kHidden + j] + r * ghb[2 * kHidden + j]);
+    const float h = (1.0f - z) * n + z * h_in[(int64_t)b * kHidden + j];
+    h_out[(int64_t)b * kHidden + j] = h;
+#pragma unroll
+    for (int a = 0; a < kMaxActions; ++a)
+      if (a < A) acc[a] += wpi[a * kHidden + j] * h;
+    acc[kMaxActions] += wv[j] * h;
+  }
+#pragma unroll
+  for (int a = 0; a <= kMaxActions; ++a) acc[a] = warp_sum(acc[a]);
+  if (lane == 0) {
+    double lg[kMaxActions];
+    double mx = -1e300;
+    for (int a = 0; a < A; ++a) {
+      lg[a] = (double)(acc[a] + bpi[a]);
+      mx = fmax(mx, lg[a]);
+      if (logits_out) logits_out[(int64_t)b * A + a] = (float)lg[a];
+    }
+    values[b] = acc[kMaxActions] + bv[0];
+    double z = 0;
+    for (int a = 0; a < A; ++a) z += exp(lg[a] - mx);
+    const double u = uniform01(key, counter0 + (uint64_t)b);
+    double cum = 0;
+    int chosen = A - 1;
+    for (int a = 0; a < A; ++a) {
+      cum += exp(lg[a] - mx) / z;
+      if (u < cum) {
+        chosen = a;
+        break;
+      }
+    }
+    actions[b] = chosen;
+    logp[b] = (float)log(fmax(exp(lg[chosen] - mx) / z, 1e-300));
+  }
+}
+
+// Stage h for GRU step t: hbf/hin rows <- hcur (fp32 -> bf16 + fp32 copy).
+__global__ void stage_h_kernel(int n_traj, int T, int t, const float* __restrict__ hcur,
+                               float* __restrict__ hin, uint16_t* __restrict__ hbf) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_traj * kHidden) return;
+  const int i = g / kHidden, j = g % kHidden;
+  const int64_t row = (t < T) ? (int64_t)i * T + t : (int64_t)n_traj * T + i;
+  const float h = hcur[g];
+  hin[row * kHidden + j] = h;
+  hbf[row * kHidden + j] = f2bf(h);
+}
+
+// Training GRU cell at step t for all trajectories; saves gates for BPTT
+// and advances hcur with the reset-after-done mask (orchestrator.hpp:402).
+__global__ void gru_train_kernel(int n_traj, int T, int t, const float* __restrict__ gi,
+                                 const float* __restrict__ gh, const uint8_t* __restrict__ done,
+                                 float* __restrict__ hcur, float* __restrict__ core,
+                                 uint16_t* __restrict__ core_bf, float* __restrict__ gates) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_traj * kHidden) return;
+  const int i = g / kHidden, j = g % kHidden;
+  const int64_t row = (t < T) ? (int64_t)i * T + t : (int64_t)n_traj * T + i;
+  const float* gir = gi + row * kGates;
+  const float* ghr = gh + (int64_t)i * kGates;
+  const float r = sigmoidf_(gir[j] + ghr[j]);
+  const float z = sigmoidf_(gir[kHidden + j] + ghr[kHidden + j]);
+  const float ghn = ghr[2 * kHidden + j];
+  const float n = tanhf(gir[2 * kHidden + j] + r * ghn);
+  const float hprev = hcur[g];
+  const float h = (1.0f - z) * n + z * hprev;
+  core[row * kHidden + j] = h;
+  core_bf[row * kHidden + j] = f2bf(h);
+  float* gs = gates + row * 4 * kHidden;
+  gs[j] = r;
+  gs[kHidden + j] = z;
+  gs[2 * kHidden + j] = n;
+  gs[3 * kHidden + j] = ghn;
+  if (t < T) hcur[g] = done[(int64_t)i * T + t] ? 0.0f : h;
+}
+
+// Heads forward: one warp per row.
+__global__ void __launch_bounds__(256)
+    heads_fwd_kernel(int64_t R, int A, const float* __restrict__ core,
+                     const float* __restrict__ wpi, const float* __restrict__ bpi,
+                     const float* __restrict__ wv, const float* __restrict__ bv,
+                     float* __restrict__ logits, float* __restrict__ values) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= R) return;
+  float acc[kMaxActions + 1];
+#pragma unroll
+  for (int a = 0; a <= kMaxActions; ++a) acc[a] = 0.0f;
+  for (int q = 0; q < kHidden / 32; ++q) {
+    const int j = lane + 32 * q;
+    const float h = core[row * kHidden + j];
+#pragma unroll
+    for (int a = 0; a < kMaxActions; ++a)
+      if (a < A) acc[a] += wpi[a * kHidden + j] * h;
+    acc[kMaxActions] += wv[j] * h;
+  }
+#pragma unroll
+  for (int a = 0; a <= kMaxActions; ++a) acc[a] = warp_sum(acc[a]);
+  if (lane == 0) {
+    for (int a = 0; a < A; ++a) logits[row * A + a] = acc[a] + bpi[a];
+    values[row] = acc[kMaxActions] + bv[0];
+  }
+}
+
+// Gather per-step scalars and h0 from trajectory slots (layout v2) in FIFO
+// order: s = i*T + t (orchestrator.hpp:781-795).  One block per trajectory.
+__global__ void gather_slots_kernel(int n_traj, int T, const uint8_t* __restrict__ region,
+                                    uint64_t slot_bytes, const int32_t* __restrict__ slot_ids,
+                                    SlotOffsets off, int32_t* __restrict__ act,
+                                    float* __restrict__ rew, float* __restrict__ blogp,
+                                    uint8_t* __restrict__ done, int64_t* __restrict__ ver,
+                                    float* __restrict__ h0, int* flags) {
+  const int i = blockIdx.x;
+  if (i >= n_traj) return;
+  const uint8_t* slot = region + (uint64_t)slot_ids[i] * slot_bytes;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int64_t s = (int64_t)i * T + t;
+    act[s] = reinterpret_cast<const int32_t*>(slot + off.actions)[t];
+    const float rw = reinterpret_cast<const float*>(slot + off.rewards)[t];
+    const float lp = reinterpret_cast<const float*>(slot + off.logp)[t];
+    rew[s] = rw;
+    blogp[s] = lp;
+    done[s] = slot[off.dones + t];
+    ver[s] = reinterpret_cast<const int64_t*>(slot + off.versions)[t];
+    if (!finitef(rw) || !finitef(lp)) atomicOr(flags + kFlagNumeric, 1);
+  }
+  for (int j = threadIdx.x; j < kHidden; j += blockDim.x)
+    h0[(int64_t)i * kHidden + j] = reinterpret_cast<const float*>(slot + off.hidden)[j];
+}
+
+// Advantage normalisation (orchestrator.hpp:838-845), one block.
+__global__ void normalize_kernel(int n, float* __restrict__ adv) {
+  __shared__ double sh[32];
+  __shared__ double mean_s, sd_s;
+  double s = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += adv[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    mean_s = t / n;
+  }
+  __syncthreads();
+  const double mean = mean_s;
+  double q = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) q += (adv[i] - mean) * (adv[i] - mean);
+  q = warp_sum(q);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    sd_s = sqrt(t / n) + 1e-8;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) adv[i] = (float)((adv[i] - mean) / sd_s);
+}
+
+// Fused PPO / value / entropy loss and its gradient wrt logits and value
+// (policy.hpp:323-375).  One thread per sample; partial sums (policy, value,
+// entropy, ratio) -> deterministic last-block reduce into stats[0..4].
+__global__ void __launch_bounds__(256)
+    ppo_loss_kernel(int B, int A, const float* __restrict__ logits,
+                    const float* __restrict__ values, const int32_t* __restrict__ act,
+                    const float* __restrict__ blogp, const float* __restrict__ adv,
+                    const float* __restrict__ vt, LossHP hp, float* __restrict__ dlog,
+                    uint16_t* __restrict__ dhead, double* partials, unsigned* counter,
+                    double* stats, int* flags) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[4] = {0, 0, 0, 0};
+  if (s < B) {
+    const float* lg = logits + (int64_t)s * A;
+    const int a_s = act[s];
+    if (a_s < 0 || a_s >= A) atomicOr(flags + kFlagContract, 1);
+    double mx = lg[0];
+    for (int a = 1; a < A; ++a) mx = fmax(mx, (double)lg[a]);
+    double z = 0;
+    for (int a = 0; a < A; ++a) z += exp((double)lg[a] - mx);
+    double p[kMaxActions], H = 0;
+    for (int a = 0; a < A; ++a) {
+      p[a] = exp((double)lg[a] - mx) / z;
+      if (p[a] > 0) H -= p[a] * log(p[a]);
+    }
+    const int ac = min(max(a_s, 0), A - 1);
+    const double logp = log(fmax(p[ac], 1e-300));
+    double d = logp - (double)blogp[s];
+    d = fmin(fmax(d, -20.0), 20.0);
+    const double ratio = exp(d);
+    const double A_s = adv[s];
+    const double cl = fmin(fmax(ratio, (double)hp.clip_low), (double)hp.clip_high);
+    const double sur = fmin(ratio * A_s, cl * A_s);
+    const double dsur = (ratio * A_s <= cl * A_s) ? A_s : 0.0;  // ties -> unclipped
+    const double invB = 1.0 / B;
+    const double dL_dlogp = -invB * dsur * ratio;
+    const double verr = (double)values[s] - (double)vt[s];
+    const double dV = hp.value_coef * invB * 2.0 * verr;
+    for (int a = 0; a < A; ++a) {
+      const double dlp = (a == ac ? 1.0 : 0.0) - p[a];
+      const double dH = p[a] > 0 ? -p[a] * (log(p[a]) + H) : 0.0;
+      const float g = (float)(dL_dlogp * dlp - hp.entropy_coef * invB * dH);
+      dlog[(int64_t)s * (A + 1) + a] = g;
+      dhead[(int64_t)s * 16 + a] = f2bf(g);
+    }
+    dlog[(int64_t)s * (A + 1) + A] = (float)dV;
+    dhead[(int64_t)s * 16 + A] = f2bf((float)dV);
+    for (int a = A + 1; a < 16; ++a) dhead[(int64_t)s * 16 + a] = 0;
+    acc[0] = -sur;
+    acc[1] = verr * verr;
+    acc[2] = H;
+    acc[3] = ratio;
+  }
+  // block reduce + last block
+  __shared__ double sh[8][4];
+  __shared__ bool last;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] = warp_sum(acc[k]);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[threadIdx.x >> 5][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 4; ++k) {
+      double t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w][k];
+      partials[blockIdx.x * 4 + k] = t;
+    }
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t[4] = {0, 0, 0, 0};
+    for (unsigned b = 0; b < gridDim.x; ++b)
+      for (int k = 0; k < 4; ++k) t[k] += ((volatile double*)partials)[b * 4 + k];
+    const double invB = 1.0 / B;
+    stats[0] = t[0] * invB;
+    stats[1] = hp.value_coef * t[1] * invB;
+    stats[2] = t[2] * invB;
+    stats[3] = stats[0] + stats[1] - hp.entropy_coef * stats[2];
+    stats[4] = t[3] * invB;
+    if (!isfinite(stats[3])) atomicOr(flags + kFlagNumeric, 1);
+    *counter = 0;
+  }
+}
+
+// dcore[s][j] = sum_a dlog[s][a] * wpi[a][j] + dV[s] * wv[j]; warp per row.
+__global__ void __launch_bounds__(256)
+    heads_bwd_kernel(int B, int A, const float* __restrict__ dlog, const float* __restrict__ wpi,
+                     const float* __restrict__ wv, float* __restrict__ dcore) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= B) return;
+  float dl[kMaxActions + 1];
+  for (int a = 0; a <= A; ++a) dl[a] = dlog[(int64_t)s * (A + 1) + a];
+  for (int q = 0; q < kHidden / 32; ++q) {
+    const int j = lane + 32 * q;
+    float acc = dl[A] * wv[j];
+    for (int a = 0; a < A; ++a) acc += dl[a] * wpi[a * kHidden + j];
+    dcore[(int64_t)s * kHidden + j] = acc;
+  }
+}
+
+// One reverse BPTT step at time t (oracle orc_learner_step): dh = dcore + keep*dnext;
+// gate gradients -> dgi / dgh rows (bf16); dnext <- dh*z (the GEMM then adds dgh . W_hh).
+__global__ void gru_bwd_kernel(int n_traj, int T, int t, const float* __restrict__ dcore,
+                               const uint8_t* __restrict__ done, const float* __restrict__ gates,
+                               const float* __restrict__ hin, float* __restrict__ dnext,
+                               uint16_t* __restrict__ dgi, uint16_t* __restrict__ dgh) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_traj * kHidden) return;
+  const int i = g / kHidden, j = g % kHidden;
+  const int64_t s = (int64_t)i * T + t;
+  const float keep = done[s] ? 0.0f : 1.0f;
+  const float dh = dcore[s * kHidden + j] + keep * dnext[g];
+  const float* gs = gates + s * 4 * kHidden;
+  const float r = gs[j], z = gs[kHidden + j], n = gs[2 * kHidden + j], ghn = gs[3 * kHidden + j];
+  const float hp = hin[s * kHidden + j];
+  const float dn = dh * (1.0f - z);
+  const float dz = dh * (hp - n);
+  const float dan = dn * (1.0f - n * n);
+  const float dr = dan * ghn;
+  const float dgr = dr * r * (1.0f - r);
+  const float dgz = dz * z * (1.0f - z);
+  uint16_t* gi_row = dgi + s * kGates;
+  uint16_t* gh_row = dgh + s * kGates;
+  gi_row[j] = f2bf(dgr);
+  gi_row[kHidden + j] = f2bf(dgz);
+  gi_row[2 * kHidden + j] = f2bf(dan);
+  gh_row[j] = f2bf(dgr);
+  gh_row[kHidden + j] = f2bf(dgz);
+  gh_row[2 * kHidden + j] = f2bf(dan * r);
+  dnext[g] = dh * z;
+}
+
+// Column sums (bias gradients): partial[chunk][n] over row chunks, then reduce.
+template <bool BF16>
+__global__ void colsum_partial_kernel(int64_t M, int N, const void* __restrict__ src,
+                                      int64_t ld, int rows_per_chunk, float* __restrict__ part) {
+  const int n = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int grp = threadIdx.x >> 5;  // 8 row groups
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t r1 = min(r0 + rows_per_chunk, M);
+  float acc = 0.0f;
+  if (n < N) {
+    for (int64_t r = r0 + grp; r < r1; r += 8) {
+      acc += BF16 ? bf2f(reinterpret_cast<const uint16_t*>(src)[r * ld + n])
+                  : reinterpret_cast<const float*>(src)[r * ld + n];
+    }
+  }
+  __shared__ float sh[8][32];
+  sh[grp][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (grp == 0 && n < N) {
+    float t = 0;
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
+    part[(int64_t)blockIdx.y * N + n] = t;
+  }
+}
+__global__ void colsum_final_kernel(int N, int chunks, const float* __restrict__ part,
+                                    float* __restrict__ out, int accumulate) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float t = 0;
+  for (int c = 0; c < chunks; ++c) t += part[(int64_t)c * N + n];
+  out[n] = accumulate ? out[n] + t : t;
+}
+
+// Scatter the padded head-weight gradient [16][512] (rows 0..A-1 policy, row A
+// value) into the flat gradient and add the head bias gradients.
+__global__ void head_grad_scatter_kernel(int A, const float* __restrict__ headw,
+                                         const float* __restrict__ bias_sums, float* gwpi,
+                                         float* gbpi, float* gwv, float* gbv) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < A * kHidden) gwpi[g] = headw[g];
+  if (g < kHidden) gwv[g] = headw[A * kHidden + g];
+  if (g < A) gbpi[g] = bias_sums[g];
+  if (g == 0) gbv[0] = bias_sums[A];
+}
+
+// Version lag statistics (orchestrator.hpp:790,862-863), one block.
+__global__ void lag_kernel(int B, const int64_t* __restrict__ ver, int64_t cur, double* stats) {
+  __shared__ double sh[32];
+  __shared__ long long mn[32];
+  double s = 0;
+  long long m = LLONG_MAX;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    s += (double)(cur - ver[i]);
+    m = min(m, (long long)ver[i]);
+  }
+  s = warp_sum(s);
+  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) {
+    sh[threadIdx.x >> 5] = s;
+    mn[threadIdx.x >> 5] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    long long mm = LLONG_MAX;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t += sh[w];
+      mm = min(mm, mn[w]);
+    }
+    stats[6] = B > 0 ? t / B : 0.0;
+    stats[7] = B > 0 ? (double)(cur - mm) : 0.0;
+  }
+}
+
+int grid_for(int64_t n, int block, int max_blocks) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  return (int)(g < max_blocks ? g : max_blocks);
+}
+
+}  // namespace
+
+int k_im2col_u8(Ctx* c, const ObsSrc& src, int64_t R, const Dims& d, uint16_t* col) {
+  const int64_t n = R * d.P1 * d.C * 8;
+  APPO_LAUNCH(c, im2col_u8_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, src, R, d.C, d.H,
+              d.W, d.H1, d.W1, col);
+  return APPO_OK;
+}
+int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Cin, int k, int s,
+                  int Ho, int Wo, uint16_t* col) {
+  const int64_t n = R * Ho * Wo * k * k * (Cin / 8);
+  APPO_LAUNCH(c, im2col_nhwc_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, act, R, Hi, Wi,
+              Cin, k, s, Ho, Wo, col);
+  return APPO_OK;
+}
+int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
+                  int Cin, int k, int s, int Ho, int Wo, uint16_t* dz) {
+  const int64_t n = R * Hi * Wi * Cin;
+  APPO_LAUNCH(c, col2im_delu_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev, R,
+              Hi, Wi, Cin, k, s, Ho, Wo, dz);
+  return APPO_OK;
+}
+int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
+                  int64_t dst_ld, int cols) {
+  APPO_LAUNCH(c, f32_to_bf16_kernel, grid_for(rows * cols, 256, c->num_sms * 16), 256, 0, rows,
+              src, src_ld, dst, dst_ld, cols);
+  return APPO_OK;
+}
+int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const float* h_in,
+                const float* wpi, const float* bpi, const float* wv, const float* bv,
+                uint64_t key, uint64_t counter0, float* h_out, int32_t* actions, float* logp,
+                float* values, float* logits) {
+  APPO_LAUNCH(c, gru_infer_kernel, (B + 7) / 8, 256, 0, B, A, gi, gh, h_in, wpi, bpi, wv, bv,
+              key, counter0, h_out, actions, logp, values, logits);
+  return APPO_OK;
+}
+int k_stage_h(Ctx* c, int n_traj, int T, int t, const float* hcur, float* hin, uint16_t* hbf) {
+  APPO_LAUNCH(c, stage_h_kernel, (n_traj * kHidden + 255) / 256, 256, 0, n_traj, T, t, hcur, hin,
+              hbf);
+  return APPO_OK;
+}
+int k_gru_train(Ctx* c, int n_traj, int T, int t, const float* gi, const float* gh,
+                const uint8_t* done, float* hcur, float* core, uint16_t* core_bf, float* gates) {
+  APPO_LAUNCH(c, gru_train_kernel, (n_traj * kHidden + 255) / 256, 256, 0, n_traj, T, t, gi, gh,
+              done, hcur, core, core_bf, gates);
+  return APPO_OK;
+}
+int k_heads_fwd(Ctx* c, int64_t R, int A, const float* core, const float* wpi, const float* bpi,
+                const float* wv, const float* bv, float* logits, float* values) {
+  APPO_LAUNCH(c, heads_fwd_kernel, (int)((R + 7) / 8), 256, 0, R, A, core, wpi, bpi, wv, bv,
+              logits, values);
+  return APPO_OK;
+}
+int k_gather_slots(Ctx* c, int n_traj, int T, const uint8_t* region, uint64_t slot_bytes,
+                   const int32_t* slot_ids, const SlotOffsets& off, int32_t* act, float* rew,
+                   float* blogp, uint8_t* done, int64_t* ver, float* h0) {
+  APPO_LAUNCH(c, gather_slots_kernel, n_traj, 128, 0, n_traj, T, region, slot_bytes, slot_ids,
+              off, act, rew, blogp, done, ver, h0, c->d_flags);
+  return APPO_OK;
+}
+int k_normalize(Ctx* c, int n, float* adv) {
+  APPO_LAUNCH(c, normalize_kernel, 1, 1024, 0, n, adv);
+  return APPO_OK;
+}
+int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
+               const int32_t* act, const float* blogp, const float* adv, const float* vt,
+               const LossHP& hp, float* dlog, uint16_t* dhead, double* stats) {
+  const int grid = (B + 255) / 256;
+  APPO_LAUNCH(c, ppo_loss_kernel, grid, 256, 0, B, A, logits, values, act, blogp, adv, vt, hp,
+              dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags);
+  return APPO_OK;
+}
+int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,
+                float* dcore) {
+  APPO_LAUNCH(c, heads_bwd_kernel, (B + 7) / 8, 256, 0, B, A, dlog, wpi, wv, dcore);
+  return APPO_OK;
+}
+int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,
+              const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh) {
+  APPO_LAUNCH(c, gru_bwd_kernel, (n_traj * kHidden + 255) / 256, 256, 0, n_traj, T, t, dcore,
+              done, gates, hin, dnext, dgi, dgh);
+  return APPO_OK;
+}
+int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, float* part,
+             float* out, bool accumulate) {
+  int chunks = (int)((M + 255) / 256);
+  if (chunks > 256) chunks = 256;
+  if (chunks < 1) chunks = 1;
+  const int rows_per_chunk = (int)((M + chunks - 1) / chunks);
+  dim3 grid((N + 31) / 32, chunks);
+  if (bf16)
+    APPO_LAUNCH(c, colsum_partial_kernel<true>, grid, 256, 0, M, N, src, ld, rows_per_chunk,
+                part);
+  else
+    APPO_LAUNCH(c, colsum_partial_kernel<false>, grid, 256, 0, M, N, src, ld, rows_per_chunk,
+                part);
+  APPO_LAUNCH(c, colsum_final_kernel, (N + 255) / 256, 256, 0, N, chunks, part, out,
+              accumulate ? 1 : 0);
+  return APPO_OK;
+}
+int k_head_grad_scatter(Ctx* c, int A, const float* headw, const float* bias_sums, float* gwpi,
+                        float* gbpi, float* gwv, float* gbv) {
+  APPO_LAUNCH(c, head_grad_scatter_kernel, (A * kHidden + 255) / 256, 256, 0, A, headw,
+              bias_sums, gwpi, gbpi, gwv, gbv);
+  return APPO_OK;
+}
+int k_lag(Ctx* c, int B, const int64_t* ver, int64_t cur, double* stats) {
+  APPO_LAUNCH(c, lag_kernel, 1, 1024, 0, B, ver, cur, stats);
+  return APPO_OK;
+}
+
+}  // namespace appo_b200

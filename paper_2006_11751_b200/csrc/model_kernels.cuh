@@ -1,0 +1,64 @@
+// Launchers for the model's SIMT kernels (model_kernels.cu).
+#pragma once
+#include <stdint.h>
+
+#include "model.cuh"
+
+namespace appo_b200 {
+
+constexpr int kMaxActions = 16;
+
+// Where encoder images come from: contiguous [R][obs_dim] (slot_ids == null)
+// or trajectory slots (layout v2): rows 0..n_traj*T-1 are steps s = i*T + t,
+// rows n_traj*T + i are the bootstrap observations.
+struct ObsSrc {
+  const uint8_t* base = nullptr;
+  int64_t img_stride = 0;
+  const int32_t* slot_ids = nullptr;
+  uint64_t slot_bytes = 0, obs_off = 0, boot_off = 0;
+  int T = 0, n_traj = 0;
+  int64_t obs_dim = 0;
+};
+
+struct SlotOffsets {
+  uint64_t obs, hidden, actions, rewards, logp, dones, versions, boot_obs, boot_hidden, total;
+};
+
+struct LossHP {
+  float clip_low, clip_high, value_coef, entropy_coef;
+};
+
+int k_im2col_u8(Ctx* c, const ObsSrc& src, int64_t R, const Dims& d, uint16_t* col);
+int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Cin, int k, int s,
+                  int Ho, int Wo, uint16_t* col);
+int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
+                  int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
+int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
+                  int64_t dst_ld, int cols);
+int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const float* h_in,
+                const float* wpi, const float* bpi, const float* wv, const float* bv,
+                uint64_t key, uint64_t counter0, float* h_out, int32_t* actions, float* logp,
+                float* values, float* logits);
+int k_stage_h(Ctx* c, int n_traj, int T, int t, const float* hcur, float* hin, uint16_t* hbf);
+int k_gru_train(Ctx* c, int n_traj, int T, int t, const float* gi, const float* gh,
+                const uint8_t* done, float* hcur, float* core, uint16_t* core_bf, float* gates);
+int k_heads_fwd(Ctx* c, int64_t R, int A, const float* core, const float* wpi, const float* bpi,
+                const float* wv, const float* bv, float* logits, float* values);
+int k_gather_slots(Ctx* c, int n_traj, int T, const uint8_t* region, uint64_t slot_bytes,
+                   const int32_t* slot_ids, const SlotOffsets& off, int32_t* act, float* rew,
+                   float* blogp, uint8_t* done, int64_t* ver, float* h0);
+int k_normalize(Ctx* c, int n, float* adv);
+int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
+               const int32_t* act, const float* blogp, const float* adv, const float* vt,
+               const LossHP& hp, float* dlog, uint16_t* dhead, double* stats);
+int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,
+                float* dcore);
+int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,
+              const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh);
+int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, float* part,
+             float* out, bool accumulate);
+int k_head_grad_scatter(Ctx* c, int A, const float* headw, const float* bias_sums, float* gwpi,
+                        float* gbpi, float* gwv, float* gbv);
+int k_lag(Ctx* c, int B, const int64_t* ver, int64_t cur, double* stats);
+
+}  // namespace appo_b200

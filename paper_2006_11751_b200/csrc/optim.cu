@@ -1,0 +1,101 @@
+// Global-norm clip + Adam (optimizer_step, policy.hpp:431-455) over the flat
+// fp32 parameter vector.  Two launches, no host round trip:
+//   1. sum of squares (fp64 partials, deterministic last-block reduce) + finite
+//      check -> d_norm_out[0] = ||g||, d_norm_out[1] = clip scale;
+//   2. fused elementwise update reading the scale from device memory; writes
+//      theta, m, v and (optionally) the bf16 inference copy the policy forward
+//      reads (the "publish" of ParamStore, policy.hpp:487-494, without a copy).
+// HBM-bound: 4 B grad + 3x(4 B read + 4 B write) + 2 B bf16 = 30 B / parameter.
+#include <cuda_bf16.h>
+
+#include "appo_common.cuh"
+
+namespace appo_b200 {
+namespace {
+
+__global__ void __launch_bounds__(256)
+    sumsq_kernel(int64_t n, const float* __restrict__ g, double* partials, unsigned* counter,
+                 double* norm_out, float clip, int* flags) {
+  double acc = 0.0;
+  bool bad = false;
+  const int64_t n4 = (reinterpret_cast<uintptr_t>(g) & 15) ? 0 : (n >> 2);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 x = g4[i];
+    bad |= !(finitef(x.x) && finitef(x.y) && finitef(x.z) && finitef(x.w));
+    acc += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bad |= !finitef(g[i]);
+    acc += (double)g[i] * g[i];
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags + kFlagNumeric, 1);
+  // block reduce
+  __shared__ double sh[32];
+  __shared__ bool last;
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double*)partials)[b];
+    const double norm = sqrt(s);
+    double scale = 1.0;
+    if (clip > 0.0f && norm > (double)clip) scale = (double)clip / norm;
+    norm_out[0] = norm;
+    norm_out[1] = scale;
+    *counter = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    adam_kernel(int64_t n, float* __restrict__ theta, float* __restrict__ m,
+                float* __restrict__ v, const float* __restrict__ g,
+                const double* __restrict__ norm_in, float lr, float b1, float b2, float eps,
+                float bc1, float bc2, __nv_bfloat16* __restrict__ bf16, float* __restrict__ f32,
+                const int* flags) {
+  if (flags[kFlagNumeric] | flags[kFlagContract]) return;  // the step throws before Adam
+  const float scale = (float)norm_in[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i] * scale;
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float th = theta[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    theta[i] = th;
+    if (bf16) bf16[i] = __float2bfloat16_rn(th);
+    if (f32) f32[i] = th;
+  }
+}
+
+}  // namespace
+
+int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
+                float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
+                uint16_t* bf16_copy, float* f32_copy) {
+  if (n == 0) return APPO_OK;
+  const int grid = 148 * 2;
+  APPO_LAUNCH(c, sumsq_kernel, grid, 256, 0, n, g, c->d_red, c->d_counter + 1, d_norm_out, clip,
+              c->d_flags);
+  const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
+  const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
+  const int grid2 = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  APPO_LAUNCH(c, adam_kernel, grid2, 256, 0, n, theta, m, v, g, d_norm_out, lr, b1, b2, eps, bc1,
+              bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags);
+  return APPO_OK;
+}
+
+}  // namespace appo_b200

@@ -1,0 +1,194 @@
+"""Model-level parity of the CUDA path against the fp64 oracle
+(oracle/appo_oracle.c; itself pinned against torch fp64 autograd and the
+reference), through the C ABI.
+
+Stated tolerances (bf16 operands, fp32 accumulation):
+  * inference: max |log pi_gpu - log pi_ref| <= 2^-6 (logits, via log-softmax),
+    |value| error <= 2e-3 + 2e-2 |ref|, h' error <= 2e-2;
+    actions equal to the oracle's inverse-CDF draw with the same uniform
+    except where u falls within 1e-3 of a CDF boundary.
+  * learner: loss components within 2e-2 relative (abs floor 1e-4);
+    per-tensor gradient relative L2 error <= 6e-2; global norm within 3e-2.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2006_11751_b200 as appo  # noqa: E402
+
+
+def log_softmax(x):
+    x = x - x.max(-1, keepdims=True)
+    return x - np.log(np.exp(x).sum(-1, keepdims=True))
+
+
+@pytest.fixture(scope="module")
+def doom():
+    return appo.Context(0, seed=5, model=appo.ModelDesc.doom(T=32))
+
+
+def test_param_count_and_layout(doom):
+    assert doom.n_params == 2872551
+    L = appo.slot_layout(doom.model)
+    assert L["total"] == 980704 and L["boot_obs"] == 951008
+
+
+def test_init_matches_oracle_init(doom, oracle):
+    th, ver = doom.get_params()
+    ref = oracle.init_params(3, 72, 128, 6, 5)
+    assert ver == 0
+    np.testing.assert_allclose(th, ref.astype(np.float32), rtol=0, atol=0)
+
+
+def test_policy_forward_matches_oracle(doom, oracle):
+    rs = np.random.default_rng(0)
+    B = 24
+    obs = rs.integers(0, 256, (B, 3 * 72 * 128), dtype=np.uint8)
+    h = rs.normal(scale=0.5, size=(B, 512)).astype(np.float32)
+    th, _ = doom.get_params()
+    out = doom.policy_forward(torch.from_numpy(obs).cuda(), torch.from_numpy(h).cuda(),
+                              rng_counter0=1000, want_logits=True)
+    torch.cuda.synchronize()
+    ref = oracle.policy_forward((3, 72, 128, 6), th.astype(np.float64), obs,
+                                h.astype(np.float64))
+    lg = out["logits"].cpu().numpy().astype(np.float64)
+    assert np.abs(log_softmax(lg) - log_softmax(ref["logits"])).max() <= 2 ** -6
+    vals = out["values"].cpu().numpy()
+    assert np.all(np.abs(vals - ref["values"]) <= 2e-3 + 2e-2 * np.abs(ref["values"]))
+    assert np.abs(out["h_out"].cpu().numpy() - ref["h_out"]).max() <= 2e-2
+    # sampling: same counter-based uniform -> same action unless u is at a boundary
+    key = oracle.L.orc_derive_seed(5, 0x9900)
+    acts = out["actions"].cpu().numpy()
+    lp = out["logp"].cpu().numpy()
+    for b in range(B):
+        u = oracle.L.orc_uniform(key, 1000 + b)
+        p = np.exp(log_softmax(ref["logits"][b]))
+        if np.min(np.abs(np.cumsum(p) - u)) < 1e-3:
+            continue
+        a, elp = oracle.sample(lg[b], u)
+        assert acts[b] == a
+        assert abs(lp[b] - elp) <= 1e-5 * max(1.0, abs(elp))
+
+
+def test_policy_forward_batch_invariance(doom):
+    # rows are independent: a batch of 300 equals its first 5 rows run alone
+    rs = np.random.default_rng(1)
+    obs = torch.from_numpy(rs.integers(0, 256, (300, 27648), dtype=np.uint8)).cuda()
+    h = torch.from_numpy(rs.normal(size=(300, 512)).astype(np.float32)).cuda()
+    a = doom.policy_forward(obs, h, want_logits=True)
+    b = doom.policy_forward(obs[:5].contiguous(), h[:5].contiguous(), want_logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a["logits"][:5], b["logits"])
+    assert torch.equal(a["actions"][:5], b["actions"])
+
+
+def fill_store(store, n_traj, rs, A):
+    T = store.T
+    data = dict(obs=[], h0=[], actions=[], blogp=[], rewards=[], dones=[])
+    for i in range(n_traj):
+        obs = rs.integers(0, 256, (T + 1, store.obs_dim), dtype=np.uint8)
+        h0 = rs.normal(scale=0.3, size=512).astype(np.float32)
+        act = rs.integers(0, A, T).astype(np.int32)
+        blogp = rs.uniform(-2.2, -1.5, T).astype(np.float32)
+        rew = rs.uniform(-1, 1, T).astype(np.float32)
+        dn = (rs.uniform(size=T) < 0.2).astype(np.uint8)
+        store.write_slot(i, obs[:T], h0, act, rew, blogp, dn, versions=np.arange(T) // 2,
+                         boot_obs=obs[T])
+        for k, v in zip(data, (obs, h0, act, blogp, rew, dn)):
+            data[k].append(v)
+    return {k: np.stack(v) for k, v in data.items()}
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("adv_source,normalize", [(0, 0), (2, 1), (1, 0)])
+def test_learner_step_matches_oracle(oracle, adv_source, normalize):
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    ctx = appo.Context(0, seed=11, model=desc)
+    store = appo.TrajectoryStore(desc, 4)
+    rs = np.random.default_rng(adv_source)
+    n_traj = 3
+    d = fill_store(store, n_traj, rs, 6)
+    th0, v0 = ctx.get_params()
+    hp = appo.HParams.defaults(adv_source=adv_source, normalize_adv=normalize, gamma=0.99,
+                               gae_lambda=0.9)
+    out = ctx.learner_step(store.region, store.slot_bytes, [0, 1, 2], hp)
+    g = ctx.grad()
+    th1, v1 = ctx.get_params()
+    assert v1 == v0 + 1 == out["version"]
+    ref = oracle.learner_step((3, 72, 128, 6), th0.astype(np.float64), np.zeros(th0.size),
+                              np.zeros(th0.size), 0, d["obs"], d["h0"].astype(np.float64),
+                              d["actions"].reshape(-1), d["blogp"].reshape(-1).astype(np.float64),
+                              d["rewards"].reshape(-1).astype(np.float64), d["dones"].reshape(-1),
+                              hp=dict(adv_source=adv_source, normalize=normalize, gamma=0.99,
+                                      gae_lambda=0.9), do_adam=False)
+    assert ref["status"] == 0
+    st = ref["stats"]
+    for got, exp in ((out["policy_loss"], st[0]), (out["value_loss"], st[1]),
+                     (out["entropy"], st[2]), (out["total_loss"], st[3]),
+                     (out["mean_ratio"], st[4])):
+        assert abs(got - exp) <= 2e-2 * abs(exp) + 1e-4, (got, exp)
+    gr = ref["grad"]
+    assert abs(out["grad_norm"] - np.linalg.norm(gr)) <= 3e-2 * np.linalg.norm(gr)
+    from oracle.oracle import Oracle  # noqa: F401  (offsets from the same contract)
+    offs = block_offsets(ctx)
+    for name, (a, b) in offs.items():
+        e = rel_l2(g[a:b].astype(np.float64), gr[a:b])
+        assert e <= 6e-2, (name, e)
+    # lag statistics (orchestrator.hpp:790,862-863): version 0 - versions[t]
+    assert out["lag_max"] == 0.0 and abs(out["lag_mean"] + 1.5) < 1e-9
+
+
+def block_offsets(ctx):
+    C_, H, W, A = ctx.model.shape
+    H1, W1 = (H - 8) // 4 + 1, (W - 8) // 4 + 1
+    H2, W2 = (H1 - 4) // 2 + 1, (W1 - 4) // 2 + 1
+    H3, W3 = (H2 - 3) // 2 + 1, (W2 - 3) // 2 + 1
+    sizes = [("c1w", 32 * C_ * 64), ("c1b", 32), ("c2w", 64 * 512), ("c2b", 64),
+             ("c3w", 128 * 576), ("c3b", 128), ("fcw", 512 * H3 * W3 * 128), ("fcb", 512),
+             ("wih", 1536 * 512), ("whh", 1536 * 512), ("bih", 1536), ("bhh", 1536),
+             ("wpi", A * 512), ("bpi", A), ("wv", 512), ("bv", 1)]
+    out, o = {}, 0
+    for k, n in sizes:
+        out[k] = (o, o + n)
+        o += n
+    return out
+
+
+def test_learner_errors():
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    ctx = appo.Context(0, seed=3, model=desc)
+    store = appo.TrajectoryStore(desc, 2)
+    rs = np.random.default_rng(5)
+    fill_store(store, 2, rs, 6)
+    with pytest.raises(appo.ConfigError):
+        ctx.learner_step(store.region, store.slot_bytes, [0, 1],
+                         appo.HParams.defaults(rho_bar=0.5, c_bar=1.0))
+    # out-of-range action -> ContractError; parameters untouched
+    store.actions(1)[3] = 9
+    th0, v0 = ctx.get_params()
+    with pytest.raises(appo.ContractError):
+        ctx.learner_step(store.region, store.slot_bytes, [0, 1])
+    th1, v1 = ctx.get_params()
+    assert v1 == v0 and np.array_equal(th0, th1)
+    # non-finite reward -> NumericError
+    store.actions(1)[3] = 0
+    store.rewards(0)[2] = float("nan")
+    with pytest.raises(appo.NumericError):
+        ctx.learner_step(store.region, store.slot_bytes, [0, 1])
+
+
+def test_learning_reduces_loss_on_fixed_batch():
+    # acceptance.cpp:508-569 analogue: repeated steps on one batch lower the loss
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    ctx = appo.Context(0, seed=7, model=desc)
+    store = appo.TrajectoryStore(desc, 4)
+    fill_store(store, 4, np.random.default_rng(9), 6)
+    hp = appo.HParams.defaults(lr=3e-4)
+    losses = [ctx.learner_step(store.region, store.slot_bytes, [0, 1, 2, 3], hp)["total_loss"]
+              for _ in range(20)]
+    assert losses[-1] < losses[0]
