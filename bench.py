@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""APPO hot-path benchmark (BASELINE.json metric: env frames/sec of policy
+inference + V-trace/PPO learning per B200, and at 2/4/8 GPUs).
+
+Workload (BASELINE.json configs[3], single GPU shard of it): 16,384 synthetic
+envs per GPU with the on-GPU observation generator (u8 3x72x128, frameskip 4),
+convnet_simple + GRU-512 + 6-way categorical head, T = 32.  One bench step =
+one full APPO iteration: a T-step rollout of every env through batched policy
+inference (obs written straight into HBM trajectory slots), then every sealed
+trajectory trained once by the learner (V-trace + PPO clipped surrogate +
+value + entropy loss, BPTT over the 32-step window, encoder backward,
+global-norm clip + Adam) in minibatches of 2048 samples (64 trajectories).
+frames per step = n_envs * T * frameskip.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun (N > 1) every rank drives its own GPU; the learner is
+data-parallel with an NCCL gradient all-reduce (appo_dp_init) unless --mode pbt
+(independent policy per GPU, configs[4]).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env frames/sec (inference + V-trace/PPO learn) per GPU and at 2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--envs", type=int, default=16384)
+    p.add_argument("--T", type=int, default=32)
+    p.add_argument("--traj-per-batch", type=int, default=64)
+    p.add_argument("--frameskip", type=int, default=4)
+    p.add_argument("--episode-len", type=int, default=256)
+    p.add_argument("--mode", default="dp", choices=["dp", "pbt"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-traj", type=int, default=0, help="trajectories per CPU-baseline sample")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [l.strip().split(",") for l in self.f.read().splitlines() if l.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(k)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------- CPU baseline
+def cpu_baseline_sample(args, n_traj=None, seed=0):
+    """Oracle port (oracle/appo_oracle.c, fp64) on the host cores: every thread
+    runs one trajectory through T+1 inference steps and one learner step over
+    it -- the same per-sample work as the GPU step, bounded in size."""
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    cores = os.cpu_count() or 1
+    n = n_traj or cores
+    shape = (3, 72, 128, 6)
+    T = args.T
+    theta = orc.init_params(*shape, 1)
+    rs = np.random.default_rng(seed)
+    obs_all = rs.integers(0, 256, (n, T + 1, 3 * 72 * 128), dtype=np.uint8)
+
+    def work(i):
+        h = np.zeros((1, 512))
+        acts, lps = [], []
+        for t in range(T + 1):
+            u = np.array([orc.L.orc_uniform(i, t)])
+            out = orc.policy_forward(shape, theta, obs_all[i, t][None], h, u=u)
+            h = out["h_out"]
+            acts.append(out["actions"][0]); lps.append(out["logp"][0])
+        th = theta.copy()
+        m = np.zeros_like(th); v = np.zeros_like(th)
+        rew = rs.uniform(-0.5, 0.5, T)
+        dn = np.zeros(T, np.uint8)
+        orc.learner_step(shape, th, m, v, 0, obs_all[i][None], np.zeros((1, 512)),
+                         np.array(acts[:T], np.int32), np.array(lps[:T]), rew, dn)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(n)]
+    t0 = time.perf_counter()
+    for th_ in threads:
+        th_.start()
+    for th_ in threads:
+        th_.join()
+    dt = time.perf_counter() - t0
+    frames = n * T * args.frameskip
+    return {"value": frames / dt, "unit": "frames/s", "cores": min(cores, n), "kind": "port",
+            "sample": f"{n} trajectories x T={T} (inference of T+1 steps + one learner step each), "
+                      f"fp64 C oracle, {min(cores, n)} threads, {dt:.1f} s"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    for _ in range(min(W, 1)):
+        cpu_baseline_sample(args, n_traj=max(1, (os.cpu_count() or 1) // 4))
+    vals = []
+    t0 = time.perf_counter()
+    res = None
+    for k in range(K):
+        res = cpu_baseline_sample(args, n_traj=args.cpu_traj or None, seed=k)
+        vals.append(res["value"])
+    wall = time.perf_counter() - t0
+    v = float(np.mean(vals))
+    line = {"metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": args.gpus, "steps": K,
+            "warmup": W, "ms_per_step": 1000.0 * wall / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C4 per-sample work (inference + learner), Doom shape",
+                       "obs": "u8 3x72x128", "T": args.T, "frameskip": args.frameskip},
+            "cpu_baseline": dict(res, value=v),
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU arm
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2006_11751_b200 as appo
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    desc = appo.ModelDesc.doom(T=args.T)
+    seed = 1 if args.mode == "dp" else 1 + rank
+    ctx = appo.Context(local, seed=seed, model=desc)
+    if ws > 1 and args.mode == "dp":
+        appo.dp_init(ctx, dist, rank, ws)
+    n = args.envs
+    tpb = args.traj_per_batch
+    assert n % tpb == 0
+    store = appo.TrajectoryStore(desc, n, device=local)
+    sampler = appo.Sampler(ctx, n, args.episode_len, seed=1000 + rank)
+    hp = appo.HParams.defaults()
+    ids = np.arange(n, dtype=np.int32).reshape(-1, tpb)
+    stream = ctx.stream
+
+    def iteration(h_obs=None, h_act=None):
+        for t in range(args.T):
+            sampler.step(store, 0, t, h_obs=h_obs[t % h_obs.shape[0]] if h_obs is not None else None,
+                         h_actions=h_act)
+        last = None
+        for mb in ids:
+            last = ctx.learner_step(store.region, store.slot_bytes, mb, hp)
+        return last
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up; the last warm-up iteration also finds the dominant kernel
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            ctx.set_timing(True)
+        iteration()
+    rep = ctx.timing_report()
+    ctx.set_timing(False)
+    total_ms = sum(r["ms"] for r in rep)
+    dom = max(rep, key=lambda r: r["ms"])
+
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    l0 = ctx.launches
+    ctx.set_timing(True, dom["name"])
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    last = None
+    for k in range(args.steps):
+        last = iteration()
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - l0
+    live = ctx.timing_report()
+    ctx.set_timing(False)
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    frames_step = n * args.T * args.frameskip
+    value = frames_step * args.steps * ws / (ms / 1000.0)
+
+    # e2e: observations from pinned host memory (CPU actors) every env step,
+    # sampled actions back to the host, learner stats back to the host
+    e2e = None
+    if not args.no_e2e:
+        h_obs = torch.from_numpy(np.random.default_rng(rank).integers(
+            0, 256, (2, n, desc.obs_dim), dtype=np.uint8)).pin_memory()
+        h_act = torch.empty(n, dtype=torch.int32).pin_memory()
+        iteration(h_obs, h_act)
+        barrier()
+        e0.record(stream)
+        for k in range(args.steps):
+            iteration(h_obs, h_act)
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        n_mb = ids.shape[0]
+        e2e = {"value": frames_step * args.steps * ws / (ems / 1000.0), "unit": "frames/s",
+               "h2d_bytes_per_step": n * desc.obs_dim * args.T + n_mb * tpb * 4,
+               "d2h_bytes_per_step": n * 4 * args.T + n_mb * (8 * 10 + 16),
+               "path": "appo_sampler_step(h_obs pinned) + appo_learner_step"}
+
+    peaks, peak_src = load_peaks()
+    roof = None
+    if live:
+        d = live[0]
+        avg_ms = d["ms"] / d["launches"]
+        if d["flops"] > 0 and "gemm" in d["name"]:
+            achieved = d["flops"] / d["launches"] / (avg_ms * 1e-3) / 1e12
+            peak = peaks["bf16_tflops_sustained"]
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak}
+        else:
+            achieved = d["bytes"] / d["launches"] / (avg_ms * 1e-3) / 1e9
+            peak = peaks["hbm_gbs"]
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak}
+        roof.update({"kernel": d["name"], "launches": d["launches"], "avg_us": avg_ms * 1e3,
+                     "share_of_step": d["ms"] / ms, "peak_source": peak_src})
+        tr = load_traffic(d["name"])
+        roof["traffic"] = tr
+        roof["kernel_shares_warmup"] = {r["name"]: round(r["ms"] / total_ms, 4) for r in
+                                        sorted(rep, key=lambda r: -r["ms"])[:8]}
+
+    if rank != 0:
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample(args, n_traj=args.cpu_traj or None)
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"error": repr(ex)}
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (on-GPU SyntheticLatencyEnv hash generator), random-init weights",
+            "config": {"workload": "C4: sampler+learner loop, convnet_simple+GRU-512, Doom shape",
+                       "envs_per_gpu": n, "T": args.T, "batch": tpb * args.T,
+                       "frameskip": args.frameskip, "obs": "u8 3x72x128",
+                       "parallelism": (f"dp{ws}" if args.mode == "dp" else f"pbt{ws}"),
+                       "learner_steps_per_step": int(ids.shape[0]),
+                       "l2": "inputs larger than L2 (16 GB slot region, 453 MB obs per env step)"},
+            "samples_per_s": value / args.frameskip,
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "last_step": last}
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

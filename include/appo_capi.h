@@ -95,6 +95,12 @@ APPO_API int appo_ctx_set_stream(appo_ctx* ctx, void* cuda_stream);
 APPO_API int appo_ctx_sync(appo_ctx* ctx);
 /* Number of launches of this library's kernels enqueued on ctx so far. */
 APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);
+/* Per-launch CUDA-event timing of this library's kernels on the ctx stream
+ * (name_filter: only kernels of that name; NULL = all).  The report is JSON
+ * lines {"name", "launches", "ms", "flops", "bytes"} (algorithmic work per
+ * launch as recorded by the launcher); it synchronizes and resets. */
+APPO_API int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter);
+APPO_API int appo_ctx_timing_report(appo_ctx* ctx, char* buf, int buflen);
 
 /* ---- off-policy returns (offpolicy.hpp) --------------------------------- */
 /* Replaces vtrace (offpolicy.hpp:139-178) for n_traj trajectories at once.
@@ -176,6 +182,34 @@ APPO_API int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, con
 APPO_API int appo_learner_step(appo_ctx* ctx, const void* d_slot_region, uint64_t slot_bytes,
                       const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp,
                       appo_step_out* out);
+
+/* ---- data-parallel learner (NCCL over NVLink) ----------------------------- */
+/* One policy on nranks GPUs: rank 0 creates the id, the host broadcasts it
+ * (e.g. torch.distributed), every rank calls appo_dp_init on its ctx.  From
+ * then on appo_learner_step averages the flat gradient with ncclAllReduce
+ * before the global-norm clip and Adam (no reference counterpart: the
+ * reference runs one learner thread per policy, orchestrator.hpp:938-946). */
+APPO_API int appo_dp_unique_id(char* out128);
+APPO_API int appo_dp_init(appo_ctx* ctx, int nranks, int rank, const char* id128);
+
+/* ---- device sampler: synthetic envs + rollout-side writer ---------------- */
+/* Restates SyntheticLatencyEnv (envs.hpp:103-158) on the device with u8 pixels
+ * and RolloutWorker::step_group/submit_group (orchestrator.hpp:435-552): every
+ * appo_sampler_step advances all n_envs envs by one step, writing step t of
+ * env e's rollout into slot slot_base + e of a layout-v2 slot region
+ * (obs, input hidden, action, behaviour logp, version, reward, done; at
+ * t == T-1 also the bootstrap obs/hidden and the in-slot header), running the
+ * batched policy on the obs in place.  h_obs != NULL: observations come from
+ * (pinned) host memory [n_envs][obs_dim] instead of the device generator (CPU
+ * actors); h_actions != NULL: sampled actions are copied back (exchange-row
+ * reply, orchestrator.hpp:652).  Asynchronous on the ctx stream. */
+typedef struct appo_sampler appo_sampler;
+APPO_API int appo_sampler_create(appo_ctx* ctx, int n_envs, int episode_len, uint64_t env_seed,
+                                 appo_sampler** out);
+APPO_API int appo_sampler_destroy(appo_sampler* s);
+APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_bytes,
+                               int32_t slot_base, int t, const uint8_t* h_obs,
+                               int32_t* h_actions);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,8 @@ _sig("appo_ctx_destroy", _i, _vp)
 _sig("appo_ctx_set_stream", _i, _vp, _vp)
 _sig("appo_ctx_sync", _i, _vp)
 _sig("appo_ctx_launch_count", _i64, _vp)
+_sig("appo_ctx_set_timing", _i, _vp, _i, C.c_char_p)
+_sig("appo_ctx_timing_report", _i, _vp, C.c_char_p, _i)
 _sig("appo_vtrace", _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _vp, _vp, _vp,
      _vp)
 _sig("appo_nstep_returns", _i, _vp, _i, _i, _vp, _vp, _vp, _f, _vp)
@@ -149,6 +151,11 @@ _sig("appo_dbg_gemm", _i, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i
      _vp, _i64, _i, _i)
 _sig("appo_dbg_model_ptrs", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp))
 _sig("appo_dbg_copy_d2h", _i, _vp, _vp, _vp, _u64)
+_sig("appo_dp_unique_id", _i, C.c_char_p)
+_sig("appo_dp_init", _i, _vp, _i, _i, C.c_char_p)
+_sig("appo_sampler_create", _i, _vp, _i, _i, _u64, C.POINTER(_vp))
+_sig("appo_sampler_destroy", _i, _vp)
+_sig("appo_sampler_step", _i, _vp, _vp, _u64, C.c_int32, _i, _vp, _vp)
 
 LIB = _L
 
@@ -218,6 +225,17 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_L.appo_ctx_launch_count(self.h))
+
+    def set_timing(self, enable: bool, name_filter: str | None = None):
+        check(_L.appo_ctx_set_timing(self.h, int(enable),
+                                     name_filter.encode() if name_filter else None))
+
+    def timing_report(self) -> list:
+        """Per-kernel aggregated CUDA-event timing since set_timing (resets)."""
+        import json
+        buf = C.create_string_buffer(1 << 20)
+        check(_L.appo_ctx_timing_report(self.h, buf, len(buf)))
+        return [json.loads(l) for l in buf.value.decode().splitlines() if l.strip()]
 
     # ---- off-policy -----------------------------------------------------
     def vtrace(self, rewards, values, bootstrap, target_logp, behavior_logp, dones, gamma=0.99,
@@ -385,6 +403,50 @@ class Context:
         check(_L.appo_dbg_gemm(self.h, M, N, K, _ptr(a), lda, int(a_mn), _ptr(b), ldb, int(b_mn),
                                _ptr(out), ldo, flags, scale, _ptr(bias), _ptr(aux), ld_aux, bn,
                                splits))
+
+
+def dp_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(_L.appo_dp_unique_id(buf))
+    return buf.raw
+
+
+def dp_init(ctx: Context, dist, rank: int, world: int):
+    """Join ``ctx`` to a data-parallel learner group of ``world`` ranks: rank 0's
+    NCCL id is broadcast over ``dist`` (torch.distributed), then every
+    learner step all-reduces (averages) the gradient before clip + Adam."""
+    obj = [dp_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    check(_L.appo_dp_init(ctx.h, world, rank, C.create_string_buffer(obj[0], 128)))
+
+
+class Sampler:
+    """Device synthetic envs + rollout writer (appo_sampler_*, include/appo_capi.h):
+    ``step(store, slot_base, t)`` advances all envs one step, writing step t of
+    env e's rollout into slot slot_base + e."""
+
+    def __init__(self, ctx: Context, n_envs: int, episode_len: int = 256, seed: int = 1):
+        self.ctx = ctx
+        self.n_envs = n_envs
+        h = C.c_void_p()
+        check(_L.appo_sampler_create(ctx.h, n_envs, episode_len, seed, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _L.appo_sampler_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, store, slot_base: int, t: int, h_obs=None, h_actions=None):
+        """h_obs / h_actions: optional pinned host tensors (CPU-actor path)."""
+        check(_L.appo_sampler_step(self.h, _ptr(store.region), store.slot_bytes, slot_base, t,
+                                   _ptr(h_obs), _ptr(h_actions)))
 
 
 EPI_BIAS, EPI_ELU, EPI_DELU, EPI_BF16, EPI_TRANS, EPI_ACCUM = 1, 2, 4, 8, 16, 32

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/appo_capi.h"
 
@@ -14,6 +15,15 @@ namespace appo_b200 {
 void set_error(const std::string& msg);
 
 struct Model;  // model.cu
+
+// Optional per-launch CUDA-event timing (appo_ctx_set_timing): the bench uses
+// it to measure the dominant kernel's average duration live, on the stream
+// the kernel runs on.
+struct TimedLaunch {
+  const char* name;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
 
 // Device flag slots raised by kernels; read by appo_ctx_sync.
 enum : int { kFlagNumeric = 0, kFlagContract = 1, kNumFlags = 4 };
@@ -30,6 +40,17 @@ struct Ctx {
   float* d_ws = nullptr;         // split-K GEMM workspace
   size_t ws_bytes = 0;
   int num_sms = 148;
+  // timing
+  bool timing = false;
+  std::string timing_filter;
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  const char* next_name = nullptr;  // overrides the kernel symbol name
+  double next_flops = 0.0, next_bytes = 0.0;
+  // data-parallel learner (dp.cu)
+  void* dp_comm = nullptr;
+  int dp_size = 1, dp_rank = 0;
   bool has_model = false;
   appo_model_desc desc{};
   Model* model = nullptr;
@@ -61,7 +82,10 @@ struct appo_ctx : appo_b200::Ctx {};
 // appo_ctx_launch_count reports how many of OUR kernels ran.
 #define APPO_LAUNCH(ctx, kernel, grid, block, smem, ...)                        \
   do {                                                                         \
+    const char* _nm = (ctx)->next_name ? (ctx)->next_name : #kernel;           \
+    cudaEvent_t _ea = appo_b200::timing_begin((ctx), _nm);                     \
     kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);            \
+    appo_b200::timing_end((ctx), _nm, _ea);                                    \
     (ctx)->launches++;                                                         \
     cudaError_t _le = cudaGetLastError();                                      \
     if (_le != cudaSuccess) {                                                  \
@@ -72,6 +96,25 @@ struct appo_ctx : appo_b200::Ctx {};
   } while (0)
 
 namespace appo_b200 {
+
+cudaEvent_t timing_event(Ctx* c);
+inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
+  if (!c->timing) return nullptr;
+  if (!c->timing_filter.empty() && c->timing_filter.compare(name) != 0) return nullptr;
+  cudaEvent_t e = timing_event(c);
+  cudaEventRecord(e, c->stream);
+  return e;
+}
+inline void timing_end(Ctx* c, const char* name, cudaEvent_t a) {
+  if (a) {
+    cudaEvent_t b = timing_event(c);
+    cudaEventRecord(b, c->stream);
+    c->timed.push_back(TimedLaunch{name, a, b, c->next_flops, c->next_bytes});
+  }
+  c->next_name = nullptr;
+  c->next_flops = 0.0;
+  c->next_bytes = 0.0;
+}
 
 __device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
 

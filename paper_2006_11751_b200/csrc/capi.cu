@@ -9,6 +9,15 @@
 namespace appo_b200 {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+cudaEvent_t timing_event(Ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
 }  // namespace appo_b200
 
 using namespace appo_b200;
@@ -46,6 +55,9 @@ int validate_vtrace(float gamma, float rho_bar, float c_bar) {
     if (_s != APPO_OK) return _s;      \
   } while (0)
 
+namespace appo_b200 {
+void dp_destroy(Ctx* c);  // dp.cu
+}
 int model_create(appo_b200::Ctx* c);   // model.cu
 void model_destroy(appo_b200::Ctx* c); // model.cu
 
@@ -95,6 +107,8 @@ int appo_ctx_destroy(appo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   cudaDeviceSynchronize();
   if (ctx->model) model_destroy(ctx);
+  appo_b200::dp_destroy(ctx);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_red);
   cudaFree(ctx->d_counter);
@@ -129,6 +143,58 @@ int appo_ctx_sync(appo_ctx* ctx) {
 }
 
 int64_t appo_ctx_launch_count(appo_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter) {
+  CTX_OR_RETURN(ctx);
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->timing = enable != 0;
+  ctx->timing_filter = name_filter ? name_filter : "";
+  ctx->timed.clear();
+  ctx->ev_used = 0;
+  return APPO_OK;
+}
+
+// Aggregated per-kernel timing since appo_ctx_set_timing, as JSON lines
+// {"name":..,"launches":..,"ms":..,"flops":..,"bytes":..}.  Synchronizes.
+int appo_ctx_timing_report(appo_ctx* ctx, char* buf, int buflen) {
+  CTX_OR_RETURN(ctx);
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  struct Agg {
+    std::string name;
+    long n = 0;
+    double ms = 0, flops = 0, bytes = 0;
+  };
+  std::vector<Agg> agg;
+  for (const auto& t : ctx->timed) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    Agg* a = nullptr;
+    for (auto& x : agg)
+      if (x.name == t.name) a = &x;
+    if (!a) {
+      agg.push_back(Agg{t.name});
+      a = &agg.back();
+    }
+    a->n++;
+    a->ms += ms;
+    a->flops += t.flops;
+    a->bytes += t.bytes;
+  }
+  std::string out;
+  for (const auto& a : agg) {
+    char line[512];
+    snprintf(line, sizeof(line),
+             "{\"name\": \"%s\", \"launches\": %ld, \"ms\": %.6f, \"flops\": %.6e, "
+             "\"bytes\": %.6e}\n",
+             a.name.c_str(), a.n, a.ms, a.flops, a.bytes);
+    out += line;
+  }
+  APPO_REQUIRE((int)out.size() < buflen, APPO_ERR_CONTRACT, "timing report buffer too small");
+  std::memcpy(buf, out.c_str(), out.size() + 1);
+  ctx->timed.clear();
+  ctx->ev_used = 0;
+  return APPO_OK;
+}
 
 int appo_vtrace(appo_ctx* ctx, int n_traj, int T, const float* r, const float* v,
                 const float* boot, const float* tl, const float* bl, const uint8_t* d,

@@ -372,6 +372,10 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
   if (per_sm < 1) per_sm = 1;
   int grid = c->num_sms * per_sm;
   if (grid > units) grid = units;
+  c->next_name = "gemm_bf16_tcgen05";
+  c->next_flops = 2.0 * p.M * p.N * p.K;
+  c->next_bytes = 2.0 * ((double)p.M * p.K + (double)p.N * p.K) +
+                  (double)p.M * p.N * ((p.epi.flags & EPI_BF16) ? 2 : 4) * (p.splits > 1 ? p.splits : 1);
   APPO_LAUNCH(c, kern, grid, THREADS, C::SMEM_BYTES, ma, mb, p);
   return APPO_OK;
 }

@@ -282,6 +282,37 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
 
 }  // namespace
 
+int dp_allreduce_grad(Ctx* c, float* grad, int64_t n);  // dp.cu
+
+// Batched inference over B observations at obs_base + b*obs_stride (contiguous
+// batch or trajectory slots): encoder + GRU + heads + sampling.
+int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, const float* h_in,
+                  uint64_t counter0, int32_t* actions, float* logp, float* h_out, float* values,
+                  float* logits) {
+  Model* M = c->model;
+  const Dims& d = M->d;
+  Scratch& s = M->si;
+  TRY(alloc_scratch(c, M, s, B, 0, false));
+  const int pub = M->published;
+  const uint16_t* wb = M->pub_bf16[pub];
+  const float* pf = M->pub_f32[pub];
+  ObsSrc src;
+  src.base = obs_base;
+  src.img_stride = obs_stride;
+  TRY(encoder_forward(c, M, s, src, B, wb, pf));
+  TRY(k_f32_to_bf16(c, B, h_in, kHidden, s.hbf, kHidden, kHidden));
+  Epilogue g;
+  g.flags = EPI_BIAS;
+  g.bias = pf + d.off_bhh;
+  g.out = s.gh;
+  g.ldo = kGates;
+  TRY(gemm_bf16(c, B, kGates, kHidden, Operand{s.hbf, kHidden, false},
+                Operand{wb + d.off_whh, kHidden, false}, g, 256));
+  TRY(k_gru_infer(c, B, d.A, s.gi, s.gh, h_in, pf + d.off_wpi, pf + d.off_bpi, pf + d.off_wv,
+                  pf + d.off_bv, M->sample_key, counter0, h_out, actions, logp, values, logits));
+  return APPO_OK;
+}
+
 }  // namespace appo_b200
 
 using namespace appo_b200;
@@ -415,7 +446,6 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
                         int64_t* h_version_out) {
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
-  const Dims& d = M->d;
   APPO_REQUIRE(B >= 0, APPO_ERR_CONTRACT, "policy_forward: batch must be >= 0");
   if (h_version_out) *h_version_out = M->version;
   if (B == 0) return APPO_OK;
@@ -423,27 +453,8 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
                "policy_forward: null buffer");
   APPO_REQUIRE((reinterpret_cast<uintptr_t>(d_obs) & 3) == 0, APPO_ERR_CONTRACT,
                "policy_forward: obs must be 4-byte aligned");
-  Scratch& s = M->si;
-  TRY(alloc_scratch(ctx, M, s, B, 0, false));
-  const int pub = M->published;
-  const uint16_t* wb = M->pub_bf16[pub];
-  const float* pf = M->pub_f32[pub];
-  ObsSrc src;
-  src.base = d_obs;
-  src.img_stride = d.obs_dim;
-  TRY(encoder_forward(ctx, M, s, src, B, wb, pf));
-  TRY(k_f32_to_bf16(ctx, B, d_h_in, kHidden, s.hbf, kHidden, kHidden));
-  Epilogue g;
-  g.flags = EPI_BIAS;
-  g.bias = pf + d.off_bhh;
-  g.out = s.gh;
-  g.ldo = kGates;
-  TRY(gemm_bf16(ctx, B, kGates, kHidden, Operand{s.hbf, kHidden, false},
-                Operand{wb + d.off_whh, kHidden, false}, g, 256));
-  TRY(k_gru_infer(ctx, B, d.A, s.gi, s.gh, d_h_in, pf + d.off_wpi, pf + d.off_bpi,
-                  pf + d.off_wv, pf + d.off_bv, M->sample_key, rng_counter0, d_h_out, d_actions,
-                  d_logp, d_values, d_logits));
-  return APPO_OK;
+  return sampler_infer(ctx, d_obs, M->d.obs_dim, B, d_h_in, rng_counter0, d_actions, d_logp,
+                       d_h_out, d_values, d_logits);
 }
 
 int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
@@ -653,6 +664,9 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
                   splits_for(ctx, 32, d.K1, d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64, M1)));
     TRY(k_colsum(ctx, M1, 32, s.dz1, 32, true, s.colsum_part, G + d.off_c1b, false));
   }
+
+  // ---- data-parallel: average the gradient over ranks before clip + Adam ----
+  TRY(dp_allreduce_grad(ctx, G, d.total));
 
   // ---- global-norm clip + Adam; publish into the other buffer ----
   const int next = pub ^ 1;

@@ -532,6 +532,7 @@ int grid_for(int64_t n, int block, int max_blocks) {
 
 int k_im2col_u8(Ctx* c, const ObsSrc& src, int64_t R, const Dims& d, uint16_t* col) {
   const int64_t n = R * d.P1 * d.C * 8;
+  c->next_bytes = (double)R * d.obs_dim + (double)R * d.P1 * d.K1 * 2;
   APPO_LAUNCH(c, im2col_u8_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, src, R, d.C, d.H,
               d.W, d.H1, d.W1, col);
   return APPO_OK;
@@ -539,6 +540,7 @@ int k_im2col_u8(Ctx* c, const ObsSrc& src, int64_t R, const Dims& d, uint16_t* c
 int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Cin, int k, int s,
                   int Ho, int Wo, uint16_t* col) {
   const int64_t n = R * Ho * Wo * k * k * (Cin / 8);
+  c->next_bytes = (double)R * Hi * Wi * Cin * 2 + (double)R * Ho * Wo * k * k * Cin * 2;
   APPO_LAUNCH(c, im2col_nhwc_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, act, R, Hi, Wi,
               Cin, k, s, Ho, Wo, col);
   return APPO_OK;
@@ -546,6 +548,7 @@ int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Ci
 int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
                   int Cin, int k, int s, int Ho, int Wo, uint16_t* dz) {
   const int64_t n = R * Hi * Wi * Cin;
+  c->next_bytes = (double)R * Ho * Wo * k * k * Cin * 4 + (double)n * 4;
   APPO_LAUNCH(c, col2im_delu_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev, R,
               Hi, Wi, Cin, k, s, Ho, Wo, dz);
   return APPO_OK;

@@ -137,6 +137,10 @@ int launch_returns(Ctx* c, const ReturnsArgs& a) {
   if (a.n_traj == 0 || a.T == 0) return APPO_OK;
   const int warps_per_block = 8;
   const int grid = (a.n_traj + warps_per_block - 1) / warps_per_block;
+  const double n = (double)a.n_traj * a.T;
+  c->next_bytes = MODE == kVTrace ? n * (17 + 8 + (a.out2 ? 4 : 0) + (a.out3 ? 4 : 0)) + a.n_traj * 4.0
+                  : MODE == kNStep ? n * 9 + a.n_traj * 4.0
+                                   : n * (13 + (a.out1 ? 8 : 4)) + a.n_traj * 4.0;
   APPO_LAUNCH(c, returns_kernel<MODE>, grid, warps_per_block * 32, 0, a);
   return APPO_OK;
 }

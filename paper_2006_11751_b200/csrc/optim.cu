@@ -88,11 +88,13 @@ int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float
                 uint16_t* bf16_copy, float* f32_copy) {
   if (n == 0) return APPO_OK;
   const int grid = 148 * 2;
+  c->next_bytes = (double)n * 4;
   APPO_LAUNCH(c, sumsq_kernel, grid, 256, 0, n, g, c->d_red, c->d_counter + 1, d_norm_out, clip,
               c->d_flags);
   const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
   const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
   const int grid2 = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  c->next_bytes = (double)n * (4 + 24 + (bf16_copy ? 2 : 0) + (f32_copy ? 4 : 0));
   APPO_LAUNCH(c, adam_kernel, grid2, 256, 0, n, theta, m, v, g, d_norm_out, lr, b1, b2, eps, bc1,
               bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags);
   return APPO_OK;

@@ -1,0 +1,248 @@
+// Device-resident sampler: n_envs synthetic environments + the rollout-side
+// writer, one call per environment step for all envs.
+//
+//   * synthetic env: restates SyntheticLatencyEnv (envs.hpp:103-158) for u8
+//     pixels -- obs bytes from the keyed hash of make_obs (envs.hpp:143-151),
+//     one splitmix64 per 8 pixels; reward schedule envs.hpp:127; done at
+//     episode_len (envs.hpp:128); env seed derive_seed(seed, (env<<24)^episode)
+//     as RolloutWorker::reset_env (orchestrator.hpp:403-404).
+//   * rollout writer: RolloutWorker::step_group / submit_group
+//     (orchestrator.hpp:435-552): the obs is written straight into the env's
+//     trajectory slot (layout v2) and the policy reads it there; the step
+//     record stores the INPUT hidden (orchestrator.hpp:518), behaviour logp and
+//     policy version (ExchangeLayout fields, :652-656); hidden <- h' and reset
+//     to zero after done (:402,528,545-547); at t == T-1 the bootstrap obs /
+//     hidden and the in-slot header are written (set_bootstrap + seal,
+//     trajstore.hpp:208-215,265-280).
+// Host-staged variant: obs arrive from pinned host memory (CPU actors) and the
+// sampled actions are copied back, i.e. the exchange-row round trip.
+#include <cuda_bf16.h>
+
+#include <cstring>
+
+#include "gemm.cuh"
+#include "model.cuh"
+#include "model_kernels.cuh"
+
+namespace appo_b200 {
+int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, const float* h_in,
+                  uint64_t counter0, int32_t* actions, float* logp, float* h_out, float* values,
+                  float* logits);
+}
+
+using namespace appo_b200;
+
+struct appo_sampler {
+  appo_ctx* ctx = nullptr;
+  int n_envs = 0;
+  int episode_len = 0;
+  uint64_t seed = 0;
+  uint32_t* step = nullptr;     // [n_envs] step within episode
+  uint32_t* episode = nullptr;  // [n_envs]
+  float* hidden = nullptr;      // [n_envs][512]
+  float* h_out = nullptr;
+  int32_t* actions = nullptr;
+  float* logp = nullptr;
+  float* values = nullptr;
+  uint64_t steps_done = 0;
+};
+
+namespace {
+
+__device__ __forceinline__ uint64_t dev_derive_seed(uint64_t seed, uint64_t stream) {
+  return splitmix64(seed ^ splitmix64(stream + 1));
+}
+
+// obs for env e at its current (episode, step): 8 pixels per hash.
+__global__ void gen_obs_kernel(int n_envs, int64_t obs_dim, uint64_t seed,
+                               const uint32_t* __restrict__ step,
+                               const uint32_t* __restrict__ episode, uint8_t* region,
+                               uint64_t slot_bytes, int64_t slot_base, uint64_t off) {
+  const int64_t words = obs_dim >> 3;
+  const int64_t total = (int64_t)n_envs * words;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(g / words);
+    const int64_t w = g % words;
+    const uint64_t es = dev_derive_seed(seed, ((uint64_t)e << 24) ^ episode[e]);
+    const uint64_t h = splitmix64(es ^ ((uint64_t)step[e] << 20) ^ (uint64_t)w);
+    *reinterpret_cast<uint64_t*>(region + (uint64_t)(slot_base + e) * slot_bytes + off + w * 8) =
+        h;
+  }
+}
+
+// Step record + env transition; one block (128 threads) per env.
+__global__ void record_kernel(int n_envs, int T, int t, int episode_len, uint32_t obs_dim,
+                              uint64_t seed,
+                              int64_t version, uint32_t* __restrict__ step,
+                              uint32_t* __restrict__ episode, float* __restrict__ hidden,
+                              const float* __restrict__ h_out, const int32_t* __restrict__ act,
+                              const float* __restrict__ logp, uint8_t* region,
+                              uint64_t slot_bytes, int64_t slot_base, SlotOffsets off) {
+  const int e = blockIdx.x;
+  if (e >= n_envs) return;
+  uint8_t* slot = region + (uint64_t)(slot_base + e) * slot_bytes;
+  const uint32_t st = step[e];
+  const uint32_t ep = episode[e];
+  const bool done = (st + 1) >= (uint32_t)episode_len;
+  // slot arrays are only guaranteed 8-byte aligned (align8 layout): float2 stores
+  float2* hs = reinterpret_cast<float2*>(hidden + (int64_t)e * kHidden);
+  const float2* ho = reinterpret_cast<const float2*>(h_out + (int64_t)e * kHidden);
+  float2* dst = reinterpret_cast<float2*>(slot + off.hidden + (uint64_t)t * kHidden * 4);
+  float2* boot = reinterpret_cast<float2*>(slot + off.boot_hidden);
+  for (int j = threadIdx.x; j < kHidden / 2; j += blockDim.x) {
+    dst[j] = hs[j];  // stored hidden = the step's INPUT hidden
+    const float2 n = ho[j];
+    if (t == T - 1) boot[j] = n;  // bootstrap hidden = h' (before any reset)
+    hs[j] = done ? make_float2(0.f, 0.f) : n;
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t es = dev_derive_seed(seed, ((uint64_t)e << 24) ^ ep);
+    reinterpret_cast<int32_t*>(slot + off.actions)[t] = act[e];
+    reinterpret_cast<float*>(slot + off.logp)[t] = logp[e];
+    reinterpret_cast<float*>(slot + off.rewards)[t] =
+        0.1f * (float)((st + 1 + es % 7) % 11) - 0.5f;
+    slot[off.dones + t] = done ? 1 : 0;
+    reinterpret_cast<int64_t*>(slot + off.versions)[t] = version;
+    if (done) {
+      step[e] = 0;
+      episode[e] = ep + 1;
+    } else {
+      step[e] = st + 1;
+    }
+    if (t == T - 1 || t == 0) {
+      uint32_t* h = reinterpret_cast<uint32_t*>(slot);
+      h[0] = T;
+      h[1] = obs_dim;
+      h[2] = kHidden;
+      h[3] = 1;
+      h[4] = t + 1;
+      h[5] = e;
+      h[6] = 0;
+      h[7] = 0;
+      h[8] = 0;
+      h[9] = (t == T - 1) ? 1u : 0u;  // bit0: bootstrap written
+    }
+  }
+}
+
+__global__ void init_env_kernel(int n_envs, int episode_len, uint32_t* step, uint32_t* episode) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_envs) return;
+  // desynchronise episodes so dones are spread over the batch
+  step[e] = (uint32_t)(((uint64_t)e * 2654435761ull) % (uint64_t)episode_len);
+  episode[e] = 0;
+}
+
+}  // namespace
+
+#define SMP_OR_RETURN(s)                                                            \
+  do {                                                                              \
+    APPO_REQUIRE((s) != nullptr && (s)->ctx != nullptr, APPO_ERR_CONTRACT,          \
+                 "null sampler");                                                   \
+    APPO_CUDA_TRY(cudaSetDevice((s)->ctx->device));                                 \
+  } while (0)
+
+extern "C" {
+
+APPO_API int appo_sampler_create(appo_ctx* ctx, int n_envs, int episode_len, uint64_t env_seed,
+                                 appo_sampler** out) {
+  APPO_REQUIRE(ctx && ctx->model && out, APPO_ERR_CONTRACT,
+               "sampler_create: needs a model context");
+  APPO_REQUIRE(n_envs >= 1 && episode_len >= 1, APPO_ERR_CONTRACT,
+               "sampler_create: n_envs and episode_len must be >= 1");
+  APPO_REQUIRE(ctx->model->d.obs_dim % 8 == 0, APPO_ERR_CONTRACT, "obs_dim must be a multiple of 8");
+  APPO_CUDA_TRY(cudaSetDevice(ctx->device));
+  appo_sampler* s = new appo_sampler();
+  s->ctx = ctx;
+  s->n_envs = n_envs;
+  s->episode_len = episode_len;
+  s->seed = env_seed;
+  const size_t H = (size_t)n_envs * kHidden * 4;
+  if (cudaMalloc(&s->step, n_envs * 4) != cudaSuccess ||
+      cudaMalloc(&s->episode, n_envs * 4) != cudaSuccess ||
+      cudaMalloc(&s->hidden, H) != cudaSuccess || cudaMalloc(&s->h_out, H) != cudaSuccess ||
+      cudaMalloc(&s->actions, n_envs * 4) != cudaSuccess ||
+      cudaMalloc(&s->logp, n_envs * 4) != cudaSuccess ||
+      cudaMalloc(&s->values, n_envs * 4) != cudaSuccess) {
+    set_error("sampler_create: allocation failed");
+    delete s;
+    return APPO_ERR_RESOURCE;
+  }
+  cudaMemsetAsync(s->hidden, 0, H, ctx->stream);
+  APPO_LAUNCH(ctx, init_env_kernel, (n_envs + 255) / 256, 256, 0, n_envs, episode_len, s->step,
+              s->episode);
+  *out = s;
+  return APPO_OK;
+}
+
+APPO_API int appo_sampler_destroy(appo_sampler* s) {
+  if (!s) return APPO_OK;
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  cudaFree(s->step);
+  cudaFree(s->episode);
+  cudaFree(s->hidden);
+  cudaFree(s->h_out);
+  cudaFree(s->actions);
+  cudaFree(s->logp);
+  cudaFree(s->values);
+  delete s;
+  return APPO_OK;
+}
+
+// One environment step for all envs into slots [slot_base, slot_base + n_envs),
+// step index t of the rollout.  h_obs == NULL: on-GPU generator; otherwise obs
+// [n_envs][obs_dim] are copied from (pinned) host memory.  h_actions (optional)
+// receives the sampled actions (device -> host, the exchange-row reply).
+APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_bytes,
+                               int32_t slot_base, int t, const uint8_t* h_obs,
+                               int32_t* h_actions) {
+  SMP_OR_RETURN(s);
+  appo_ctx* c = s->ctx;
+  Model* M = c->model;
+  const Dims& d = M->d;
+  APPO_REQUIRE(t >= 0 && t < d.T, APPO_ERR_CONTRACT, "sampler_step: t outside [0, T)");
+  APPO_REQUIRE(slot_bytes >= d.slot[9] && d_region, APPO_ERR_CONTRACT,
+               "sampler_step: bad slot region");
+  uint8_t* region = static_cast<uint8_t*>(d_region);
+  const uint64_t obs_off = d.slot[0] + (uint64_t)t * d.obs_dim;
+  if (h_obs) {
+    APPO_CUDA_TRY(cudaMemcpy2DAsync(region + (uint64_t)slot_base * slot_bytes + obs_off,
+                                    slot_bytes, h_obs, d.obs_dim, d.obs_dim, s->n_envs,
+                                    cudaMemcpyHostToDevice, c->stream));
+  } else {
+    const int64_t n = (int64_t)s->n_envs * (d.obs_dim >> 3);
+    int grid = (int)((n + 255) / 256);
+    if (grid > c->num_sms * 32) grid = c->num_sms * 32;
+    c->next_bytes = (double)s->n_envs * d.obs_dim;
+    APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
+                s->episode, region, slot_bytes, (int64_t)slot_base, obs_off);
+  }
+  const int64_t version = M->version;
+  int st = sampler_infer(c, region + (uint64_t)slot_base * slot_bytes + obs_off, slot_bytes,
+                         s->n_envs, s->hidden, s->steps_done * (uint64_t)s->n_envs, s->actions,
+                         s->logp, s->h_out, s->values, nullptr);
+  if (st) return st;
+  SlotOffsets off;
+  std::memcpy(&off, d.slot, sizeof(off));
+  APPO_LAUNCH(c, record_kernel, s->n_envs, 128, 0, s->n_envs, d.T, t, s->episode_len,
+              (uint32_t)d.obs_dim, s->seed,
+              version, s->step, s->episode, s->hidden, s->h_out, s->actions, s->logp, region,
+              slot_bytes, (int64_t)slot_base, off);
+  if (t == d.T - 1) {
+    // bootstrap obs = next observation of every env (post-transition state)
+    const int64_t n = (int64_t)s->n_envs * (d.obs_dim >> 3);
+    int grid = (int)((n + 255) / 256);
+    if (grid > c->num_sms * 32) grid = c->num_sms * 32;
+    APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
+                s->episode, region, slot_bytes, (int64_t)slot_base, d.slot[7]);
+  }
+  if (h_actions)
+    APPO_CUDA_TRY(cudaMemcpyAsync(h_actions, s->actions, sizeof(int32_t) * s->n_envs,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  s->steps_done++;
+  return APPO_OK;
+}
+
+}  // extern "C"

@@ -23,7 +23,11 @@ class TrajectoryStore:
         self.torch = torch
         self.desc = desc
         self.layout = slot_layout(desc)
-        self.slot_bytes = self.layout["total"]
+        # slot stride: the layout-v2 slot rounded up to 16 B (vector loads need
+        # 16-byte aligned slot bases); at the Doom shape it is exactly the
+        # reference's dense stride (980,704 B).  The in-slot byte layout is
+        # exactly trajstore.hpp's Offsets algorithm.
+        self.slot_bytes = (self.layout["total"] + 15) // 16 * 16
         self.n_slots = n_slots
         self.T = desc.T
         self.obs_dim = desc.obs_dim
