@@ -218,10 +218,9 @@ def run_ours(args, ws, rank, local):
         for t in range(args.T):
             sampler.step(store, 0, t, h_obs=h_obs[t % h_obs.shape[0]] if h_obs is not None else None,
                          h_actions=h_act)
-        last = None
-        for mb in ids:
-            last = ctx.learner_step(store.region, store.slot_bytes, mb, hp)
-        return last
+        for mb in ids:  # asynchronous: no host round trip between learner steps
+            ctx.learner_submit(store.region, store.slot_bytes, mb, hp)
+        return ctx.learner_collect()
 
     def barrier():
         torch.cuda.synchronize()

@@ -183,6 +183,16 @@ APPO_API int appo_learner_step(appo_ctx* ctx, const void* d_slot_region, uint64_
                       const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp,
                       appo_step_out* out);
 
+/* Asynchronous form of appo_learner_step: _submit validates the arguments and
+ * enqueues the whole step (including Adam and the publish of the inference
+ * copy) on the ctx stream without waiting; _collect waits for everything
+ * submitted, returns the statistics of the last submitted step and the first
+ * device-detected error (a rejected step leaves the parameters untouched and
+ * does not advance the version, as when optimizer_step throws). */
+APPO_API int appo_learner_submit(appo_ctx* ctx, const void* d_slot_region, uint64_t slot_bytes,
+                                 const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp);
+APPO_API int appo_learner_collect(appo_ctx* ctx, appo_step_out* out);
+
 /* ---- data-parallel learner (NCCL over NVLink) ----------------------------- */
 /* One policy on nranks GPUs: rank 0 creates the id, the host broadcasts it
  * (e.g. torch.distributed), every rank calls appo_dp_init on its ctx.  From

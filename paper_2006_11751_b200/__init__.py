@@ -151,6 +151,8 @@ _sig("appo_dbg_gemm", _i, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i
      _vp, _i64, _i, _i)
 _sig("appo_dbg_model_ptrs", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp))
 _sig("appo_dbg_copy_d2h", _i, _vp, _vp, _vp, _u64)
+_sig("appo_learner_submit", _i, _vp, _vp, _u64, _vp, _i, C.POINTER(HParams))
+_sig("appo_learner_collect", _i, _vp, C.POINTER(StepOut))
 _sig("appo_dp_unique_id", _i, C.c_char_p)
 _sig("appo_dp_init", _i, _vp, _i, _i, C.c_char_p)
 _sig("appo_sampler_create", _i, _vp, _i, _i, _u64, C.POINTER(_vp))
@@ -382,6 +384,19 @@ class Context:
         check(_L.appo_learner_step(self.h, _ptr(region), slot_bytes,
                                    ids.ctypes.data_as(C.c_void_p), ids.size, C.byref(hp),
                                    C.byref(out)))
+        return out.as_dict()
+
+    def learner_submit(self, region, slot_bytes: int, slot_ids, hp: HParams | None = None):
+        """Enqueue one learner step without waiting (appo_learner_submit)."""
+        ids = np.ascontiguousarray(slot_ids, dtype=np.int32)
+        hp = hp or HParams.defaults()
+        check(_L.appo_learner_submit(self.h, _ptr(region), slot_bytes,
+                                     ids.ctypes.data_as(C.c_void_p), ids.size, C.byref(hp)))
+
+    def learner_collect(self):
+        """Wait for submitted steps; stats of the last one (appo_learner_collect)."""
+        out = StepOut()
+        check(_L.appo_learner_collect(self.h, C.byref(out)))
         return out.as_dict()
 
     def model_ptrs(self):

@@ -100,7 +100,9 @@ namespace appo_b200 {
 cudaEvent_t timing_event(Ctx* c);
 inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
   if (!c->timing) return nullptr;
-  if (!c->timing_filter.empty() && c->timing_filter.compare(name) != 0) return nullptr;
+  if (!c->timing_filter.empty() && c->timing_filter != "gemm_shapes" &&
+      c->timing_filter.compare(name) != 0)
+    return nullptr;
   cudaEvent_t e = timing_event(c);
   cudaEventRecord(e, c->stream);
   return e;
@@ -165,6 +167,6 @@ int launch_sample(Ctx* c, int B, int A, const float* logits, uint64_t key, uint6
                   int32_t* actions, float* logp);
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
-                uint16_t* bf16_copy, float* f32_copy);
+                uint16_t* bf16_copy, float* f32_copy, unsigned* applied);
 
 }  // namespace appo_b200

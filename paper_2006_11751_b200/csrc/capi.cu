@@ -263,7 +263,8 @@ int appo_adam_step(appo_ctx* ctx, int64_t n, float* theta, float* m, float* v, c
   CTX_OR_RETURN(ctx);
   APPO_REQUIRE(n >= 0 && t >= 1, APPO_ERR_CONTRACT, "adam: n >= 0 and t >= 1 required");
   double* d_norm = ctx->d_red + kRedSlots - 16;
-  int st = launch_adam(ctx, n, theta, m, v, g, t, lr, b1, b2, eps, clip, d_norm, nullptr, nullptr);
+  int st = launch_adam(ctx, n, theta, m, v, g, t, lr, b1, b2, eps, clip, d_norm, nullptr, nullptr,
+                       nullptr);
   if (st) return st;
   if (h_grad_norm) {
     APPO_CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned, d_norm, sizeof(double), cudaMemcpyDeviceToHost,

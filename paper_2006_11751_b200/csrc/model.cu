@@ -159,7 +159,9 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
     a.take(&s.core_bf, (size_t)R * kHidden);
     a.take(&s.gates, (size_t)R * 4 * kHidden);
     a.take(&s.hin, (size_t)R * kHidden);
-    a.take(&s.hcur, (size_t)n_traj * kHidden);
+    a.take(&s.hcur, (size_t)2 * n_traj * kHidden);  // ping-pong h_t for the persistent GRU
+    a.take(&s.dghx, (size_t)2 * n_traj * kGates);
+    a.take(&s.hcur_bf, (size_t)2 * n_traj * kHidden);
     a.take(&s.logits, (size_t)R * d.A);
     a.take(&s.values, (size_t)R);
     a.take(&s.tlogp, (size_t)B);
@@ -200,7 +202,7 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
   reloc(s.gh, base); reloc(s.hbf, base);
   if (learner) {
     reloc(s.core, base); reloc(s.core_bf, base); reloc(s.gates, base); reloc(s.hin, base);
-    reloc(s.hcur, base); reloc(s.logits, base); reloc(s.values, base); reloc(s.tlogp, base);
+    reloc(s.hcur, base); reloc(s.dghx, base); reloc(s.hcur_bf, base); reloc(s.logits, base); reloc(s.values, base); reloc(s.tlogp, base);
     reloc(s.ent, base); reloc(s.vt, base); reloc(s.pg, base); reloc(s.adv, base);
     reloc(s.rew, base); reloc(s.blogp, base); reloc(s.act, base); reloc(s.done, base);
     reloc(s.ver, base); reloc(s.dlog, base); reloc(s.dhead, base); reloc(s.dcore, base);
@@ -335,6 +337,9 @@ int model_create(Ctx* c) {
     APPO_CUDA_TRY(cudaMalloc(&M->pub_f32[k], P * 4));
   }
   M->sample_key = host_derive_seed(c->seed, 0x9900);
+  APPO_CUDA_TRY(cudaMallocHost(&M->ring_host, sizeof(double) * Model::kRing * Model::kRingStride));
+  for (int k = 0; k < Model::kRing; ++k)
+    APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->ring_ev[k], cudaEventDisableTiming));
   std::vector<float> th;
   init_params_host(M->d, c->seed, th);
   return appo_params_set(static_cast<appo_ctx*>(c), th.data(), 0);
@@ -351,6 +356,9 @@ void model_destroy(Ctx* c) {
     cudaFree(M->pub_bf16[k]);
     cudaFree(M->pub_f32[k]);
   }
+  if (M->ring_host) cudaFreeHost(M->ring_host);
+  for (int k = 0; k < Model::kRing; ++k)
+    if (M->ring_ev[k]) cudaEventDestroy(M->ring_ev[k]);
   for (Scratch* s : {&M->si, &M->sl}) {
     if (s->col1) cudaFree(s->col1);
     if (s->h_stats) cudaFreeHost(s->h_stats);
@@ -457,13 +465,12 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
                        d_h_out, d_values, d_logits);
 }
 
-int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
-                      const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp,
-                      appo_step_out* out) {
+int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
+                        const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp) {
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
   const Dims& d = M->d;
-  APPO_REQUIRE(hp && out && d_region && h_slot_ids && n_traj >= 1, APPO_ERR_CONTRACT,
+  APPO_REQUIRE(hp && d_region && h_slot_ids && n_traj >= 1, APPO_ERR_CONTRACT,
                "learner_step: bad arguments");
   APPO_REQUIRE(slot_bytes >= d.slot[9], APPO_ERR_CONTRACT,
                "learner_step: slot_bytes smaller than the layout v2 slot");
@@ -488,7 +495,12 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
   const float* th = M->theta;  // fp32 master (== pub_f32[pub])
   const uint8_t* region = static_cast<const uint8_t*>(d_region);
 
-  int32_t* h_ids = reinterpret_cast<int32_t*>(s.h_stats + 16);
+  // pinned ring slot for this step's slot ids (H2D) and stats (D2H)
+  const int ring = M->ring_pos;
+  M->ring_pos = (M->ring_pos + 1) % Model::kRing;
+  APPO_CUDA_TRY(cudaEventSynchronize(M->ring_ev[ring]));
+  double* h_st = M->ring_host + (size_t)ring * Model::kRingStride;
+  int32_t* h_ids = reinterpret_cast<int32_t*>(h_st + 16);
   std::memcpy(h_ids, h_slot_ids, sizeof(int32_t) * n_traj);
   APPO_CUDA_TRY(cudaMemcpyAsync(s.slot_ids, h_ids, sizeof(int32_t) * n_traj,
                                 cudaMemcpyHostToDevice, st));
@@ -510,12 +522,16 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
   TRY(encoder_forward(ctx, M, s, src, R, wb, th));
 
   // ---- GRU unrolled over T steps (+ bootstrap step) ----
+  const bool seq = gru_seq_supported(n_traj);
   Epilogue g;
   g.flags = EPI_BIAS;
   g.bias = th + d.off_bhh;
   g.out = s.gh;
   g.ldo = kGates;
-  for (int t = 0; t <= T; ++t) {
+  if (seq)
+    TRY(k_gru_seq_fwd(ctx, n_traj, T, s.gi, wb + d.off_whh, th + d.off_bhh, s.done, s.hcur,
+                      s.hcur_bf, s.core, s.core_bf, s.gates, s.hin, s.hbf, ctx->d_counter + 4));
+  for (int t = 0; !seq && t <= T; ++t) {
     TRY(k_stage_h(ctx, n_traj, T, t, s.hcur, s.hin, s.hbf));
     const uint16_t* a = (t < T) ? s.hbf + (size_t)t * kHidden : s.hbf + (size_t)B * kHidden;
     const int64_t lda = (t < T) ? (int64_t)T * kHidden : kHidden;
@@ -567,8 +583,12 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
   }
 
   // ---- BPTT through the GRU ----
-  APPO_CUDA_TRY(cudaMemsetAsync(s.dnext, 0, sizeof(float) * n_traj * kHidden, st));
-  {
+  if (seq)
+    TRY(k_gru_seq_bwd(ctx, n_traj, T, s.dcore, s.done, s.gates, s.hin, wb + d.off_whh, s.dghx,
+                      s.dgi, s.dgh, ctx->d_counter + 5));
+  else
+    APPO_CUDA_TRY(cudaMemsetAsync(s.dnext, 0, sizeof(float) * n_traj * kHidden, st));
+  if (!seq) {
     Epilogue e;
     e.flags = EPI_ACCUM;
     e.out = s.dnext;
@@ -630,11 +650,12 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
                   192, splits_for(ctx, 128, 576, 192, M3)));
     TRY(k_colsum(ctx, M3, 128, s.dz3, 128, true, s.colsum_part, G + d.off_c3b, false));
     Epilogue x;
+    x.flags = EPI_BF16;
     x.out = s.dcol3;
     x.ldo = 576;
     TRY(gemm_bf16(ctx, M3, 576, 128, Operand{s.dz3, 128, false},
                   Operand{wb + d.off_c3w, 576, true}, x, 192));
-    TRY(k_col2im_delu(ctx, s.dcol3, s.a2, B, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.dz2));
+    TRY(k_col2im_delu_bf16(ctx, s.dcol3, s.a2, B, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.dz2));
   }
   // ---- conv2 backward ----
   {
@@ -646,11 +667,12 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
                   splits_for(ctx, 64, 512, 256, M2)));
     TRY(k_colsum(ctx, M2, 64, s.dz2, 64, true, s.colsum_part, G + d.off_c2b, false));
     Epilogue x;
+    x.flags = EPI_BF16;
     x.out = s.dcol2;
     x.ldo = 512;
     TRY(gemm_bf16(ctx, M2, 512, 64, Operand{s.dz2, 64, false},
                   Operand{wb + d.off_c2w, 512, true}, x, 256));
-    TRY(k_col2im_delu(ctx, s.dcol2, s.a1, B, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.dz1));
+    TRY(k_col2im_delu_bf16(ctx, s.dcol2, s.a1, B, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.dz1));
   }
   // ---- conv1 weight gradient (input is data) ----
   {
@@ -673,28 +695,60 @@ int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
   M->adam_t += 1;
   TRY(launch_adam(ctx, d.total, M->theta, M->m, M->v, G, M->adam_t, hp->lr, hp->beta1,
                   hp->beta2, hp->eps, hp->grad_clip, s.stats + 8, M->pub_bf16[next],
-                  M->pub_f32[next]));
-  APPO_CUDA_TRY(cudaMemcpyAsync(s.h_stats, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost,
-                                st));
-  const int sync_st = appo_ctx_sync(ctx);
-  const double* hs = s.h_stats;
-  out->policy_loss = hs[0];
-  out->value_loss = hs[1];
-  out->entropy = hs[2];
-  out->total_loss = hs[3];
-  out->mean_ratio = hs[4];
-  out->lag_mean = hs[6];
-  out->lag_max = hs[7];
-  out->grad_norm = hs[8];
-  if (sync_st != APPO_OK) {
-    M->adam_t -= 1;  // optimizer_step threw: params untouched (adam kernel checks the flag)
-    out->version = M->version;
-    return sync_st;
-  }
+                  M->pub_f32[next], ctx->d_counter + 6));
+  APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
+  APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
+  M->last_ring = ring;
+  // Optimistic publish: the Adam kernel always rewrites pub[next] (with the
+  // unchanged parameters when the step is rejected), so inference launched
+  // after this point on the stream reads a consistent buffer.
   M->published = next;
   M->version += 1;
-  out->version = M->version;
+  M->pending += 1;
   return APPO_OK;
+}
+
+// Waits for the submitted learner steps; reports the last one's statistics
+// and any NumericError / ContractError raised on the device since the last
+// collect.  Steps rejected by the device flag do not count as versions.
+int appo_learner_collect(appo_ctx* ctx, appo_step_out* out) {
+  MODEL_OR_RETURN(ctx);
+  Model* M = ctx->model;
+  const int sync_st = appo_ctx_sync(ctx);
+  unsigned applied = 0;
+  APPO_CUDA_TRY(cudaMemcpy(&applied, ctx->d_counter + 6, sizeof(unsigned),
+                           cudaMemcpyDeviceToHost));
+  const int64_t ok_steps = (int64_t)(applied - M->applied_synced);
+  const int64_t rejected = M->pending - ok_steps;
+  M->version -= rejected;
+  M->adam_t -= rejected;
+  M->applied_synced = applied;
+  M->pending = 0;
+  if (out) {
+    std::memset(out, 0, sizeof(*out));
+    if (M->last_ring >= 0) {
+      const double* hs = M->ring_host + (size_t)M->last_ring * Model::kRingStride;
+      out->policy_loss = hs[0];
+      out->value_loss = hs[1];
+      out->entropy = hs[2];
+      out->total_loss = hs[3];
+      out->mean_ratio = hs[4];
+      out->lag_mean = hs[6];
+      out->lag_max = hs[7];
+      out->grad_norm = hs[8];
+    }
+    out->version = M->version;
+  }
+  return sync_st;
+}
+
+int appo_learner_step(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
+                      const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp,
+                      appo_step_out* out) {
+  APPO_REQUIRE(out != nullptr, APPO_ERR_CONTRACT, "learner_step: null out");
+  const int st = appo_learner_submit(ctx, d_region, slot_bytes, h_slot_ids, n_traj, hp);
+  if (st != APPO_OK) return st;
+  return appo_learner_collect(ctx, out);
 }
 
 }  // extern "C"

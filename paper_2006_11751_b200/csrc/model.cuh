@@ -47,9 +47,11 @@ struct Scratch {
   uint16_t* dhead = nullptr;    // [B][16] bf16
   float* dcore = nullptr;       // [B][512]
   float* dnext = nullptr;       // [n_traj][512]
+  uint16_t* dghx = nullptr;     // [2][n_traj][1536] bf16 BPTT exchange (persistent GRU)
+  uint16_t* hcur_bf = nullptr;  // [2][n_traj][512] bf16 h_t exchange (persistent GRU)
   uint16_t *dgi = nullptr, *dgh = nullptr;  // [B][1536] bf16
   uint16_t *dzfc = nullptr, *dz3 = nullptr, *dz2 = nullptr, *dz1 = nullptr;
-  float *dcol3 = nullptr, *dcol2 = nullptr;
+  uint16_t *dcol3 = nullptr, *dcol2 = nullptr;  // bf16 im2col-space input gradients
   float* headw = nullptr;       // [16][512]
   float* colsum_part = nullptr; // partials for bias grads
   int32_t* slot_ids = nullptr;
@@ -69,6 +71,15 @@ struct Model {
   int64_t version = 0;
   int64_t adam_t = 0;
   uint64_t sample_key = 0;
+  // asynchronous learner submissions (appo_learner_submit / _collect)
+  static constexpr int kRing = 8;
+  static constexpr int kRingStride = 16 + 4096 / 2;  // doubles: 16 stats + 4096 slot ids
+  double* ring_host = nullptr;  // pinned [kRing][kRingStride]
+  cudaEvent_t ring_ev[kRing] = {};
+  int ring_pos = 0;
+  int last_ring = -1;
+  int64_t pending = 0;
+  unsigned applied_synced = 0;
   Scratch si;  // inference scratch
   Scratch sl;  // learner scratch
 };

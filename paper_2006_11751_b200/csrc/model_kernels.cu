@@ -116,6 +116,54 @@ __global__ void col2im_delu_kernel(const float* __restrict__ dcol,
   }
 }
 
+// Same as above with bf16 dcol and 8 channels per thread (16-byte loads/stores).
+__global__ void col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol,
+                                        const uint16_t* __restrict__ aprev, int64_t R, int Hi,
+                                        int Wi, int Cin, int k, int s, int Ho, int Wo,
+                                        uint16_t* __restrict__ dz) {
+  const int cg = Cin >> 3;
+  const int64_t total = R * Hi * Wi * cg;
+  const int K = k * k * Cin;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(g % cg);
+    int64_t rest = g / cg;
+    const int xi = (int)(rest % Wi);
+    rest /= Wi;
+    const int yi = (int)(rest % Hi);
+    const int64_t r = rest / Hi;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int kh = yi % s; kh < k; kh += s) {
+      const int yo = (yi - kh) / s;
+      if (yo < 0 || yo >= Ho) continue;
+      for (int kw = xi % s; kw < k; kw += s) {
+        const int xo = (xi - kw) / s;
+        if (xo < 0 || xo >= Wo) continue;
+        const uint4 v = *reinterpret_cast<const uint4*>(
+            dcol + (r * Ho * Wo + (int64_t)yo * Wo + xo) * K + (kh * k + kw) * Cin + c8 * 8);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] += bf2f((uint16_t)(w[q] & 0xFFFF));
+          acc[2 * q + 1] += bf2f((uint16_t)(w[q] >> 16));
+        }
+      }
+    }
+    const int64_t o = g * 8;
+    const uint4 av = *reinterpret_cast<const uint4*>(aprev + o);
+    const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+    uint32_t out[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a0 = bf2f((uint16_t)(aw[q] & 0xFFFF)), a1 = bf2f((uint16_t)(aw[q] >> 16));
+      const float d0 = acc[2 * q] * (a0 > 0.0f ? 1.0f : a0 + 1.0f);
+      const float d1 = acc[2 * q + 1] * (a1 > 0.0f ? 1.0f : a1 + 1.0f);
+      out[q] = (uint32_t)f2bf(d0) | ((uint32_t)f2bf(d1) << 16);
+    }
+    *reinterpret_cast<uint4*>(dz + o) = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
 __global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int64_t src_ld,
                                    uint16_t* __restrict__ dst, int64_t dst_ld, int cols) {
   const int64_t total = n * cols;
@@ -551,6 +599,14 @@ int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, i
   c->next_bytes = (double)R * Ho * Wo * k * k * Cin * 4 + (double)n * 4;
   APPO_LAUNCH(c, col2im_delu_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev, R,
               Hi, Wi, Cin, k, s, Ho, Wo, dz);
+  return APPO_OK;
+}
+int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
+                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz) {
+  const int64_t n = R * Hi * Wi * (Cin / 8);
+  c->next_bytes = (double)R * Ho * Wo * k * k * Cin * 2 + (double)R * Hi * Wi * Cin * 4;
+  APPO_LAUNCH(c, col2im_delu_bf16_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev,
+              R, Hi, Wi, Cin, k, s, Ho, Wo, dz);
   return APPO_OK;
 }
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,

@@ -33,6 +33,8 @@ int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Ci
                   int Ho, int Wo, uint16_t* col);
 int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
                   int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
+int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
+                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
                   int64_t dst_ld, int cols);
 int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const float* h_in,
@@ -60,5 +62,15 @@ int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, f
 int k_head_grad_scatter(Ctx* c, int A, const float* headw, const float* bias_sums, float* gwpi,
                         float* gbpi, float* gwv, float* gbv);
 int k_lag(Ctx* c, int B, const int64_t* ver, int64_t cur, double* stats);
+
+// persistent GRU recurrence (gru_seq.cu)
+int gru_seq_supported(int n_traj);
+int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* whh,
+                  const float* bhh, const uint8_t* done, float* hbuf, uint16_t* hbuf_bf,
+                  float* core, uint16_t* core_bf, float* gates, float* hin, uint16_t* hbf,
+                  unsigned* bar);
+int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* done,
+                  const float* gates, const float* hin, const uint16_t* whh, uint16_t* dghx,
+                  uint16_t* dgi, uint16_t* dgh, unsigned* bar);
 
 }  // namespace appo_b200

@@ -64,8 +64,19 @@ __global__ void __launch_bounds__(256)
                 float* __restrict__ v, const float* __restrict__ g,
                 const double* __restrict__ norm_in, float lr, float b1, float b2, float eps,
                 float bc1, float bc2, __nv_bfloat16* __restrict__ bf16, float* __restrict__ f32,
-                const int* flags) {
-  if (flags[kFlagNumeric] | flags[kFlagContract]) return;  // the step throws before Adam
+                const int* flags, unsigned* applied) {
+  if (flags[kFlagNumeric] | flags[kFlagContract]) {
+    // the step threw before Adam: parameters untouched, but the publish target
+    // still receives the current parameters so the published copy stays valid
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const float th = theta[i];
+      if (bf16) bf16[i] = __float2bfloat16_rn(th);
+      if (f32) f32[i] = th;
+    }
+    return;
+  }
+  if (applied && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(applied, 1u);
   const float scale = (float)norm_in[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -85,7 +96,7 @@ __global__ void __launch_bounds__(256)
 
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
-                uint16_t* bf16_copy, float* f32_copy) {
+                uint16_t* bf16_copy, float* f32_copy, unsigned* applied) {
   if (n == 0) return APPO_OK;
   const int grid = 148 * 2;
   c->next_bytes = (double)n * 4;
@@ -96,7 +107,7 @@ int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float
   const int grid2 = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
   c->next_bytes = (double)n * (4 + 24 + (bf16_copy ? 2 : 0) + (f32_copy ? 4 : 0));
   APPO_LAUNCH(c, adam_kernel, grid2, 256, 0, n, theta, m, v, g, d_norm_out, lr, b1, b2, eps, bc1,
-              bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags);
+              bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags, applied);
   return APPO_OK;
 }
 

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+timeout -s KILL 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/t_all.log 2>&1; echo "gpu tests rc=$?"
+tail -6 gpurun_out/t_all.log
+timeout -s KILL 300 python scripts/gemm_bench.py > gpurun_out/gemm_bench.txt 2>&1; cat gpurun_out/gemm_bench.txt
+timeout -s KILL 300 python scripts/profile_step.py > gpurun_out/profile_step.txt 2>&1; echo "profile rc=$?"
+grep -A10 "learner step (2048 samples) \[None\]" gpurun_out/profile_step.txt; grep -A8 "inference step (16384 envs) \[None\]" gpurun_out/profile_step.txt; tail -3 gpurun_out/profile_step.txt

@@ -1,0 +1,48 @@
+"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list into
+per-kernel counts, total/avg device time and share (cold-cache, serialised
+timings: compare SHARES with bench.py's live numbers, not absolutes).
+
+usage: python scripts/ncu_launch_summary.py gpurun_out/launches.csv [--skip N]
+"""
+import collections
+import csv
+import re
+import sys
+
+
+def kname(full: str) -> str:
+    s = full
+    if s.startswith("void "):
+        s = s[5:]
+    s = s.replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
+    s = s.replace("appo_b200::", "")
+    s = s.split("(")[0]
+    return re.sub(r"<.*", "", s)
+
+
+def main():
+    path = sys.argv[1]
+    skip = int(sys.argv[sys.argv.index("--skip") + 1]) if "--skip" in sys.argv else 0
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1 + skip:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-3)
+        a = agg[kname(r[ki])]
+        a[0] += 1
+        a[1] += v
+    tot = sum(v[1] for v in agg.values())
+    print(f"| kernel | launches | total us | avg us | share |")
+    print(f"|---|---:|---:|---:|---:|")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| {k} | {n} | {t:.1f} | {t / n:.2f} | {t / tot:.3f} |")
+    print(f"\ntotal {tot:.1f} us over {sum(v[0] for v in agg.values())} launches")
+
+
+if __name__ == "__main__":
+    main()

@@ -192,3 +192,38 @@ def test_learning_reduces_loss_on_fixed_batch():
     losses = [ctx.learner_step(store.region, store.slot_bytes, [0, 1, 2, 3], hp)["total_loss"]
               for _ in range(20)]
     assert losses[-1] < losses[0]
+
+
+def test_async_submit_collect_determinism_and_rejected_steps():
+    # bitwise determinism (acceptance.cpp:673-708 analogue) + the async form:
+    # a rejected step (NumericError) leaves params/version untouched and the
+    # sticky flag rejects every later step until collect
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    store = appo.TrajectoryStore(desc, 4)
+    fill_store(store, 4, np.random.default_rng(2), 6)
+    ref = appo.Context(0, seed=13, model=desc)
+    for _ in range(3):
+        ref.learner_step(store.region, store.slot_bytes, [0, 1])
+    ref_th, ref_v = ref.get_params()
+    ctx = appo.Context(0, seed=13, model=desc)
+    ctx.learner_submit(store.region, store.slot_bytes, [0, 1])
+    ctx.learner_submit(store.region, store.slot_bytes, [0, 1])
+    out = ctx.learner_collect()
+    assert out["version"] == 2
+    ctx.learner_submit(store.region, store.slot_bytes, [0, 1])
+    store.rewards(2)[0] = float("nan")  # same stream: ordered after the submits
+    ctx.learner_submit(store.region, store.slot_bytes, [2, 3])
+    ctx.learner_submit(store.region, store.slot_bytes, [0, 1])
+    with pytest.raises(appo.NumericError):
+        ctx.learner_collect()
+    th, v = ctx.get_params()
+    assert v == ref_v == 3
+    assert np.array_equal(th, ref_th)
+    # the published inference copy matches the master parameters
+    rs = np.random.default_rng(4)
+    obs = torch.from_numpy(rs.integers(0, 256, (4, desc.obs_dim), dtype=np.uint8)).cuda()
+    h = torch.zeros(4, 512, device="cuda")
+    a = ctx.policy_forward(obs, h, want_logits=True)
+    b = ref.policy_forward(obs, h, want_logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a["logits"], b["logits"])
