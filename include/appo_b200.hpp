@@ -1,0 +1,194 @@
+// appo_b200.hpp -- header-only C++ host mirror of the reference's hot-path API
+// over the C ABI (appo_capi.h).  A host that used
+//   appo::vtrace / appo::nstep_returns / appo::total_loss   (offpolicy.hpp)
+//   appo::log_prob_and_entropy / appo::optimizer_step        (policy.hpp)
+//   PolicyWorkerUnit::run_once / LearnerUnit::step            (orchestrator.hpp)
+// switches to the same names in namespace appo_b200, with std::span arguments,
+// the same output structs and the same exception taxonomy (ContractError /
+// ConfigError / NumericError, common.hpp:20-45).  Host-span overloads stage
+// through device memory (the reference-facing e2e path); device-pointer
+// overloads are the zero-copy path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "appo_capi.h"
+
+namespace appo_b200 {
+
+class ContractError : public std::logic_error {
+ public:
+  explicit ContractError(const std::string& w) : std::logic_error(w) {}
+};
+class ConfigError : public std::runtime_error {
+ public:
+  explicit ConfigError(const std::string& w) : std::runtime_error(w) {}
+};
+class NumericError : public std::runtime_error {
+ public:
+  explicit NumericError(const std::string& w) : std::runtime_error(w) {}
+};
+class ResourceError : public std::runtime_error {
+ public:
+  explicit ResourceError(const std::string& w) : std::runtime_error(w) {}
+};
+
+inline void check(int st) {
+  if (st == APPO_OK) return;
+  const std::string m = appo_last_error();
+  switch (st) {
+    case APPO_ERR_CONTRACT: throw ContractError(m);
+    case APPO_ERR_CONFIG: throw ConfigError(m);
+    case APPO_ERR_NUMERIC: throw NumericError(m);
+    default: throw ResourceError(m);
+  }
+}
+
+// offpolicy.hpp:18-45 defaults
+struct VTraceConfig {
+  double rho_bar = 1.0;
+  double c_bar = 1.0;
+  double gamma = 0.99;
+};
+struct VTraceOutput {  // offpolicy.hpp:30-35
+  std::vector<double> v, pg_adv, rho, c;
+};
+struct LossComponents {  // offpolicy.hpp:214-219
+  double policy = 0, value = 0, entropy = 0, total = 0;
+};
+
+// RAII device buffer (plumbing only).
+template <class T>
+class DeviceBuffer {
+ public:
+  explicit DeviceBuffer(size_t n) : n_(n) {
+    if (n && cudaMalloc(&p_, n * sizeof(T)) != cudaSuccess) throw ResourceError("cudaMalloc");
+  }
+  ~DeviceBuffer() { cudaFree(p_); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  void upload(const T* h) { cudaMemcpy(p_, h, n_ * sizeof(T), cudaMemcpyHostToDevice); }
+  void download(T* h) const { cudaMemcpy(h, p_, n_ * sizeof(T), cudaMemcpyDeviceToHost); }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_;
+};
+
+// One device context (appo_ctx): stream, optional model (parameters + Adam).
+class Context {
+ public:
+  explicit Context(int device = 0, uint64_t seed = 1, const appo_model_desc* model = nullptr) {
+    if (model) desc_ = *model;
+    check(appo_ctx_create(model, device, seed, &h_));
+  }
+  ~Context() { appo_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  appo_ctx* get() const { return h_; }
+  void sync() const { check(appo_ctx_sync(h_)); }
+
+  // vtrace (offpolicy.hpp:139): one trajectory, host spans, fp64 in/out like
+  // the reference (computed in fp32 on the device; |err| <= 1e-5 max(|ref|,1)).
+  VTraceOutput vtrace(std::span<const double> rewards, std::span<const double> values,
+                      double bootstrap_value, std::span<const double> target_logp,
+                      std::span<const double> behavior_logp, std::span<const uint8_t> dones,
+                      const VTraceConfig& cfg) const {
+    const size_t T = rewards.size();
+    if (values.size() != T || target_logp.size() != T || behavior_logp.size() != T ||
+        dones.size() != T)
+      throw ContractError("vtrace inputs must share length T");
+    auto f = [](std::span<const double> s) { return std::vector<float>(s.begin(), s.end()); };
+    const std::vector<float> r = f(rewards), v = f(values), tl = f(target_logp),
+                             bl = f(behavior_logp);
+    const float boot = static_cast<float>(bootstrap_value);
+    DeviceBuffer<float> dr(T), dv(T), dtl(T), dbl(T), dboot(1), o0(T), o1(T), o2(T), o3(T);
+    DeviceBuffer<uint8_t> dd(T);
+    dr.upload(r.data()); dv.upload(v.data()); dtl.upload(tl.data()); dbl.upload(bl.data());
+    dboot.upload(&boot); dd.upload(dones.data());
+    check(appo_vtrace(h_, 1, static_cast<int>(T), dr.get(), dv.get(), dboot.get(), dtl.get(),
+                      dbl.get(), dd.get(), static_cast<float>(cfg.gamma),
+                      static_cast<float>(cfg.rho_bar), static_cast<float>(cfg.c_bar), o0.get(),
+                      o1.get(), o2.get(), o3.get()));
+    sync();
+    std::vector<float> a(T), b(T), c(T), d(T);
+    o0.download(a.data()); o1.download(b.data()); o2.download(c.data()); o3.download(d.data());
+    VTraceOutput out;
+    out.v.assign(a.begin(), a.end());
+    out.pg_adv.assign(b.begin(), b.end());
+    out.rho.assign(c.begin(), c.end());
+    out.c.assign(d.begin(), d.end());
+    return out;
+  }
+
+  // Batched device form: [n_traj x T] row-major, the learner gather order.
+  void vtrace(int n_traj, int T, const float* d_rewards, const float* d_values,
+              const float* d_boot, const float* d_tlogp, const float* d_blogp,
+              const uint8_t* d_dones, const VTraceConfig& cfg, float* d_v, float* d_pg) const {
+    check(appo_vtrace(h_, n_traj, T, d_rewards, d_values, d_boot, d_tlogp, d_blogp, d_dones,
+                      static_cast<float>(cfg.gamma), static_cast<float>(cfg.rho_bar),
+                      static_cast<float>(cfg.c_bar), d_v, d_pg, nullptr, nullptr));
+  }
+
+  // total_loss (offpolicy.hpp:224), device arrays of length n
+  LossComponents total_loss(int n, const float* d_ratios, const float* d_adv,
+                            const float* d_values, const float* d_vt, const float* d_ent,
+                            double clip_low = 1.0 / 1.1, double clip_high = 1.1,
+                            double value_coef = 0.5, double entropy_coef = 0.003) const {
+    double o[4];
+    check(appo_total_loss(h_, n, d_ratios, d_adv, d_values, d_vt, d_ent,
+                          static_cast<float>(clip_low), static_cast<float>(clip_high),
+                          static_cast<float>(value_coef), static_cast<float>(entropy_coef), o));
+    return LossComponents{o[0], o[1], o[2], o[3]};
+  }
+
+  // Policy-worker batch inference (orchestrator.hpp:643-656).
+  int64_t policy_forward(int B, const uint8_t* d_obs, const float* d_h_in, uint64_t counter,
+                         int32_t* d_actions, float* d_logp, float* d_h_out, float* d_values,
+                         float* d_logits = nullptr) const {
+    int64_t version = -1;
+    check(appo_policy_forward(h_, B, d_obs, d_h_in, counter, d_actions, d_logp, d_h_out,
+                              d_values, d_logits, &version));
+    return version;
+  }
+
+  // LearnerUnit::step (orchestrator.hpp:760-868) over layout-v2 slots.
+  appo_step_out learner_step(const void* d_region, uint64_t slot_bytes,
+                             std::span<const int32_t> slot_ids, const appo_hparams& hp) const {
+    appo_step_out out{};
+    check(appo_learner_step(h_, d_region, slot_bytes, slot_ids.data(),
+                            static_cast<int>(slot_ids.size()), &hp, &out));
+    return out;
+  }
+
+  // ParamStore::fetch (policy.hpp:498): newest parameters + version
+  int64_t fetch(std::vector<float>& theta) const {
+    theta.resize(static_cast<size_t>(appo_param_count(&desc_)));
+    int64_t v = -1;
+    check(appo_params_get(h_, theta.data(), &v));
+    return v;
+  }
+
+ private:
+  appo_model_desc desc_{};
+  appo_ctx* h_ = nullptr;
+};
+
+inline appo_hparams default_hparams() {
+  appo_hparams hp{};
+  hp.lr = 1e-4f; hp.beta1 = 0.9f; hp.beta2 = 0.999f; hp.eps = 1e-6f; hp.grad_clip = 4.0f;
+  hp.entropy_coef = 0.003f; hp.value_coef = 0.5f; hp.clip_low = 1.0f / 1.1f; hp.clip_high = 1.1f;
+  hp.rho_bar = 1.0f; hp.c_bar = 1.0f; hp.gamma = 0.99f; hp.gae_lambda = 0.95f;
+  hp.adv_source = 0; hp.normalize_adv = 0;
+  return hp;
+}
+
+}  // namespace appo_b200

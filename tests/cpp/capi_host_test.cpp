@@ -1,0 +1,63 @@
+// C++ host test of the reference-facing API (include/appo_b200.hpp over the
+// C ABI): known-answer V-trace (test_offpolicy.cpp:71-86), the reference
+// exception taxonomy, and one batched inference + learner step.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "appo_b200.hpp"
+
+#define REQUIRE(c)                                                     \
+  do {                                                                 \
+    if (!(c)) {                                                        \
+      std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      return 1;                                                        \
+    }                                                                  \
+  } while (0)
+
+int main() {
+  using namespace appo_b200;
+  Context ctx(0, 1);
+  // known answer: v = [2, 1], pg_adv = [2, 1]
+  std::vector<double> r{1.0, 1.0}, v{0.0, 0.0}, tl{-0.5, -0.7}, bl{-0.5, -0.7};
+  std::vector<uint8_t> d{0, 0};
+  auto out = ctx.vtrace(r, v, 0.0, tl, bl, d, VTraceConfig{1.0, 1.0, 1.0});
+  REQUIRE(std::fabs(out.v[0] - 2.0) < 1e-6 && std::fabs(out.v[1] - 1.0) < 1e-6);
+  REQUIRE(std::fabs(out.pg_adv[0] - 2.0) < 1e-6 && std::fabs(out.pg_adv[1] - 1.0) < 1e-6);
+  REQUIRE(out.rho[0] == 1.0 && out.c[1] == 1.0);
+  // error taxonomy: rho_bar < c_bar -> ConfigError; NaN -> NumericError; shape -> ContractError
+  bool got = false;
+  try { ctx.vtrace(r, v, 0.0, tl, bl, d, VTraceConfig{0.5, 1.0, 0.99}); } catch (const ConfigError&) { got = true; }
+  REQUIRE(got);
+  got = false;
+  std::vector<double> rn{NAN, 1.0};
+  try { ctx.vtrace(rn, v, 0.0, tl, bl, d, VTraceConfig{}); } catch (const NumericError&) { got = true; }
+  REQUIRE(got);
+  got = false;
+  std::vector<double> r3{1.0, 1.0, 1.0};
+  try { ctx.vtrace(r3, v, 0.0, tl, bl, d, VTraceConfig{}); } catch (const ContractError&) { got = true; }
+  REQUIRE(got);
+
+  // model: one inference batch and one learner step through the C ABI
+  appo_model_desc desc{3, 72, 128, 6, 8, {0, 0, 0}};
+  Context m(0, 7, &desc);
+  const int B = 16;
+  const size_t od = 3 * 72 * 128;
+  DeviceBuffer<uint8_t> obs(B * od);
+  DeviceBuffer<float> h(B * 512), hout(B * 512), lp(B), val(B);
+  DeviceBuffer<int32_t> act(B);
+  std::vector<uint8_t> hobs(B * od);
+  for (size_t i = 0; i < hobs.size(); ++i) hobs[i] = static_cast<uint8_t>((i * 2654435761u) >> 24);
+  obs.upload(hobs.data());
+  cudaMemset(h.get(), 0, B * 512 * 4);
+  const int64_t ver = m.policy_forward(B, obs.get(), h.get(), 0, act.get(), lp.get(), hout.get(), val.get());
+  m.sync();
+  REQUIRE(ver == 0);
+  std::vector<int32_t> ha(B);
+  act.download(ha.data());
+  for (int a : ha) REQUIRE(a >= 0 && a < 6);
+  std::vector<float> theta;
+  REQUIRE(m.fetch(theta) == 0 && theta.size() == 2872551);
+  std::printf("capi_host_test ok\n");
+  return 0;
+}
