@@ -91,7 +91,17 @@ APPO_API int appo_capi_version(void);
 /* desc may be NULL for a context that only runs the stateless kernels. */
 APPO_API int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo_ctx** out);
 APPO_API int appo_ctx_destroy(appo_ctx* ctx);
+/* A second context on the same device sharing base's model (parameters,
+ * published copies, Adam state) with its own stream and scratch flags: run
+ * the sampler / policy inference on it concurrently with the learner on base
+ * (the policy-worker / learner split of orchestrator.hpp:938-946).  Inference
+ * takes the newest COMPLETED publish (cross-stream events, triple-buffered),
+ * so it never reads a half-written version.  base must outlive it. */
+APPO_API int appo_ctx_create_shared(appo_ctx* base, appo_ctx** out);
 APPO_API int appo_ctx_set_stream(appo_ctx* ctx, void* cuda_stream);
+/* Size persistent / grid-stride grids of this context for n_sms SMs (default:
+ * all), leaving the rest to a concurrently running context (e.g. the learner). */
+APPO_API int appo_ctx_set_sm_budget(appo_ctx* ctx, int n_sms);
 APPO_API int appo_ctx_sync(appo_ctx* ctx);
 /* Number of launches of this library's kernels enqueued on ctx so far. */
 APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);

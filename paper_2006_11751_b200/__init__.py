@@ -122,6 +122,8 @@ _sig("appo_last_error", C.c_char_p)
 _sig("appo_capi_version", _i)
 _sig("appo_ctx_create", _i, C.POINTER(ModelDesc), _i, _u64, C.POINTER(_vp))
 _sig("appo_ctx_destroy", _i, _vp)
+_sig("appo_ctx_create_shared", _i, _vp, C.POINTER(_vp))
+_sig("appo_ctx_set_sm_budget", _i, _vp, _i)
 _sig("appo_ctx_set_stream", _i, _vp, _vp)
 _sig("appo_ctx_sync", _i, _vp)
 _sig("appo_ctx_launch_count", _i64, _vp)
@@ -209,6 +211,26 @@ class Context:
         self.h = h
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         check(_L.appo_ctx_set_stream(self.h, C.c_void_p(self.stream.cuda_stream)))
+
+    def shared(self, stream=None) -> "Context":
+        """A context sharing this one's model on its own CUDA stream
+        (appo_ctx_create_shared): run the sampler there concurrently with the
+        learner on this context."""
+        torch = self.torch
+        c = Context.__new__(Context)
+        c.torch = torch
+        c.device = self.device
+        c.model = self.model
+        c._base = self  # keep the owner alive
+        h = C.c_void_p()
+        check(_L.appo_ctx_create_shared(self.h, C.byref(h)))
+        c.h = h
+        c.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        check(_L.appo_ctx_set_stream(c.h, C.c_void_p(c.stream.cuda_stream)))
+        return c
+
+    def set_sm_budget(self, n_sms: int):
+        check(_L.appo_ctx_set_sm_budget(self.h, n_sms))
 
     def close(self):
         if getattr(self, "h", None):

@@ -52,6 +52,7 @@ struct Ctx {
   void* dp_comm = nullptr;
   int dp_size = 1, dp_rank = 0;
   bool has_model = false;
+  bool owns_model = true;  // false for appo_ctx_create_shared contexts
   appo_model_desc desc{};
   Model* model = nullptr;
 };

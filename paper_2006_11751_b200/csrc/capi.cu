@@ -101,12 +101,26 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
   return APPO_OK;
 }
 
+int appo_ctx_create_shared(appo_ctx* base, appo_ctx** out) {
+  APPO_REQUIRE(base && base->model && out, APPO_ERR_CONTRACT,
+               "appo_ctx_create_shared: base context with a model required");
+  appo_ctx* c = nullptr;
+  int st = appo_ctx_create(nullptr, base->device, base->seed, &c);
+  if (st) return st;
+  c->has_model = true;
+  c->desc = base->desc;
+  c->model = base->model;
+  c->owns_model = false;
+  *out = c;
+  return APPO_OK;
+}
+
 int appo_ctx_destroy(appo_ctx* ctx) {
   if (!ctx) return APPO_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   cudaDeviceSynchronize();
-  if (ctx->model) model_destroy(ctx);
+  if (ctx->model && ctx->owns_model) model_destroy(ctx);
   appo_b200::dp_destroy(ctx);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaFree(ctx->d_flags);
@@ -114,6 +128,15 @@ int appo_ctx_destroy(appo_ctx* ctx) {
   cudaFree(ctx->d_counter);
   cudaFreeHost(ctx->h_pinned);
   delete ctx;
+  return APPO_OK;
+}
+
+int appo_ctx_set_sm_budget(appo_ctx* ctx, int n_sms) {
+  CTX_OR_RETURN(ctx);
+  int dev_sms = 0;
+  APPO_CUDA_TRY(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  APPO_REQUIRE(n_sms >= 1, APPO_ERR_CONTRACT, "sm budget must be >= 1");
+  ctx->num_sms = n_sms < dev_sms ? n_sms : dev_sms;
   return APPO_OK;
 }
 

@@ -2,19 +2,22 @@
 // bootstrap step) and the BPTT reverse sweep each run as ONE cooperative
 // kernel; the per-step recurrent product runs on tcgen05.
 //
-// Partition: 32 CTAs x 16 hidden units.  A CTA owns units j in [16c, 16c+16)
-// for all (<= 64) trajectories:
-//   forward : D[i][g] = sum_k h_t[i][k] W_hh[g][k], g over the CTA's 48 gate
-//             rows (r, z, n of its 16 units).  UMMA M=64 (trajectories) x N=48
-//             x K=512; B = W slice resident in smem (bf16, SW128 K-major), A =
-//             h_t staged from global each step.  The epilogue applies the cell
-//             (PyTorch r,z,n convention; oracle gru_fwd) for its units, so the
-//             only cross-CTA traffic is h_{t+1} (64 x 512 bf16, L2-resident).
-//   backward: gate gradients for own units (oracle orc_learner_step BPTT),
-//             published as dgh_t (64 x 1536 bf16); after a grid barrier
-//             dnext[i][j] = dh*z + sum_g dgh_t[i][g] W_hh[g][j] as UMMA M=64 x
-//             N=16 x K=1536 with W_hh[:, own units]^T resident (K-major) and
-//             dgh_t staged in three 512-wide K chunks (double-buffered).
+//   forward : 32 CTAs x 16 hidden units.  D[i][g] = sum_k h_t[i][k] W_hh[g][k]
+//             over the CTA's 48 gate rows (r, z, n of its units): UMMA M=64
+//             (trajectories) x N=48 x K=512, B = W slice resident in smem
+//             (bf16, SW128 K-major), A = h_t staged from global each step.
+//             The epilogue applies the cell (PyTorch r,z,n; oracle gru_fwd)
+//             for the CTA's units; the only cross-CTA traffic is h_{t+1}
+//             (64 x 512 bf16, L2-resident) behind one grid barrier per step.
+//   backward: 64 CTAs x 8 units.  Gate gradients for own units (oracle
+//             orc_learner_step BPTT) are published as dgh_t (64 x 1536 bf16);
+//             after the barrier dnext[i][j] = dh*z + sum_g dgh_t[i][g] W_hh[g][j]
+//             as UMMA M=64 x N=8 x K=1536 with W_hh[:, own]^T resident and all
+//             of dgh_t staged at once (three 64 KB K chunks).
+// Staging uses cp.async (16 B, L2-only) straight into the swizzled tile, so a
+// step costs one L2 round trip + one UMMA chain + one barrier.  Per-cell state
+// (h, b_hh, prefetched next-step inputs, dh*z) lives in registers because a
+// thread owns the same (trajectory, unit) cells every step.
 // TMEM layout for M=64 (cta_group::1): row m lives in lane (m % 16) + 32*(m/16)
 // (CuTe "half subpartitions" atom, mma_traits_sm100.hpp), so warp w's lanes
 // 0..15 hold rows 16w..16w+15.
@@ -27,22 +30,24 @@
 namespace appo_b200 {
 namespace {
 
-constexpr int UPC = 16;                    // hidden units per CTA
-constexpr int NCTA = kHidden / UPC;        // 32
 constexpr int MAXTRAJ = 64;                // UMMA M
 constexpr int THR = 256;
-constexpr int NG = 3 * UPC;                // 48 gate rows per CTA (forward N)
-constexpr int KB_BYTES_A = MAXTRAJ * 128;  // one 64-wide K block of the A tile
-constexpr int A_FWD = 8 * KB_BYTES_A;      // 64 x 512 bf16 = 64 KB
+constexpr int KB_BYTES_A = MAXTRAJ * 128;  // one 64-wide K block of a 64-row A tile
+constexpr int A_TILE = 8 * KB_BYTES_A;     // 64 x 512 bf16 = 64 KB
+
+constexpr int UPC_F = 16;                  // forward: units per CTA
+constexpr int NCTA_F = kHidden / UPC_F;    // 32
+constexpr int NG = 3 * UPC_F;              // 48 gate rows per CTA (forward N)
 constexpr int B_FWD = 8 * NG * 128;        // 48 x 512 bf16 = 48 KB
-constexpr int A_CH = 8 * KB_BYTES_A;       // backward K chunk 64 x 512 bf16 = 64 KB
-constexpr int B_BWD = 24 * UPC * 128;      // 16 x 1536 bf16 = 48 KB
+
+constexpr int UPC_B = 8;                   // backward: units per CTA (UMMA N)
+constexpr int NCTA_B = kHidden / UPC_B;    // 64
+constexpr int B_BWD = 24 * UPC_B * 128;    // 8 x 1536 bf16 = 24 KB
 
 __device__ __forceinline__ uint16_t f2bf_(float f) {
   __nv_bfloat16 h = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&h);
 }
-__device__ __forceinline__ float bf2f_(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 __device__ __forceinline__ float sig_(float x) { return 1.0f / (1.0f + expf(-x)); }
 
 __device__ __forceinline__ void fence_async_smem() {
@@ -70,30 +75,27 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target)
   __syncthreads();
 }
 
-// Stage rows [n_rows] x 512 bf16 (global row stride ld elements, starting at
-// column col0) into a 64-row SW128 K-major tile; rows >= n_rows are zero.
-__device__ __forceinline__ void stage_a(uint8_t* tile, const uint16_t* src, int n_rows, int64_t ld,
-                                        int col0) {
+// Issue cp.async copies of rows [n_rows] x 512 bf16 (global row stride ld
+// elements, from column col0) into a 64-row SW128 K-major tile; rows >=
+// n_rows are zero-filled.  Caller commits / waits.
+__device__ __forceinline__ void stage_async(uint8_t* tile, const uint16_t* src, int n_rows,
+                                            int64_t ld, int col0) {
   constexpr int CH = MAXTRAJ * 64;  // 16-byte chunks in 64 x 512
-  for (int base = threadIdx.x; base < CH; base += THR * 8) {
-    uint4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = base + u * THR;
-      const int r = e >> 6, c = e & 63;
-      v[u] = (e < CH && r < n_rows)
-                 ? __ldcg(reinterpret_cast<const uint4*>(src + (int64_t)r * ld + col0) + c)
-                 : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = base + u * THR;
-      if (e < CH) {
-        const int r = e >> 6, c = e & 63;
-        *reinterpret_cast<uint4*>(tile + sw128(MAXTRAJ, r, c >> 3, c & 7)) = v[u];
-      }
-    }
+  const uint32_t base = sm100::smem_u32(tile);
+#pragma unroll 4
+  for (int e = threadIdx.x; e < CH; e += THR) {
+    const int r = e >> 6, c = e & 63;
+    const bool ok = r < n_rows;
+    const uint16_t* g = src + (int64_t)(ok ? r : 0) * ld + col0 + c * 8;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                     base + sw128(MAXTRAJ, r, c >> 3, c & 7)),
+                 "l"(g), "r"(ok ? 16 : 0)
+                 : "memory");
   }
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 struct FwdArgs {
@@ -102,8 +104,8 @@ struct FwdArgs {
   const uint16_t* whh;   // bf16 [1536][512] (published copy of the master)
   const float* bhh;      // [1536]
   const uint8_t* done;   // [B]
-  float* hbuf;           // [2][n_traj][512] fp32 ping-pong (hbuf[0] = h0 on entry)
-  uint16_t* hbuf_bf;     // [2][n_traj][512] bf16 ping-pong
+  float* hbuf;           // [n_traj][512] fp32 h0 on entry
+  uint16_t* hbuf_bf;     // [2][n_traj][512] bf16 ping-pong h_t (exchange)
   float* core;           // [R][512]
   uint16_t* core_bf;     // [R][512]
   float* gates;          // [R][4][512]
@@ -117,18 +119,18 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* tA = sm;
-  uint8_t* tB = sm + A_FWD;
+  uint8_t* tB = sm + A_TILE;
   float* gh = reinterpret_cast<float*>(tB + B_FWD);              // [64][NG]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(gh + MAXTRAJ * NG);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int j0 = blockIdx.x * UPC;
+  const int j0 = blockIdx.x * UPC_F;
   const int B = a.n_traj * a.T;
 
   // resident B operand: gate row n = g*16 + u (g in r,z,n) -> W_hh row g*512 + j0 + u
   for (int e = tid; e < NG * 64; e += THR) {
     const int n = e >> 6, c = e & 63;
-    const int grow = (n / UPC) * kHidden + j0 + (n % UPC);
+    const int grow = (n / UPC_F) * kHidden + j0 + (n % UPC_F);
     *reinterpret_cast<uint4*>(tB + sw128(NG, n, c >> 3, c & 7)) =
         reinterpret_cast<const uint4*>(a.whh + (int64_t)grow * kHidden)[c];
   }
@@ -140,11 +142,39 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
     sm100::tmem_alloc(tslot, 64);
     sm100::tmem_relinquish();
   }
-  // first h_t (bf16) from the fp32 h0, own columns only
-  for (int e = tid; e < a.n_traj * UPC; e += THR) {
-    const int64_t o = (int64_t)(e / UPC) * kHidden + j0 + (e % UPC);
-    a.hbuf_bf[o] = f2bf_(a.hbuf[o]);
+  // Per-thread cells (trajectory i, own unit u) are fixed across steps.
+  constexpr int CPT = MAXTRAJ * UPC_F / THR;  // 4
+  const int n_cells = a.n_traj * UPC_F;
+  float hreg[CPT], b3[CPT][3], g3[CPT][3];
+  uint8_t dn[CPT];
+  auto prefetch = [&](int t) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = tid + c * THR;
+      if (e < n_cells) {
+        const int i = e / UPC_F, j = j0 + e % UPC_F;
+        const int64_t row = (t < a.T) ? (int64_t)i * a.T + t : (int64_t)B + i;
+        const float* gir = a.gi + row * kGates;
+        g3[c][0] = __ldg(gir + j);
+        g3[c][1] = __ldg(gir + kHidden + j);
+        g3[c][2] = __ldg(gir + 2 * kHidden + j);
+        dn[c] = (t < a.T) ? a.done[(int64_t)i * a.T + t] : 0;
+      }
+    }
+  };
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int e = tid + c * THR;
+    if (e < n_cells) {
+      const int i = e / UPC_F, j = j0 + e % UPC_F;
+      hreg[c] = a.hbuf[(int64_t)i * kHidden + j];
+      a.hbuf_bf[(int64_t)i * kHidden + j] = f2bf_(hreg[c]);  // first h_t, own columns
+      b3[c][0] = a.bhh[j];
+      b3[c][1] = a.bhh[kHidden + j];
+      b3[c][2] = a.bhh[2 * kHidden + j];
+    }
   }
+  prefetch(0);
   sm100::tc_fence_before();
   grid_barrier(a.bar, gridDim.x);  // h0 bf16 complete everywhere
   sm100::tc_fence_after();
@@ -156,7 +186,8 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
   for (int t = 0; t <= a.T; ++t) {
     const size_t cur = (size_t)(t & 1) * a.n_traj * kHidden;
     const size_t nxt = (size_t)((t + 1) & 1) * a.n_traj * kHidden;
-    stage_a(tA, a.hbuf_bf + cur, a.n_traj, kHidden, 0);
+    stage_async(tA, a.hbuf_bf + cur, a.n_traj, kHidden, 0);
+    cp_async_wait_all();
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -188,18 +219,19 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
     }
     sm100::tc_fence_before();
     __syncthreads();
-    // cells: 64 traj x 16 units, 4 per thread
-    for (int e = tid; e < a.n_traj * UPC; e += THR) {
-      const int i = e / UPC, u = e % UPC, j = j0 + u;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = tid + c * THR;
+      if (e >= n_cells) continue;
+      const int i = e / UPC_F, u = e % UPC_F, j = j0 + u;
       const int64_t row = (t < a.T) ? (int64_t)i * a.T + t : (int64_t)B + i;
-      const float* gir = a.gi + row * kGates;
-      const float ghr = gh[i * NG + u] + a.bhh[j];
-      const float ghz = gh[i * NG + UPC + u] + a.bhh[kHidden + j];
-      const float ghn = gh[i * NG + 2 * UPC + u] + a.bhh[2 * kHidden + j];
-      const float rr = sig_(gir[j] + ghr);
-      const float z = sig_(gir[kHidden + j] + ghz);
-      const float n = tanhf(gir[2 * kHidden + j] + rr * ghn);
-      const float hp = __ldcg(a.hbuf + cur + (int64_t)i * kHidden + j);
+      const float ghr = gh[i * NG + u] + b3[c][0];
+      const float ghz = gh[i * NG + UPC_F + u] + b3[c][1];
+      const float ghn = gh[i * NG + 2 * UPC_F + u] + b3[c][2];
+      const float rr = sig_(g3[c][0] + ghr);
+      const float z = sig_(g3[c][1] + ghz);
+      const float n = tanhf(g3[c][2] + rr * ghn);
+      const float hp = hreg[c];
       const float h = (1.0f - z) * n + z * hp;
       a.core[row * kHidden + j] = h;
       a.core_bf[row * kHidden + j] = f2bf_(h);
@@ -211,12 +243,15 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
       a.hin[row * kHidden + j] = hp;
       a.hbf[row * kHidden + j] = f2bf_(hp);
       if (t < a.T) {
-        const float hn = a.done[(int64_t)i * a.T + t] ? 0.0f : h;
-        a.hbuf[nxt + (int64_t)i * kHidden + j] = hn;
+        const float hn = dn[c] ? 0.0f : h;
+        hreg[c] = hn;
         a.hbuf_bf[nxt + (int64_t)i * kHidden + j] = f2bf_(hn);
       }
     }
-    if (t < a.T) grid_barrier(a.bar, ++epoch * gridDim.x);
+    if (t < a.T) {
+      prefetch(t + 1);  // independent of the exchange: overlaps the barrier
+      grid_barrier(a.bar, ++epoch * gridDim.x);
+    }
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -243,17 +278,16 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
-  uint8_t* tA[2] = {sm, sm + A_CH};
-  uint8_t* tB = sm + 2 * A_CH;
-  float* dn = reinterpret_cast<float*>(tB + B_BWD);     // [64][16] dnext (own units)
-  float* dd = dn + MAXTRAJ * UPC;                       // [64][16] dh * z
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(dd + MAXTRAJ * UPC);  // [2] per A buffer
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+  uint8_t* tA = sm;                                      // 3 x 64 KB: all of dgh_t
+  uint8_t* tB = sm + 3 * A_TILE;
+  float* mm = reinterpret_cast<float*>(tB + B_BWD);      // [64][8] dgh . W_hh[:, own]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(mm + MAXTRAJ * UPC_B);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int j0 = blockIdx.x * UPC;
+  const int j0 = blockIdx.x * UPC_B;
 
   // resident B: row n = own unit u, K = gate g: B[u][g] = W_hh[g][j0 + u] (K-major)
-  for (int e = tid; e < UPC * (kGates / 8); e += THR) {
+  for (int e = tid; e < UPC_B * (kGates / 8); e += THR) {
     const int u = e / (kGates / 8), c8 = e % (kGates / 8);  // chunk of 8 gates
     uint32_t w[4];
 #pragma unroll
@@ -262,13 +296,11 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
       w[p] = (uint32_t)a.whh[(int64_t)g * kHidden + j0 + u] |
              ((uint32_t)a.whh[(int64_t)(g + 1) * kHidden + j0 + u] << 16);
     }
-    *reinterpret_cast<uint4*>(tB + sw128(UPC, u, c8 >> 3, c8 & 7)) =
+    *reinterpret_cast<uint4*>(tB + sw128(UPC_B, u, c8 >> 3, c8 & 7)) =
         make_uint4(w[0], w[1], w[2], w[3]);
   }
-  for (int e = tid; e < MAXTRAJ * UPC; e += THR) dn[e] = 0.0f;
   if (tid == 0) {
-    sm100::mbar_init(&mbar[0], 1);
-    sm100::mbar_init(&mbar[1], 1);
+    sm100::mbar_init(mbar, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) {
@@ -279,22 +311,45 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
-  constexpr uint32_t idesc = sm100::make_idesc_bf16(MAXTRAJ, UPC, 0, 0);
+  constexpr uint32_t idesc = sm100::make_idesc_bf16(MAXTRAJ, UPC_B, 0, 0);
   unsigned epoch = 0;
-  uint32_t ph[2] = {0, 0};
+  uint32_t phase = 0;
+
+  constexpr int CPT = MAXTRAJ * UPC_B / THR;  // 2 cells per thread
+  const int n_cells = a.n_traj * UPC_B;
+  float pf[CPT][7];  // dcore, r, z, n, ghn, h_in, keep
+  float ddr[CPT];    // dh*z of the later step
+  auto prefetch = [&](int t) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = tid + c * THR;
+      if (e < n_cells) {
+        const int i = e / UPC_B, j = j0 + e % UPC_B;
+        const int64_t s = (int64_t)i * a.T + t;
+        const float* gs = a.gates + s * 4 * kHidden;
+        pf[c][0] = __ldg(a.dcore + s * kHidden + j);
+        pf[c][1] = __ldg(gs + j);
+        pf[c][2] = __ldg(gs + kHidden + j);
+        pf[c][3] = __ldg(gs + 2 * kHidden + j);
+        pf[c][4] = __ldg(gs + 3 * kHidden + j);
+        pf[c][5] = __ldg(a.hin + s * kHidden + j);
+        pf[c][6] = a.done[s] ? 0.0f : 1.0f;
+      }
+    }
+  };
+  prefetch(a.T - 1);
 
   for (int t = a.T - 1; t >= 0; --t) {
     uint16_t* xb = a.dghx + (size_t)(t & 1) * a.n_traj * kGates;
-    // gate gradients for own units
-    for (int e = tid; e < a.n_traj * UPC; e += THR) {
-      const int i = e / UPC, u = e % UPC, j = j0 + u;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = tid + c * THR;
+      if (e >= n_cells) continue;
+      const int i = e / UPC_B, u = e % UPC_B, j = j0 + u;
       const int64_t s = (int64_t)i * a.T + t;
-      const float keep = a.done[s] ? 0.0f : 1.0f;
-      const float dh = a.dcore[s * kHidden + j] + keep * dn[i * UPC + u];
-      const float* gs = a.gates + s * 4 * kHidden;
-      const float r = gs[j], z = gs[kHidden + j], n = gs[2 * kHidden + j];
-      const float ghn = gs[3 * kHidden + j];
-      const float hp = a.hin[s * kHidden + j];
+      const float dnext = (t == a.T - 1) ? 0.0f : ddr[c] + mm[i * UPC_B + u];
+      const float dh = pf[c][0] + pf[c][6] * dnext;
+      const float r = pf[c][1], z = pf[c][2], n = pf[c][3], ghn = pf[c][4], hp = pf[c][5];
       const float dnn = dh * (1.0f - z);
       const float dz = dh * (hp - n);
       const float dan = dnn * (1.0f - n * n);
@@ -313,49 +368,41 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
       xr[j] = dgr;
       xr[kHidden + j] = dgz;
       xr[2 * kHidden + j] = dgn;
-      dd[i * UPC + u] = dh * z;
+      ddr[c] = dh * z;
     }
     if (t == 0) break;  // d(h0) is not needed
+    prefetch(t - 1);    // independent of the exchange: overlaps barrier + MMA
     grid_barrier(a.bar, ++epoch * gridDim.x);
-    // dnext = dd + dgh_t . W_hh[:, own]: three K chunks of 512, double-buffered A
-    for (int ch = 0; ch < 3; ++ch) {
-      const int buf = ch & 1;
-      if (ch >= 2) {  // buffer reuse: wait for the MMAs of chunk ch-2
-        sm100::mbar_wait(&mbar[buf], ph[buf]);
-        ph[buf] ^= 1;
-      }
-      stage_a(tA[buf], xb, a.n_traj, kGates, ch * 512);
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        sm100::tc_fence_after();
-        const uint32_t a0 = sm100::smem_u32(tA[buf]), b0 = sm100::smem_u32(tB);
+    // dnext = dh*z + dgh_t . W_hh[:, own]: all of dgh_t in one async stage
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int kg = ch * 32 + k;  // global K16 step over 1536
-          const uint64_t ad =
-              sm100::make_sdesc(a0 + (k >> 2) * KB_BYTES_A + (k & 3) * 32, 16, 1024);
-          const uint64_t bd =
-              sm100::make_sdesc(b0 + (kg >> 2) * UPC * 128 + (kg & 3) * 32, 16, 1024);
-          sm100::umma_f16(tmem, ad, bd, idesc, kg > 0 ? 1u : 0u);
-        }
-        sm100::umma_commit(&mbar[buf]);
+    for (int ch = 0; ch < 3; ++ch) stage_async(tA + ch * A_TILE, xb, a.n_traj, kGates, ch * 512);
+    cp_async_wait_all();
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      sm100::tc_fence_after();
+      const uint32_t a0 = sm100::smem_u32(tA), b0 = sm100::smem_u32(tB);
+#pragma unroll 8
+      for (int kg = 0; kg < 96; ++kg) {  // K16 steps over 1536
+        const uint64_t ad = sm100::make_sdesc(
+            a0 + (kg >> 5) * A_TILE + ((kg & 31) >> 2) * KB_BYTES_A + (kg & 3) * 32, 16, 1024);
+        const uint64_t bd =
+            sm100::make_sdesc(b0 + (kg >> 2) * UPC_B * 128 + (kg & 3) * 32, 16, 1024);
+        sm100::umma_f16(tmem, ad, bd, idesc, kg > 0 ? 1u : 0u);
       }
+      sm100::umma_commit(mbar);
     }
-    // chunks 1 (buf 1) and 2 (buf 0) still outstanding; MMAs complete in order
-    sm100::mbar_wait(&mbar[1], ph[1]);
-    ph[1] ^= 1;
-    sm100::mbar_wait(&mbar[0], ph[0]);
-    ph[0] ^= 1;
+    sm100::mbar_wait(mbar, phase);
+    phase ^= 1;
     sm100::tc_fence_after();
     if (warp < 4) {
       uint32_t r[16];
-      sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16), r);
+      sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16), r);  // cols 0..7 used
       sm100::tmem_ld_wait();
       if (lane < 16) {
         const int i = 16 * warp + lane;
 #pragma unroll
-        for (int u = 0; u < UPC; ++u) dn[i * UPC + u] = dd[i * UPC + u] + __uint_as_float(r[u]);
+        for (int u = 0; u < UPC_B; ++u) mm[i * UPC_B + u] = __uint_as_float(r[u]);
       }
     }
     sm100::tc_fence_before();
@@ -369,8 +416,9 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   }
 }
 
-constexpr int FWD_SMEM = 1024 + A_FWD + B_FWD + MAXTRAJ * NG * 4 + 64;
-constexpr int BWD_SMEM = 1024 + 2 * A_CH + B_BWD + 2 * MAXTRAJ * UPC * 4 + 64;
+constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + MAXTRAJ * NG * 4 + 64;
+constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + MAXTRAJ * UPC_B * 4 + 64;
+static_assert(BWD_SMEM <= 227 * 1024, "backward GRU smem");
 
 }  // namespace
 
@@ -390,8 +438,8 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
   FwdArgs a{n_traj, T, gi, whh, bhh, done, hbuf, hbuf_bf, core, core_bf, gates, hin, hbf, bar};
   void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_fwd_kernel");
-  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_fwd_kernel, dim3(NCTA), dim3(THR), args,
-                                            FWD_SMEM, c->stream));
+  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_fwd_kernel, dim3(NCTA_F), dim3(THR),
+                                            args, FWD_SMEM, c->stream));
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T + 1);
   timing_end(c, "gru_seq_fwd_kernel", ev);
   c->launches++;
@@ -411,8 +459,8 @@ int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* 
   BwdArgs a{n_traj, T, dcore, done, gates, hin, whh, dghx, dgi, dgh, bar};
   void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_bwd_kernel");
-  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_bwd_kernel, dim3(NCTA), dim3(THR), args,
-                                            BWD_SMEM, c->stream));
+  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_bwd_kernel, dim3(NCTA_B), dim3(THR),
+                                            args, BWD_SMEM, c->stream));
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T - 1);
   timing_end(c, "gru_seq_bwd_kernel", ev);
   c->launches++;

@@ -290,12 +290,23 @@ int dp_allreduce_grad(Ctx* c, float* grad, int64_t n);  // dp.cu
 // batch or trajectory slots): encoder + GRU + heads + sampling.
 int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, const float* h_in,
                   uint64_t counter0, int32_t* actions, float* logp, float* h_out, float* values,
-                  float* logits) {
+                  float* logits, int64_t* version_out) {
   Model* M = c->model;
   const Dims& d = M->d;
   Scratch& s = M->si;
   TRY(alloc_scratch(c, M, s, B, 0, false));
-  const int pub = M->published;
+  // ParamStore::fetch (policy.hpp:498-509): newest COMPLETED publish; if the
+  // newest Adam step is still running (possibly on the learner's stream) take
+  // the previous one instead of waiting for it.
+  // Candidates: the newest kPub-1 publishes (the oldest slot is the learner's
+  // next write target); take the newest whose Adam step has completed.
+  int pub = M->published;
+  for (int back = 0; back <= Model::kPub - 2; ++back) {
+    pub = (M->published - back + Model::kPub) % Model::kPub;
+    if (cudaEventQuery(M->ready_ev[pub]) == cudaSuccess) break;
+  }
+  APPO_CUDA_TRY(cudaStreamWaitEvent(c->stream, M->ready_ev[pub], 0));
+  if (version_out) *version_out = M->pub_version[pub];
   const uint16_t* wb = M->pub_bf16[pub];
   const float* pf = M->pub_f32[pub];
   ObsSrc src;
@@ -312,6 +323,9 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
                 Operand{wb + d.off_whh, kHidden, false}, g, 256));
   TRY(k_gru_infer(c, B, d.A, s.gi, s.gh, h_in, pf + d.off_wpi, pf + d.off_bpi, pf + d.off_wv,
                   pf + d.off_bv, M->sample_key, counter0, h_out, actions, logp, values, logits));
+  // last reader of pub[pub] on this stream: the learner waits on this event
+  // before overwriting the buffer (it may run on another stream)
+  APPO_CUDA_TRY(cudaEventRecord(M->pub_ev[pub], c->stream));
   return APPO_OK;
 }
 
@@ -332,9 +346,11 @@ int model_create(Ctx* c) {
   APPO_CUDA_TRY(cudaMalloc(&M->m, P * 4));
   APPO_CUDA_TRY(cudaMalloc(&M->v, P * 4));
   APPO_CUDA_TRY(cudaMalloc(&M->grad, P * 4));
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < Model::kPub; ++k) {
     APPO_CUDA_TRY(cudaMalloc(&M->pub_bf16[k], P * 2));
     APPO_CUDA_TRY(cudaMalloc(&M->pub_f32[k], P * 4));
+    APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->pub_ev[k], cudaEventDisableTiming));
+    APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->ready_ev[k], cudaEventDisableTiming));
   }
   M->sample_key = host_derive_seed(c->seed, 0x9900);
   APPO_CUDA_TRY(cudaMallocHost(&M->ring_host, sizeof(double) * Model::kRing * Model::kRingStride));
@@ -352,9 +368,11 @@ void model_destroy(Ctx* c) {
   cudaFree(M->m);
   cudaFree(M->v);
   cudaFree(M->grad);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < Model::kPub; ++k) {
     cudaFree(M->pub_bf16[k]);
     cudaFree(M->pub_f32[k]);
+    if (M->pub_ev[k]) cudaEventDestroy(M->pub_ev[k]);
+    if (M->ready_ev[k]) cudaEventDestroy(M->ready_ev[k]);
   }
   if (M->ring_host) cudaFreeHost(M->ring_host);
   for (int k = 0; k < Model::kRing; ++k)
@@ -400,17 +418,19 @@ int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version) {
   APPO_REQUIRE(h_src != nullptr, APPO_ERR_CONTRACT, "params_set: null source");
   std::vector<uint16_t> bf(P);
   for (int64_t i = 0; i < P; ++i) bf[i] = host_f2bf(h_src[i]);
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(cudaDeviceSynchronize());  // no stream may be reading the published copies
   APPO_CUDA_TRY(cudaMemcpy(M->theta, h_src, P * 4, cudaMemcpyHostToDevice));
   APPO_CUDA_TRY(cudaMemset(M->m, 0, P * 4));
   APPO_CUDA_TRY(cudaMemset(M->v, 0, P * 4));
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < Model::kPub; ++k) {
     APPO_CUDA_TRY(cudaMemcpy(M->pub_f32[k], h_src, P * 4, cudaMemcpyHostToDevice));
     APPO_CUDA_TRY(cudaMemcpy(M->pub_bf16[k], bf.data(), P * 2, cudaMemcpyHostToDevice));
   }
   M->version = version;
   M->adam_t = 0;
   M->published = 0;
+  M->published_prev = 0;
+  for (int k = 0; k < Model::kPub; ++k) M->pub_version[k] = version;
   return APPO_OK;
 }
 
@@ -455,14 +475,14 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
   APPO_REQUIRE(B >= 0, APPO_ERR_CONTRACT, "policy_forward: batch must be >= 0");
-  if (h_version_out) *h_version_out = M->version;
+  if (h_version_out) *h_version_out = M->pub_version[M->published];
   if (B == 0) return APPO_OK;
   APPO_REQUIRE(d_obs && d_h_in && d_actions && d_logp && d_h_out && d_values, APPO_ERR_CONTRACT,
                "policy_forward: null buffer");
   APPO_REQUIRE((reinterpret_cast<uintptr_t>(d_obs) & 3) == 0, APPO_ERR_CONTRACT,
                "policy_forward: obs must be 4-byte aligned");
   return sampler_infer(ctx, d_obs, M->d.obs_dim, B, d_h_in, rng_counter0, d_actions, d_logp,
-                       d_h_out, d_values, d_logits);
+                       d_h_out, d_values, d_logits, h_version_out);
 }
 
 int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
@@ -691,17 +711,22 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   TRY(dp_allreduce_grad(ctx, G, d.total));
 
   // ---- global-norm clip + Adam; publish into the other buffer ----
-  const int next = pub ^ 1;
+  const int next = (pub + 1) % Model::kPub;
+  // do not overwrite a published copy an inference (any stream) may still read
+  APPO_CUDA_TRY(cudaStreamWaitEvent(st, M->pub_ev[next], 0));
   M->adam_t += 1;
   TRY(launch_adam(ctx, d.total, M->theta, M->m, M->v, G, M->adam_t, hp->lr, hp->beta1,
                   hp->beta2, hp->eps, hp->grad_clip, s.stats + 8, M->pub_bf16[next],
                   M->pub_f32[next], ctx->d_counter + 6));
   APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
   APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
+  APPO_CUDA_TRY(cudaEventRecord(M->ready_ev[next], st));
   M->last_ring = ring;
   // Optimistic publish: the Adam kernel always rewrites pub[next] (with the
-  // unchanged parameters when the step is rejected), so inference launched
-  // after this point on the stream reads a consistent buffer.
+  // unchanged parameters when the step is rejected); readers on other streams
+  // wait on ready_ev[next] (or take the previous buffer while it runs).
+  M->pub_version[next] = M->version + 1;
+  M->published_prev = M->published;
   M->published = next;
   M->version += 1;
   M->pending += 1;

@@ -65,9 +65,19 @@ struct Model {
   float* m = nullptr;
   float* v = nullptr;
   float* grad = nullptr;
-  uint16_t* pub_bf16[2] = {nullptr, nullptr};
-  float* pub_f32[2] = {nullptr, nullptr};
-  int published = 0;
+  // Published inference copies, triple-buffered: the learner writes
+  // pub[(published+1)%3] (after waiting on pub_ev of that buffer, recorded by
+  // the last inference that read it, possibly on another stream), then flips
+  // `published` -- the device-side counterpart of ParamStore's seqlock
+  // (policy.hpp:457-519): inference never observes a half-written version.
+  static constexpr int kPub = 8;
+  uint16_t* pub_bf16[kPub] = {};
+  float* pub_f32[kPub] = {};
+  cudaEvent_t pub_ev[kPub] = {};    // recorded after the last inference read of pub[k]
+  cudaEvent_t ready_ev[kPub] = {};  // recorded after the Adam step that wrote pub[k]
+  int64_t pub_version[kPub] = {};   // parameter version held by pub[k]
+  int published = 0;                // newest submitted publish
+  int published_prev = 0;           // the one before (complete when `published` is in flight)
   int64_t version = 0;
   int64_t adam_t = 0;
   uint64_t sample_key = 0;

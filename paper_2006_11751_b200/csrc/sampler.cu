@@ -27,7 +27,7 @@
 namespace appo_b200 {
 int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, const float* h_in,
                   uint64_t counter0, int32_t* actions, float* logp, float* h_out, float* values,
-                  float* logits);
+                  float* logits, int64_t* version_out);
 }
 
 using namespace appo_b200;
@@ -219,10 +219,10 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
     APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
                 s->episode, region, slot_bytes, (int64_t)slot_base, obs_off);
   }
-  const int64_t version = M->version;
+  int64_t version = 0;  // version of the parameters this inference used (ExchangeLayout field)
   int st = sampler_infer(c, region + (uint64_t)slot_base * slot_bytes + obs_off, slot_bytes,
                          s->n_envs, s->hidden, s->steps_done * (uint64_t)s->n_envs, s->actions,
-                         s->logp, s->h_out, s->values, nullptr);
+                         s->logp, s->h_out, s->values, nullptr, &version);
   if (st) return st;
   SlotOffsets off;
   std::memcpy(&off, d.slot, sizeof(off));

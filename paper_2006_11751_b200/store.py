@@ -33,6 +33,9 @@ class TrajectoryStore:
         self.obs_dim = desc.obs_dim
         self.region = torch.zeros(n_slots * self.slot_bytes, dtype=torch.uint8,
                                   device=f"cuda:{device}")
+        # the region is written by library streams other than torch's: make the
+        # zero fill visible to them before first use
+        torch.cuda.synchronize(device)
 
     # ---- typed views of one slot (device tensors aliasing the region) ----
     def _view(self, slot: int, field: str, dtype, count: int):

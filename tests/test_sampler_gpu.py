@@ -98,3 +98,34 @@ def test_learner_consumes_sampler_slots(setup):
     out = ctx.learner_step(store.region, store.slot_bytes, list(range(n, 2 * n)))
     assert np.isfinite(out["total_loss"]) and out["version"] == 1
     assert out["lag_mean"] == 0.0  # every step stamped with version 0
+
+
+def test_overlapped_sampler_and_learner_streams():
+    # APPO decoupling: the sampler runs on a context sharing the model on its own
+    # stream while the learner trains on the other rollout set.  Inference must
+    # only ever see complete published versions: stamped versions are
+    # non-decreasing within a trajectory (trajstore.hpp:174-176) and never ahead
+    # of the learner.
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    learner = appo.Context(0, seed=4, model=desc)
+    actor = learner.shared()
+    n = 128
+    store = appo.TrajectoryStore(desc, 2 * n)
+    smp = appo.Sampler(actor, n, episode_len=9, seed=5)
+    ids = np.arange(n, dtype=np.int32).reshape(-1, 32)
+    for k in range(4):
+        base = (k % 2) * n
+        for t in range(desc.T):
+            smp.step(store, base, t)
+        if k > 0:
+            prev = ((k - 1) % 2) * n
+            for mb in ids:
+                learner.learner_submit(store.region, store.slot_bytes, mb + prev)
+            out = learner.learner_collect()
+            assert np.isfinite(out["total_loss"])
+        torch.cuda.synchronize()
+    final = learner.version
+    assert final == 3 * len(ids)
+    for s in range(2 * n):
+        v = store.versions(s).cpu().numpy()
+        assert np.all(np.diff(v) >= 0) and v.min() >= 0 and v.max() <= final
