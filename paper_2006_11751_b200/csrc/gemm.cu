@@ -36,11 +36,24 @@ constexpr int STAGES = 4;
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int A_TILE_BYTES = BM * BK * 2;  // 16 KB
 
+// Implicit-GEMM A operand (convolution forward): row m = output position
+// (image r = m / P, p = m % P, y = p / Wo, x = p % Wo), K = receptive field.
+struct GatherP {
+  const uint8_t* src;  // AG_NHWC: bf16 NHWC activations; AG_U8: first u8 CHW image
+  int64_t img_stride;  // AG_U8: bytes between images (obs_dim, or the slot stride)
+  int P, Wo;           // output positions per image, output width
+  int Hi, Wi, Cin;     // input geometry (AG_U8: channels C, H, W)
+  int ksz, s;          // kernel size, stride
+};
+enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2 };
+constexpr int GATHER_THREADS = 128;  // warps 10..13
+
 struct KParams {
   int M, N, K;
   int tiles_m, tiles_n, splits, kb_per_split, nkb;
   Epilogue epi;
   float* partial;  // split-K workspace [splits][M][N]
+  GatherP g;
 };
 
 template <int BN>
@@ -228,8 +241,115 @@ __device__ __forceinline__ void epilogue_dispatch(const KParams& p, int m, int n
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EV>
-__global__ void __launch_bounds__(THREADS, 1)
+// A-tile gatherers (warps 10..13, one output row per thread, all 8 chunks of
+// the 64-wide K block): NHWC bf16 rows via cp.async straight into the SW128
+// layout (completion tracked by the stage's full mbarrier), or u8 pixels
+// loaded, converted to bf16 (exact integers; 1/255 folded into the epilogue)
+// and stored to shared memory.
+// Window origin of output row m (image r, position y, x): computed once per
+// tile, the per-chunk offsets come from a per-CTA table (NHWC) or are affine
+// in (channel, kh) (u8).
+template <int AG>
+__device__ __forceinline__ const uint8_t* gather_row_origin(const KParams& p, int m, bool& valid) {
+  const GatherP& g = p.g;
+  valid = m < p.M;
+  const int mm = valid ? m : 0;
+  const int r = mm / g.P, pp = mm % g.P;
+  const int y = pp / g.Wo, x = pp % g.Wo;
+  if constexpr (AG == AG_NHWC)
+    return g.src + 2 * ((((int64_t)r * g.Hi + y * g.s) * g.Wi + x * g.s) * g.Cin);
+  else
+    return g.src + (int64_t)r * g.img_stride + (int64_t)(y * g.s) * g.Wi + x * g.s;
+}
+
+template <int AG>
+__device__ __forceinline__ void gather_stage(const KParams& p, uint8_t* sA, uint64_t* full,
+                                             const uint8_t* origin, bool valid, int kb, int gt,
+                                             const int* off_tab) {
+  const GatherP& g = p.g;
+  const uint32_t row_base = sm100::smem_u32(sA) + gt * 128;
+  if constexpr (AG == AG_NHWC) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint8_t* src = origin + off_tab[kb * 8 + c];
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                       row_base + ((c ^ (gt & 7)) << 4)),
+                   "l"(src), "r"(valid ? 16 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                     sm100::smem_u32(full))
+                 : "memory");
+  } else {
+    const uint8_t* img = origin + (int64_t)kb * g.Hi * g.Wi;  // channel kb
+    uint32_t lo[8], hi[8];
+#pragma unroll
+    for (int kh = 0; kh < 8; ++kh) {
+      const uint8_t* s = img + (int64_t)kh * g.Wi;
+      lo[kh] = valid ? __ldg(reinterpret_cast<const uint32_t*>(s)) : 0u;
+      hi[kh] = valid ? __ldg(reinterpret_cast<const uint32_t*>(s + 4)) : 0u;
+    }
+#pragma unroll
+    for (int kh = 0; kh < 8; ++kh) {
+      // u8 -> exact bf16 without I2F: PRMT places byte k into the float bits of
+      // 2^23 + v, one FADD removes 2^23 (exact), and since v has <= 8
+      // significant bits the upper 16 bits of the float ARE its bf16 encoding.
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t word = q < 2 ? lo[kh] : hi[kh];
+        const int k0 = (q & 1) * 2;
+        const float f0 = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0)) - 8388608.0f;
+        const float f1 =
+            __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0 + 1)) - 8388608.0f;
+        w[q] = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632);
+      }
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                       row_base + ((kh ^ (gt & 7)) << 4)),
+                   "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                   : "memory");
+    }
+    sm100::mbar_arrive(full);
+  }
+}
+
+// u8 gather split into its load and convert/store halves so the gatherers
+// can keep the next stage's 16 loads in flight while converting this one.
+__device__ __forceinline__ void u8_load(const KParams& p, const uint8_t* origin, bool valid,
+                                        int kb, uint32_t (&lo)[8], uint32_t (&hi)[8]) {
+  const uint8_t* img = origin + (int64_t)kb * p.g.Hi * p.g.Wi;
+#pragma unroll
+  for (int kh = 0; kh < 8; ++kh) {
+    const uint8_t* s = img + (int64_t)kh * p.g.Wi;
+    lo[kh] = valid ? __ldg(reinterpret_cast<const uint32_t*>(s)) : 0u;
+    hi[kh] = valid ? __ldg(reinterpret_cast<const uint32_t*>(s + 4)) : 0u;
+  }
+}
+__device__ __forceinline__ void u8_store(uint8_t* sA, uint64_t* full, int gt,
+                                         const uint32_t (&lo)[8], const uint32_t (&hi)[8]) {
+  const uint32_t row_base = sm100::smem_u32(sA) + gt * 128;
+#pragma unroll
+  for (int kh = 0; kh < 8; ++kh) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // exact u8 -> bf16 (see gather_stage)
+      const uint32_t word = q < 2 ? lo[kh] : hi[kh];
+      const int k0 = (q & 1) * 2;
+      const float f0 = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0)) - 8388608.0f;
+      const float f1 =
+          __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0 + 1)) - 8388608.0f;
+      w[q] = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632);
+    }
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row_base +
+                                                                 ((kh ^ (gt & 7)) << 4)),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
+  }
+  sm100::mbar_arrive(full);
+}
+
+template <int BN, bool A_MN, bool B_MN, int EV, int AG = AG_NONE>
+__global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, const KParams p) {
   using C = Cfg<BN>;
@@ -249,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     sm100::tma_prefetch(&mapA);
     sm100::tma_prefetch(&mapB);
     for (int s = 0; s < STAGES; ++s) {
-      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&full[s], AG ? 1 + GATHER_THREADS : 1);
       sm100::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -284,8 +404,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_TILE_BYTES;
-          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          if (!A_MN) {
+          sm100::mbar_arrive_expect_tx(&full[stage], AG ? C::B_TILE_BYTES : C::STAGE_BYTES);
+          if (AG) {
+            // A tile produced by the gather warps
+          } else if (!A_MN) {
             sm100::tma_load_2d(sA, &mapA, &full[stage], kb * BK, m0);
           } else {
             sm100::tma_load_2d(sA, &mapA, &full[stage], m0, kb * BK);
@@ -321,6 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
+          if (AG) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           sm100::tc_fence_after();
           const uint32_t a0 = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b0 = a0 + A_TILE_BYTES;
@@ -342,6 +465,79 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (AG && warp >= THREADS / 32) {
+    // A gatherers: same (unit, k block) schedule as the TMA producer
+    const int gt = threadIdx.x - THREADS;
+    // byte offset of chunk (kb, c) from the window origin (NHWC: (kh, kw, ci) order)
+    __shared__ int off_tab[16 * 8];
+    if (AG == AG_NHWC) {
+      for (int e = gt; e < p.nkb * 8; e += GATHER_THREADS) {
+        const int kk = e * 8;  // (kb*64 + c*8)
+        const int tap = kk / p.g.Cin, ci0 = kk % p.g.Cin;
+        const int kh = tap / p.g.ksz, kw = tap % p.g.ksz;
+        off_tab[e] = 2 * ((kh * p.g.Wi + kw) * p.g.Cin + ci0);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(GATHER_THREADS));  // gatherers only
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    if constexpr (AG == AG_U8) {
+      // software-pipelined: loads of work item j+1 in flight while item j is
+      // converted (u8 conv1 has no split-K: one tile = nkb consecutive items)
+      int u = blockIdx.x, kb = 0;
+      bool valid = false;
+      const uint8_t* origin = nullptr;
+      uint32_t lo[8], hi[8], nlo[8], nhi[8];
+      if (u < units) {
+        origin = gather_row_origin<AG>(p, (u % p.tiles_m) * BM + gt, valid);
+        u8_load(p, origin, valid, 0, lo, hi);
+      }
+      while (u < units) {
+        int nu = u, nkb = kb + 1;
+        if (nkb == p.nkb) {
+          nu = u + gridDim.x;
+          nkb = 0;
+        }
+        bool nvalid = valid;
+        const uint8_t* norigin = origin;
+        if (nu < units) {
+          if (nu != u) norigin = gather_row_origin<AG>(p, (nu % p.tiles_m) * BM + gt, nvalid);
+          u8_load(p, norigin, nvalid, nkb, nlo, nhi);
+        }
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        u8_store(smem + stage * C::STAGE_BYTES, &full[stage], gt, lo, hi);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          lo[q] = nlo[q];
+          hi[q] = nhi[q];
+        }
+        u = nu;
+        kb = nkb;
+        valid = nvalid;
+        origin = norigin;
+      }
+    }
+    for (int u = blockIdx.x; AG != AG_U8 && u < units; u += gridDim.x) {
+      const int tm = u % p.tiles_m;
+      const int z = u / (p.tiles_m * p.tiles_n);
+      const int kb0 = z * p.kb_per_split;
+      const int kb1 = min(kb0 + p.kb_per_split, p.nkb);
+      bool valid;
+      const uint8_t* origin = gather_row_origin<AG>(p, tm * BM + gt, valid);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        gather_stage<AG>(p, smem + stage * C::STAGE_BYTES, &full[stage], origin, valid, kb, gt,
+                         off_tab);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -473,10 +669,11 @@ int choose_ev(const KParams& p) {
   return EV_GENERIC;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EV>
+template <int BN, bool A_MN, bool B_MN, int EV, int AG = AG_NONE>
 int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& p) {
   using C = Cfg<BN>;
-  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EV>;
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EV, AG>;
+  constexpr int kThreads = AG ? THREADS + GATHER_THREADS : THREADS;
   static bool attr_set[64] = {};
   int dev = c->device & 63;
   if (!attr_set[dev]) {
@@ -496,15 +693,30 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     // per-shape tag for the profiling scripts (names must outlive the report)
     static std::set<std::string> names;
     char buf[96];
-    snprintf(buf, sizeof(buf), "gemm %dx%dx%d bn%d s%d %s%s", p.M, p.N, p.K, BN, p.splits,
-             A_MN ? "M" : "K", B_MN ? "M" : "K");
+    snprintf(buf, sizeof(buf), "gemm %dx%dx%d bn%d s%d %s%s%s", p.M, p.N, p.K, BN, p.splits,
+             A_MN ? "M" : "K", B_MN ? "M" : "K", AG == AG_U8 ? " conv-u8" : AG ? " conv" : "");
     c->next_name = names.insert(buf).first->c_str();
   }
   c->next_flops = 2.0 * p.M * p.N * p.K;
   c->next_bytes = 2.0 * ((double)p.M * p.K + (double)p.N * p.K) +
                   (double)p.M * p.N * ((p.epi.flags & EPI_BF16) ? 2 : 4) * (p.splits > 1 ? p.splits : 1);
-  APPO_LAUNCH(c, kern, grid, THREADS, C::SMEM_BYTES, ma, mb, p);
+  if (AG == AG_U8) {  // implicit conv1: the A operand is the u8 images, read once
+    const double imgs = (double)p.M / p.g.P;
+    c->next_bytes = imgs * p.g.Cin * p.g.Hi * p.g.Wi + 2.0 * p.N * p.K + 2.0 * p.M * p.N;
+  } else if (AG == AG_NHWC) {
+    const double imgs = (double)p.M / p.g.P;
+    c->next_bytes = 2.0 * imgs * p.g.Hi * p.g.Wi * p.g.Cin + 2.0 * p.N * p.K + 2.0 * p.M * p.N;
+  }
+  if (AG && !(c->timing && c->timing_filter == "gemm_shapes"))
+    c->next_name = "gemm_conv_implicit_tcgen05";
+  APPO_LAUNCH(c, kern, grid, kThreads, C::SMEM_BYTES, ma, mb, p);
   return APPO_OK;
+}
+
+template <int BN, int AG>
+int launch_conv(Ctx* c, const CUtensorMap& mb, const KParams& p) {
+  return choose_ev(p) == EV_ELU_BF16 ? launch_gemm<BN, false, false, EV_ELU_BF16, AG>(c, mb, mb, p)
+                                     : launch_gemm<BN, false, false, EV_GENERIC, AG>(c, mb, mb, p);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -593,6 +805,44 @@ int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
     APPO_LAUNCH(c, splitk_reduce_kernel, grid, 256, 0, M, N, p.splits, p.partial, epi);
   }
   return APPO_OK;
+}
+
+int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
+                       int bn) {
+  const int K = in.u8 ? in.Cin * 64 : in.ksz * in.ksz * in.Cin;
+  const int M = in.n_img * in.Ho * in.Wo;
+  if (M <= 0) return APPO_OK;
+  APPO_REQUIRE(!W.mn_major && K % 64 == 0 && (in.u8 || in.Cin % 8 == 0), APPO_ERR_CONTRACT,
+               "conv_implicit: K-major weights, K % 64 == 0 and Cin % 8 == 0 required");
+  APPO_REQUIRE(!in.u8 || (in.ksz == 8 && in.Wi % 4 == 0 &&
+                          (reinterpret_cast<uintptr_t>(in.src) & 3) == 0 && in.img_stride % 4 == 0),
+               APPO_ERR_CONTRACT, "conv_implicit u8: k8, W % 4 == 0, 4-byte aligned images");
+  CUtensorMap mb;
+  int st = make_map(&mb, W.ptr, K, N, W.ld, bn);
+  if (st) return st;
+  KParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.tiles_m = (M + BM - 1) / BM;
+  p.tiles_n = (N + bn - 1) / bn;
+  p.nkb = K / BK;
+  p.splits = 1;
+  p.kb_per_split = p.nkb;
+  p.epi = epi;
+  p.partial = nullptr;
+  p.g = GatherP{in.src, in.img_stride, in.Ho * in.Wo, in.Wo, in.Hi, in.Wi, in.Cin, in.ksz, in.s};
+  if (in.u8) {
+    switch (bn) {
+      case 32: return launch_conv<32, AG_U8>(c, mb, p);
+      default: return APPO_ERR_CONTRACT;
+    }
+  }
+  switch (bn) {
+    case 64: return launch_conv<64, AG_NHWC>(c, mb, p);
+    case 128: return launch_conv<128, AG_NHWC>(c, mb, p);
+    default: set_error("conv_implicit: unsupported BN"); return APPO_ERR_CONTRACT;
+  }
 }
 
 }  // namespace appo_b200

@@ -40,6 +40,19 @@ struct Operand {
 int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
               const Epilogue& epi, int bn, int splits = 1);
 
+// Implicit-GEMM convolution forward: out[img, y, x][n] = epi(sum_k A[...] W[n][k])
+// with the A tile gathered on the fly (no im2col in HBM).
+//   u8   : CHW u8 images (conv1; K = Cin*64 in (c, kh, kw) order, k8 s4)
+//   NHWC : bf16 activations [img][Hi][Wi][Cin] (K = ksz*ksz*Cin in (kh, kw, c) order)
+struct ConvIn {
+  const uint8_t* src = nullptr;  // first image (u8) / activation base (NHWC bf16 bytes)
+  int64_t img_stride = 0;        // u8: bytes between images
+  int n_img = 0, Hi = 0, Wi = 0, Cin = 0, ksz = 0, s = 0, Ho = 0, Wo = 0;
+  bool u8 = false;
+};
+int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
+                       int bn);
+
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);
 

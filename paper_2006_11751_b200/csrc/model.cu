@@ -144,11 +144,13 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
   const int B = learner ? n_traj * d.T : R;
   const int G = learner ? n_traj : R;  // rows of gh per GEMM
   Arena a;
-  a.take(&s.col1, (size_t)R * d.P1 * d.K1);
+  // im2col matrices only for the learner (inference gathers them on the fly);
+  // col1 stays the arena base (it is what gets freed)
+  a.take(&s.col1, learner ? (size_t)R * d.P1 * d.K1 : 64);
   a.take(&s.a1, (size_t)R * d.P1 * 32);
-  a.take(&s.col2, (size_t)R * d.P2 * 512);
+  a.take(&s.col2, learner ? (size_t)R * d.P2 * 512 : 64);
   a.take(&s.a2, (size_t)R * d.P2 * 64);
-  a.take(&s.col3, (size_t)R * d.P3 * 576);
+  a.take(&s.col3, learner ? (size_t)R * d.P3 * 576 : 64);
   a.take(&s.a3, (size_t)R * d.F);
   a.take(&s.x, (size_t)R * kHidden);
   a.take(&s.gi, (size_t)R * kGates);
@@ -241,10 +243,13 @@ int splits_for(Ctx* c, int M, int N, int bn, int K) {
   } while (0)
 
 // Encoder forward over R images: col1..a3 -> x (bf16 [R][512]) and gi.
+// Encoder forward over R images.  implicit: the three convolutions gather
+// their A operand on the fly (inference: no im2col traffic); otherwise the
+// im2col matrices are materialised because the learner's weight gradients
+// consume them.
 int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, const uint16_t* wb,
-                    const float* pf) {
+                    const float* pf, bool implicit) {
   const Dims& d = M->d;
-  TRY(k_im2col_u8(c, src, R, d, s.col1));
   Epilogue e;
   // conv1: [R*P1, 32] = col1 [R*P1, K1] . W1[32, K1]^T, x/255 folded into scale
   e.flags = EPI_BIAS | EPI_ELU | EPI_BF16;
@@ -252,21 +257,48 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   e.bias = pf + d.off_c1b;
   e.out = s.a1;
   e.ldo = 32;
-  TRY(gemm_bf16(c, R * d.P1, 32, d.K1, Operand{s.col1, d.K1, false},
-                Operand{wb + d.off_c1w, d.K1, false}, e, 32));
-  TRY(k_im2col_nhwc(c, s.a1, R, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.col2));
+  if (implicit) {
+    ConvIn in;
+    in.src = src.base;
+    in.img_stride = src.img_stride;
+    in.n_img = R;
+    in.Hi = d.H; in.Wi = d.W; in.Cin = d.C; in.ksz = 8; in.s = 4; in.Ho = d.H1; in.Wo = d.W1;
+    in.u8 = true;
+    TRY(conv_implicit_bf16(c, in, 32, Operand{wb + d.off_c1w, d.K1, false}, e, 32));
+  } else {
+    TRY(k_im2col_u8(c, src, R, d, s.col1));
+    TRY(gemm_bf16(c, R * d.P1, 32, d.K1, Operand{s.col1, d.K1, false},
+                  Operand{wb + d.off_c1w, d.K1, false}, e, 32));
+  }
   e.scale = 1.0f;
   e.bias = pf + d.off_c2b;
   e.out = s.a2;
   e.ldo = 64;
-  TRY(gemm_bf16(c, R * d.P2, 64, 512, Operand{s.col2, 512, false},
-                Operand{wb + d.off_c2w, 512, false}, e, 64));
-  TRY(k_im2col_nhwc(c, s.a2, R, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.col3));
+  if (implicit) {
+    ConvIn in;
+    in.src = reinterpret_cast<const uint8_t*>(s.a1);
+    in.n_img = R;
+    in.Hi = d.H1; in.Wi = d.W1; in.Cin = 32; in.ksz = 4; in.s = 2; in.Ho = d.H2; in.Wo = d.W2;
+    TRY(conv_implicit_bf16(c, in, 64, Operand{wb + d.off_c2w, 512, false}, e, 64));
+  } else {
+    TRY(k_im2col_nhwc(c, s.a1, R, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.col2));
+    TRY(gemm_bf16(c, R * d.P2, 64, 512, Operand{s.col2, 512, false},
+                  Operand{wb + d.off_c2w, 512, false}, e, 64));
+  }
   e.bias = pf + d.off_c3b;
   e.out = s.a3;
   e.ldo = 128;
-  TRY(gemm_bf16(c, R * d.P3, 128, 576, Operand{s.col3, 576, false},
-                Operand{wb + d.off_c3w, 576, false}, e, 128));
+  if (implicit) {
+    ConvIn in;
+    in.src = reinterpret_cast<const uint8_t*>(s.a2);
+    in.n_img = R;
+    in.Hi = d.H2; in.Wi = d.W2; in.Cin = 64; in.ksz = 3; in.s = 2; in.Ho = d.H3; in.Wo = d.W3;
+    TRY(conv_implicit_bf16(c, in, 128, Operand{wb + d.off_c3w, 576, false}, e, 128));
+  } else {
+    TRY(k_im2col_nhwc(c, s.a2, R, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.col3));
+    TRY(gemm_bf16(c, R * d.P3, 128, 576, Operand{s.col3, 576, false},
+                  Operand{wb + d.off_c3w, 576, false}, e, 128));
+  }
   e.bias = pf + d.off_fcb;
   e.out = s.x;
   e.ldo = kHidden;
@@ -312,7 +344,7 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
   ObsSrc src;
   src.base = obs_base;
   src.img_stride = obs_stride;
-  TRY(encoder_forward(c, M, s, src, B, wb, pf));
+  TRY(encoder_forward(c, M, s, src, B, wb, pf, /*implicit=*/true));
   TRY(k_f32_to_bf16(c, B, h_in, kHidden, s.hbf, kHidden, kHidden));
   Epilogue g;
   g.flags = EPI_BIAS;
@@ -539,7 +571,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   src.T = T;
   src.n_traj = n_traj;
   src.obs_dim = d.obs_dim;
-  TRY(encoder_forward(ctx, M, s, src, R, wb, th));
+  TRY(encoder_forward(ctx, M, s, src, R, wb, th, /*implicit=*/false));
 
   // ---- GRU unrolled over T steps (+ bootstrap step) ----
   const bool seq = gru_seq_supported(n_traj);

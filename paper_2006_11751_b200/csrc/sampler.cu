@@ -54,21 +54,19 @@ __device__ __forceinline__ uint64_t dev_derive_seed(uint64_t seed, uint64_t stre
 }
 
 // obs for env e at its current (episode, step): 8 pixels per hash.
+// grid (ceil(words / 256), n_envs): env from blockIdx.y, no 64-bit division
 __global__ void gen_obs_kernel(int n_envs, int64_t obs_dim, uint64_t seed,
                                const uint32_t* __restrict__ step,
                                const uint32_t* __restrict__ episode, uint8_t* region,
                                uint64_t slot_bytes, int64_t slot_base, uint64_t off) {
-  const int64_t words = obs_dim >> 3;
-  const int64_t total = (int64_t)n_envs * words;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int e = (int)(g / words);
-    const int64_t w = g % words;
-    const uint64_t es = dev_derive_seed(seed, ((uint64_t)e << 24) ^ episode[e]);
-    const uint64_t h = splitmix64(es ^ ((uint64_t)step[e] << 20) ^ (uint64_t)w);
-    *reinterpret_cast<uint64_t*>(region + (uint64_t)(slot_base + e) * slot_bytes + off + w * 8) =
-        h;
-  }
+  const int words = (int)(obs_dim >> 3);
+  const int e = blockIdx.y;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  const uint64_t es = dev_derive_seed(seed, ((uint64_t)e << 24) ^ episode[e]);
+  const uint64_t h = splitmix64(es ^ ((uint64_t)step[e] << 20) ^ (uint64_t)w);
+  *reinterpret_cast<uint64_t*>(region + (uint64_t)(slot_base + e) * slot_bytes + off +
+                               (uint64_t)w * 8) = h;
 }
 
 // Step record + env transition; one block (128 threads) per env.
@@ -149,8 +147,8 @@ APPO_API int appo_sampler_create(appo_ctx* ctx, int n_envs, int episode_len, uin
                                  appo_sampler** out) {
   APPO_REQUIRE(ctx && ctx->model && out, APPO_ERR_CONTRACT,
                "sampler_create: needs a model context");
-  APPO_REQUIRE(n_envs >= 1 && episode_len >= 1, APPO_ERR_CONTRACT,
-               "sampler_create: n_envs and episode_len must be >= 1");
+  APPO_REQUIRE(n_envs >= 1 && n_envs <= 65535 && episode_len >= 1, APPO_ERR_CONTRACT,
+               "sampler_create: 1 <= n_envs <= 65535 and episode_len >= 1 required");
   APPO_REQUIRE(ctx->model->d.obs_dim % 8 == 0, APPO_ERR_CONTRACT, "obs_dim must be a multiple of 8");
   APPO_CUDA_TRY(cudaSetDevice(ctx->device));
   appo_sampler* s = new appo_sampler();
@@ -212,9 +210,7 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
                                     slot_bytes, h_obs, d.obs_dim, d.obs_dim, s->n_envs,
                                     cudaMemcpyHostToDevice, c->stream));
   } else {
-    const int64_t n = (int64_t)s->n_envs * (d.obs_dim >> 3);
-    int grid = (int)((n + 255) / 256);
-    if (grid > c->num_sms * 32) grid = c->num_sms * 32;
+    const dim3 grid((unsigned)(((d.obs_dim >> 3) + 255) / 256), (unsigned)s->n_envs);
     c->next_bytes = (double)s->n_envs * d.obs_dim;
     APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
                 s->episode, region, slot_bytes, (int64_t)slot_base, obs_off);
@@ -232,9 +228,7 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
               slot_bytes, (int64_t)slot_base, off);
   if (t == d.T - 1) {
     // bootstrap obs = next observation of every env (post-transition state)
-    const int64_t n = (int64_t)s->n_envs * (d.obs_dim >> 3);
-    int grid = (int)((n + 255) / 256);
-    if (grid > c->num_sms * 32) grid = c->num_sms * 32;
+    const dim3 grid((unsigned)(((d.obs_dim >> 3) + 255) / 256), (unsigned)s->n_envs);
     APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
                 s->episode, region, slot_bytes, (int64_t)slot_base, d.slot[7]);
   }
