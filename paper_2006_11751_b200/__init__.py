@@ -51,8 +51,8 @@ _ERRS = {1: ContractError, 2: ConfigError, 3: NumericError, 4: ResourceError}
 
 
 def _load():
-    if not os.path.exists(LIB_PATH):
-        from . import _build
+    from . import _build
+    if _build.needs_build():  # missing or older than its sources: rebuild in-tree
         _build.build()
     return C.CDLL(LIB_PATH)
 

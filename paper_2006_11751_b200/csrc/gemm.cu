@@ -581,16 +581,39 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
   }
 }
 
-// Split-K reduction + epilogue (fp32 outputs only).
-__global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ partial,
-                                     Epilogue e) {
+// Split-K reduction + epilogue (fp32 outputs only).  Block = 32 consecutive
+// outputs x 8 split groups: group g sums splits z = g, g+8, ... in order, then
+// the 8 group sums are added in order -- deterministic, and enough threads in
+// flight for the partial stream even when M*N is small and splits is large.
+__global__ void __launch_bounds__(256)
+    splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
   const int64_t total = (int64_t)M * N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.0f;
-    for (int z = 0; z < splits; ++z) s += partial[(size_t)z * total + i];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  float s = 0.0f;
+  if (i < total) {
+    int z = g;
+    for (; z + 24 < splits; z += 32) {
+      const float a0 = __ldg(partial + (size_t)z * total + i);
+      const float a1 = __ldg(partial + (size_t)(z + 8) * total + i);
+      const float a2 = __ldg(partial + (size_t)(z + 16) * total + i);
+      const float a3 = __ldg(partial + (size_t)(z + 24) * total + i);
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; z < splits; z += 8) s += __ldg(partial + (size_t)z * total + i);
+  }
+  __shared__ float sh[8][33];
+  sh[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && i < total) {
+    float t = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][lane];
     const int m = (int)(i / N), n = (int)(i % N);
-    float x = s * e.scale;
+    float x = t * e.scale;
     if (e.flags & EPI_BIAS) x += e.bias[n];
     const size_t o = (e.flags & EPI_TRANS) ? (size_t)n * e.ldo + m : (size_t)m * e.ldo + n;
     float* dst = reinterpret_cast<float*>(e.out) + o;
@@ -800,8 +823,8 @@ int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
   if (st) return st;
   if (p.splits > 1) {
     const int64_t total = (int64_t)M * N;
-    int grid = (int)((total + 255) / 256);
-    if (grid > c->num_sms * 8) grid = c->num_sms * 8;
+    const int grid = (int)((total + 31) / 32);
+    c->next_bytes = (double)p.splits * total * 4 + (double)total * 4;
     APPO_LAUNCH(c, splitk_reduce_kernel, grid, 256, 0, M, N, p.splits, p.partial, epi);
   }
   return APPO_OK;

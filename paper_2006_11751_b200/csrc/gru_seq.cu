@@ -271,6 +271,8 @@ struct BwdArgs {
   uint16_t* dghx;       // [2][n_traj][1536] bf16 exchange
   uint16_t* dgi;        // [B][1536]
   uint16_t* dgh;        // [B][1536]
+  float* gbih;          // [1536] bias gradients (sums over all B rows)
+  float* gbhh;          // [1536]
   unsigned* bar;
 };
 
@@ -319,6 +321,9 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   const int n_cells = a.n_traj * UPC_B;
   float pf[CPT][7];  // dcore, r, z, n, ghn, h_in, keep
   float ddr[CPT];    // dh*z of the later step
+  float bsum[CPT][4];  // per-cell sums over t of dgr, dgz, dan, dgn (bias gradients)
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) bsum[c][0] = bsum[c][1] = bsum[c][2] = bsum[c][3] = 0.0f;
   auto prefetch = [&](int t) {
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -353,9 +358,16 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
       const float dnn = dh * (1.0f - z);
       const float dz = dh * (hp - n);
       const float dan = dnn * (1.0f - n * n);
-      const uint16_t dgr = f2bf_(dan * ghn * r * (1.0f - r));
-      const uint16_t dgz = f2bf_(dz * z * (1.0f - z));
-      const uint16_t dgn = f2bf_(dan * r);
+      const float fgr = dan * ghn * r * (1.0f - r);
+      const float fgz = dz * z * (1.0f - z);
+      const float fgn = dan * r;
+      bsum[c][0] += fgr;
+      bsum[c][1] += fgz;
+      bsum[c][2] += dan;
+      bsum[c][3] += fgn;
+      const uint16_t dgr = f2bf_(fgr);
+      const uint16_t dgz = f2bf_(fgz);
+      const uint16_t dgn = f2bf_(fgn);
       uint16_t* gi_row = a.dgi + s * kGates;
       uint16_t* gh_row = a.dgh + s * kGates;
       gi_row[j] = dgr;
@@ -408,6 +420,35 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
     sm100::tc_fence_before();
     __syncthreads();
   }
+  // bias gradients of the CTA's gate columns: fixed-order sum over trajectories
+  // (the A staging tile is free now: every MMA has completed)
+  float* red = reinterpret_cast<float*>(tA);  // [64][8][4]
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int e = tid + c * THR;
+    if (e < n_cells)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red[e * 4 + k] = bsum[c][k];
+  }
+  __syncthreads();
+  if (tid < UPC_B * 4) {
+    const int u = tid >> 2, k = tid & 3;
+    float t = 0.0f;
+    for (int i = 0; i < a.n_traj; ++i) t += red[(i * UPC_B + u) * 4 + k];
+    const int j = j0 + u;
+    if (k == 0) {
+      a.gbih[j] = t;
+      a.gbhh[j] = t;
+    } else if (k == 1) {
+      a.gbih[kHidden + j] = t;
+      a.gbhh[kHidden + j] = t;
+    } else if (k == 2) {
+      a.gbih[2 * kHidden + j] = t;
+    } else {
+      a.gbhh[2 * kHidden + j] = t;
+    }
+  }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -448,7 +489,7 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
 
 int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* done,
                   const float* gates, const float* hin, const uint16_t* whh, uint16_t* dghx,
-                  uint16_t* dgi, uint16_t* dgh, unsigned* bar) {
+                  uint16_t* dgi, uint16_t* dgh, float* gbih, float* gbhh, unsigned* bar) {
   static bool attr = false;
   if (!attr) {
     APPO_CUDA_TRY(cudaFuncSetAttribute(gru_seq_bwd_kernel,
@@ -456,7 +497,7 @@ int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* 
     attr = true;
   }
   APPO_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));
-  BwdArgs a{n_traj, T, dcore, done, gates, hin, whh, dghx, dgi, dgh, bar};
+  BwdArgs a{n_traj, T, dcore, done, gates, hin, whh, dghx, dgi, dgh, gbih, gbhh, bar};
   void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_bwd_kernel");
   APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_bwd_kernel, dim3(NCTA_B), dim3(THR),

@@ -190,6 +190,8 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
     a.take(&s.dcol2, (size_t)B * d.P2 * 512);
     a.take(&s.headw, (size_t)16 * kHidden);
     a.take(&s.colsum_part, (size_t)256 * kGates + 64);
+    a.take(&s.bias_acc, (size_t)4 * kBiasAccCols);
+    a.take(&s.bias_cnt, (size_t)4);
     a.take(&s.slot_ids, (size_t)n_traj);
     a.take(&s.stats, (size_t)16);
   }
@@ -211,6 +213,14 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
     reloc(s.dnext, base); reloc(s.dgi, base); reloc(s.dgh, base); reloc(s.dzfc, base);
     reloc(s.dz3, base); reloc(s.dz2, base); reloc(s.dz1, base); reloc(s.dcol3, base);
     reloc(s.dcol2, base); reloc(s.headw, base); reloc(s.colsum_part, base);
+    reloc(s.bias_acc, base); reloc(s.bias_cnt, base);
+    if (cudaMemset(s.bias_acc, 0, sizeof(unsigned long long) * 4 * kBiasAccCols) != cudaSuccess ||
+        cudaMemset(s.bias_cnt, 0, sizeof(unsigned) * 4) != cudaSuccess) {
+      cudaFree(base);
+      s = Scratch{};
+      set_error("scratch memset failed");
+      return APPO_ERR_RESOURCE;
+    }
     reloc(s.slot_ids, base); reloc(s.stats, base);
     if (cudaMallocHost(&s.h_stats, sizeof(double) * 16 + sizeof(int32_t) * n_traj) !=
         cudaSuccess) {
@@ -228,12 +238,39 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
   return APPO_OK;
 }
 
+// Split-K factor for a GEMM with a long reduction (weight gradients): the
+// main loop shrinks with more splits, the fp32 partial traffic (write + read
+// by the reduce) and one extra launch grow.  Per-k-block SM time: the larger
+// of the MMA (2*BN clk for 128xBNx64) and the L2->SMEM operand stream
+// (~100 B/clk per SM); partials at ~6 TB/s.
 int splits_for(Ctx* c, int M, int N, int bn, int K) {
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   const int nkb = (K + 63) / 64;
-  int sp = (2 * c->num_sms + tiles - 1) / tiles;
-  if (sp > nkb / 2) sp = nkb / 2;  // keep >= 2 k-blocks per split
-  return sp < 1 ? 1 : sp;
+  const int smem = 4 * (16384 + bn * 128) + 1280;
+  int per_sm = (227 * 1024) / smem;
+  const int tmem_cols = 2 * bn <= 32 ? 32 : 2 * bn <= 64 ? 64 : 2 * bn <= 128 ? 128 : 2 * bn <= 256 ? 256 : 512;
+  if (per_sm > 512 / tmem_cols) per_sm = 512 / tmem_cols;
+  if (per_sm < 1) per_sm = 1;
+  const double clk_kb = std::fmax(2.0 * bn, (16384.0 + bn * 128.0) / 100.0);
+  const double us_kb = clk_kb / 1900.0;
+  const int slots = c->num_sms * per_sm;
+  double best_t = 1e30;
+  int best = 1;
+  for (int sp = 1; sp <= nkb / 2 || sp == 1; ++sp) {
+    const int kbps = (nkb + sp - 1) / sp;
+    if (sp > 1 && (nkb + kbps - 1) / kbps != sp) continue;  // same as a smaller split
+    const int units = tiles * sp;
+    const int waves = (units + slots - 1) / slots;
+    const int conc = units < slots ? (units + c->num_sms - 1) / c->num_sms : per_sm;
+    double t = waves * (conc < 1 ? 1 : conc) * kbps * us_kb;
+    if (sp > 1) t += 2.0 * sp * (double)M * N * 4.0 / 6.0e6 + 2.0;
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = sp;
+    }
+    if (sp > 1024) break;
+  }
+  return best;
 }
 
 #define TRY(x)                    \
@@ -634,10 +671,21 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
                             G + d.off_bv));
   }
 
+  // bias gradients of fc / conv layers, fused into the kernels producing /
+  // reading their dz (deterministic fixed-point sums, model_kernels.cu)
+  auto bias_out = [&](int k, float* out, int N) {
+    BiasOut b;
+    b.out = out;
+    b.acc = s.bias_acc + (size_t)k * kBiasAccCols;
+    b.counter = s.bias_cnt + k;
+    b.N = N;
+    return b;
+  };
+
   // ---- BPTT through the GRU ----
   if (seq)
     TRY(k_gru_seq_bwd(ctx, n_traj, T, s.dcore, s.done, s.gates, s.hin, wb + d.off_whh, s.dghx,
-                      s.dgi, s.dgh, ctx->d_counter + 5));
+                      s.dgi, s.dgh, G + d.off_bih, G + d.off_bhh, ctx->d_counter + 5));
   else
     APPO_CUDA_TRY(cudaMemsetAsync(s.dnext, 0, sizeof(float) * n_traj * kHidden, st));
   if (!seq) {
@@ -663,8 +711,10 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     e.out = G + d.off_whh;
     TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgh, kGates, true},
                   Operand{s.hbf, kHidden, true}, e, 256, splits_for(ctx, kGates, kHidden, 256, B)));
-    TRY(k_colsum(ctx, B, kGates, s.dgi, kGates, true, s.colsum_part, G + d.off_bih, false));
-    TRY(k_colsum(ctx, B, kGates, s.dgh, kGates, true, s.colsum_part, G + d.off_bhh, false));
+    if (!seq) {
+      TRY(k_colsum(ctx, B, kGates, s.dgi, kGates, true, s.colsum_part, G + d.off_bih, false));
+      TRY(k_colsum(ctx, B, kGates, s.dgh, kGates, true, s.colsum_part, G + d.off_bhh, false));
+    }
     // dx = dgi . W_ih, times ELU'(fc) -> dz_fc
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
@@ -682,7 +732,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     e.ldo = d.F;
     TRY(gemm_bf16(ctx, kHidden, d.F, B, Operand{s.dzfc, kHidden, true},
                   Operand{s.a3, d.F, true}, e, 256, splits_for(ctx, kHidden, d.F, 256, B)));
-    TRY(k_colsum(ctx, B, kHidden, s.dzfc, kHidden, true, s.colsum_part, G + d.off_fcb, false));
+    TRY(k_colsum_v(ctx, B, s.dzfc, bias_out(0, G + d.off_fcb, kHidden)));
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
     x.aux = s.a3;
@@ -700,14 +750,15 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     e.ldo = 576;
     TRY(gemm_bf16(ctx, 128, 576, M3, Operand{s.dz3, 128, true}, Operand{s.col3, 576, true}, e,
                   192, splits_for(ctx, 128, 576, 192, M3)));
-    TRY(k_colsum(ctx, M3, 128, s.dz3, 128, true, s.colsum_part, G + d.off_c3b, false));
+    TRY(k_colsum_v(ctx, M3, s.dz3, bias_out(1, G + d.off_c3b, 128)));
     Epilogue x;
     x.flags = EPI_BF16;
     x.out = s.dcol3;
     x.ldo = 576;
     TRY(gemm_bf16(ctx, M3, 576, 128, Operand{s.dz3, 128, false},
                   Operand{wb + d.off_c3w, 576, true}, x, 192));
-    TRY(k_col2im_delu_bf16(ctx, s.dcol3, s.a2, B, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.dz2));
+    TRY(k_col2im_delu_bf16(ctx, s.dcol3, s.a2, B, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.dz2,
+                           bias_out(2, G + d.off_c2b, 64)));
   }
   // ---- conv2 backward ----
   {
@@ -717,14 +768,14 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     e.ldo = 512;
     TRY(gemm_bf16(ctx, 64, 512, M2, Operand{s.dz2, 64, true}, Operand{s.col2, 512, true}, e, 256,
                   splits_for(ctx, 64, 512, 256, M2)));
-    TRY(k_colsum(ctx, M2, 64, s.dz2, 64, true, s.colsum_part, G + d.off_c2b, false));
     Epilogue x;
     x.flags = EPI_BF16;
     x.out = s.dcol2;
     x.ldo = 512;
     TRY(gemm_bf16(ctx, M2, 512, 64, Operand{s.dz2, 64, false},
                   Operand{wb + d.off_c2w, 512, true}, x, 256));
-    TRY(k_col2im_delu_bf16(ctx, s.dcol2, s.a1, B, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.dz1));
+    TRY(k_col2im_delu_bf16(ctx, s.dcol2, s.a1, B, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.dz1,
+                           bias_out(3, G + d.off_c1b, 32)));
   }
   // ---- conv1 weight gradient (input is data) ----
   {
@@ -736,7 +787,6 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     TRY(gemm_bf16(ctx, 32, d.K1, M1, Operand{s.dz1, 32, true}, Operand{s.col1, d.K1, true}, e,
                   d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64,
                   splits_for(ctx, 32, d.K1, d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64, M1)));
-    TRY(k_colsum(ctx, M1, 32, s.dz1, 32, true, s.colsum_part, G + d.off_c1b, false));
   }
 
   // ---- data-parallel: average the gradient over ranks before clip + Adam ----

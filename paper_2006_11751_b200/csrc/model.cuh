@@ -11,6 +11,8 @@ namespace appo_b200 {
 
 constexpr int kHidden = 512;
 constexpr int kGates = 3 * kHidden;
+constexpr int kBiasCopies = 16;                  // accumulator copies per bias vector
+constexpr int kBiasAccCols = 512 * kBiasCopies;  // per bias vector (N <= 512)
 
 struct Dims {
   int C, H, W, A, T;
@@ -54,6 +56,8 @@ struct Scratch {
   uint16_t *dcol3 = nullptr, *dcol2 = nullptr;  // bf16 im2col-space input gradients
   float* headw = nullptr;       // [16][512]
   float* colsum_part = nullptr; // partials for bias grads
+  unsigned long long* bias_acc = nullptr;  // [4][kBiasAccCols] fixed-point bias-gradient sums
+  unsigned* bias_cnt = nullptr;            // [4] last-block counters
   int32_t* slot_ids = nullptr;
   double* stats = nullptr;      // device stats block
   double* h_stats = nullptr;    // pinned

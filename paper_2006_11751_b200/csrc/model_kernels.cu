@@ -116,14 +116,62 @@ __global__ void col2im_delu_kernel(const float* __restrict__ dcol,
   }
 }
 
+// Block-level column sums of per-thread 8-wide partials over contiguous bf16
+// [M][N] data walked in 16-byte chunks: thread t always owns column group
+// t % (N/8) because the grid stride is a multiple of N/8 (256 % (N/8) == 0).
+// The block's sums are added as 2^-32 fixed point into int64 accumulators
+// (integer adds commute: the result is bit-identical whatever the block
+// order); the last block converts them to fp32 into out[N] and re-zeroes the
+// accumulators and the counter for the next call.
+__device__ __forceinline__ void block_colsum_reduce(const float (&acc)[8], int cg, const BiasOut& o) {
+  __shared__ float sh[256][9];
+  __shared__ bool last;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sh[threadIdx.x][k] = acc[k];
+  __syncthreads();
+  for (int n = threadIdx.x; n < o.N; n += blockDim.x) {
+    const int g = n >> 3, k = n & 7;
+    float t = 0.0f;
+    for (int th = g; th < (int)blockDim.x; th += cg) t += sh[th][k];
+    // kBiasCopies interleaved accumulator copies spread the same-address atomics
+    atomicAdd(o.acc + (size_t)(blockIdx.x % kBiasCopies) * o.N + n,
+              (unsigned long long)llrint((double)t * 4294967296.0));
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(o.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    for (int n = threadIdx.x; n < o.N; n += blockDim.x) {
+      unsigned long long v = 0;
+      for (int k = 0; k < kBiasCopies; ++k) v += atomicExch(o.acc + (size_t)k * o.N + n, 0ull);
+      o.out[n] = (float)((double)(long long)v * (1.0 / 4294967296.0));
+    }
+    if (threadIdx.x == 0) *o.counter = 0;
+  }
+}
+
+__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    acc[2 * q] += bf2f((uint16_t)(w[q] & 0xFFFF));
+    acc[2 * q + 1] += bf2f((uint16_t)(w[q] >> 16));
+  }
+}
+
 // Same as above with bf16 dcol and 8 channels per thread (16-byte loads/stores).
-__global__ void col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol,
-                                        const uint16_t* __restrict__ aprev, int64_t R, int Hi,
-                                        int Wi, int Cin, int k, int s, int Ho, int Wo,
-                                        uint16_t* __restrict__ dz) {
+// With part != null the bias gradient of the produced dz (column sums over all
+// rows and positions) is reduced on the fly into per-block partials.
+__global__ void __launch_bounds__(256)
+    col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol, const uint16_t* __restrict__ aprev,
+                            int64_t R, int Hi, int Wi, int Cin, int k, int s, int Ho, int Wo,
+                            uint16_t* __restrict__ dz, BiasOut bias) {
   const int cg = Cin >> 3;
   const int64_t total = R * Hi * Wi * cg;
   const int K = k * k * Cin;
+  float bsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int c8 = (int)(g % cg);
@@ -139,14 +187,9 @@ __global__ void col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol,
       for (int kw = xi % s; kw < k; kw += s) {
         const int xo = (xi - kw) / s;
         if (xo < 0 || xo >= Wo) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(
-            dcol + (r * Ho * Wo + (int64_t)yo * Wo + xo) * K + (kh * k + kw) * Cin + c8 * 8);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          acc[2 * q] += bf2f((uint16_t)(w[q] & 0xFFFF));
-          acc[2 * q + 1] += bf2f((uint16_t)(w[q] >> 16));
-        }
+        acc_bf16x8(acc, *reinterpret_cast<const uint4*>(
+                            dcol + (r * Ho * Wo + (int64_t)yo * Wo + xo) * K + (kh * k + kw) * Cin +
+                            c8 * 8));
       }
     }
     const int64_t o = g * 8;
@@ -156,12 +199,37 @@ __global__ void col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol,
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float a0 = bf2f((uint16_t)(aw[q] & 0xFFFF)), a1 = bf2f((uint16_t)(aw[q] >> 16));
-      const float d0 = acc[2 * q] * (a0 > 0.0f ? 1.0f : a0 + 1.0f);
-      const float d1 = acc[2 * q + 1] * (a1 > 0.0f ? 1.0f : a1 + 1.0f);
-      out[q] = (uint32_t)f2bf(d0) | ((uint32_t)f2bf(d1) << 16);
+      const uint16_t d0 = f2bf(acc[2 * q] * (a0 > 0.0f ? 1.0f : a0 + 1.0f));
+      const uint16_t d1 = f2bf(acc[2 * q + 1] * (a1 > 0.0f ? 1.0f : a1 + 1.0f));
+      bsum[2 * q] += bf2f(d0);
+      bsum[2 * q + 1] += bf2f(d1);
+      out[q] = (uint32_t)d0 | ((uint32_t)d1 << 16);
     }
     *reinterpret_cast<uint4*>(dz + o) = make_uint4(out[0], out[1], out[2], out[3]);
   }
+  if (bias.out) block_colsum_reduce(bsum, cg, bias);
+}
+
+// Column sums of a contiguous bf16 [M][N] matrix (N % 8 == 0, 256 % (N/8) ==
+// 0) into per-block partials part[blockIdx.x][N]; bias_finalize_kernel sums
+// the blocks.
+__global__ void __launch_bounds__(256)
+    colsum_v_kernel(int64_t M, const uint16_t* __restrict__ src, BiasOut bias) {
+  const int N = bias.N;
+  const int cg = N >> 3;
+  const int64_t total = M * cg;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; q + 3 * stride < total; q += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(src) + q + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc_bf16x8(acc, v[u]);
+  }
+  for (; q < total; q += stride) acc_bf16x8(acc, __ldg(reinterpret_cast<const uint4*>(src) + q));
+  block_colsum_reduce(acc, cg, bias);
 }
 
 __global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int64_t src_ld,
@@ -602,11 +670,26 @@ int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, i
   return APPO_OK;
 }
 int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
-                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz) {
+                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz,
+                       const BiasOut& bias) {
   const int64_t n = R * Hi * Wi * (Cin / 8);
+  APPO_REQUIRE(!bias.out || (Cin % 8 == 0 && 256 % (Cin / 8) == 0 && bias.N == Cin),
+               APPO_ERR_CONTRACT, "col2im: fused bias sums need 256 % (Cin/8) == 0");
   c->next_bytes = (double)R * Ho * Wo * k * k * Cin * 2 + (double)R * Hi * Wi * Cin * 4;
   APPO_LAUNCH(c, col2im_delu_bf16_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev,
-              R, Hi, Wi, Cin, k, s, Ho, Wo, dz);
+              R, Hi, Wi, Cin, k, s, Ho, Wo, dz, bias);
+  return APPO_OK;
+}
+int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias) {
+  const int N = bias.N;
+  APPO_REQUIRE(N % 8 == 0 && 256 % (N / 8) == 0 && bias.out, APPO_ERR_CONTRACT,
+               "colsum_v: need N % 8 == 0 and 256 % (N/8) == 0");
+  const int64_t chunks = M * (N / 8);
+  int grid = (int)((chunks + 256 * 8 - 1) / (256 * 8));  // ~8 chunks per thread
+  if (grid > c->num_sms * 8) grid = c->num_sms * 8;
+  if (grid < 1) grid = 1;
+  c->next_bytes = (double)M * N * 2;
+  APPO_LAUNCH(c, colsum_v_kernel, grid, 256, 0, M, src, bias);
   return APPO_OK;
 }
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,

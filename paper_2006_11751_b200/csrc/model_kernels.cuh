@@ -33,8 +33,20 @@ int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Ci
                   int Ho, int Wo, uint16_t* col);
 int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
                   int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
+// Bias-gradient output of a fused column sum: deterministic int64 fixed-point
+// accumulation (acc[N], zero between calls) + last-block conversion to out[N].
+struct BiasOut {
+  float* out = nullptr;
+  unsigned long long* acc = nullptr;
+  unsigned* counter = nullptr;
+  int N = 0;
+};
+// bias.out != null: also writes the bias gradient (column sums of dz)
 int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
-                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
+                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz,
+                       const BiasOut& bias = BiasOut());
+// Column sums of contiguous bf16 [M][bias.N] into bias.out
+int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias);
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
                   int64_t dst_ld, int cols);
 int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const float* h_in,
@@ -69,8 +81,9 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
                   const float* bhh, const uint8_t* done, float* hbuf, uint16_t* hbuf_bf,
                   float* core, uint16_t* core_bf, float* gates, float* hin, uint16_t* hbf,
                   unsigned* bar);
+// also writes the bias gradients gb_ih / gb_hh (sums of the gate gradients)
 int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* done,
                   const float* gates, const float* hin, const uint16_t* whh, uint16_t* dghx,
-                  uint16_t* dgi, uint16_t* dgh, unsigned* bar);
+                  uint16_t* dgi, uint16_t* dgh, float* gbih, float* gbhh, unsigned* bar);
 
 }  // namespace appo_b200
