@@ -45,8 +45,27 @@ struct GatherP {
   int Hi, Wi, Cin;     // input geometry (AG_U8: channels C, H, W)
   int ksz, s;          // kernel size, stride
 };
-enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2 };
+enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3 };
 constexpr int GATHER_THREADS = 128;  // warps 10..13
+
+// Input gradient of a stride-2 convolution (kernel k <= 4, no padding) by
+// sub-pixel decomposition.  Input position (2yy+py, 2xx+px) only receives
+// taps kh = py + 2a, kw = px + 2b (a, b in {0, 1}) from dz_next[yy-a][xx-b],
+// so for a COARSE position (yy, xx) all four parity classes read the same
+// 2x2 neighbourhood: one GEMM with rows = coarse positions, K = (a, b, co)
+// and N = (class, ci) computes the four output pixels of the 2x2 block:
+//   D[(r,yy,xx)][(cls,ci)] = sum_{a,b,co} dz_next[r][yy-a][xx-b][co] Wt[(cls,ci)][(a,b,co)]
+// The A tile is one 4-D TMA box {64 ch, Wb x, Hb y, Ib images} of dz_next at
+// (x, y) offset (-b, -a): out-of-range taps are zero-filled by the TMA unit.
+struct DgradP {
+  int Hcc, Wcc;      // coarse grid (ceil(Hi/2), ceil(Wi/2)); boxes cover its live part
+  int Hb, Wb, Ib;    // TMA box (Hb * Wb * Ib == 128 rows)
+  int Hi, Wi, Ci;    // produced dz [img][Hi][Wi][Ci]
+  int n_img, apt;    // images; 64-channel atoms per tap (Co / 64)
+  unsigned long long* bacc;  // fused bias gradient: fixed-point accumulators [16][Ci]
+  unsigned* bcnt;            // CTA completion counter
+  float* bout;               // bias gradient [Ci]
+};
 
 struct KParams {
   int M, N, K;
@@ -54,7 +73,22 @@ struct KParams {
   Epilogue epi;
   float* partial;  // split-K workspace [splits][M][N]
   GatherP g;
+  DgradP dg;
 };
+
+// Work unit u of the persistent schedule: output tile + K-block range.
+struct Unit {
+  int tm, tn, z, kb0, kb1;
+};
+__device__ __forceinline__ Unit decode_unit(const KParams& p, int u) {
+  Unit r;
+  r.tm = u % p.tiles_m;
+  r.tn = (u / p.tiles_m) % p.tiles_n;
+  r.z = u / (p.tiles_m * p.tiles_n);
+  r.kb0 = r.z * p.kb_per_split;
+  r.kb1 = min(r.kb0 + p.kb_per_split, p.nkb);
+  return r;
+}
 
 template <int BN>
 struct Cfg {
@@ -67,6 +101,12 @@ struct Cfg {
                                                      : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) {
   return __uint_as_float(((uint32_t)b) << 16);
@@ -159,6 +199,7 @@ enum EpiVariant : int {
   EV_ELU_BF16 = 3,  // bf16: ELU(x*scale + bias)
   EV_DELU_BF16 = 4, // bf16: x * ELU'(aux)
   EV_BF16 = 5,      // bf16: x*scale
+  EV_DGRAD = 6,     // bf16: x * ELU'(aux) at the sub-pixel position + bias sums
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -348,8 +389,80 @@ __device__ __forceinline__ void u8_store(uint8_t* sA, uint64_t* full, int gt,
   sm100::mbar_arrive(full);
 }
 
+// Sub-pixel dgrad epilogue for 16 columns (class cls, channels ci0..ci0+15)
+// of coarse row m: output offset of dz at (2yy+py, 2xx+px), or -1 when the
+// position is outside the image / the row is padding.
+template <int CI>
+__device__ __forceinline__ int64_t dgrad_offset(const KParams& p, int m, int col) {
+  const DgradP& g = p.dg;
+  const int per = g.Hb * g.Wb;
+  const int img = m / per, rem = m % per;  // tile rows: (image, y, x) of the TMA box
+  const int yy = rem / g.Wb, xx = rem % g.Wb;
+  const int cls = col / CI, ci0 = col % CI;
+  const int yi = 2 * yy + (cls >> 1), xi = 2 * xx + (cls & 1);
+  if (img >= g.n_img || yy >= g.Hcc || xx >= g.Wcc || yi >= g.Hi || xi >= g.Wi) return -1;
+  return (((int64_t)img * g.Hi + yi) * g.Wi + xi) * CI + ci0;
+}
+// x * ELU'(a_prev) -> bf16 store; bias sums of the stored values.
+__device__ __forceinline__ void dgrad_finish(const KParams& p, int64_t off,
+                                             const uint32_t (&r)[16], const uint4 (&a)[2],
+                                             float (&sv)[16]) {
+  uint32_t o[8];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t ww[4] = {a[h].x, a[h].y, a[h].z, a[h].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a0 = bf16_bits_to_float((uint16_t)(ww[q] & 0xFFFF));
+      const float a1 = bf16_bits_to_float((uint16_t)(ww[q] >> 16));
+      const float v0 = __uint_as_float(r[8 * h + 2 * q]) * (a0 > 0.0f ? 1.0f : a0 + 1.0f);
+      const float v1 = __uint_as_float(r[8 * h + 2 * q + 1]) * (a1 > 0.0f ? 1.0f : a1 + 1.0f);
+      o[4 * h + q] = pack_bf16(v0, v1);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // the stored (rounded) values feed the bias gradient
+    sv[2 * j] = bf16_bits_to_float((uint16_t)(o[j] & 0xFFFF));
+    sv[2 * j + 1] = bf16_bits_to_float((uint16_t)(o[j] >> 16));
+  }
+  uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.epi.out) + off);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+template <int AG>
+constexpr bool has_gather() {
+  return AG == AG_NHWC || AG == AG_U8;
+}
+// Epilogue warps: 8 (two per TMEM lane quarter); 16 for the sub-pixel dgrad,
+// whose epilogue gathers its ELU' operand from HBM and needs more loads in flight.
+template <int EV>
+constexpr int epi_warps() {
+  return EV == EV_DGRAD ? 16 : 8;
+}
+template <int EV, int AG>
+constexpr int kernel_threads() {
+  return 64 + 32 * epi_warps<EV>() + (has_gather<AG>() ? GATHER_THREADS : 0);
+}
+
+// Lane l ends with the sum over all 32 lanes of v[l & 15] (recursive halving,
+// 16 shuffles instead of 16 full butterflies).
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int k = 8; k >= 1; k >>= 1) {
+    const bool up = (lane & k) != 0;
+#pragma unroll
+    for (int j = 0; j < k; ++j) {
+      const float send = up ? v[j] : v[j + k];
+      const float keep = up ? v[j + k] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
 template <int BN, bool A_MN, bool B_MN, int EV, int AG = AG_NONE>
-__global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
+__global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, const KParams p) {
   using C = Cfg<BN>;
@@ -369,12 +482,12 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
     sm100::tma_prefetch(&mapA);
     sm100::tma_prefetch(&mapB);
     for (int s = 0; s < STAGES; ++s) {
-      sm100::mbar_init(&full[s], AG ? 1 + GATHER_THREADS : 1);
+      sm100::mbar_init(&full[s], has_gather<AG>() ? 1 + GATHER_THREADS : 1);
       sm100::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&acc_full[s], 1);
-      sm100::mbar_init(&acc_empty[s], 8);
+      sm100::mbar_init(&acc_empty[s], epi_warps<EV>());
     }
     sm100::fence_barrier_init();
   }
@@ -394,19 +507,21 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int tm = u % p.tiles_m;
-        const int tn = (u / p.tiles_m) % p.tiles_n;
-        const int z = u / (p.tiles_m * p.tiles_n);
-        const int kb0 = z * p.kb_per_split;
-        const int kb1 = min(kb0 + p.kb_per_split, p.nkb);
-        const int m0 = tm * BM, n0 = tn * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const Unit un = decode_unit(p, u);
+        const int m0 = un.tm * BM, n0 = un.tn * BN;
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + A_TILE_BYTES;
-          sm100::mbar_arrive_expect_tx(&full[stage], AG ? C::B_TILE_BYTES : C::STAGE_BYTES);
-          if (AG) {
+          sm100::mbar_arrive_expect_tx(&full[stage],
+                                       has_gather<AG>() ? C::B_TILE_BYTES : C::STAGE_BYTES);
+          if (has_gather<AG>()) {
             // A tile produced by the gather warps
+          } else if (AG == AG_DGRAD) {
+            // coarse rows (img, y, x) of the box; K block = (tap (a, b), channel atom)
+            const int tap = kb / p.dg.apt, at = kb % p.dg.apt;
+            sm100::tma_load_4d(sA, &mapA, &full[stage], at * 64, -(tap & 1), -(tap >> 1),
+                               un.tm * p.dg.Ib);
           } else if (!A_MN) {
             sm100::tma_load_2d(sA, &mapA, &full[stage], kb * BK, m0);
           } else {
@@ -435,15 +550,14 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int z = u / (p.tiles_m * p.tiles_n);
-        const int kb0 = z * p.kb_per_split;
-        const int kb1 = min(kb0 + p.kb_per_split, p.nkb);
+        const Unit un = decode_unit(p, u);
+        const int kb0 = un.kb0, kb1 = un.kb1;
         sm100::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
-          if (AG) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (has_gather<AG>()) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           sm100::tc_fence_after();
           const uint32_t a0 = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b0 = a0 + A_TILE_BYTES;
@@ -468,9 +582,9 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
         }
       }
     }
-  } else if (AG && warp >= THREADS / 32) {
+  } else if (has_gather<AG>() && warp >= 2 + epi_warps<EV>()) {
     // A gatherers: same (unit, k block) schedule as the TMA producer
-    const int gt = threadIdx.x - THREADS;
+    const int gt = threadIdx.x - 32 * (2 + epi_warps<EV>());
     // byte offset of chunk (kb, c) from the window origin (NHWC: (kh, kw, ci) order)
     __shared__ int off_tab[16 * 8];
     if (AG == AG_NHWC) {
@@ -524,7 +638,7 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
         origin = norigin;
       }
     }
-    for (int u = blockIdx.x; AG != AG_U8 && u < units; u += gridDim.x) {
+    for (int u = blockIdx.x; AG == AG_NHWC && u < units; u += gridDim.x) {
       const int tm = u % p.tiles_m;
       const int z = u / (p.tiles_m * p.tiles_n);
       const int kb0 = z * p.kb_per_split;
@@ -542,27 +656,61 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
       }
     }
   } else {
-    // epilogue warps 2..9: TMEM lane quarter (warp % 4), column half (warp - 2) / 4
+    // epilogue warps 2..: TMEM lane quarter (warp % 4), column part (warp - 2) / 4
+    constexpr int EPIW = epi_warps<EV>();
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
-    constexpr int HALF = BN / 2;
+    const int half = (warp - 2) >> 2;  // column part
+    constexpr int HALF = BN / (EPIW / 4);
     int acc = 0;
     uint32_t acc_phase = 0;
+    constexpr int CI = EV == EV_DGRAD ? BN / 4 : 1;  // dgrad: N = 4 classes x CI channels
+    constexpr int NCHB = EV == EV_DGRAD ? HALF / 16 : 1;
+    float bsum[NCHB];  // dgrad bias sums: lane l < 16 owns column part*HALF + ch*16 + l
+#pragma unroll
+    for (int j = 0; j < NCHB; ++j) bsum[j] = 0.0f;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int tm = u % p.tiles_m;
-      const int tn = (u / p.tiles_m) % p.tiles_n;
-      const int z = u / (p.tiles_m * p.tiles_n);
+      const Unit un = decode_unit(p, u);
+      const int tn = un.tn, z = un.z;
       sm100::mbar_wait(&acc_full[acc], acc_phase);
       sm100::tc_fence_after();
-      const int m = tm * BM + q * 32 + lane;
+      const int m = un.tm * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (EV == EV_DGRAD) {
+        // all ELU' operands of this warp's columns first (independent of the
+        // accumulator), then TMEM chunk by chunk
+        constexpr int NCH = HALF / 16;
+        int64_t off[NCH];
+        uint4 av[NCH][2];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          off[ch] = dgrad_offset<CI>(p, m, half * HALF + ch * 16);
+          const uint4* a4 = reinterpret_cast<const uint4*>(p.epi.aux + (off[ch] < 0 ? 0 : off[ch]));
+          av[ch][0] = off[ch] < 0 ? make_uint4(0, 0, 0, 0) : __ldg(a4);
+          av[ch][1] = off[ch] < 0 ? make_uint4(0, 0, 0, 0) : __ldg(a4 + 1);
+        }
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          uint32_t r[16];
+          sm100::tmem_ld16(tbase + half * HALF + ch * 16, r);
+          sm100::tmem_ld_wait();
+          float sv[16];
+          if (off[ch] >= 0) {
+            dgrad_finish(p, off[ch], r, av[ch], sv);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sv[j] = 0.0f;
+          }
+          bsum[ch] += transpose_reduce16(sv, lane);
+        }
+      } else {
 #pragma unroll 1
-      for (int c = half * HALF; c < (half + 1) * HALF; c += 16) {
-        if (tn * BN + c >= p.N) break;  // warp-uniform
-        uint32_t r[16];
-        sm100::tmem_ld16(tbase + c, r);
-        sm100::tmem_ld_wait();
-        epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
+        for (int c = half * HALF; c < (half + 1) * HALF; c += 16) {
+          if (tn * BN + c >= p.N) break;  // warp-uniform
+          uint32_t r[16];
+          sm100::tmem_ld16(tbase + c, r);
+          sm100::tmem_ld_wait();
+          epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -570,6 +718,32 @@ __global__ void __launch_bounds__(AG ? THREADS + GATHER_THREADS : THREADS, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+    }
+    if constexpr (EV == EV_DGRAD) {
+      // bias gradient: rows -> warp sums -> 2^-32 fixed-point atomics (order
+      // independent), last CTA converts and re-zeroes (model_kernels.cu scheme)
+      const DgradP& g = p.dg;
+      if (lane < 16) {
+#pragma unroll
+        for (int ch = 0; ch < NCHB; ++ch)
+          atomicAdd(g.bacc + (size_t)(blockIdx.x % 16) * CI + (half * HALF + ch * 16 + lane) % CI,
+                    (unsigned long long)llrint((double)bsum[ch] * 4294967296.0));
+      }
+      __threadfence();
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");  // epilogue warps only
+      __shared__ unsigned last_cta;
+      if (warp == 2 && lane == 0) last_cta = atomicAdd(g.bcnt, 1u) == gridDim.x - 1;
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");
+      if (last_cta) {
+        __threadfence();
+        const int et = threadIdx.x - 64;
+        for (int n = et; n < CI; n += 32 * EPIW) {
+          unsigned long long v = 0;
+          for (int k = 0; k < 16; ++k) v += atomicExch(g.bacc + (size_t)k * CI + n, 0ull);
+          g.bout[n] = (float)((double)(long long)v * (1.0 / 4294967296.0));
+        }
+        if (et == 0) *g.bcnt = 0;
       }
     }
   }
@@ -696,7 +870,7 @@ template <int BN, bool A_MN, bool B_MN, int EV, int AG = AG_NONE>
 int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& p) {
   using C = Cfg<BN>;
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EV, AG>;
-  constexpr int kThreads = AG ? THREADS + GATHER_THREADS : THREADS;
+  constexpr int kThreads = kernel_threads<EV, AG>();
   static bool attr_set[64] = {};
   int dev = c->device & 63;
   if (!attr_set[dev]) {
@@ -717,7 +891,8 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     static std::set<std::string> names;
     char buf[96];
     snprintf(buf, sizeof(buf), "gemm %dx%dx%d bn%d s%d %s%s%s", p.M, p.N, p.K, BN, p.splits,
-             A_MN ? "M" : "K", B_MN ? "M" : "K", AG == AG_U8 ? " conv-u8" : AG ? " conv" : "");
+             A_MN ? "M" : "K", B_MN ? "M" : "K",
+             AG == AG_U8 ? " conv-u8" : AG == AG_DGRAD ? " dgrad" : AG ? " conv" : "");
     c->next_name = names.insert(buf).first->c_str();
   }
   c->next_flops = 2.0 * p.M * p.N * p.K;
@@ -730,8 +905,13 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     const double imgs = (double)p.M / p.g.P;
     c->next_bytes = 2.0 * imgs * p.g.Hi * p.g.Wi * p.g.Cin + 2.0 * p.N * p.K + 2.0 * p.M * p.N;
   }
+  if (AG == AG_DGRAD) {  // useful MACs only (taps inside the kernel), HBM bytes
+    const DgradP& g = p.dg;
+    c->next_flops = 2.0 * g.n_img * p.g.Hi * p.g.Wi * (double)p.g.Cin * g.Ci;
+    c->next_bytes = 2.0 * g.n_img * ((double)p.g.Hi * p.g.Wi * p.g.Cin + 3.0 * g.Hi * g.Wi * g.Ci);
+  }
   if (AG && !(c->timing && c->timing_filter == "gemm_shapes"))
-    c->next_name = "gemm_conv_implicit_tcgen05";
+    c->next_name = AG == AG_DGRAD ? "gemm_dgrad_implicit_tcgen05" : "gemm_conv_implicit_tcgen05";
   APPO_LAUNCH(c, kern, grid, kThreads, C::SMEM_BYTES, ma, mb, p);
   return APPO_OK;
 }
@@ -866,6 +1046,95 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
     case 128: return launch_conv<128, AG_NHWC>(c, mb, p);
     default: set_error("conv_implicit: unsupported BN"); return APPO_ERR_CONTRACT;
   }
+}
+
+// 4-D bf16 map over NHWC [n][h][w][c], box {64, bw, bh, bn}, 128B swizzle,
+// zero OOB fill (negative / past-the-end coordinates read as zero).
+int make_map_nhwc(CUtensorMap* map, const void* ptr, int n, int h, int w, int c, int bw, int bh,
+                  int bn) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return APPO_ERR_RESOURCE;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  cuuint32_t box[4] = {64u, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (nhwc) failed: " + std::to_string((int)r));
+    return APPO_ERR_CONTRACT;
+  }
+  return APPO_OK;
+}
+
+int conv_dgrad_s2_bf16(Ctx* c, const DgradIn& in) {
+  APPO_REQUIRE(in.N == 32 || in.N == 64, APPO_ERR_CONTRACT, "conv_dgrad: N must be 32 or 64");
+  APPO_REQUIRE(in.Co % 64 == 0 && (in.k == 3 || in.k == 4), APPO_ERR_CONTRACT,
+               "conv_dgrad: Co % 64 == 0 and k in {3, 4}");
+  APPO_REQUIRE(in.bias.out && in.bias.acc && in.bias.counter, APPO_ERR_CONTRACT,
+               "conv_dgrad: bias outputs required");
+  APPO_REQUIRE((reinterpret_cast<uintptr_t>(in.dz_next) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(in.dz) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(in.aprev) & 15) == 0,
+               APPO_ERR_CONTRACT, "conv_dgrad: 16-byte aligned tensors required");
+  DgradP g{};
+  g.Hi = in.Hi;
+  g.Wi = in.Wi;
+  g.Ci = in.N;
+  g.n_img = in.n_img;
+  g.apt = in.Co / 64;
+  g.Hcc = (in.Hi + 1) / 2;
+  g.Wcc = (in.Wi + 1) / 2;
+  // live coarse region: rows with at least one tap inside dz_next
+  const int hl = in.Ho + 1 < g.Hcc ? in.Ho + 1 : g.Hcc;
+  const int wl = in.Wo + 1 < g.Wcc ? in.Wo + 1 : g.Wcc;
+  int wb = 1;
+  while (wb < g.Wcc) wb *= 2;  // box covers every coarse column (dead ones write zeros)
+  int hb = 1;
+  while (hb < hl) hb *= 2;
+  APPO_REQUIRE(wb * hb <= 128 && wl <= wb, APPO_ERR_CONTRACT, "conv_dgrad: image too large");
+  g.Wb = wb;
+  g.Hb = hb;
+  g.Ib = 128 / (wb * hb);
+  g.bacc = in.bias.acc;
+  g.bcnt = in.bias.counter;
+  g.bout = in.bias.out;
+  // coarse rows beyond the box (y >= Hb) have no taps: their outputs are zero
+  for (int yy = hb; yy < g.Hcc; ++yy)
+    for (int py = 0; py < 2; ++py) {
+      const int yi = 2 * yy + py;
+      if (yi >= in.Hi) continue;
+      APPO_CUDA_TRY(cudaMemset2DAsync(in.dz + (size_t)yi * in.Wi * in.N,
+                                      (size_t)in.Hi * in.Wi * in.N * 2, 0,
+                                      (size_t)in.Wi * in.N * 2, in.n_img, c->stream));
+    }
+  CUtensorMap ma, mb;
+  int st = make_map_nhwc(&ma, in.dz_next, in.n_img, in.Ho, in.Wo, in.Co, g.Wb, g.Hb, g.Ib);
+  if (st) return st;
+  const int kdim = 4 * in.Co, ndim = 4 * in.N;
+  st = make_map(&mb, in.wt, kdim, ndim, kdim, ndim);
+  if (st) return st;
+  KParams p{};
+  p.N = ndim;
+  p.K = kdim;
+  p.tiles_m = (in.n_img + g.Ib - 1) / g.Ib;
+  p.M = p.tiles_m * BM;
+  p.tiles_n = 1;
+  p.splits = 1;
+  p.nkb = kdim / BK;
+  p.kb_per_split = p.nkb;
+  p.epi.aux = in.aprev;
+  p.epi.out = in.dz;
+  p.g.Hi = in.Ho;  // for the byte / flop accounting
+  p.g.Wi = in.Wo;
+  p.g.Cin = in.Co * in.k * in.k;
+  p.dg = g;
+  if (in.N == 32) return launch_gemm<128, false, false, EV_DGRAD, AG_DGRAD>(c, ma, mb, p);
+  return launch_gemm<256, false, false, EV_DGRAD, AG_DGRAD>(c, ma, mb, p);
 }
 
 }  // namespace appo_b200

@@ -53,6 +53,30 @@ struct ConvIn {
 int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
                        int bn);
 
+// Bias-gradient output of a fused column sum: deterministic int64 fixed-point
+// accumulation (acc[16][N], zero between calls) + last-block conversion to out[N].
+struct BiasOut {
+  float* out = nullptr;
+  unsigned long long* acc = nullptr;
+  unsigned* counter = nullptr;
+  int N = 0;
+};
+
+// Input gradient of a stride-2 convolution (no padding) fused with ELU' of the
+// layer below and its bias gradient, as ONE implicit GEMM over the four
+// sub-pixel parity classes (no dcol matrix, no col2im):
+//   dz[r][y][x][n] = ELU'(aprev[r][y][x][n]) * sum_{kh,kw,co} dz_next[r][(y-kh)/2][(x-kw)/2][co] W[co][kh][kw][n]
+// wt = rearranged weights [4 classes][N][4 taps][Co] (k_dgrad_weights); k <= 4.
+struct DgradIn {
+  const uint16_t* dz_next = nullptr;  // bf16 NHWC [n_img][Ho][Wo][Co]
+  const uint16_t* wt = nullptr;
+  const uint16_t* aprev = nullptr;    // bf16 NHWC [n_img][Hi][Wi][N] (post-ELU activation)
+  uint16_t* dz = nullptr;             // bf16 NHWC [n_img][Hi][Wi][N]
+  int n_img = 0, Ho = 0, Wo = 0, Co = 0, Hi = 0, Wi = 0, N = 0, k = 0;
+  BiasOut bias;
+};
+int conv_dgrad_s2_bf16(Ctx* c, const DgradIn& in);
+
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);
 

@@ -186,8 +186,8 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
     a.take(&s.dz3, (size_t)B * d.F);
     a.take(&s.dz2, (size_t)B * d.P2 * 64);
     a.take(&s.dz1, (size_t)B * d.P1 * 32);
-    a.take(&s.dcol3, (size_t)B * d.P3 * 576);
-    a.take(&s.dcol2, (size_t)B * d.P2 * 512);
+    a.take(&s.wt3, (size_t)4 * 64 * 512);
+    a.take(&s.wt2, (size_t)4 * 32 * 256);
     a.take(&s.headw, (size_t)16 * kHidden);
     a.take(&s.colsum_part, (size_t)256 * kGates + 64);
     a.take(&s.bias_acc, (size_t)4 * kBiasAccCols);
@@ -211,8 +211,8 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
     reloc(s.rew, base); reloc(s.blogp, base); reloc(s.act, base); reloc(s.done, base);
     reloc(s.ver, base); reloc(s.dlog, base); reloc(s.dhead, base); reloc(s.dcore, base);
     reloc(s.dnext, base); reloc(s.dgi, base); reloc(s.dgh, base); reloc(s.dzfc, base);
-    reloc(s.dz3, base); reloc(s.dz2, base); reloc(s.dz1, base); reloc(s.dcol3, base);
-    reloc(s.dcol2, base); reloc(s.headw, base); reloc(s.colsum_part, base);
+    reloc(s.dz3, base); reloc(s.dz2, base); reloc(s.dz1, base); reloc(s.wt3, base);
+    reloc(s.wt2, base); reloc(s.headw, base); reloc(s.colsum_part, base);
     reloc(s.bias_acc, base); reloc(s.bias_cnt, base);
     if (cudaMemset(s.bias_acc, 0, sizeof(unsigned long long) * 4 * kBiasAccCols) != cudaSuccess ||
         cudaMemset(s.bias_cnt, 0, sizeof(unsigned) * 4) != cudaSuccess) {
@@ -671,6 +671,10 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
                             G + d.off_bv));
   }
 
+  // sub-pixel dgrad operands of conv2 / conv3 for this step's weights
+  TRY(k_dgrad_weights(ctx, wb + d.off_c3w, 128, 3, 64, s.wt3));
+  TRY(k_dgrad_weights(ctx, wb + d.off_c2w, 64, 4, 32, s.wt2));
+
   // bias gradients of fc / conv layers, fused into the kernels producing /
   // reading their dz (deterministic fixed-point sums, model_kernels.cu)
   auto bias_out = [&](int k, float* out, int N) {
@@ -751,14 +755,16 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     TRY(gemm_bf16(ctx, 128, 576, M3, Operand{s.dz3, 128, true}, Operand{s.col3, 576, true}, e,
                   192, splits_for(ctx, 128, 576, 192, M3)));
     TRY(k_colsum_v(ctx, M3, s.dz3, bias_out(1, G + d.off_c3b, 128)));
-    Epilogue x;
-    x.flags = EPI_BF16;
-    x.out = s.dcol3;
-    x.ldo = 576;
-    TRY(gemm_bf16(ctx, M3, 576, 128, Operand{s.dz3, 128, false},
-                  Operand{wb + d.off_c3w, 576, true}, x, 192));
-    TRY(k_col2im_delu_bf16(ctx, s.dcol3, s.a2, B, d.H2, d.W2, 64, 3, 2, d.H3, d.W3, s.dz2,
-                           bias_out(2, G + d.off_c2b, 64)));
+    // dz2 = ELU'(a2) * conv3^T(dz3): sub-pixel implicit GEMM (+ conv2 bias grad)
+    DgradIn in;
+    in.dz_next = s.dz3;
+    in.wt = s.wt3;
+    in.aprev = s.a2;
+    in.dz = s.dz2;
+    in.n_img = B;
+    in.Ho = d.H3; in.Wo = d.W3; in.Co = 128; in.Hi = d.H2; in.Wi = d.W2; in.N = 64; in.k = 3;
+    in.bias = bias_out(2, G + d.off_c2b, 64);
+    TRY(conv_dgrad_s2_bf16(ctx, in));
   }
   // ---- conv2 backward ----
   {
@@ -768,14 +774,16 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     e.ldo = 512;
     TRY(gemm_bf16(ctx, 64, 512, M2, Operand{s.dz2, 64, true}, Operand{s.col2, 512, true}, e, 256,
                   splits_for(ctx, 64, 512, 256, M2)));
-    Epilogue x;
-    x.flags = EPI_BF16;
-    x.out = s.dcol2;
-    x.ldo = 512;
-    TRY(gemm_bf16(ctx, M2, 512, 64, Operand{s.dz2, 64, false},
-                  Operand{wb + d.off_c2w, 512, true}, x, 256));
-    TRY(k_col2im_delu_bf16(ctx, s.dcol2, s.a1, B, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.dz1,
-                           bias_out(3, G + d.off_c1b, 32)));
+    // dz1 = ELU'(a1) * conv2^T(dz2) (+ conv1 bias grad)
+    DgradIn in;
+    in.dz_next = s.dz2;
+    in.wt = s.wt2;
+    in.aprev = s.a1;
+    in.dz = s.dz1;
+    in.n_img = B;
+    in.Ho = d.H2; in.Wo = d.W2; in.Co = 64; in.Hi = d.H1; in.Wi = d.W1; in.N = 32; in.k = 4;
+    in.bias = bias_out(3, G + d.off_c1b, 32);
+    TRY(conv_dgrad_s2_bf16(ctx, in));
   }
   // ---- conv1 weight gradient (input is data) ----
   {

@@ -53,7 +53,7 @@ struct Scratch {
   uint16_t* hcur_bf = nullptr;  // [2][n_traj][512] bf16 h_t exchange (persistent GRU)
   uint16_t *dgi = nullptr, *dgh = nullptr;  // [B][1536] bf16
   uint16_t *dzfc = nullptr, *dz3 = nullptr, *dz2 = nullptr, *dz1 = nullptr;
-  uint16_t *dcol3 = nullptr, *dcol2 = nullptr;  // bf16 im2col-space input gradients
+  uint16_t *wt3 = nullptr, *wt2 = nullptr;  // sub-pixel dgrad weight operands
   float* headw = nullptr;       // [16][512]
   float* colsum_part = nullptr; // partials for bias grads
   unsigned long long* bias_acc = nullptr;  // [4][kBiasAccCols] fixed-point bias-gradient sums

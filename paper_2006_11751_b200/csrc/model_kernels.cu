@@ -232,6 +232,20 @@ __global__ void __launch_bounds__(256)
   block_colsum_reduce(acc, cg, bias);
 }
 
+// Sub-pixel dgrad weight operand (see k_dgrad_weights): one thread per element.
+// wt[(cls, ci)][(a, b, co)] = W[co][py+2a][px+2b][ci] for taps inside the kernel, else 0.
+__global__ void dgrad_weights_kernel(const uint16_t* __restrict__ w, int Co, int k, int Ci,
+                                     uint16_t* __restrict__ wt) {
+  const int kmax = 4 * Co;
+  const int total = 4 * Ci * kmax;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int kk = g % kmax, ci = (g / kmax) % Ci, cls = g / (kmax * Ci);
+    const int tap = kk / Co, co = kk % Co;
+    const int kh = (cls >> 1) + 2 * (tap >> 1), kw = (cls & 1) + 2 * (tap & 1);
+    wt[g] = (kh < k && kw < k) ? w[(((size_t)co * k + kh) * k + kw) * Ci + ci] : (uint16_t)0;
+  }
+}
+
 __global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int64_t src_ld,
                                    uint16_t* __restrict__ dst, int64_t dst_ld, int cols) {
   const int64_t total = n * cols;
@@ -690,6 +704,10 @@ int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias) {
   if (grid < 1) grid = 1;
   c->next_bytes = (double)M * N * 2;
   APPO_LAUNCH(c, colsum_v_kernel, grid, 256, 0, M, src, bias);
+  return APPO_OK;
+}
+int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* wt) {
+  APPO_LAUNCH(c, dgrad_weights_kernel, grid_for(16 * Ci * Co, 256, 64), 256, 0, w, Co, k, Ci, wt);
   return APPO_OK;
 }
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,

@@ -2,6 +2,7 @@
 #pragma once
 #include <stdint.h>
 
+#include "gemm.cuh"
 #include "model.cuh"
 
 namespace appo_b200 {
@@ -33,14 +34,9 @@ int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Ci
                   int Ho, int Wo, uint16_t* col);
 int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
                   int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
-// Bias-gradient output of a fused column sum: deterministic int64 fixed-point
-// accumulation (acc[N], zero between calls) + last-block conversion to out[N].
-struct BiasOut {
-  float* out = nullptr;
-  unsigned long long* acc = nullptr;
-  unsigned* counter = nullptr;
-  int N = 0;
-};
+// Rearranges W[co][k][k][ci] (bf16) into the sub-pixel dgrad operand
+// wt[class (py,px)][ci][(2a + b)*Co + co] = W[co][py+2a][px+2b][ci] (0 outside the kernel).
+int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* wt);
 // bias.out != null: also writes the bias gradient (column sums of dz)
 int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
                        int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz,
