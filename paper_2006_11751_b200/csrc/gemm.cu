@@ -503,83 +503,82 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   const int units = p.tiles_m * p.tiles_n * p.splits;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit un = decode_unit(p, u);
-        const int m0 = un.tm * BM, n0 = un.tn * BN;
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sA = smem + stage * C::STAGE_BYTES;
-          uint8_t* sB = sA + A_TILE_BYTES;
-          sm100::mbar_arrive_expect_tx(&full[stage],
-                                       has_gather<AG>() ? C::B_TILE_BYTES : C::STAGE_BYTES);
-          if (has_gather<AG>()) {
-            // A tile produced by the gather warps
-          } else if (AG == AG_DGRAD) {
-            // coarse rows (img, y, x) of the box; K block = (tap (a, b), channel atom)
-            const int tap = kb / p.dg.apt, at = kb % p.dg.apt;
-            sm100::tma_load_4d(sA, &mapA, &full[stage], at * 64, -(tap & 1), -(tap >> 1),
-                               un.tm * p.dg.Ib);
-          } else if (!A_MN) {
-            sm100::tma_load_2d(sA, &mapA, &full[stage], kb * BK, m0);
-          } else {
-            sm100::tma_load_2d(sA, &mapA, &full[stage], m0, kb * BK);
-            sm100::tma_load_2d(sA + 8192, &mapA, &full[stage], m0 + 64, kb * BK);
-          }
-          if (!B_MN) {
-            sm100::tma_load_2d(sB, &mapB, &full[stage], kb * BK, n0);
-          } else {
+    // TMA producer: whole warp, one elected lane issues (sm100.cuh *_warp)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit un = decode_unit(p, u);
+      const int m0 = un.tm * BM, n0 = un.tn * BN;
+      for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        sm100::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sA = smem + stage * C::STAGE_BYTES;
+        uint8_t* sB = sA + A_TILE_BYTES;
+        sm100::mbar_arrive_expect_tx_warp(&full[stage],
+                                          has_gather<AG>() ? C::B_TILE_BYTES : C::STAGE_BYTES);
+        if (has_gather<AG>()) {
+          // A tile produced by the gather warps
+        } else if (AG == AG_DGRAD) {
+          // coarse rows (img, y, x) of the box; K block = (tap (a, b), channel atom)
+          const int tap = kb / p.dg.apt, at = kb % p.dg.apt;
+          sm100::tma_load_4d_warp(sA, &mapA, &full[stage], at * 64, -(tap & 1), -(tap >> 1),
+                                  un.tm * p.dg.Ib);
+        } else if (!A_MN) {
+          sm100::tma_load_2d_warp(sA, &mapA, &full[stage], kb * BK, m0);
+        } else {
+          sm100::tma_load_2d_warp(sA, &mapA, &full[stage], m0, kb * BK);
+          sm100::tma_load_2d_warp(sA + 8192, &mapA, &full[stage], m0 + 64, kb * BK);
+        }
+        if (!B_MN) {
+          sm100::tma_load_2d_warp(sB, &mapB, &full[stage], kb * BK, n0);
+        } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              sm100::tma_load_2d(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, kb * BK);
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          for (int j = 0; j < BN / 64; ++j)
+            sm100::tma_load_2d_warp(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, kb * BK);
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = sm100::make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit un = decode_unit(p, u);
-        const int kb0 = un.kb0, kb1 = un.kb1;
-        sm100::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+    // MMA issuer: the whole warp runs the loop; elect.sync inside the tcgen05
+    // asm picks the issuing lane (no per-instruction waterfall, sm100.cuh)
+    constexpr uint32_t idesc = sm100::make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit un = decode_unit(p, u);
+      const int kb0 = un.kb0, kb1 = un.kb1;
+      sm100::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      sm100::tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        sm100::mbar_wait(&full[stage], phase);
+        if (has_gather<AG>()) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sm100::tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          sm100::mbar_wait(&full[stage], phase);
-          if (has_gather<AG>()) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          sm100::tc_fence_after();
-          const uint32_t a0 = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
-          const uint32_t b0 = a0 + A_TILE_BYTES;
+        const uint32_t a0 = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
+        const uint32_t b0 = a0 + A_TILE_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? sm100::make_sdesc(a0 + k * 2048, 8192, 1024)
-                                     : sm100::make_sdesc(a0 + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sm100::make_sdesc(b0 + k * 2048, 8192, 1024)
-                                     : sm100::make_sdesc(b0 + k * 32, 16, 1024);
-            sm100::umma_f16(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          }
-          sm100::umma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = A_MN ? sm100::make_sdesc(a0 + k * 2048, 8192, 1024)
+                                   : sm100::make_sdesc(a0 + k * 32, 16, 1024);
+          const uint64_t bd = B_MN ? sm100::make_sdesc(b0 + k * 2048, 8192, 1024)
+                                   : sm100::make_sdesc(b0 + k * 32, 16, 1024);
+          sm100::umma_f16_warp(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
         }
-        sm100::umma_commit(&acc_full[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        sm100::umma_commit_warp(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
+      }
+      sm100::umma_commit_warp(&acc_full[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else if (has_gather<AG>() && warp >= 2 + epi_warps<EV>()) {
@@ -1066,6 +1065,28 @@ int make_map_nhwc(CUtensorMap* map, const void* ptr, int n, int h, int w, int c,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (nhwc) failed: " + std::to_string((int)r));
+    return APPO_ERR_CONTRACT;
+  }
+  return APPO_OK;
+}
+
+int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                      uint32_t b2) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return APPO_ERR_RESOURCE;
+  }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3d) failed: " + std::to_string((int)r));
     return APPO_ERR_CONTRACT;
   }
   return APPO_OK;

@@ -1,5 +1,6 @@
 // Host interface of the tcgen05 GEMM engine (gemm.cu).
 #pragma once
+#include <cuda.h>
 #include <stdint.h>
 
 #include "appo_common.cuh"
@@ -76,6 +77,12 @@ struct DgradIn {
   BiasOut bias;
 };
 int conv_dgrad_s2_bf16(Ctx* c, const DgradIn& in);
+
+// 3-D bf16 tensor map (dims innermost first, byte strides of dims 1 and 2),
+// 128B swizzle, zero OOB fill.
+int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                      uint32_t b2);
 
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);

@@ -23,6 +23,11 @@
 // 0..15 hold rows 16w..16w+15.
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "gemm.cuh"
 #include "model.cuh"
 #include "model_kernels.cuh"
 #include "sm100.cuh"
@@ -48,7 +53,13 @@ __device__ __forceinline__ uint16_t f2bf_(float f) {
   __nv_bfloat16 h = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&h);
 }
-__device__ __forceinline__ float sig_(float x) { return 1.0f / (1.0f + expf(-x)); }
+// fast-math gates: MUFU ex2 + fast divide (|err| ~1e-7, far below the bf16
+// operand rounding of the recurrent product)
+__device__ __forceinline__ float sig_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_(float x) { return 2.0f * sig_(2.0f * x) - 1.0f; }
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -99,6 +110,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 struct FwdArgs {
+  CUtensorMap hmap;      // 3-D map over hbuf_bf {512, n_traj, 2}, box {64, 64, 1}, SW128
   int n_traj, T;
   const float* gi;       // [R][1536] (x W_ih^T + b_ih), rows s = i*T+t, boot rows B+i
   const uint16_t* whh;   // bf16 [1536][512] (published copy of the master)
@@ -112,9 +124,10 @@ struct FwdArgs {
   float* hin;            // [R][512]
   uint16_t* hbf;         // [R][512]
   unsigned* bar;
+  long long* prof;       // optional phase timestamps (APPO_GRU_PROF): [steps][4]
 };
 
-__global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
+__global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_constant__ FwdArgs a) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
@@ -122,7 +135,8 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
   uint8_t* tB = sm + A_TILE;
   float* gh = reinterpret_cast<float*>(tB + B_FWD);              // [64][NG]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(gh + MAXTRAJ * NG);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+  uint64_t* kbar = mbar + 1;  // [8] one per staged K block of h_t
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kbar + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j0 = blockIdx.x * UPC_F;
   const int B = a.n_traj * a.T;
@@ -136,6 +150,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
   }
   if (tid == 0) {
     sm100::mbar_init(mbar, 1);
+    for (int k = 0; k < 8; ++k) sm100::mbar_init(&kbar[k], 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) {
@@ -175,6 +190,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
     }
   }
   prefetch(0);
+  fence_proxy_async_global();  // h0 stores -> visible to the TMA (async proxy) reads
   sm100::tc_fence_before();
   grid_barrier(a.bar, gridDim.x);  // h0 bf16 complete everywhere
   sm100::tc_fence_after();
@@ -184,25 +200,37 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
   uint32_t phase = 0;
 
   for (int t = 0; t <= a.T; ++t) {
-    const size_t cur = (size_t)(t & 1) * a.n_traj * kHidden;
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 0] = clock64();
     const size_t nxt = (size_t)((t + 1) & 1) * a.n_traj * kHidden;
-    stage_async(tA, a.hbuf_bf + cur, a.n_traj, kHidden, 0);
-    cp_async_wait_all();
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      sm100::tc_fence_after();
+    // h_t (written by every CTA before the barrier) -> smem by TMA, one K block
+    // per mbarrier so the MMAs start on the first block while the rest land
+    if (warp == 1) {
+      fence_proxy_async_global();
+#pragma unroll
+      for (int kb = 0; kb < 8; ++kb) {
+        sm100::mbar_arrive_expect_tx_warp(&kbar[kb], KB_BYTES_A);
+        sm100::tma_load_3d_warp(tA + kb * KB_BYTES_A, &a.hmap, &kbar[kb], kb * 64, 0, t & 1);
+      }
+    }
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 1] = clock64();
+    if (warp == 0) {  // whole warp: elect.sync inside (no per-MMA waterfall)
       const uint32_t a0 = sm100::smem_u32(tA), b0 = sm100::smem_u32(tB);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const uint64_t ad = sm100::make_sdesc(a0 + (k >> 2) * KB_BYTES_A + (k & 3) * 32, 16, 1024);
-        const uint64_t bd = sm100::make_sdesc(b0 + (k >> 2) * NG * 128 + (k & 3) * 32, 16, 1024);
-        sm100::umma_f16(tmem, ad, bd, idesc, k > 0 ? 1u : 0u);
+      for (int kb = 0; kb < 8; ++kb) {
+        sm100::mbar_wait(&kbar[kb], t & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ad = sm100::make_sdesc(a0 + kb * KB_BYTES_A + k * 32, 16, 1024);
+          const uint64_t bd = sm100::make_sdesc(b0 + kb * NG * 128 + k * 32, 16, 1024);
+          sm100::umma_f16_warp(tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+        }
       }
-      sm100::umma_commit(mbar);
+      sm100::umma_commit_warp(mbar);
     }
     sm100::mbar_wait(mbar, phase);
     phase ^= 1;
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
     sm100::tc_fence_after();
     if (warp < 4) {
       uint32_t r[16];
@@ -230,7 +258,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
       const float ghn = gh[i * NG + 2 * UPC_F + u] + b3[c][2];
       const float rr = sig_(g3[c][0] + ghr);
       const float z = sig_(g3[c][1] + ghz);
-      const float n = tanhf(g3[c][2] + rr * ghn);
+      const float n = tanh_(g3[c][2] + rr * ghn);
       const float hp = hreg[c];
       const float h = (1.0f - z) * n + z * hp;
       a.core[row * kHidden + j] = h;
@@ -248,8 +276,10 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
         a.hbuf_bf[nxt + (int64_t)i * kHidden + j] = f2bf_(hn);
       }
     }
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 3] = clock64();
     if (t < a.T) {
       prefetch(t + 1);  // independent of the exchange: overlaps the barrier
+      fence_proxy_async_global();
       grid_barrier(a.bar, ++epoch * gridDim.x);
     }
   }
@@ -262,6 +292,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(FwdArgs a) {
 }
 
 struct BwdArgs {
+  CUtensorMap xmap;     // 3-D map over dghx {1536, n_traj, 2}, box {64, 64, 1}, SW128
   int n_traj, T;
   const float* dcore;   // [B][512]
   const uint8_t* done;  // [B]
@@ -274,9 +305,10 @@ struct BwdArgs {
   float* gbih;          // [1536] bias gradients (sums over all B rows)
   float* gbhh;          // [1536]
   unsigned* bar;
+  long long* prof;      // optional phase timestamps (APPO_GRU_PROF): [steps][4]
 };
 
-__global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
+__global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_constant__ BwdArgs a) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
@@ -284,7 +316,8 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   uint8_t* tB = sm + 3 * A_TILE;
   float* mm = reinterpret_cast<float*>(tB + B_BWD);      // [64][8] dgh . W_hh[:, own]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(mm + MAXTRAJ * UPC_B);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+  uint64_t* kbar = mbar + 1;  // [6] one per 4 staged K blocks (32 KB) of dgh_t
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kbar + 6);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j0 = blockIdx.x * UPC_B;
 
@@ -303,6 +336,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   }
   if (tid == 0) {
     sm100::mbar_init(mbar, 1);
+    for (int k = 0; k < 6; ++k) sm100::mbar_init(&kbar[k], 1);
     sm100::fence_barrier_init();
   }
   if (warp == 0) {
@@ -315,7 +349,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   const uint32_t tmem = *tslot;
   constexpr uint32_t idesc = sm100::make_idesc_bf16(MAXTRAJ, UPC_B, 0, 0);
   unsigned epoch = 0;
-  uint32_t phase = 0;
+  uint32_t phase = 0, kphase = 0;
 
   constexpr int CPT = MAXTRAJ * UPC_B / THR;  // 2 cells per thread
   const int n_cells = a.n_traj * UPC_B;
@@ -345,6 +379,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   prefetch(a.T - 1);
 
   for (int t = a.T - 1; t >= 0; --t) {
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 0] = clock64();
     uint16_t* xb = a.dghx + (size_t)(t & 1) * a.n_traj * kGates;
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -384,26 +419,42 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
     }
     if (t == 0) break;  // d(h0) is not needed
     prefetch(t - 1);    // independent of the exchange: overlaps barrier + MMA
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 1] = clock64();
+    fence_proxy_async_global();  // dgh_t stores -> visible to the TMA reads
     grid_barrier(a.bar, ++epoch * gridDim.x);
-    // dnext = dh*z + dgh_t . W_hh[:, own]: all of dgh_t in one async stage
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
+    // dnext = dh*z + dgh_t . W_hh[:, own]: dgh_t (24 K blocks of 8 KB) by TMA in
+    // six 32 KB groups; the MMAs of a group start as soon as it lands
+    if (warp == 1) {
+      fence_proxy_async_global();
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) stage_async(tA + ch * A_TILE, xb, a.n_traj, kGates, ch * 512);
-    cp_async_wait_all();
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      sm100::tc_fence_after();
-      const uint32_t a0 = sm100::smem_u32(tA), b0 = sm100::smem_u32(tB);
-#pragma unroll 8
-      for (int kg = 0; kg < 96; ++kg) {  // K16 steps over 1536
-        const uint64_t ad = sm100::make_sdesc(
-            a0 + (kg >> 5) * A_TILE + ((kg & 31) >> 2) * KB_BYTES_A + (kg & 3) * 32, 16, 1024);
-        const uint64_t bd =
-            sm100::make_sdesc(b0 + (kg >> 2) * UPC_B * 128 + (kg & 3) * 32, 16, 1024);
-        sm100::umma_f16(tmem, ad, bd, idesc, kg > 0 ? 1u : 0u);
+      for (int g = 0; g < 6; ++g) {
+        sm100::mbar_arrive_expect_tx_warp(&kbar[g], 4 * KB_BYTES_A);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          sm100::tma_load_3d_warp(tA + (4 * g + q) * KB_BYTES_A, &a.xmap, &kbar[g],
+                                  (4 * g + q) * 64, 0, t & 1);
       }
-      sm100::umma_commit(mbar);
     }
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 3] = clock64();
+    if (warp == 0) {  // whole warp: elect.sync inside (no per-MMA waterfall)
+      const uint32_t a0 = sm100::smem_u32(tA), b0 = sm100::smem_u32(tB);
+      for (int g = 0; g < 6; ++g) {
+        sm100::mbar_wait(&kbar[g], kphase);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {  // K16 steps of this 256-wide group
+          const int kg = 16 * g + kk;
+          const uint64_t ad =
+              sm100::make_sdesc(a0 + (kg >> 2) * KB_BYTES_A + (kg & 3) * 32, 16, 1024);
+          const uint64_t bd =
+              sm100::make_sdesc(b0 + (kg >> 2) * UPC_B * 128 + (kg & 3) * 32, 16, 1024);
+          sm100::umma_f16_warp(tmem, ad, bd, idesc, kg > 0 ? 1u : 0u);
+        }
+      }
+      sm100::umma_commit_warp(mbar);
+    }
+    kphase ^= 1;
     sm100::mbar_wait(mbar, phase);
     phase ^= 1;
     sm100::tc_fence_after();
@@ -457,9 +508,41 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(BwdArgs a) {
   }
 }
 
-constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + MAXTRAJ * NG * 4 + 64;
-constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + MAXTRAJ * UPC_B * 4 + 64;
+constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + MAXTRAJ * NG * 4 + 128;
+constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + MAXTRAJ * UPC_B * 4 + 128;
 static_assert(BWD_SMEM <= 227 * 1024, "backward GRU smem");
+
+// Phase profiling of block 0 (env APPO_GRU_PROF=1; diagnostics only): clock64
+// stamps per step, averaged and printed to stderr after a synchronize.
+long long* prof_buffer(Ctx* c) {
+  static long long* buf = nullptr;
+  if (!getenv("APPO_GRU_PROF")) return nullptr;
+  if (!buf && cudaMalloc(&buf, sizeof(long long) * 4 * 64) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(buf, 0, sizeof(long long) * 4 * 64, c->stream);
+  return buf;
+}
+void prof_report(Ctx* c, long long* d, int steps, const char* what) {
+  long long h[4 * 64];
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(h, d, sizeof(long long) * 4 * steps, cudaMemcpyDeviceToHost);
+  double acc[4] = {0, 0, 0, 0};
+  int n = 0;
+  for (int t = 0; t + 1 < steps; ++t) {
+    const long long* a = h + 4 * t;
+    const long long* b = h + 4 * (t + 1);
+    if (!a[0] || !b[0]) continue;
+    // forward order: stamps 0..3 then next step's 0; backward steps run downwards
+    const long long* nxt = strstr(what, "bwd") ? h + 4 * (t > 0 ? t - 1 : 0) : b;
+    (void)nxt;
+    acc[0] += a[1] - a[0];
+    acc[1] += a[2] - a[1];
+    acc[2] += a[3] - a[2];
+    acc[3] += (strstr(what, "bwd") ? (t > 0 ? h[4 * (t - 1)] - a[3] : 0) : b[0] - a[3]);
+    ++n;
+  }
+  fprintf(stderr, "[gru prof] %s (cycles/step, %d steps): %.0f %.0f %.0f %.0f\n", what, n,
+          acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n);
+}
 
 }  // namespace
 
@@ -476,7 +559,14 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
     attr = true;
   }
   APPO_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));
-  FwdArgs a{n_traj, T, gi, whh, bhh, done, hbuf, hbuf_bf, core, core_bf, gates, hin, hbf, bar};
+  long long* prof = prof_buffer(c);
+  FwdArgs a{};
+  int st = make_tmap_bf16_3d(&a.hmap, hbuf_bf, kHidden, n_traj, 2, kHidden * 2,
+                             (uint64_t)n_traj * kHidden * 2, 64, MAXTRAJ, 1);
+  if (st) return st;
+  a.n_traj = n_traj; a.T = T; a.gi = gi; a.whh = whh; a.bhh = bhh; a.done = done; a.hbuf = hbuf;
+  a.hbuf_bf = hbuf_bf; a.core = core; a.core_bf = core_bf; a.gates = gates; a.hin = hin;
+  a.hbf = hbf; a.bar = bar; a.prof = prof;
   void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_fwd_kernel");
   APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_fwd_kernel, dim3(NCTA_F), dim3(THR),
@@ -484,6 +574,7 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T + 1);
   timing_end(c, "gru_seq_fwd_kernel", ev);
   c->launches++;
+  if (prof) prof_report(c, prof, T + 1, "fwd: stage | mma | epilogue+barrier");
   return APPO_OK;
 }
 
@@ -497,7 +588,14 @@ int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* 
     attr = true;
   }
   APPO_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));
-  BwdArgs a{n_traj, T, dcore, done, gates, hin, whh, dghx, dgi, dgh, gbih, gbhh, bar};
+  long long* prof = prof_buffer(c);
+  BwdArgs a{};
+  int st = make_tmap_bf16_3d(&a.xmap, dghx, kGates, n_traj, 2, kGates * 2,
+                             (uint64_t)n_traj * kGates * 2, 64, MAXTRAJ, 1);
+  if (st) return st;
+  a.n_traj = n_traj; a.T = T; a.dcore = dcore; a.done = done; a.gates = gates; a.hin = hin;
+  a.whh = whh; a.dghx = dghx; a.dgi = dgi; a.dgh = dgh; a.gbih = gbih; a.gbhh = gbhh;
+  a.bar = bar; a.prof = prof;
   void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_bwd_kernel");
   APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_bwd_kernel, dim3(NCTA_B), dim3(THR),
@@ -505,6 +603,7 @@ int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* 
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T - 1);
   timing_end(c, "gru_seq_bwd_kernel", ev);
   c->launches++;
+  if (prof) prof_report(c, prof, T, "bwd: cell | barrier | stage | mma");
   return APPO_OK;
 }
 
