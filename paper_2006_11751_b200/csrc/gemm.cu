@@ -18,6 +18,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -32,21 +34,28 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int STAGES = 4;
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int A_TILE_BYTES = BM * BK * 2;  // 16 KB
 
 // Implicit-GEMM A operand (convolution forward): row m = output position
 // (image r = m / P, p = m % P, y = p / Wo, x = p % Wo), K = receptive field.
 struct GatherP {
-  const uint8_t* src;  // AG_NHWC: bf16 NHWC activations; AG_U8: first u8 CHW image
-  int64_t img_stride;  // AG_U8: bytes between images (obs_dim, or the slot stride)
+  const uint8_t* src;  // AG_NHWC: bf16 NHWC activations; AG_U8: first u8 CHW image / slot region
+  int64_t img_stride;  // AG_U8: bytes between images (contiguous batches)
   int P, Wo;           // output positions per image, output width
   int Hi, Wi, Cin;     // input geometry (AG_U8: channels C, H, W)
   int ksz, s;          // kernel size, stride
+  // AG_U8 images in trajectory slots (layout v2): image r < n_traj*T is step
+  // r % T of slot slot_ids[r / T]; later images are the bootstrap observations
+  const int32_t* slot_ids;
+  uint64_t slot_bytes, obs_off, boot_off;
+  int T, n_traj;
+  int nq;    // AG_U8: output rows (images x Ho)
+  int tma;   // AG_U8 staging: 1 = tensor-map boxes (mapA / map2), 0 = bulk copies
 };
 enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3 };
-constexpr int GATHER_THREADS = 128;  // warps 10..13
+constexpr int GATHER_THREADS = 128;  // NHWC gather warps (after the epilogue warps)
+constexpr int U8_GATHER_THREADS = 256;  // conv1 staging/convert warps: two per tile row
 
 // Input gradient of a stride-2 convolution (kernel k <= 4, no padding) by
 // sub-pixel decomposition.  Input position (2yy+py, 2xx+px) only receives
@@ -68,13 +77,20 @@ struct DgradP {
 };
 
 struct KParams {
+  CUtensorMap map2;  // AG_U8 from trajectory slots: the bootstrap-observation map
   int M, N, K;
   int tiles_m, tiles_n, splits, kb_per_split, nkb;
   Epilogue epi;
   float* partial;  // split-K workspace [splits][M][N]
   GatherP g;
   DgradP dg;
+  long long* prof;  // optional per-role timestamps of CTA 0 (APPO_GEMM_PROF), [16 units][8]
 };
+#define GEMM_PROF(slot)                                                      \
+  do {                                                                       \
+    if (p.prof && blockIdx.x == 0 && (u - (int)blockIdx.x) / (int)gridDim.x < 16) \
+      p.prof[((u - blockIdx.x) / gridDim.x) * 16 + (slot)] = clock64();      \
+  } while (0)
 
 // Work unit u of the persistent schedule: output tile + K-block range.
 struct Unit {
@@ -99,8 +115,15 @@ struct Cfg {
                                    : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256
                                                      : 512;
+  // small-N tiles (conv1) are latency-bound per K block: deeper ring
+  static constexpr int STAGES = BN <= 32 ? 8 : 4;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
+
+// ELU with the MUFU exponential: |error| <= ~1e-7 absolute, far below the
+// bf16 rounding of the stored activation (accurate expm1f costs ~25 instructions
+// per element, which made the small-N conv epilogues instruction-bound).
+__device__ __forceinline__ float elu_fast(float x) { return x > 0.0f ? x : __expf(x) - 1.0f; }
 
 __device__ __forceinline__ float warp_sum_f(float v) {
 #pragma unroll
@@ -136,7 +159,7 @@ __device__ __forceinline__ void epilogue_chunk(const KParams& p, int m, int n0, 
     const int n = n0 + j;
     float x = v[j] * e.scale;
     if ((e.flags & EPI_BIAS) && n < p.N) x += e.bias[n];
-    if (e.flags & EPI_ELU) x = x > 0.0f ? x : expm1f(x);
+    if (e.flags & EPI_ELU) x = elu_fast(x);
     if ((e.flags & EPI_DELU) && n < p.N) {
       const float a = bf16_bits_to_float(e.aux[(size_t)m * e.ld_aux + n]);
       x *= (a > 0.0f ? 1.0f : a + 1.0f);
@@ -248,7 +271,7 @@ __device__ __forceinline__ void epilogue_dispatch(const KParams& p, int m, int n
     }
     if constexpr (EV == EV_ELU_BF16) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = v[j] > 0.0f ? v[j] : expm1f(v[j]);
+      for (int j = 0; j < 16; ++j) v[j] = elu_fast(v[j]);
     }
     if constexpr (EV == EV_DELU_BF16) {
       const uint4* a4 = reinterpret_cast<const uint4*>(e.aux + (size_t)m * e.ld_aux + n0);
@@ -354,39 +377,156 @@ __device__ __forceinline__ void gather_stage(const KParams& p, uint8_t* sA, uint
   }
 }
 
-// u8 gather split into its load and convert/store halves so the gatherers
-// can keep the next stage's 16 loads in flight while converting this one.
-__device__ __forceinline__ void u8_load(const KParams& p, const uint8_t* origin, bool valid,
-                                        int kb, uint32_t (&lo)[8], uint32_t (&hi)[8]) {
-  const uint8_t* img = origin + (int64_t)kb * p.g.Hi * p.g.Wi;
+// ---- conv1 (u8, k8 s4) implicit GEMM with smem-staged input ------------------
+// Tile = 4 consecutive output rows q (q = image * Ho + y) x 32 columns (the
+// last one padding for Wo = 31): tile row m = 32 * (q - 4 * tile) + x.  The
+// gather warps cp.async the 8 input rows of every (output row, channel) into
+// a double-buffered staging area (12 KB, the next tile's while this one is
+// converted), then build each channel's [128 rows x 64 (kh, kw)] A block from
+// shared memory (u8 -> exact bf16; 1/255 folded into the epilogue scale).
+constexpr int U8_ROWS = 4;  // output rows per tile (x 32 columns = BM)
+constexpr int U8_NSTG = 4;  // staging ring depth (tiles in flight per CTA)
+
+__device__ __forceinline__ const uint8_t* u8_image(const GatherP& g, int img) {
+  if (!g.slot_ids) return g.src + (int64_t)img * g.img_stride;
+  const int B = g.n_traj * g.T;
+  if (img < B)
+    return g.src + (uint64_t)g.slot_ids[img / g.T] * g.slot_bytes + g.obs_off +
+           (uint64_t)(img % g.T) * ((uint64_t)g.Hi * g.Wi * g.Cin);
+  return g.src + (uint64_t)g.slot_ids[img - B] * g.slot_bytes + g.boot_off;
+}
+
+// Staging slot layout: block (output row k, channel c) of U8_BLK bytes holds
+// the 8 input rows (8*W contiguous bytes in global memory), copied from the
+// 16-byte aligned address at or below them; delta[k] (0 or 8, per image) is
+// where they start inside the block.
+constexpr int U8_BLK = 8 * 128 + 16;
+constexpr int U8_SID_CACHE = 256;  // slot ids cached in shared memory by the staging warp
+constexpr int U8_BOX_ROWS = 4 * (U8_ROWS - 1) + 8;  // input rows of U8_ROWS output rows
+__host__ __device__ constexpr int u8_stage_bytes(int C) {
+  // max of the bulk layout and the two-run tensor-box layout (+16 B overread slack)
+  // (rounded to 128 B: tensor-TMA destinations must be 128-byte aligned)
+  return ((U8_ROWS * U8_BLK > 2 * U8_BOX_ROWS * 128 ? U8_ROWS * U8_BLK : 2 * U8_BOX_ROWS * 128) * C +
+          16 + 127) & ~127;
+}
+
+// Tensor-map staging (one TMA box {W, 20 rows, C} per run of consecutive
+// output rows of the same image: at most two per tile).  meta[k] = byte
+// offset of output row k's first input row (channel 0) in the slot; channel
+// planes are U8_BOX_ROWS * W apart.
+__device__ __forceinline__ void u8_stage_tma(const KParams& p, const CUtensorMap* mapA, int tile,
+                                             uint8_t* buf, int* meta, uint64_t* bar, int lane,
+                                             const int* sids, long long* pf = nullptr) {
+  const GatherP& g = p.g;
+  const int Ho = g.P / g.Wo;
+  const int q0 = tile * U8_ROWS;
+  const int nrow = min(U8_ROWS, g.nq - q0);
+  const int img0 = q0 / Ho, y0 = q0 - img0 * Ho;
+  const int n0 = min(nrow, Ho - y0);  // rows of the first image
+  const int box = g.Cin * U8_BOX_ROWS * g.Wi;
+  if (pf && lane == 0) pf[8] = clock64();
+  if (lane == 0)
 #pragma unroll
-  for (int kh = 0; kh < 8; ++kh) {
-    const uint8_t* s = img + (int64_t)kh * p.g.Wi;
-    lo[kh] = valid ? __ldg(reinterpret_cast<const uint32_t*>(s)) : 0u;
-    hi[kh] = valid ? __ldg(reinterpret_cast<const uint32_t*>(s + 4)) : 0u;
+    for (int k = 0; k < U8_ROWS; ++k)
+      meta[k] = k < n0 ? 4 * k * g.Wi : box + 4 * (k - n0) * g.Wi;
+  __syncwarp();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of buf
+  if (pf && lane == 0) pf[9] = clock64();
+  sm100::mbar_arrive_expect_tx_warp(bar, (n0 < nrow ? 2 : 1) * box);
+  if (pf && lane == 0) pf[10] = clock64();
+  for (int r = 0; r < (n0 < nrow ? 2 : 1); ++r) {
+    const int img = r ? img0 + 1 : img0, y = r ? 0 : y0;
+    uint8_t* dst = buf + r * box;
+    if (!g.slot_ids) {
+      sm100::tma_load_4d_warp(dst, mapA, bar, 0, 4 * y, 0, img);
+    } else {
+      const int B = g.n_traj * g.T;
+      const int si = img < B ? img / g.T : img - B;
+      const int sid = si < U8_SID_CACHE ? sids[si] : g.slot_ids[si];
+      if (img < B)
+        sm100::tma_load_5d_warp(dst, mapA, bar, 0, 4 * y, 0, img % g.T, sid);
+      else
+        sm100::tma_load_4d_warp(dst, &p.map2, bar, 0, 4 * y, 0, sid);
+    }
   }
 }
-__device__ __forceinline__ void u8_store(uint8_t* sA, uint64_t* full, int gt,
-                                         const uint32_t (&lo)[8], const uint32_t (&hi)[8]) {
-  const uint32_t row_base = sm100::smem_u32(sA) + gt * 128;
+
+// Producer side (whole warp; one elected lane issues): bulk copies of tile
+// `tile`'s input rows into a staging slot, completion on its mbarrier.  Image
+// addresses are computed for all rows first (independent slot-id loads in
+// flight together), the per-row alignment deltas are stored afterwards.
+__device__ __forceinline__ void u8_stage_bulk(const GatherP& g, int tile, uint8_t* buf,
+                                              int* delta, uint64_t* bar, int lane) {
+  const int Ho = g.P / g.Wo;
+  const uint32_t bytes = 8u * g.Wi;
+  const uint8_t* r0[U8_ROWS];
 #pragma unroll
-  for (int kh = 0; kh < 8; ++kh) {
-    uint32_t w[4];
+  for (int k = 0; k < U8_ROWS; ++k) {
+    const int q = min(tile * U8_ROWS + k, g.nq - 1);  // clamp: padding rows are not copied
+    const int img = q / Ho, y = q - img * Ho;
+    r0[k] = u8_image(g, img) + (int64_t)(y * 4) * g.Wi;
+  }
+  uint32_t total = 0;
+  int d[U8_ROWS];
+  uint32_t cbytes[U8_ROWS];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // exact u8 -> bf16 (see gather_stage)
-      const uint32_t word = q < 2 ? lo[kh] : hi[kh];
-      const int k0 = (q & 1) * 2;
-      const float f0 = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0)) - 8388608.0f;
-      const float f1 =
-          __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0 + 1)) - 8388608.0f;
-      w[q] = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632);
-    }
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row_base +
-                                                                 ((kh ^ (gt & 7)) << 4)),
-                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+  for (int k = 0; k < U8_ROWS; ++k) {
+    const bool ok = tile * U8_ROWS + k < g.nq;
+    d[k] = (int)(reinterpret_cast<uintptr_t>(r0[k]) & 15);
+    cbytes[k] = ok ? (bytes + d[k] + 15) & ~15u : 0u;
+    total += g.Cin * cbytes[k];
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < U8_ROWS; ++k) delta[k] = k * g.Cin * U8_BLK + d[k];  // meta: block + delta
+  __syncwarp();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of buf
+  sm100::mbar_arrive_expect_tx_warp(bar, total);
+#pragma unroll
+  for (int k = 0; k < U8_ROWS; ++k) {
+    if (!cbytes[k]) continue;
+    for (int c = 0; c < g.Cin; ++c)
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+              sm100::smem_u32(buf + (k * g.Cin + c) * U8_BLK)),
+          "l"(r0[k] - d[k] + (int64_t)c * g.Hi * g.Wi), "r"(cbytes[k]), "r"(sm100::smem_u32(bar))
+          : "memory");
+  }
+}
+
+// Build half a row of channel c's A block from the staged bytes (SW128
+// K-major): thread gt handles tile row gt & 127, kernel rows kh = 4*(gt>>7)..+3.
+// Values are written as fp16 (1024 + v): one PRMT per pair, exact for v in
+// 0..255 (fp16 has unit spacing on [1024, 2048)); the constant 1024 * sum(W)
+// is removed through the epilogue bias (k_conv1_half_weights).
+__device__ __forceinline__ void u8_convert(const GatherP& g, const uint8_t* buf, const int* meta,
+                                           uint8_t* sA, int c, int gt) {
+  const int row = gt & 127, kh0 = (gt >> 7) * 4;
+  const int k = row >> 5, x = row & 31;
+  const int plane = g.tma ? U8_BOX_ROWS * g.Wi : U8_BLK;
+  const uint32_t src = sm100::smem_u32(buf) + meta[k] + c * plane + kh0 * g.Wi + 4 * x;
+  const uint32_t row_base = sm100::smem_u32(sA) + row * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t lo, hi;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(src + j * g.Wi));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(src + j * g.Wi + 4));
+    const uint32_t w0 = __byte_perm(lo, 0x64646464u, 0x4140);
+    const uint32_t w1 = __byte_perm(lo, 0x64646464u, 0x4342);
+    const uint32_t w2 = __byte_perm(hi, 0x64646464u, 0x4140);
+    const uint32_t w3 = __byte_perm(hi, 0x64646464u, 0x4342);
+    const int kh = kh0 + j;
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row_base + ((kh ^ (row & 7)) << 4)),
+                 "r"(w0), "r"(w1), "r"(w2), "r"(w3)
                  : "memory");
   }
-  sm100::mbar_arrive(full);
+}
+
+// Output row of tile row m (conv1 epilogue), -1 for padding.
+__device__ __forceinline__ int u8_out_row(const GatherP& g, int m) {
+  const int q = m >> 5, x = m & 31;
+  return (q < g.nq && x < g.Wo) ? q * g.Wo + x : -1;
 }
 
 // Sub-pixel dgrad epilogue for 16 columns (class cls, channels ci0..ci0+15)
@@ -440,9 +580,14 @@ template <int EV>
 constexpr int epi_warps() {
   return EV == EV_DGRAD ? 16 : 8;
 }
+template <int AG>
+constexpr int gather_threads() {
+  return AG == AG_U8 ? U8_GATHER_THREADS : has_gather<AG>() ? GATHER_THREADS : 0;
+}
 template <int EV, int AG>
 constexpr int kernel_threads() {
-  return 64 + 32 * epi_warps<EV>() + (has_gather<AG>() ? GATHER_THREADS : 0);
+  // conv1 adds U8_NSTG staging warps after the gatherers (input rows -> smem ring)
+  return 64 + 32 * epi_warps<EV>() + gather_threads<AG>() + (AG == AG_U8 ? 32 * U8_NSTG : 0);
 }
 
 // Lane l ends with the sum over all 32 lanes of v[l & 15] (recursive halving,
@@ -464,14 +609,14 @@ __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 template <int BN, bool A_MN, bool B_MN, int EV, int AG = AG_NONE>
 __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA,
-                     const __grid_constant__ CUtensorMap mapB, const KParams p) {
+                     const __grid_constant__ CUtensorMap mapB, const __grid_constant__ KParams p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* acc_full = empty + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* acc_full = empty + C::STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -481,13 +626,20 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&mapA);
     sm100::tma_prefetch(&mapB);
-    for (int s = 0; s < STAGES; ++s) {
-      sm100::mbar_init(&full[s], has_gather<AG>() ? 1 + GATHER_THREADS : 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      sm100::mbar_init(&full[s], 1 + gather_threads<AG>());
       sm100::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&acc_full[s], 1);
       sm100::mbar_init(&acc_empty[s], epi_warps<EV>());
+    }
+    if (AG == AG_U8) {  // conv1 input staging ring: full (tx) / empty (all gatherers)
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+      for (int s = 0; s < U8_NSTG; ++s) {
+        sm100::mbar_init(&sfull[s], 1);
+        sm100::mbar_init(&sfull[U8_NSTG + s], gather_threads<AG>());
+      }
     }
     sm100::fence_barrier_init();
   }
@@ -511,6 +663,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       const int m0 = un.tm * BM, n0 = un.tn * BN;
       for (int kb = un.kb0; kb < un.kb1; ++kb) {
         sm100::mbar_wait(&empty[stage], phase ^ 1);
+
         uint8_t* sA = smem + stage * C::STAGE_BYTES;
         uint8_t* sB = sA + A_TILE_BYTES;
         sm100::mbar_arrive_expect_tx_warp(&full[stage],
@@ -535,7 +688,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           for (int j = 0; j < BN / 64; ++j)
             sm100::tma_load_2d_warp(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, kb * BK);
         }
-        if (++stage == STAGES) {
+        if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
         }
@@ -544,7 +697,9 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   } else if (warp == 1) {
     // MMA issuer: the whole warp runs the loop; elect.sync inside the tcgen05
     // asm picks the issuing lane (no per-instruction waterfall, sm100.cuh)
-    constexpr uint32_t idesc = sm100::make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    // conv1 (AG_U8) runs on fp16 operands (exact 1024 + u8, fp16 weights)
+    constexpr uint32_t idesc = AG == AG_U8 ? sm100::make_idesc_f16(BM, BN, 0, 0)
+                                           : sm100::make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -553,6 +708,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       const Unit un = decode_unit(p, u);
       const int kb0 = un.kb0, kb1 = un.kb1;
       sm100::mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      if (lane == 0) GEMM_PROF(3);
       sm100::tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -570,16 +726,45 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           sm100::umma_f16_warp(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
         }
         sm100::umma_commit_warp(&empty[stage]);
-        if (++stage == STAGES) {
+        if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
       sm100::umma_commit_warp(&acc_full[acc]);
+      if (lane == 0) GEMM_PROF(4);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
+    }
+  } else if (AG == AG_U8 && warp >= 2 + epi_warps<EV>() + gather_threads<AG>() / 32) {
+    // conv1 staging warps: warp w owns ring slot w and stages the CTA's units
+    // j = w, w + U8_NSTG, ... (a TMA issue costs ~1000 cycles of the issuing
+    // warp, so the slots are filled in parallel)
+    uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+    uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES + 256;
+    int* smeta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
+    __shared__ int sids[U8_SID_CACHE];
+    if (p.g.slot_ids)
+      for (int i = lane; i < min(p.g.n_traj, U8_SID_CACHE); i += 32) sids[i] = p.g.slot_ids[i];
+    __syncwarp();
+    const int slot = warp - (2 + epi_warps<EV>() + gather_threads<AG>() / 32);
+    uint32_t sphase = 0;
+    for (int u = blockIdx.x + slot * gridDim.x; u < units; u += U8_NSTG * gridDim.x) {
+      const Unit un = decode_unit(p, u);
+      sm100::mbar_wait(&sfull[U8_NSTG + slot], sphase ^ 1);
+      if (lane == 0) GEMM_PROF(0);
+      if (p.g.tma)
+        u8_stage_tma(p, &mapA, un.tm, stg + slot * u8_stage_bytes(p.g.Cin), smeta + slot * U8_ROWS,
+                     &sfull[slot], lane, sids,
+                     (p.prof && blockIdx.x == 0 && u / (int)gridDim.x < 16)
+                         ? p.prof + (u / gridDim.x) * 16 : nullptr);
+      else
+        u8_stage_bulk(p.g, un.tm, stg + slot * u8_stage_bytes(p.g.Cin), smeta + slot * U8_ROWS,
+                      &sfull[slot], lane);
+      if (lane == 0) GEMM_PROF(7);
+      sphase ^= 1;
     }
   } else if (has_gather<AG>() && warp >= 2 + epi_warps<EV>()) {
     // A gatherers: same (unit, k block) schedule as the TMA producer
@@ -598,43 +783,33 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     int stage = 0;
     uint32_t phase = 0;
     if constexpr (AG == AG_U8) {
-      // software-pipelined: loads of work item j+1 in flight while item j is
-      // converted (u8 conv1 has no split-K: one tile = nkb consecutive items)
-      int u = blockIdx.x, kb = 0;
-      bool valid = false;
-      const uint8_t* origin = nullptr;
-      uint32_t lo[8], hi[8], nlo[8], nhi[8];
-      if (u < units) {
-        origin = gather_row_origin<AG>(p, (u % p.tiles_m) * BM + gt, valid);
-        u8_load(p, origin, valid, 0, lo, hi);
-      }
-      while (u < units) {
-        int nu = u, nkb = kb + 1;
-        if (nkb == p.nkb) {
-          nu = u + gridDim.x;
-          nkb = 0;
+      // staged input ring (filled by the producer warp): wait slot -> convert
+      // the tile channel by channel -> release the slot
+      uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES + 256;
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+      uint64_t* sempty = sfull + U8_NSTG;
+      int* sdelta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
+      int slot = 0;
+      uint32_t sphase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        sm100::mbar_wait(&sfull[slot], sphase);
+        if (gt == 0) GEMM_PROF(1);
+        for (int c = 0; c < p.nkb; ++c) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          u8_convert(p.g, stg + slot * u8_stage_bytes(p.g.Cin), sdelta + slot * U8_ROWS,
+                     smem + stage * C::STAGE_BYTES, c, gt);
+          sm100::mbar_arrive(&full[stage]);
+          if (gt == 0 && c == 0) GEMM_PROF(2);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        bool nvalid = valid;
-        const uint8_t* norigin = origin;
-        if (nu < units) {
-          if (nu != u) norigin = gather_row_origin<AG>(p, (nu % p.tiles_m) * BM + gt, nvalid);
-          u8_load(p, norigin, nvalid, nkb, nlo, nhi);
+        sm100::mbar_arrive(&sempty[slot]);
+        if (++slot == U8_NSTG) {
+          slot = 0;
+          sphase ^= 1;
         }
-        sm100::mbar_wait(&empty[stage], phase ^ 1);
-        u8_store(smem + stage * C::STAGE_BYTES, &full[stage], gt, lo, hi);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          lo[q] = nlo[q];
-          hi[q] = nhi[q];
-        }
-        u = nu;
-        kb = nkb;
-        valid = nvalid;
-        origin = norigin;
       }
     }
     for (int u = blockIdx.x; AG == AG_NHWC && u < units; u += gridDim.x) {
@@ -648,7 +823,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
         sm100::mbar_wait(&empty[stage], phase ^ 1);
         gather_stage<AG>(p, smem + stage * C::STAGE_BYTES, &full[stage], origin, valid, kb, gt,
                          off_tab);
-        if (++stage == STAGES) {
+        if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
         }
@@ -671,6 +846,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       const Unit un = decode_unit(p, u);
       const int tn = un.tn, z = un.z;
       sm100::mbar_wait(&acc_full[acc], acc_phase);
+      if (warp == 2 && lane == 0) GEMM_PROF(5);
       sm100::tc_fence_after();
       const int m = un.tm * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -708,12 +884,18 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           uint32_t r[16];
           sm100::tmem_ld16(tbase + c, r);
           sm100::tmem_ld_wait();
-          epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
+          if constexpr (AG == AG_U8) {  // tile rows -> (output row, x); padding skipped
+            const int mo = u8_out_row(p.g, m);
+            if (mo >= 0) epilogue_dispatch<EV>(p, mo, tn * BN + c, z, r);
+          } else {
+            epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
+          }
         }
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
+      if (warp == 2 && lane == 0) GEMM_PROF(6);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -869,16 +1051,19 @@ template <int BN, bool A_MN, bool B_MN, int EV, int AG = AG_NONE>
 int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& p) {
   using C = Cfg<BN>;
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EV, AG>;
+  // conv1: input staging ring after the barriers (+16 B overread slack)
+  const int smem_bytes =
+      C::SMEM_BYTES + (AG == AG_U8 ? U8_NSTG * u8_stage_bytes(p.g.Cin) + 64 : 0);
   constexpr int kThreads = kernel_threads<EV, AG>();
-  static bool attr_set[64] = {};
+  static int attr_bytes[64] = {};
   int dev = c->device & 63;
-  if (!attr_set[dev]) {
+  if (attr_bytes[dev] < smem_bytes) {
     APPO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::SMEM_BYTES));
-    attr_set[dev] = true;
+                                       smem_bytes));
+    attr_bytes[dev] = smem_bytes;
   }
   const int units = p.tiles_m * p.tiles_n * p.splits;
-  int per_sm = (227 * 1024) / C::SMEM_BYTES;
+  int per_sm = (227 * 1024) / smem_bytes;
   const int tmem_per_sm = 512 / C::TMEM_COLS;
   per_sm = per_sm < tmem_per_sm ? per_sm : tmem_per_sm;
   if (per_sm < 1) per_sm = 1;
@@ -911,14 +1096,37 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
   }
   if (AG && !(c->timing && c->timing_filter == "gemm_shapes"))
     c->next_name = AG == AG_DGRAD ? "gemm_dgrad_implicit_tcgen05" : "gemm_conv_implicit_tcgen05";
-  APPO_LAUNCH(c, kern, grid, kThreads, C::SMEM_BYTES, ma, mb, p);
+  APPO_LAUNCH(c, kern, grid, kThreads, smem_bytes, ma, mb, p);
   return APPO_OK;
 }
 
 template <int BN, int AG>
-int launch_conv(Ctx* c, const CUtensorMap& mb, const KParams& p) {
-  return choose_ev(p) == EV_ELU_BF16 ? launch_gemm<BN, false, false, EV_ELU_BF16, AG>(c, mb, mb, p)
-                                     : launch_gemm<BN, false, false, EV_GENERIC, AG>(c, mb, mb, p);
+int launch_conv(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& p) {
+  return choose_ev(p) == EV_ELU_BF16 ? launch_gemm<BN, false, false, EV_ELU_BF16, AG>(c, ma, mb, p)
+                                     : launch_gemm<BN, false, false, EV_GENERIC, AG>(c, ma, mb, p);
+}
+
+// u8 tensor map (no swizzle) over images; dims innermost first, byte strides of dims 1..
+int make_tmap_u8(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims,
+                 const uint64_t* strides, const uint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return APPO_ERR_RESOURCE;
+  if (reinterpret_cast<uintptr_t>(ptr) & 15) return APPO_ERR_CONTRACT;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) {
+      st[i] = strides[i];
+      if (st[i] % 16) return APPO_ERR_CONTRACT;
+    }
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void*>(ptr), d, st, b, e,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? APPO_OK : APPO_ERR_CONTRACT;
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -973,7 +1181,7 @@ int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
   st = B.mn_major ? make_map(&mb, B.ptr, N, K, B.ld, BK) : make_map(&mb, B.ptr, K, N, B.ld, bn);
   if (st) return st;
 
-  KParams p;
+  KParams p{};
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1016,10 +1224,16 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
   if (M <= 0) return APPO_OK;
   APPO_REQUIRE(!W.mn_major && K % 64 == 0 && (in.u8 || in.Cin % 8 == 0), APPO_ERR_CONTRACT,
                "conv_implicit: K-major weights, K % 64 == 0 and Cin % 8 == 0 required");
-  APPO_REQUIRE(!in.u8 || (in.ksz == 8 && in.Wi % 4 == 0 &&
-                          (reinterpret_cast<uintptr_t>(in.src) & 3) == 0 && in.img_stride % 4 == 0),
-               APPO_ERR_CONTRACT, "conv_implicit u8: k8, W % 4 == 0, 4-byte aligned images");
-  CUtensorMap mb;
+  // staging copies whole 8-row blocks from 16-byte aligned addresses at or below
+  // them (images need 8-byte alignment; blocks hold at most 8*128 + 16 bytes)
+  APPO_REQUIRE(!in.u8 || (in.ksz == 8 && in.s == 4 && in.Wi % 16 == 0 && in.Wi <= 128 &&
+                          in.Wo <= 32 && (reinterpret_cast<uintptr_t>(in.src) & 7) == 0 &&
+                          in.img_stride % 8 == 0 && in.slot_bytes % 8 == 0 &&
+                          in.obs_off % 8 == 0 && in.boot_off % 8 == 0 && in.Cin <= 4),
+               APPO_ERR_CONTRACT,
+               "conv_implicit u8: k8 s4, W % 16 == 0, W <= 128, C <= 4, 8-byte aligned images");
+  CUtensorMap mb, mb_u8;
+  std::memset(&mb_u8, 0, sizeof(mb_u8));
   int st = make_map(&mb, W.ptr, K, N, W.ld, bn);
   if (st) return st;
   KParams p{};
@@ -1033,16 +1247,55 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
   p.kb_per_split = p.nkb;
   p.epi = epi;
   p.partial = nullptr;
-  p.g = GatherP{in.src, in.img_stride, in.Ho * in.Wo, in.Wo, in.Hi, in.Wi, in.Cin, in.ksz, in.s};
+  p.g = GatherP{in.src, in.img_stride, in.Ho * in.Wo, in.Wo, in.Hi, in.Wi, in.Cin, in.ksz, in.s,
+                in.slot_ids, in.slot_bytes, in.obs_off, in.boot_off, in.T, in.n_traj,
+                in.n_img * in.Ho};
   if (in.u8) {
+    // tiles of U8_ROWS output rows x 32 columns (see u8_stage_tma)
+    p.tiles_m = (p.g.nq + U8_ROWS - 1) / U8_ROWS;
+    // staging by tensor-map boxes when the images are 16-byte aligned, else bulk copies
+    const uint64_t W = in.Wi, H = in.Hi, C = in.Cin, plane = W * H, od = plane * C;
+    const uint32_t box[5] = {(uint32_t)W, (uint32_t)U8_BOX_ROWS, (uint32_t)C, 1, 1};
+    p.g.tma = 0;
+    if (!in.slot_ids) {
+      const uint64_t dims[4] = {W, H, C, (uint64_t)in.n_img};
+      const uint64_t str[3] = {W, plane, (uint64_t)in.img_stride};
+      if (make_tmap_u8(&mb_u8, in.src, 4, dims, str, box) == APPO_OK) p.g.tma = 1;
+    } else if (in.n_slots > 0) {
+      const uint64_t dims[5] = {W, H, C, (uint64_t)in.T, (uint64_t)in.n_slots};
+      const uint64_t str[4] = {W, plane, od, in.slot_bytes};
+      const uint64_t bdims[4] = {W, H, C, (uint64_t)in.n_slots};
+      const uint64_t bstr[3] = {W, plane, in.slot_bytes};
+      if (make_tmap_u8(&mb_u8, in.src + in.obs_off, 5, dims, str, box) == APPO_OK &&
+          make_tmap_u8(&p.map2, in.src + in.boot_off, 4, bdims, bstr, box) == APPO_OK)
+        p.g.tma = 1;
+    }
+
+    static long long* prof = nullptr;
+    if (getenv("APPO_GEMM_PROF")) {
+      if (!prof) cudaMalloc(&prof, sizeof(long long) * 256);
+      cudaMemsetAsync(prof, 0, sizeof(long long) * 256, c->stream);
+      p.prof = prof;
+      st = launch_conv<32, AG_U8>(c, mb_u8, mb, p);
+      long long h[256];
+      cudaStreamSynchronize(c->stream);
+      cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[gemm prof] nq=%d units of CTA0 (cycles rel. to unit0 gather start): gth_start stg_ready cvt0 | mma_accfree mma_commit | epi_start epi_done | prod_first\n", p.g.nq);
+      for (int i = 0; i < 16; ++i) {
+        fprintf(stderr, "  u%-2d", i);
+        for (int k = 0; k < 11; ++k) fprintf(stderr, " %7lld", h[i * 16 + k] ? h[i * 16 + k] - h[0] : -1);
+        fprintf(stderr, "\n");
+      }
+      return st;
+    }
     switch (bn) {
-      case 32: return launch_conv<32, AG_U8>(c, mb, p);
+      case 32: return launch_conv<32, AG_U8>(c, mb_u8, mb, p);
       default: return APPO_ERR_CONTRACT;
     }
   }
   switch (bn) {
-    case 64: return launch_conv<64, AG_NHWC>(c, mb, p);
-    case 128: return launch_conv<128, AG_NHWC>(c, mb, p);
+    case 64: return launch_conv<64, AG_NHWC>(c, mb, mb, p);
+    case 128: return launch_conv<128, AG_NHWC>(c, mb, mb, p);
     default: set_error("conv_implicit: unsupported BN"); return APPO_ERR_CONTRACT;
   }
 }

@@ -50,6 +50,12 @@ struct ConvIn {
   int64_t img_stride = 0;        // u8: bytes between images
   int n_img = 0, Hi = 0, Wi = 0, Cin = 0, ksz = 0, s = 0, Ho = 0, Wo = 0;
   bool u8 = false;
+  // u8 images in trajectory slots: src = slot region, image r < n_traj*T is
+  // step r % T of slot slot_ids[r / T], later ones the bootstrap observations
+  const int32_t* slot_ids = nullptr;
+  uint64_t slot_bytes = 0, obs_off = 0, boot_off = 0;
+  int T = 0, n_traj = 0;
+  int n_slots = 0;  // slots in the region (max slot id + 1): bounds of the tensor maps
 };
 int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
                        int bn);

@@ -285,27 +285,34 @@ int splits_for(Ctx* c, int M, int N, int bn, int K) {
 // im2col matrices are materialised because the learner's weight gradients
 // consume them.
 int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, const uint16_t* wb,
-                    const float* pf, bool implicit) {
+                    const float* pf, int pub, bool implicit) {
   const Dims& d = M->d;
   Epilogue e;
-  // conv1: [R*P1, 32] = col1 [R*P1, K1] . W1[32, K1]^T, x/255 folded into scale
+  // conv1: [R*P1, 32] = (1024 + obs) . W1h^T / 255 + bias' (fp16 operands,
+  // offset removed by the corrected bias of the published copy)
   e.flags = EPI_BIAS | EPI_ELU | EPI_BF16;
   e.scale = 1.0f / 255.0f;
-  e.bias = pf + d.off_c1b;
+  e.bias = M->pub_c1b[pub];
   e.out = s.a1;
   e.ldo = 32;
-  if (implicit) {
+  {
+    // conv1 always gathers its input from the u8 images (smem-staged implicit
+    // GEMM); the learner additionally materialises col1 for the weight gradient
     ConvIn in;
     in.src = src.base;
     in.img_stride = src.img_stride;
+    in.slot_ids = src.slot_ids;
+    in.slot_bytes = src.slot_bytes;
+    in.obs_off = src.obs_off;
+    in.boot_off = src.boot_off;
+    in.T = src.T;
+    in.n_traj = src.n_traj;
+    in.n_slots = src.n_slots;
     in.n_img = R;
     in.Hi = d.H; in.Wi = d.W; in.Cin = d.C; in.ksz = 8; in.s = 4; in.Ho = d.H1; in.Wo = d.W1;
     in.u8 = true;
-    TRY(conv_implicit_bf16(c, in, 32, Operand{wb + d.off_c1w, d.K1, false}, e, 32));
-  } else {
-    TRY(k_im2col_u8(c, src, R, d, s.col1));
-    TRY(gemm_bf16(c, R * d.P1, 32, d.K1, Operand{s.col1, d.K1, false},
-                  Operand{wb + d.off_c1w, d.K1, false}, e, 32));
+    TRY(conv_implicit_bf16(c, in, 32, Operand{M->pub_c1h[pub], d.K1, false}, e, 32));
+    if (!implicit) TRY(k_im2col_u8(c, src, R, d, s.col1));
   }
   e.scale = 1.0f;
   e.bias = pf + d.off_c2b;
@@ -381,7 +388,7 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
   ObsSrc src;
   src.base = obs_base;
   src.img_stride = obs_stride;
-  TRY(encoder_forward(c, M, s, src, B, wb, pf, /*implicit=*/true));
+  TRY(encoder_forward(c, M, s, src, B, wb, pf, pub, /*implicit=*/true));
   TRY(k_f32_to_bf16(c, B, h_in, kHidden, s.hbf, kHidden, kHidden));
   Epilogue g;
   g.flags = EPI_BIAS;
@@ -409,6 +416,12 @@ int model_create(Ctx* c) {
     delete M;
     return st;
   }
+  // encoder kernel envelope (conv1 input staging): W in {64, 128}, C*W <= 512
+  if ((M->d.W != 64 && M->d.W != 128) || M->d.C * M->d.W > 512) {
+    delete M;
+    set_error("model desc: the sm_100a encoder needs obs width 64 or 128 and C*W <= 512");
+    return APPO_ERR_CONFIG;
+  }
   c->model = M;
   const int64_t P = M->d.total;
   APPO_CUDA_TRY(cudaMalloc(&M->theta, P * 4));
@@ -418,6 +431,8 @@ int model_create(Ctx* c) {
   for (int k = 0; k < Model::kPub; ++k) {
     APPO_CUDA_TRY(cudaMalloc(&M->pub_bf16[k], P * 2));
     APPO_CUDA_TRY(cudaMalloc(&M->pub_f32[k], P * 4));
+    APPO_CUDA_TRY(cudaMalloc(&M->pub_c1h[k], (size_t)32 * M->d.K1 * 2));
+    APPO_CUDA_TRY(cudaMalloc(&M->pub_c1b[k], 32 * 4));
     APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->pub_ev[k], cudaEventDisableTiming));
     APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->ready_ev[k], cudaEventDisableTiming));
   }
@@ -440,6 +455,8 @@ void model_destroy(Ctx* c) {
   for (int k = 0; k < Model::kPub; ++k) {
     cudaFree(M->pub_bf16[k]);
     cudaFree(M->pub_f32[k]);
+    cudaFree(M->pub_c1h[k]);
+    cudaFree(M->pub_c1b[k]);
     if (M->pub_ev[k]) cudaEventDestroy(M->pub_ev[k]);
     if (M->ready_ev[k]) cudaEventDestroy(M->ready_ev[k]);
   }
@@ -495,6 +512,10 @@ int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version) {
     APPO_CUDA_TRY(cudaMemcpy(M->pub_f32[k], h_src, P * 4, cudaMemcpyHostToDevice));
     APPO_CUDA_TRY(cudaMemcpy(M->pub_bf16[k], bf.data(), P * 2, cudaMemcpyHostToDevice));
   }
+  for (int k = 0; k < Model::kPub; ++k)
+    TRY(k_conv1_half(ctx, M->pub_f32[k] + M->d.off_c1w, M->pub_f32[k] + M->d.off_c1b, M->d.K1,
+                     M->pub_c1h[k], M->pub_c1b[k]));
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   M->version = version;
   M->adam_t = 0;
   M->published = 0;
@@ -607,8 +628,13 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   src.boot_off = d.slot[7];
   src.T = T;
   src.n_traj = n_traj;
+  {
+    int mx = 0;
+    for (int i = 0; i < n_traj; ++i) mx = h_slot_ids[i] > mx ? h_slot_ids[i] : mx;
+    src.n_slots = mx + 1;
+  }
   src.obs_dim = d.obs_dim;
-  TRY(encoder_forward(ctx, M, s, src, R, wb, th, /*implicit=*/false));
+  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false));
 
   // ---- GRU unrolled over T steps (+ bootstrap step) ----
   const bool seq = gru_seq_supported(n_traj);
@@ -810,6 +836,8 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
                   M->pub_f32[next], ctx->d_counter + 6));
   APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
   APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
+  TRY(k_conv1_half(ctx, M->pub_f32[next] + d.off_c1w, M->pub_f32[next] + d.off_c1b, d.K1,
+                   M->pub_c1h[next], M->pub_c1b[next]));
   APPO_CUDA_TRY(cudaEventRecord(M->ready_ev[next], st));
   M->last_ring = ring;
   // Optimistic publish: the Adam kernel always rewrites pub[next] (with the

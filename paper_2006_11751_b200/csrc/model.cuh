@@ -77,6 +77,10 @@ struct Model {
   static constexpr int kPub = 8;
   uint16_t* pub_bf16[kPub] = {};
   float* pub_f32[kPub] = {};
+  // conv1 operands of the published copy: fp16 weights [32][K1] and the bias
+  // with the fp16-input offset removed (b - 1024/255 * sum_k W), see gemm.cu
+  uint16_t* pub_c1h[kPub] = {};
+  float* pub_c1b[kPub] = {};
   cudaEvent_t pub_ev[kPub] = {};    // recorded after the last inference read of pub[k]
   cudaEvent_t ready_ev[kPub] = {};  // recorded after the Adam step that wrote pub[k]
   int64_t pub_version[kPub] = {};   // parameter version held by pub[k]

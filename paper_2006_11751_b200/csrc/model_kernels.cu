@@ -7,6 +7,7 @@
 // coalesced along the innermost (channel / hidden) dimension, 16-byte vector
 // accesses where the layout allows it.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "model_kernels.cuh"
 
@@ -243,6 +244,24 @@ __global__ void dgrad_weights_kernel(const uint16_t* __restrict__ w, int Co, int
     const int tap = kk / Co, co = kk % Co;
     const int kh = (cls >> 1) + 2 * (tap >> 1), kw = (cls & 1) + 2 * (tap & 1);
     wt[g] = (kh < k && kw < k) ? w[(((size_t)co * k + kh) * k + kw) * Ci + ci] : (uint16_t)0;
+  }
+}
+
+// conv1 fp16 operands of a published parameter copy (one block, warp per
+// output channel): wh = fp16(W), bias' = b - (1024/255) * sum_k wh (the conv1
+// GEMM multiplies fp16 (1024 + pixel) inputs, gemm.cu u8_convert).
+__global__ void conv1_half_kernel(const float* __restrict__ w, const float* __restrict__ b,
+                                  int K, uint16_t* __restrict__ wh, float* __restrict__ bh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int co = warp; co < 32; co += blockDim.x >> 5) {
+    float acc = 0.0f;
+    for (int k = lane; k < K; k += 32) {
+      const __half h = __float2half_rn(w[(size_t)co * K + k]);
+      wh[(size_t)co * K + k] = __half_as_ushort(h);
+      acc += __half2float(h);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) bh[co] = b[co] - (1024.0f / 255.0f) * acc;
   }
 }
 
@@ -708,6 +727,10 @@ int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias) {
 }
 int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* wt) {
   APPO_LAUNCH(c, dgrad_weights_kernel, grid_for(16 * Ci * Co, 256, 64), 256, 0, w, Co, k, Ci, wt);
+  return APPO_OK;
+}
+int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, float* bh) {
+  APPO_LAUNCH(c, conv1_half_kernel, 1, 1024, 0, w, b, K, wh, bh);
   return APPO_OK;
 }
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,

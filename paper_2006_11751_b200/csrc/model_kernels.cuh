@@ -19,6 +19,7 @@ struct ObsSrc {
   uint64_t slot_bytes = 0, obs_off = 0, boot_off = 0;
   int T = 0, n_traj = 0;
   int64_t obs_dim = 0;
+  int n_slots = 0;  // slots in the region (max slot id + 1), 0 = unknown
 };
 
 struct SlotOffsets {
@@ -43,6 +44,8 @@ int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int6
                        const BiasOut& bias = BiasOut());
 // Column sums of contiguous bf16 [M][bias.N] into bias.out
 int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias);
+// fp16 conv1 weights + offset-corrected bias of a published copy (gemm.cu u8 path)
+int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, float* bh);
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
                   int64_t dst_ld, int cols);
 int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const float* h_in,
