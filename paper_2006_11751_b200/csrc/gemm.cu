@@ -53,7 +53,7 @@ struct GatherP {
   int nq;    // AG_U8: output rows (images x Ho)
   int tma;   // AG_U8 staging: 1 = tensor-map boxes (mapA / map2), 0 = bulk copies
 };
-enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3 };
+enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3, AG_U8W = 4 };
 constexpr int GATHER_THREADS = 128;  // NHWC gather warps (after the epilogue warps)
 constexpr int U8_GATHER_THREADS = 256;  // conv1 staging/convert warps: two per tile row
 
@@ -77,7 +77,8 @@ struct DgradP {
 };
 
 struct KParams {
-  CUtensorMap map2;  // AG_U8 from trajectory slots: the bootstrap-observation map
+  CUtensorMap map2;  // AG_U8 / AG_U8W image staging: observation map (4-D contiguous / 5-D slots)
+  CUtensorMap map3;  // ... and the bootstrap-observation map (slots)
   int M, N, K;
   int tiles_m, tiles_n, splits, kb_per_split, nkb;
   Epilogue epi;
@@ -410,11 +411,75 @@ __host__ __device__ constexpr int u8_stage_bytes(int C) {
           16 + 127) & ~127;
 }
 
+// One staging box (rows row0.. of every channel of image img) from the
+// observation maps: contiguous batch (4-D) or trajectory slots (5-D steps /
+// 4-D bootstrap observations), slot ids from the shared-memory cache.
+__device__ __forceinline__ void u8_box_load(const KParams& p, void* dst, uint64_t* bar, int img,
+                                            int row0, const int* sids) {
+  const GatherP& g = p.g;
+  if (!g.slot_ids) {
+    sm100::tma_load_4d_warp(dst, &p.map2, bar, 0, row0, 0, img);
+  } else {
+    const int B = g.n_traj * g.T;
+    const int si = img < B ? img / g.T : img - B;
+    const int sid = si < U8_SID_CACHE ? sids[si] : g.slot_ids[si];
+    if (img < B)
+      sm100::tma_load_5d_warp(dst, &p.map2, bar, 0, row0, 0, img % g.T, sid);
+    else
+      sm100::tma_load_4d_warp(dst, &p.map3, bar, 0, row0, 0, sid);
+  }
+}
+
+// conv1 weight gradient staging: K block kb = output rows (2*(kb % KPI),
+// +1) of image kb / KPI -> one box {W, 12 rows, C}.
+constexpr int U8W_ROWS = 2;                          // output rows per K block (x 32 = 64 pixels)
+constexpr int U8W_BOX_ROWS = 4 * (U8W_ROWS - 1) + 8;  // 12 input rows
+__device__ __forceinline__ void u8w_stage(const KParams& p, int kb, uint8_t* buf, uint64_t* bar,
+                                          const int* sids) {
+  const GatherP& g = p.g;
+  const int Ho = g.P / g.Wo;
+  const int kpi = (Ho + U8W_ROWS - 1) / U8W_ROWS;
+  const int img = kb / kpi, y0 = (kb - img * kpi) * U8W_ROWS;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of buf
+  sm100::mbar_arrive_expect_tx_warp(bar, g.Cin * U8W_BOX_ROWS * g.Wi);
+  u8_box_load(p, buf, bar, img, 4 * y0, sids);
+}
+
+// conv1 weight gradient B block (MN-major SW128, one 64-wide atom per channel):
+// K row = pixel (ky, x) of the K block, N = (c, kh, kw); exact bf16 of u8.
+// Thread gt < 64*C: row gt & 63, channel gt >> 6.
+__device__ __forceinline__ void u8w_convert(const GatherP& g, const uint8_t* buf, uint8_t* sB,
+                                            int gt) {
+  const int row = gt & 63, c = gt >> 6;
+  if (c >= g.Cin) return;
+  const int ky = row >> 5, x = row & 31;
+  const uint32_t src = sm100::smem_u32(buf) + (c * U8W_BOX_ROWS + 4 * ky) * g.Wi + 4 * x;
+  const uint32_t row_base = sm100::smem_u32(sB) + c * 8192 + row * 128;
+#pragma unroll
+  for (int kh = 0; kh < 8; ++kh) {
+    uint32_t lo, hi;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(src + kh * g.Wi));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(src + kh * g.Wi + 4));
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // exact u8 -> bf16 (2^23 + v trick, see u8_convert history)
+      const uint32_t word = q < 2 ? lo : hi;
+      const int k0 = (q & 1) * 2;
+      const float f0 = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0)) - 8388608.0f;
+      const float f1 = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7650 + k0 + 1)) - 8388608.0f;
+      w[q] = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632);
+    }
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row_base + ((kh ^ (row & 7)) << 4)),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
+  }
+}
+
 // Tensor-map staging (one TMA box {W, 20 rows, C} per run of consecutive
 // output rows of the same image: at most two per tile).  meta[k] = byte
 // offset of output row k's first input row (channel 0) in the slot; channel
 // planes are U8_BOX_ROWS * W apart.
-__device__ __forceinline__ void u8_stage_tma(const KParams& p, const CUtensorMap* mapA, int tile,
+__device__ __forceinline__ void u8_stage_tma(const KParams& p, int tile,
                                              uint8_t* buf, int* meta, uint64_t* bar, int lane,
                                              const int* sids, long long* pf = nullptr) {
   const GatherP& g = p.g;
@@ -437,17 +502,7 @@ __device__ __forceinline__ void u8_stage_tma(const KParams& p, const CUtensorMap
   for (int r = 0; r < (n0 < nrow ? 2 : 1); ++r) {
     const int img = r ? img0 + 1 : img0, y = r ? 0 : y0;
     uint8_t* dst = buf + r * box;
-    if (!g.slot_ids) {
-      sm100::tma_load_4d_warp(dst, mapA, bar, 0, 4 * y, 0, img);
-    } else {
-      const int B = g.n_traj * g.T;
-      const int si = img < B ? img / g.T : img - B;
-      const int sid = si < U8_SID_CACHE ? sids[si] : g.slot_ids[si];
-      if (img < B)
-        sm100::tma_load_5d_warp(dst, mapA, bar, 0, 4 * y, 0, img % g.T, sid);
-      else
-        sm100::tma_load_4d_warp(dst, &p.map2, bar, 0, 4 * y, 0, sid);
-    }
+    u8_box_load(p, dst, bar, img, 4 * y, sids);
   }
 }
 
@@ -572,7 +627,7 @@ __device__ __forceinline__ void dgrad_finish(const KParams& p, int64_t off,
 
 template <int AG>
 constexpr bool has_gather() {
-  return AG == AG_NHWC || AG == AG_U8;
+  return AG == AG_NHWC || AG == AG_U8 || AG == AG_U8W;
 }
 // Epilogue warps: 8 (two per TMEM lane quarter); 16 for the sub-pixel dgrad,
 // whose epilogue gathers its ELU' operand from HBM and needs more loads in flight.
@@ -582,12 +637,13 @@ constexpr int epi_warps() {
 }
 template <int AG>
 constexpr int gather_threads() {
-  return AG == AG_U8 ? U8_GATHER_THREADS : has_gather<AG>() ? GATHER_THREADS : 0;
+  return (AG == AG_U8 || AG == AG_U8W) ? U8_GATHER_THREADS : has_gather<AG>() ? GATHER_THREADS : 0;
 }
 template <int EV, int AG>
 constexpr int kernel_threads() {
   // conv1 adds U8_NSTG staging warps after the gatherers (input rows -> smem ring)
-  return 64 + 32 * epi_warps<EV>() + gather_threads<AG>() + (AG == AG_U8 ? 32 * U8_NSTG : 0);
+  return 64 + 32 * epi_warps<EV>() + gather_threads<AG>() +
+         ((AG == AG_U8 || AG == AG_U8W) ? 32 * U8_NSTG : 0);
 }
 
 // Lane l ends with the sum over all 32 lanes of v[l & 15] (recursive halving,
@@ -634,7 +690,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       sm100::mbar_init(&acc_full[s], 1);
       sm100::mbar_init(&acc_empty[s], epi_warps<EV>());
     }
-    if (AG == AG_U8) {  // conv1 input staging ring: full (tx) / empty (all gatherers)
+    if (AG == AG_U8 || AG == AG_U8W) {  // conv1 staging ring: full (tx) / empty (all gatherers)
       uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
       for (int s = 0; s < U8_NSTG; ++s) {
         sm100::mbar_init(&sfull[s], 1);
@@ -646,6 +702,15 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   if (warp == 1) {
     sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
     sm100::tmem_relinquish();
+  }
+  if (AG == AG_U8W) {
+    // conv1 wgrad: M = 32 output channels; A rows 64..127 (the second MN atom,
+    // never written by the TMA) must read as zero
+    for (int i = threadIdx.x; i < C::STAGES * 512; i += blockDim.x) {
+      uint4* z = reinterpret_cast<uint4*>(smem + (i >> 9) * C::STAGE_BYTES + 8192) + (i & 511);
+      *z = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -666,6 +731,20 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
 
         uint8_t* sA = smem + stage * C::STAGE_BYTES;
         uint8_t* sB = sA + A_TILE_BYTES;
+        if (AG == AG_U8W) {
+          // dz1^T (MN-major A) box {64 ch (32 real), 32 x, 2 rows} of K block kb;
+          // B (col1 rows) is built by the converter warps
+          const int Ho = p.g.P / p.g.Wo;
+          const int kpi = (Ho + U8W_ROWS - 1) / U8W_ROWS;
+          const int img = kb / kpi;
+          sm100::mbar_arrive_expect_tx_warp(&full[stage], 8192);
+          sm100::tma_load_4d_warp(sA, &mapA, &full[stage], 0, 0, (kb - img * kpi) * U8W_ROWS, img);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         sm100::mbar_arrive_expect_tx_warp(&full[stage],
                                           has_gather<AG>() ? C::B_TILE_BYTES : C::STAGE_BYTES);
         if (has_gather<AG>()) {
@@ -738,7 +817,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
         acc_phase ^= 1;
       }
     }
-  } else if (AG == AG_U8 && warp >= 2 + epi_warps<EV>() + gather_threads<AG>() / 32) {
+  } else if ((AG == AG_U8 || AG == AG_U8W) &&
+             warp >= 2 + epi_warps<EV>() + gather_threads<AG>() / 32) {
     // conv1 staging warps: warp w owns ring slot w and stages the CTA's units
     // j = w, w + U8_NSTG, ... (a TMA issue costs ~1000 cycles of the issuing
     // warp, so the slots are filled in parallel)
@@ -751,12 +831,26 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     __syncwarp();
     const int slot = warp - (2 + epi_warps<EV>() + gather_threads<AG>() / 32);
     uint32_t sphase = 0;
-    for (int u = blockIdx.x + slot * gridDim.x; u < units; u += U8_NSTG * gridDim.x) {
+    if constexpr (AG == AG_U8W) {
+      // work items = the CTA's K blocks in order; item j goes to slot j % U8_NSTG
+      int j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit un = decode_unit(p, u);
+        for (int kb = un.kb0; kb < un.kb1; ++kb, ++j) {
+          if (j % U8_NSTG != slot) continue;
+          sm100::mbar_wait(&sfull[U8_NSTG + slot], sphase ^ 1);
+          u8w_stage(p, kb, stg + slot * u8_stage_bytes(p.g.Cin), &sfull[slot], sids);
+          sphase ^= 1;
+        }
+      }
+    }
+    for (int u = blockIdx.x + slot * gridDim.x; AG == AG_U8 && u < units;
+         u += U8_NSTG * gridDim.x) {
       const Unit un = decode_unit(p, u);
       sm100::mbar_wait(&sfull[U8_NSTG + slot], sphase ^ 1);
       if (lane == 0) GEMM_PROF(0);
       if (p.g.tma)
-        u8_stage_tma(p, &mapA, un.tm, stg + slot * u8_stage_bytes(p.g.Cin), smeta + slot * U8_ROWS,
+        u8_stage_tma(p, un.tm, stg + slot * u8_stage_bytes(p.g.Cin), smeta + slot * U8_ROWS,
                      &sfull[slot], lane, sids,
                      (p.prof && blockIdx.x == 0 && u / (int)gridDim.x < 16)
                          ? p.prof + (u / gridDim.x) * 16 : nullptr);
@@ -782,6 +876,33 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     }
     int stage = 0;
     uint32_t phase = 0;
+    if constexpr (AG == AG_U8W) {
+      // one staged box per K block -> the B (col1) block of that stage
+      uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES + 256;
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+      uint64_t* sempty = sfull + U8_NSTG;
+      int slot = 0;
+      uint32_t sphase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit un = decode_unit(p, u);
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+          sm100::mbar_wait(&sfull[slot], sphase);
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          u8w_convert(p.g, stg + slot * u8_stage_bytes(p.g.Cin),
+                      smem + stage * C::STAGE_BYTES + A_TILE_BYTES, gt);
+          sm100::mbar_arrive(&full[stage]);
+          sm100::mbar_arrive(&sempty[slot]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++slot == U8_NSTG) {
+            slot = 0;
+            sphase ^= 1;
+          }
+        }
+      }
+    }
     if constexpr (AG == AG_U8) {
       // staged input ring (filled by the producer warp): wait slot -> convert
       // the tile channel by channel -> release the slot
@@ -976,6 +1097,47 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Few splits, many outputs (GRU / FC weight gradients): one thread per 4
+// consecutive outputs, splits summed in order (deterministic).
+__global__ void __launch_bounds__(256)
+    splitk_reduce4_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
+  const int64_t total = (int64_t)M * N;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= total) return;
+  float4 s = __ldg(reinterpret_cast<const float4*>(partial + i));
+  for (int z = 1; z < splits; ++z) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(partial + (size_t)z * total + i));
+    s.x += v.x;
+    s.y += v.y;
+    s.z += v.z;
+    s.w += v.w;
+  }
+  const float t[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int m = (int)((i + k) / N), n = (int)((i + k) % N);
+    float x = t[k] * e.scale;
+    if (e.flags & EPI_BIAS) x += e.bias[n];
+    const size_t o = (e.flags & EPI_TRANS) ? (size_t)n * e.ldo + m : (size_t)m * e.ldo + n;
+    float* dst = reinterpret_cast<float*>(e.out) + o;
+    *dst = (e.flags & EPI_ACCUM) ? *dst + x : x;
+  }
+}
+
+int launch_splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial,
+                         const Epilogue& epi) {
+  const int64_t total = (int64_t)M * N;
+  c->next_bytes = (double)splits * total * 4 + (double)total * 4;
+  if (splits <= 16 && total % 4 == 0) {
+    APPO_LAUNCH(c, splitk_reduce4_kernel, (int)((total / 4 + 255) / 256), 256, 0, M, N, splits,
+                partial, epi);
+  } else {
+    APPO_LAUNCH(c, splitk_reduce_kernel, (int)((total + 31) / 32), 256, 0, M, N, splits, partial,
+                epi);
+  }
+  return APPO_OK;
+}
+
 // ---- host side: tensor maps ----------------------------------------------------
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1053,7 +1215,8 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EV, AG>;
   // conv1: input staging ring after the barriers (+16 B overread slack)
   const int smem_bytes =
-      C::SMEM_BYTES + (AG == AG_U8 ? U8_NSTG * u8_stage_bytes(p.g.Cin) + 64 : 0);
+      C::SMEM_BYTES +
+      ((AG == AG_U8 || AG == AG_U8W) ? U8_NSTG * u8_stage_bytes(p.g.Cin) + 64 : 0);
   constexpr int kThreads = kernel_threads<EV, AG>();
   static int attr_bytes[64] = {};
   int dev = c->device & 63;
@@ -1209,12 +1372,29 @@ int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
   }
   if (st) return st;
   if (p.splits > 1) {
-    const int64_t total = (int64_t)M * N;
-    const int grid = (int)((total + 31) / 32);
-    c->next_bytes = (double)p.splits * total * 4 + (double)total * 4;
-    APPO_LAUNCH(c, splitk_reduce_kernel, grid, 256, 0, M, N, p.splits, p.partial, epi);
+    return launch_splitk_reduce(c, M, N, p.splits, p.partial, epi);
   }
   return APPO_OK;
+}
+
+// Image staging maps (p.map2 observations, p.map3 bootstrap observations) with
+// boxes of box_rows input rows x all channels; false if the images are not
+// 16-byte aligned (then the bulk-copy path is used).
+bool make_image_maps(KParams& p, const ConvIn& in, int box_rows) {
+  const uint64_t W = in.Wi, H = in.Hi, C = in.Cin, plane = W * H, od = plane * C;
+  const uint32_t box[5] = {(uint32_t)W, (uint32_t)box_rows, (uint32_t)C, 1, 1};
+  if (!in.slot_ids) {
+    const uint64_t dims[4] = {W, H, C, (uint64_t)in.n_img};
+    const uint64_t str[3] = {W, plane, (uint64_t)in.img_stride};
+    return make_tmap_u8(&p.map2, in.src, 4, dims, str, box) == APPO_OK;
+  }
+  if (in.n_slots <= 0) return false;
+  const uint64_t dims[5] = {W, H, C, (uint64_t)in.T, (uint64_t)in.n_slots};
+  const uint64_t str[4] = {W, plane, od, in.slot_bytes};
+  const uint64_t bdims[4] = {W, H, C, (uint64_t)in.n_slots};
+  const uint64_t bstr[3] = {W, plane, in.slot_bytes};
+  return make_tmap_u8(&p.map2, in.src + in.obs_off, 5, dims, str, box) == APPO_OK &&
+         make_tmap_u8(&p.map3, in.src + in.boot_off, 4, bdims, bstr, box) == APPO_OK;
 }
 
 int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
@@ -1232,8 +1412,7 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
                           in.obs_off % 8 == 0 && in.boot_off % 8 == 0 && in.Cin <= 4),
                APPO_ERR_CONTRACT,
                "conv_implicit u8: k8 s4, W % 16 == 0, W <= 128, C <= 4, 8-byte aligned images");
-  CUtensorMap mb, mb_u8;
-  std::memset(&mb_u8, 0, sizeof(mb_u8));
+  CUtensorMap mb;
   int st = make_map(&mb, W.ptr, K, N, W.ld, bn);
   if (st) return st;
   KParams p{};
@@ -1254,29 +1433,14 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
     // tiles of U8_ROWS output rows x 32 columns (see u8_stage_tma)
     p.tiles_m = (p.g.nq + U8_ROWS - 1) / U8_ROWS;
     // staging by tensor-map boxes when the images are 16-byte aligned, else bulk copies
-    const uint64_t W = in.Wi, H = in.Hi, C = in.Cin, plane = W * H, od = plane * C;
-    const uint32_t box[5] = {(uint32_t)W, (uint32_t)U8_BOX_ROWS, (uint32_t)C, 1, 1};
-    p.g.tma = 0;
-    if (!in.slot_ids) {
-      const uint64_t dims[4] = {W, H, C, (uint64_t)in.n_img};
-      const uint64_t str[3] = {W, plane, (uint64_t)in.img_stride};
-      if (make_tmap_u8(&mb_u8, in.src, 4, dims, str, box) == APPO_OK) p.g.tma = 1;
-    } else if (in.n_slots > 0) {
-      const uint64_t dims[5] = {W, H, C, (uint64_t)in.T, (uint64_t)in.n_slots};
-      const uint64_t str[4] = {W, plane, od, in.slot_bytes};
-      const uint64_t bdims[4] = {W, H, C, (uint64_t)in.n_slots};
-      const uint64_t bstr[3] = {W, plane, in.slot_bytes};
-      if (make_tmap_u8(&mb_u8, in.src + in.obs_off, 5, dims, str, box) == APPO_OK &&
-          make_tmap_u8(&p.map2, in.src + in.boot_off, 4, bdims, bstr, box) == APPO_OK)
-        p.g.tma = 1;
-    }
+    p.g.tma = make_image_maps(p, in, U8_BOX_ROWS) ? 1 : 0;
 
     static long long* prof = nullptr;
     if (getenv("APPO_GEMM_PROF")) {
       if (!prof) cudaMalloc(&prof, sizeof(long long) * 256);
       cudaMemsetAsync(prof, 0, sizeof(long long) * 256, c->stream);
       p.prof = prof;
-      st = launch_conv<32, AG_U8>(c, mb_u8, mb, p);
+      st = launch_conv<32, AG_U8>(c, mb, mb, p);
       long long h[256];
       cudaStreamSynchronize(c->stream);
       cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
@@ -1289,7 +1453,7 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
       return st;
     }
     switch (bn) {
-      case 32: return launch_conv<32, AG_U8>(c, mb_u8, mb, p);
+      case 32: return launch_conv<32, AG_U8>(c, mb, mb, p);
       default: return APPO_ERR_CONTRACT;
     }
   }
@@ -1321,6 +1485,61 @@ int make_map_nhwc(CUtensorMap* map, const void* ptr, int n, int h, int w, int c,
     return APPO_ERR_CONTRACT;
   }
   return APPO_OK;
+}
+
+// conv1 weight gradient without col1: dW[co][(c,kh,kw)] = scale * sum over
+// pixels of dz1[pixel][co] * obs window[pixel][(c,kh,kw)], K split across the
+// CTAs, deterministic split reduce.  Returns APPO_ERR_CONTRACT when the images
+// cannot be staged by TMA (caller falls back to im2col + GEMM).
+int conv1_wgrad_implicit(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* dw, float scale) {
+  const int Ho = in.Ho, Wo = in.Wo, Cout = 32;
+  APPO_REQUIRE(in.u8 && in.ksz == 8 && in.s == 4 && in.Wo <= 32 && in.Cin <= 3 && in.Wi <= 128,
+               APPO_ERR_CONTRACT, "conv1_wgrad: unsupported geometry");
+  KParams p{};
+  p.g = GatherP{in.src, in.img_stride, Ho * Wo, Wo, in.Hi, in.Wi, in.Cin, in.ksz, in.s,
+                in.slot_ids, in.slot_bytes, in.obs_off, in.boot_off, in.T, in.n_traj,
+                in.n_img * Ho};
+  if (!make_image_maps(p, in, U8W_BOX_ROWS)) return APPO_ERR_CONTRACT;
+  p.g.tma = 1;
+  // A = dz1^T: 4-D map over dz1 [img][Ho][Wo][32] bf16, box {64 ch (32 real), 32 x, 2 rows, 1}
+  CUtensorMap ma, mb;
+  {
+    EncodeTiledFn enc = get_encode();
+    APPO_REQUIRE(enc != nullptr, APPO_ERR_RESOURCE, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[4] = {(cuuint64_t)Cout, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)in.n_img};
+    cuuint64_t str[3] = {(cuuint64_t)Cout * 2, (cuuint64_t)Wo * Cout * 2,
+                         (cuuint64_t)Ho * Wo * Cout * 2};
+    cuuint32_t box[4] = {64u, 32u, (cuuint32_t)U8W_ROWS, 1u};
+    cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+    CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(dz1), dims, str,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    APPO_REQUIRE(r == CUDA_SUCCESS, APPO_ERR_CONTRACT, "conv1_wgrad: dz1 tensor map");
+    mb = ma;  // unused (B is gathered)
+  }
+  const int N = in.Cin * 64;
+  const int kpi = (Ho + U8W_ROWS - 1) / U8W_ROWS;
+  p.M = Cout;
+  p.N = N;
+  p.K = in.n_img * kpi * 64;
+  p.tiles_m = 1;
+  p.tiles_n = 1;
+  p.nkb = in.n_img * kpi;
+  int splits = c->num_sms;
+  if (splits > p.nkb) splits = p.nkb;
+  p.kb_per_split = (p.nkb + splits - 1) / splits;
+  p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
+  APPO_REQUIRE(N == 192, APPO_ERR_CONTRACT, "conv1_wgrad: 3 input channels expected");
+  int st = gemm_workspace(c, (size_t)p.splits * Cout * N * sizeof(float), &p.partial);
+  if (st) return st;
+  p.epi.flags = 0;
+  st = launch_gemm<192, true, true, EV_SPLIT, AG_U8W>(c, ma, mb, p);
+  if (st) return st;
+  Epilogue e;
+  e.scale = scale;
+  e.out = dw;
+  e.ldo = N;
+  return launch_splitk_reduce(c, Cout, N, p.splits, p.partial, e);
 }
 
 int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,

@@ -90,6 +90,12 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
                       uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
                       uint32_t b2);
 
+// conv1 weight gradient straight from the u8 images (no im2col):
+// dw[co][(c,kh,kw)] = scale * sum_pixels dz1[pixel][co] * obs window; in
+// describes the images exactly as for the forward.  APPO_ERR_CONTRACT when the
+// images are not TMA-stageable (16-byte alignment).
+int conv1_wgrad_implicit(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* dw, float scale);
+
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);
 

@@ -284,6 +284,24 @@ int splits_for(Ctx* c, int M, int N, int bn, int K) {
 // their A operand on the fly (inference: no im2col traffic); otherwise the
 // im2col matrices are materialised because the learner's weight gradients
 // consume them.
+// conv1 input description (u8 images, contiguous batch or trajectory slots)
+ConvIn conv1_in(const ObsSrc& src, int R, const Dims& d) {
+  ConvIn in;
+  in.src = src.base;
+  in.img_stride = src.img_stride;
+  in.slot_ids = src.slot_ids;
+  in.slot_bytes = src.slot_bytes;
+  in.obs_off = src.obs_off;
+  in.boot_off = src.boot_off;
+  in.T = src.T;
+  in.n_traj = src.n_traj;
+  in.n_slots = src.n_slots;
+  in.n_img = R;
+  in.Hi = d.H; in.Wi = d.W; in.Cin = d.C; in.ksz = 8; in.s = 4; in.Ho = d.H1; in.Wo = d.W1;
+  in.u8 = true;
+  return in;
+}
+
 int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, const uint16_t* wb,
                     const float* pf, int pub, bool implicit) {
   const Dims& d = M->d;
@@ -295,25 +313,10 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   e.bias = M->pub_c1b[pub];
   e.out = s.a1;
   e.ldo = 32;
-  {
-    // conv1 always gathers its input from the u8 images (smem-staged implicit
-    // GEMM); the learner additionally materialises col1 for the weight gradient
-    ConvIn in;
-    in.src = src.base;
-    in.img_stride = src.img_stride;
-    in.slot_ids = src.slot_ids;
-    in.slot_bytes = src.slot_bytes;
-    in.obs_off = src.obs_off;
-    in.boot_off = src.boot_off;
-    in.T = src.T;
-    in.n_traj = src.n_traj;
-    in.n_slots = src.n_slots;
-    in.n_img = R;
-    in.Hi = d.H; in.Wi = d.W; in.Cin = d.C; in.ksz = 8; in.s = 4; in.Ho = d.H1; in.Wo = d.W1;
-    in.u8 = true;
-    TRY(conv_implicit_bf16(c, in, 32, Operand{M->pub_c1h[pub], d.K1, false}, e, 32));
-    if (!implicit) TRY(k_im2col_u8(c, src, R, d, s.col1));
-  }
+  // conv1 gathers its input from the u8 images (smem-staged implicit GEMM);
+  // so does its weight gradient in the learner (conv1_wgrad_implicit)
+  TRY(conv_implicit_bf16(c, conv1_in(src, R, d), 32, Operand{M->pub_c1h[pub], d.K1, false}, e,
+                         32));
   e.scale = 1.0f;
   e.bias = pf + d.off_c2b;
   e.out = s.a2;
@@ -811,16 +814,24 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     in.bias = bias_out(3, G + d.off_c1b, 32);
     TRY(conv_dgrad_s2_bf16(ctx, in));
   }
-  // ---- conv1 weight gradient (input is data) ----
+  // ---- conv1 weight gradient (input is data): straight from the u8 images;
+  //      im2col + GEMM only when the images cannot be TMA-staged ----
   {
-    const int M1 = B * d.P1;
-    Epilogue e;
-    e.scale = 1.0f / 255.0f;
-    e.out = G + d.off_c1w;
-    e.ldo = d.K1;
-    TRY(gemm_bf16(ctx, 32, d.K1, M1, Operand{s.dz1, 32, true}, Operand{s.col1, d.K1, true}, e,
-                  d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64,
-                  splits_for(ctx, 32, d.K1, d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64, M1)));
+    const int wst = conv1_wgrad_implicit(ctx, conv1_in(src, B, d), s.dz1, G + d.off_c1w,
+                                         1.0f / 255.0f);
+    if (wst == APPO_ERR_CONTRACT) {
+      const int M1 = B * d.P1;
+      TRY(k_im2col_u8(ctx, src, B, d, s.col1));
+      Epilogue e;
+      e.scale = 1.0f / 255.0f;
+      e.out = G + d.off_c1w;
+      e.ldo = d.K1;
+      TRY(gemm_bf16(ctx, 32, d.K1, M1, Operand{s.dz1, 32, true}, Operand{s.col1, d.K1, true}, e,
+                    d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64,
+                    splits_for(ctx, 32, d.K1, d.K1 % 64 == 0 && d.K1 <= 256 ? d.K1 : 64, M1)));
+    } else if (wst != APPO_OK) {
+      return wst;
+    }
   }
 
   // ---- data-parallel: average the gradient over ranks before clip + Adam ----

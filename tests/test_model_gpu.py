@@ -143,6 +143,36 @@ def test_learner_step_matches_oracle(oracle, adv_source, normalize):
     assert out["lag_max"] == 0.0 and abs(out["lag_mean"] + 1.5) < 1e-9
 
 
+def test_learner_step_matches_oracle_T32_slot_order(oracle):
+    # the bench layout (T=32, 16-byte aligned bootstrap obs): conv1 and its weight
+    # gradient stage the u8 images straight from the slots by TMA (no im2col);
+    # FIFO order != slot order exercises the slot-id indirection
+    desc = appo.ModelDesc.doom(T=32)
+    ctx = appo.Context(0, seed=13, model=desc)
+    store = appo.TrajectoryStore(desc, 3)
+    rs = np.random.default_rng(21)
+    d = fill_store(store, 3, rs, 6)
+    order = [2, 0]
+    th0, _ = ctx.get_params()
+    hp = appo.HParams.defaults(gamma=0.99)
+    out = ctx.learner_step(store.region, store.slot_bytes, order, hp)
+    g = ctx.grad()
+    sel = {k: v[order] for k, v in d.items()}
+    ref = oracle.learner_step((3, 72, 128, 6), th0.astype(np.float64), np.zeros(th0.size),
+                              np.zeros(th0.size), 0, sel["obs"], sel["h0"].astype(np.float64),
+                              sel["actions"].reshape(-1),
+                              sel["blogp"].reshape(-1).astype(np.float64),
+                              sel["rewards"].reshape(-1).astype(np.float64),
+                              sel["dones"].reshape(-1), hp=dict(gamma=0.99), do_adam=False)
+    assert ref["status"] == 0
+    st = ref["stats"]
+    assert abs(out["total_loss"] - st[3]) <= 2e-2 * abs(st[3]) + 1e-4
+    gr = ref["grad"]
+    for name, (a, b) in block_offsets(ctx).items():
+        e = rel_l2(g[a:b].astype(np.float64), gr[a:b])
+        assert e <= 6e-2, (name, e)
+
+
 def block_offsets(ctx):
     C_, H, W, A = ctx.model.shape
     H1, W1 = (H - 8) // 4 + 1, (W - 8) // 4 + 1
