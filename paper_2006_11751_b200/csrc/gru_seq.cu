@@ -76,8 +76,9 @@ __device__ __forceinline__ uint32_t sw128(int rows, int r, int kb, int c) {
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(counter, 1u);
+    // release-add (cumulative over the CTA's writes ordered by the bar.sync)
+    // instead of a full fence + relaxed atomic
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");

@@ -436,6 +436,8 @@ int model_create(Ctx* c) {
     APPO_CUDA_TRY(cudaMalloc(&M->pub_f32[k], P * 4));
     APPO_CUDA_TRY(cudaMalloc(&M->pub_c1h[k], (size_t)32 * M->d.K1 * 2));
     APPO_CUDA_TRY(cudaMalloc(&M->pub_c1b[k], 32 * 4));
+    APPO_CUDA_TRY(cudaMalloc(&M->pub_wt2[k], (size_t)4 * 32 * 256 * 2));
+    APPO_CUDA_TRY(cudaMalloc(&M->pub_wt3[k], (size_t)4 * 64 * 512 * 2));
     APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->pub_ev[k], cudaEventDisableTiming));
     APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->ready_ev[k], cudaEventDisableTiming));
   }
@@ -460,6 +462,8 @@ void model_destroy(Ctx* c) {
     cudaFree(M->pub_f32[k]);
     cudaFree(M->pub_c1h[k]);
     cudaFree(M->pub_c1b[k]);
+    cudaFree(M->pub_wt2[k]);
+    cudaFree(M->pub_wt3[k]);
     if (M->pub_ev[k]) cudaEventDestroy(M->pub_ev[k]);
     if (M->ready_ev[k]) cudaEventDestroy(M->ready_ev[k]);
   }
@@ -516,8 +520,8 @@ int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version) {
     APPO_CUDA_TRY(cudaMemcpy(M->pub_bf16[k], bf.data(), P * 2, cudaMemcpyHostToDevice));
   }
   for (int k = 0; k < Model::kPub; ++k)
-    TRY(k_conv1_half(ctx, M->pub_f32[k] + M->d.off_c1w, M->pub_f32[k] + M->d.off_c1b, M->d.K1,
-                     M->pub_c1h[k], M->pub_c1b[k]));
+    TRY(k_publish_derived(ctx, M->pub_bf16[k], M->pub_f32[k], M->d, M->pub_c1h[k], M->pub_c1b[k],
+                          M->pub_wt2[k], M->pub_wt3[k]));
   APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   M->version = version;
   M->adam_t = 0;
@@ -658,10 +662,9 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     TRY(k_gru_train(ctx, n_traj, T, t, s.gi, s.gh, s.done, s.hcur, s.core, s.core_bf, s.gates));
   }
   TRY(k_heads_fwd(ctx, R, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
-                  th + d.off_bv, s.logits, s.values));
+                  th + d.off_bv, s.logits, s.values, B, s.act, s.tlogp, s.ent));
 
   // ---- targets: logp/entropy, V-trace, advantages ----
-  TRY(launch_logp_entropy(ctx, B, d.A, s.logits, s.act, s.tlogp, s.ent));
   TRY(launch_vtrace(ctx, n_traj, T, s.rew, s.values, s.values + B, s.tlogp, s.blogp, s.done,
                     hp->gamma, hp->rho_bar, hp->c_bar, s.vt, s.pg, nullptr, nullptr));
   const float* adv = s.pg;
@@ -679,8 +682,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   // ---- loss and its gradient wrt logits / value ----
   LossHP lh{hp->clip_low, hp->clip_high, hp->value_coef, hp->entropy_coef};
   TRY(k_ppo_loss(ctx, B, d.A, s.logits, s.values, s.act, s.blogp, adv, s.vt, lh, s.dlog,
-                 s.dhead, s.stats));
-  TRY(k_lag(ctx, B, s.ver, M->version, s.stats));
+                 s.dhead, s.stats, s.ver, M->version));
 
   float* G = M->grad;
   APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
@@ -700,9 +702,6 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
                             G + d.off_bv));
   }
 
-  // sub-pixel dgrad operands of conv2 / conv3 for this step's weights
-  TRY(k_dgrad_weights(ctx, wb + d.off_c3w, 128, 3, 64, s.wt3));
-  TRY(k_dgrad_weights(ctx, wb + d.off_c2w, 64, 4, 32, s.wt2));
 
   // bias gradients of fc / conv layers, fused into the kernels producing /
   // reading their dz (deterministic fixed-point sums, model_kernels.cu)
@@ -787,7 +786,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     // dz2 = ELU'(a2) * conv3^T(dz3): sub-pixel implicit GEMM (+ conv2 bias grad)
     DgradIn in;
     in.dz_next = s.dz3;
-    in.wt = s.wt3;
+    in.wt = M->pub_wt3[pub];
     in.aprev = s.a2;
     in.dz = s.dz2;
     in.n_img = B;
@@ -806,7 +805,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     // dz1 = ELU'(a1) * conv2^T(dz2) (+ conv1 bias grad)
     DgradIn in;
     in.dz_next = s.dz2;
-    in.wt = s.wt2;
+    in.wt = M->pub_wt2[pub];
     in.aprev = s.a1;
     in.dz = s.dz1;
     in.n_img = B;
@@ -847,8 +846,8 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
                   M->pub_f32[next], ctx->d_counter + 6));
   APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
   APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
-  TRY(k_conv1_half(ctx, M->pub_f32[next] + d.off_c1w, M->pub_f32[next] + d.off_c1b, d.K1,
-                   M->pub_c1h[next], M->pub_c1b[next]));
+  TRY(k_publish_derived(ctx, M->pub_bf16[next], M->pub_f32[next], d, M->pub_c1h[next],
+                        M->pub_c1b[next], M->pub_wt2[next], M->pub_wt3[next]));
   APPO_CUDA_TRY(cudaEventRecord(M->ready_ev[next], st));
   M->last_ring = ring;
   // Optimistic publish: the Adam kernel always rewrites pub[next] (with the

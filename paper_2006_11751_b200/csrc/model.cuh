@@ -81,6 +81,9 @@ struct Model {
   // with the fp16-input offset removed (b - 1024/255 * sum_k W), see gemm.cu
   uint16_t* pub_c1h[kPub] = {};
   float* pub_c1b[kPub] = {};
+  // sub-pixel dgrad operands of conv2 / conv3 (k_dgrad_weights layout)
+  uint16_t* pub_wt2[kPub] = {};
+  uint16_t* pub_wt3[kPub] = {};
   cudaEvent_t pub_ev[kPub] = {};    // recorded after the last inference read of pub[k]
   cudaEvent_t ready_ev[kPub] = {};  // recorded after the Adam step that wrote pub[k]
   int64_t pub_version[kPub] = {};   // parameter version held by pub[k]

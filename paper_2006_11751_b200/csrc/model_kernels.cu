@@ -247,6 +247,46 @@ __global__ void dgrad_weights_kernel(const uint16_t* __restrict__ w, int Co, int
   }
 }
 
+// Operands derived from a published copy in ONE launch (after the Adam step
+// that wrote it): blocks 0..nb-2 rearrange the conv3 / conv2 weights for the
+// sub-pixel dgrad (k_dgrad_weights layout), the last block writes the conv1
+// fp16 weights and offset-corrected bias (conv1_half_kernel).
+__global__ void __launch_bounds__(256)
+    publish_derived_kernel(const uint16_t* __restrict__ wb, const float* __restrict__ pf,
+                           int64_t off_c1w, int64_t off_c1b, int K1, int64_t off_c2w,
+                           int64_t off_c3w, uint16_t* __restrict__ c1h, float* __restrict__ c1b,
+                           uint16_t* __restrict__ wt2, uint16_t* __restrict__ wt3) {
+  if (blockIdx.x == gridDim.x - 1) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int co = warp; co < 32; co += blockDim.x >> 5) {
+      float acc = 0.0f;
+      for (int k = lane; k < K1; k += 32) {
+        const __half h = __float2half_rn(pf[off_c1w + (size_t)co * K1 + k]);
+        c1h[(size_t)co * K1 + k] = __half_as_ushort(h);
+        acc += __half2float(h);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) c1b[co] = pf[off_c1b + co] - (1024.0f / 255.0f) * acc;
+    }
+    return;
+  }
+  // wt3: Co=128, k=3, Ci=64 (4*64*512 elements); wt2: Co=64, k=4, Ci=32 (4*32*256)
+  const int n3 = 4 * 64 * 512, n2 = 4 * 32 * 256;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n3 + n2;
+       g += (gridDim.x - 1) * blockDim.x) {
+    const bool is3 = g < n3;
+    const int e = is3 ? g : g - n3;
+    const int Co = is3 ? 128 : 64, k = is3 ? 3 : 4, Ci = is3 ? 64 : 32;
+    const int kmax = 4 * Co;
+    const int kk = e % kmax, ci = (e / kmax) % Ci, cls = e / (kmax * Ci);
+    const int tap = kk / Co, co = kk % Co;
+    const int kh = (cls >> 1) + 2 * (tap >> 1), kw = (cls & 1) + 2 * (tap & 1);
+    const uint16_t* w = wb + (is3 ? off_c3w : off_c2w);
+    const uint16_t v = (kh < k && kw < k) ? w[(((size_t)co * k + kh) * k + kw) * Ci + ci] : (uint16_t)0;
+    (is3 ? wt3 : wt2)[e] = v;
+  }
+}
+
 // conv1 fp16 operands of a published parameter copy (one block, warp per
 // output channel): wh = fp16(W), bias' = b - (1024/255) * sum_k wh (the conv1
 // GEMM multiplies fp16 (1024 + pixel) inputs, gemm.cu u8_convert).
@@ -376,11 +416,16 @@ __global__ void gru_train_kernel(int n_traj, int T, int t, const float* __restri
 }
 
 // Heads forward: one warp per row.
+// Heads forward, warp per row; rows < B also get the target log-probability of
+// the stored action and the policy entropy (log_prob_and_entropy,
+// policy.hpp:262-281, learner use orchestrator.hpp:803-814) in fp64.
 __global__ void __launch_bounds__(256)
     heads_fwd_kernel(int64_t R, int A, const float* __restrict__ core,
                      const float* __restrict__ wpi, const float* __restrict__ bpi,
                      const float* __restrict__ wv, const float* __restrict__ bv,
-                     float* __restrict__ logits, float* __restrict__ values) {
+                     float* __restrict__ logits, float* __restrict__ values, int64_t B,
+                     const int32_t* __restrict__ act, float* __restrict__ tlogp,
+                     float* __restrict__ ent, int* flags) {
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
@@ -398,8 +443,31 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int a = 0; a <= kMaxActions; ++a) acc[a] = warp_sum(acc[a]);
   if (lane == 0) {
-    for (int a = 0; a < A; ++a) logits[row * A + a] = acc[a] + bpi[a];
+    float lg[kMaxActions];
+    for (int a = 0; a < A; ++a) {
+      lg[a] = acc[a] + bpi[a];
+      logits[row * A + a] = lg[a];
+    }
     values[row] = acc[kMaxActions] + bv[0];
+    if (act && row < B) {
+      const int ac = act[row];
+      if (ac < 0 || ac >= A) {
+        atomicOr(flags + kFlagContract, 1);
+        return;
+      }
+      double mx = lg[0];
+      for (int a = 1; a < A; ++a) mx = fmax(mx, (double)lg[a]);
+      double z = 0;
+      for (int a = 0; a < A; ++a) z += exp((double)lg[a] - mx);
+      double h = 0;
+      for (int a = 0; a < A; ++a) {
+        const double pr = exp((double)lg[a] - mx) / z;
+        if (pr > 0) h -= pr * log(pr);
+      }
+      const double pa = exp((double)lg[ac] - mx) / z;
+      tlogp[row] = (float)log(fmax(pa, 1e-300));
+      ent[row] = (float)h;
+    }
   }
 }
 
@@ -469,9 +537,10 @@ __global__ void __launch_bounds__(256)
                     const float* __restrict__ blogp, const float* __restrict__ adv,
                     const float* __restrict__ vt, LossHP hp, float* __restrict__ dlog,
                     uint16_t* __restrict__ dhead, double* partials, unsigned* counter,
-                    double* stats, int* flags) {
+                    double* stats, int* flags, const int64_t* __restrict__ ver, int64_t cur) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  double acc[4] = {0, 0, 0, 0};
+  // policy, value, entropy, ratio sums; version-lag sum and max (orchestrator.hpp:790,862-863)
+  double acc[6] = {0, 0, 0, 0, 0, -1e300};
   if (s < B) {
     const float* lg = logits + (int64_t)s * A;
     const int a_s = act[s];
@@ -512,21 +581,25 @@ __global__ void __launch_bounds__(256)
     acc[1] = verr * verr;
     acc[2] = H;
     acc[3] = ratio;
+    acc[4] = (double)(cur - ver[s]);
+    acc[5] = (double)(cur - ver[s]);
   }
   // block reduce + last block
-  __shared__ double sh[8][4];
+  __shared__ double sh[8][6];
   __shared__ bool last;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) acc[k] = warp_sum(acc[k]);
+  for (int k = 0; k < 5; ++k) acc[k] = warp_sum(acc[k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc[5] = fmax(acc[5], __shfl_xor_sync(0xffffffffu, acc[5], o));
   if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) sh[threadIdx.x >> 5][k] = acc[k];
+    for (int k = 0; k < 6; ++k) sh[threadIdx.x >> 5][k] = acc[k];
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int k = 0; k < 4; ++k) {
-      double t = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w][k];
-      partials[blockIdx.x * 4 + k] = t;
+    for (int k = 0; k < 6; ++k) {
+      double t = k == 5 ? -1e300 : 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = k == 5 ? fmax(t, sh[w][k]) : t + sh[w][k];
+      partials[blockIdx.x * 6 + k] = t;
     }
     __threadfence();
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
@@ -534,15 +607,20 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence();
-    double t[4] = {0, 0, 0, 0};
+    double t[6] = {0, 0, 0, 0, 0, -1e300};
     for (unsigned b = 0; b < gridDim.x; ++b)
-      for (int k = 0; k < 4; ++k) t[k] += ((volatile double*)partials)[b * 4 + k];
+      for (int k = 0; k < 6; ++k) {
+        const double x = ((volatile double*)partials)[b * 6 + k];
+        t[k] = k == 5 ? fmax(t[k], x) : t[k] + x;
+      }
     const double invB = 1.0 / B;
     stats[0] = t[0] * invB;
     stats[1] = hp.value_coef * t[1] * invB;
     stats[2] = t[2] * invB;
     stats[3] = stats[0] + stats[1] - hp.entropy_coef * stats[2];
     stats[4] = t[3] * invB;
+    stats[6] = B > 0 ? t[4] * invB : 0.0;
+    stats[7] = B > 0 ? t[5] : 0.0;
     if (!isfinite(stats[3])) atomicOr(flags + kFlagNumeric, 1);
     *counter = 0;
   }
@@ -729,6 +807,12 @@ int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* 
   APPO_LAUNCH(c, dgrad_weights_kernel, grid_for(16 * Ci * Co, 256, 64), 256, 0, w, Co, k, Ci, wt);
   return APPO_OK;
 }
+int k_publish_derived(Ctx* c, const uint16_t* wb, const float* pf, const Dims& d, uint16_t* c1h,
+                      float* c1b, uint16_t* wt2, uint16_t* wt3) {
+  APPO_LAUNCH(c, publish_derived_kernel, 97, 256, 0, wb, pf, d.off_c1w, d.off_c1b, d.K1, d.off_c2w,
+              d.off_c3w, c1h, c1b, wt2, wt3);
+  return APPO_OK;
+}
 int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, float* bh) {
   APPO_LAUNCH(c, conv1_half_kernel, 1, 1024, 0, w, b, K, wh, bh);
   return APPO_OK;
@@ -759,9 +843,10 @@ int k_gru_train(Ctx* c, int n_traj, int T, int t, const float* gi, const float* 
   return APPO_OK;
 }
 int k_heads_fwd(Ctx* c, int64_t R, int A, const float* core, const float* wpi, const float* bpi,
-                const float* wv, const float* bv, float* logits, float* values) {
+                const float* wv, const float* bv, float* logits, float* values, int64_t B,
+                const int32_t* act, float* tlogp, float* ent) {
   APPO_LAUNCH(c, heads_fwd_kernel, (int)((R + 7) / 8), 256, 0, R, A, core, wpi, bpi, wv, bv,
-              logits, values);
+              logits, values, B, act, tlogp, ent, c->d_flags);
   return APPO_OK;
 }
 int k_gather_slots(Ctx* c, int n_traj, int T, const uint8_t* region, uint64_t slot_bytes,
@@ -777,10 +862,12 @@ int k_normalize(Ctx* c, int n, float* adv) {
 }
 int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
                const int32_t* act, const float* blogp, const float* adv, const float* vt,
-               const LossHP& hp, float* dlog, uint16_t* dhead, double* stats) {
+               const LossHP& hp, float* dlog, uint16_t* dhead, double* stats, const int64_t* ver,
+               int64_t cur) {
   const int grid = (B + 255) / 256;
+  APPO_REQUIRE(grid * 6 <= kRedSlots, APPO_ERR_CONTRACT, "ppo_loss: batch too large");
   APPO_LAUNCH(c, ppo_loss_kernel, grid, 256, 0, B, A, logits, values, act, blogp, adv, vt, hp,
-              dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags);
+              dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
   return APPO_OK;
 }
 int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,

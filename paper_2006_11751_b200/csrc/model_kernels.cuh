@@ -44,6 +44,9 @@ int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int6
                        const BiasOut& bias = BiasOut());
 // Column sums of contiguous bf16 [M][bias.N] into bias.out
 int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias);
+// All operands derived from a published copy (conv1 fp16 + bias', dgrad weights), one launch
+int k_publish_derived(Ctx* c, const uint16_t* wb, const float* pf, const Dims& d, uint16_t* c1h,
+                      float* c1b, uint16_t* wt2, uint16_t* wt3);
 // fp16 conv1 weights + offset-corrected bias of a published copy (gemm.cu u8 path)
 int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, float* bh);
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
@@ -55,15 +58,18 @@ int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const fl
 int k_stage_h(Ctx* c, int n_traj, int T, int t, const float* hcur, float* hin, uint16_t* hbf);
 int k_gru_train(Ctx* c, int n_traj, int T, int t, const float* gi, const float* gh,
                 const uint8_t* done, float* hcur, float* core, uint16_t* core_bf, float* gates);
+// act != null: rows < B also get tlogp / ent of the stored action (fused log_prob_and_entropy)
 int k_heads_fwd(Ctx* c, int64_t R, int A, const float* core, const float* wpi, const float* bpi,
-                const float* wv, const float* bv, float* logits, float* values);
+                const float* wv, const float* bv, float* logits, float* values, int64_t B = 0,
+                const int32_t* act = nullptr, float* tlogp = nullptr, float* ent = nullptr);
 int k_gather_slots(Ctx* c, int n_traj, int T, const uint8_t* region, uint64_t slot_bytes,
                    const int32_t* slot_ids, const SlotOffsets& off, int32_t* act, float* rew,
                    float* blogp, uint8_t* done, int64_t* ver, float* h0);
 int k_normalize(Ctx* c, int n, float* adv);
 int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
                const int32_t* act, const float* blogp, const float* adv, const float* vt,
-               const LossHP& hp, float* dlog, uint16_t* dhead, double* stats);
+               const LossHP& hp, float* dlog, uint16_t* dhead, double* stats, const int64_t* ver,
+               int64_t cur);
 int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,
                 float* dcore);
 int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,

@@ -46,10 +46,19 @@ __global__ void __launch_bounds__(256)
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {  // whole last block: strided partial sums, fixed-order tree (deterministic)
     __threadfence();
+    double t = 0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+      t += ((volatile double*)partials)[b];
+    t = warp_sum(t);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+    __syncthreads();
+  }
+  if (last && threadIdx.x == 0) {
     double s = 0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += ((volatile double*)partials)[b];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
     const double norm = sqrt(s);
     double scale = 1.0;
     if (clip > 0.0f && norm > (double)clip) scale = (double)clip / norm;
