@@ -50,10 +50,10 @@ struct GatherP {
   const int32_t* slot_ids;
   uint64_t slot_bytes, obs_off, boot_off;
   int T, n_traj;
-  int nq;    // AG_U8: output rows (images x Ho)
+  int nq;    // AG_U8: output rows (images x Ho); AG_TAPS: images per M tile
   int tma;   // AG_U8 staging: 1 = tensor-map boxes (mapA / map2), 0 = bulk copies
 };
-enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3, AG_U8W = 4 };
+enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3, AG_U8W = 4, AG_TAPS = 5 };
 constexpr int GATHER_THREADS = 128;  // NHWC gather warps (after the epilogue warps)
 constexpr int U8_GATHER_THREADS = 256;  // conv1 staging/convert warps: two per tile row
 
@@ -116,8 +116,11 @@ struct Cfg {
                                    : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256
                                                      : 512;
-  // small-N tiles (conv1) are latency-bound per K block: deeper ring
-  static constexpr int STAGES = BN <= 32 ? 8 : 4;
+  // as many stages as fit in ~192 KB (4..8): the gathered / HBM-streamed
+  // operands are latency-bound, bytes in flight per SM set the rate
+  static constexpr int STAGES = (196608 / STAGE_BYTES) > 8   ? 8
+                                : (196608 / STAGE_BYTES) < 4 ? 4
+                                                             : (196608 / STAGE_BYTES);
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -332,13 +335,15 @@ __device__ __forceinline__ void gather_stage(const KParams& p, uint8_t* sA, uint
                                              const uint8_t* origin, bool valid, int kb, int gt,
                                              const int* off_tab) {
   const GatherP& g = p.g;
-  const uint32_t row_base = sm100::smem_u32(sA) + gt * 128;
   if constexpr (AG == AG_NHWC) {
+    // two threads per tile row: chunks 4*(gt >> 7) .. +3 of row gt & 127
+    const int row = gt & 127, c0 = (gt >> 7) * 4;
+    const uint32_t row_base = sm100::smem_u32(sA) + row * 128;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = c0; c < c0 + 4; ++c) {
       const uint8_t* src = origin + off_tab[kb * 8 + c];
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
-                       row_base + ((c ^ (gt & 7)) << 4)),
+                       row_base + ((c ^ (row & 7)) << 4)),
                    "l"(src), "r"(valid ? 16 : 0)
                    : "memory");
     }
@@ -346,6 +351,7 @@ __device__ __forceinline__ void gather_stage(const KParams& p, uint8_t* sA, uint
                      sm100::smem_u32(full))
                  : "memory");
   } else {
+    const uint32_t row_base = sm100::smem_u32(sA) + gt * 128;
     const uint8_t* img = origin + (int64_t)kb * g.Hi * g.Wi;  // channel kb
     uint32_t lo[8], hi[8];
 #pragma unroll
@@ -625,6 +631,10 @@ __device__ __forceinline__ void dgrad_finish(const KParams& p, int64_t off,
   dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
+// AG_TAPS ring depth: A-only stages of 16 KB next to the resident weights
+// (as many bytes in flight as fit: the strided boxes are latency-bound)
+constexpr int taps_stages(int bn) { return bn <= 64 ? 8 : 4; }
+
 template <int AG>
 constexpr bool has_gather() {
   return AG == AG_NHWC || AG == AG_U8 || AG == AG_U8W;
@@ -637,7 +647,7 @@ constexpr int epi_warps() {
 }
 template <int AG>
 constexpr int gather_threads() {
-  return (AG == AG_U8 || AG == AG_U8W) ? U8_GATHER_THREADS : has_gather<AG>() ? GATHER_THREADS : 0;
+  return has_gather<AG>() ? U8_GATHER_THREADS : 0;  // 256 gather / convert threads
 }
 template <int EV, int AG>
 constexpr int kernel_threads() {
@@ -670,9 +680,14 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* acc_full = empty + C::STAGES;
+  // stage ring (AG_TAPS: A only, the whole B operand stays resident after it)
+  constexpr int NST = AG == AG_TAPS ? taps_stages(BN) : C::STAGES;
+  constexpr int SST = AG == AG_TAPS ? A_TILE_BYTES : C::STAGE_BYTES;
+  uint8_t* const bres = smem + NST * SST;
+  uint8_t* const bar_base = bres + (AG == AG_TAPS ? p.nkb * BN * 128 : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(bar_base);
+  uint64_t* empty = full + NST;
+  uint64_t* acc_full = empty + NST;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -682,7 +697,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&mapA);
     sm100::tma_prefetch(&mapB);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       sm100::mbar_init(&full[s], 1 + gather_threads<AG>());
       sm100::mbar_init(&empty[s], 1);
     }
@@ -690,8 +705,9 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       sm100::mbar_init(&acc_full[s], 1);
       sm100::mbar_init(&acc_empty[s], epi_warps<EV>());
     }
+    if (AG == AG_TAPS) sm100::mbar_init(reinterpret_cast<uint64_t*>(bar_base + 192), 1);
     if (AG == AG_U8 || AG == AG_U8W) {  // conv1 staging ring: full (tx) / empty (all gatherers)
-      uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
       for (int s = 0; s < U8_NSTG; ++s) {
         sm100::mbar_init(&sfull[s], 1);
         sm100::mbar_init(&sfull[U8_NSTG + s], gather_threads<AG>());
@@ -706,8 +722,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   if (AG == AG_U8W) {
     // conv1 wgrad: M = 32 output channels; A rows 64..127 (the second MN atom,
     // never written by the TMA) must read as zero
-    for (int i = threadIdx.x; i < C::STAGES * 512; i += blockDim.x) {
-      uint4* z = reinterpret_cast<uint4*>(smem + (i >> 9) * C::STAGE_BYTES + 8192) + (i & 511);
+    for (int i = threadIdx.x; i < NST * 512; i += blockDim.x) {
+      uint4* z = reinterpret_cast<uint4*>(smem + (i >> 9) * SST + 8192) + (i & 511);
       *z = make_uint4(0, 0, 0, 0);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -723,13 +739,19 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     // TMA producer: whole warp, one elected lane issues (sm100.cuh *_warp)
     int stage = 0;
     uint32_t phase = 0;
+    if (AG == AG_TAPS) {  // the whole weight operand, once, resident for every tile
+      uint64_t* bb = reinterpret_cast<uint64_t*>(bar_base + 192);
+      sm100::mbar_arrive_expect_tx_warp(bb, (uint32_t)p.nkb * BN * 128);
+      for (int kb = 0; kb < p.nkb; ++kb)
+        sm100::tma_load_2d_warp(bres + kb * BN * 128, &mapB, bb, kb * BK, 0);
+    }
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit un = decode_unit(p, u);
       const int m0 = un.tm * BM, n0 = un.tn * BN;
       for (int kb = un.kb0; kb < un.kb1; ++kb) {
         sm100::mbar_wait(&empty[stage], phase ^ 1);
 
-        uint8_t* sA = smem + stage * C::STAGE_BYTES;
+        uint8_t* sA = smem + stage * SST;
         uint8_t* sB = sA + A_TILE_BYTES;
         if (AG == AG_U8W) {
           // dz1^T (MN-major A) box {64 ch (32 real), 32 x, 2 rows} of K block kb;
@@ -739,7 +761,23 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           const int img = kb / kpi;
           sm100::mbar_arrive_expect_tx_warp(&full[stage], 8192);
           sm100::tma_load_4d_warp(sA, &mapA, &full[stage], 0, 0, (kb - img * kpi) * U8W_ROWS, img);
-          if (++stage == C::STAGES) {
+          if (++stage == NST) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
+        if (AG == AG_TAPS) {
+          // NHWC convolution, K block = one kernel tap (Cin channels): A = the
+          // stride-s sampled input window of the tile's images (4-D box with
+          // element strides {1, s, s, 1}), B = the tap's weight slice
+          // K block = 64 channels: one tap (Cin 64) or a pair of horizontally
+          // adjacent taps (Cin 32, "pixel pair" view of the input: 128 B rows)
+          const int tpr = p.g.Cin == 64 ? p.g.ksz : p.g.ksz / 2;  // K blocks per kernel row
+          const int kh = kb / tpr, kw = kb % tpr;
+          sm100::mbar_arrive_expect_tx_warp(&full[stage], 128u * p.g.P * p.g.nq);
+          sm100::tma_load_4d_warp(sA, &mapA, &full[stage], 0, kw, kh, un.tm * p.g.nq);
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1;
           }
@@ -767,7 +805,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           for (int j = 0; j < BN / 64; ++j)
             sm100::tma_load_2d_warp(sB + j * 8192, &mapB, &full[stage], n0 + 64 * j, kb * BK);
         }
-        if (++stage == C::STAGES) {
+        if (++stage == NST) {
           stage = 0;
           phase ^= 1;
         }
@@ -776,6 +814,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   } else if (warp == 1) {
     // MMA issuer: the whole warp runs the loop; elect.sync inside the tcgen05
     // asm picks the issuing lane (no per-instruction waterfall, sm100.cuh)
+    if (AG == AG_TAPS) sm100::mbar_wait(reinterpret_cast<uint64_t*>(bar_base + 192), 0);
     // conv1 (AG_U8) runs on fp16 operands (exact 1024 + u8, fp16 weights)
     constexpr uint32_t idesc = AG == AG_U8 ? sm100::make_idesc_f16(BM, BN, 0, 0)
                                            : sm100::make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
@@ -792,10 +831,11 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       const uint32_t tmem_d = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
         sm100::mbar_wait(&full[stage], phase);
+        if (lane == 0 && kb == kb0) GEMM_PROF(8);
         if (has_gather<AG>()) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sm100::tc_fence_after();
-        const uint32_t a0 = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
-        const uint32_t b0 = a0 + A_TILE_BYTES;
+        const uint32_t a0 = sm100::smem_u32(smem + stage * SST);
+        const uint32_t b0 = AG == AG_TAPS ? sm100::smem_u32(bres + kb * BN * 128) : a0 + A_TILE_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           const uint64_t ad = A_MN ? sm100::make_sdesc(a0 + k * 2048, 8192, 1024)
@@ -805,7 +845,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           sm100::umma_f16_warp(tmem_d, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
         }
         sm100::umma_commit_warp(&empty[stage]);
-        if (++stage == C::STAGES) {
+        if (++stage == NST) {
           stage = 0;
           phase ^= 1;
         }
@@ -822,8 +862,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     // conv1 staging warps: warp w owns ring slot w and stages the CTA's units
     // j = w, w + U8_NSTG, ... (a TMA issue costs ~1000 cycles of the issuing
     // warp, so the slots are filled in parallel)
-    uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
-    uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES + 256;
+    uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
+    uint8_t* stg = bar_base + 256;
     int* smeta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
     __shared__ int sids[U8_SID_CACHE];
     if (p.g.slot_ids)
@@ -866,20 +906,20 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     // byte offset of chunk (kb, c) from the window origin (NHWC: (kh, kw, ci) order)
     __shared__ int off_tab[16 * 8];
     if (AG == AG_NHWC) {
-      for (int e = gt; e < p.nkb * 8; e += GATHER_THREADS) {
+      for (int e = gt; e < p.nkb * 8; e += gather_threads<AG>()) {
         const int kk = e * 8;  // (kb*64 + c*8)
         const int tap = kk / p.g.Cin, ci0 = kk % p.g.Cin;
         const int kh = tap / p.g.ksz, kw = tap % p.g.ksz;
         off_tab[e] = 2 * ((kh * p.g.Wi + kw) * p.g.Cin + ci0);
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(GATHER_THREADS));  // gatherers only
+      asm volatile("bar.sync 1, %0;" ::"n"(gather_threads<AG>()));  // gatherers only
     }
     int stage = 0;
     uint32_t phase = 0;
     if constexpr (AG == AG_U8W) {
       // one staged box per K block -> the B (col1) block of that stage
-      uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES + 256;
-      uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+      uint8_t* stg = bar_base + 256;
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
       uint64_t* sempty = sfull + U8_NSTG;
       int slot = 0;
       uint32_t sphase = 0;
@@ -889,10 +929,10 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           sm100::mbar_wait(&sfull[slot], sphase);
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           u8w_convert(p.g, stg + slot * u8_stage_bytes(p.g.Cin),
-                      smem + stage * C::STAGE_BYTES + A_TILE_BYTES, gt);
+                      smem + stage * SST + A_TILE_BYTES, gt);
           sm100::mbar_arrive(&full[stage]);
           sm100::mbar_arrive(&sempty[slot]);
-          if (++stage == C::STAGES) {
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1;
           }
@@ -906,8 +946,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     if constexpr (AG == AG_U8) {
       // staged input ring (filled by the producer warp): wait slot -> convert
       // the tile channel by channel -> release the slot
-      uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES + 256;
-      uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 192);
+      uint8_t* stg = bar_base + 256;
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
       uint64_t* sempty = sfull + U8_NSTG;
       int* sdelta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
       int slot = 0;
@@ -918,10 +958,10 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
         for (int c = 0; c < p.nkb; ++c) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           u8_convert(p.g, stg + slot * u8_stage_bytes(p.g.Cin), sdelta + slot * U8_ROWS,
-                     smem + stage * C::STAGE_BYTES, c, gt);
+                     smem + stage * SST, c, gt);
           sm100::mbar_arrive(&full[stage]);
           if (gt == 0 && c == 0) GEMM_PROF(2);
-          if (++stage == C::STAGES) {
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1;
           }
@@ -939,12 +979,15 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.nkb);
       bool valid;
-      const uint8_t* origin = gather_row_origin<AG>(p, tm * BM + gt, valid);
+      if (gt == 0) GEMM_PROF(0);
+      const uint8_t* origin = gather_row_origin<AG>(p, tm * BM + (gt & 127), valid);
       for (int kb = kb0; kb < kb1; ++kb) {
         sm100::mbar_wait(&empty[stage], phase ^ 1);
-        gather_stage<AG>(p, smem + stage * C::STAGE_BYTES, &full[stage], origin, valid, kb, gt,
+        if (gt == 0 && kb == kb0) GEMM_PROF(1);
+        gather_stage<AG>(p, smem + stage * SST, &full[stage], origin, valid, kb, gt,
                          off_tab);
-        if (++stage == C::STAGES) {
+        if (gt == 0 && kb == kb1 - 1) GEMM_PROF(2);
+        if (++stage == NST) {
           stage = 0;
           phase ^= 1;
         }
@@ -1008,6 +1051,9 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           if constexpr (AG == AG_U8) {  // tile rows -> (output row, x); padding skipped
             const int mo = u8_out_row(p.g, m);
             if (mo >= 0) epilogue_dispatch<EV>(p, mo, tn * BN + c, z, r);
+          } else if constexpr (AG == AG_TAPS) {  // tile = nq whole images, rows beyond are padding
+            const int rpt = p.g.P * p.g.nq, loc = m - un.tm * BM;
+            if (loc < rpt) epilogue_dispatch<EV>(p, un.tm * rpt + loc, tn * BN + c, z, r);
           } else {
             epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
           }
@@ -1215,8 +1261,10 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN, EV, AG>;
   // conv1: input staging ring after the barriers (+16 B overread slack)
   const int smem_bytes =
-      C::SMEM_BYTES +
-      ((AG == AG_U8 || AG == AG_U8W) ? U8_NSTG * u8_stage_bytes(p.g.Cin) + 64 : 0);
+      AG == AG_TAPS
+          ? taps_stages(BN) * A_TILE_BYTES + p.nkb * BN * 128 + 1024 + 256
+          : C::SMEM_BYTES +
+                ((AG == AG_U8 || AG == AG_U8W) ? U8_NSTG * u8_stage_bytes(p.g.Cin) + 64 : 0);
   constexpr int kThreads = kernel_threads<EV, AG>();
   static int attr_bytes[64] = {};
   int dev = c->device & 63;
@@ -1259,6 +1307,26 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
   }
   if (AG && !(c->timing && c->timing_filter == "gemm_shapes"))
     c->next_name = AG == AG_DGRAD ? "gemm_dgrad_implicit_tcgen05" : "gemm_conv_implicit_tcgen05";
+  // phase timeline of CTA 0 (diagnostics): APPO_GEMM_PROF=<AG mode number>
+  static long long* prof = nullptr;
+  const char* pe = getenv("APPO_GEMM_PROF");
+  if (pe && atoi(pe) == AG) {
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 256);
+    cudaMemsetAsync(prof, 0, sizeof(long long) * 256, c->stream);
+    KParams q = p;
+    q.prof = prof;
+    APPO_LAUNCH(c, kern, grid, kThreads, smem_bytes, ma, mb, q);
+    long long h[256];
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[gemm prof] AG=%d M=%d N=%d K=%d units of CTA0 (cycles): g0 g1 g2 | mma_accfree mma_commit | epi_start epi_done | g7 g8 g9 g10\n", AG, p.M, p.N, p.K);
+    for (int i = 0; i < 16; ++i) {
+      fprintf(stderr, "  u%-2d", i);
+      for (int k = 0; k < 11; ++k) fprintf(stderr, " %7lld", h[i * 16 + k] ? h[i * 16 + k] - h[0] : -1);
+      fprintf(stderr, "\n");
+    }
+    return APPO_OK;
+  }
   APPO_LAUNCH(c, kern, grid, kThreads, smem_bytes, ma, mb, p);
   return APPO_OK;
 }
@@ -1435,26 +1503,51 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
     // staging by tensor-map boxes when the images are 16-byte aligned, else bulk copies
     p.g.tma = make_image_maps(p, in, U8_BOX_ROWS) ? 1 : 0;
 
-    static long long* prof = nullptr;
-    if (getenv("APPO_GEMM_PROF")) {
-      if (!prof) cudaMalloc(&prof, sizeof(long long) * 256);
-      cudaMemsetAsync(prof, 0, sizeof(long long) * 256, c->stream);
-      p.prof = prof;
-      st = launch_conv<32, AG_U8>(c, mb, mb, p);
-      long long h[256];
-      cudaStreamSynchronize(c->stream);
-      cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
-      fprintf(stderr, "[gemm prof] nq=%d units of CTA0 (cycles rel. to unit0 gather start): gth_start stg_ready cvt0 | mma_accfree mma_commit | epi_start epi_done | prod_first\n", p.g.nq);
-      for (int i = 0; i < 16; ++i) {
-        fprintf(stderr, "  u%-2d", i);
-        for (int k = 0; k < 11; ++k) fprintf(stderr, " %7lld", h[i * 16 + k] ? h[i * 16 + k] - h[0] : -1);
-        fprintf(stderr, "\n");
-      }
-      return st;
-    }
+
     switch (bn) {
       case 32: return launch_conv<32, AG_U8>(c, mb, mb, p);
       default: return APPO_ERR_CONTRACT;
+    }
+  }
+  // whole images per M tile with per-tap strided TMA boxes (no gather warps)
+  if ((in.Cin == 64 || (in.Cin == 32 && in.s == 2 && in.ksz % 2 == 0)) && in.Ho * in.Wo <= BM &&
+      in.s <= 8 && bn <= 128 &&
+      (int64_t)K * bn * 2 + taps_stages(bn) * A_TILE_BYTES + 1280 <= 227 * 1024 &&
+      (reinterpret_cast<uintptr_t>(in.src) & 15) == 0) {
+    const int per = BM / (in.Ho * in.Wo);
+    CUtensorMap ma, mw;
+    EncodeTiledFn enc = get_encode();
+    APPO_REQUIRE(enc != nullptr, APPO_ERR_RESOURCE, "cuTensorMapEncodeTiled unavailable");
+    const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
+    // Cin 64: pixels; Cin 32 (stride 2, even kernel): pairs of adjacent pixels
+    // (128-byte rows) whose traversal stride along W is 1 pair
+    const bool pairs = in.Cin == 32;
+    const int wdim = pairs ? in.Wi / 2 : in.Wi;
+    const int wstr = pairs ? in.s / 2 : in.s;
+    cuuint64_t dims[4] = {64, (cuuint64_t)wdim, (cuuint64_t)in.Hi, (cuuint64_t)in.n_img};
+    cuuint64_t str[3] = {128, (cuuint64_t)in.Wi * in.Cin * 2, (cuuint64_t)in.Hi * in.Wi * in.Cin * 2};
+    cuuint32_t box[4] = {64u, (cuuint32_t)(in.Wo * wstr), (cuuint32_t)(in.Ho * in.s), (cuuint32_t)per};
+    cuuint32_t es[4] = {1u, (cuuint32_t)wstr, (cuuint32_t)in.s, 1u};
+    CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint8_t*>(in.src), dims,
+                     str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint64_t wd[2] = {(cuuint64_t)K, (cuuint64_t)N};
+    cuuint64_t ws[1] = {(cuuint64_t)W.ld * 2};
+    cuuint32_t wb[2] = {64u, (cuuint32_t)bn};
+    cuuint32_t we[2] = {1u, 1u};
+    CUresult r2 = enc(&mw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(W.ptr), wd, ws,
+                      wb, we, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS && r2 == CUDA_SUCCESS) {
+      p.g.nq = per;
+      p.tiles_m = (in.n_img + per - 1) / per;
+      p.nkb = K / 64;  // one tap (Cin 64) or tap pair (Cin 32) per K block
+      p.kb_per_split = p.nkb;
+      switch (bn) {
+        case 64: return launch_conv<64, AG_TAPS>(c, ma, mw, p);
+        case 128: return launch_conv<128, AG_TAPS>(c, ma, mw, p);
+        default: break;
+      }
     }
   }
   switch (bn) {
