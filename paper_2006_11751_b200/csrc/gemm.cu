@@ -1287,7 +1287,8 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     char buf[96];
     snprintf(buf, sizeof(buf), "gemm %dx%dx%d bn%d s%d %s%s%s", p.M, p.N, p.K, BN, p.splits,
              A_MN ? "M" : "K", B_MN ? "M" : "K",
-             AG == AG_U8 ? " conv-u8" : AG == AG_DGRAD ? " dgrad" : AG ? " conv" : "");
+             AG == AG_U8 ? " conv1-u8" : AG == AG_U8W ? " conv1-wgrad" : AG == AG_DGRAD ? " dgrad"
+             : AG == AG_TAPS ? " conv-taps" : AG ? " conv-nhwc" : "");
     c->next_name = names.insert(buf).first->c_str();
   }
   c->next_flops = 2.0 * p.M * p.N * p.K;
@@ -1306,7 +1307,11 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     c->next_bytes = 2.0 * g.n_img * ((double)p.g.Hi * p.g.Wi * p.g.Cin + 3.0 * g.Hi * g.Wi * g.Ci);
   }
   if (AG && !(c->timing && c->timing_filter == "gemm_shapes"))
-    c->next_name = AG == AG_DGRAD ? "gemm_dgrad_implicit_tcgen05" : "gemm_conv_implicit_tcgen05";
+    c->next_name = AG == AG_DGRAD  ? "gemm_dgrad_implicit_tcgen05"
+                   : AG == AG_U8   ? "gemm_conv1_u8_implicit_tcgen05"
+                   : AG == AG_U8W  ? "gemm_conv1_wgrad_implicit_tcgen05"
+                   : AG == AG_TAPS ? "gemm_conv_taps_implicit_tcgen05"
+                                   : "gemm_conv_nhwc_gather_tcgen05";
   // phase timeline of CTA 0 (diagnostics): APPO_GEMM_PROF=<AG mode number>
   static long long* prof = nullptr;
   const char* pe = getenv("APPO_GEMM_PROF");
