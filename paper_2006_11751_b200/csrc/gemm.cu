@@ -53,7 +53,9 @@ struct GatherP {
   int nq;    // AG_U8: output rows (images x Ho); AG_TAPS: images per M tile
   int tma;   // AG_U8 staging: 1 = tensor-map boxes (mapA / map2), 0 = bulk copies
 };
-enum AGather : int { AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3, AG_U8W = 4, AG_TAPS = 5 };
+enum AGather : int {
+  AG_NONE = 0, AG_NHWC = 1, AG_U8 = 2, AG_DGRAD = 3, AG_U8W = 4, AG_TAPS = 5, AG_TAPSW = 6
+};
 constexpr int GATHER_THREADS = 128;  // NHWC gather warps (after the epilogue warps)
 constexpr int U8_GATHER_THREADS = 256;  // conv1 staging/convert warps: two per tile row
 
@@ -719,8 +721,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
     sm100::tmem_relinquish();
   }
-  if (AG == AG_U8W) {
-    // conv1 wgrad: M = 32 output channels; A rows 64..127 (the second MN atom,
+  if (AG == AG_U8W || AG == AG_TAPSW) {
+    // weight gradients with M <= 64 output channels; A rows 64..127 (the second MN atom,
     // never written by the TMA) must read as zero
     for (int i = threadIdx.x; i < NST * 512; i += blockDim.x) {
       uint4* z = reinterpret_cast<uint4*>(smem + (i >> 9) * SST + 8192) + (i & 511);
@@ -753,6 +755,26 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
 
         uint8_t* sA = smem + stage * SST;
         uint8_t* sB = sA + A_TILE_BYTES;
+        if (AG == AG_TAPSW) {
+          // weight gradient of a stride-2 NHWC conv (32 input channels): K block =
+          // 4 output rows x 16 columns of one image (zero padded); A = dz^T box,
+          // B = BN/64 tap pairs of the input window (pixel-pair view, strided)
+          const int img = kb >> 1, half = kb & 1;
+          sm100::mbar_arrive_expect_tx_warp(&full[stage], 8192u * (1 + BN / 64));
+          sm100::tma_load_4d_warp(sA, &mapA, &full[stage], 0, 0, 4 * half, img);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            const int tp = un.tn * (BN / 64) + j;  // tap pair: kernel row tp / tpr, pair tp % tpr
+            const int tpr = p.g.ksz / 2;
+            sm100::tma_load_4d_warp(sB + j * 8192, &p.map2, &full[stage], 0, tp % tpr,
+                                    8 * half + tp / tpr, img);
+          }
+          if (++stage == NST) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         if (AG == AG_U8W) {
           // dz1^T (MN-major A) box {64 ch (32 real), 32 x, 2 rows} of K block kb;
           // B (col1 rows) is built by the converter warps
@@ -1288,7 +1310,8 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     snprintf(buf, sizeof(buf), "gemm %dx%dx%d bn%d s%d %s%s%s", p.M, p.N, p.K, BN, p.splits,
              A_MN ? "M" : "K", B_MN ? "M" : "K",
              AG == AG_U8 ? " conv1-u8" : AG == AG_U8W ? " conv1-wgrad" : AG == AG_DGRAD ? " dgrad"
-             : AG == AG_TAPS ? " conv-taps" : AG ? " conv-nhwc" : "");
+             : AG == AG_TAPS ? " conv-taps" : AG == AG_TAPSW ? " taps-wgrad"
+             : AG ? " conv-nhwc" : "");
     c->next_name = names.insert(buf).first->c_str();
   }
   c->next_flops = 2.0 * p.M * p.N * p.K;
@@ -1311,6 +1334,7 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
                    : AG == AG_U8   ? "gemm_conv1_u8_implicit_tcgen05"
                    : AG == AG_U8W  ? "gemm_conv1_wgrad_implicit_tcgen05"
                    : AG == AG_TAPS ? "gemm_conv_taps_implicit_tcgen05"
+                   : AG == AG_TAPSW ? "gemm_conv_taps_wgrad_tcgen05"
                                    : "gemm_conv_nhwc_gather_tcgen05";
   // phase timeline of CTA 0 (diagnostics): APPO_GEMM_PROF=<AG mode number>
   static long long* prof = nullptr;
@@ -1635,6 +1659,63 @@ int conv1_wgrad_implicit(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* d
   if (st) return st;
   Epilogue e;
   e.scale = scale;
+  e.out = dw;
+  e.ldo = N;
+  return launch_splitk_reduce(c, Cout, N, p.splits, p.partial, e);
+}
+
+// Weight gradient of conv2-like layers (NHWC bf16 input with 32 channels,
+// stride 2, even kernel, output <= 8 x 16): dw[co][(kh, kw, ci)] = sum over
+// output pixels of dz[pixel][co] * x[2oy+kh][2ox+kw][ci], both operands by TMA
+// (no im2col): K blocks of 4 x 16 zero-padded output pixels, B = tap-pair
+// windows of the pixel-pair view.  Split-K over the CTAs + deterministic reduce.
+int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, const uint16_t* dz,
+                    int Ho, int Wo, int Cout, int k, float* dw) {
+  APPO_REQUIRE(Cout == 64 && k % 2 == 0 && Ho <= 8 && Wo <= 16 && (Wi / 2) >= Wo + k / 2 - 1,
+               APPO_ERR_CONTRACT, "conv_taps_wgrad: unsupported geometry");
+  const int Cin = 32, N = k * k * Cin;
+  EncodeTiledFn enc = get_encode();
+  APPO_REQUIRE(enc != nullptr, APPO_ERR_RESOURCE, "cuTensorMapEncodeTiled unavailable");
+  KParams p{};
+  CUtensorMap ma;
+  {  // A = dz^T: [img][Ho][Wo][64] bf16, box {64, 16, 4, 1} (columns >= Wo, rows >= Ho -> 0)
+    cuuint64_t dims[4] = {(cuuint64_t)Cout, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)n_img};
+    cuuint64_t str[3] = {(cuuint64_t)Cout * 2, (cuuint64_t)Wo * Cout * 2,
+                         (cuuint64_t)Ho * Wo * Cout * 2};
+    cuuint32_t box[4] = {64u, 16u, 4u, 1u};
+    cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+    CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(dz), dims, str,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    APPO_REQUIRE(r == CUDA_SUCCESS, APPO_ERR_CONTRACT, "conv_taps_wgrad: dz map");
+  }
+  {  // B = input windows, pixel-pair view {64, Wi/2, Hi, n}, box {64, 16, 8 (stride 2), 1}
+    cuuint64_t dims[4] = {64, (cuuint64_t)(Wi / 2), (cuuint64_t)Hi, (cuuint64_t)n_img};
+    cuuint64_t str[3] = {128, (cuuint64_t)Wi * Cin * 2, (cuuint64_t)Hi * Wi * Cin * 2};
+    cuuint32_t box[4] = {64u, 16u, 8u, 1u};
+    cuuint32_t es[4] = {1u, 1u, 2u, 1u};
+    CUresult r = enc(&p.map2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(x), dims,
+                     str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    APPO_REQUIRE(r == CUDA_SUCCESS, APPO_ERR_CONTRACT, "conv_taps_wgrad: input map");
+  }
+  p.g.ksz = k;
+  p.M = Cout;
+  p.N = N;
+  p.nkb = 2 * n_img;
+  p.K = p.nkb * 64;
+  p.tiles_m = 1;
+  p.tiles_n = N / 256;
+  int splits = (2 * c->num_sms) / p.tiles_n;
+  if (splits > p.nkb) splits = p.nkb;
+  if (splits < 1) splits = 1;
+  p.kb_per_split = (p.nkb + splits - 1) / splits;
+  p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
+  int st = gemm_workspace(c, (size_t)p.splits * Cout * N * sizeof(float), &p.partial);
+  if (st) return st;
+  st = launch_gemm<256, true, true, EV_SPLIT, AG_TAPSW>(c, ma, ma, p);
+  if (st) return st;
+  Epilogue e;
   e.out = dw;
   e.ldo = N;
   return launch_splitk_reduce(c, Cout, N, p.splits, p.partial, e);

@@ -303,7 +303,7 @@ ConvIn conv1_in(const ObsSrc& src, int R, const Dims& d) {
 }
 
 int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, const uint16_t* wb,
-                    const float* pf, int pub, bool implicit) {
+                    const float* pf, int pub, bool implicit, bool conv2_implicit) {
   const Dims& d = M->d;
   Epilogue e;
   // conv1: [R*P1, 32] = (1024 + obs) . W1h^T / 255 + bias' (fp16 operands,
@@ -321,7 +321,7 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   e.bias = pf + d.off_c2b;
   e.out = s.a2;
   e.ldo = 64;
-  if (implicit) {
+  if (implicit || conv2_implicit) {
     ConvIn in;
     in.src = reinterpret_cast<const uint8_t*>(s.a1);
     in.n_img = R;
@@ -391,7 +391,7 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
   ObsSrc src;
   src.base = obs_base;
   src.img_stride = obs_stride;
-  TRY(encoder_forward(c, M, s, src, B, wb, pf, pub, /*implicit=*/true));
+  TRY(encoder_forward(c, M, s, src, B, wb, pf, pub, /*implicit=*/true, true));
   TRY(k_f32_to_bf16(c, B, h_in, kHidden, s.hbf, kHidden, kHidden));
   Epilogue g;
   g.flags = EPI_BIAS;
@@ -641,7 +641,9 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     src.n_slots = mx + 1;
   }
   src.obs_dim = d.obs_dim;
-  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false));
+  // learner: conv1 / conv2 gather their inputs (their weight gradients do too);
+  // conv3 keeps col3 for its weight-gradient GEMM
+  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false, /*conv2=*/true));
 
   // ---- GRU unrolled over T steps (+ bootstrap step) ----
   const bool seq = gru_seq_supported(n_traj);
@@ -796,12 +798,8 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   }
   // ---- conv2 backward ----
   {
-    const int M2 = B * d.P2;
-    Epilogue e;
-    e.out = G + d.off_c2w;
-    e.ldo = 512;
-    TRY(gemm_bf16(ctx, 64, 512, M2, Operand{s.dz2, 64, true}, Operand{s.col2, 512, true}, e, 256,
-                  splits_for(ctx, 64, 512, 256, M2)));
+    // weight gradient straight from a1 / dz2 (strided TMA windows, no col2)
+    TRY(conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, s.dz2, d.H2, d.W2, 64, 4, G + d.off_c2w));
     // dz1 = ELU'(a1) * conv2^T(dz2) (+ conv1 bias grad)
     DgradIn in;
     in.dz_next = s.dz2;
