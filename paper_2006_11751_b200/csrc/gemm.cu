@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
     sm100::tmem_relinquish();
   }
-  if (AG == AG_U8W || AG == AG_TAPSW) {
+  if (AG == AG_U8W || (AG == AG_TAPSW && p.M <= 64)) {
     // weight gradients with M <= 64 output channels; A rows 64..127 (the second MN atom,
     // never written by the TMA) must read as zero
     for (int i = threadIdx.x; i < NST * 512; i += blockDim.x) {
@@ -759,15 +759,22 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           // weight gradient of a stride-2 NHWC conv (32 input channels): K block =
           // 4 output rows x 16 columns of one image (zero padded); A = dz^T box,
           // B = BN/64 tap pairs of the input window (pixel-pair view, strided)
-          const int img = kb >> 1, half = kb & 1;
-          sm100::mbar_arrive_expect_tx_warp(&full[stage], 8192u * (1 + BN / 64));
-          sm100::tma_load_4d_warp(sA, &mapA, &full[stage], 0, 0, 4 * half, img);
+          // K block kb: images img0.. (p.g.nq per block) or a row block oy0.. of one
+          // image (p.g.T blocks per image); A = the dz^T box (one per 64 output
+          // channels), B = one window box per 64 K-values (tap, or tap pair when
+          // the input has 32 channels)
+          const int kpi = p.g.T;
+          const int img0 = (kb / kpi) * p.g.nq, oy0 = (kb % kpi) * p.g.P;
+          const int natoms = p.M > 64 ? 2 : 1;
+          sm100::mbar_arrive_expect_tx_warp(&full[stage], 8192u * (natoms + BN / 64));
+          for (int a = 0; a < natoms; ++a)
+            sm100::tma_load_4d_warp(sA + a * 8192, &mapA, &full[stage], 64 * a, 0, oy0, img0);
+          const int tpr = p.g.Cin == 32 ? p.g.ksz / 2 : p.g.ksz;  // K atoms per kernel row
 #pragma unroll
           for (int j = 0; j < BN / 64; ++j) {
-            const int tp = un.tn * (BN / 64) + j;  // tap pair: kernel row tp / tpr, pair tp % tpr
-            const int tpr = p.g.ksz / 2;
+            const int tp = un.tn * (BN / 64) + j;
             sm100::tma_load_4d_warp(sB + j * 8192, &p.map2, &full[stage], 0, tp % tpr,
-                                    8 * half + tp / tpr, img);
+                                    2 * oy0 + tp / tpr, img0);
           }
           if (++stage == NST) {
             stage = 0;
@@ -1669,43 +1676,58 @@ int conv1_wgrad_implicit(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* d
 // output pixels of dz[pixel][co] * x[2oy+kh][2ox+kw][ci], both operands by TMA
 // (no im2col): K blocks of 4 x 16 zero-padded output pixels, B = tap-pair
 // windows of the pixel-pair view.  Split-K over the CTAs + deterministic reduce.
-int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, const uint16_t* dz,
-                    int Ho, int Wo, int Cout, int k, float* dw) {
-  APPO_REQUIRE(Cout == 64 && k % 2 == 0 && Ho <= 8 && Wo <= 16 && (Wi / 2) >= Wo + k / 2 - 1,
+int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, int Cin,
+                    const uint16_t* dz, int Ho, int Wo, int Cout, int k, float* dw) {
+  // K block = 64 zero-padded output pixels: Wb columns x Hb rows x ipk images
+  const bool pairs = Cin == 32;
+  const int Wb = Wo <= 8 ? 8 : 16;
+  const int Hb = Wb == 16 ? 4 : (Ho <= 4 ? 4 : 8);
+  const int ipk = 64 / (Wb * Hb);          // images per K block (1 when row blocks)
+  const int kpi = ipk == 1 ? (Ho + Hb - 1) / Hb : 1;  // K blocks per image
+  APPO_REQUIRE((Cout == 64 || Cout == 128) && (Cin == 64 || (pairs && k % 2 == 0)) && Wo <= 16 &&
+                   ipk >= 1 && Wb * Hb * ipk == 64,
                APPO_ERR_CONTRACT, "conv_taps_wgrad: unsupported geometry");
-  const int Cin = 32, N = k * k * Cin;
+  const int N = k * k * Cin;
+  const int bn = N % 256 == 0 ? 256 : 192;
+  APPO_REQUIRE(N % bn == 0, APPO_ERR_CONTRACT, "conv_taps_wgrad: N must be a multiple of 192/256");
   EncodeTiledFn enc = get_encode();
   APPO_REQUIRE(enc != nullptr, APPO_ERR_RESOURCE, "cuTensorMapEncodeTiled unavailable");
   KParams p{};
   CUtensorMap ma;
-  {  // A = dz^T: [img][Ho][Wo][64] bf16, box {64, 16, 4, 1} (columns >= Wo, rows >= Ho -> 0)
+  {  // A = dz^T: [img][Ho][Wo][Cout] bf16, box {64, Wb, Hb, ipk} (outside Ho x Wo -> 0)
     cuuint64_t dims[4] = {(cuuint64_t)Cout, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)n_img};
     cuuint64_t str[3] = {(cuuint64_t)Cout * 2, (cuuint64_t)Wo * Cout * 2,
                          (cuuint64_t)Ho * Wo * Cout * 2};
-    cuuint32_t box[4] = {64u, 16u, 4u, 1u};
+    cuuint32_t box[4] = {64u, (cuuint32_t)Wb, (cuuint32_t)Hb, (cuuint32_t)ipk};
     cuuint32_t es[4] = {1u, 1u, 1u, 1u};
     CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(dz), dims, str,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     APPO_REQUIRE(r == CUDA_SUCCESS, APPO_ERR_CONTRACT, "conv_taps_wgrad: dz map");
   }
-  {  // B = input windows, pixel-pair view {64, Wi/2, Hi, n}, box {64, 16, 8 (stride 2), 1}
-    cuuint64_t dims[4] = {64, (cuuint64_t)(Wi / 2), (cuuint64_t)Hi, (cuuint64_t)n_img};
+  {  // B = input windows (pixel-pair view for 32 channels), stride-2 traversal
+    const int wdim = pairs ? Wi / 2 : Wi;
+    const int ws = pairs ? 1 : 2;
+    cuuint64_t dims[4] = {64, (cuuint64_t)wdim, (cuuint64_t)Hi, (cuuint64_t)n_img};
     cuuint64_t str[3] = {128, (cuuint64_t)Wi * Cin * 2, (cuuint64_t)Hi * Wi * Cin * 2};
-    cuuint32_t box[4] = {64u, 16u, 8u, 1u};
-    cuuint32_t es[4] = {1u, 1u, 2u, 1u};
+    cuuint32_t box[4] = {64u, (cuuint32_t)(Wb * ws), (cuuint32_t)(Hb * 2), (cuuint32_t)ipk};
+    cuuint32_t es[4] = {1u, (cuuint32_t)ws, 2u, 1u};
     CUresult r = enc(&p.map2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(x), dims,
                      str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     APPO_REQUIRE(r == CUDA_SUCCESS, APPO_ERR_CONTRACT, "conv_taps_wgrad: input map");
   }
   p.g.ksz = k;
+  p.g.Cin = Cin;
+  p.g.P = Hb;    // output rows per K block
+  p.g.nq = ipk;  // images per K block
+  p.g.T = kpi;   // K blocks per image
   p.M = Cout;
   p.N = N;
-  p.nkb = 2 * n_img;
+  p.nkb = ipk == 1 ? n_img * kpi : (n_img + ipk - 1) / ipk;
   p.K = p.nkb * 64;
   p.tiles_m = 1;
-  p.tiles_n = N / 256;
+  p.tiles_n = N / bn;
   int splits = (2 * c->num_sms) / p.tiles_n;
   if (splits > p.nkb) splits = p.nkb;
   if (splits < 1) splits = 1;
@@ -1713,7 +1735,8 @@ int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, const 
   p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
   int st = gemm_workspace(c, (size_t)p.splits * Cout * N * sizeof(float), &p.partial);
   if (st) return st;
-  st = launch_gemm<256, true, true, EV_SPLIT, AG_TAPSW>(c, ma, ma, p);
+  st = bn == 256 ? launch_gemm<256, true, true, EV_SPLIT, AG_TAPSW>(c, ma, ma, p)
+                 : launch_gemm<192, true, true, EV_SPLIT, AG_TAPSW>(c, ma, ma, p);
   if (st) return st;
   Epilogue e;
   e.out = dw;

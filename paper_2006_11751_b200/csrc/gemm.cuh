@@ -97,9 +97,10 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
 int conv1_wgrad_implicit(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* dw, float scale);
 
 // Weight gradient of a stride-2 convolution over NHWC bf16 input with 32
-// channels (conv2), both operands by TMA (no im2col): dw[co][(kh,kw,ci)].
-int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, const uint16_t* dz,
-                    int Ho, int Wo, int Cout, int k, float* dw);
+// (even kernel) or 64 channels (conv2, conv3), both operands by TMA (no
+// im2col): dw[co][(kh,kw,ci)], Cout 64 or 128.
+int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, int Cin,
+                    const uint16_t* dz, int Ho, int Wo, int Cout, int k, float* dw);
 
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);

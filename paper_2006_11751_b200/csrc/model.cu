@@ -148,9 +148,9 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
   // col1 stays the arena base (it is what gets freed)
   a.take(&s.col1, learner ? (size_t)R * d.P1 * d.K1 : 64);
   a.take(&s.a1, (size_t)R * d.P1 * 32);
-  a.take(&s.col2, learner ? (size_t)R * d.P2 * 512 : 64);
+  a.take(&s.col2, 64);  // im2col matrices are no longer materialised
   a.take(&s.a2, (size_t)R * d.P2 * 64);
-  a.take(&s.col3, learner ? (size_t)R * d.P3 * 576 : 64);
+  a.take(&s.col3, 64);
   a.take(&s.a3, (size_t)R * d.F);
   a.take(&s.x, (size_t)R * kHidden);
   a.take(&s.gi, (size_t)R * kGates);
@@ -335,7 +335,7 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   e.bias = pf + d.off_c3b;
   e.out = s.a3;
   e.ldo = 128;
-  if (implicit) {
+  if (implicit || conv2_implicit) {
     ConvIn in;
     in.src = reinterpret_cast<const uint8_t*>(s.a2);
     in.n_img = R;
@@ -641,9 +641,9 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     src.n_slots = mx + 1;
   }
   src.obs_dim = d.obs_dim;
-  // learner: conv1 / conv2 gather their inputs (their weight gradients do too);
-  // conv3 keeps col3 for its weight-gradient GEMM
-  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false, /*conv2=*/true));
+  // learner: every convolution gathers its input by TMA (so do the weight
+  // gradients: conv1_wgrad_implicit, conv_taps_wgrad) -- no im2col matrices
+  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false, /*learner=*/true));
 
   // ---- GRU unrolled over T steps (+ bootstrap step) ----
   const bool seq = gru_seq_supported(n_traj);
@@ -779,11 +779,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   // ---- conv3 backward ----
   {
     const int M3 = B * d.P3;
-    Epilogue e;
-    e.out = G + d.off_c3w;
-    e.ldo = 576;
-    TRY(gemm_bf16(ctx, 128, 576, M3, Operand{s.dz3, 128, true}, Operand{s.col3, 576, true}, e,
-                  192, splits_for(ctx, 128, 576, 192, M3)));
+    TRY(conv_taps_wgrad(ctx, s.a2, B, d.H2, d.W2, 64, s.dz3, d.H3, d.W3, 128, 3, G + d.off_c3w));
     TRY(k_colsum_v(ctx, M3, s.dz3, bias_out(1, G + d.off_c3b, 128)));
     // dz2 = ELU'(a2) * conv3^T(dz3): sub-pixel implicit GEMM (+ conv2 bias grad)
     DgradIn in;
@@ -799,7 +795,7 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   // ---- conv2 backward ----
   {
     // weight gradient straight from a1 / dz2 (strided TMA windows, no col2)
-    TRY(conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, s.dz2, d.H2, d.W2, 64, 4, G + d.off_c2w));
+    TRY(conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, 32, s.dz2, d.H2, d.W2, 64, 4, G + d.off_c2w));
     // dz1 = ELU'(a1) * conv2^T(dz2) (+ conv1 bias grad)
     DgradIn in;
     in.dz_next = s.dz2;
