@@ -189,7 +189,7 @@ int alloc_scratch(Ctx* c, Model* M, Scratch& s, int R, int n_traj, bool learner)
     a.take(&s.wt3, (size_t)4 * 64 * 512);
     a.take(&s.wt2, (size_t)4 * 32 * 256);
     a.take(&s.headw, (size_t)16 * kHidden);
-    a.take(&s.colsum_part, (size_t)256 * kGates + 64);
+    a.take(&s.colsum_part, (size_t)160 * (kMaxActions + 1) * (kHidden + 1) + 256 * kGates);
     a.take(&s.bias_acc, (size_t)4 * kBiasAccCols);
     a.take(&s.bias_cnt, (size_t)4);
     a.take(&s.slot_ids, (size_t)n_traj);
@@ -689,21 +689,9 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   float* G = M->grad;
   APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
 
-  // ---- heads backward ----
-  TRY(k_heads_bwd(ctx, B, d.A, s.dlog, th + d.off_wpi, th + d.off_wv, s.dcore));
-  {
-    Epilogue e;
-    e.out = s.headw;
-    e.ldo = kHidden;
-    TRY(gemm_bf16(ctx, 16, kHidden, B, Operand{s.dhead, 16, true},
-                  Operand{s.core_bf, kHidden, true}, e, 256,
-                  splits_for(ctx, 16, kHidden, 256, B)));
-    float* bsum = s.colsum_part + 256 * kGates;
-    TRY(k_colsum(ctx, B, d.A + 1, s.dlog, d.A + 1, false, s.colsum_part, bsum, false));
-    TRY(k_head_grad_scatter(ctx, d.A, s.headw, bsum, G + d.off_wpi, G + d.off_bpi, G + d.off_wv,
-                            G + d.off_bv));
-  }
-
+  // ---- heads backward: dcore + head weight / bias gradients, one launch ----
+  TRY(k_heads_bwd_fused(ctx, B, d.A, s.dlog, s.core, th + d.off_wpi, th + d.off_wv, s.dcore,
+                        s.colsum_part, G + d.off_wpi, G + d.off_bpi, G + d.off_wv, G + d.off_bv));
 
   // bias gradients of fc / conv layers, fused into the kernels producing /
   // reading their dz (deterministic fixed-point sums, model_kernels.cu)

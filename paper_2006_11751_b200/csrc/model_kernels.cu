@@ -442,29 +442,31 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int a = 0; a <= kMaxActions; ++a) acc[a] = warp_sum(acc[a]);
-  if (lane == 0) {
-    float lg[kMaxActions];
-    for (int a = 0; a < A; ++a) {
-      lg[a] = acc[a] + bpi[a];
-      logits[row * A + a] = lg[a];
+  // lane a < A holds logit a (all lanes hold the sums after warp_sum)
+  float my = 0.0f;
+#pragma unroll
+  for (int a = 0; a < kMaxActions; ++a)
+    if (a == lane) my = acc[a];
+  const float lgf = lane < A ? my + bpi[lane] : -INFINITY;
+  if (lane < A) logits[row * A + lane] = lgf;
+  if (lane == 0) values[row] = acc[kMaxActions] + bv[0];
+  if (act && row < B) {
+    const int ac = act[row];
+    if (ac < 0 || ac >= A) {
+      if (lane == 0) atomicOr(flags + kFlagContract, 1);
+      return;
     }
-    values[row] = acc[kMaxActions] + bv[0];
-    if (act && row < B) {
-      const int ac = act[row];
-      if (ac < 0 || ac >= A) {
-        atomicOr(flags + kFlagContract, 1);
-        return;
-      }
-      double mx = lg[0];
-      for (int a = 1; a < A; ++a) mx = fmax(mx, (double)lg[a]);
-      double z = 0;
-      for (int a = 0; a < A; ++a) z += exp((double)lg[a] - mx);
-      double h = 0;
-      for (int a = 0; a < A; ++a) {
-        const double pr = exp((double)lg[a] - mx) / z;
-        if (pr > 0) h -= pr * log(pr);
-      }
-      const double pa = exp((double)lg[ac] - mx) / z;
+    // log_prob_and_entropy in fp64, one action per lane
+    double mx = lane < A ? (double)lgf : -1e300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double e = lane < A ? exp((double)lgf - mx) : 0.0;
+    const double z = warp_sum(e);
+    const double pr = e / z;
+    const double hterm = (lane < A && pr > 0) ? -pr * log(pr) : 0.0;
+    const double h = warp_sum(hterm);
+    const double pa = __shfl_sync(0xffffffffu, pr, ac);
+    if (lane == 0) {
       tlogp[row] = (float)log(fmax(pa, 1e-300));
       ent[row] = (float)h;
     }
@@ -641,6 +643,66 @@ __global__ void __launch_bounds__(256)
     for (int a = 0; a < A; ++a) acc += dl[a] * wpi[a * kHidden + j];
     dcore[(int64_t)s * kHidden + j] = acc;
   }
+}
+
+// Heads backward in one kernel (policy.hpp:377-383 analogue for the heads):
+// dcore[s][j] = sum_a dlog[s][a] * Wh[a][j] (Wh = policy rows then the value
+// row) and the head gradients dWh[a][j] = sum_s dlog[s][a] * core[s][j],
+// dbh[a] = sum_s dlog[s][a] in fp32.  Block = a chunk of rows x 512 columns
+// (thread j); per-block partials, the last block sums them in block order
+// (deterministic) straight into the flat gradient.
+__global__ void __launch_bounds__(512)
+    heads_bwd_fused_kernel(int B, int A, const float* __restrict__ dlog,
+                           const float* __restrict__ core, const float* __restrict__ wpi,
+                           const float* __restrict__ wv, float* __restrict__ dcore,
+                           float* __restrict__ part, unsigned* counter, float* gwpi, float* gbpi,
+                           float* gwv, float* gbv) {
+  const int j = threadIdx.x;
+  const int A1 = A + 1;
+  const int rows = (B + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows, r1 = min(B, r0 + rows);
+  float w[kMaxActions + 1], sw[kMaxActions + 1], sb = 0.0f;
+#pragma unroll
+  for (int a = 0; a <= kMaxActions; ++a) {
+    w[a] = a < A ? wpi[a * kHidden + j] : (a == A ? wv[j] : 0.0f);
+    sw[a] = 0.0f;
+  }
+  for (int s = r0; s < r1; ++s) {
+    const float* dl = dlog + (int64_t)s * A1;
+    const float c = core[(int64_t)s * kHidden + j];
+    float dc = 0.0f;
+#pragma unroll
+    for (int a = 0; a <= kMaxActions; ++a) {
+      if (a < A1) {
+        const float g = dl[a];
+        dc += g * w[a];
+        sw[a] += g * c;
+      }
+    }
+    dcore[(int64_t)s * kHidden + j] = dc;
+    if (j < A1) sb += dl[j];
+  }
+  float* pb = part + (size_t)blockIdx.x * (A1 * kHidden + A1);
+#pragma unroll
+  for (int a = 0; a <= kMaxActions; ++a)
+    if (a < A1) pb[a * kHidden + j] = sw[a];
+  if (j < A1) pb[A1 * kHidden + j] = sb;
+}
+
+// Sums the per-block head-gradient partials in block order (thread per output).
+__global__ void __launch_bounds__(256)
+    heads_grad_reduce_kernel(int A, int nb, const float* __restrict__ part, float* gwpi,
+                             float* gbpi, float* gwv, float* gbv) {
+  const int A1 = A + 1;
+  const int stride = A1 * kHidden + A1;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= stride) return;
+  float t = 0.0f;
+  for (int b = 0; b < nb; ++b) t += part[(size_t)b * stride + o];
+  if (o < A * kHidden) gwpi[o] = t;
+  else if (o < A1 * kHidden) gwv[o - A * kHidden] = t;
+  else if (o - A1 * kHidden < A) gbpi[o - A1 * kHidden] = t;
+  else gbv[0] = t;
 }
 
 // One reverse BPTT step at time t (oracle orc_learner_step): dh = dcore + keep*dnext;
@@ -868,6 +930,19 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
   APPO_REQUIRE(grid * 6 <= kRedSlots, APPO_ERR_CONTRACT, "ppo_loss: batch too large");
   APPO_LAUNCH(c, ppo_loss_kernel, grid, 256, 0, B, A, logits, values, act, blogp, adv, vt, hp,
               dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
+  return APPO_OK;
+}
+int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core,
+                      const float* wpi, const float* wv, float* dcore, float* part, float* gwpi,
+                      float* gbpi, float* gwv, float* gbv) {
+  int grid = (B + 15) / 16;  // 16 rows per block
+  if (grid > 160) grid = 160;
+  if (grid < 1) grid = 1;
+  APPO_LAUNCH(c, heads_bwd_fused_kernel, grid, 512, 0, B, A, dlog, core, wpi, wv, dcore, part,
+              c->d_counter + 7, gwpi, gbpi, gwv, gbv);
+  const int outs = (A + 1) * (kHidden + 1);
+  APPO_LAUNCH(c, heads_grad_reduce_kernel, (outs + 255) / 256, 256, 0, A, grid, part, gwpi, gbpi,
+              gwv, gbv);
   return APPO_OK;
 }
 int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,

@@ -72,6 +72,11 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
                int64_t cur);
 int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,
                 float* dcore);
+// dcore + head weight / bias gradients (fp32, deterministic) in one launch;
+// part: >= 148 * (A+1) * 513 floats of workspace
+int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core,
+                      const float* wpi, const float* wv, float* dcore, float* part, float* gwpi,
+                      float* gbpi, float* gwv, float* gbv);
 int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,
               const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh);
 int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, float* part,
