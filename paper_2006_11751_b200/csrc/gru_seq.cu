@@ -509,6 +509,218 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
   }
 }
 
+// ---- forward recurrence in ONE 16-CTA cluster -------------------------------
+// CTA c owns units 32c..32c+31 (gate rows g*32+u: UMMA N = 96, W_hh slice
+// resident, SW128).  h_t is exchanged without any grid barrier: every CTA
+// writes its 64 x 32 bf16 slice to global and multicasts it by TMA (SW64 box =
+// exactly its K block of the A operand) into the h buffer of all 16 CTAs,
+// double-buffered by step parity; per-slice mbarriers (complete_tx) tell the
+// MMA warp which K blocks have landed.  A CTA multicasts h_{t+1} only after its
+// MMA(t), which needed every CTA's h_t -- so buffer (t+1)&1 (last read by the
+// MMAs of step t-1) is free everywhere, and the per-buffer barriers are re-armed
+// right after MMA(t-1) completes, before any byte of step t+1 can arrive.
+// Cells are read straight from TMEM (16x256b: all 32 lanes busy), 4 per thread.
+constexpr int CL_CTAS = 16;
+constexpr int CL_UPC = kHidden / CL_CTAS;      // 32 units per CTA
+constexpr int CL_NG = 3 * CL_UPC;              // 96 gate rows
+constexpr int CL_THR = 512;
+constexpr int CL_B = 8 * CL_NG * 128;          // W slice: 8 K blocks x 96 rows x 128 B = 96 KB
+constexpr int CL_KB = 4096;                    // one SW64 K block of h: 64 rows x 64 B
+constexpr int CL_A = CL_CTAS * CL_KB;          // 64 KB
+constexpr int CL_SMEM = 1024 + CL_B + 2 * CL_A + (2 * CL_CTAS + 1) * 8 + 16;
+
+struct ClFwdArgs {
+  CUtensorMap xmap;      // 3-D map over xbuf {512, n_traj, 2}, box {32, 64, 1}, SW64
+  int n_traj, T;
+  const float* gi;       // [R][1536]
+  const uint16_t* whh;   // bf16 [1536][512]
+  const float* bhh;      // [1536]
+  const uint8_t* done;   // [B]
+  const float* h0;       // [n_traj][512]
+  uint16_t* xbuf;        // [2][n_traj][512] bf16 exchange
+  float* core;
+  uint16_t* core_bf;
+  float* gates;
+  float* hin;
+  uint16_t* hbf;
+  long long* prof;
+};
+
+__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THR, 1)
+    gru_cl_fwd_kernel(const __grid_constant__ ClFwdArgs a) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* tB = sm;                 // W slice (SW128 K-major)
+  uint8_t* tA = sm + CL_B;          // [2][16 K blocks][64 rows][64 B] (SW64 K-major)
+  uint64_t* kbar = reinterpret_cast<uint64_t*>(tA + 2 * CL_A);  // [2][16]
+  uint64_t* mbar = kbar + 2 * CL_CTAS;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;  // == rank in the (single) cluster
+  const int j0 = cta * CL_UPC;
+  const int B = a.n_traj * a.T;
+
+  // resident B operand: row n = g*32 + u -> W_hh row g*512 + j0 + u
+  for (int e = tid; e < CL_NG * 64; e += CL_THR) {
+    const int n = e >> 6, c = e & 63;
+    const int grow = (n / CL_UPC) * kHidden + j0 + (n % CL_UPC);
+    *reinterpret_cast<uint4*>(tB + sw128(CL_NG, n, c >> 3, c & 7)) =
+        reinterpret_cast<const uint4*>(a.whh + (int64_t)grow * kHidden)[c];
+  }
+  if (tid == 0) {
+    for (int k = 0; k < 2 * CL_CTAS; ++k) sm100::mbar_init(&kbar[k], 1);
+    sm100::mbar_init(mbar, 1);
+    sm100::fence_barrier_init();
+    // arm the slice barriers of steps 0 and 1
+    for (int k = 0; k < 2 * CL_CTAS; ++k) sm100::mbar_arrive_expect_tx(&kbar[k], CL_KB);
+  }
+  if (warp == 0) {
+    sm100::tmem_alloc(tslot, 128);
+    sm100::tmem_relinquish();
+  }
+  // TMEM readout: warp w -> lane quarter sp = w % 4 (rows 16sp..16sp+15), unit
+  // group ug = w / 4; the gate pre-activations go through shared memory (the
+  // consumed h buffer) so that cells map to threads as (row, unit) with
+  // consecutive units per warp: every global store is a coalesced 128-B row.
+  const int sp = warp & 3, ug = warp >> 2;
+  const int ti0 = 16 * sp + (lane >> 2), tu0 = 8 * ug + 2 * (lane & 3);
+  int ci[4], cj[4];
+  bool cv[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int e = tid + c * CL_THR;
+    ci[c] = e / CL_UPC;
+    cj[c] = j0 + e % CL_UPC;
+    cv[c] = ci[c] < a.n_traj;
+  }
+  float hreg[4], b3[4][3], g3[4][3];
+  uint8_t dn[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    hreg[c] = cv[c] ? a.h0[(int64_t)ci[c] * kHidden + cj[c]] : 0.0f;
+#pragma unroll
+    for (int g = 0; g < 3; ++g) b3[c][g] = a.bhh[g * kHidden + cj[c]];
+    if (cv[c]) a.xbuf[(int64_t)ci[c] * kHidden + cj[c]] = f2bf_(hreg[c]);
+  }
+  auto prefetch = [&](int t) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (!cv[c]) continue;
+      const int64_t row = (t < a.T) ? (int64_t)ci[c] * a.T + t : (int64_t)B + ci[c];
+      const float* gir = a.gi + row * kGates + cj[c];
+      g3[c][0] = __ldg(gir);
+      g3[c][1] = __ldg(gir + kHidden);
+      g3[c][2] = __ldg(gir + 2 * kHidden);
+      dn[c] = (t < a.T) ? a.done[(int64_t)ci[c] * a.T + t] : 0;
+    }
+  };
+  prefetch(0);
+  fence_proxy_async_global();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::cluster_sync();  // every CTA's barriers armed and h0 slice in global
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (tid == 0)
+    sm100::tma_load_3d_mc(tA + cta * CL_KB, &a.xmap, &kbar[cta], j0, 0, 0, 0xFFFF);
+  constexpr uint32_t idesc = sm100::make_idesc_bf16(MAXTRAJ, CL_NG, 0, 0);
+  uint32_t phase = 0;
+
+  for (int t = 0; t <= a.T; ++t) {
+    const int buf = t & 1;
+    const uint32_t kpar = (t >> 1) & 1;
+    if (warp == 0) {  // MMAs per landed K block (whole warp, elect inside)
+      const uint32_t a0 = sm100::smem_u32(tA + buf * CL_A), b0 = sm100::smem_u32(tB);
+      if (a.prof && cta == 0 && lane == 0) a.prof[t * 4 + 0] = clock64();
+#pragma unroll 1
+      for (int kb = 0; kb < CL_CTAS; ++kb) {
+        sm100::mbar_wait(&kbar[buf * CL_CTAS + kb], kpar);
+        if (a.prof && cta == 0 && lane == 0 && kb == CL_CTAS - 1) a.prof[t * 4 + 1] = clock64();
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const uint64_t ad = sm100::make_sdesc_sw64(a0 + kb * CL_KB + kk * 32, 512);
+          const uint64_t bd = sm100::make_sdesc(
+              b0 + (kb >> 1) * CL_NG * 128 + ((kb & 1) * 2 + kk) * 32, 16, 1024);
+          sm100::umma_f16_warp(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+        }
+      }
+      sm100::umma_commit_warp(mbar);
+    }
+    sm100::mbar_wait(mbar, phase);
+    phase ^= 1;
+    if (a.prof && cta == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
+    sm100::tc_fence_after();
+    if (tid == 0 && t + 2 <= a.T)  // buffer `buf` is consumed: arm it for step t+2
+      for (int kb = 0; kb < CL_CTAS; ++kb)
+        sm100::mbar_arrive_expect_tx(&kbar[buf * CL_CTAS + kb], CL_KB);
+    {
+      uint32_t r3[3][4];
+      const uint32_t ta = tmem + ((uint32_t)(32 * sp) << 16) + 8 * ug;
+#pragma unroll
+      for (int g = 0; g < 3; ++g) sm100::tmem_ld_16x256b(ta + g * CL_UPC, r3[g]);
+      sm100::tmem_ld_wait();
+      float* gh = reinterpret_cast<float*>(tA + buf * CL_A);  // [64][96], buffer consumed
+#pragma unroll
+      for (int g = 0; g < 3; ++g)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          gh[(ti0 + (c >> 1) * 8) * CL_NG + g * CL_UPC + tu0 + (c & 1)] = __uint_as_float(r3[g][c]);
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    const float* gh = reinterpret_cast<const float*>(tA + buf * CL_A);
+    const size_t nxt = (size_t)((t + 1) & 1) * a.n_traj * kHidden;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (!cv[c]) continue;
+      const int i = ci[c], j = cj[c], u = j - j0;
+      const int64_t row = (t < a.T) ? (int64_t)i * a.T + t : (int64_t)B + i;
+      const float ghr = gh[i * CL_NG + u] + b3[c][0];
+      const float ghz = gh[i * CL_NG + CL_UPC + u] + b3[c][1];
+      const float ghn = gh[i * CL_NG + 2 * CL_UPC + u] + b3[c][2];
+      const float rr = sig_(g3[c][0] + ghr);
+      const float z = sig_(g3[c][1] + ghz);
+      const float n = tanh_(g3[c][2] + rr * ghn);
+      const float hp = hreg[c];
+      const float h = (1.0f - z) * n + z * hp;
+      a.core[row * kHidden + j] = h;
+      a.core_bf[row * kHidden + j] = f2bf_(h);
+      float* gs = a.gates + row * 4 * kHidden;
+      gs[j] = rr;
+      gs[kHidden + j] = z;
+      gs[2 * kHidden + j] = n;
+      gs[3 * kHidden + j] = ghn;
+      a.hin[row * kHidden + j] = hp;
+      a.hbf[row * kHidden + j] = f2bf_(hp);
+      if (t < a.T) {
+        const float hn = dn[c] ? 0.0f : h;
+        hreg[c] = hn;
+        a.xbuf[nxt + (int64_t)i * kHidden + j] = f2bf_(hn);
+      }
+    }
+    if (a.prof && cta == 0 && tid == 0) a.prof[t * 4 + 3] = clock64();
+    if (t < a.T) {
+      prefetch(t + 1);
+      fence_proxy_async_global();  // h_{t+1} slice -> visible to the TMA read
+      fence_async_smem();          // staging reads of the consumed buffer before any TMA refill
+      sm100::tc_fence_before();
+      __syncthreads();             // slice complete; TMEM reads of step t done
+      if (tid == 0)
+        sm100::tma_load_3d_mc(tA + ((t + 1) & 1) * CL_A + cta * CL_KB, &a.xmap,
+                              &kbar[((t + 1) & 1) * CL_CTAS + cta], j0, 0, (t + 1) & 1, 0xFFFF);
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 128);
+  }
+  sm100::cluster_sync();  // no CTA leaves while a peer may still multicast into it
+}
+
 constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + MAXTRAJ * NG * 4 + 128;
 constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + MAXTRAJ * UPC_B * 4 + 128;
 static_assert(BWD_SMEM <= 227 * 1024, "backward GRU smem");
@@ -553,6 +765,58 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
                   const float* bhh, const uint8_t* done, float* hbuf, uint16_t* hbuf_bf,
                   float* core, uint16_t* core_bf, float* gates, float* hin, uint16_t* hbf,
                   unsigned* bar) {
+  // one 16-CTA cluster (TMA-multicast exchange, no grid barrier) when it can be
+  // scheduled; the cooperative 32-CTA kernel otherwise
+  // opt-in (APPO_GRU_CLUSTER=1): measured slower than the cooperative kernel at
+  // n_traj = 64 (16 CTAs carry twice the cell work per SM: ~8.8k vs 8.1k cycles
+  // per step), kept for smaller / different GRU shapes
+  static int cl_state = getenv("APPO_GRU_CLUSTER") ? 0 : -1;  // 0 untried, 1 ok, -1 off
+  if (cl_state >= 0) {
+    if (cl_state == 0) {
+      if (cudaFuncSetAttribute(gru_cl_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               CL_SMEM) != cudaSuccess ||
+          cudaFuncSetAttribute(gru_cl_fwd_kernel,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        cl_state = -1;
+      } else {
+        cl_state = 1;
+      }
+    }
+    if (cl_state == 1) {
+      ClFwdArgs a{};
+      int st = make_tmap_bf16_3d(&a.xmap, hbuf_bf, kHidden, n_traj, 2, kHidden * 2,
+                                 (uint64_t)n_traj * kHidden * 2, 32, MAXTRAJ, 1, 64);
+      if (st) return st;
+      a.n_traj = n_traj; a.T = T; a.gi = gi; a.whh = whh; a.bhh = bhh; a.done = done;
+      a.h0 = hbuf; a.xbuf = hbuf_bf; a.core = core; a.core_bf = core_bf; a.gates = gates;
+      a.hin = hin; a.hbf = hbf;
+      a.prof = prof_buffer(c);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(CL_CTAS);
+      cfg.blockDim = dim3(CL_THR);
+      cfg.dynamicSmemBytes = CL_SMEM;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL_CTAS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaEvent_t ev = timing_begin(c, "gru_seq_fwd_kernel");
+      cudaError_t e = cudaLaunchKernelEx(&cfg, gru_cl_fwd_kernel, a);
+      c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T + 1);
+      timing_end(c, "gru_seq_fwd_kernel", ev);
+      if (e == cudaSuccess) {
+        c->launches++;
+        if (a.prof) prof_report(c, a.prof, T + 1, "cluster fwd: data-wait | mma | cells | (next)");
+        return APPO_OK;
+      }
+      cudaGetLastError();
+      cl_state = -1;  // fall back for good
+    }
+  }
   static bool attr = false;
   if (!attr) {
     APPO_CUDA_TRY(cudaFuncSetAttribute(gru_seq_fwd_kernel,

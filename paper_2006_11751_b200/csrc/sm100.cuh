@@ -105,6 +105,29 @@ __device__ __forceinline__ void tma_load_5d_warp(void* dst, const CUtensorMap* m
       "r"(c3), "r"(c4)
       : "memory");
 }
+// Multicast 3-D load: the box lands at the same CTA-relative smem offset in
+// every CTA of ctaMask (cluster), each signalling its own mbarrier at `bar`'s
+// offset.  Single issuing thread.
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int32_t c0, int32_t c1, int32_t c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// 16 TMEM lanes x 256 bits: thread t gets (lane t/4, cols 2(t%4), +1) and
+// (lane t/4 + 8, same cols) -- the M=64 accumulator's row layout
+__device__ __forceinline__ void tmem_ld_16x256b(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tma_load_4d_warp(void* dst, const CUtensorMap* map, uint64_t* bar,
                                                  int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
   asm volatile(
