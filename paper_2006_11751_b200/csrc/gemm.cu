@@ -229,6 +229,7 @@ enum EpiVariant : int {
   EV_DELU_BF16 = 4, // bf16: x * ELU'(aux)
   EV_BF16 = 5,      // bf16: x*scale
   EV_DGRAD = 6,     // bf16: x * ELU'(aux) at the sub-pixel position + bias sums
+  EV_DELU_BSUM = 7, // EV_DELU_BF16 + fused bias gradient (Epilogue::bsum_*)
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -238,7 +239,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 template <int EV>
 __device__ __forceinline__ void epilogue_dispatch(const KParams& p, int m, int n0, int z,
-                                                  const uint32_t (&r)[16]) {
+                                                  const uint32_t (&r)[16],
+                                                  float* sv = nullptr) {
   if constexpr (EV == EV_GENERIC) {
     epilogue_chunk<0>(p, m, n0, z, r);
   } else {
@@ -279,7 +281,7 @@ __device__ __forceinline__ void epilogue_dispatch(const KParams& p, int m, int n
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = elu_fast(v[j]);
     }
-    if constexpr (EV == EV_DELU_BF16) {
+    if constexpr (EV == EV_DELU_BF16 || EV == EV_DELU_BSUM) {
       const uint4* a4 = reinterpret_cast<const uint4*>(e.aux + (size_t)m * e.ld_aux + n0);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -303,10 +305,18 @@ __device__ __forceinline__ void epilogue_dispatch(const KParams& p, int m, int n
     } else {
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.out) +
                                             (size_t)m * e.ldo + n0);
-      dst[0] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                          pack_bf16(v[6], v[7]));
-      dst[1] = make_uint4(pack_bf16(v[8], v[9]), pack_bf16(v[10], v[11]),
-                          pack_bf16(v[12], v[13]), pack_bf16(v[14], v[15]));
+      uint32_t w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = pack_bf16(v[2 * q], v[2 * q + 1]);
+      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      if constexpr (EV == EV_DELU_BSUM) {  // stored (rounded) values feed the bias gradient
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          sv[2 * q] = bf16_bits_to_float((uint16_t)(w[q] & 0xFFFF));
+          sv[2 * q + 1] = bf16_bits_to_float((uint16_t)(w[q] >> 16));
+        }
+      }
     }
   }
 }
@@ -1077,6 +1087,18 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           uint32_t r[16];
           sm100::tmem_ld16(tbase + c, r);
           sm100::tmem_ld_wait();
+          if constexpr (EV == EV_DELU_BSUM) {
+            float sv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sv[j] = 0.0f;
+            epilogue_dispatch<EV>(p, m, tn * BN + c, z, r, sv);
+            const float t = transpose_reduce16(sv, lane);  // lane l < 16: column c + l
+            if (lane < 16)
+              atomicAdd(p.epi.bsum_acc + (size_t)(blockIdx.x % 16) * p.epi.bsum_mod +
+                            (tn * BN + c + lane) % p.epi.bsum_mod,
+                        (unsigned long long)llrint((double)t * 4294967296.0));
+            continue;
+          }
           if constexpr (AG == AG_U8) {  // tile rows -> (output row, x); padding skipped
             const int mo = u8_out_row(p.g, m);
             if (mo >= 0) epilogue_dispatch<EV>(p, mo, tn * BN + c, z, r);
@@ -1095,6 +1117,24 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+    }
+    if constexpr (EV == EV_DELU_BSUM) {  // last CTA converts the bias-gradient sums
+      const Epilogue& e = p.epi;
+      __threadfence();
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");  // epilogue warps only
+      __shared__ unsigned last_cta_b;
+      if (warp == 2 && lane == 0) last_cta_b = atomicAdd(e.bsum_cnt, 1u) == gridDim.x - 1;
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * EPIW) : "memory");
+      if (last_cta_b) {
+        __threadfence();
+        const int et = threadIdx.x - 64;
+        for (int n = et; n < e.bsum_mod; n += 32 * EPIW) {
+          unsigned long long v = 0;
+          for (int k = 0; k < 16; ++k) v += atomicExch(e.bsum_acc + (size_t)k * e.bsum_mod + n, 0ull);
+          e.bsum_out[n] = (float)((double)(long long)v * (1.0 / 4294967296.0));
+        }
+        if (et == 0) *e.bsum_cnt = 0;
       }
     }
     if constexpr (EV == EV_DGRAD) {
@@ -1275,7 +1315,10 @@ int choose_ev(const KParams& p) {
     const int g = f & ~EPI_BF16;
     if (g == (EPI_BIAS | EPI_ELU) || g == EPI_ELU)
       return (!(f & EPI_BIAS) || al16(e.bias)) ? EV_ELU_BF16 : EV_GENERIC;
-    if (g == EPI_DELU) return ((e.ld_aux & 7) || !al16(e.aux)) ? EV_GENERIC : EV_DELU_BF16;
+    if (g == EPI_DELU) {
+      if ((e.ld_aux & 7) || !al16(e.aux)) return EV_GENERIC;
+      return e.bsum_out ? EV_DELU_BSUM : EV_DELU_BF16;
+    }
     if (g == 0) return EV_BF16;
     return EV_GENERIC;
   }
@@ -1403,6 +1446,7 @@ int dispatch_ev(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
     case EV_F32: return launch_gemm<BN, A_MN, B_MN, EV_F32>(c, ma, mb, p);
     case EV_ELU_BF16: return launch_gemm<BN, A_MN, B_MN, EV_ELU_BF16>(c, ma, mb, p);
     case EV_DELU_BF16: return launch_gemm<BN, A_MN, B_MN, EV_DELU_BF16>(c, ma, mb, p);
+    case EV_DELU_BSUM: return launch_gemm<BN, A_MN, B_MN, EV_DELU_BSUM>(c, ma, mb, p);
     case EV_BF16: return launch_gemm<BN, A_MN, B_MN, EV_BF16>(c, ma, mb, p);
     default: return launch_gemm<BN, A_MN, B_MN, EV_GENERIC>(c, ma, mb, p);
   }
@@ -1461,6 +1505,9 @@ int gemm_bf16(Ctx* c, int M, int N, int K, const Operand& A, const Operand& B,
   p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
   p.epi = epi;
   p.partial = nullptr;
+  APPO_REQUIRE(!epi.bsum_out || (p.splits == 1 && choose_ev(p) == EV_DELU_BSUM && epi.bsum_acc &&
+                                 epi.bsum_cnt && epi.bsum_mod > 0 && N % 16 == 0),
+               APPO_ERR_CONTRACT, "gemm: fused bias sums need an aligned bf16 DELU epilogue");
   if (p.splits > 1) {
     APPO_REQUIRE(!(epi.flags & (EPI_BF16 | EPI_ELU | EPI_DELU)), APPO_ERR_CONTRACT,
                  "gemm: split-K supports fp32 (+bias/accum/trans) epilogues only");

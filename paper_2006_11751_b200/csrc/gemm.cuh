@@ -24,6 +24,13 @@ struct Epilogue {
   int64_t ld_aux = 0;
   void* out = nullptr;
   int64_t ldo = 0;
+  // optional fused bias gradient of a DELU/bf16 epilogue: column sums of the
+  // stored values folded modulo bsum_mod (NHWC channel), 2^-32 fixed-point
+  // accumulators [16][bsum_mod] + CTA counter, last CTA writes bsum_out
+  unsigned long long* bsum_acc = nullptr;
+  unsigned* bsum_cnt = nullptr;
+  float* bsum_out = nullptr;
+  int bsum_mod = 0;
 };
 
 // One GEMM operand in global memory (bf16).

@@ -744,6 +744,13 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     x.ld_aux = kHidden;
     x.out = s.dzfc;
     x.ldo = kHidden;
+    {  // fc bias gradient = column sums of dz_fc, fused into this epilogue
+      const BiasOut bo = bias_out(0, G + d.off_fcb, kHidden);
+      x.bsum_acc = bo.acc;
+      x.bsum_cnt = bo.counter;
+      x.bsum_out = bo.out;
+      x.bsum_mod = kHidden;
+    }
     TRY(gemm_bf16(ctx, B, kHidden, kGates, Operand{s.dgi, kGates, false},
                   Operand{wb + d.off_wih, kHidden, true}, x, 128));
   }
@@ -754,13 +761,19 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
     e.ldo = d.F;
     TRY(gemm_bf16(ctx, kHidden, d.F, B, Operand{s.dzfc, kHidden, true},
                   Operand{s.a3, d.F, true}, e, 256, splits_for(ctx, kHidden, d.F, 256, B)));
-    TRY(k_colsum_v(ctx, B, s.dzfc, bias_out(0, G + d.off_fcb, kHidden)));
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
     x.aux = s.a3;
     x.ld_aux = d.F;
     x.out = s.dz3;
     x.ldo = d.F;
+    {  // conv3 bias gradient = dz3 column sums folded over the (h, w) positions
+      const BiasOut bo = bias_out(1, G + d.off_c3b, 128);
+      x.bsum_acc = bo.acc;
+      x.bsum_cnt = bo.counter;
+      x.bsum_out = bo.out;
+      x.bsum_mod = 128;
+    }
     TRY(gemm_bf16(ctx, B, d.F, kHidden, Operand{s.dzfc, kHidden, false},
                   Operand{wb + d.off_fcw, d.F, true}, x, 128));
   }
@@ -768,7 +781,6 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   {
     const int M3 = B * d.P3;
     TRY(conv_taps_wgrad(ctx, s.a2, B, d.H2, d.W2, 64, s.dz3, d.H3, d.W3, 128, 3, G + d.off_c3w));
-    TRY(k_colsum_v(ctx, M3, s.dz3, bias_out(1, G + d.off_c3b, 128)));
     // dz2 = ELU'(a2) * conv3^T(dz3): sub-pixel implicit GEMM (+ conv2 bias grad)
     DgradIn in;
     in.dz_next = s.dz3;
