@@ -101,6 +101,14 @@ struct Unit {
 };
 __device__ __forceinline__ Unit decode_unit(const KParams& p, int u) {
   Unit r;
+  if (p.tiles_n == 1 && p.splits == 1) {  // (conv / dgrad shapes) no integer divisions
+    r.tm = u;
+    r.tn = 0;
+    r.z = 0;
+    r.kb0 = 0;
+    r.kb1 = p.nkb;
+    return r;
+  }
   r.tm = u % p.tiles_m;
   r.tn = (u / p.tiles_m) % p.tiles_n;
   r.z = u / (p.tiles_m * p.tiles_n);
