@@ -51,7 +51,9 @@ def parse():
     p.add_argument("--mode", default="dp", choices=["dp", "pbt"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-overlap", action="store_true", help="sampler and learner on one stream")
-    p.add_argument("--sampler-sms", type=int, default=0, help="SM budget of the sampler context")
+    p.add_argument("--sampler-sms", type=int, default=64,
+                   help="SM budget of the sampler context (persistent grids sized to it; 0 = all): "
+                        "leaves SMs to the learner's kernels while both streams run")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-traj", type=int, default=0, help="trajectories per CPU-baseline sample")
     return p.parse_args()
@@ -387,7 +389,8 @@ def run_ours(args, ws, rank, local):
                        "frameskip": args.frameskip, "obs": "u8 3x72x128",
                        "parallelism": (f"dp{ws}" if args.mode == "dp" else f"pbt{ws}"),
                        "learner_steps_per_step": int(ids.shape[0]),
-                       "overlap": "sampler stream || learner stream" if sctx is not lctx else "off",
+                       "overlap": ("sampler stream || learner stream, sampler grids on "
+                                   f"{args.sampler_sms or 'all'} SMs") if sctx is not lctx else "off",
                        "l2": "inputs larger than L2 (2 x 16 GB slot sets, 453 MB obs per env step)"},
             "samples_per_s": value / args.frameskip,
             "gpu_launches": n_launch,
