@@ -117,21 +117,30 @@ __device__ __forceinline__ Unit decode_unit(const KParams& p, int u) {
   return r;
 }
 
+// barrier area after the stage ring / resident operands: full[<=8] empty[<=8]
+// acc_full[<=8] acc_empty[<=8] tmem slot, then (conv1 staging / resident-B)
+// barriers at +BAR_AUX, conv1 staging data at +BAR_BYTES
+constexpr int BAR_AUX = 320;
+constexpr int BAR_BYTES = 512;
+
 template <int BN>
 struct Cfg {
   static constexpr int B_TILE_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
-  static constexpr int TMEM_COLS = (2 * BN <= 32)    ? 32
-                                   : (2 * BN <= 64)  ? 64
-                                   : (2 * BN <= 128) ? 128
-                                   : (2 * BN <= 256) ? 256
-                                                     : 512;
+  // TMEM accumulator ring: small tiles keep more tiles in flight (the
+  // full -> MMA -> epilogue chain per tile is latency-bound, not MMA-bound)
+  static constexpr int NACC = BN <= 32 ? 8 : BN <= 64 ? 4 : 2;
+  static constexpr int TMEM_COLS = (NACC * BN <= 32)    ? 32
+                                   : (NACC * BN <= 64)  ? 64
+                                   : (NACC * BN <= 128) ? 128
+                                   : (NACC * BN <= 256) ? 256
+                                                        : 512;
   // as many stages as fit in ~192 KB (4..8): the gathered / HBM-streamed
   // operands are latency-bound, bytes in flight per SM set the rate
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8   ? 8
                                 : (196608 / STAGE_BYTES) < 4 ? 4
                                                              : (196608 / STAGE_BYTES);
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + BAR_BYTES;
 };
 
 // ELU with the MUFU exponential: |error| <= ~1e-7 absolute, far below the
@@ -708,8 +717,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(bar_base);
   uint64_t* empty = full + NST;
   uint64_t* acc_full = empty + NST;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_empty = acc_full + C::NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::NACC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -721,13 +730,13 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       sm100::mbar_init(&full[s], 1 + gather_threads<AG>());
       sm100::mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NACC; ++s) {
       sm100::mbar_init(&acc_full[s], 1);
       sm100::mbar_init(&acc_empty[s], epi_warps<EV>());
     }
-    if (AG == AG_TAPS) sm100::mbar_init(reinterpret_cast<uint64_t*>(bar_base + 192), 1);
+    if (AG == AG_TAPS) sm100::mbar_init(reinterpret_cast<uint64_t*>(bar_base + BAR_AUX), 1);
     if (AG == AG_U8 || AG == AG_U8W) {  // conv1 staging ring: full (tx) / empty (all gatherers)
-      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + BAR_AUX);
       for (int s = 0; s < U8_NSTG; ++s) {
         sm100::mbar_init(&sfull[s], 1);
         sm100::mbar_init(&sfull[U8_NSTG + s], gather_threads<AG>());
@@ -760,7 +769,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     int stage = 0;
     uint32_t phase = 0;
     if (AG == AG_TAPS) {  // the whole weight operand, once, resident for every tile
-      uint64_t* bb = reinterpret_cast<uint64_t*>(bar_base + 192);
+      uint64_t* bb = reinterpret_cast<uint64_t*>(bar_base + BAR_AUX);
       sm100::mbar_arrive_expect_tx_warp(bb, (uint32_t)p.nkb * BN * 128);
       for (int kb = 0; kb < p.nkb; ++kb)
         sm100::tma_load_2d_warp(bres + kb * BN * 128, &mapB, bb, kb * BK, 0);
@@ -861,7 +870,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   } else if (warp == 1) {
     // MMA issuer: the whole warp runs the loop; elect.sync inside the tcgen05
     // asm picks the issuing lane (no per-instruction waterfall, sm100.cuh)
-    if (AG == AG_TAPS) sm100::mbar_wait(reinterpret_cast<uint64_t*>(bar_base + 192), 0);
+    if (AG == AG_TAPS) sm100::mbar_wait(reinterpret_cast<uint64_t*>(bar_base + BAR_AUX), 0);
     // conv1 (AG_U8) runs on fp16 operands (exact 1024 + u8, fp16 weights)
     constexpr uint32_t idesc = AG == AG_U8 ? sm100::make_idesc_f16(BM, BN, 0, 0)
                                            : sm100::make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
@@ -899,7 +908,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       }
       sm100::umma_commit_warp(&acc_full[acc]);
       if (lane == 0) GEMM_PROF(4);
-      if (++acc == 2) {
+      if (++acc == C::NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -909,8 +918,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     // conv1 staging warps: warp w owns ring slot w and stages the CTA's units
     // j = w, w + U8_NSTG, ... (a TMA issue costs ~1000 cycles of the issuing
     // warp, so the slots are filled in parallel)
-    uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
-    uint8_t* stg = bar_base + 256;
+    uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + BAR_AUX);
+    uint8_t* stg = bar_base + BAR_BYTES;
     int* smeta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
     __shared__ int sids[U8_SID_CACHE];
     if (p.g.slot_ids)
@@ -965,8 +974,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     uint32_t phase = 0;
     if constexpr (AG == AG_U8W) {
       // one staged box per K block -> the B (col1) block of that stage
-      uint8_t* stg = bar_base + 256;
-      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
+      uint8_t* stg = bar_base + BAR_BYTES;
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + BAR_AUX);
       uint64_t* sempty = sfull + U8_NSTG;
       int slot = 0;
       uint32_t sphase = 0;
@@ -993,8 +1002,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     if constexpr (AG == AG_U8) {
       // staged input ring (filled by the producer warp): wait slot -> convert
       // the tile channel by channel -> release the slot
-      uint8_t* stg = bar_base + 256;
-      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + 192);
+      uint8_t* stg = bar_base + BAR_BYTES;
+      uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + BAR_AUX);
       uint64_t* sempty = sfull + U8_NSTG;
       int* sdelta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
       int slot = 0;
@@ -1122,7 +1131,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
       if (warp == 2 && lane == 0) GEMM_PROF(6);
-      if (++acc == 2) {
+      if (++acc == C::NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -1342,7 +1351,7 @@ int launch_gemm(Ctx* c, const CUtensorMap& ma, const CUtensorMap& mb, const KPar
   // conv1: input staging ring after the barriers (+16 B overread slack)
   const int smem_bytes =
       AG == AG_TAPS
-          ? taps_stages(BN) * A_TILE_BYTES + p.nkb * BN * 128 + 1024 + 256
+          ? taps_stages(BN) * A_TILE_BYTES + p.nkb * BN * 128 + 1024 + BAR_BYTES
           : C::SMEM_BYTES +
                 ((AG == AG_U8 || AG == AG_U8W) ? U8_NSTG * u8_stage_bytes(p.g.Cin) + 64 : 0);
   constexpr int kThreads = kernel_threads<EV, AG>();
@@ -1603,7 +1612,7 @@ int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const 
   // whole images per M tile with per-tap strided TMA boxes (no gather warps)
   if ((in.Cin == 64 || (in.Cin == 32 && in.s == 2 && in.ksz % 2 == 0)) && in.Ho * in.Wo <= BM &&
       in.s <= 8 && bn <= 128 &&
-      (int64_t)K * bn * 2 + taps_stages(bn) * A_TILE_BYTES + 1280 <= 227 * 1024 &&
+      (int64_t)K * bn * 2 + taps_stages(bn) * A_TILE_BYTES + 1024 + BAR_BYTES <= 227 * 1024 &&
       (reinterpret_cast<uintptr_t>(in.src) & 15) == 0) {
     const int per = BM / (in.Ho * in.Wo);
     CUtensorMap ma, mw;
