@@ -1,6 +1,7 @@
-"""One inference step (16384 envs) + one learner step (2048 samples) at the bench
-shapes inside a cudaProfilerStart/Stop range, for `ncu --profile-from-start off`
-captures (DRAM traffic per kernel -> profiles/traffic.json via traffic_summary.py)."""
+"""One inference step (16384 envs) + 8 learner steps (2048 samples each) at the
+bench shapes -- the bench's 32 : 256 launch mix -- inside a cudaProfilerStart/Stop
+range, for `ncu --profile-from-start off` captures (DRAM traffic per kernel class
+-> profiles/traffic.json via traffic_summary.py)."""
 import os
 import sys
 
@@ -25,7 +26,8 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     smp.step(store, 0, 5)
-    ctx.learner_step(store.region, store.slot_bytes, ids)
+    for _ in range(8):
+        ctx.learner_step(store.region, store.slot_bytes, ids)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     print("traffic step done")

@@ -56,8 +56,9 @@ def main(path):
                               "us_total": s["us"]} for k, s in per.items()},
                "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                          "gpu__time_duration.sum --clock-control none over "
-                         "scripts/traffic_step.py (1 inference step of 16384 envs + 1 learner "
-                         "step of 2048 samples); cold-cache serialized replays"},
+                         "scripts/traffic_step.py (1 inference step of 16384 envs + 8 learner "
+                         "steps of 2048 samples = the bench's 32:256 launch mix); "
+                         "cold-cache serialized replays"},
               sys.stdout, indent=1, sort_keys=True)
 
 
