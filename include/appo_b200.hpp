@@ -177,6 +177,14 @@ class Context {
     return v;
   }
 
+  // save_checkpoint / load_checkpoint (policy.hpp:545-605): APPOCKP1 file
+  void save_checkpoint(const std::string& path) const {
+    check(appo_checkpoint_save(h_, path.c_str()));
+  }
+  void load_checkpoint(const std::string& path) const {
+    check(appo_checkpoint_load(h_, path.c_str()));
+  }
+
  private:
   appo_model_desc desc_{};
   appo_ctx* h_ = nullptr;

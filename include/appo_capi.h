@@ -170,6 +170,22 @@ APPO_API int appo_adam_get(appo_ctx* ctx, float* h_m, float* h_v, int64_t* t_out
 APPO_API int appo_adam_set(appo_ctx* ctx, const float* h_m, const float* h_v, int64_t t);
 APPO_API int64_t appo_params_version(appo_ctx* ctx);
 
+/* Checkpoint / resume in the reference's APPOCKP1 format: replaces
+ * save_checkpoint / load_checkpoint (policy.hpp:545-605; byte layout
+ * docs/shared_memory_layout.md:95-107).  load: ConfigError on a spec-hash or
+ * parameter-count mismatch, resource error on I/O / checksum failures; the
+ * published copy, Adam moments, step counter and version are all restored. */
+APPO_API int appo_checkpoint_save(appo_ctx* ctx, const char* path);
+APPO_API int appo_checkpoint_load(appo_ctx* ctx, const char* path);
+/* Any APPOCKP1 file (also the reference's own): header, and theta|m|v as f64
+ * when tmv != NULL (*n_inout = capacity in, n out); magic + checksum checked. */
+APPO_API int appo_checkpoint_read_raw(const char* path, uint64_t* spec_hash, int64_t* version,
+                                      int64_t* adam_t, uint64_t* n_inout, double* tmv);
+/* ModelShape::spec_hash analogue (policy.hpp:54-58) of this model contract. */
+APPO_API uint64_t appo_model_spec_hash(const appo_model_desc* desc);
+/* fnv1a64 (common.hpp:66-74). */
+APPO_API uint64_t appo_fnv1a64(const void* data, uint64_t n);
+
 /* Batched policy inference: replaces forward_batch + sample_action + the row
  * writes of PolicyWorkerUnit::run_once (orchestrator.hpp:643-656).
  * d_obs u8 [B][C*H*W], d_h_in f32 [B][512] -> d_actions i32 [B], d_logp f32 [B],

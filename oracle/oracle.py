@@ -235,9 +235,26 @@ class Oracle:
 class Reference:
     """The reference headers compiled unchanged (oracle/_ref/libappo_ref.so)."""
 
+    def save_checkpoint_mlp(self, path, obs_dim, trunk, heads, seed, version, t):
+        """save_checkpoint (policy.hpp:545-564) of an init_params MLP; returns n."""
+        h = np.ascontiguousarray(heads, dtype=np.int32)
+        return int(self.L.ref_save_checkpoint_mlp(os.fsencode(path), obs_dim, trunk, h, len(h),
+                                                  seed, version, t))
+
+    def spec_hash_mlp(self, obs_dim, hidden, trunk, heads):
+        h = np.ascontiguousarray(heads, dtype=np.int32)
+        return int(self.L.ref_spec_hash_mlp(obs_dim, hidden, trunk, h, len(h)))
+
     def __init__(self, path: str = REF_LIB):
         L = C.CDLL(path)
         self.L = L
+        L.ref_save_checkpoint_mlp.restype = C.c_longlong
+        L.ref_save_checkpoint_mlp.argtypes = [C.c_char_p, C.c_int, C.c_int, _i32p, C.c_int,
+                                              C.c_uint64, C.c_longlong, C.c_longlong]
+        L.ref_spec_hash_mlp.restype = C.c_uint64
+        L.ref_fnv1a64.restype = C.c_uint64
+        L.ref_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
+        L.ref_spec_hash_mlp.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, C.c_int]
         L.ref_vtrace.restype = C.c_int
         L.ref_vtrace.argtypes = [C.c_int, _dp, _dp, C.c_double, _dp, _dp, _u8p, C.c_double,
                                  C.c_double, C.c_double, _dp, _dp, _dp, _dp]

@@ -195,4 +195,39 @@ std::uint64_t ref_splitmix64(std::uint64_t x) { return splitmix64(x); }
 std::uint64_t ref_derive_seed(std::uint64_t s, std::uint64_t k) { return derive_seed(s, k); }
 std::uint64_t ref_fnv1a64(const void* p, std::size_t n) { return fnv1a64(p, n); }
 
+// policy.hpp:545-564 save_checkpoint of an init_params MLP (format-parity
+// fixture: the library's APPOCKP1 reader must read the reference's own files);
+// returns n_params, or -1 on error.  theta / m / v / version / t are set to
+// recognisable values first.
+long long ref_save_checkpoint_mlp(const char* path, int obs_dim, int trunk_hidden,
+                                  const int* heads, int n_heads, std::uint64_t seed,
+                                  long long version, long long t) {
+  long long n = -1;
+  guarded([&] {
+    ModelShape s;
+    s.obs_dim = obs_dim;
+    s.trunk_hidden = trunk_hidden;
+    s.heads.sizes.assign(heads, heads + n_heads);
+    PolicyParams p = init_params(s, seed);
+    for (std::size_t i = 0; i < p.theta.size(); ++i) {
+      p.adam.m[i] = 0.5 * p.theta[i];
+      p.adam.v[i] = p.theta[i] * p.theta[i];
+    }
+    p.version = version;
+    p.adam.t = t;
+    save_checkpoint(path, p);
+    n = (long long)p.theta.size();
+  });
+  return n;
+}
+std::uint64_t ref_spec_hash_mlp(int obs_dim, int hidden_dim, int trunk_hidden, const int* heads,
+                                int n_heads) {
+  ModelShape s;
+  s.obs_dim = obs_dim;
+  s.hidden_dim = hidden_dim;
+  s.trunk_hidden = trunk_hidden;
+  s.heads.sizes.assign(heads, heads + n_heads);
+  return s.spec_hash();
+}
+
 }  // extern "C"

@@ -101,6 +101,30 @@ class HParams(C.Structure):
         return HParams(**d)
 
 
+def checkpoint_read(path: str, arrays: bool = True) -> dict:
+    """Reads any APPOCKP1 file (also the reference's): header + f64 theta, m, v."""
+    h, ver, t, n = _u64(), C.c_int64(), C.c_int64(), _u64(0)
+    check(_L.appo_checkpoint_read_raw(os.fsencode(path), C.byref(h), C.byref(ver), C.byref(t),
+                                      C.byref(n), None))
+    out = {"spec_hash": h.value, "version": ver.value, "adam_t": t.value, "n": n.value}
+    if arrays:
+        buf = np.zeros(3 * n.value, dtype=np.float64)
+        check(_L.appo_checkpoint_read_raw(os.fsencode(path), None, None, None, C.byref(n),
+                                          buf.ctypes.data_as(C.c_void_p)))
+        k = n.value
+        out.update(theta=buf[:k], m=buf[k:2 * k], v=buf[2 * k:])
+    return out
+
+
+def model_spec_hash(desc) -> int:
+    return int(_L.appo_model_spec_hash(C.byref(desc)))
+
+
+def fnv1a64(data: bytes) -> int:
+    b = bytes(data)
+    return int(_L.appo_fnv1a64(C.c_char_p(b), len(b)))
+
+
 class StepOut(C.Structure):
     _fields_ = [("policy_loss", C.c_double), ("value_loss", C.c_double),
                 ("entropy", C.c_double), ("total_loss", C.c_double),
@@ -119,6 +143,12 @@ def _sig(name, res, *args):
 
 
 _sig("appo_last_error", C.c_char_p)
+_sig("appo_checkpoint_save", _i, _vp, C.c_char_p)
+_sig("appo_checkpoint_load", _i, _vp, C.c_char_p)
+_sig("appo_checkpoint_read_raw", _i, C.c_char_p, C.POINTER(_u64), C.POINTER(C.c_int64),
+     C.POINTER(C.c_int64), C.POINTER(_u64), _vp)
+_sig("appo_model_spec_hash", _u64, C.POINTER(ModelDesc))
+_sig("appo_fnv1a64", _u64, _vp, _u64)
 _sig("appo_capi_version", _i)
 _sig("appo_ctx_create", _i, C.POINTER(ModelDesc), _i, _u64, C.POINTER(_vp))
 _sig("appo_ctx_destroy", _i, _vp)
@@ -373,6 +403,14 @@ class Context:
     @property
     def version(self) -> int:
         return int(_L.appo_params_version(self.h))
+
+    def save_checkpoint(self, path: str):
+        """save_checkpoint (policy.hpp:545-564), APPOCKP1 format."""
+        check(_L.appo_checkpoint_save(self.h, os.fsencode(path)))
+
+    def load_checkpoint(self, path: str):
+        """load_checkpoint (policy.hpp:567-605): ConfigError on a shape mismatch."""
+        check(_L.appo_checkpoint_load(self.h, os.fsencode(path)))
 
     def policy_forward(self, obs, h_in, rng_counter0=0, want_logits=False, out=None):
         """Batched inference: obs u8 [B, C*H*W], h_in f32 [B, 512] (CUDA) ->

@@ -3,6 +3,7 @@
 // exception taxonomy, and one batched inference + learner step.
 #include <cmath>
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "appo_b200.hpp"
@@ -58,6 +59,14 @@ int main() {
   for (int a : ha) REQUIRE(a >= 0 && a < 6);
   std::vector<float> theta;
   REQUIRE(m.fetch(theta) == 0 && theta.size() == 2872551);
+  // checkpoint round trip into a differently seeded context
+  const std::string ck = "/tmp/capi_host_test.ckpt";
+  m.save_checkpoint(ck);
+  Context m2(0, 77, &desc);
+  std::vector<float> theta2;
+  m2.load_checkpoint(ck);
+  REQUIRE(m2.fetch(theta2) == 0 && theta2 == theta);
+  std::remove(ck.c_str());
   std::printf("capi_host_test ok\n");
   return 0;
 }
