@@ -247,6 +247,43 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
                                int32_t slot_base, int t, const uint8_t* h_obs,
                                int32_t* h_actions);
 
+/* ---- device slot queues: ready queue + free list ------------------------- */
+/* Replaces the host BoundedFifo ready_q drained by assemble_minibatch
+ * (trajstore.hpp:293-331; fed by RolloutWorker::submit_group,
+ * orchestrator.hpp:535-552) and the slot release after the learner step
+ * (orchestrator.hpp:870) with device-resident FIFOs of slot ids in
+ * [0, n_slots).  Pushes (any stream, any number of producers) keep the ids of
+ * one push contiguous and in order; pops (one consumer per queue) wait on the
+ * device until the whole request is published, up to timeout_s, and on timeout
+ * consume nothing and raise APPO_ERR_RESOURCE at the next sync/collect.
+ * capacity is rounded up to a power of two >= n_slots; at most capacity ids
+ * may be queued at once (each slot in at most one queue never overflows it).
+ * Kernels a consumer waits for must already be loaded (CUDA lazy loading):
+ * appo_slotq_create loads every kernel of this library. */
+typedef struct appo_slotq appo_slotq;
+APPO_API int appo_slotq_create(int device, int32_t n_slots, int32_t capacity, double timeout_s,
+                               appo_slotq** out);
+APPO_API int appo_slotq_destroy(appo_slotq* q);
+/* enqueue n device-resident ids / the range [first_id, first_id + n) on ctx's stream */
+APPO_API int appo_slotq_push(appo_ctx* ctx, appo_slotq* q, const int32_t* d_ids, int n);
+APPO_API int appo_slotq_push_range(appo_ctx* ctx, appo_slotq* q, int32_t first_id, int n);
+/* dequeue n ids (FIFO) into device memory d_out on ctx's stream */
+APPO_API int appo_slotq_pop(appo_ctx* ctx, appo_slotq* q, int32_t* d_out, int n);
+/* counters (synchronous read; call after syncing the streams that use q) */
+APPO_API int appo_slotq_stats(appo_slotq* q, int64_t* pushed, int64_t* popped, int64_t* timeouts);
+
+/* appo_learner_submit whose minibatch is the next n_traj slots of ready_q
+ * (assemble_minibatch: strict FIFO, lag statistics from the slots' versions);
+ * after the step the slots are pushed to free_q (may be NULL).  The host never
+ * sees the slot ids. */
+APPO_API int appo_learner_submit_queued(appo_ctx* ctx, const void* d_slot_region,
+                                        uint64_t slot_bytes, appo_slotq* ready_q,
+                                        appo_slotq* free_q, int n_traj, const appo_hparams* hp);
+
+/* The sampler pushes slots [slot_base, slot_base + n_envs) to q after writing
+ * step T-1 of a rollout (submit_group).  q = NULL detaches. */
+APPO_API int appo_sampler_set_ready_queue(appo_sampler* s, appo_slotq* q);
+
 #ifdef __cplusplus
 }
 #endif

@@ -190,6 +190,14 @@ _sig("appo_dp_init", _i, _vp, _i, _i, C.c_char_p)
 _sig("appo_sampler_create", _i, _vp, _i, _i, _u64, C.POINTER(_vp))
 _sig("appo_sampler_destroy", _i, _vp)
 _sig("appo_sampler_step", _i, _vp, _vp, _u64, C.c_int32, _i, _vp, _vp)
+_sig("appo_sampler_set_ready_queue", _i, _vp, _vp)
+_sig("appo_slotq_create", _i, _i, C.c_int32, C.c_int32, C.c_double, C.POINTER(_vp))
+_sig("appo_slotq_destroy", _i, _vp)
+_sig("appo_slotq_push", _i, _vp, _vp, _vp, _i)
+_sig("appo_slotq_push_range", _i, _vp, _vp, C.c_int32, _i)
+_sig("appo_slotq_pop", _i, _vp, _vp, _vp, _i)
+_sig("appo_slotq_stats", _i, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
+_sig("appo_learner_submit_queued", _i, _vp, _vp, _u64, _vp, _vp, _i, C.POINTER(HParams))
 
 LIB = _L
 
@@ -453,6 +461,17 @@ class Context:
         check(_L.appo_learner_submit(self.h, _ptr(region), slot_bytes,
                                      ids.ctypes.data_as(C.c_void_p), ids.size, C.byref(hp)))
 
+    def learner_submit_queued(self, region, slot_bytes: int, ready_q: "SlotQueue",
+                              free_q: "SlotQueue | None", n_traj: int,
+                              hp: HParams | None = None):
+        """Enqueue one learner step over the next n_traj slots of ``ready_q``
+        (popped on the device, FIFO); the slots go to ``free_q`` afterwards."""
+        _need_cuda(region)
+        hp = hp or HParams.defaults()
+        check(_L.appo_learner_submit_queued(self.h, _ptr(region), slot_bytes, ready_q.h,
+                                            free_q.h if free_q is not None else None, n_traj,
+                                            C.byref(hp)))
+
     def learner_collect(self):
         """Wait for submitted steps; stats of the last one (appo_learner_collect)."""
         out = StepOut()
@@ -522,6 +541,54 @@ class Sampler:
         """h_obs / h_actions: optional pinned host tensors (CPU-actor path)."""
         check(_L.appo_sampler_step(self.h, _ptr(store.region), store.slot_bytes, slot_base, t,
                                    _ptr(h_obs), _ptr(h_actions)))
+
+    def set_ready_queue(self, q: "SlotQueue | None"):
+        """After step T-1 of a rollout the written slots are pushed to ``q``."""
+        self._ready_q = q  # keep the queue alive while attached
+        check(_L.appo_sampler_set_ready_queue(self.h, q.h if q is not None else None))
+
+
+class SlotQueue:
+    """Device FIFO of slot ids (appo_slotq_*): the ready queue between rollout
+    writers and the learner (trajstore.hpp:293-331) or the free list."""
+
+    def __init__(self, device: int, n_slots: int, capacity: int = 0, timeout_s: float = 2.0):
+        h = C.c_void_p()
+        check(_L.appo_slotq_create(device, n_slots, capacity, timeout_s, C.byref(h)))
+        self.h = h
+        self.n_slots = n_slots
+
+    def close(self):
+        if getattr(self, "h", None):
+            _L.appo_slotq_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def push(self, ctx: Context, ids):
+        """ids: int32 CUDA tensor, enqueued in order on ctx's stream."""
+        _need_cuda(ids)
+        check(_L.appo_slotq_push(ctx.h, self.h, _ptr(ids), ids.numel()))
+
+    def push_range(self, ctx: Context, first: int, n: int):
+        check(_L.appo_slotq_push_range(ctx.h, self.h, first, n))
+
+    def pop(self, ctx: Context, n: int, out=None):
+        import torch
+        if out is None:
+            out = torch.empty(n, dtype=torch.int32, device=f"cuda:{ctx.device}")
+        check(_L.appo_slotq_pop(ctx.h, self.h, _ptr(out), n))
+        return out
+
+    def stats(self) -> dict:
+        p, q, t = _i64(), _i64(), _i64()
+        check(_L.appo_slotq_stats(self.h, C.byref(p), C.byref(q), C.byref(t)))
+        return {"pushed": p.value, "popped": q.value, "timeouts": t.value,
+                "size": p.value - q.value}
 
 
 EPI_BIAS, EPI_ELU, EPI_DELU, EPI_BF16, EPI_TRANS, EPI_ACCUM = 1, 2, 4, 8, 16, 32

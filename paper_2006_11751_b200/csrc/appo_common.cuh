@@ -26,7 +26,7 @@ struct TimedLaunch {
 };
 
 // Device flag slots raised by kernels; read by appo_ctx_sync.
-enum : int { kFlagNumeric = 0, kFlagContract = 1, kNumFlags = 4 };
+enum : int { kFlagNumeric = 0, kFlagContract = 1, kFlagQueue = 2, kNumFlags = 4 };
 
 struct Ctx {
   int device = 0;

@@ -152,9 +152,13 @@ int appo_ctx_sync(appo_ctx* ctx) {
   APPO_CUDA_TRY(cudaMemcpyAsync(flags, ctx->d_flags, sizeof(flags), cudaMemcpyDeviceToHost,
                                 ctx->stream));
   APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (flags[kFlagNumeric] || flags[kFlagContract]) {
+  if (flags[kFlagNumeric] || flags[kFlagContract] || flags[kFlagQueue]) {
     APPO_CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(flags), ctx->stream));
     APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (flags[kFlagQueue]) {
+      set_error("slot queue: timed out waiting on the device for published slot ids");
+      return APPO_ERR_RESOURCE;
+    }
     if (flags[kFlagContract]) {
       set_error("contract violation detected on device (action index out of range?)");
       return APPO_ERR_CONTRACT;

@@ -1480,6 +1480,9 @@ int dispatch_major(Ctx* c, bool amn, bool bmn, const CUtensorMap& ma, const CUte
 
 }  // namespace
 
+// module anchor for preload_library_kernels (slotq.cu)
+const void* kanchor_gemm() { return reinterpret_cast<const void*>(&splitk_reduce_kernel); }
+
 int gemm_workspace(Ctx* c, size_t bytes, float** out) {
   if (bytes > c->ws_bytes) {
     if (c->d_ws) {

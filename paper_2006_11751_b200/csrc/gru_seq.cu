@@ -759,6 +759,9 @@ void prof_report(Ctx* c, long long* d, int steps, const char* what) {
 
 }  // namespace
 
+// module anchor for preload_library_kernels (slotq.cu)
+const void* kanchor_gru() { return reinterpret_cast<const void*>(&gru_seq_fwd_kernel); }
+
 int gru_seq_supported(int n_traj) { return n_traj >= 1 && n_traj <= MAXTRAJ; }
 
 int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* whh,

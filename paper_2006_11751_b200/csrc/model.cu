@@ -17,6 +17,7 @@
 #include "gemm.cuh"
 #include "model.cuh"
 #include "model_kernels.cuh"
+#include "slotq.cuh"
 
 namespace appo_b200 {
 
@@ -582,13 +583,19 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
                        d_h_out, d_values, d_logits, h_version_out);
 }
 
-int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
-                        const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp) {
+// h_slot_ids != null: ids from the host (FIFO order given by the caller);
+// else ids popped on the device from rq (FIFO arrival order) and, when fq is
+// set, returned to fq after the last kernel reading the slots.
+static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
+                               const int32_t* h_slot_ids, appo_slotq* rq, appo_slotq* fq,
+                               int n_traj, const appo_hparams* hp) {
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
   const Dims& d = M->d;
-  APPO_REQUIRE(hp && d_region && h_slot_ids && n_traj >= 1, APPO_ERR_CONTRACT,
+  APPO_REQUIRE(hp && d_region && (h_slot_ids || rq) && n_traj >= 1, APPO_ERR_CONTRACT,
                "learner_step: bad arguments");
+  APPO_REQUIRE(!rq || (uint32_t)n_traj <= rq->capacity, APPO_ERR_CONTRACT,
+               "learner_step: minibatch larger than the ready queue");
   APPO_REQUIRE(slot_bytes >= d.slot[9], APPO_ERR_CONTRACT,
                "learner_step: slot_bytes smaller than the layout v2 slot");
   APPO_REQUIRE(n_traj <= 4096, APPO_ERR_CONTRACT, "learner_step: at most 4096 trajectories");
@@ -618,9 +625,14 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   APPO_CUDA_TRY(cudaEventSynchronize(M->ring_ev[ring]));
   double* h_st = M->ring_host + (size_t)ring * Model::kRingStride;
   int32_t* h_ids = reinterpret_cast<int32_t*>(h_st + 16);
-  std::memcpy(h_ids, h_slot_ids, sizeof(int32_t) * n_traj);
-  APPO_CUDA_TRY(cudaMemcpyAsync(s.slot_ids, h_ids, sizeof(int32_t) * n_traj,
-                                cudaMemcpyHostToDevice, st));
+  int* q_ok = reinterpret_cast<int*>(ctx->d_counter + 9);
+  if (h_slot_ids) {
+    std::memcpy(h_ids, h_slot_ids, sizeof(int32_t) * n_traj);
+    APPO_CUDA_TRY(cudaMemcpyAsync(s.slot_ids, h_ids, sizeof(int32_t) * n_traj,
+                                  cudaMemcpyHostToDevice, st));
+  } else {
+    TRY(slotq_pop_launch(ctx, rq, s.slot_ids, n_traj, q_ok));
+  }
   SlotOffsets off;
   std::memcpy(&off, d.slot, sizeof(off));
   TRY(k_gather_slots(ctx, n_traj, T, region, slot_bytes, s.slot_ids, off, s.act, s.rew, s.blogp,
@@ -635,10 +647,12 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   src.boot_off = d.slot[7];
   src.T = T;
   src.n_traj = n_traj;
-  {
+  if (h_slot_ids) {
     int mx = 0;
     for (int i = 0; i < n_traj; ++i) mx = h_slot_ids[i] > mx ? h_slot_ids[i] : mx;
     src.n_slots = mx + 1;
+  } else {
+    src.n_slots = rq->n_slots;
   }
   src.obs_dim = d.obs_dim;
   // learner: every convolution gathers its input by TMA (so do the weight
@@ -826,6 +840,8 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
       return wst;
     }
   }
+  // the slots are no longer read: hand them back (free list, orchestrator.hpp:870)
+  if (fq) TRY(slotq_push_launch(ctx, fq, s.slot_ids, 0, n_traj, q_ok));
 
   // ---- data-parallel: average the gradient over ranks before clip + Adam ----
   TRY(dp_allreduce_grad(ctx, G, d.total));
@@ -853,6 +869,21 @@ int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes
   M->version += 1;
   M->pending += 1;
   return APPO_OK;
+}
+
+int appo_learner_submit(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
+                        const int32_t* h_slot_ids, int n_traj, const appo_hparams* hp) {
+  APPO_REQUIRE(h_slot_ids != nullptr, APPO_ERR_CONTRACT, "learner_step: null slot ids");
+  return learner_submit_impl(ctx, d_region, slot_bytes, h_slot_ids, nullptr, nullptr, n_traj, hp);
+}
+
+int appo_learner_submit_queued(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
+                               appo_slotq* ready_q, appo_slotq* free_q, int n_traj,
+                               const appo_hparams* hp) {
+  APPO_REQUIRE(ready_q != nullptr, APPO_ERR_CONTRACT, "learner_step: null ready queue");
+  APPO_REQUIRE(!free_q || free_q->n_slots >= ready_q->n_slots, APPO_ERR_CONTRACT,
+               "learner_step: free queue smaller than the ready queue's slot range");
+  return learner_submit_impl(ctx, d_region, slot_bytes, nullptr, ready_q, free_q, n_traj, hp);
 }
 
 // Waits for the submitted learner steps; reports the last one's statistics

@@ -819,6 +819,9 @@ int grid_for(int64_t n, int block, int max_blocks) {
 
 }  // namespace
 
+// module anchor for preload_library_kernels (slotq.cu)
+const void* kanchor_model() { return reinterpret_cast<const void*>(&im2col_u8_kernel); }
+
 int k_im2col_u8(Ctx* c, const ObsSrc& src, int64_t R, const Dims& d, uint16_t* col) {
   const int64_t n = R * d.P1 * d.C * 8;
   c->next_bytes = (double)R * d.obs_dim + (double)R * d.P1 * d.K1 * 2;

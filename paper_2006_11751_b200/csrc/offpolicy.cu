@@ -266,6 +266,9 @@ __global__ void sample_kernel(int B, int A, const float* __restrict__ logits, ui
 
 }  // namespace
 
+// module anchor for preload_library_kernels (slotq.cu)
+const void* kanchor_offpolicy() { return reinterpret_cast<const void*>(&logp_entropy_kernel); }
+
 int launch_vtrace(Ctx* c, int n_traj, int T, const float* r, const float* v, const float* boot,
                   const float* tl, const float* bl, const uint8_t* d, float gamma, float rho_bar,
                   float c_bar, float* v_out, float* pg_out, float* rho_out, float* c_out) {

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ norm_in, float lr, float b1, float b2, float eps,
                 float bc1, float bc2, __nv_bfloat16* __restrict__ bf16, float* __restrict__ f32,
                 const int* flags, unsigned* applied) {
-  if (flags[kFlagNumeric] | flags[kFlagContract]) {
+  if (flags[kFlagNumeric] | flags[kFlagContract] | flags[kFlagQueue]) {
     // the step threw before Adam: parameters untouched, but the publish target
     // still receives the current parameters so the published copy stays valid
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -102,6 +102,9 @@ __global__ void __launch_bounds__(256)
 }
 
 }  // namespace
+
+// module anchor for preload_library_kernels (slotq.cu)
+const void* kanchor_optim() { return reinterpret_cast<const void*>(&sumsq_kernel); }
 
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,

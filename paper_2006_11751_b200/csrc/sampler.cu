@@ -23,6 +23,7 @@
 #include "gemm.cuh"
 #include "model.cuh"
 #include "model_kernels.cuh"
+#include "slotq.cuh"
 
 namespace appo_b200 {
 int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, const float* h_in,
@@ -45,6 +46,7 @@ struct appo_sampler {
   float* logp = nullptr;
   float* values = nullptr;
   uint64_t steps_done = 0;
+  appo_slotq* ready_q = nullptr;  // sealed slots are pushed here at t == T-1
 };
 
 namespace {
@@ -133,6 +135,11 @@ __global__ void init_env_kernel(int n_envs, int episode_len, uint32_t* step, uin
 }
 
 }  // namespace
+
+// module anchor for preload_library_kernels (slotq.cu)
+namespace appo_b200 {
+const void* kanchor_sampler() { return reinterpret_cast<const void*>(&init_env_kernel); }
+}  // namespace appo_b200
 
 #define SMP_OR_RETURN(s)                                                            \
   do {                                                                              \
@@ -232,10 +239,25 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
     APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
                 s->episode, region, slot_bytes, (int64_t)slot_base, d.slot[7]);
   }
+  if (t == d.T - 1 && s->ready_q) {
+    // submit_group: the sealed trajectories enter the ready queue in env order
+    APPO_REQUIRE((int64_t)slot_base + s->n_envs <= s->ready_q->n_slots, APPO_ERR_CONTRACT,
+                 "sampler_step: slots outside the ready queue's range");
+    const int pst = slotq_push_launch(c, s->ready_q, nullptr, slot_base, s->n_envs, nullptr);
+    if (pst != APPO_OK) return pst;
+  }
   if (h_actions)
     APPO_CUDA_TRY(cudaMemcpyAsync(h_actions, s->actions, sizeof(int32_t) * s->n_envs,
                                   cudaMemcpyDeviceToHost, c->stream));
   s->steps_done++;
+  return APPO_OK;
+}
+
+int appo_sampler_set_ready_queue(appo_sampler* s, appo_slotq* q) {
+  SMP_OR_RETURN(s);
+  APPO_REQUIRE(!q || (uint32_t)s->n_envs <= q->capacity, APPO_ERR_CONTRACT,
+               "sampler_set_ready_queue: queue smaller than one rollout group");
+  s->ready_q = q;
   return APPO_OK;
 }
 
