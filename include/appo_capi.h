@@ -284,6 +284,72 @@ APPO_API int appo_learner_submit_queued(appo_ctx* ctx, const void* d_slot_region
  * step T-1 of a rollout (submit_group).  q = NULL detaches. */
 APPO_API int appo_sampler_set_ready_queue(appo_sampler* s, appo_slotq* q);
 
+/* ---- population-based training over per-GPU learners --------------------- */
+/* pbt_step (population.hpp:131-186) and PbtController (runner.hpp:169-252):
+ * per-policy score windows (ScoreWindow, population.hpp:72-98), PBT steps on
+ * pbt_period frame boundaries, mutation of the bottom cohort, weight +
+ * hyper-parameter exchange into the worst cohort through copy_weights.  The
+ * decision stream is the reference's std::mt19937_64 stream: seeded alike, it
+ * reproduces the reference's decision log byte for byte. */
+#define APPO_PBT_MAX_REWARD_WEIGHTS 8
+typedef struct {
+  int64_t pbt_period;           /* frames between PBT steps (<= 0: never)    */
+  double mutate_fraction;       /* 0.70 */
+  double mutation_rate;         /* 0.15, per hyper-parameter                 */
+  double mutation_factor;       /* 1.2 */
+  double replace_fraction;      /* 0.30 */
+  double exchange_threshold;    /* win-rate gap gate (0.35 in duel mode)     */
+  int32_t has_exchange_threshold;
+  int32_t window;               /* ScoreWindow capacity, 100                 */
+} appo_pbt_config;
+typedef struct {                /* AgentMeta (population.hpp:41-58) */
+  uint32_t policy_id;
+  int32_t n_reward_weights;
+  double learning_rate, entropy_coef, adam_beta1;
+  double reward_weights[APPO_PBT_MAX_REWARD_WEIGHTS];
+} appo_agent_meta;
+typedef struct {                /* PbtEvent (population.hpp:100-107) */
+  int64_t frame;
+  uint32_t agent;
+  int32_t event;                /* 0 mutate, 1 exchange, 2 skip-threshold    */
+  char field[32];
+  double old_value, new_value;
+} appo_pbt_event;
+/* copy_weights(dst, src): dst learner takes src's theta + Adam state */
+typedef int (*appo_pbt_copy_fn)(void* user, uint32_t dst, uint32_t src);
+typedef struct appo_pbt appo_pbt;
+
+/* init may be NULL (lr 1e-4, entropy 0.003, beta1 0.9, no reward weights);
+ * policy ids are 0..P-1.  rng_seed seeds the decision stream directly; the
+ * reference controller uses appo_pbt_controller_seed(pipeline seed). */
+APPO_API int appo_pbt_create(const appo_pbt_config* cfg, int P, uint64_t rng_seed,
+                             const appo_agent_meta* init, appo_pbt** out);
+APPO_API int appo_pbt_destroy(appo_pbt* pbt);
+APPO_API uint64_t appo_pbt_controller_seed(uint64_t pipeline_seed);
+/* an episode result of policy: return, or 1/0 for win/(tie, loss) */
+APPO_API int appo_pbt_record(appo_pbt* pbt, uint32_t policy, double value);
+APPO_API int appo_pbt_score(appo_pbt* pbt, uint32_t policy, double* score, int* has_score);
+/* one PBT step on explicit scores (has_score[i] == 0: exempt) */
+APPO_API int appo_pbt_step(appo_pbt* pbt, const double* scores, const uint8_t* has_score,
+                           int64_t frame, appo_pbt_copy_fn copy_weights, void* user,
+                           appo_pbt_event* events, int max_events, int* n_events);
+/* PbtController::tick: a step on the window scores once frames reach the next
+ * period boundary (*fired = 1), else nothing */
+APPO_API int appo_pbt_tick(appo_pbt* pbt, int64_t frames, appo_pbt_copy_fn copy_weights,
+                           void* user, appo_pbt_event* events, int max_events, int* n_events,
+                           int* fired);
+APPO_API int appo_pbt_get_agent(appo_pbt* pbt, int i, appo_agent_meta* out);
+APPO_API int appo_pbt_max_events(appo_pbt* pbt);
+/* CSV text of append_pbt_events_csv (population.hpp:110-118) */
+APPO_API int appo_pbt_format_events(const appo_pbt_event* events, int n, int header, char* buf,
+                                    uint64_t cap, uint64_t* len);
+/* dst takes src's parameters and Adam state (device to device, peer copy
+ * across GPUs) and publishes them as its next version (PbtController's
+ * copy_weights, runner.hpp:211-219); dst must have no uncollected steps */
+APPO_API int appo_params_copy(appo_ctx* dst, appo_ctx* src);
+/* copy_weights over user = appo_ctx*[P] (learner of policy i at index i) */
+APPO_API int appo_pbt_copy_contexts(void* user, uint32_t dst, uint32_t src);
+
 #ifdef __cplusplus
 }
 #endif

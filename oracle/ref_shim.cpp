@@ -10,10 +10,12 @@
 // path.  No reference source is copied into this repository; this file only
 // includes the headers and forwards arguments.
 #include <cstring>
+#include <sstream>
 #include <random>
 #include <vector>
 
 #include "appo/offpolicy.hpp"
+#include "appo/population.hpp"
 #include "appo/policy.hpp"
 #include "appo/trajstore.hpp"
 
@@ -228,6 +230,44 @@ std::uint64_t ref_spec_hash_mlp(int obs_dim, int hidden_dim, int trunk_hidden, c
   s.trunk_hidden = trunk_hidden;
   s.heads.sizes.assign(heads, heads + n_heads);
   return s.spec_hash();
+}
+
+// pbt_step (population.hpp:131-186) over `periods` periods of the synthetic
+// score schedule of acceptance.cpp's PBT criterion (P agents, reward weights
+// {1.0, 0.2, -0.5}, every third period compressed below the threshold);
+// writes the CSV decision log (with header) and returns its length, or -1
+// when cap is too small.  threshold < 0: no exchange gate.
+long ref_pbt_log(int P, std::uint64_t seed, int periods, double threshold, char* buf,
+                 std::size_t cap) {
+  PopulationConfig cfg;
+  cfg.P = static_cast<std::uint32_t>(P);
+  if (threshold >= 0.0) cfg.exchange_threshold = threshold;
+  std::mt19937_64 rng(seed);
+  std::vector<AgentMeta> agents(P);
+  for (int i = 0; i < P; ++i) {
+    agents[i].policy_id = static_cast<std::uint32_t>(i);
+    agents[i].reward_weights = {1.0, 0.2, -0.5};
+  }
+  std::vector<PbtEvent> all;
+  for (int period = 0; period < periods; ++period) {
+    std::vector<std::optional<double>> scores(P);
+    for (int i = 0; i < P; ++i) {
+      const double base = ((i * 13 + period * 7) % 23) / 23.0;
+      scores[i] = (period % 3 == 2) ? 0.5 + 0.2 * base : base;
+    }
+    auto ev = pbt_step(agents, scores, cfg, rng, period * 5000000LL,
+                       [](std::uint32_t, std::uint32_t) {});
+    all.insert(all.end(), ev.begin(), ev.end());
+  }
+  std::ostringstream log;
+  log << "frame,agent,event,field,old,new\n";
+  for (const auto& e : all)
+    log << e.frame << ',' << e.agent << ',' << e.event << ',' << e.field << ',' << e.old_value
+        << ',' << e.new_value << "\n";
+  const std::string t = log.str();
+  if (t.size() + 1 > cap) return -1;
+  std::memcpy(buf, t.c_str(), t.size() + 1);
+  return static_cast<long>(t.size());
 }
 
 }  // extern "C"

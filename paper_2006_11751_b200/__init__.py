@@ -197,6 +197,17 @@ _sig("appo_slotq_push", _i, _vp, _vp, _vp, _i)
 _sig("appo_slotq_push_range", _i, _vp, _vp, C.c_int32, _i)
 _sig("appo_slotq_pop", _i, _vp, _vp, _vp, _i)
 _sig("appo_slotq_stats", _i, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
+_sig("appo_params_copy", _i, _vp, _vp)
+_sig("appo_pbt_create", _i, C.c_void_p, _i, _u64, _vp, C.POINTER(_vp))
+_sig("appo_pbt_destroy", _i, _vp)
+_sig("appo_pbt_controller_seed", _u64, _u64)
+_sig("appo_pbt_record", _i, _vp, C.c_uint32, C.c_double)
+_sig("appo_pbt_score", _i, _vp, C.c_uint32, C.POINTER(C.c_double), C.POINTER(_i))
+_sig("appo_pbt_step", _i, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i, C.POINTER(_i))
+_sig("appo_pbt_tick", _i, _vp, _i64, _vp, _vp, _vp, _i, C.POINTER(_i), C.POINTER(_i))
+_sig("appo_pbt_get_agent", _i, _vp, _i, _vp)
+_sig("appo_pbt_max_events", _i, _vp)
+_sig("appo_pbt_format_events", _i, _vp, _i, _i, C.c_char_p, _u64, C.POINTER(_u64))
 _sig("appo_learner_submit_queued", _i, _vp, _vp, _u64, _vp, _vp, _i, C.POINTER(HParams))
 
 LIB = _L
@@ -589,6 +600,171 @@ class SlotQueue:
         check(_L.appo_slotq_stats(self.h, C.byref(p), C.byref(q), C.byref(t)))
         return {"pushed": p.value, "popped": q.value, "timeouts": t.value,
                 "size": p.value - q.value}
+
+
+# ---------------------------------------------------------------- PBT
+PBT_MAX_REWARD_WEIGHTS = 8
+PBT_EVENTS = ("mutate", "exchange", "skip-threshold")
+
+
+class PbtConfig(C.Structure):
+    """PopulationConfig (population.hpp:22-37) + ScoreWindow capacity."""
+    _fields_ = [("pbt_period", C.c_int64), ("mutate_fraction", C.c_double),
+                ("mutation_rate", C.c_double), ("mutation_factor", C.c_double),
+                ("replace_fraction", C.c_double), ("exchange_threshold", C.c_double),
+                ("has_exchange_threshold", C.c_int32), ("window", C.c_int32)]
+
+    @staticmethod
+    def defaults(exchange_threshold=None, **kw) -> "PbtConfig":
+        d = dict(pbt_period=5_000_000, mutate_fraction=0.70, mutation_rate=0.15,
+                 mutation_factor=1.2, replace_fraction=0.30, window=100)
+        d.update(kw)
+        c = PbtConfig(**d)
+        if exchange_threshold is not None:
+            c.has_exchange_threshold = 1
+            c.exchange_threshold = exchange_threshold
+        return c
+
+
+class AgentMeta(C.Structure):
+    """AgentMeta (population.hpp:41-58)."""
+    _fields_ = [("policy_id", C.c_uint32), ("n_reward_weights", C.c_int32),
+                ("learning_rate", C.c_double), ("entropy_coef", C.c_double),
+                ("adam_beta1", C.c_double),
+                ("reward_weights", C.c_double * PBT_MAX_REWARD_WEIGHTS)]
+
+    @staticmethod
+    def make(learning_rate=1e-4, entropy_coef=0.003, adam_beta1=0.9, reward_weights=()):
+        a = AgentMeta(0, len(reward_weights), learning_rate, entropy_coef, adam_beta1)
+        for i, w in enumerate(reward_weights):
+            a.reward_weights[i] = w
+        return a
+
+    def as_dict(self):
+        return {"policy_id": self.policy_id, "learning_rate": self.learning_rate,
+                "entropy_coef": self.entropy_coef, "adam_beta1": self.adam_beta1,
+                "reward_weights": list(self.reward_weights[:self.n_reward_weights])}
+
+
+class PbtEvent(C.Structure):
+    _fields_ = [("frame", C.c_int64), ("agent", C.c_uint32), ("event", C.c_int32),
+                ("field", C.c_char * 32), ("old_value", C.c_double), ("new_value", C.c_double)]
+
+    def as_tuple(self):
+        return (self.frame, self.agent, PBT_EVENTS[self.event], self.field.decode(),
+                self.old_value, self.new_value)
+
+
+PBT_COPY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32)
+
+
+def params_copy(dst: "Context", src: "Context"):
+    """dst learner takes src's parameters + Adam state and publishes them."""
+    check(_L.appo_params_copy(dst.h, src.h))
+
+
+class PbtController:
+    """Population-based training over P learners (appo_pbt_*; population.hpp
+    pbt_step + runner.hpp PbtController).  copy_weights: None, a list of
+    learner Contexts (device-to-device copies), or a Python callable
+    ``f(dst, src)``."""
+
+    def __init__(self, cfg: PbtConfig, P: int, seed: int, init=None, copy_weights=None,
+                 pipeline_seed: bool = False):
+        if pipeline_seed:
+            seed = int(_L.appo_pbt_controller_seed(seed))
+        arr = None
+        if init is not None:
+            arr = (AgentMeta * P)(*init)
+        h = C.c_void_p()
+        check(_L.appo_pbt_create(C.byref(cfg), P, seed, arr, C.byref(h)))
+        self.h, self.P = h, P
+        self._set_copy(copy_weights)
+
+    def _set_copy(self, copy_weights):
+        self._user = None
+        if copy_weights is None:
+            self._fn = None
+        elif isinstance(copy_weights, (list, tuple)):
+            self._learners = list(copy_weights)
+            self._user = (C.c_void_p * len(copy_weights))(*[c.h.value for c in copy_weights])
+            self._fn = C.cast(_L.appo_pbt_copy_contexts, C.c_void_p)
+        else:
+            def tramp(_user, dst, src, f=copy_weights):
+                try:
+                    f(dst, src)
+                    return 0
+                except Exception:  # surfaced as a ContractError by the library
+                    return 1
+            self._cb = PBT_COPY_FN(tramp)
+            self._fn = C.cast(self._cb, C.c_void_p)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _L.appo_pbt_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _events(self, buf, n):
+        return [buf[i] for i in range(n)]
+
+    def step(self, scores, frame: int):
+        """One pbt_step; scores: list of float or None (exempt)."""
+        sc = np.array([0.0 if s is None else float(s) for s in scores], dtype=np.float64)
+        has = np.array([s is not None for s in scores], dtype=np.uint8)
+        assert sc.size == self.P
+        cap = int(_L.appo_pbt_max_events(self.h))
+        buf = (PbtEvent * cap)()
+        n = _i()
+        check(_L.appo_pbt_step(self.h, sc.ctypes.data_as(C.c_void_p),
+                               has.ctypes.data_as(C.c_void_p), frame, self._fn,
+                               C.cast(self._user, C.c_void_p) if self._user else None, buf, cap,
+                               C.byref(n)))
+        return self._events(buf, n.value)
+
+    def record(self, policy: int, value: float):
+        check(_L.appo_pbt_record(self.h, policy, value))
+
+    def score(self, policy: int):
+        s, has = C.c_double(), _i()
+        check(_L.appo_pbt_score(self.h, policy, C.byref(s), C.byref(has)))
+        return s.value if has.value else None
+
+    def tick(self, frames: int):
+        """PbtController::tick: returns the events of a step, or None."""
+        cap = int(_L.appo_pbt_max_events(self.h))
+        buf = (PbtEvent * cap)()
+        n, fired = _i(), _i()
+        check(_L.appo_pbt_tick(self.h, frames, self._fn,
+                               C.cast(self._user, C.c_void_p) if self._user else None, buf, cap,
+                               C.byref(n), C.byref(fired)))
+        return self._events(buf, n.value) if fired.value else None
+
+    def agent(self, i: int) -> AgentMeta:
+        a = AgentMeta()
+        check(_L.appo_pbt_get_agent(self.h, i, C.byref(a)))
+        return a
+
+    def hparams(self, i: int, base: HParams | None = None) -> HParams:
+        """Learner hyper-parameters of policy i (HyperBlock hand-back, runner.hpp:222-232)."""
+        a = self.agent(i)
+        hp = HParams.defaults() if base is None else HParams.from_buffer_copy(base)
+        hp.lr, hp.entropy_coef, hp.beta1 = a.learning_rate, a.entropy_coef, a.adam_beta1
+        return hp
+
+    @staticmethod
+    def format_events(events, header: bool = True) -> str:
+        arr = (PbtEvent * max(1, len(events)))(*events)
+        ln = _u64()
+        check(_L.appo_pbt_format_events(arr, len(events), int(header), None, 0, C.byref(ln)))
+        out = C.create_string_buffer(ln.value + 1)
+        check(_L.appo_pbt_format_events(arr, len(events), int(header), out, ln.value + 1, None))
+        return out.value.decode()
 
 
 EPI_BIAS, EPI_ELU, EPI_DELU, EPI_BF16, EPI_TRANS, EPI_ACCUM = 1, 2, 4, 8, 16, 32

@@ -562,6 +562,54 @@ int appo_adam_set(appo_ctx* ctx, const float* h_m, const float* h_v, int64_t t) 
   return APPO_OK;
 }
 
+// PbtController's copy_weights (runner.hpp:211-219): dst takes src's theta and
+// Adam state and publishes them as its next version.  Device to device (peer
+// copy over NVLink when the learners live on different GPUs), ordered after
+// src's queued work; dst must have no uncollected learner steps.
+int appo_params_copy(appo_ctx* dst, appo_ctx* src) {
+  MODEL_OR_RETURN(dst);
+  MODEL_OR_RETURN(src);
+  Model* D = dst->model;
+  Model* S = src->model;
+  APPO_REQUIRE(dst != src && D != S, APPO_ERR_CONTRACT, "params_copy: same learner");
+  APPO_REQUIRE(D->d.total == S->d.total && dst->desc.obs_c == src->desc.obs_c &&
+                   dst->desc.obs_h == src->desc.obs_h && dst->desc.obs_w == src->desc.obs_w &&
+                   dst->desc.n_actions == src->desc.n_actions,
+               APPO_ERR_CONFIG, "params_copy: different model shapes");
+  APPO_REQUIRE(D->pending == 0, APPO_ERR_CONTRACT,
+               "params_copy: collect the destination's learner steps first");
+  const int64_t P = D->d.total;
+  // src's published state is final once its stream drained (its version and
+  // adam_t are host values advanced at submit)
+  APPO_CUDA_TRY(cudaSetDevice(src->device));
+  APPO_CUDA_TRY(cudaStreamSynchronize(src->stream));
+  APPO_CUDA_TRY(cudaSetDevice(dst->device));
+  cudaStream_t st = dst->stream;
+  const int next = (D->published + 1) % Model::kPub;
+  APPO_CUDA_TRY(cudaStreamWaitEvent(st, D->pub_ev[next], 0));
+  auto copy = [&](float* to, const float* from) -> int {
+    if (dst->device == src->device)
+      APPO_CUDA_TRY(cudaMemcpyAsync(to, from, P * 4, cudaMemcpyDeviceToDevice, st));
+    else
+      APPO_CUDA_TRY(cudaMemcpyPeerAsync(to, dst->device, from, src->device, P * 4, st));
+    return APPO_OK;
+  };
+  TRY(copy(D->theta, S->theta));
+  TRY(copy(D->m, S->m));
+  TRY(copy(D->v, S->v));
+  APPO_CUDA_TRY(cudaMemcpyAsync(D->pub_f32[next], D->theta, P * 4, cudaMemcpyDeviceToDevice, st));
+  TRY(k_f32_to_bf16(dst, 1, D->theta, P, D->pub_bf16[next], P, (int)P));
+  TRY(k_publish_derived(dst, D->pub_bf16[next], D->pub_f32[next], D->d, D->pub_c1h[next],
+                        D->pub_c1b[next], D->pub_wt2[next], D->pub_wt3[next]));
+  APPO_CUDA_TRY(cudaEventRecord(D->ready_ev[next], st));
+  D->adam_t = S->adam_t;
+  D->pub_version[next] = D->version + 1;
+  D->published_prev = D->published;
+  D->published = next;
+  D->version += 1;  // ParamStore::publish of the copied weights
+  return APPO_OK;
+}
+
 int64_t appo_params_version(appo_ctx* ctx) {
   return (ctx && ctx->model) ? ctx->model->version : -1;
 }
