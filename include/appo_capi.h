@@ -102,6 +102,12 @@ APPO_API int appo_ctx_set_stream(appo_ctx* ctx, void* cuda_stream);
 /* Size persistent / grid-stride grids of this context for n_sms SMs (default:
  * all), leaving the rest to a concurrently running context (e.g. the learner). */
 APPO_API int appo_ctx_set_sm_budget(appo_ctx* ctx, int n_sms);
+/* Programmatic dependent launch for this context's kernels: the next
+ * kernel's launch and prologue overlap the current kernel's tail.  Default:
+ * on for contexts that own a model (learners), off for shared contexts
+ * (samplers running next to a learner); env APPO_PDL=0/1/B/S overrides
+ * (none / all / owners only / shared only). */
+APPO_API int appo_ctx_set_pdl(appo_ctx* ctx, int enable);
 APPO_API int appo_ctx_sync(appo_ctx* ctx);
 /* Number of launches of this library's kernels enqueued on ctx so far. */
 APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);

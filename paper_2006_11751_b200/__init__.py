@@ -154,6 +154,7 @@ _sig("appo_ctx_create", _i, C.POINTER(ModelDesc), _i, _u64, C.POINTER(_vp))
 _sig("appo_ctx_destroy", _i, _vp)
 _sig("appo_ctx_create_shared", _i, _vp, C.POINTER(_vp))
 _sig("appo_ctx_set_sm_budget", _i, _vp, _i)
+_sig("appo_ctx_set_pdl", _i, _vp, _i)
 _sig("appo_ctx_set_stream", _i, _vp, _vp)
 _sig("appo_ctx_sync", _i, _vp)
 _sig("appo_ctx_launch_count", _i64, _vp)
@@ -280,6 +281,10 @@ class Context:
 
     def set_sm_budget(self, n_sms: int):
         check(_L.appo_ctx_set_sm_budget(self.h, n_sms))
+
+    def set_pdl(self, enable: bool):
+        """Programmatic dependent launch of this context's kernels."""
+        check(_L.appo_ctx_set_pdl(self.h, int(enable)))
 
     def close(self):
         if getattr(self, "h", None):

@@ -77,6 +77,7 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
   c->seed = seed;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (c->num_sms <= 0) c->num_sms = 148;
+  c->pdl = pdl_default(false);
   if (cudaMalloc(&c->d_flags, sizeof(int) * kNumFlags) != cudaSuccess ||
       cudaMalloc(&c->d_red, sizeof(double) * kRedSlots) != cudaSuccess ||
       cudaMalloc(&c->d_counter, sizeof(unsigned) * 16) != cudaSuccess ||
@@ -101,6 +102,12 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
   return APPO_OK;
 }
 
+int appo_ctx_set_pdl(appo_ctx* ctx, int enable) {
+  CTX_OR_RETURN(ctx);
+  ctx->pdl = enable != 0;
+  return APPO_OK;
+}
+
 int appo_ctx_create_shared(appo_ctx* base, appo_ctx** out) {
   APPO_REQUIRE(base && base->model && out, APPO_ERR_CONTRACT,
                "appo_ctx_create_shared: base context with a model required");
@@ -111,6 +118,7 @@ int appo_ctx_create_shared(appo_ctx* base, appo_ctx** out) {
   c->desc = base->desc;
   c->model = base->model;
   c->owns_model = false;
+  c->pdl = pdl_default(true);
   *out = c;
   return APPO_OK;
 }

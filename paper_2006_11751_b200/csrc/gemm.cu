@@ -761,6 +761,9 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above is local (barriers, TMEM, descriptor prefetch): overlap
+  // it with the previous kernel's tail, then wait for its results
+  APPO_PDL_ENTRY();
 
   const int units = p.tiles_m * p.tiles_n * p.splits;
 
@@ -1195,6 +1198,7 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
 // flight for the partial stream even when M*N is small and splits is large.
 __global__ void __launch_bounds__(256)
     splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
+  APPO_PDL_ENTRY();
   const int64_t total = (int64_t)M * N;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + lane;
@@ -1233,6 +1237,7 @@ __global__ void __launch_bounds__(256)
 // consecutive outputs, splits summed in order (deterministic).
 __global__ void __launch_bounds__(256)
     splitk_reduce4_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
+  APPO_PDL_ENTRY();
   const int64_t total = (int64_t)M * N;
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= total) return;

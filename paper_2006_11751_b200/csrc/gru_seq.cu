@@ -129,6 +129,7 @@ struct FwdArgs {
 };
 
 __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_constant__ FwdArgs a) {
+  APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
@@ -310,6 +311,7 @@ struct BwdArgs {
 };
 
 __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_constant__ BwdArgs a) {
+  APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
@@ -548,6 +550,7 @@ struct ClFwdArgs {
 
 __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THR, 1)
     gru_cl_fwd_kernel(const __grid_constant__ ClFwdArgs a) {
+  APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));

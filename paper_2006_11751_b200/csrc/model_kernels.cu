@@ -36,6 +36,7 @@ __device__ __forceinline__ const uint8_t* obs_ptr(const ObsSrc& o, int64_t r) {
 // GEMM epilogue scale).  One thread = one (row, c, kh): 8 bytes in, 16 B out.
 __global__ void im2col_u8_kernel(ObsSrc src, int64_t R, int C, int H, int W, int H1, int W1,
                                  uint16_t* __restrict__ col) {
+  APPO_PDL_ENTRY();
   const int64_t P1 = (int64_t)H1 * W1;
   const int64_t total = R * P1 * C * 8;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -68,6 +69,7 @@ __global__ void im2col_u8_kernel(ObsSrc src, int64_t R, int C, int H, int W, int
 __global__ void im2col_nhwc_kernel(const uint16_t* __restrict__ act, int64_t R, int Hi, int Wi,
                                    int Cin, int k, int s, int Ho, int Wo,
                                    uint16_t* __restrict__ col) {
+  APPO_PDL_ENTRY();
   const int cg = Cin / 8;
   const int64_t Po = (int64_t)Ho * Wo;
   const int64_t total = R * Po * k * k * cg;
@@ -92,6 +94,7 @@ __global__ void col2im_delu_kernel(const float* __restrict__ dcol,
                                    const uint16_t* __restrict__ aprev, int64_t R, int Hi, int Wi,
                                    int Cin, int k, int s, int Ho, int Wo,
                                    uint16_t* __restrict__ dz) {
+  APPO_PDL_ENTRY();
   const int64_t total = R * Hi * Wi * Cin;
   const int K = k * k * Cin;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(256)
     col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol, const uint16_t* __restrict__ aprev,
                             int64_t R, int Hi, int Wi, int Cin, int k, int s, int Ho, int Wo,
                             uint16_t* __restrict__ dz, BiasOut bias) {
+  APPO_PDL_ENTRY();
   const int cg = Cin >> 3;
   const int64_t total = R * Hi * Wi * cg;
   const int K = k * k * Cin;
@@ -216,6 +220,7 @@ __global__ void __launch_bounds__(256)
 // the blocks.
 __global__ void __launch_bounds__(256)
     colsum_v_kernel(int64_t M, const uint16_t* __restrict__ src, BiasOut bias) {
+  APPO_PDL_ENTRY();
   const int N = bias.N;
   const int cg = N >> 3;
   const int64_t total = M * cg;
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(256)
 // wt[(cls, ci)][(a, b, co)] = W[co][py+2a][px+2b][ci] for taps inside the kernel, else 0.
 __global__ void dgrad_weights_kernel(const uint16_t* __restrict__ w, int Co, int k, int Ci,
                                      uint16_t* __restrict__ wt) {
+  APPO_PDL_ENTRY();
   const int kmax = 4 * Co;
   const int total = 4 * Ci * kmax;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
@@ -256,6 +262,7 @@ __global__ void __launch_bounds__(256)
                            int64_t off_c1w, int64_t off_c1b, int K1, int64_t off_c2w,
                            int64_t off_c3w, uint16_t* __restrict__ c1h, float* __restrict__ c1b,
                            uint16_t* __restrict__ wt2, uint16_t* __restrict__ wt3) {
+  APPO_PDL_ENTRY();
   if (blockIdx.x == gridDim.x - 1) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int co = warp; co < 32; co += blockDim.x >> 5) {
@@ -292,6 +299,7 @@ __global__ void __launch_bounds__(256)
 // GEMM multiplies fp16 (1024 + pixel) inputs, gemm.cu u8_convert).
 __global__ void conv1_half_kernel(const float* __restrict__ w, const float* __restrict__ b,
                                   int K, uint16_t* __restrict__ wh, float* __restrict__ bh) {
+  APPO_PDL_ENTRY();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int co = warp; co < 32; co += blockDim.x >> 5) {
     float acc = 0.0f;
@@ -307,6 +315,7 @@ __global__ void conv1_half_kernel(const float* __restrict__ w, const float* __re
 
 __global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int64_t src_ld,
                                    uint16_t* __restrict__ dst, int64_t dst_ld, int cols) {
+  APPO_PDL_ENTRY();
   const int64_t total = n * cols;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -326,6 +335,7 @@ __global__ void __launch_bounds__(256)
                      float* __restrict__ h_out, int32_t* __restrict__ actions,
                      float* __restrict__ logp, float* __restrict__ values,
                      float* __restrict__ logits_out) {
+  APPO_PDL_ENTRY();
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -378,6 +388,7 @@ __global__ void __launch_bounds__(256)
 // Stage h for GRU step t: hbf/hin rows <- hcur (fp32 -> bf16 + fp32 copy).
 __global__ void stage_h_kernel(int n_traj, int T, int t, const float* __restrict__ hcur,
                                float* __restrict__ hin, uint16_t* __restrict__ hbf) {
+  APPO_PDL_ENTRY();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_traj * kHidden) return;
   const int i = g / kHidden, j = g % kHidden;
@@ -393,6 +404,7 @@ __global__ void gru_train_kernel(int n_traj, int T, int t, const float* __restri
                                  const float* __restrict__ gh, const uint8_t* __restrict__ done,
                                  float* __restrict__ hcur, float* __restrict__ core,
                                  uint16_t* __restrict__ core_bf, float* __restrict__ gates) {
+  APPO_PDL_ENTRY();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_traj * kHidden) return;
   const int i = g / kHidden, j = g % kHidden;
@@ -426,6 +438,7 @@ __global__ void __launch_bounds__(256)
                      float* __restrict__ logits, float* __restrict__ values, int64_t B,
                      const int32_t* __restrict__ act, float* __restrict__ tlogp,
                      float* __restrict__ ent, int* flags) {
+  APPO_PDL_ENTRY();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
@@ -481,6 +494,7 @@ __global__ void gather_slots_kernel(int n_traj, int T, const uint8_t* __restrict
                                     float* __restrict__ rew, float* __restrict__ blogp,
                                     uint8_t* __restrict__ done, int64_t* __restrict__ ver,
                                     float* __restrict__ h0, int* flags) {
+  APPO_PDL_ENTRY();
   const int i = blockIdx.x;
   if (i >= n_traj) return;
   const uint8_t* slot = region + (uint64_t)slot_ids[i] * slot_bytes;
@@ -501,6 +515,7 @@ __global__ void gather_slots_kernel(int n_traj, int T, const uint8_t* __restrict
 
 // Advantage normalisation (orchestrator.hpp:838-845), one block.
 __global__ void normalize_kernel(int n, float* __restrict__ adv) {
+  APPO_PDL_ENTRY();
   __shared__ double sh[32];
   __shared__ double mean_s, sd_s;
   double s = 0;
@@ -540,6 +555,7 @@ __global__ void __launch_bounds__(256)
                     const float* __restrict__ vt, LossHP hp, float* __restrict__ dlog,
                     uint16_t* __restrict__ dhead, double* partials, unsigned* counter,
                     double* stats, int* flags, const int64_t* __restrict__ ver, int64_t cur) {
+  APPO_PDL_ENTRY();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   // policy, value, entropy, ratio sums; version-lag sum and max (orchestrator.hpp:790,862-863)
   double acc[6] = {0, 0, 0, 0, 0, -1e300};
@@ -632,6 +648,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     heads_bwd_kernel(int B, int A, const float* __restrict__ dlog, const float* __restrict__ wpi,
                      const float* __restrict__ wv, float* __restrict__ dcore) {
+  APPO_PDL_ENTRY();
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= B) return;
@@ -657,6 +674,7 @@ __global__ void __launch_bounds__(512)
                            const float* __restrict__ wv, float* __restrict__ dcore,
                            float* __restrict__ part, unsigned* counter, float* gwpi, float* gbpi,
                            float* gwv, float* gbv) {
+  APPO_PDL_ENTRY();
   const int j = threadIdx.x;
   const int A1 = A + 1;
   const int rows = (B + gridDim.x - 1) / gridDim.x;
@@ -693,6 +711,7 @@ __global__ void __launch_bounds__(512)
 __global__ void __launch_bounds__(256)
     heads_grad_reduce_kernel(int A, int nb, const float* __restrict__ part, float* gwpi,
                              float* gbpi, float* gwv, float* gbv) {
+  APPO_PDL_ENTRY();
   const int A1 = A + 1;
   const int stride = A1 * kHidden + A1;
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
@@ -711,6 +730,7 @@ __global__ void gru_bwd_kernel(int n_traj, int T, int t, const float* __restrict
                                const uint8_t* __restrict__ done, const float* __restrict__ gates,
                                const float* __restrict__ hin, float* __restrict__ dnext,
                                uint16_t* __restrict__ dgi, uint16_t* __restrict__ dgh) {
+  APPO_PDL_ENTRY();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_traj * kHidden) return;
   const int i = g / kHidden, j = g % kHidden;
@@ -741,6 +761,7 @@ __global__ void gru_bwd_kernel(int n_traj, int T, int t, const float* __restrict
 template <bool BF16>
 __global__ void colsum_partial_kernel(int64_t M, int N, const void* __restrict__ src,
                                       int64_t ld, int rows_per_chunk, float* __restrict__ part) {
+  APPO_PDL_ENTRY();
   const int n = blockIdx.x * 32 + (threadIdx.x & 31);
   const int grp = threadIdx.x >> 5;  // 8 row groups
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
@@ -763,6 +784,7 @@ __global__ void colsum_partial_kernel(int64_t M, int N, const void* __restrict__
 }
 __global__ void colsum_final_kernel(int N, int chunks, const float* __restrict__ part,
                                     float* __restrict__ out, int accumulate) {
+  APPO_PDL_ENTRY();
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float t = 0;
@@ -775,6 +797,7 @@ __global__ void colsum_final_kernel(int N, int chunks, const float* __restrict__
 __global__ void head_grad_scatter_kernel(int A, const float* __restrict__ headw,
                                          const float* __restrict__ bias_sums, float* gwpi,
                                          float* gbpi, float* gwv, float* gbv) {
+  APPO_PDL_ENTRY();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g < A * kHidden) gwpi[g] = headw[g];
   if (g < kHidden) gwv[g] = headw[A * kHidden + g];
@@ -784,6 +807,7 @@ __global__ void head_grad_scatter_kernel(int A, const float* __restrict__ headw,
 
 // Version lag statistics (orchestrator.hpp:790,862-863), one block.
 __global__ void lag_kernel(int B, const int64_t* __restrict__ ver, int64_t cur, double* stats) {
+  APPO_PDL_ENTRY();
   __shared__ double sh[32];
   __shared__ long long mn[32];
   double s = 0;

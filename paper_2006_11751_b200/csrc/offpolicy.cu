@@ -60,6 +60,7 @@ __device__ __forceinline__ void step_coeffs(const ReturnsArgs& a, const float* r
 
 template <int MODE>
 __global__ void __launch_bounds__(256) returns_kernel(ReturnsArgs a) {
+  APPO_PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= a.n_traj) return;
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(256)
                       const float* __restrict__ values, const float* __restrict__ vt,
                       const float* __restrict__ ent, float lo, float hi, float vc, float ec,
                       double* partials, unsigned* counter, double* out, int* flags) {
+  APPO_PDL_ENTRY();
   double acc[3] = {0, 0, 0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double r = ratios[i], A = adv[i];
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(256)
 __global__ void logp_entropy_kernel(int B, int A, const float* __restrict__ logits,
                                     const int32_t* __restrict__ actions, float* logp, float* ent,
                                     int* flags) {
+  APPO_PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const float* lg = logits + (size_t)b * A;
@@ -243,6 +246,7 @@ __global__ void logp_entropy_kernel(int B, int A, const float* __restrict__ logi
 // fallback A-1, joint logp = log(max(p, 1e-300)); u is counter-based.
 __global__ void sample_kernel(int B, int A, const float* __restrict__ logits, uint64_t key,
                               uint64_t counter0, int32_t* actions, float* logp) {
+  APPO_PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const float* lg = logits + (size_t)b * A;

@@ -16,6 +16,7 @@ namespace {
 __global__ void __launch_bounds__(256)
     sumsq_kernel(int64_t n, const float* __restrict__ g, double* partials, unsigned* counter,
                  double* norm_out, float clip, int* flags) {
+  APPO_PDL_ENTRY();
   double acc = 0.0;
   bool bad = false;
   const int64_t n4 = (reinterpret_cast<uintptr_t>(g) & 15) ? 0 : (n >> 2);
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ norm_in, float lr, float b1, float b2, float eps,
                 float bc1, float bc2, __nv_bfloat16* __restrict__ bf16, float* __restrict__ f32,
                 const int* flags, unsigned* applied) {
+  APPO_PDL_ENTRY();
   if (flags[kFlagNumeric] | flags[kFlagContract] | flags[kFlagQueue]) {
     // the step threw before Adam: parameters untouched, but the publish target
     // still receives the current parameters so the published copy stays valid

@@ -61,6 +61,7 @@ __global__ void gen_obs_kernel(int n_envs, int64_t obs_dim, uint64_t seed,
                                const uint32_t* __restrict__ step,
                                const uint32_t* __restrict__ episode, uint8_t* region,
                                uint64_t slot_bytes, int64_t slot_base, uint64_t off) {
+  APPO_PDL_ENTRY();
   const int words = (int)(obs_dim >> 3);
   const int e = blockIdx.y;
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
@@ -79,6 +80,7 @@ __global__ void record_kernel(int n_envs, int T, int t, int episode_len, uint32_
                               const float* __restrict__ h_out, const int32_t* __restrict__ act,
                               const float* __restrict__ logp, uint8_t* region,
                               uint64_t slot_bytes, int64_t slot_base, SlotOffsets off) {
+  APPO_PDL_ENTRY();
   const int e = blockIdx.x;
   if (e >= n_envs) return;
   uint8_t* slot = region + (uint64_t)(slot_base + e) * slot_bytes;
@@ -127,6 +129,7 @@ __global__ void record_kernel(int n_envs, int T, int t, int episode_len, uint32_
 }
 
 __global__ void init_env_kernel(int n_envs, int episode_len, uint32_t* step, uint32_t* episode) {
+  APPO_PDL_ENTRY();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_envs) return;
   // desynchronise episodes so dones are spread over the batch

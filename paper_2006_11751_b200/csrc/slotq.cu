@@ -46,6 +46,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 __global__ void slotq_init_kernel(unsigned long long* seq, uint32_t cap) {
+  APPO_PDL_ENTRY();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x)
     seq[i] = i;
 }
@@ -56,6 +57,7 @@ __global__ void __launch_bounds__(1024)
                       unsigned long long* ctr, uint32_t mask, int n,
                       const int32_t* __restrict__ src, int32_t first, const int* ok,
                       int64_t timeout_ns, int* flags) {
+  APPO_PDL_ENTRY();
   __shared__ unsigned long long base;
   if (ok && *ok == 0) return;
   if (threadIdx.x == 0) base = atomicAdd(ctr + 0, (unsigned long long)n);
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(1024)
     slotq_pop_kernel(int32_t* __restrict__ ids, unsigned long long* __restrict__ seq,
                      unsigned long long* ctr, uint32_t mask, uint32_t cap, int n, int32_t n_slots,
                      int32_t* __restrict__ out, int* ok, int64_t timeout_ns, int* flags) {
+  APPO_PDL_ENTRY();
   __shared__ int timed_out;
   const unsigned long long head = *reinterpret_cast<volatile unsigned long long*>(ctr + 1);
   const uint64_t t0 = global_ns();
