@@ -58,6 +58,10 @@ enum AGather : int {
 };
 constexpr int GATHER_THREADS = 128;  // NHWC gather warps (after the epilogue warps)
 constexpr int U8_GATHER_THREADS = 256;  // conv1 staging/convert warps: two per tile row
+#ifndef APPO_U8_CONV_THREADS
+#define APPO_U8_CONV_THREADS 256
+#endif
+constexpr int U8_CONV_THREADS = APPO_U8_CONV_THREADS;  // conv1 forward converters (128 x 2^k)
 
 // Input gradient of a stride-2 convolution (kernel k <= 4, no padding) by
 // sub-pixel decomposition.  Input position (2yy+py, 2xx+px) only receives
@@ -592,13 +596,14 @@ __device__ __forceinline__ void u8_stage_bulk(const GatherP& g, int tile, uint8_
 // is removed through the epilogue bias (k_conv1_half_weights).
 __device__ __forceinline__ void u8_convert(const GatherP& g, const uint8_t* buf, const int* meta,
                                            uint8_t* sA, int c, int gt) {
-  const int row = gt & 127, kh0 = (gt >> 7) * 4;
+  constexpr int KHT = 8 / (U8_CONV_THREADS / 128);  // kernel rows per thread
+  const int row = gt & 127, kh0 = (gt >> 7) * KHT;
   const int k = row >> 5, x = row & 31;
   const int plane = g.tma ? U8_BOX_ROWS * g.Wi : U8_BLK;
   const uint32_t src = sm100::smem_u32(buf) + meta[k] + c * plane + kh0 * g.Wi + 4 * x;
   const uint32_t row_base = sm100::smem_u32(sA) + row * 128;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < KHT; ++j) {
     uint32_t lo, hi;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(src + j * g.Wi));
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(src + j * g.Wi + 4));
@@ -676,7 +681,7 @@ constexpr int epi_warps() {
 }
 template <int AG>
 constexpr int gather_threads() {
-  return has_gather<AG>() ? U8_GATHER_THREADS : 0;  // 256 gather / convert threads
+  return AG == AG_U8 ? U8_CONV_THREADS : has_gather<AG>() ? U8_GATHER_THREADS : 0;
 }
 template <int EV, int AG>
 constexpr int kernel_threads() {

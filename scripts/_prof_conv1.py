@@ -1,0 +1,13 @@
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.getcwd())
+import paper_2006_11751_b200 as appo
+desc = appo.ModelDesc.doom()
+ctx = appo.Context(0, seed=1, model=desc)
+n = 16384
+store = appo.TrajectoryStore(desc, n)
+smp = appo.Sampler(ctx, n, 256, seed=3)
+smp.step(store, 0, 0)
+torch.cuda.synchronize()
+os.environ["APPO_GEMM_PROF"] = "2"
+smp.step(store, 0, 1)
+torch.cuda.synchronize()
