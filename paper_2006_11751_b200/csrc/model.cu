@@ -350,15 +350,17 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   e.bias = pf + d.off_fcb;
   e.out = s.x;
   e.ldo = kHidden;
+  // learner-sized batches: narrow N tiles fill more SMs (scripts/gemm_sweep.py)
+  const bool small = R <= 4096;
   TRY(gemm_bf16(c, R, kHidden, d.F, Operand{s.a3, d.F, false}, Operand{wb + d.off_fcw, d.F, false},
-                e, 128));
+                e, small ? 64 : 128));
   Epilogue g;
   g.flags = EPI_BIAS;
   g.bias = pf + d.off_bih;
   g.out = s.gi;
   g.ldo = kGates;
   TRY(gemm_bf16(c, R, kGates, kHidden, Operand{s.x, kHidden, false},
-                Operand{wb + d.off_wih, kHidden, false}, g, 256));
+                Operand{wb + d.off_wih, kHidden, false}, g, small ? 64 : 256));
   return APPO_OK;
 }
 
@@ -786,15 +788,16 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     }
   }
   {
-    // dW_ih = dgi^T x, dW_hh = dgh^T h_in, biases = column sums
+    // dW_ih = dgi^T x, dW_hh = dgh^T h_in, biases = column sums (64-wide N
+    // tiles, no split-K: measured fastest at these shapes, scripts/gemm_sweep.py)
     Epilogue e;
     e.out = G + d.off_wih;
     e.ldo = kHidden;
     TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgi, kGates, true},
-                  Operand{s.x, kHidden, true}, e, 256, splits_for(ctx, kGates, kHidden, 256, B)));
+                  Operand{s.x, kHidden, true}, e, 64, 1));
     e.out = G + d.off_whh;
     TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgh, kGates, true},
-                  Operand{s.hbf, kHidden, true}, e, 256, splits_for(ctx, kGates, kHidden, 256, B)));
+                  Operand{s.hbf, kHidden, true}, e, 64, 1));
     if (!seq) {
       TRY(k_colsum(ctx, B, kGates, s.dgi, kGates, true, s.colsum_part, G + d.off_bih, false));
       TRY(k_colsum(ctx, B, kGates, s.dgh, kGates, true, s.colsum_part, G + d.off_bhh, false));
@@ -822,7 +825,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     e.out = G + d.off_fcw;
     e.ldo = d.F;
     TRY(gemm_bf16(ctx, kHidden, d.F, B, Operand{s.dzfc, kHidden, true},
-                  Operand{s.a3, d.F, true}, e, 256, splits_for(ctx, kHidden, d.F, 256, B)));
+                  Operand{s.a3, d.F, true}, e, 64, 1));
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
     x.aux = s.a3;
