@@ -353,14 +353,14 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   // learner-sized batches: narrow N tiles fill more SMs (scripts/gemm_sweep.py)
   const bool small = R <= 4096;
   TRY(gemm_bf16(c, R, kHidden, d.F, Operand{s.a3, d.F, false}, Operand{wb + d.off_fcw, d.F, false},
-                e, small ? 64 : 128));
+                e, small ? 64 : 256));
   Epilogue g;
   g.flags = EPI_BIAS;
   g.bias = pf + d.off_bih;
   g.out = s.gi;
   g.ldo = kGates;
   TRY(gemm_bf16(c, R, kGates, kHidden, Operand{s.x, kHidden, false},
-                Operand{wb + d.off_wih, kHidden, false}, g, small ? 64 : 256));
+                Operand{wb + d.off_wih, kHidden, false}, g, small ? 64 : 128));
   return APPO_OK;
 }
 
@@ -402,7 +402,7 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
   g.out = s.gh;
   g.ldo = kGates;
   TRY(gemm_bf16(c, B, kGates, kHidden, Operand{s.hbf, kHidden, false},
-                Operand{wb + d.off_whh, kHidden, false}, g, 256));
+                Operand{wb + d.off_whh, kHidden, false}, g, 128));
   TRY(k_gru_infer(c, B, d.A, s.gi, s.gh, h_in, pf + d.off_wpi, pf + d.off_bpi, pf + d.off_wv,
                   pf + d.off_bv, M->sample_key, counter0, h_out, actions, logp, values, logits));
   // last reader of pub[pub] on this stream: the learner waits on this event

@@ -313,6 +313,18 @@ __global__ void conv1_half_kernel(const float* __restrict__ w, const float* __re
   }
 }
 
+// contiguous rows: 4 values per thread, no index division
+__global__ void f32_to_bf16_vec_kernel(int64_t n4, const float4* __restrict__ src,
+                                       uint2* __restrict__ dst) {
+  APPO_PDL_ENTRY();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(src + i);
+    dst[i] = make_uint2(((uint32_t)f2bf(v.y) << 16) | f2bf(v.x),
+                        ((uint32_t)f2bf(v.w) << 16) | f2bf(v.z));
+  }
+}
+
 __global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int64_t src_ld,
                                    uint16_t* __restrict__ dst, int64_t dst_ld, int cols) {
   APPO_PDL_ENTRY();
@@ -908,6 +920,14 @@ int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, fl
 }
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
                   int64_t dst_ld, int cols) {
+  const int64_t n = rows * cols;
+  if (src_ld == cols && dst_ld == cols && n % 4 == 0 &&
+      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    c->next_bytes = 6.0 * (double)n;
+    APPO_LAUNCH(c, f32_to_bf16_vec_kernel, grid_for(n / 4, 256, c->num_sms * 16), 256, 0, n / 4,
+                reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst));
+    return APPO_OK;
+  }
   APPO_LAUNCH(c, f32_to_bf16_kernel, grid_for(rows * cols, 256, c->num_sms * 16), 256, 0, rows,
               src, src_ld, dst, dst_ld, cols);
   return APPO_OK;

@@ -55,6 +55,8 @@ __device__ __forceinline__ uint64_t dev_derive_seed(uint64_t seed, uint64_t stre
   return splitmix64(seed ^ splitmix64(stream + 1));
 }
 
+constexpr int kObsWordsPerThread = 4;
+
 // obs for env e at its current (episode, step): 8 pixels per hash.
 // grid (ceil(words / 256), n_envs): env from blockIdx.y, no 64-bit division
 __global__ void gen_obs_kernel(int n_envs, int64_t obs_dim, uint64_t seed,
@@ -64,12 +66,18 @@ __global__ void gen_obs_kernel(int n_envs, int64_t obs_dim, uint64_t seed,
   APPO_PDL_ENTRY();
   const int words = (int)(obs_dim >> 3);
   const int e = blockIdx.y;
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= words) return;
+  const int w0 = blockIdx.x * (kObsWordsPerThread * 256) + threadIdx.x;
+  if (w0 >= words) return;
+  // the env's episode seed once per thread, then kObsWordsPerThread hashes
+  // (coalesced: word w0 + 256 k)
   const uint64_t es = dev_derive_seed(seed, ((uint64_t)e << 24) ^ episode[e]);
-  const uint64_t h = splitmix64(es ^ ((uint64_t)step[e] << 20) ^ (uint64_t)w);
-  *reinterpret_cast<uint64_t*>(region + (uint64_t)(slot_base + e) * slot_bytes + off +
-                               (uint64_t)w * 8) = h;
+  const uint64_t key = es ^ ((uint64_t)step[e] << 20);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(region + (uint64_t)(slot_base + e) * slot_bytes + off);
+#pragma unroll
+  for (int k = 0; k < kObsWordsPerThread; ++k) {
+    const int w = w0 + 256 * k;
+    if (w < words) dst[w] = splitmix64(key ^ (uint64_t)w);
+  }
 }
 
 // Step record + env transition; one block (128 threads) per env.
@@ -220,7 +228,9 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
                                     slot_bytes, h_obs, d.obs_dim, d.obs_dim, s->n_envs,
                                     cudaMemcpyHostToDevice, c->stream));
   } else {
-    const dim3 grid((unsigned)(((d.obs_dim >> 3) + 255) / 256), (unsigned)s->n_envs);
+    const dim3 grid((unsigned)(((d.obs_dim >> 3) + 256 * kObsWordsPerThread - 1) /
+                             (256 * kObsWordsPerThread)),
+                  (unsigned)s->n_envs);
     c->next_bytes = (double)s->n_envs * d.obs_dim;
     APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
                 s->episode, region, slot_bytes, (int64_t)slot_base, obs_off);
@@ -238,7 +248,9 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
               slot_bytes, (int64_t)slot_base, off);
   if (t == d.T - 1) {
     // bootstrap obs = next observation of every env (post-transition state)
-    const dim3 grid((unsigned)(((d.obs_dim >> 3) + 255) / 256), (unsigned)s->n_envs);
+    const dim3 grid((unsigned)(((d.obs_dim >> 3) + 256 * kObsWordsPerThread - 1) /
+                             (256 * kObsWordsPerThread)),
+                  (unsigned)s->n_envs);
     APPO_LAUNCH(c, gen_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim, s->seed, s->step,
                 s->episode, region, slot_bytes, (int64_t)slot_base, d.slot[7]);
   }

@@ -32,6 +32,11 @@ def run(ctx, M, N, K, a_mn=False, b_mn=False, bn=128, splits=1, reps=50):
 def main():
     ctx = appo.Context(0)
     torch.cuda._sleep(10)
+    if os.environ.get("SWEEP") == "infer":
+        for bn in (64, 128, 256):
+            run(ctx, 16384, 1536, 512, bn=bn, reps=20)
+            run(ctx, 16384, 512, 2304, bn=bn, reps=20)
+        return
     if os.environ.get("SWEEP") == "wgrad":
         for bn, sp in ((256, 1), (256, 2), (256, 3), (128, 1), (128, 2), (128, 4), (64, 1)):
             run(ctx, 1536, 512, 2048, a_mn=True, b_mn=True, bn=bn, splits=sp)
