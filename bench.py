@@ -133,7 +133,7 @@ def cpu_baseline_sample(args, n_traj=None, seed=0):
     from oracle.oracle import Oracle
     orc = Oracle()
     cores = os.cpu_count() or 1
-    n = n_traj or cores
+    n = n_traj or 8 * cores  # ~8-10 s of CPU work on the GPU box's host
     shape = (3, 72, 128, 6)
     T = args.T
     theta = orc.init_params(*shape, 1)

@@ -10,7 +10,20 @@ import re
 import sys
 
 
+AG_NAMES = {0: "gemm_bf16_tcgen05", 1: "gemm_conv_nhwc_gather_tcgen05",
+            2: "gemm_conv1_u8_implicit_tcgen05", 3: "gemm_dgrad_implicit_tcgen05",
+            4: "gemm_conv1_wgrad_implicit_tcgen05", 5: "gemm_conv_taps_implicit_tcgen05",
+            6: "gemm_conv_taps_wgrad_tcgen05"}
+
+
 def kname(full: str) -> str:
+    """Kernel class; GEMM engine instantiations by gather mode (the same names
+    bench.py / the timing report use)."""
+    m = re.search(r"gemm_bf16_kernel<([^>]*)>", full.replace("(int)", "").replace("(bool)", ""))
+    if m:
+        args = [a.strip() for a in m.group(1).split(",")]
+        ag = int(args[4]) if len(args) > 4 and args[4].lstrip("-").isdigit() else 0
+        return AG_NAMES.get(ag, "gemm_bf16_tcgen05")
     s = full
     if s.startswith("void "):
         s = s[5:]
@@ -27,10 +40,11 @@ def main():
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[hi + 1 + skip:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-3)
         a = agg[kname(r[ki])]

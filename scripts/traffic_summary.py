@@ -8,7 +8,8 @@ from collections import defaultdict
 
 AG_NAMES = {0: "gemm_bf16_tcgen05", 1: "gemm_conv_nhwc_gather_tcgen05",
             2: "gemm_conv1_u8_implicit_tcgen05", 3: "gemm_dgrad_implicit_tcgen05",
-            4: "gemm_conv1_wgrad_implicit_tcgen05", 5: "gemm_conv_taps_implicit_tcgen05"}
+            4: "gemm_conv1_wgrad_implicit_tcgen05", 5: "gemm_conv_taps_implicit_tcgen05",
+            6: "gemm_conv_taps_wgrad_tcgen05"}
 
 
 def klass(name):
