@@ -338,7 +338,8 @@ __global__ void f32_to_bf16_kernel(int64_t n, const float* __restrict__ src, int
 }
 
 // GRU cell (PyTorch gate order r, z, n) + heads + sampling for inference.
-// One warp per env; lane owns hidden units j = lane + 32q.
+// One warp per env; lane owns hidden units j = 4 lane + 128 q (float4 loads
+// and stores of every operand row).
 __global__ void __launch_bounds__(256)
     gru_infer_kernel(int B, int A, const float* __restrict__ gi, const float* __restrict__ gh,
                      const float* __restrict__ h_in, const float* __restrict__ wpi,
@@ -351,26 +352,48 @@ __global__ void __launch_bounds__(256)
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
-  const float* gib = gi + (int64_t)b * kGates;
-  const float* ghb = gh + (int64_t)b * kGates;
+  const float4* gib = reinterpret_cast<const float4*>(gi + (int64_t)b * kGates);
+  const float4* ghb = reinterpret_cast<const float4*>(gh + (int64_t)b * kGates);
+  const float4* hib = reinterpret_cast<const float4*>(h_in + (int64_t)b * kHidden);
+  float4* hob = reinterpret_cast<float4*>(h_out + (int64_t)b * kHidden);
+  constexpr int H4 = kHidden / 4;
   float acc[kMaxActions + 1];
 #pragma unroll
   for (int a = 0; a <= kMaxActions; ++a) acc[a] = 0.0f;
-#pragma unroll 4
-  for (int q = 0; q < kHidden / 32; ++q) {
-    const int j = lane + 32 * q;
-    const float r = sigmoidf_(gib[j] + ghb[j]);
-    const float z = sigmoidf_(gib[kHidden + j] + ghb[kHidden + j]);
-    const float n = tanhf(gib[2 * kHidden + j] + r * ghb[2 * kHidden + j]);
-    const float h = (1.0f - z) * n + z * h_in[(int64_t)b * kHidden + j];
-    h_out[(int64_t)b * kHidden + j] = h;
+#pragma unroll
+  for (int q = 0; q < kHidden / 128; ++q) {
+    const int j4 = lane + 32 * q;  // float4 index: units 4 j4 .. 4 j4 + 3
+    const float4 ir = __ldg(gib + j4), iz = __ldg(gib + H4 + j4), in_ = __ldg(gib + 2 * H4 + j4);
+    const float4 hr = __ldg(ghb + j4), hz = __ldg(ghb + H4 + j4), hn = __ldg(ghb + 2 * H4 + j4);
+    const float4 hp = __ldg(hib + j4);
+    const float xr[4] = {ir.x + hr.x, ir.y + hr.y, ir.z + hr.z, ir.w + hr.w};
+    const float xz[4] = {iz.x + hz.x, iz.y + hz.y, iz.z + hz.z, iz.w + hz.w};
+    const float xi[4] = {in_.x, in_.y, in_.z, in_.w};
+    const float xh[4] = {hn.x, hn.y, hn.z, hn.w};
+    const float xp[4] = {hp.x, hp.y, hp.z, hp.w};
+    float h[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float r = sigmoidf_(xr[k]);
+      const float z = sigmoidf_(xz[k]);
+      const float n = tanhf(xi[k] + r * xh[k]);
+      h[k] = (1.0f - z) * n + z * xp[k];
+    }
+    hob[j4] = make_float4(h[0], h[1], h[2], h[3]);
 #pragma unroll
     for (int a = 0; a < kMaxActions; ++a)
-      if (a < A) acc[a] += wpi[a * kHidden + j] * h;
-    acc[kMaxActions] += wv[j] * h;
+      if (a < A) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(wpi + a * kHidden) + j4);
+        acc[a] += w.x * h[0] + w.y * h[1] + w.z * h[2] + w.w * h[3];
+      }
+    // wv sits at an odd offset of the parameter vector: scalar loads
+    acc[kMaxActions] += __ldg(wv + 4 * j4) * h[0] + __ldg(wv + 4 * j4 + 1) * h[1] +
+                        __ldg(wv + 4 * j4 + 2) * h[2] + __ldg(wv + 4 * j4 + 3) * h[3];
   }
 #pragma unroll
-  for (int a = 0; a <= kMaxActions; ++a) acc[a] = warp_sum(acc[a]);
+  for (int a = 0; a < kMaxActions; ++a)
+    if (a < A) acc[a] = warp_sum(acc[a]);
+  acc[kMaxActions] = warp_sum(acc[kMaxActions]);
   if (lane == 0) {
     double lg[kMaxActions];
     double mx = -1e300;
@@ -936,6 +959,10 @@ int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const fl
                 const float* wpi, const float* bpi, const float* wv, const float* bv,
                 uint64_t key, uint64_t counter0, float* h_out, int32_t* actions, float* logp,
                 float* values, float* logits) {
+  APPO_REQUIRE(((reinterpret_cast<uintptr_t>(gi) | reinterpret_cast<uintptr_t>(gh) |
+                 reinterpret_cast<uintptr_t>(h_in) | reinterpret_cast<uintptr_t>(h_out) |
+                 reinterpret_cast<uintptr_t>(wpi)) & 15) == 0,
+               APPO_ERR_CONTRACT, "policy_forward: hidden-state buffers must be 16-byte aligned");
   APPO_LAUNCH(c, gru_infer_kernel, (B + 7) / 8, 256, 0, B, A, gi, gh, h_in, wpi, bpi, wv, bv,
               key, counter0, h_out, actions, logp, values, logits);
   return APPO_OK;

@@ -21,9 +21,21 @@ __global__ void __launch_bounds__(256)
   bool bad = false;
   const int64_t n4 = (reinterpret_cast<uintptr_t>(g) & 15) ? 0 : (n >> 2);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 x = g4[i];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {  // four loads in flight per thread
+    float4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __ldg(g4 + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bad |= !(finitef(x[k].x) && finitef(x[k].y) && finitef(x[k].z) && finitef(x[k].w));
+      acc += (double)x[k].x * x[k].x + (double)x[k].y * x[k].y + (double)x[k].z * x[k].z +
+             (double)x[k].w * x[k].w;
+    }
+  }
+  for (; i < n4; i += stride) {
+    const float4 x = __ldg(g4 + i);
     bad |= !(finitef(x.x) && finitef(x.y) && finitef(x.z) && finitef(x.w));
     acc += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
   }
@@ -112,7 +124,7 @@ int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
                 uint16_t* bf16_copy, float* f32_copy, unsigned* applied) {
   if (n == 0) return APPO_OK;
-  const int grid = 148 * 2;
+  const int grid = 148 * 4;  // partials fit kRedSlots; enough loads in flight for HBM
   c->next_bytes = (double)n * 4;
   APPO_LAUNCH(c, sumsq_kernel, grid, 256, 0, n, g, c->d_red, c->d_counter + 1, d_norm_out, clip,
               c->d_flags);
