@@ -73,6 +73,23 @@ __device__ __forceinline__ uint32_t sw128(int rows, int r, int kb, int c) {
 
 // Grid-wide barrier on a monotonically increasing counter (zeroed by the host
 // before the launch); all CTAs are co-resident (cooperative launch).
+// Split form: arrive (release of everything the CTA stored before it), then
+// work that no other CTA needs (deferred stores, prefetches), then wait.
+__device__ __forceinline__ void grid_arrive(unsigned* counter) {
+  __syncthreads();
+  if (threadIdx.x == 0)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+}
+__device__ __forceinline__ void grid_wait(unsigned* counter, unsigned target) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -249,12 +266,14 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
     }
     sm100::tc_fence_before();
     __syncthreads();
+    // the cell; only the exchange (next h, bf16) is stored before the barrier
+    // arrive -- the rest of the step's outputs are stored while it completes
+    float cv[CPT][6];  // r, z, n, ghn, h_prev, h
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int e = tid + c * THR;
       if (e >= n_cells) continue;
       const int i = e / UPC_F, u = e % UPC_F, j = j0 + u;
-      const int64_t row = (t < a.T) ? (int64_t)i * a.T + t : (int64_t)B + i;
       const float ghr = gh[i * NG + u] + b3[c][0];
       const float ghz = gh[i * NG + UPC_F + u] + b3[c][1];
       const float ghn = gh[i * NG + 2 * UPC_F + u] + b3[c][2];
@@ -263,26 +282,42 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
       const float n = tanh_(g3[c][2] + rr * ghn);
       const float hp = hreg[c];
       const float h = (1.0f - z) * n + z * hp;
-      a.core[row * kHidden + j] = h;
-      a.core_bf[row * kHidden + j] = f2bf_(h);
-      float* gs = a.gates + row * 4 * kHidden;
-      gs[j] = rr;
-      gs[kHidden + j] = z;
-      gs[2 * kHidden + j] = n;
-      gs[3 * kHidden + j] = ghn;
-      a.hin[row * kHidden + j] = hp;
-      a.hbf[row * kHidden + j] = f2bf_(hp);
+      cv[c][0] = rr;
+      cv[c][1] = z;
+      cv[c][2] = n;
+      cv[c][3] = ghn;
+      cv[c][4] = hp;
+      cv[c][5] = h;
       if (t < a.T) {
         const float hn = dn[c] ? 0.0f : h;
         hreg[c] = hn;
         a.hbuf_bf[nxt + (int64_t)i * kHidden + j] = f2bf_(hn);
       }
     }
+    if (t < a.T) {
+      fence_proxy_async_global();
+      grid_arrive(a.bar);
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = tid + c * THR;
+      if (e >= n_cells) continue;
+      const int i = e / UPC_F, j = j0 + e % UPC_F;
+      const int64_t row = (t < a.T) ? (int64_t)i * a.T + t : (int64_t)B + i;
+      a.core[row * kHidden + j] = cv[c][5];
+      a.core_bf[row * kHidden + j] = f2bf_(cv[c][5]);
+      float* gs = a.gates + row * 4 * kHidden;
+      gs[j] = cv[c][0];
+      gs[kHidden + j] = cv[c][1];
+      gs[2 * kHidden + j] = cv[c][2];
+      gs[3 * kHidden + j] = cv[c][3];
+      a.hin[row * kHidden + j] = cv[c][4];
+      a.hbf[row * kHidden + j] = f2bf_(cv[c][4]);
+    }
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 3] = clock64();
     if (t < a.T) {
       prefetch(t + 1);  // independent of the exchange: overlaps the barrier
-      fence_proxy_async_global();
-      grid_barrier(a.bar, ++epoch * gridDim.x);
+      grid_wait(a.bar, ++epoch * gridDim.x);
     }
   }
   sm100::tc_fence_before();
@@ -384,6 +419,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
   for (int t = a.T - 1; t >= 0; --t) {
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 0] = clock64();
     uint16_t* xb = a.dghx + (size_t)(t & 1) * a.n_traj * kGates;
+    uint16_t dq[CPT][4];  // dgr, dgz, dgn, dan (bf16) of this step's cells
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int e = tid + c * THR;
@@ -406,25 +442,41 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
       const uint16_t dgr = f2bf_(fgr);
       const uint16_t dgz = f2bf_(fgz);
       const uint16_t dgn = f2bf_(fgn);
+      dq[c][0] = dgr;
+      dq[c][1] = dgz;
+      dq[c][2] = dgn;
+      dq[c][3] = f2bf_(dan);
+      if (t > 0) {  // the exchange: the only store other CTAs wait for
+        uint16_t* xr = xb + (int64_t)i * kGates;
+        xr[j] = dgr;
+        xr[kHidden + j] = dgz;
+        xr[2 * kHidden + j] = dgn;
+      }
+      ddr[c] = dh * z;
+    }
+    if (t > 0) {
+      fence_proxy_async_global();  // dgh_t stores -> visible to the TMA reads
+      grid_arrive(a.bar);
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {  // gradient rows for the weight GEMMs: after the arrive
+      const int e = tid + c * THR;
+      if (e >= n_cells) continue;
+      const int i = e / UPC_B, j = j0 + e % UPC_B;
+      const int64_t s = (int64_t)i * a.T + t;
       uint16_t* gi_row = a.dgi + s * kGates;
       uint16_t* gh_row = a.dgh + s * kGates;
-      gi_row[j] = dgr;
-      gi_row[kHidden + j] = dgz;
-      gi_row[2 * kHidden + j] = f2bf_(dan);
-      gh_row[j] = dgr;
-      gh_row[kHidden + j] = dgz;
-      gh_row[2 * kHidden + j] = dgn;
-      uint16_t* xr = xb + (int64_t)i * kGates;
-      xr[j] = dgr;
-      xr[kHidden + j] = dgz;
-      xr[2 * kHidden + j] = dgn;
-      ddr[c] = dh * z;
+      gi_row[j] = dq[c][0];
+      gi_row[kHidden + j] = dq[c][1];
+      gi_row[2 * kHidden + j] = dq[c][3];
+      gh_row[j] = dq[c][0];
+      gh_row[kHidden + j] = dq[c][1];
+      gh_row[2 * kHidden + j] = dq[c][2];
     }
     if (t == 0) break;  // d(h0) is not needed
     prefetch(t - 1);    // independent of the exchange: overlaps barrier + MMA
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 1] = clock64();
-    fence_proxy_async_global();  // dgh_t stores -> visible to the TMA reads
-    grid_barrier(a.bar, ++epoch * gridDim.x);
+    grid_wait(a.bar, ++epoch * gridDim.x);
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
     // dnext = dh*z + dgh_t . W_hh[:, own]: dgh_t (24 K blocks of 8 KB) by TMA in
     // six 32 KB groups; the MMAs of a group start as soon as it lands
