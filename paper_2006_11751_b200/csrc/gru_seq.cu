@@ -343,7 +343,14 @@ struct BwdArgs {
   float* gbhh;          // [1536]
   unsigned* bar;
   long long* prof;      // optional phase timestamps (APPO_GRU_PROF): [steps][4]
+  int mc;               // 1: launched in CTA pairs, dgh_t staged by TMA multicast
 };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 
 __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_constant__ BwdArgs a) {
   APPO_PDL_ENTRY();
@@ -482,13 +489,33 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
     // six 32 KB groups; the MMAs of a group start as soon as it lands
     if (warp == 1) {
       fence_proxy_async_global();
+      if (a.mc) {
+        // CTA pair: each CTA fetches every other 32 KB group once for both
+        // (multicast into the same smem offsets, completing both CTAs' kbar[g]);
+        // the peer finished reading its tA (previous step's MMAs) before the barrier
+        const uint32_t rank = cluster_rank();
 #pragma unroll
-      for (int g = 0; g < 6; ++g) {
-        sm100::mbar_arrive_expect_tx_warp(&kbar[g], 4 * KB_BYTES_A);
+        for (int g = 0; g < 6; ++g) sm100::mbar_arrive_expect_tx_warp(&kbar[g], 4 * KB_BYTES_A);
+        if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          sm100::tma_load_3d_warp(tA + (4 * g + q) * KB_BYTES_A, &a.xmap, &kbar[g],
-                                  (4 * g + q) * 64, 0, t & 1);
+          for (int g = 0; g < 6; ++g) {
+            if ((uint32_t)(g & 1) != rank) continue;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              sm100::tma_load_3d_mc(tA + (4 * g + q) * KB_BYTES_A, &a.xmap, &kbar[g],
+                                    (4 * g + q) * 64, 0, t & 1, (uint16_t)0x3);
+          }
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int g = 0; g < 6; ++g) {
+          sm100::mbar_arrive_expect_tx_warp(&kbar[g], 4 * KB_BYTES_A);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            sm100::tma_load_3d_warp(tA + (4 * g + q) * KB_BYTES_A, &a.xmap, &kbar[g],
+                                    (4 * g + q) * 64, 0, t & 1);
+        }
       }
     }
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 3] = clock64();
@@ -557,6 +584,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
   }
   sm100::tc_fence_before();
   __syncthreads();
+  if (a.mc) sm100::cluster_sync();  // no CTA leaves while its pair may still multicast into it
   if (warp == 0) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, 32);
@@ -921,8 +949,38 @@ int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* 
   a.bar = bar; a.prof = prof;
   void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_bwd_kernel");
-  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_bwd_kernel, dim3(NCTA_B), dim3(THR),
-                                            args, BWD_SMEM, c->stream));
+  // opt-in (APPO_GRU_MC=1): CTA pairs with multicast staging of dgh_t (half
+  // the L2 reads of the exchange) -- measured slower (191 vs 177 us: the pair
+  // couples two CTAs' step latencies), so the default is the plain launch
+  static int mc_ok = getenv("APPO_GRU_MC") && getenv("APPO_GRU_MC")[0] == '1' ? 1 : 0;
+  cudaError_t le = cudaErrorUnknown;
+  if (mc_ok) {
+    a.mc = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(NCTA_B);
+    cfg.blockDim = dim3(THR);
+    cfg.dynamicSmemBytes = BWD_SMEM;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    le = cudaLaunchKernelEx(&cfg, gru_seq_bwd_kernel, a);
+    if (le != cudaSuccess) {
+      (void)cudaGetLastError();
+      mc_ok = 0;
+    }
+  }
+  if (!mc_ok) {
+    a.mc = 0;
+    APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_seq_bwd_kernel, dim3(NCTA_B), dim3(THR),
+                                              args, BWD_SMEM, c->stream));
+  }
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T - 1);
   timing_end(c, "gru_seq_bwd_kernel", ev);
   c->launches++;
