@@ -359,24 +359,30 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
                                            ~uintptr_t(1023));
   uint8_t* tA = sm;                                      // 3 x 64 KB: all of dgh_t
   uint8_t* tB = sm + 3 * A_TILE;
-  float* mm = reinterpret_cast<float*>(tB + B_BWD);      // [64][8] dgh . W_hh[:, own]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(mm + MAXTRAJ * UPC_B);
+  // dgh_t . W_hh[:, own] as two K halves: one M=128 MMA chain whose rows are
+  // (trajectory, half) and whose N = (unit, half); the diagonal blocks are the
+  // two partial sums (half the MMA instructions of an M=64, N=8 chain)
+  float* mm = reinterpret_cast<float*>(tB + B_BWD);      // [64][8] K half 0
+  float* mm2 = mm + MAXTRAJ * UPC_B;                     // [64][8] K half 1
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(mm2 + MAXTRAJ * UPC_B);
   uint64_t* kbar = mbar + 1;  // [6] one per 4 staged K blocks (32 KB) of dgh_t
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kbar + 6);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j0 = blockIdx.x * UPC_B;
 
-  // resident B: row n = own unit u, K = gate g: B[u][g] = W_hh[g][j0 + u] (K-major)
-  for (int e = tid; e < UPC_B * (kGates / 8); e += THR) {
-    const int u = e / (kGates / 8), c8 = e % (kGates / 8);  // chunk of 8 gates
+  // resident B (K-major, 16 rows x 768): row n = u + 8 h, K = k':
+  // B[n][k'] = W_hh[h * 768 + k'][j0 + u]
+  for (int e = tid; e < 2 * UPC_B * (kGates / 16); e += THR) {
+    const int n = e / (kGates / 16), c8 = e % (kGates / 16);  // chunk of 8 gates
+    const int u = n & (UPC_B - 1), h = n / UPC_B;
     uint32_t w[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      const int g = c8 * 8 + 2 * p;
+      const int g = h * (kGates / 2) + c8 * 8 + 2 * p;
       w[p] = (uint32_t)a.whh[(int64_t)g * kHidden + j0 + u] |
              ((uint32_t)a.whh[(int64_t)(g + 1) * kHidden + j0 + u] << 16);
     }
-    *reinterpret_cast<uint4*>(tB + sw128(UPC_B, u, c8 >> 3, c8 & 7)) =
+    *reinterpret_cast<uint4*>(tB + sw128(2 * UPC_B, n, c8 >> 3, c8 & 7)) =
         make_uint4(w[0], w[1], w[2], w[3]);
   }
   if (tid == 0) {
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
-  constexpr uint32_t idesc = sm100::make_idesc_bf16(MAXTRAJ, UPC_B, 0, 0);
+  constexpr uint32_t idesc = sm100::make_idesc_bf16(2 * MAXTRAJ, 2 * UPC_B, 0, 0);
   unsigned epoch = 0;
   uint32_t phase = 0, kphase = 0;
 
@@ -433,7 +439,8 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
       if (e >= n_cells) continue;
       const int i = e / UPC_B, u = e % UPC_B, j = j0 + u;
       const int64_t s = (int64_t)i * a.T + t;
-      const float dnext = (t == a.T - 1) ? 0.0f : ddr[c] + mm[i * UPC_B + u];
+      const float dnext =
+          (t == a.T - 1) ? 0.0f : ddr[c] + (mm[i * UPC_B + u] + mm2[i * UPC_B + u]);
       const float dh = pf[c][0] + pf[c][6] * dnext;
       const float r = pf[c][1], z = pf[c][2], n = pf[c][3], ghn = pf[c][4], hp = pf[c][5];
       const float dnn = dh * (1.0f - z);
@@ -501,9 +508,10 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
           for (int g = 0; g < 6; ++g) {
             if ((uint32_t)(g & 1) != rank) continue;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              sm100::tma_load_3d_mc(tA + (4 * g + q) * KB_BYTES_A, &a.xmap, &kbar[g],
-                                    (4 * g + q) * 64, 0, t & 1, (uint16_t)0x3);
+            for (int q = 0; q < 4; ++q)  // K block 2g + (q >> 1) of half q & 1
+              sm100::tma_load_3d_mc(tA + (2 * g + (q >> 1)) * 2 * KB_BYTES_A + (q & 1) * KB_BYTES_A,
+                                    &a.xmap, &kbar[g], (q & 1) * (kGates / 2) + (2 * g + (q >> 1)) * 64,
+                                    0, t & 1, (uint16_t)0x3);
           }
         }
         __syncwarp();
@@ -512,9 +520,10 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
         for (int g = 0; g < 6; ++g) {
           sm100::mbar_arrive_expect_tx_warp(&kbar[g], 4 * KB_BYTES_A);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            sm100::tma_load_3d_warp(tA + (4 * g + q) * KB_BYTES_A, &a.xmap, &kbar[g],
-                                    (4 * g + q) * 64, 0, t & 1);
+          for (int q = 0; q < 4; ++q)  // K block 2g + (q >> 1) of half q & 1: rows 64 (q & 1)..
+            sm100::tma_load_3d_warp(tA + (2 * g + (q >> 1)) * 2 * KB_BYTES_A + (q & 1) * KB_BYTES_A,
+                                    &a.xmap, &kbar[g],
+                                    (q & 1) * (kGates / 2) + (2 * g + (q >> 1)) * 64, 0, t & 1);
         }
       }
     }
@@ -525,12 +534,12 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
         sm100::mbar_wait(&kbar[g], kphase);
         sm100::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {  // K16 steps of this 256-wide group
-          const int kg = 16 * g + kk;
+        for (int kk = 0; kk < 8; ++kk) {  // K16 steps of this group's two 128-row K blocks
+          const int kg = 8 * g + kk;        // K16 step in the 768-wide half
           const uint64_t ad =
-              sm100::make_sdesc(a0 + (kg >> 2) * KB_BYTES_A + (kg & 3) * 32, 16, 1024);
+              sm100::make_sdesc(a0 + (kg >> 2) * 2 * KB_BYTES_A + (kg & 3) * 32, 16, 1024);
           const uint64_t bd =
-              sm100::make_sdesc(b0 + (kg >> 2) * UPC_B * 128 + (kg & 3) * 32, 16, 1024);
+              sm100::make_sdesc(b0 + (kg >> 2) * 2 * UPC_B * 128 + (kg & 3) * 32, 16, 1024);
           sm100::umma_f16_warp(tmem, ad, bd, idesc, kg > 0 ? 1u : 0u);
         }
       }
@@ -540,15 +549,15 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_consta
     sm100::mbar_wait(mbar, phase);
     phase ^= 1;
     sm100::tc_fence_after();
-    if (warp < 4) {
+    if (warp < 4) {  // M=128 accumulator: TMEM lane = row = trajectory + 64 * half
       uint32_t r[16];
-      sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16), r);  // cols 0..7 used
+      sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16), r);
       sm100::tmem_ld_wait();
-      if (lane < 16) {
-        const int i = 16 * warp + lane;
+      const int row = 32 * warp + lane;
+      float* dst = warp < 2 ? mm + row * UPC_B : mm2 + (row - MAXTRAJ) * UPC_B;
+      const int c0 = warp < 2 ? 0 : UPC_B;  // diagonal block of the row's K half
 #pragma unroll
-        for (int u = 0; u < UPC_B; ++u) mm[i * UPC_B + u] = __uint_as_float(r[u]);
-      }
+      for (int u = 0; u < UPC_B; ++u) dst[u] = __uint_as_float(r[c0 + u]);
     }
     sm100::tc_fence_before();
     __syncthreads();
@@ -805,7 +814,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THR, 1)
 }
 
 constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + MAXTRAJ * NG * 4 + 128;
-constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + MAXTRAJ * UPC_B * 4 + 128;
+constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + 2 * MAXTRAJ * UPC_B * 4 + 128;
 static_assert(BWD_SMEM <= 227 * 1024, "backward GRU smem");
 
 // Phase profiling of block 0 (env APPO_GRU_PROF=1; diagnostics only): clock64
