@@ -152,20 +152,26 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
                                            ~uintptr_t(1023));
   uint8_t* tA = sm;
   uint8_t* tB = sm + A_TILE;
-  float* gh = reinterpret_cast<float*>(tB + B_FWD);              // [64][NG]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(gh + MAXTRAJ * NG);
+  // h_t . W_hh[own gates]^T as one M=128 chain over the two K halves: rows =
+  // (trajectory, half), N = (gate row, half); the diagonal blocks are the two
+  // partial sums (half the MMA instructions of an M=64 chain)
+  float* gh = reinterpret_cast<float*>(tB + B_FWD);              // [64][NG] K half 0
+  float* gh2 = gh + MAXTRAJ * NG;                                 // [64][NG] K half 1
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(gh2 + MAXTRAJ * NG);
   uint64_t* kbar = mbar + 1;  // [8] one per staged K block of h_t
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kbar + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j0 = blockIdx.x * UPC_F;
   const int B = a.n_traj * a.T;
 
-  // resident B operand: gate row n = g*16 + u (g in r,z,n) -> W_hh row g*512 + j0 + u
-  for (int e = tid; e < NG * 64; e += THR) {
-    const int n = e >> 6, c = e & 63;
+  // resident B operand (2 NG rows x 256): row n + NG h = gate row n = g*16 + u
+  // (g in r,z,n) -> W_hh row g*512 + j0 + u, columns h*256 ..
+  for (int e = tid; e < 2 * NG * 32; e += THR) {
+    const int nn = e >> 5, c = e & 31;  // 16-byte chunk c of the half
+    const int n = nn % NG, h = nn / NG;
     const int grow = (n / UPC_F) * kHidden + j0 + (n % UPC_F);
-    *reinterpret_cast<uint4*>(tB + sw128(NG, n, c >> 3, c & 7)) =
-        reinterpret_cast<const uint4*>(a.whh + (int64_t)grow * kHidden)[c];
+    *reinterpret_cast<uint4*>(tB + sw128(2 * NG, nn, c >> 3, c & 7)) =
+        reinterpret_cast<const uint4*>(a.whh + (int64_t)grow * kHidden)[h * 32 + c];
   }
   if (tid == 0) {
     sm100::mbar_init(mbar, 1);
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
     sm100::fence_barrier_init();
   }
   if (warp == 0) {
-    sm100::tmem_alloc(tslot, 64);
+    sm100::tmem_alloc(tslot, 128);
     sm100::tmem_relinquish();
   }
   // Per-thread cells (trajectory i, own unit u) are fixed across steps.
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
   grid_barrier(a.bar, gridDim.x);  // h0 bf16 complete everywhere
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
-  constexpr uint32_t idesc = sm100::make_idesc_bf16(MAXTRAJ, NG, 0, 0);
+  constexpr uint32_t idesc = sm100::make_idesc_bf16(2 * MAXTRAJ, 2 * NG, 0, 0);
   unsigned epoch = 1;
   uint32_t phase = 0;
 
@@ -226,22 +232,25 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
     if (warp == 1) {
       fence_proxy_async_global();
 #pragma unroll
-      for (int kb = 0; kb < 8; ++kb) {
-        sm100::mbar_arrive_expect_tx_warp(&kbar[kb], KB_BYTES_A);
-        sm100::tma_load_3d_warp(tA + kb * KB_BYTES_A, &a.hmap, &kbar[kb], kb * 64, 0, t & 1);
+      for (int q = 0; q < 8; ++q) {  // K block kb = q >> 1 of half q & 1 (h_t columns 64 q')
+        const int kb = q >> 1, h = q & 1, col = (h * 4 + kb) * 64;
+        sm100::mbar_arrive_expect_tx_warp(&kbar[q], KB_BYTES_A);
+        sm100::tma_load_3d_warp(tA + kb * 2 * KB_BYTES_A + h * KB_BYTES_A, &a.hmap, &kbar[q], col,
+                                0, t & 1);
       }
     }
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 1] = clock64();
     if (warp == 0) {  // whole warp: elect.sync inside (no per-MMA waterfall)
       const uint32_t a0 = sm100::smem_u32(tA), b0 = sm100::smem_u32(tB);
 #pragma unroll
-      for (int kb = 0; kb < 8; ++kb) {
-        sm100::mbar_wait(&kbar[kb], t & 1);
+      for (int kb = 0; kb < 4; ++kb) {
+        sm100::mbar_wait(&kbar[2 * kb], t & 1);
+        sm100::mbar_wait(&kbar[2 * kb + 1], t & 1);
         sm100::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint64_t ad = sm100::make_sdesc(a0 + kb * KB_BYTES_A + k * 32, 16, 1024);
-          const uint64_t bd = sm100::make_sdesc(b0 + kb * NG * 128 + k * 32, 16, 1024);
+          const uint64_t ad = sm100::make_sdesc(a0 + kb * 2 * KB_BYTES_A + k * 32, 16, 1024);
+          const uint64_t bd = sm100::make_sdesc(b0 + kb * 2 * NG * 128 + k * 32, 16, 1024);
           sm100::umma_f16_warp(tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
         }
       }
@@ -251,17 +260,17 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
     phase ^= 1;
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
     sm100::tc_fence_after();
-    if (warp < 4) {
+    if (warp < 4) {  // M=128 accumulator: TMEM lane = row = trajectory + 64 * half
       uint32_t r[16];
+      const int row = 32 * warp + lane;
+      float* dst = warp < 2 ? gh + row * NG : gh2 + (row - MAXTRAJ) * NG;
+      const int c0 = warp < 2 ? 0 : NG;  // diagonal block of the row's K half
 #pragma unroll
       for (int cb = 0; cb < NG; cb += 16) {
-        sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + cb, r);
+        sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0 + cb, r);
         sm100::tmem_ld_wait();
-        if (lane < 16) {
-          const int i = 16 * warp + lane;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) gh[i * NG + cb + q] = __uint_as_float(r[q]);
-        }
+        for (int q = 0; q < 16; ++q) dst[cb + q] = __uint_as_float(r[q]);
       }
     }
     sm100::tc_fence_before();
@@ -274,9 +283,9 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
       const int e = tid + c * THR;
       if (e >= n_cells) continue;
       const int i = e / UPC_F, u = e % UPC_F, j = j0 + u;
-      const float ghr = gh[i * NG + u] + b3[c][0];
-      const float ghz = gh[i * NG + UPC_F + u] + b3[c][1];
-      const float ghn = gh[i * NG + 2 * UPC_F + u] + b3[c][2];
+      const float ghr = (gh[i * NG + u] + gh2[i * NG + u]) + b3[c][0];
+      const float ghz = (gh[i * NG + UPC_F + u] + gh2[i * NG + UPC_F + u]) + b3[c][1];
+      const float ghn = (gh[i * NG + 2 * UPC_F + u] + gh2[i * NG + 2 * UPC_F + u]) + b3[c][2];
       const float rr = sig_(g3[c][0] + ghr);
       const float z = sig_(g3[c][1] + ghz);
       const float n = tanh_(g3[c][2] + rr * ghn);
@@ -324,7 +333,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
   __syncthreads();
   if (warp == 0) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc(tmem, 64);
+    sm100::tmem_dealloc(tmem, 128);
   }
 }
 
@@ -813,7 +822,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THR, 1)
   sm100::cluster_sync();  // no CTA leaves while a peer may still multicast into it
 }
 
-constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + MAXTRAJ * NG * 4 + 128;
+constexpr int FWD_SMEM = 1024 + A_TILE + B_FWD + 2 * MAXTRAJ * NG * 4 + 128;
 constexpr int BWD_SMEM = 1024 + 3 * A_TILE + B_BWD + 2 * MAXTRAJ * UPC_B * 4 + 128;
 static_assert(BWD_SMEM <= 227 * 1024, "backward GRU smem");
 
