@@ -480,16 +480,26 @@ __global__ void __launch_bounds__(256)
   float acc[kMaxActions + 1];
 #pragma unroll
   for (int a = 0; a <= kMaxActions; ++a) acc[a] = 0.0f;
-  for (int q = 0; q < kHidden / 32; ++q) {
-    const int j = lane + 32 * q;
-    const float h = core[row * kHidden + j];
+  // lane owns units 4 j4 .. 4 j4 + 3, j4 = lane + 32 q (float4 rows; wv sits at
+  // an odd parameter offset: scalar loads)
+  const float4* crow = reinterpret_cast<const float4*>(core + row * kHidden);
+#pragma unroll
+  for (int q = 0; q < kHidden / 128; ++q) {
+    const int j4 = lane + 32 * q;
+    const float4 h = __ldg(crow + j4);
 #pragma unroll
     for (int a = 0; a < kMaxActions; ++a)
-      if (a < A) acc[a] += wpi[a * kHidden + j] * h;
-    acc[kMaxActions] += wv[j] * h;
+      if (a < A) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(wpi + a * kHidden) + j4);
+        acc[a] += w.x * h.x + w.y * h.y + w.z * h.z + w.w * h.w;
+      }
+    acc[kMaxActions] += __ldg(wv + 4 * j4) * h.x + __ldg(wv + 4 * j4 + 1) * h.y +
+                        __ldg(wv + 4 * j4 + 2) * h.z + __ldg(wv + 4 * j4 + 3) * h.w;
   }
 #pragma unroll
-  for (int a = 0; a <= kMaxActions; ++a) acc[a] = warp_sum(acc[a]);
+  for (int a = 0; a < kMaxActions; ++a)
+    if (a < A) acc[a] = warp_sum(acc[a]);
+  acc[kMaxActions] = warp_sum(acc[kMaxActions]);
   // lane a < A holds logit a (all lanes hold the sums after warp_sum)
   float my = 0.0f;
 #pragma unroll
@@ -981,6 +991,8 @@ int k_gru_train(Ctx* c, int n_traj, int T, int t, const float* gi, const float* 
 int k_heads_fwd(Ctx* c, int64_t R, int A, const float* core, const float* wpi, const float* bpi,
                 const float* wv, const float* bv, float* logits, float* values, int64_t B,
                 const int32_t* act, float* tlogp, float* ent) {
+  APPO_REQUIRE(((reinterpret_cast<uintptr_t>(core) | reinterpret_cast<uintptr_t>(wpi)) & 15) == 0,
+               APPO_ERR_CONTRACT, "heads: core / policy head must be 16-byte aligned");
   APPO_LAUNCH(c, heads_fwd_kernel, (int)((R + 7) / 8), 256, 0, R, A, core, wpi, bpi, wv, bv,
               logits, values, B, act, tlogp, ent, c->d_flags);
   return APPO_OK;
