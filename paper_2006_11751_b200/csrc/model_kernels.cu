@@ -608,17 +608,23 @@ __global__ void __launch_bounds__(256)
     const float* lg = logits + (int64_t)s * A;
     const int a_s = act[s];
     if (a_s < 0 || a_s >= A) atomicOr(flags + kFlagContract, 1);
+    // fp64 log-softmax: one exp per action and a single log
     double mx = lg[0];
     for (int a = 1; a < A; ++a) mx = fmax(mx, (double)lg[a]);
-    double z = 0;
-    for (int a = 0; a < A; ++a) z += exp((double)lg[a] - mx);
-    double p[kMaxActions], H = 0;
+    double ex[kMaxActions], z = 0;
     for (int a = 0; a < A; ++a) {
-      p[a] = exp((double)lg[a] - mx) / z;
-      if (p[a] > 0) H -= p[a] * log(p[a]);
+      ex[a] = exp((double)lg[a] - mx);
+      z += ex[a];
+    }
+    const double lz = log(z);
+    double p[kMaxActions], lp[kMaxActions], H = 0;
+    for (int a = 0; a < A; ++a) {
+      p[a] = ex[a] / z;
+      lp[a] = ((double)lg[a] - mx) - lz;
+      if (p[a] > 0) H -= p[a] * lp[a];
     }
     const int ac = min(max(a_s, 0), A - 1);
-    const double logp = log(fmax(p[ac], 1e-300));
+    const double logp = fmax(lp[ac], -690.7755278982137);  // log(1e-300) floor
     double d = logp - (double)blogp[s];
     d = fmin(fmax(d, -20.0), 20.0);
     const double ratio = exp(d);
@@ -632,7 +638,7 @@ __global__ void __launch_bounds__(256)
     const double dV = hp.value_coef * invB * 2.0 * verr;
     for (int a = 0; a < A; ++a) {
       const double dlp = (a == ac ? 1.0 : 0.0) - p[a];
-      const double dH = p[a] > 0 ? -p[a] * (log(p[a]) + H) : 0.0;
+      const double dH = p[a] > 0 ? -p[a] * (lp[a] + H) : 0.0;
       const float g = (float)(dL_dlogp * dlp - hp.entropy_coef * invB * dH);
       dlog[(int64_t)s * (A + 1) + a] = g;
       dhead[(int64_t)s * 16 + a] = f2bf(g);
@@ -1012,9 +1018,10 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
                const int32_t* act, const float* blogp, const float* adv, const float* vt,
                const LossHP& hp, float* dlog, uint16_t* dhead, double* stats, const int64_t* ver,
                int64_t cur) {
-  const int grid = (B + 255) / 256;
+  // 64-thread blocks: the per-row fp64 softmax is latency-bound, spread it over SMs
+  const int grid = (B + 63) / 64;
   APPO_REQUIRE(grid * 6 <= kRedSlots, APPO_ERR_CONTRACT, "ppo_loss: batch too large");
-  APPO_LAUNCH(c, ppo_loss_kernel, grid, 256, 0, B, A, logits, values, act, blogp, adv, vt, hp,
+  APPO_LAUNCH(c, ppo_loss_kernel, grid, 64, 0, B, A, logits, values, act, blogp, adv, vt, hp,
               dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
   return APPO_OK;
 }
