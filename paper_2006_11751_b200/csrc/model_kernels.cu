@@ -263,9 +263,11 @@ __global__ void __launch_bounds__(256)
                            int64_t off_c3w, uint16_t* __restrict__ c1h, float* __restrict__ c1b,
                            uint16_t* __restrict__ wt2, uint16_t* __restrict__ wt3) {
   APPO_PDL_ENTRY();
-  if (blockIdx.x == gridDim.x - 1) {
+  constexpr int kC1Blocks = 4;  // conv1 operands: 8 output channels (a warp each) per block
+  if (blockIdx.x >= gridDim.x - kC1Blocks) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int co = warp; co < 32; co += blockDim.x >> 5) {
+    const int cb = blockIdx.x - (gridDim.x - kC1Blocks);
+    for (int co = cb * 8 + warp; co < 32 && warp < 8; co += 32) {
       float acc = 0.0f;
       for (int k = lane; k < K1; k += 32) {
         const __half h = __float2half_rn(pf[off_c1w + (size_t)co * K1 + k]);
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(256)
   // wt3: Co=128, k=3, Ci=64 (4*64*512 elements); wt2: Co=64, k=4, Ci=32 (4*32*256)
   const int n3 = 4 * 64 * 512, n2 = 4 * 32 * 256;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n3 + n2;
-       g += (gridDim.x - 1) * blockDim.x) {
+       g += (gridDim.x - kC1Blocks) * blockDim.x) {
     const bool is3 = g < n3;
     const int e = is3 ? g : g - n3;
     const int Co = is3 ? 128 : 64, k = is3 ? 3 : 4, Ci = is3 ? 64 : 32;
@@ -949,7 +951,7 @@ int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* 
 }
 int k_publish_derived(Ctx* c, const uint16_t* wb, const float* pf, const Dims& d, uint16_t* c1h,
                       float* c1b, uint16_t* wt2, uint16_t* wt3) {
-  APPO_LAUNCH(c, publish_derived_kernel, 97, 256, 0, wb, pf, d.off_c1w, d.off_c1b, d.K1, d.off_c2w,
+  APPO_LAUNCH(c, publish_derived_kernel, 148, 256, 0, wb, pf, d.off_c1w, d.off_c1b, d.K1, d.off_c2w,
               d.off_c3w, c1h, c1b, wt2, wt3);
   return APPO_OK;
 }

@@ -257,3 +257,29 @@ def test_async_submit_collect_determinism_and_rejected_steps():
     b = ref.policy_forward(obs, h, want_logits=True)
     torch.cuda.synchronize()
     assert torch.equal(a["logits"], b["logits"])
+
+
+@pytest.mark.parametrize("pdl", [False, True])
+def test_programmatic_dependent_launch_is_bitwise_neutral(pdl):
+    # every kernel waits on griddepcontrol before touching its predecessor's
+    # outputs: learner steps and inference give identical bits with PDL on/off
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    store = appo.TrajectoryStore(desc, 4)
+    fill_store(store, 4, np.random.default_rng(12), 6)
+    hp = appo.HParams.defaults(lr=3e-4)
+    ref = appo.Context(0, seed=31, model=desc)
+    ref.set_pdl(False)
+    ctx = appo.Context(0, seed=31, model=desc)
+    ctx.set_pdl(pdl)
+    for _ in range(3):
+        a = ref.learner_step(store.region, store.slot_bytes, [3, 1, 0], hp)
+        b = ctx.learner_step(store.region, store.slot_bytes, [3, 1, 0], hp)
+        assert a["total_loss"] == b["total_loss"] and a["grad_norm"] == b["grad_norm"]
+    assert np.array_equal(ref.get_params()[0], ctx.get_params()[0])
+    rs = np.random.default_rng(3)
+    obs = torch.from_numpy(rs.integers(0, 256, (64, desc.obs_dim), dtype=np.uint8)).cuda()
+    h = torch.from_numpy(rs.normal(size=(64, 512)).astype(np.float32)).cuda()
+    oa = ref.policy_forward(obs, h, want_logits=True)
+    ob = ctx.policy_forward(obs, h, want_logits=True)
+    torch.cuda.synchronize()
+    assert torch.equal(oa["logits"], ob["logits"]) and torch.equal(oa["h_out"], ob["h_out"])
