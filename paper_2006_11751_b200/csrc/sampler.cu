@@ -18,6 +18,7 @@
 // sampled actions are copied back, i.e. the exchange-row round trip.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "gemm.cuh"
@@ -47,6 +48,15 @@ struct appo_sampler {
   float* values = nullptr;
   uint64_t steps_done = 0;
   appo_slotq* ready_q = nullptr;  // sealed slots are pushed here at t == T-1
+  // host observations (CPU actors): contiguous pinned -> device copies on an
+  // internal copy stream into two staging buffers, so step t+1's transfer
+  // overlaps step t's inference; a scatter kernel on the ctx stream moves them
+  // into the slots (region writes stay ordered on the ctx stream)
+  cudaStream_t copy_stream = nullptr;
+  uint8_t* staging[2] = {nullptr, nullptr};
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  cudaEvent_t consumed[2] = {nullptr, nullptr};
+  int stage_next = 0;
 };
 
 namespace {
@@ -78,6 +88,20 @@ __global__ void gen_obs_kernel(int n_envs, int64_t obs_dim, uint64_t seed,
     const int w = w0 + 256 * k;
     if (w < words) dst[w] = splitmix64(key ^ (uint64_t)w);
   }
+}
+
+// Staged host observations [n_envs][obs_dim] -> slot rows (16-byte vectors).
+__global__ void scatter_obs_kernel(int n_envs, int64_t obs_dim, const uint4* __restrict__ src,
+                                   uint8_t* region, uint64_t slot_bytes, int64_t slot_base,
+                                   uint64_t off) {
+  APPO_PDL_ENTRY();
+  const int64_t v = obs_dim >> 4;
+  const int e = blockIdx.y;
+  uint4* dst = reinterpret_cast<uint4*>(region + (uint64_t)(slot_base + e) * slot_bytes + off);
+  const uint4* srow = src + (int64_t)e * v;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < v;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldg(srow + i);
 }
 
 // Step record + env transition; one block (128 threads) per env.
@@ -203,6 +227,15 @@ APPO_API int appo_sampler_destroy(appo_sampler* s) {
   cudaFree(s->actions);
   cudaFree(s->logp);
   cudaFree(s->values);
+  for (int k = 0; k < 2; ++k) {
+    if (s->staging[k]) cudaFree(s->staging[k]);
+    if (s->copied[k]) cudaEventDestroy(s->copied[k]);
+    if (s->consumed[k]) cudaEventDestroy(s->consumed[k]);
+  }
+  if (s->copy_stream) {
+    cudaStreamSynchronize(s->copy_stream);
+    cudaStreamDestroy(s->copy_stream);
+  }
   delete s;
   return APPO_OK;
 }
@@ -223,7 +256,35 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
                "sampler_step: bad slot region");
   uint8_t* region = static_cast<uint8_t*>(d_region);
   const uint64_t obs_off = d.slot[0] + (uint64_t)t * d.obs_dim;
-  if (h_obs) {
+  const bool staged = h_obs && d.obs_dim % 16 == 0 && slot_bytes % 16 == 0 &&
+                      ((reinterpret_cast<uintptr_t>(region) + obs_off) & 15) == 0;
+  if (h_obs && staged) {
+    const size_t bytes = (size_t)s->n_envs * d.obs_dim;
+    if (!s->copy_stream) {
+      APPO_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        APPO_CUDA_TRY(cudaMalloc(&s->staging[k], bytes));
+        APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->copied[k], cudaEventDisableTiming));
+        APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->consumed[k], cudaEventDisableTiming));
+        APPO_CUDA_TRY(cudaEventRecord(s->consumed[k], c->stream));
+      }
+    }
+    const int k = s->stage_next;
+    s->stage_next ^= 1;
+    // the buffer's previous contents were scattered (ctx stream) before it is refilled
+    APPO_CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->consumed[k], 0));
+    APPO_CUDA_TRY(cudaMemcpyAsync(s->staging[k], h_obs, bytes, cudaMemcpyHostToDevice,
+                                  s->copy_stream));
+    APPO_CUDA_TRY(cudaEventRecord(s->copied[k], s->copy_stream));
+    APPO_CUDA_TRY(cudaStreamWaitEvent(c->stream, s->copied[k], 0));
+    const dim3 grid((unsigned)std::min<int64_t>(((d.obs_dim >> 4) + 255) / 256, 8),
+                    (unsigned)s->n_envs);
+    c->next_bytes = 2.0 * (double)bytes;
+    APPO_LAUNCH(c, scatter_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim,
+                reinterpret_cast<const uint4*>(s->staging[k]), region, slot_bytes,
+                (int64_t)slot_base, obs_off);
+    APPO_CUDA_TRY(cudaEventRecord(s->consumed[k], c->stream));
+  } else if (h_obs) {
     APPO_CUDA_TRY(cudaMemcpy2DAsync(region + (uint64_t)slot_base * slot_bytes + obs_off,
                                     slot_bytes, h_obs, d.obs_dim, d.obs_dim, s->n_envs,
                                     cudaMemcpyHostToDevice, c->stream));

@@ -129,3 +129,25 @@ def test_overlapped_sampler_and_learner_streams():
     for s in range(2 * n):
         v = store.versions(s).cpu().numpy()
         assert np.all(np.diff(v) >= 0) and v.min() >= 0 and v.max() <= final
+
+
+def test_host_observations_staged_into_slots():
+    # CPU-actor path: pinned host obs per step, copied on the sampler's copy
+    # stream through two staging buffers and scattered into the slots
+    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    ctx = appo.Context(0, seed=4, model=desc)
+    n = 24
+    store = appo.TrajectoryStore(desc, 2 * n)
+    smp = appo.Sampler(ctx, n, episode_len=9, seed=5)
+    rs = np.random.default_rng(7)
+    host = [torch.from_numpy(rs.integers(0, 256, (n, desc.obs_dim), dtype=np.uint8)).pin_memory()
+            for _ in range(desc.T)]
+    acts = torch.empty(n, dtype=torch.int32).pin_memory()
+    for rep in range(2):  # second rollout reuses the staging buffers
+        for t in range(desc.T):
+            smp.step(store, n * rep, t, h_obs=host[(t + rep) % desc.T], h_actions=acts)
+        torch.cuda.synchronize()
+        for e in (0, 11, n - 1):
+            got = store.obs(n * rep + e).cpu()
+            for t in range(desc.T):
+                assert torch.equal(got[t], host[(t + rep) % desc.T][e]), (rep, e, t)
