@@ -190,6 +190,69 @@ class Context {
   appo_ctx* h_ = nullptr;
 };
 
+// Device slot FIFO (ready queue / free list, trajstore.hpp:293-331).
+class SlotQueue {
+ public:
+  SlotQueue(int device, int32_t n_slots, int32_t capacity = 0, double timeout_s = 2.0) {
+    check(appo_slotq_create(device, n_slots, capacity, timeout_s, &q_));
+  }
+  ~SlotQueue() { appo_slotq_destroy(q_); }
+  SlotQueue(const SlotQueue&) = delete;
+  SlotQueue& operator=(const SlotQueue&) = delete;
+  appo_slotq* get() const { return q_; }
+  void push(const Context& c, const int32_t* d_ids, int n) const {
+    check(appo_slotq_push(c.get(), q_, d_ids, n));
+  }
+  void push_range(const Context& c, int32_t first, int n) const {
+    check(appo_slotq_push_range(c.get(), q_, first, n));
+  }
+  void pop(const Context& c, int32_t* d_out, int n) const { check(appo_slotq_pop(c.get(), q_, d_out, n)); }
+  // assemble_minibatch + LearnerUnit::step without the host seeing slot ids
+  void learner_submit(const Context& c, const void* d_region, uint64_t slot_bytes,
+                      const SlotQueue* free_q, int n_traj, const appo_hparams& hp) const {
+    check(appo_learner_submit_queued(c.get(), d_region, slot_bytes, q_,
+                                     free_q ? free_q->get() : nullptr, n_traj, &hp));
+  }
+
+ private:
+  appo_slotq* q_ = nullptr;
+};
+
+// PbtController (runner.hpp:169-252) over learner contexts; copy_weights is
+// appo_params_copy between the contexts (device to device).
+class PbtController {
+ public:
+  PbtController(const appo_pbt_config& cfg, std::vector<Context*> learners, uint64_t rng_seed,
+                const std::vector<appo_agent_meta>* init = nullptr)
+      : learners_(learners.size()) {
+    for (size_t i = 0; i < learners.size(); ++i) learners_[i] = learners[i]->get();
+    check(appo_pbt_create(&cfg, static_cast<int>(learners.size()), rng_seed,
+                          init ? init->data() : nullptr, &p_));
+  }
+  ~PbtController() { appo_pbt_destroy(p_); }
+  PbtController(const PbtController&) = delete;
+  PbtController& operator=(const PbtController&) = delete;
+  void record(uint32_t policy, double value) const { check(appo_pbt_record(p_, policy, value)); }
+  // PbtController::tick: the events of a PBT step, or nothing before the boundary
+  std::vector<appo_pbt_event> tick(int64_t frames) {
+    std::vector<appo_pbt_event> ev(static_cast<size_t>(appo_pbt_max_events(p_)));
+    int n = 0, fired = 0;
+    check(appo_pbt_tick(p_, frames, appo_pbt_copy_contexts, learners_.data(), ev.data(),
+                        static_cast<int>(ev.size()), &n, &fired));
+    ev.resize(fired ? static_cast<size_t>(n) : 0);
+    return ev;
+  }
+  appo_agent_meta agent(int i) const {
+    appo_agent_meta a{};
+    check(appo_pbt_get_agent(p_, i, &a));
+    return a;
+  }
+
+ private:
+  std::vector<appo_ctx*> learners_;
+  appo_pbt* p_ = nullptr;
+};
+
 inline appo_hparams default_hparams() {
   appo_hparams hp{};
   hp.lr = 1e-4f; hp.beta1 = 0.9f; hp.beta2 = 0.999f; hp.eps = 1e-6f; hp.grad_clip = 4.0f;

@@ -67,6 +67,34 @@ int main() {
   m2.load_checkpoint(ck);
   REQUIRE(m2.fetch(theta2) == 0 && theta2 == theta);
   std::remove(ck.c_str());
+
+  // PBT over two learners: policy 0 scores higher, policy 1 takes its weights
+  appo_pbt_config pc{};
+  pc.pbt_period = 100; pc.mutate_fraction = 0.0; pc.mutation_rate = 0.15;
+  pc.mutation_factor = 1.2; pc.replace_fraction = 0.5; pc.window = 10;
+  Context l0(0, 5, &desc), l1(0, 6, &desc);
+  PbtController pbt(pc, {&l0, &l1}, appo_pbt_controller_seed(1));
+  pbt.record(0, 1.0);
+  pbt.record(1, 0.0);
+  REQUIRE(pbt.tick(50).empty());
+  const auto ev = pbt.tick(100);
+  REQUIRE(ev.size() == 1 && ev[0].event == 1 && ev[0].agent == 1);
+  std::vector<float> p0, p1;
+  l0.fetch(p0);
+  l1.fetch(p1);
+  REQUIRE(p0 == p1);
+
+  // device ready queue: ids pushed on the device come back in FIFO order
+  SlotQueue q(0, 8);
+  DeviceBuffer<int32_t> ids(3), popped(3);
+  const int32_t h_ids[3] = {5, 2, 7};
+  ids.upload(h_ids);
+  q.push(m, ids.get(), 3);
+  q.pop(m, popped.get(), 3);
+  m.sync();
+  int32_t h_got[3];
+  popped.download(h_got);
+  REQUIRE(h_got[0] == 5 && h_got[1] == 2 && h_got[2] == 7);
   std::printf("capi_host_test ok\n");
   return 0;
 }
