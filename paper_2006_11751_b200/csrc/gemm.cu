@@ -1070,6 +1070,16 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
     float bsum[NCHB];  // dgrad bias sums: lane l < 16 owns column part*HALF + ch*16 + l
 #pragma unroll
     for (int j = 0; j < NCHB; ++j) bsum[j] = 0.0f;
+    // conv1 forward (N == BN == 32, HALF == 16): this warp's bias columns and
+    // the scale, loaded once for every tile
+    float u8_bias[16];
+    float u8_scale = 1.0f;
+    if constexpr (AG == AG_U8 && EV == EV_ELU_BF16) {
+      u8_scale = p.epi.scale;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        u8_bias[j] = (p.epi.flags & EPI_BIAS) ? __ldg(p.epi.bias + half * HALF + j) : 0.0f;
+    }
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit un = decode_unit(p, u);
       const int tn = un.tn, z = un.z;
@@ -1124,7 +1134,23 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
                         (unsigned long long)llrint((double)t * 4294967296.0));
             continue;
           }
-          if constexpr (AG == AG_U8) {  // tile rows -> (output row, x); padding skipped
+          if constexpr (AG == AG_U8 && EV == EV_ELU_BF16) {
+            // conv1: the warp's 16 columns never change (N == BN), so scale and
+            // bias stay in registers; x*scale + bias -> ELU -> bf16 row store
+            const int mo = u8_out_row(p.g, m);
+            if (mo >= 0 && mo < p.M) {
+              uint32_t w[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                w[q] = pack_bf16(elu_fast(fmaf(__uint_as_float(r[2 * q]), u8_scale, u8_bias[2 * q])),
+                                 elu_fast(fmaf(__uint_as_float(r[2 * q + 1]), u8_scale,
+                                               u8_bias[2 * q + 1])));
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.epi.out) +
+                                                    (size_t)mo * p.epi.ldo + c);
+              dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+          } else if constexpr (AG == AG_U8) {  // tile rows -> (output row, x); padding skipped
             const int mo = u8_out_row(p.g, m);
             if (mo >= 0) epilogue_dispatch<EV>(p, mo, tn * BN + c, z, r);
           } else if constexpr (AG == AG_TAPS) {  // tile = nq whole images, rows beyond are padding
