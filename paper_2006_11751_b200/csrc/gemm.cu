@@ -594,13 +594,22 @@ __device__ __forceinline__ void u8_stage_bulk(const GatherP& g, int tile, uint8_
 // Values are written as fp16 (1024 + v): one PRMT per pair, exact for v in
 // 0..255 (fp16 has unit spacing on [1024, 2048)); the constant 1024 * sum(W)
 // is removed through the epilogue bias (k_conv1_half_weights).
-__device__ __forceinline__ void u8_convert(const GatherP& g, const uint8_t* buf, const int* meta,
+// Thread gt's source address (channel 0) in a staged tile: slot base + the row's
+// meta offset (read through a shared-space load) + its kernel rows and column.
+__device__ __forceinline__ uint32_t u8_src0(const GatherP& g, const uint8_t* buf, const int* meta,
+                                            int gt) {
+  constexpr int KHT = 8 / (U8_CONV_THREADS / 128);
+  const int row = gt & 127, kh0 = (gt >> 7) * KHT;
+  int mk;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mk) : "r"(sm100::smem_u32(meta + (row >> 5))));
+  return sm100::smem_u32(buf) + mk + kh0 * g.Wi + 4 * (row & 31);
+}
+
+__device__ __forceinline__ void u8_convert(const GatherP& g, uint32_t src0, int plane,
                                            uint8_t* sA, int c, int gt) {
   constexpr int KHT = 8 / (U8_CONV_THREADS / 128);  // kernel rows per thread
   const int row = gt & 127, kh0 = (gt >> 7) * KHT;
-  const int k = row >> 5, x = row & 31;
-  const int plane = g.tma ? U8_BOX_ROWS * g.Wi : U8_BLK;
-  const uint32_t src = sm100::smem_u32(buf) + meta[k] + c * plane + kh0 * g.Wi + 4 * x;
+  const uint32_t src = src0 + c * plane;
   const uint32_t row_base = sm100::smem_u32(sA) + row * 128;
 #pragma unroll
   for (int j = 0; j < KHT; ++j) {
@@ -1014,15 +1023,17 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
       uint64_t* sfull = reinterpret_cast<uint64_t*>(bar_base + BAR_AUX);
       uint64_t* sempty = sfull + U8_NSTG;
       int* sdelta = reinterpret_cast<int*>(stg + U8_NSTG * u8_stage_bytes(p.g.Cin));
+      const int u8_plane = p.g.tma ? U8_BOX_ROWS * p.g.Wi : U8_BLK;
       int slot = 0;
       uint32_t sphase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         sm100::mbar_wait(&sfull[slot], sphase);
         if (gt == 0) GEMM_PROF(1);
+        const uint32_t src0 = u8_src0(p.g, stg + slot * u8_stage_bytes(p.g.Cin),
+                                      sdelta + slot * U8_ROWS, gt);
         for (int c = 0; c < p.nkb; ++c) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
-          u8_convert(p.g, stg + slot * u8_stage_bytes(p.g.Cin), sdelta + slot * U8_ROWS,
-                     smem + stage * SST, c, gt);
+          u8_convert(p.g, src0, u8_plane, smem + stage * SST, c, gt);
           sm100::mbar_arrive(&full[stage]);
           if (gt == 0 && c == 0) GEMM_PROF(2);
           if (++stage == NST) {
