@@ -341,6 +341,8 @@ def run_ours(args, ws, rank, local):
                "h2d_bytes_per_step": n * desc.obs_dim * args.T + n_mb * tpb * 4,
                "d2h_bytes_per_step": n * 4 * args.T + n_mb * (8 * 10 + 16),
                "path": "appo_sampler_step(h_obs pinned) + appo_learner_submit/collect"}
+        # the host link is the e2e bound: H2D rate achieved over the timed region
+        e2e["h2d_gbps"] = e2e["h2d_bytes_per_step"] * args.steps / (ems / 1000.0) / 1e9
 
     peaks, peak_src = load_peaks()
     roof = None
