@@ -1167,6 +1167,45 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
           } else if constexpr (AG == AG_TAPS) {  // tile = nq whole images, rows beyond are padding
             const int rpt = p.g.P * p.g.nq, loc = m - un.tm * BM;
             if (loc < rpt) epilogue_dispatch<EV>(p, un.tm * rpt + loc, tn * BN + c, z, r);
+          } else if constexpr (EV == EV_F32 && AG == AG_NONE) {
+            // fp32 rows: lane pairs (row m, row m ^ 1) swap half-chunks so each
+            // 16-byte store instruction of the warp covers whole 32-byte sectors
+            const int n0 = tn * BN + c;
+            const bool paired = __all_sync(0xffffffffu, m < p.M) && n0 + 16 <= p.N &&
+                                (p.epi.ldo & 7) == 0;
+            if (!paired) {
+              epilogue_dispatch<EV>(p, m, n0, z, r);
+            } else {
+              const Epilogue& e = p.epi;
+              float v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * e.scale;
+              if (e.flags & EPI_BIAS) {
+                const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float4 b = __ldg(b4 + j);
+                  v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+                }
+              }
+              const int par = lane & 1;
+              float* base = reinterpret_cast<float*>(e.out) + (size_t)(m - par) * e.ldo + n0 + 4 * par;
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                float snd[4], rcv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  snd[k] = par ? v[8 * q + k] : v[8 * q + 4 + k];
+                  rcv[k] = __shfl_xor_sync(0xffffffffu, snd[k], 1);
+                }
+                const float4 first = par ? make_float4(rcv[0], rcv[1], rcv[2], rcv[3])
+                                         : make_float4(v[8 * q], v[8 * q + 1], v[8 * q + 2], v[8 * q + 3]);
+                const float4 second = par ? make_float4(v[8 * q + 4], v[8 * q + 5], v[8 * q + 6], v[8 * q + 7])
+                                          : make_float4(rcv[0], rcv[1], rcv[2], rcv[3]);
+                *reinterpret_cast<float4*>(base + 8 * q) = first;             // row m - par
+                *reinterpret_cast<float4*>(base + e.ldo + 8 * q) = second;    // row m - par + 1
+              }
+            }
           } else {
             epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
           }
