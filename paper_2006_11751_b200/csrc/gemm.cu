@@ -1206,6 +1206,30 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
                 *reinterpret_cast<float4*>(base + e.ldo + 8 * q) = second;    // row m - par + 1
               }
             }
+          } else if constexpr (EV == EV_SPLIT) {
+            // split-K fp32 partials: the same sector-aligned lane-pair stores
+            const int n0 = tn * BN + c;
+            const bool paired = __all_sync(0xffffffffu, m < p.M) && n0 + 16 <= p.N &&
+                                (p.N & 7) == 0;
+            if (!paired) {
+              epilogue_dispatch<EV>(p, m, n0, z, r);
+            } else {
+              const int par = lane & 1;
+              float* base = p.partial + ((size_t)z * p.M + (m - par)) * p.N + n0 + 4 * par;
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                uint32_t rcv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  rcv[k] = __shfl_xor_sync(0xffffffffu, par ? r[8 * q + k] : r[8 * q + 4 + k], 1);
+                const uint4 first = par ? make_uint4(rcv[0], rcv[1], rcv[2], rcv[3])
+                                        : make_uint4(r[8 * q], r[8 * q + 1], r[8 * q + 2], r[8 * q + 3]);
+                const uint4 second = par ? make_uint4(r[8 * q + 4], r[8 * q + 5], r[8 * q + 6], r[8 * q + 7])
+                                         : make_uint4(rcv[0], rcv[1], rcv[2], rcv[3]);
+                *reinterpret_cast<uint4*>(base + 8 * q) = first;
+                *reinterpret_cast<uint4*>(base + p.N + 8 * q) = second;
+              }
+            }
           } else {
             epilogue_dispatch<EV>(p, m, tn * BN + c, z, r);
           }
