@@ -65,7 +65,7 @@ __device__ __forceinline__ uint64_t dev_derive_seed(uint64_t seed, uint64_t stre
   return splitmix64(seed ^ splitmix64(stream + 1));
 }
 
-constexpr int kObsWordsPerThread = 4;
+constexpr int kObsWordsPerThread = 8;
 
 // obs for env e at its current (episode, step): 8 pixels per hash.
 // grid (ceil(words / 256), n_envs): env from blockIdx.y, no 64-bit division
