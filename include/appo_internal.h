@@ -25,6 +25,15 @@ APPO_API int appo_dbg_gemm(appo_ctx* ctx, int M, int N, int K, const void* d_a, 
  * published bf16 copy (for tests that compare against the oracle). */
 APPO_API int appo_dbg_model_ptrs(appo_ctx* ctx, float** theta, float** grad, void** pub_bf16);
 
+/* The learner's fused PPO loss kernel on injected logits [B][A] / values [B]:
+ * d_dlog [B][A+1] receives dL/dlogits and dL/dV per sample (batch-mean loss);
+ * h_stats8 = {policy, value, entropy, total, mean_ratio, -, lag mean, lag max}. */
+APPO_API int appo_dbg_ppo_loss(appo_ctx* ctx, int B, int A, const float* d_logits,
+                               const float* d_values, const int32_t* d_actions,
+                               const float* d_blogp, const float* d_adv, const float* d_vt,
+                               float clip_low, float clip_high, float value_coef,
+                               float entropy_coef, float* d_dlog, double* h_stats8);
+
 /* Synchronous device->host copy on the ctx stream (test plumbing). */
 APPO_API int appo_dbg_copy_d2h(appo_ctx* ctx, void* h_dst, const void* d_src, uint64_t bytes);
 

@@ -297,6 +297,24 @@ class Reference:
         L.ref_derive_seed.restype = C.c_uint64
         L.ref_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
 
+    def ppo_grads_injected(self, logits, values, actions, blogp, adv, vt, lo=1 / 1.1, hi=1.1,
+                           vc=0.5, ec=0.003):
+        """compute_gradients with injected logits/values (ref_shim.cpp): per-sample
+        dlogits [n][A] and dL/dV [n] of the batch-mean loss, loss4, mean ratio."""
+        lg = _c(logits, np.float64)
+        n, A = lg.shape
+        dl = np.zeros((n, A)); dv = np.zeros(n); loss = np.zeros(4); mr = C.c_double()
+        L = self.L
+        L.ref_ppo_grads_injected.restype = C.c_int
+        L.ref_ppo_grads_injected.argtypes = [C.c_int, C.c_int, _dp, _dp, _i32p, _dp, _dp, _dp,
+                                             C.c_double, C.c_double, C.c_double, C.c_double,
+                                             _dp, _dp, _dp, C.POINTER(C.c_double)]
+        st = L.ref_ppo_grads_injected(n, A, lg, _c(values, np.float64), _c(actions, np.int32),
+                                      _c(blogp, np.float64), _c(adv, np.float64),
+                                      _c(vt, np.float64), lo, hi, vc, ec, dl, dv, loss,
+                                      C.byref(mr))
+        return st, dict(dlogits=dl, dv=dv, loss=loss, mean_ratio=mr.value)
+
     @staticmethod
     def available(path: str = REF_LIB) -> bool:
         return os.path.exists(path)

@@ -232,6 +232,58 @@ std::uint64_t ref_spec_hash_mlp(int obs_dim, int hidden_dim, int trunk_hidden, c
   return s.spec_hash();
 }
 
+// compute_gradients (policy.hpp:302-428) with injected logits and values: for
+// each sample an MLP whose head / value weights are zero and whose biases ARE
+// the sample's logits and value (obs_dim 1, trunk 1), run on a batch of one,
+// so the head-bias gradient is exactly the reference's dlogits row and the
+// value-bias gradient its dL/dV (policy.hpp:349-372,357).  Rows are scaled by
+// 1/n (the batch mean, policy.hpp:318); loss4 = {policy, value, entropy,
+// total} and *mean_ratio are the batch means of the per-sample results.
+int ref_ppo_grads_injected(int n, int A, const double* logits, const double* values,
+                           const int* actions, const double* blogp, const double* adv,
+                           const double* vt, double lo, double hi, double value_coef,
+                           double entropy_coef, double* dlogits, double* dv, double* loss4,
+                           double* mean_ratio) {
+  return guarded([&] {
+    ModelShape s;
+    s.obs_dim = 1;
+    s.trunk_hidden = 1;
+    s.heads.sizes = {A};
+    ParamLayout L(s);
+    PolicyParams p;
+    p.shape = s;
+    LossConfig cfg;
+    cfg.clip = ClipConfig{lo, hi};
+    cfg.value_coef = value_coef;
+    cfg.entropy_coef = entropy_coef;
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < n; ++i) {
+      p.theta.assign(L.total, 0.0);
+      for (int k = 0; k < A; ++k) p.theta[L.bh + k] = logits[(size_t)i * A + k];
+      p.theta[L.bv] = values[i];
+      SampleBatch b;
+      b.batch = 1;
+      b.obs = {0.0};
+      b.actions = {actions[i]};
+      b.behavior_logp = {blogp[i]};
+      b.advantages = {adv[i]};
+      b.v_targets = {vt[i]};
+      GradientResult g = compute_gradients(p, b, cfg);
+      for (int k = 0; k < A; ++k) dlogits[(size_t)i * A + k] = g.grad[L.bh + k] / n;
+      dv[i] = g.grad[L.bv] / n;
+      acc[0] += g.loss.policy;
+      acc[1] += g.loss.value;
+      acc[2] += g.loss.entropy;
+      acc[4] += g.mean_ratio;
+    }
+    loss4[0] = acc[0] / n;
+    loss4[1] = acc[1] / n;
+    loss4[2] = acc[2] / n;
+    loss4[3] = loss4[0] + loss4[1] - entropy_coef * loss4[2];
+    *mean_ratio = acc[4] / n;
+  });
+}
+
 // pbt_step (population.hpp:131-186) over `periods` periods of the synthetic
 // score schedule of acceptance.cpp's PBT criterion (P agents, reward weights
 // {1.0, 0.2, -0.5}, every third period compressed below the threshold);

@@ -184,6 +184,8 @@ _sig("appo_dbg_gemm", _i, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i
      _vp, _i64, _i, _i)
 _sig("appo_dbg_model_ptrs", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp))
 _sig("appo_dbg_copy_d2h", _i, _vp, _vp, _vp, _u64)
+_sig("appo_dbg_ppo_loss", _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _f, _vp,
+     _vp)
 _sig("appo_learner_submit", _i, _vp, _vp, _u64, _vp, _i, C.POINTER(HParams))
 _sig("appo_learner_collect", _i, _vp, C.POINTER(StepOut))
 _sig("appo_dp_unique_id", _i, C.c_char_p)
@@ -506,6 +508,21 @@ class Context:
         check(_L.appo_dbg_copy_d2h(self.h, out.ctypes.data_as(C.c_void_p), C.c_void_p(g),
                                    out.nbytes))
         return out
+
+    def ppo_loss_injected(self, logits, values, actions, blogp, adv, vt, clip_low=1 / 1.1,
+                          clip_high=1.1, value_coef=0.5, entropy_coef=0.003):
+        """The learner's fused loss kernel on injected inputs (include/appo_internal.h):
+        returns dlog [B][A+1] (dL/dlogits, dL/dV) and the 8 loss statistics."""
+        _need_cuda(logits, values, actions, blogp, adv, vt)
+        B, A = logits.shape
+        import torch
+        dlog = torch.empty(B, A + 1, dtype=torch.float32, device=logits.device)
+        stats = np.zeros(8)
+        check(_L.appo_dbg_ppo_loss(self.h, B, A, _ptr(logits), _ptr(values), _ptr(actions),
+                                   _ptr(blogp), _ptr(adv), _ptr(vt), clip_low, clip_high,
+                                   value_coef, entropy_coef, _ptr(dlog),
+                                   stats.ctypes.data_as(C.c_void_p)))
+        return dlog, stats
 
     def gemm(self, M, N, K, a, lda, a_mn, b, ldb, b_mn, out, ldo, flags=0, scale=1.0, bias=None,
              aux=None, ld_aux=0, bn=128, splits=1):

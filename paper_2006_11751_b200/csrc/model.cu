@@ -997,3 +997,35 @@ extern "C" int appo_dbg_copy_d2h(appo_ctx* ctx, void* h_dst, const void* d_src, 
   APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return APPO_OK;
 }
+
+// The learner's fused loss kernel (ppo_loss_kernel) on caller-supplied logits /
+// values: parity of the loss and its logit / value gradient against the
+// reference's compute_gradients (policy.hpp:323-375) with injected inputs.
+extern "C" int appo_dbg_ppo_loss(appo_ctx* ctx, int B, int A, const float* d_logits,
+                                 const float* d_values, const int32_t* d_actions,
+                                 const float* d_blogp, const float* d_adv, const float* d_vt,
+                                 float clip_low, float clip_high, float value_coef,
+                                 float entropy_coef, float* d_dlog, double* h_stats8) {
+  APPO_REQUIRE(ctx != nullptr && B >= 1 && A >= 1 && A < kMaxActions, APPO_ERR_CONTRACT,
+               "dbg_ppo_loss: bad arguments");
+  APPO_CUDA_TRY(cudaSetDevice(ctx->device));
+  uint16_t* dhead = nullptr;
+  double* stats = nullptr;
+  int64_t* ver = nullptr;
+  APPO_CUDA_TRY(cudaMalloc(&dhead, (size_t)B * 16 * 2));
+  APPO_CUDA_TRY(cudaMalloc(&stats, sizeof(double) * 16));
+  APPO_CUDA_TRY(cudaMalloc(&ver, sizeof(int64_t) * B));
+  APPO_CUDA_TRY(cudaMemsetAsync(ver, 0, sizeof(int64_t) * B, ctx->stream));
+  LossHP lh{clip_low, clip_high, value_coef, entropy_coef};
+  int st = k_ppo_loss(ctx, B, A, d_logits, d_values, d_actions, d_blogp, d_adv, d_vt, lh, d_dlog,
+                      dhead, stats, ver, 0);
+  if (st == APPO_OK) {
+    APPO_CUDA_TRY(cudaMemcpyAsync(h_stats8, stats, sizeof(double) * 8, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(dhead);
+  cudaFree(stats);
+  cudaFree(ver);
+  return st;
+}

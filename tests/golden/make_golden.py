@@ -145,6 +145,29 @@ def main():
     offs = np.array([ref.slot_offsets(*s) for s in shapes], dtype=np.uint64)
     np.savez(os.path.join(HERE, "layout.npz"), shapes=np.array(shapes, dtype=np.uint32),
              offsets=offs)
+    # 8. PPO loss + its logit / value gradient from the reference's own
+    #    compute_gradients with injected logits and values (policy.hpp:302-428,
+    #    ref_shim.cpp ref_ppo_grads_injected): fp32-representable inputs, 6
+    #    actions, a few samples beyond the +-20 log-ratio clamp
+    #    (offpolicy.hpp:48-54) and several right at the clip bounds.
+    rs = np.random.default_rng(77)
+    n, A = 1024, 6
+    lg = rs.normal(scale=1.5, size=(n, A)).astype(np.float32).astype(np.float64)
+    vals = rs.normal(size=n).astype(np.float32).astype(np.float64)
+    acts = rs.integers(0, A, n).astype(np.int32)
+    shift = rs.uniform(-0.3, 0.3, n)
+    shift[:8] = [25.0, -25.0, 21.0, -21.0, 19.5, -19.5, 30.0, -30.0]  # clamp
+    lp = np.zeros(n)
+    for i in range(n):
+        _, lp[i], _ = ref.logp_entropy(lg[i], acts[i])
+    blogp = (lp - shift).astype(np.float32).astype(np.float64)
+    advs = rs.normal(size=n).astype(np.float32).astype(np.float64)
+    vt = rs.normal(size=n).astype(np.float32).astype(np.float64)
+    st, g = ref.ppo_grads_injected(lg, vals, acts, blogp, advs, vt)
+    assert st == 0
+    np.savez(os.path.join(HERE, "ppo_grad.npz"), logits=lg, values=vals, actions=acts,
+             blogp=blogp, adv=advs, vt=vt, dlogits=g["dlogits"], dv=g["dv"], loss=g["loss"],
+             mean_ratio=g["mean_ratio"])
     print("golden vectors written to", HERE)
 
 

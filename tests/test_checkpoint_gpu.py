@@ -12,7 +12,7 @@ from test_model_gpu import fill_store  # noqa: E402
 
 
 def test_checkpoint_roundtrip_and_resume(tmp_path):
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     a = appo.Context(0, seed=21, model=desc)
     store = appo.TrajectoryStore(desc, 4)
     fill_store(store, 4, np.random.default_rng(4), 6)
@@ -45,7 +45,7 @@ def test_checkpoint_roundtrip_and_resume(tmp_path):
 
 
 def test_checkpoint_shape_mismatch_is_config_error(tmp_path):
-    a = appo.Context(0, seed=1, model=appo.ModelDesc(3, 72, 128, 6, 8))
+    a = appo.Context(0, seed=1, model=appo.ModelDesc(3, 72, 128, 6, 32))
     path = str(tmp_path / "a.ckpt")
     a.save_checkpoint(path)
     b = appo.Context(0, seed=1, model=appo.ModelDesc(3, 72, 128, 5, 8))

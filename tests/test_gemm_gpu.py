@@ -105,3 +105,25 @@ def test_strided_rows(ctx):
     torch.cuda.synchronize()
     r = a.float() @ W.float()
     assert (out - r).abs().max().item() <= 1e-3 * r.abs().max().item()
+
+
+@pytest.mark.parametrize("bn,flags", [(64, 0), (128, appo.EPI_BIAS | appo.EPI_ELU | appo.EPI_BF16),
+                                      (256, appo.EPI_BIAS)])
+def test_many_tiles_per_cta(ctx, bn, flags):
+    # production-size M (the inference FC / gate GEMMs run M = 16,384; conv GEMMs
+    # millions of rows): every persistent CTA cycles its smem ring's mbarrier
+    # phases and the double-buffered TMEM accumulator over dozens of tiles
+    M, N, K = 148 * 128 * 6 + 77, bn * 2, 512
+    A, B, a, lda, b, ldb = operands(M, N, K, False, False, 11)
+    bias = torch.randn(N, device="cuda")
+    dt = torch.bfloat16 if flags & appo.EPI_BF16 else torch.float32
+    out = torch.zeros(M, N, device="cuda", dtype=dt)
+    ctx.gemm(M, N, K, a, lda, False, b, ldb, False, out, N, flags=flags, bias=bias, bn=bn)
+    torch.cuda.synchronize()
+    r = ref(A, B)
+    if flags & appo.EPI_BIAS:
+        r = r + bias
+    if flags & appo.EPI_ELU:
+        r = torch.nn.functional.elu(r)
+    tol = (1e-2 if dt == torch.bfloat16 else 1e-3) * r.abs().max().item()
+    assert (out.float() - r).abs().max().item() <= tol

@@ -2,13 +2,17 @@
 (oracle/appo_oracle.c; itself pinned against torch fp64 autograd and the
 reference), through the C ABI.
 
-Stated tolerances (bf16 operands, fp32 accumulation):
-  * inference: max |log pi_gpu - log pi_ref| <= 2^-6 (logits, via log-softmax),
-    |value| error <= 2e-3 + 2e-2 |ref|, h' error <= 2e-2;
+Stated tolerances (bf16 operands, fp32 accumulation), set at
+about 3-10x the errors observed at the production shapes
+(tests/test_parity_prod_gpu.py, profiles/r02_parity_errors.jsonl):
+  * inference: max |log pi_gpu - log pi_ref| <= 5e-4 (observed 4.4e-5; the
+    north_star's stated bf16 tolerance), |value| error <= 2e-4 + 2e-3 |ref|
+    (observed 4e-5), h' error <= 1.5e-2 (observed 6.4e-3);
     actions equal to the oracle's inverse-CDF draw with the same uniform
     except where u falls within 1e-3 of a CDF boundary.
-  * learner: loss components within 2e-2 relative (abs floor 1e-4);
-    per-tensor gradient relative L2 error <= 6e-2; global norm within 3e-2.
+  * learner: loss components within 1e-3 relative (abs floor 1e-5; observed
+    <= 1e-4); per-tensor gradient relative L2 error <= 1.5e-2 (observed
+    <= 4.8e-3); global norm within 2e-3 (observed <= 6.3e-4).
 """
 import numpy as np
 import pytest
@@ -17,6 +21,13 @@ import torch
 pytestmark = pytest.mark.gpu
 
 import paper_2006_11751_b200 as appo  # noqa: E402
+
+
+LOGPI_TOL = 5e-4   # max |d log pi| (bf16 operands)
+H_TOL = 1.5e-2     # max |d h'|
+LOSS_RTOL, LOSS_ATOL = 1e-3, 1e-5
+GRAD_TOL = 1.5e-2  # per-tensor relative L2
+GNORM_TOL = 2e-3
 
 
 def log_softmax(x):
@@ -54,10 +65,10 @@ def test_policy_forward_matches_oracle(doom, oracle):
     ref = oracle.policy_forward((3, 72, 128, 6), th.astype(np.float64), obs,
                                 h.astype(np.float64))
     lg = out["logits"].cpu().numpy().astype(np.float64)
-    assert np.abs(log_softmax(lg) - log_softmax(ref["logits"])).max() <= 2 ** -6
+    assert np.abs(log_softmax(lg) - log_softmax(ref["logits"])).max() <= LOGPI_TOL
     vals = out["values"].cpu().numpy()
-    assert np.all(np.abs(vals - ref["values"]) <= 2e-3 + 2e-2 * np.abs(ref["values"]))
-    assert np.abs(out["h_out"].cpu().numpy() - ref["h_out"]).max() <= 2e-2
+    assert np.all(np.abs(vals - ref["values"]) <= 2e-4 + 2e-3 * np.abs(ref["values"]))
+    assert np.abs(out["h_out"].cpu().numpy() - ref["h_out"]).max() <= H_TOL
     # sampling: same counter-based uniform -> same action unless u is at a boundary
     key = oracle.L.orc_derive_seed(5, 0x9900)
     acts = out["actions"].cpu().numpy()
@@ -105,9 +116,12 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
-@pytest.mark.parametrize("adv_source,normalize", [(0, 0), (2, 1), (1, 0)])
-def test_learner_step_matches_oracle(oracle, adv_source, normalize):
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+# T = 8 keeps one case on the conv1 weight-gradient fallback (bootstrap images
+# not 16-byte aligned -> im2col + GEMM instead of TMA staging from the slots)
+@pytest.mark.parametrize("adv_source,normalize,T", [(0, 0, 32), (2, 1, 32), (1, 0, 32),
+                                                     (0, 0, 8)])
+def test_learner_step_matches_oracle(oracle, adv_source, normalize, T):
+    desc = appo.ModelDesc(3, 72, 128, 6, T)
     ctx = appo.Context(0, seed=11, model=desc)
     store = appo.TrajectoryStore(desc, 4)
     rs = np.random.default_rng(adv_source)
@@ -131,16 +145,16 @@ def test_learner_step_matches_oracle(oracle, adv_source, normalize):
     for got, exp in ((out["policy_loss"], st[0]), (out["value_loss"], st[1]),
                      (out["entropy"], st[2]), (out["total_loss"], st[3]),
                      (out["mean_ratio"], st[4])):
-        assert abs(got - exp) <= 2e-2 * abs(exp) + 1e-4, (got, exp)
+        assert abs(got - exp) <= LOSS_RTOL * abs(exp) + LOSS_ATOL, (got, exp)
     gr = ref["grad"]
-    assert abs(out["grad_norm"] - np.linalg.norm(gr)) <= 3e-2 * np.linalg.norm(gr)
+    assert abs(out["grad_norm"] - np.linalg.norm(gr)) <= GNORM_TOL * np.linalg.norm(gr)
     from oracle.oracle import Oracle  # noqa: F401  (offsets from the same contract)
     offs = block_offsets(ctx)
     for name, (a, b) in offs.items():
         e = rel_l2(g[a:b].astype(np.float64), gr[a:b])
-        assert e <= 6e-2, (name, e)
+        assert e <= GRAD_TOL, (name, e)
     # lag statistics (orchestrator.hpp:790,862-863): version 0 - versions[t]
-    assert out["lag_max"] == 0.0 and abs(out["lag_mean"] + 1.5) < 1e-9
+    assert out["lag_max"] == 0.0 and abs(out["lag_mean"] + np.mean(np.arange(T) // 2)) < 1e-9
 
 
 def test_learner_step_matches_oracle_T32_slot_order(oracle):
@@ -166,11 +180,11 @@ def test_learner_step_matches_oracle_T32_slot_order(oracle):
                               sel["dones"].reshape(-1), hp=dict(gamma=0.99), do_adam=False)
     assert ref["status"] == 0
     st = ref["stats"]
-    assert abs(out["total_loss"] - st[3]) <= 2e-2 * abs(st[3]) + 1e-4
+    assert abs(out["total_loss"] - st[3]) <= LOSS_RTOL * abs(st[3]) + LOSS_ATOL
     gr = ref["grad"]
     for name, (a, b) in block_offsets(ctx).items():
         e = rel_l2(g[a:b].astype(np.float64), gr[a:b])
-        assert e <= 6e-2, (name, e)
+        assert e <= GRAD_TOL, (name, e)
 
 
 def block_offsets(ctx):
@@ -190,7 +204,7 @@ def block_offsets(ctx):
 
 
 def test_learner_errors():
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     ctx = appo.Context(0, seed=3, model=desc)
     store = appo.TrajectoryStore(desc, 2)
     rs = np.random.default_rng(5)
@@ -214,7 +228,7 @@ def test_learner_errors():
 
 def test_learning_reduces_loss_on_fixed_batch():
     # acceptance.cpp:508-569 analogue: repeated steps on one batch lower the loss
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     ctx = appo.Context(0, seed=7, model=desc)
     store = appo.TrajectoryStore(desc, 4)
     fill_store(store, 4, np.random.default_rng(9), 6)
@@ -228,7 +242,7 @@ def test_async_submit_collect_determinism_and_rejected_steps():
     # bitwise determinism (acceptance.cpp:673-708 analogue) + the async form:
     # a rejected step (NumericError) leaves params/version untouched and the
     # sticky flag rejects every later step until collect
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     store = appo.TrajectoryStore(desc, 4)
     fill_store(store, 4, np.random.default_rng(2), 6)
     ref = appo.Context(0, seed=13, model=desc)
@@ -263,7 +277,7 @@ def test_async_submit_collect_determinism_and_rejected_steps():
 def test_programmatic_dependent_launch_is_bitwise_neutral(pdl):
     # every kernel waits on griddepcontrol before touching its predecessor's
     # outputs: learner steps and inference give identical bits with PDL on/off
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     store = appo.TrajectoryStore(desc, 4)
     fill_store(store, 4, np.random.default_rng(12), 6)
     hp = appo.HParams.defaults(lr=3e-4)

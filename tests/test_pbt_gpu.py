@@ -12,7 +12,7 @@ import paper_2006_11751_b200 as appo  # noqa: E402
 
 from test_model_gpu import fill_store  # noqa: E402
 
-DESC = appo.ModelDesc(3, 72, 128, 6, 8)
+DESC = appo.ModelDesc(3, 72, 128, 6, 32)
 
 
 @pytest.fixture(scope="module")

@@ -11,7 +11,7 @@ import paper_2006_11751_b200 as appo  # noqa: E402
 
 @pytest.fixture(scope="module")
 def setup():
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     ctx = appo.Context(0, seed=2, model=desc)
     n = 40
     store = appo.TrajectoryStore(desc, 2 * n)
@@ -106,7 +106,7 @@ def test_overlapped_sampler_and_learner_streams():
     # only ever see complete published versions: stamped versions are
     # non-decreasing within a trajectory (trajstore.hpp:174-176) and never ahead
     # of the learner.
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     learner = appo.Context(0, seed=4, model=desc)
     actor = learner.shared()
     n = 128
@@ -134,7 +134,7 @@ def test_overlapped_sampler_and_learner_streams():
 def test_host_observations_staged_into_slots():
     # CPU-actor path: pinned host obs per step, copied on the sampler's copy
     # stream through two staging buffers and scattered into the slots
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     ctx = appo.Context(0, seed=4, model=desc)
     n = 24
     store = appo.TrajectoryStore(desc, 2 * n)

@@ -89,7 +89,7 @@ def test_foreign_id_is_contract_error():
 
 
 def test_queued_learner_step_matches_host_ids():
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     store = appo.TrajectoryStore(desc, 6)
     fill_store(store, 6, np.random.default_rng(5), 6)
     hp = appo.HParams.defaults(lr=3e-4)
@@ -113,7 +113,7 @@ def test_queued_learner_step_matches_host_ids():
 
 
 def test_queued_learner_step_timeout_is_rejected():
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     store = appo.TrajectoryStore(desc, 4)
     fill_store(store, 4, np.random.default_rng(6), 6)
     ctx = appo.Context(0, seed=3, model=desc)
@@ -138,7 +138,7 @@ def test_queued_learner_step_timeout_is_rejected():
 
 
 def test_sampler_feeds_ready_queue():
-    desc = appo.ModelDesc(3, 72, 128, 6, 8)
+    desc = appo.ModelDesc(3, 72, 128, 6, 32)
     lctx = appo.Context(0, seed=5, model=desc, stream=torch.cuda.Stream(0))
     sctx = lctx.shared(torch.cuda.Stream(0))
     n = 16
