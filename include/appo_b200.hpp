@@ -59,7 +59,7 @@ struct VTraceConfig {
 struct VTraceOutput {  // offpolicy.hpp:30-35
   std::vector<double> v, pg_adv, rho, c;
 };
-struct LossComponents {  // offpolicy.hpp:214-219
+struct LossComponents {  // offpolicy.hpp:136-141
   double policy = 0, value = 0, entropy = 0, total = 0;
 };
 
@@ -96,7 +96,7 @@ class Context {
   appo_ctx* get() const { return h_; }
   void sync() const { check(appo_ctx_sync(h_)); }
 
-  // vtrace (offpolicy.hpp:139): one trajectory, host spans, fp64 in/out like
+  // vtrace (offpolicy.hpp:61): one trajectory, host spans, fp64 in/out like
   // the reference (computed in fp32 on the device; |err| <= 1e-5 max(|ref|,1)).
   VTraceOutput vtrace(std::span<const double> rewards, std::span<const double> values,
                       double bootstrap_value, std::span<const double> target_logp,
@@ -138,7 +138,7 @@ class Context {
                       static_cast<float>(cfg.c_bar), d_v, d_pg, nullptr, nullptr));
   }
 
-  // total_loss (offpolicy.hpp:224), device arrays of length n
+  // total_loss (offpolicy.hpp:146), device arrays of length n
   LossComponents total_loss(int n, const float* d_ratios, const float* d_adv,
                             const float* d_values, const float* d_vt, const float* d_ent,
                             double clip_low = 1.0 / 1.1, double clip_high = 1.1,

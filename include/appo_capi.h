@@ -64,7 +64,7 @@ typedef struct {
 } appo_model_desc;
 
 /* Learner hyper-parameters: AdamConfig (policy.hpp:88-94), LossConfig
- * (offpolicy.hpp:208-212), VTraceConfig (offpolicy.hpp:96-106), advantage
+ * (offpolicy.hpp:130-134), VTraceConfig (offpolicy.hpp:18-28), advantage
  * source / normalisation (orchestrator.hpp:47,838-845). */
 typedef struct {
   float lr, beta1, beta2, eps, grad_clip;
@@ -119,14 +119,14 @@ APPO_API int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_fil
 APPO_API int appo_ctx_timing_report(appo_ctx* ctx, char* buf, int buflen);
 
 /* ---- off-policy returns (offpolicy.hpp) --------------------------------- */
-/* Replaces vtrace (offpolicy.hpp:139-178) for n_traj trajectories at once.
+/* Replaces vtrace (offpolicy.hpp:61-100) for n_traj trajectories at once.
  * d_rho_out / d_c_out may be NULL.  Validation as VTraceConfig::validate. */
 APPO_API int appo_vtrace(appo_ctx* ctx, int n_traj, int T, const float* d_rewards, const float* d_values,
                 const float* d_bootstrap, const float* d_target_logp,
                 const float* d_behavior_logp, const uint8_t* d_dones, float gamma, float rho_bar,
                 float c_bar, float* d_v_out, float* d_pg_adv_out, float* d_rho_out,
                 float* d_c_out);
-/* Replaces nstep_returns (offpolicy.hpp:182-192). */
+/* Replaces nstep_returns (offpolicy.hpp:104-114). */
 APPO_API int appo_nstep_returns(appo_ctx* ctx, int n_traj, int T, const float* d_rewards,
                        const float* d_bootstrap, const uint8_t* d_dones, float gamma,
                        float* d_ret_out);
@@ -134,7 +134,7 @@ APPO_API int appo_nstep_returns(appo_ctx* ctx, int n_traj, int T, const float* d
 APPO_API int appo_gae(appo_ctx* ctx, int n_traj, int T, const float* d_rewards, const float* d_values,
              const float* d_bootstrap, const uint8_t* d_dones, float gamma, float lambda,
              float* d_adv_out, float* d_ret_out);
-/* Replaces total_loss (offpolicy.hpp:224-246); h_out4 = {policy, value, entropy,
+/* Replaces total_loss (offpolicy.hpp:146-168); h_out4 = {policy, value, entropy,
  * total} in fp64, written after an internal sync (this call is synchronous). */
 APPO_API int appo_total_loss(appo_ctx* ctx, int n, const float* d_ratios, const float* d_adv,
                     const float* d_values, const float* d_v_targets, const float* d_entropies,
@@ -230,9 +230,18 @@ APPO_API int appo_learner_collect(appo_ctx* ctx, appo_step_out* out);
  * (e.g. torch.distributed), every rank calls appo_dp_init on its ctx.  From
  * then on appo_learner_step averages the flat gradient with ncclAllReduce
  * before the global-norm clip and Adam (no reference counterpart: the
- * reference runs one learner thread per policy, orchestrator.hpp:938-946). */
+ * reference runs one learner thread per policy, orchestrator.hpp:938-946):
+ * three buckets in reverse layer order on a side stream, each launched as
+ * soon as the backward pass finished it (overlapping the rest of the
+ * backward), the last one grouped with a max-reduction of the ranks' step
+ * rejection flags so a step any rank rejects is rejected on every rank.
+ * nranks = 1 is allowed (the same path over a one-rank communicator). */
 APPO_API int appo_dp_unique_id(char* out128);
 APPO_API int appo_dp_init(appo_ctx* ctx, int nranks, int rank, const char* id128);
+/* The gradient buckets in reduction order as (offset, count) pairs over the
+ * flat parameter vector (host-only; *n_out = 3). */
+APPO_API int appo_dp_bucket_plan(const appo_model_desc* desc, int64_t* out_pairs, int cap,
+                                 int* n_out);
 
 /* ---- device sampler: synthetic envs + rollout-side writer ---------------- */
 /* Restates SyntheticLatencyEnv (envs.hpp:103-158) on the device with u8 pixels
@@ -353,8 +362,23 @@ APPO_API int appo_pbt_format_events(const appo_pbt_event* events, int n, int hea
  * across GPUs) and publishes them as its next version (PbtController's
  * copy_weights, runner.hpp:211-219); dst must have no uncollected steps */
 APPO_API int appo_params_copy(appo_ctx* dst, appo_ctx* src);
-/* copy_weights over user = appo_ctx*[P] (learner of policy i at index i) */
+/* copy_weights over user = appo_ctx*[P] (learner of policy i at index i);
+ * dst == src is a no-op (the reference's self-copy) */
 APPO_API int appo_pbt_copy_contexts(void* user, uint32_t dst, uint32_t src);
+
+/* copy_weights between PROCESSES (one learner per process / GPU, configs[4]):
+ * the source exports its state -- CUDA IPC handles of theta, m, v plus Adam t
+ * and version, APPO_STATE_HANDLE_BYTES of plain bytes the host ships to the
+ * destination (e.g. torch.distributed) -- and the destination imports it:
+ * a device-to-device copy (NVLink peer copy across GPUs, the copy engines of
+ * one GPU otherwise) published as its next version, as appo_params_copy.
+ * Export waits for the source's queued work; the source must not run another
+ * learner step until the import returned (runner.hpp:217-218 holds both
+ * learners' pbt_lock for the copy).  Import from this same process is a
+ * contract error (use appo_params_copy). */
+#define APPO_STATE_HANDLE_BYTES 512
+APPO_API int appo_params_export(appo_ctx* ctx, void* handle_out);
+APPO_API int appo_params_import(appo_ctx* dst, const void* handle);
 
 #ifdef __cplusplus
 }

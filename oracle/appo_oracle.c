@@ -69,7 +69,7 @@ double orc_uniform(uint64_t key, uint64_t counter) {
 
 static int finite(double x) { return isfinite(x); }
 
-/* offpolicy.hpp:128-132 */
+/* offpolicy.hpp:50-54 */
 double orc_importance_ratio(double target_logp, double behavior_logp) {
   double d = target_logp - behavior_logp;
   if (d < -20.0) d = -20.0;
@@ -77,14 +77,14 @@ double orc_importance_ratio(double target_logp, double behavior_logp) {
   return exp(d);
 }
 
-/* offpolicy.hpp:101-105 */
+/* offpolicy.hpp:23-27 */
 int orc_vtrace_validate(double rho_bar, double c_bar, double gamma) {
   if (!(rho_bar >= c_bar && c_bar > 0.0)) return ORC_CONFIG;
   if (!(gamma > 0.0 && gamma <= 1.0)) return ORC_CONFIG;
   return ORC_OK;
 }
 
-/* offpolicy.hpp:139-178: backward recursion over one trajectory. */
+/* offpolicy.hpp:61-100: backward recursion over one trajectory. */
 int orc_vtrace(int T, const double* rewards, const double* values, double bootstrap,
                const double* tlogp, const double* blogp, const uint8_t* dones, double rho_bar,
                double c_bar, double gamma, double* v_out, double* pg_out, double* rho_out,
@@ -128,7 +128,7 @@ int orc_vtrace_batch(int n_traj, int T, const double* rewards, const double* val
   return ORC_OK;
 }
 
-/* offpolicy.hpp:182-192 */
+/* offpolicy.hpp:104-114 */
 void orc_nstep_returns(int T, const double* rewards, double bootstrap, const uint8_t* dones,
                        double gamma, double* ret) {
   double acc = bootstrap;
@@ -158,20 +158,20 @@ void orc_gae(int T, const double* rewards, const double* values, double bootstra
   }
 }
 
-/* offpolicy.hpp:195-198 */
+/* offpolicy.hpp:117-120 */
 double orc_ppo_objective(double ratio, double adv, double lo, double hi) {
   double cl = ratio < lo ? lo : (ratio > hi ? hi : ratio);
   double a = ratio * adv, b = cl * adv;
   return a < b ? a : b;
 }
 
-/* offpolicy.hpp:202-206: unclipped branch wins ties */
+/* offpolicy.hpp:124-128: unclipped branch wins ties */
 double orc_ppo_dratio(double ratio, double adv, double lo, double hi) {
   double cl = ratio < lo ? lo : (ratio > hi ? hi : ratio);
   return (ratio * adv <= cl * adv) ? adv : 0.0;
 }
 
-/* offpolicy.hpp:224-246; out = {policy, value, entropy, total} */
+/* offpolicy.hpp:146-168; out = {policy, value, entropy, total} */
 int orc_total_loss(int n, const double* ratios, const double* adv, const double* values,
                    const double* vt, const double* ent, double lo, double hi, double value_coef,
                    double entropy_coef, double* out4) {
@@ -599,7 +599,7 @@ static void encoder_bwd(const orc_model* m, const double* th, const uint8_t* obs
  *   GRU unrolled from the stored h0 with h_{t+1} = h'_t * (1 - done_t)
  *   (hidden reset after done, orchestrator.hpp:402,545-547);
  *   target logp / entropy (policy.hpp:262-281); vtrace per trajectory
- *   (offpolicy.hpp:139-178); advantage = pg_adv (adv_source 0), nstep - V (1,
+ *   (offpolicy.hpp:61-100); advantage = pg_adv (adv_source 0), nstep - V (1,
  *   orchestrator.hpp:831-833) or GAE(lambda) (2); optional normalisation
  *   (orchestrator.hpp:838-845); exact gradient of the loss with adv and v
  *   targets constant (policy.hpp:299-428), back-propagated through the GRU

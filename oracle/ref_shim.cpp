@@ -41,7 +41,7 @@ int guarded(F&& f) {
 
 extern "C" {
 
-// offpolicy.hpp:139 vtrace
+// offpolicy.hpp:61 vtrace
 int ref_vtrace(int T, const double* r, const double* v, double boot, const double* tl,
                const double* bl, const std::uint8_t* d, double rho_bar, double c_bar, double gamma,
                double* v_out, double* pg_out, double* rho_out, double* c_out) {
@@ -72,14 +72,14 @@ int ref_vtrace_range(int lo, int hi, int T, const double* r, const double* v, co
   });
 }
 
-// offpolicy.hpp:182 nstep_returns
+// offpolicy.hpp:104 nstep_returns
 void ref_nstep_returns(int T, const double* r, double boot, const std::uint8_t* d, double gamma,
                        double* ret) {
   auto o = nstep_returns({r, (size_t)T}, boot, {d, (size_t)T}, gamma);
   std::memcpy(ret, o.data(), sizeof(double) * T);
 }
 
-// offpolicy.hpp:195 / :202
+// offpolicy.hpp:117 / :124
 double ref_ppo_objective(double ratio, double adv, double lo, double hi) {
   ClipConfig c{lo, hi};
   return ppo_clip_objective(ratio, adv, c);
@@ -90,7 +90,7 @@ double ref_ppo_dratio(double ratio, double adv, double lo, double hi) {
 }
 double ref_importance_ratio(double t, double b) { return importance_ratio(t, b); }
 
-// offpolicy.hpp:224 total_loss ; out = policy, value, entropy, total
+// offpolicy.hpp:146 total_loss ; out = policy, value, entropy, total
 int ref_total_loss(int n, const double* ratios, const double* adv, const double* values,
                    const double* vt, const double* ent, double lo, double hi, double value_coef,
                    double entropy_coef, double* out4) {

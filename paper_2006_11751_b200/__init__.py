@@ -3,7 +3,7 @@
 Python host mirror of the reference's hot-path interface over the C ABI in
 include/appo_capi.h (libappo_b200.so, hand-written sm_100a CUDA).  Function
 names, argument meaning and error behaviour follow the reference
-(/root/reference/proj/include/appo): ``vtrace`` (offpolicy.hpp:139),
+(/root/reference/proj/include/appo): ``vtrace`` (offpolicy.hpp:61),
 ``nstep_returns`` (:182), ``total_loss`` (:224), ``log_prob_and_entropy``
 (policy.hpp:262), ``optimizer_step`` (policy.hpp:431), the policy-worker batch
 inference (orchestrator.hpp:602-673) and the learner step
@@ -190,6 +190,7 @@ _sig("appo_learner_submit", _i, _vp, _vp, _u64, _vp, _i, C.POINTER(HParams))
 _sig("appo_learner_collect", _i, _vp, C.POINTER(StepOut))
 _sig("appo_dp_unique_id", _i, C.c_char_p)
 _sig("appo_dp_init", _i, _vp, _i, _i, C.c_char_p)
+_sig("appo_dp_bucket_plan", _i, C.POINTER(ModelDesc), _vp, _i, C.POINTER(_i))
 _sig("appo_sampler_create", _i, _vp, _i, _i, _u64, C.POINTER(_vp))
 _sig("appo_sampler_destroy", _i, _vp)
 _sig("appo_sampler_step", _i, _vp, _vp, _u64, C.c_int32, _i, _vp, _vp)
@@ -201,6 +202,8 @@ _sig("appo_slotq_push_range", _i, _vp, _vp, C.c_int32, _i)
 _sig("appo_slotq_pop", _i, _vp, _vp, _vp, _i)
 _sig("appo_slotq_stats", _i, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64))
 _sig("appo_params_copy", _i, _vp, _vp)
+_sig("appo_params_export", _i, _vp, _vp)
+_sig("appo_params_import", _i, _vp, _vp)
 _sig("appo_pbt_create", _i, C.c_void_p, _i, _u64, _vp, C.POINTER(_vp))
 _sig("appo_pbt_destroy", _i, _vp)
 _sig("appo_pbt_controller_seed", _u64, _u64)
@@ -320,7 +323,7 @@ class Context:
     # ---- off-policy -----------------------------------------------------
     def vtrace(self, rewards, values, bootstrap, target_logp, behavior_logp, dones, gamma=0.99,
                rho_bar=1.0, c_bar=1.0, with_weights=False, sync=True):
-        """vtrace (offpolicy.hpp:139-178) over [n_traj, T] tensors."""
+        """vtrace (offpolicy.hpp:61-100) over [n_traj, T] tensors."""
         torch = self.torch
         _need_cuda(rewards, values, bootstrap, target_logp, behavior_logp, dones)
         n, T = rewards.shape
@@ -358,7 +361,7 @@ class Context:
 
     def total_loss(self, ratios, adv, values, v_targets, entropies, clip_low=1 / 1.1,
                    clip_high=1.1, value_coef=0.5, entropy_coef=0.003):
-        """total_loss (offpolicy.hpp:224-246) -> dict(policy, value, entropy, total)."""
+        """total_loss (offpolicy.hpp:146-168) -> dict(policy, value, entropy, total)."""
         _need_cuda(ratios, adv, values, v_targets, entropies)
         out = (C.c_double * 4)()
         check(_L.appo_total_loss(self.h, ratios.numel(), _ptr(ratios), _ptr(adv), _ptr(values),
@@ -509,6 +512,17 @@ class Context:
                                    out.nbytes))
         return out
 
+    def export_params(self) -> bytes:
+        """appo_params_export: this learner's state as a handle for another process."""
+        buf = C.create_string_buffer(STATE_HANDLE_BYTES)
+        check(_L.appo_params_export(self.h, buf))
+        return buf.raw
+
+    def import_params(self, handle: bytes):
+        """appo_params_import: take another process's exported learner state."""
+        check(_L.appo_params_import(self.h, C.create_string_buffer(bytes(handle),
+                                                                   STATE_HANDLE_BYTES)))
+
     def ppo_loss_injected(self, logits, values, actions, blogp, adv, vt, clip_low=1 / 1.1,
                           clip_high=1.1, value_coef=0.5, entropy_coef=0.003):
         """The learner's fused loss kernel on injected inputs (include/appo_internal.h):
@@ -543,8 +557,35 @@ def dp_init(ctx: Context, dist, rank: int, world: int):
     NCCL id is broadcast over ``dist`` (torch.distributed), then every
     learner step all-reduces (averages) the gradient before clip + Adam."""
     obj = [dp_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
     check(_L.appo_dp_init(ctx.h, world, rank, C.create_string_buffer(obj[0], 128)))
+
+
+STATE_HANDLE_BYTES = 512
+
+
+def pbt_exchange(ctx: "Context", dist, rank: int, dst: int, src: int):
+    """copy_weights(dst, src) across processes (one policy learner per rank):
+    called on EVERY rank with the same pair (each rank runs an identical PBT
+    controller on all-gathered scores).  The source exports, the destination
+    imports, and the barrier keeps the source from training until the copy
+    is done (the pbt_lock pair of runner.hpp:217-218)."""
+    if dst == src:
+        return
+    obj = [ctx.export_params() if rank == src else None]
+    dist.broadcast_object_list(obj, src=src)
+    if rank == dst:
+        ctx.import_params(obj[0])
+    dist.barrier()
+
+
+def dp_bucket_plan(desc: ModelDesc) -> list:
+    """The data-parallel gradient buckets in reduction order: [(offset, count)]."""
+    buf = (C.c_int64 * 16)()
+    n = C.c_int()
+    check(_L.appo_dp_bucket_plan(C.byref(desc), C.cast(buf, C.c_void_p), 8, C.byref(n)))
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)]
 
 
 class Sampler:

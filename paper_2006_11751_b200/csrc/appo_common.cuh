@@ -15,7 +15,8 @@ namespace appo_b200 {
 
 void set_error(const std::string& msg);
 
-struct Model;  // model.cu
+struct Model;   // model.cu
+struct Reader;  // model.cuh: per-context inference scratch + read events
 
 // Optional per-launch CUDA-event timing (appo_ctx_set_timing): the bench uses
 // it to measure the dominant kernel's average duration live, on the stream
@@ -50,13 +51,20 @@ struct Ctx {
   size_t ev_used = 0;
   const char* next_name = nullptr;  // overrides the kernel symbol name
   double next_flops = 0.0, next_bytes = 0.0;
-  // data-parallel learner (dp.cu)
+  // data-parallel learner (dp.cu): communicator, side stream for the bucketed
+  // gradient all-reduce, its events, and the rank-consensus rejection flags
   void* dp_comm = nullptr;
   int dp_size = 1, dp_rank = 0;
+  cudaStream_t dp_stream = nullptr;
+  static constexpr int kDpEvents = 8;
+  cudaEvent_t dp_ev[kDpEvents] = {};
+  unsigned dp_ev_next = 0;
+  int* d_dp_flags = nullptr;
   bool has_model = false;
   bool owns_model = true;  // false for appo_ctx_create_shared contexts
   appo_model_desc desc{};
   Model* model = nullptr;
+  Reader* reader = nullptr;  // inference state of this context (model.cu)
 };
 constexpr int kRedSlots = 148 * 8 * 8;
 
@@ -71,6 +79,12 @@ struct appo_ctx : appo_b200::Ctx {};
       appo_b200::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));      \
       return APPO_ERR_RESOURCE;                                                      \
     }                                                                                \
+  } while (0)
+
+#define APPO_TRY(x)                       \
+  do {                                    \
+    int _st_ = (x);                       \
+    if (_st_ != APPO_OK) return _st_;     \
   } while (0)
 
 #define APPO_REQUIRE(cond, code, msg)  \
@@ -138,6 +152,10 @@ inline bool pdl_default(bool shared) {
 namespace appo_b200 {
 
 cudaEvent_t timing_event(Ctx* c);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) for `kernel` on the
+// current device, once per (kernel, device): the attribute is per device, so a
+// process driving learners on several GPUs must set it on each.
+int ensure_smem_attr(const void* kernel, int bytes, int device);
 inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
   if (!c->timing) return nullptr;
   if (!c->timing_filter.empty() && c->timing_filter != "gemm_shapes" &&
@@ -205,8 +223,11 @@ int launch_logp_entropy(Ctx* c, int B, int A, const float* logits, const int32_t
                         float* logp, float* ent);
 int launch_sample(Ctx* c, int B, int A, const float* logits, uint64_t key, uint64_t counter0,
                   int32_t* actions, float* logp);
+// peer_flags (data-parallel): the ranks' max-reduced rejection flags, folded
+// into c's flags before the update so every rank accepts or rejects together
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
-                uint16_t* bf16_copy, float* f32_copy, unsigned* applied);
+                uint16_t* bf16_copy, float* f32_copy, unsigned* applied,
+                const int* peer_flags = nullptr);
 
 }  // namespace appo_b200

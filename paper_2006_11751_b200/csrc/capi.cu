@@ -2,6 +2,8 @@
 // stateless hot-path kernels.  Model-level entry points live in model.cu.
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "appo_common.cuh"
@@ -17,6 +19,16 @@ cudaEvent_t timing_event(Ctx* c) {
     c->ev_pool.push_back(e);
   }
   return c->ev_pool[c->ev_used++];
+}
+int ensure_smem_attr(const void* kernel, int bytes, int device) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> set;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = set[{kernel, device}];
+  if (have >= bytes) return APPO_OK;
+  APPO_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+  return APPO_OK;
 }
 }  // namespace appo_b200
 
@@ -35,7 +47,7 @@ int check_ctx(appo_ctx* ctx) {
   }
   return APPO_OK;
 }
-// VTraceConfig::validate (offpolicy.hpp:101-105)
+// VTraceConfig::validate (offpolicy.hpp:23-27)
 int validate_vtrace(float gamma, float rho_bar, float c_bar) {
   if (!(rho_bar >= c_bar && c_bar > 0.0f)) {
     set_error("vtrace requires rho_bar >= c_bar > 0");
@@ -56,7 +68,8 @@ int validate_vtrace(float gamma, float rho_bar, float c_bar) {
   } while (0)
 
 namespace appo_b200 {
-void dp_destroy(Ctx* c);  // dp.cu
+void dp_destroy(Ctx* c);      // dp.cu
+void reader_release(Ctx* c);  // model.cu
 }
 int model_create(appo_b200::Ctx* c);   // model.cu
 void model_destroy(appo_b200::Ctx* c); // model.cu
@@ -128,6 +141,7 @@ int appo_ctx_destroy(appo_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   cudaDeviceSynchronize();
+  if (ctx->model) appo_b200::reader_release(ctx);
   if (ctx->model && ctx->owns_model) model_destroy(ctx);
   appo_b200::dp_destroy(ctx);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);

@@ -80,7 +80,7 @@ struct BiasOut {
 // layer below and its bias gradient, as ONE implicit GEMM over the four
 // sub-pixel parity classes (no dcol matrix, no col2im):
 //   dz[r][y][x][n] = ELU'(aprev[r][y][x][n]) * sum_{kh,kw,co} dz_next[r][(y-kh)/2][(x-kw)/2][co] W[co][kh][kw][n]
-// wt = rearranged weights [4 classes][N][4 taps][Co] (k_dgrad_weights); k <= 4.
+// wt = rearranged weights [4 classes][N][4 taps][Co] (k_publish_derived); k <= 4.
 struct DgradIn {
   const uint16_t* dz_next = nullptr;  // bf16 NHWC [n_img][Ho][Wo][Co]
   const uint16_t* wt = nullptr;

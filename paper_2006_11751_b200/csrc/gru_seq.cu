@@ -877,8 +877,7 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
   static int cl_state = getenv("APPO_GRU_CLUSTER") ? 0 : -1;  // 0 untried, 1 ok, -1 off
   if (cl_state >= 0) {
     if (cl_state == 0) {
-      if (cudaFuncSetAttribute(gru_cl_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               CL_SMEM) != cudaSuccess ||
+      if (ensure_smem_attr((const void*)gru_cl_fwd_kernel, CL_SMEM, c->device) != APPO_OK ||
           cudaFuncSetAttribute(gru_cl_fwd_kernel,
                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
         cudaGetLastError();
@@ -921,12 +920,7 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
       cl_state = -1;  // fall back for good
     }
   }
-  static bool attr = false;
-  if (!attr) {
-    APPO_CUDA_TRY(cudaFuncSetAttribute(gru_seq_fwd_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM));
-    attr = true;
-  }
+  APPO_TRY(ensure_smem_attr((const void*)gru_seq_fwd_kernel, FWD_SMEM, c->device));
   APPO_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));
   long long* prof = prof_buffer(c);
   FwdArgs a{};
@@ -950,12 +944,7 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
 int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* done,
                   const float* gates, const float* hin, const uint16_t* whh, uint16_t* dghx,
                   uint16_t* dgi, uint16_t* dgh, float* gbih, float* gbhh, unsigned* bar) {
-  static bool attr = false;
-  if (!attr) {
-    APPO_CUDA_TRY(cudaFuncSetAttribute(gru_seq_bwd_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM));
-    attr = true;
-  }
+  APPO_TRY(ensure_smem_attr((const void*)gru_seq_bwd_kernel, BWD_SMEM, c->device));
   APPO_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));
   long long* prof = prof_buffer(c);
   BwdArgs a{};

@@ -10,8 +10,12 @@
 // layer's NHWC input, and conv3's output rows flatten (h, w, c) for the FC.
 #include <cuda_bf16.h>
 
+#include <unistd.h>
+
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "gemm.cuh"
@@ -366,7 +370,9 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
 
 }  // namespace
 
-int dp_allreduce_grad(Ctx* c, float* grad, int64_t n);  // dp.cu
+// dp.cu: bucketed data-parallel gradient all-reduce
+int dp_bucket(Ctx* c, float* buf, int64_t n);
+int dp_finish(Ctx* c, float* buf, int64_t n, const int** peer_flags);
 
 // Batched inference over B observations at obs_base + b*obs_stride (contiguous
 // batch or trajectory slots): encoder + GRU + heads + sampling.
@@ -375,7 +381,9 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
                   float* logits, int64_t* version_out) {
   Model* M = c->model;
   const Dims& d = M->d;
-  Scratch& s = M->si;
+  Reader* rd = reader_of(c);
+  APPO_REQUIRE(rd != nullptr, APPO_ERR_RESOURCE, "inference state allocation failed");
+  Scratch& s = rd->s;
   TRY(alloc_scratch(c, M, s, B, 0, false));
   // ParamStore::fetch (policy.hpp:498-509): newest COMPLETED publish; if the
   // newest Adam step is still running (possibly on the learner's stream) take
@@ -405,9 +413,56 @@ int sampler_infer(Ctx* c, const uint8_t* obs_base, int64_t obs_stride, int B, co
                 Operand{wb + d.off_whh, kHidden, false}, g, 128));
   TRY(k_gru_infer(c, B, d.A, s.gi, s.gh, h_in, pf + d.off_wpi, pf + d.off_bpi, pf + d.off_wv,
                   pf + d.off_bv, M->sample_key, counter0, h_out, actions, logp, values, logits));
-  // last reader of pub[pub] on this stream: the learner waits on this event
-  // before overwriting the buffer (it may run on another stream)
-  APPO_CUDA_TRY(cudaEventRecord(M->pub_ev[pub], c->stream));
+  // last read of pub[pub] by this context: the learner waits on this event
+  // (and every other reader's) before overwriting the buffer
+  APPO_CUDA_TRY(cudaEventRecord(rd->read_ev[pub], c->stream));
+  return APPO_OK;
+}
+
+Reader* reader_of(Ctx* c) {
+  if (c->reader) return c->reader;
+  Reader* r = new Reader();
+  for (int k = 0; k < Model::kPub; ++k)
+    if (cudaEventCreateWithFlags(&r->read_ev[k], cudaEventDisableTiming) != cudaSuccess) {
+      for (int j = 0; j < k; ++j) cudaEventDestroy(r->read_ev[j]);
+      delete r;
+      return nullptr;
+    }
+  {
+    std::lock_guard<std::mutex> lk(c->model->readers_mu);
+    c->model->readers.push_back(r);
+  }
+  c->reader = r;
+  return r;
+}
+
+static void reader_free(Reader* r) {
+  if (r->s.col1) cudaFree(r->s.col1);
+  if (r->s.h_stats) cudaFreeHost(r->s.h_stats);
+  for (int k = 0; k < Model::kPub; ++k)
+    if (r->read_ev[k]) cudaEventDestroy(r->read_ev[k]);
+  delete r;
+}
+
+void reader_release(Ctx* c) {
+  Reader* r = c->reader;
+  if (!r) return;
+  c->reader = nullptr;
+  if (c->model) {
+    std::lock_guard<std::mutex> lk(c->model->readers_mu);
+    auto& v = c->model->readers;
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i] == r) {
+        v.erase(v.begin() + (long)i);
+        break;
+      }
+  }
+  reader_free(r);
+}
+
+int wait_readers(Model* M, cudaStream_t st, int k) {
+  std::lock_guard<std::mutex> lk(M->readers_mu);
+  for (Reader* r : M->readers) APPO_CUDA_TRY(cudaStreamWaitEvent(st, r->read_ev[k], 0));
   return APPO_OK;
 }
 
@@ -441,7 +496,6 @@ int model_create(Ctx* c) {
     APPO_CUDA_TRY(cudaMalloc(&M->pub_c1b[k], 32 * 4));
     APPO_CUDA_TRY(cudaMalloc(&M->pub_wt2[k], (size_t)4 * 32 * 256 * 2));
     APPO_CUDA_TRY(cudaMalloc(&M->pub_wt3[k], (size_t)4 * 64 * 512 * 2));
-    APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->pub_ev[k], cudaEventDisableTiming));
     APPO_CUDA_TRY(cudaEventCreateWithFlags(&M->ready_ev[k], cudaEventDisableTiming));
   }
   M->sample_key = host_derive_seed(c->seed, 0x9900);
@@ -467,16 +521,16 @@ void model_destroy(Ctx* c) {
     cudaFree(M->pub_c1b[k]);
     cudaFree(M->pub_wt2[k]);
     cudaFree(M->pub_wt3[k]);
-    if (M->pub_ev[k]) cudaEventDestroy(M->pub_ev[k]);
     if (M->ready_ev[k]) cudaEventDestroy(M->ready_ev[k]);
   }
   if (M->ring_host) cudaFreeHost(M->ring_host);
   for (int k = 0; k < Model::kRing; ++k)
     if (M->ring_ev[k]) cudaEventDestroy(M->ring_ev[k]);
-  for (Scratch* s : {&M->si, &M->sl}) {
-    if (s->col1) cudaFree(s->col1);
-    if (s->h_stats) cudaFreeHost(s->h_stats);
-  }
+  if (M->sl.col1) cudaFree(M->sl.col1);
+  if (M->sl.h_stats) cudaFreeHost(M->sl.h_stats);
+  // readers of shared contexts still alive (contract: destroy those first)
+  for (Reader* r : M->readers) reader_free(r);
+  M->readers.clear();
   delete M;
   c->model = nullptr;
 }
@@ -564,6 +618,29 @@ int appo_adam_set(appo_ctx* ctx, const float* h_m, const float* h_v, int64_t t) 
   return APPO_OK;
 }
 
+// After theta / m / v of dst were overwritten on dst's stream: derive and
+// publish the inference copy into buffer `next`, adopt the Adam step count
+// (copy_weights copies d.adam = s.adam, runner.hpp:221-222) and count the
+// publish as dst's next version.  (The reference republishes with dst's
+// unchanged version, so its policy workers keep the old weights until the next
+// SGD step; here inference switches to the copied weights at once.)
+static int publish_copied(appo_ctx* dst, int next, int64_t adam_t) {
+  Model* D = dst->model;
+  const int64_t P = D->d.total;
+  cudaStream_t st = dst->stream;
+  APPO_CUDA_TRY(cudaMemcpyAsync(D->pub_f32[next], D->theta, P * 4, cudaMemcpyDeviceToDevice, st));
+  TRY(k_f32_to_bf16(dst, 1, D->theta, P, D->pub_bf16[next], P, (int)P));
+  TRY(k_publish_derived(dst, D->pub_bf16[next], D->pub_f32[next], D->d, D->pub_c1h[next],
+                        D->pub_c1b[next], D->pub_wt2[next], D->pub_wt3[next]));
+  APPO_CUDA_TRY(cudaEventRecord(D->ready_ev[next], st));
+  D->adam_t = adam_t;
+  D->pub_version[next] = D->version + 1;
+  D->published_prev = D->published;
+  D->published = next;
+  D->version += 1;  // ParamStore::publish of the copied weights
+  return APPO_OK;
+}
+
 // PbtController's copy_weights (runner.hpp:211-219): dst takes src's theta and
 // Adam state and publishes them as its next version.  Device to device (peer
 // copy over NVLink when the learners live on different GPUs), ordered after
@@ -588,7 +665,7 @@ int appo_params_copy(appo_ctx* dst, appo_ctx* src) {
   APPO_CUDA_TRY(cudaSetDevice(dst->device));
   cudaStream_t st = dst->stream;
   const int next = (D->published + 1) % Model::kPub;
-  APPO_CUDA_TRY(cudaStreamWaitEvent(st, D->pub_ev[next], 0));
+  TRY(wait_readers(D, st, next));
   auto copy = [&](float* to, const float* from) -> int {
     if (dst->device == src->device)
       APPO_CUDA_TRY(cudaMemcpyAsync(to, from, P * 4, cudaMemcpyDeviceToDevice, st));
@@ -599,16 +676,93 @@ int appo_params_copy(appo_ctx* dst, appo_ctx* src) {
   TRY(copy(D->theta, S->theta));
   TRY(copy(D->m, S->m));
   TRY(copy(D->v, S->v));
-  APPO_CUDA_TRY(cudaMemcpyAsync(D->pub_f32[next], D->theta, P * 4, cudaMemcpyDeviceToDevice, st));
-  TRY(k_f32_to_bf16(dst, 1, D->theta, P, D->pub_bf16[next], P, (int)P));
-  TRY(k_publish_derived(dst, D->pub_bf16[next], D->pub_f32[next], D->d, D->pub_c1h[next],
-                        D->pub_c1b[next], D->pub_wt2[next], D->pub_wt3[next]));
-  APPO_CUDA_TRY(cudaEventRecord(D->ready_ev[next], st));
-  D->adam_t = S->adam_t;
-  D->pub_version[next] = D->version + 1;
-  D->published_prev = D->published;
-  D->published = next;
-  D->version += 1;  // ParamStore::publish of the copied weights
+  return publish_copied(dst, next, S->adam_t);
+}
+
+// The published state a peer PROCESS imports (appo_params_export/_import):
+// CUDA IPC handles of the exporter's theta / m / v plus the host values that
+// go with them.  Fixed layout inside APPO_STATE_HANDLE_BYTES.
+struct StateHandle {
+  uint64_t magic;
+  int64_t pid, device, n_params, adam_t, version;
+  uint64_t spec_hash;
+  cudaIpcMemHandle_t theta, m, v;
+};
+static_assert(sizeof(StateHandle) <= APPO_STATE_HANDLE_BYTES, "state handle too large");
+constexpr uint64_t kStateMagic = 0x31455441545341ull;  // "ASTATE1"
+
+int appo_params_export(appo_ctx* ctx, void* handle_out) {
+  MODEL_OR_RETURN(ctx);
+  APPO_REQUIRE(handle_out != nullptr, APPO_ERR_CONTRACT, "params_export: null handle");
+  Model* M = ctx->model;
+  APPO_REQUIRE(M->pending == 0, APPO_ERR_CONTRACT,
+               "params_export: collect the learner steps first");
+  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the exported state is final
+  StateHandle h{};
+  h.magic = kStateMagic;
+  h.pid = (int64_t)getpid();
+  h.device = ctx->device;
+  h.n_params = M->d.total;
+  h.adam_t = M->adam_t;
+  h.version = M->version;
+  h.spec_hash = appo_model_spec_hash(&ctx->desc);
+  APPO_CUDA_TRY(cudaIpcGetMemHandle(&h.theta, M->theta));
+  APPO_CUDA_TRY(cudaIpcGetMemHandle(&h.m, M->m));
+  APPO_CUDA_TRY(cudaIpcGetMemHandle(&h.v, M->v));
+  std::memset(handle_out, 0, APPO_STATE_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return APPO_OK;
+}
+
+// Opened peer allocations, kept for the life of the process (PBT exchanges
+// repeat between the same learners; opening a handle costs milliseconds).
+static void* open_peer(const cudaIpcMemHandle_t& mh, int device, int* status) {
+  static std::mutex mu;
+  static std::map<std::pair<std::string, int>, void*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(std::string(mh.reserved, sizeof(mh.reserved)), device);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  void* p = nullptr;
+  const cudaError_t e = cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    *status = APPO_ERR_RESOURCE;
+    return nullptr;
+  }
+  cache[key] = p;
+  return p;
+}
+
+int appo_params_import(appo_ctx* dst, const void* handle) {
+  MODEL_OR_RETURN(dst);
+  APPO_REQUIRE(handle != nullptr, APPO_ERR_CONTRACT, "params_import: null handle");
+  StateHandle h;
+  std::memcpy(&h, handle, sizeof(h));
+  APPO_REQUIRE(h.magic == kStateMagic, APPO_ERR_CONTRACT, "params_import: not a state handle");
+  APPO_REQUIRE(h.pid != (int64_t)getpid(), APPO_ERR_CONTRACT,
+               "params_import: exporter is this process (use appo_params_copy)");
+  Model* D = dst->model;
+  APPO_REQUIRE(h.n_params == D->d.total && h.spec_hash == appo_model_spec_hash(&dst->desc),
+               APPO_ERR_CONFIG, "params_import: different model shapes");
+  APPO_REQUIRE(D->pending == 0, APPO_ERR_CONTRACT,
+               "params_import: collect the destination's learner steps first");
+  int st = APPO_OK;
+  const float* th = static_cast<const float*>(open_peer(h.theta, dst->device, &st));
+  const float* m = th ? static_cast<const float*>(open_peer(h.m, dst->device, &st)) : nullptr;
+  const float* v = m ? static_cast<const float*>(open_peer(h.v, dst->device, &st)) : nullptr;
+  if (!v) return st;
+  const int64_t P = D->d.total;
+  cudaStream_t s = dst->stream;
+  const int next = (D->published + 1) % Model::kPub;
+  TRY(wait_readers(D, s, next));
+  // unified addressing: same-GPU device copy or NVLink peer copy
+  APPO_CUDA_TRY(cudaMemcpyAsync(D->theta, th, P * 4, cudaMemcpyDefault, s));
+  APPO_CUDA_TRY(cudaMemcpyAsync(D->m, m, P * 4, cudaMemcpyDefault, s));
+  APPO_CUDA_TRY(cudaMemcpyAsync(D->v, v, P * 4, cudaMemcpyDefault, s));
+  TRY(publish_copied(dst, next, h.adam_t));
+  // the exporter may resume once this returns (its state was read)
+  APPO_CUDA_TRY(cudaStreamSynchronize(s));
   return APPO_OK;
 }
 
@@ -649,7 +803,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   APPO_REQUIRE(slot_bytes >= d.slot[9], APPO_ERR_CONTRACT,
                "learner_step: slot_bytes smaller than the layout v2 slot");
   APPO_REQUIRE(n_traj <= 4096, APPO_ERR_CONTRACT, "learner_step: at most 4096 trajectories");
-  // VTraceConfig / ClipConfig validation (offpolicy.hpp:101-122)
+  // VTraceConfig / ClipConfig validation (offpolicy.hpp:23-44)
   APPO_REQUIRE(hp->rho_bar >= hp->c_bar && hp->c_bar > 0.0f, APPO_ERR_CONFIG,
                "vtrace requires rho_bar >= c_bar > 0");
   APPO_REQUIRE(hp->gamma > 0.0f && hp->gamma <= 1.0f, APPO_ERR_CONFIG,
@@ -802,6 +956,9 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
       TRY(k_colsum(ctx, B, kGates, s.dgi, kGates, true, s.colsum_part, G + d.off_bih, false));
       TRY(k_colsum(ctx, B, kGates, s.dgh, kGates, true, s.colsum_part, G + d.off_bhh, false));
     }
+    // data-parallel bucket 1 (GRU + heads) is final: reduce it while the
+    // encoder backward runs
+    TRY(dp_bucket(ctx, G + d.off_wih, d.total - d.off_wih));
     // dx = dgi . W_ih, times ELU'(fc) -> dz_fc
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
@@ -842,6 +999,8 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     TRY(gemm_bf16(ctx, B, d.F, kHidden, Operand{s.dzfc, kHidden, false},
                   Operand{wb + d.off_fcw, d.F, true}, x, 128));
   }
+  // bucket 2 (FC weight + bias) is final
+  TRY(dp_bucket(ctx, G + d.off_fcw, d.off_wih - d.off_fcw));
   // ---- conv3 backward ----
   {
     const int M3 = B * d.P3;
@@ -894,17 +1053,19 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   // the slots are no longer read: hand them back (free list, orchestrator.hpp:870)
   if (fq) TRY(slotq_push_launch(ctx, fq, s.slot_ids, 0, n_traj, q_ok));
 
-  // ---- data-parallel: average the gradient over ranks before clip + Adam ----
-  TRY(dp_allreduce_grad(ctx, G, d.total));
+  // ---- data-parallel: last bucket (convolutions) + rejection consensus;
+  //      the averaged gradient is complete before clip + Adam ----
+  const int* peer_flags = nullptr;
+  TRY(dp_finish(ctx, G, d.off_fcw, &peer_flags));
 
   // ---- global-norm clip + Adam; publish into the other buffer ----
   const int next = (pub + 1) % Model::kPub;
   // do not overwrite a published copy an inference (any stream) may still read
-  APPO_CUDA_TRY(cudaStreamWaitEvent(st, M->pub_ev[next], 0));
+  TRY(wait_readers(M, st, next));
   M->adam_t += 1;
   TRY(launch_adam(ctx, d.total, M->theta, M->m, M->v, G, M->adam_t, hp->lr, hp->beta1,
                   hp->beta2, hp->eps, hp->grad_clip, s.stats + 8, M->pub_bf16[next],
-                  M->pub_f32[next], ctx->d_counter + 6));
+                  M->pub_f32[next], ctx->d_counter + 6, peer_flags));
   APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
   APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
   TRY(k_publish_derived(ctx, M->pub_bf16[next], M->pub_f32[next], d, M->pub_c1h[next],

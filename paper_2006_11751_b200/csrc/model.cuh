@@ -5,6 +5,9 @@
 #pragma once
 #include <stdint.h>
 
+#include <mutex>
+#include <vector>
+
 #include "appo_common.cuh"
 
 namespace appo_b200 {
@@ -63,17 +66,20 @@ struct Scratch {
   double* h_stats = nullptr;    // pinned
 };
 
+struct Reader;
+
 struct Model {
   Dims d;
   float* theta = nullptr;  // fp32 master [P]
   float* m = nullptr;
   float* v = nullptr;
   float* grad = nullptr;
-  // Published inference copies, triple-buffered: the learner writes
-  // pub[(published+1)%3] (after waiting on pub_ev of that buffer, recorded by
-  // the last inference that read it, possibly on another stream), then flips
-  // `published` -- the device-side counterpart of ParamStore's seqlock
-  // (policy.hpp:457-519): inference never observes a half-written version.
+  // Published inference copies, kPub-buffered: the learner writes
+  // pub[(published+1)%kPub] (after waiting on every reader context's read
+  // event of that buffer, recorded by its last inference that read it,
+  // possibly on another stream), then flips `published` -- the device-side
+  // counterpart of ParamStore's seqlock (policy.hpp:457-519): inference never
+  // observes a half-written version.
   static constexpr int kPub = 8;
   uint16_t* pub_bf16[kPub] = {};
   float* pub_f32[kPub] = {};
@@ -81,10 +87,9 @@ struct Model {
   // with the fp16-input offset removed (b - 1024/255 * sum_k W), see gemm.cu
   uint16_t* pub_c1h[kPub] = {};
   float* pub_c1b[kPub] = {};
-  // sub-pixel dgrad operands of conv2 / conv3 (k_dgrad_weights layout)
+  // sub-pixel dgrad operands of conv2 / conv3 (k_publish_derived layout)
   uint16_t* pub_wt2[kPub] = {};
   uint16_t* pub_wt3[kPub] = {};
-  cudaEvent_t pub_ev[kPub] = {};    // recorded after the last inference read of pub[k]
   cudaEvent_t ready_ev[kPub] = {};  // recorded after the Adam step that wrote pub[k]
   int64_t pub_version[kPub] = {};   // parameter version held by pub[k]
   int published = 0;                // newest submitted publish
@@ -101,8 +106,27 @@ struct Model {
   int last_ring = -1;
   int64_t pending = 0;
   unsigned applied_synced = 0;
-  Scratch si;  // inference scratch
   Scratch sl;  // learner scratch
+  // contexts running inference on this model (the owner and its
+  // appo_ctx_create_shared contexts), each with its own scratch and read events
+  std::mutex readers_mu;
+  std::vector<Reader*> readers;
 };
+
+// Per-context inference state: activation scratch and, per published buffer,
+// the event recorded after this context's last inference read of it.  Shared
+// contexts run inference concurrently on their own streams, so none of this
+// may be shared between them.
+struct Reader {
+  Scratch s;
+  cudaEvent_t read_ev[Model::kPub] = {};
+};
+
+// Make `st` wait until no reader context still reads published buffer k.
+int wait_readers(Model* M, cudaStream_t st, int k);
+// The ctx's reader state (created and registered with its model on first use).
+Reader* reader_of(Ctx* c);
+// Unregister and free the ctx's reader state (appo_ctx_destroy).
+void reader_release(Ctx* c);
 
 }  // namespace appo_b200

@@ -1,4 +1,4 @@
-// SIMT kernels around the tcgen05 GEMMs of the model: im2col / col2im(+ELU'),
+// SIMT kernels around the tcgen05 GEMMs of the model: im2col (fallbacks),
 // the GRU cell (inference: fused with heads + sampling; training: with saved
 // gates and done-masked recurrence), heads forward/backward, the fused PPO
 // loss, slot gathers, column sums for bias gradients.
@@ -88,175 +88,10 @@ __global__ void im2col_nhwc_kernel(const uint16_t* __restrict__ act, int64_t R, 
   }
 }
 
-// Backward of im2col (gather form) fused with ELU': for each input element
-// dz[r][yi][xi][ci] = aprev'(.) * sum_{kh,kw: (yi-kh)%s==0, (xi-kw)%s==0} dcol[row(yo,xo)][(kh*k+kw)*Cin+ci]
-__global__ void col2im_delu_kernel(const float* __restrict__ dcol,
-                                   const uint16_t* __restrict__ aprev, int64_t R, int Hi, int Wi,
-                                   int Cin, int k, int s, int Ho, int Wo,
-                                   uint16_t* __restrict__ dz) {
-  APPO_PDL_ENTRY();
-  const int64_t total = R * Hi * Wi * Cin;
-  const int K = k * k * Cin;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int ci = (int)(g % Cin);
-    int64_t rest = g / Cin;
-    const int xi = (int)(rest % Wi);
-    rest /= Wi;
-    const int yi = (int)(rest % Hi);
-    const int64_t r = rest / Hi;
-    float acc = 0.0f;
-    for (int kh = yi % s; kh < k; kh += s) {
-      const int yo = (yi - kh) / s;
-      if (yo < 0 || yo >= Ho) continue;
-      for (int kw = xi % s; kw < k; kw += s) {
-        const int xo = (xi - kw) / s;
-        if (xo < 0 || xo >= Wo) continue;
-        acc += dcol[(r * Ho * Wo + (int64_t)yo * Wo + xo) * K + (kh * k + kw) * Cin + ci];
-      }
-    }
-    const float a = bf2f(aprev[g]);
-    dz[g] = f2bf(acc * (a > 0.0f ? 1.0f : a + 1.0f));
-  }
-}
-
-// Block-level column sums of per-thread 8-wide partials over contiguous bf16
-// [M][N] data walked in 16-byte chunks: thread t always owns column group
-// t % (N/8) because the grid stride is a multiple of N/8 (256 % (N/8) == 0).
-// The block's sums are added as 2^-32 fixed point into int64 accumulators
-// (integer adds commute: the result is bit-identical whatever the block
-// order); the last block converts them to fp32 into out[N] and re-zeroes the
-// accumulators and the counter for the next call.
-__device__ __forceinline__ void block_colsum_reduce(const float (&acc)[8], int cg, const BiasOut& o) {
-  __shared__ float sh[256][9];
-  __shared__ bool last;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) sh[threadIdx.x][k] = acc[k];
-  __syncthreads();
-  for (int n = threadIdx.x; n < o.N; n += blockDim.x) {
-    const int g = n >> 3, k = n & 7;
-    float t = 0.0f;
-    for (int th = g; th < (int)blockDim.x; th += cg) t += sh[th][k];
-    // kBiasCopies interleaved accumulator copies spread the same-address atomics
-    atomicAdd(o.acc + (size_t)(blockIdx.x % kBiasCopies) * o.N + n,
-              (unsigned long long)llrint((double)t * 4294967296.0));
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(o.counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    for (int n = threadIdx.x; n < o.N; n += blockDim.x) {
-      unsigned long long v = 0;
-      for (int k = 0; k < kBiasCopies; ++k) v += atomicExch(o.acc + (size_t)k * o.N + n, 0ull);
-      o.out[n] = (float)((double)(long long)v * (1.0 / 4294967296.0));
-    }
-    if (threadIdx.x == 0) *o.counter = 0;
-  }
-}
-
-__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4 v) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    acc[2 * q] += bf2f((uint16_t)(w[q] & 0xFFFF));
-    acc[2 * q + 1] += bf2f((uint16_t)(w[q] >> 16));
-  }
-}
-
-// Same as above with bf16 dcol and 8 channels per thread (16-byte loads/stores).
-// With part != null the bias gradient of the produced dz (column sums over all
-// rows and positions) is reduced on the fly into per-block partials.
-__global__ void __launch_bounds__(256)
-    col2im_delu_bf16_kernel(const uint16_t* __restrict__ dcol, const uint16_t* __restrict__ aprev,
-                            int64_t R, int Hi, int Wi, int Cin, int k, int s, int Ho, int Wo,
-                            uint16_t* __restrict__ dz, BiasOut bias) {
-  APPO_PDL_ENTRY();
-  const int cg = Cin >> 3;
-  const int64_t total = R * Hi * Wi * cg;
-  const int K = k * k * Cin;
-  float bsum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int c8 = (int)(g % cg);
-    int64_t rest = g / cg;
-    const int xi = (int)(rest % Wi);
-    rest /= Wi;
-    const int yi = (int)(rest % Hi);
-    const int64_t r = rest / Hi;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int kh = yi % s; kh < k; kh += s) {
-      const int yo = (yi - kh) / s;
-      if (yo < 0 || yo >= Ho) continue;
-      for (int kw = xi % s; kw < k; kw += s) {
-        const int xo = (xi - kw) / s;
-        if (xo < 0 || xo >= Wo) continue;
-        acc_bf16x8(acc, *reinterpret_cast<const uint4*>(
-                            dcol + (r * Ho * Wo + (int64_t)yo * Wo + xo) * K + (kh * k + kw) * Cin +
-                            c8 * 8));
-      }
-    }
-    const int64_t o = g * 8;
-    const uint4 av = *reinterpret_cast<const uint4*>(aprev + o);
-    const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
-    uint32_t out[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float a0 = bf2f((uint16_t)(aw[q] & 0xFFFF)), a1 = bf2f((uint16_t)(aw[q] >> 16));
-      const uint16_t d0 = f2bf(acc[2 * q] * (a0 > 0.0f ? 1.0f : a0 + 1.0f));
-      const uint16_t d1 = f2bf(acc[2 * q + 1] * (a1 > 0.0f ? 1.0f : a1 + 1.0f));
-      bsum[2 * q] += bf2f(d0);
-      bsum[2 * q + 1] += bf2f(d1);
-      out[q] = (uint32_t)d0 | ((uint32_t)d1 << 16);
-    }
-    *reinterpret_cast<uint4*>(dz + o) = make_uint4(out[0], out[1], out[2], out[3]);
-  }
-  if (bias.out) block_colsum_reduce(bsum, cg, bias);
-}
-
-// Column sums of a contiguous bf16 [M][N] matrix (N % 8 == 0, 256 % (N/8) ==
-// 0) into per-block partials part[blockIdx.x][N]; bias_finalize_kernel sums
-// the blocks.
-__global__ void __launch_bounds__(256)
-    colsum_v_kernel(int64_t M, const uint16_t* __restrict__ src, BiasOut bias) {
-  APPO_PDL_ENTRY();
-  const int N = bias.N;
-  const int cg = N >> 3;
-  const int64_t total = M * cg;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  for (; q + 3 * stride < total; q += 4 * stride) {
-    uint4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(src) + q + u * stride);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc_bf16x8(acc, v[u]);
-  }
-  for (; q < total; q += stride) acc_bf16x8(acc, __ldg(reinterpret_cast<const uint4*>(src) + q));
-  block_colsum_reduce(acc, cg, bias);
-}
-
-// Sub-pixel dgrad weight operand (see k_dgrad_weights): one thread per element.
-// wt[(cls, ci)][(a, b, co)] = W[co][py+2a][px+2b][ci] for taps inside the kernel, else 0.
-__global__ void dgrad_weights_kernel(const uint16_t* __restrict__ w, int Co, int k, int Ci,
-                                     uint16_t* __restrict__ wt) {
-  APPO_PDL_ENTRY();
-  const int kmax = 4 * Co;
-  const int total = 4 * Ci * kmax;
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
-    const int kk = g % kmax, ci = (g / kmax) % Ci, cls = g / (kmax * Ci);
-    const int tap = kk / Co, co = kk % Co;
-    const int kh = (cls >> 1) + 2 * (tap >> 1), kw = (cls & 1) + 2 * (tap & 1);
-    wt[g] = (kh < k && kw < k) ? w[(((size_t)co * k + kh) * k + kw) * Ci + ci] : (uint16_t)0;
-  }
-}
-
 // Operands derived from a published copy in ONE launch (after the Adam step
 // that wrote it): blocks 0..nb-2 rearrange the conv3 / conv2 weights for the
-// sub-pixel dgrad (k_dgrad_weights layout), the last block writes the conv1
-// fp16 weights and offset-corrected bias (conv1_half_kernel).
+// sub-pixel dgrad (k_publish_derived layout), the last block writes the conv1
+// fp16 weights and offset-corrected bias.
 __global__ void __launch_bounds__(256)
     publish_derived_kernel(const uint16_t* __restrict__ wb, const float* __restrict__ pf,
                            int64_t off_c1w, int64_t off_c1b, int K1, int64_t off_c2w,
@@ -293,25 +128,6 @@ __global__ void __launch_bounds__(256)
     const uint16_t* w = wb + (is3 ? off_c3w : off_c2w);
     const uint16_t v = (kh < k && kw < k) ? w[(((size_t)co * k + kh) * k + kw) * Ci + ci] : (uint16_t)0;
     (is3 ? wt3 : wt2)[e] = v;
-  }
-}
-
-// conv1 fp16 operands of a published parameter copy (one block, warp per
-// output channel): wh = fp16(W), bias' = b - (1024/255) * sum_k wh (the conv1
-// GEMM multiplies fp16 (1024 + pixel) inputs, gemm.cu u8_convert).
-__global__ void conv1_half_kernel(const float* __restrict__ w, const float* __restrict__ b,
-                                  int K, uint16_t* __restrict__ wh, float* __restrict__ bh) {
-  APPO_PDL_ENTRY();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int co = warp; co < 32; co += blockDim.x >> 5) {
-    float acc = 0.0f;
-    for (int k = lane; k < K; k += 32) {
-      const __half h = __float2half_rn(w[(size_t)co * K + k]);
-      wh[(size_t)co * K + k] = __half_as_ushort(h);
-      acc += __half2float(h);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) bh[co] = b[co] - (1024.0f / 255.0f) * acc;
   }
 }
 
@@ -697,24 +513,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dcore[s][j] = sum_a dlog[s][a] * wpi[a][j] + dV[s] * wv[j]; warp per row.
-__global__ void __launch_bounds__(256)
-    heads_bwd_kernel(int B, int A, const float* __restrict__ dlog, const float* __restrict__ wpi,
-                     const float* __restrict__ wv, float* __restrict__ dcore) {
-  APPO_PDL_ENTRY();
-  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (s >= B) return;
-  float dl[kMaxActions + 1];
-  for (int a = 0; a <= A; ++a) dl[a] = dlog[(int64_t)s * (A + 1) + a];
-  for (int q = 0; q < kHidden / 32; ++q) {
-    const int j = lane + 32 * q;
-    float acc = dl[A] * wv[j];
-    for (int a = 0; a < A; ++a) acc += dl[a] * wpi[a * kHidden + j];
-    dcore[(int64_t)s * kHidden + j] = acc;
-  }
-}
-
 // Heads backward in one kernel (policy.hpp:377-383 analogue for the heads):
 // dcore[s][j] = sum_a dlog[s][a] * Wh[a][j] (Wh = policy rows then the value
 // row) and the head gradients dWh[a][j] = sum_s dlog[s][a] * core[s][j],
@@ -845,49 +643,6 @@ __global__ void colsum_final_kernel(int N, int chunks, const float* __restrict__
   out[n] = accumulate ? out[n] + t : t;
 }
 
-// Scatter the padded head-weight gradient [16][512] (rows 0..A-1 policy, row A
-// value) into the flat gradient and add the head bias gradients.
-__global__ void head_grad_scatter_kernel(int A, const float* __restrict__ headw,
-                                         const float* __restrict__ bias_sums, float* gwpi,
-                                         float* gbpi, float* gwv, float* gbv) {
-  APPO_PDL_ENTRY();
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < A * kHidden) gwpi[g] = headw[g];
-  if (g < kHidden) gwv[g] = headw[A * kHidden + g];
-  if (g < A) gbpi[g] = bias_sums[g];
-  if (g == 0) gbv[0] = bias_sums[A];
-}
-
-// Version lag statistics (orchestrator.hpp:790,862-863), one block.
-__global__ void lag_kernel(int B, const int64_t* __restrict__ ver, int64_t cur, double* stats) {
-  APPO_PDL_ENTRY();
-  __shared__ double sh[32];
-  __shared__ long long mn[32];
-  double s = 0;
-  long long m = LLONG_MAX;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) {
-    s += (double)(cur - ver[i]);
-    m = min(m, (long long)ver[i]);
-  }
-  s = warp_sum(s);
-  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) {
-    sh[threadIdx.x >> 5] = s;
-    mn[threadIdx.x >> 5] = m;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0;
-    long long mm = LLONG_MAX;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      t += sh[w];
-      mm = min(mm, mn[w]);
-    }
-    stats[6] = B > 0 ? t / B : 0.0;
-    stats[7] = B > 0 ? (double)(cur - mm) : 0.0;
-  }
-}
-
 int grid_for(int64_t n, int block, int max_blocks) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
@@ -914,49 +669,10 @@ int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Ci
               Cin, k, s, Ho, Wo, col);
   return APPO_OK;
 }
-int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
-                  int Cin, int k, int s, int Ho, int Wo, uint16_t* dz) {
-  const int64_t n = R * Hi * Wi * Cin;
-  c->next_bytes = (double)R * Ho * Wo * k * k * Cin * 4 + (double)n * 4;
-  APPO_LAUNCH(c, col2im_delu_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev, R,
-              Hi, Wi, Cin, k, s, Ho, Wo, dz);
-  return APPO_OK;
-}
-int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
-                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz,
-                       const BiasOut& bias) {
-  const int64_t n = R * Hi * Wi * (Cin / 8);
-  APPO_REQUIRE(!bias.out || (Cin % 8 == 0 && 256 % (Cin / 8) == 0 && bias.N == Cin),
-               APPO_ERR_CONTRACT, "col2im: fused bias sums need 256 % (Cin/8) == 0");
-  c->next_bytes = (double)R * Ho * Wo * k * k * Cin * 2 + (double)R * Hi * Wi * Cin * 4;
-  APPO_LAUNCH(c, col2im_delu_bf16_kernel, grid_for(n, 256, c->num_sms * 32), 256, 0, dcol, aprev,
-              R, Hi, Wi, Cin, k, s, Ho, Wo, dz, bias);
-  return APPO_OK;
-}
-int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias) {
-  const int N = bias.N;
-  APPO_REQUIRE(N % 8 == 0 && 256 % (N / 8) == 0 && bias.out, APPO_ERR_CONTRACT,
-               "colsum_v: need N % 8 == 0 and 256 % (N/8) == 0");
-  const int64_t chunks = M * (N / 8);
-  int grid = (int)((chunks + 256 * 8 - 1) / (256 * 8));  // ~8 chunks per thread
-  if (grid > c->num_sms * 8) grid = c->num_sms * 8;
-  if (grid < 1) grid = 1;
-  c->next_bytes = (double)M * N * 2;
-  APPO_LAUNCH(c, colsum_v_kernel, grid, 256, 0, M, src, bias);
-  return APPO_OK;
-}
-int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* wt) {
-  APPO_LAUNCH(c, dgrad_weights_kernel, grid_for(16 * Ci * Co, 256, 64), 256, 0, w, Co, k, Ci, wt);
-  return APPO_OK;
-}
 int k_publish_derived(Ctx* c, const uint16_t* wb, const float* pf, const Dims& d, uint16_t* c1h,
                       float* c1b, uint16_t* wt2, uint16_t* wt3) {
   APPO_LAUNCH(c, publish_derived_kernel, 148, 256, 0, wb, pf, d.off_c1w, d.off_c1b, d.K1, d.off_c2w,
               d.off_c3w, c1h, c1b, wt2, wt3);
-  return APPO_OK;
-}
-int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, float* bh) {
-  APPO_LAUNCH(c, conv1_half_kernel, 1, 1024, 0, w, b, K, wh, bh);
   return APPO_OK;
 }
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
@@ -1040,11 +756,6 @@ int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core
               gwv, gbv);
   return APPO_OK;
 }
-int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,
-                float* dcore) {
-  APPO_LAUNCH(c, heads_bwd_kernel, (B + 7) / 8, 256, 0, B, A, dlog, wpi, wv, dcore);
-  return APPO_OK;
-}
 int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,
               const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh) {
   APPO_LAUNCH(c, gru_bwd_kernel, (n_traj * kHidden + 255) / 256, 256, 0, n_traj, T, t, dcore,
@@ -1068,15 +779,4 @@ int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, f
               accumulate ? 1 : 0);
   return APPO_OK;
 }
-int k_head_grad_scatter(Ctx* c, int A, const float* headw, const float* bias_sums, float* gwpi,
-                        float* gbpi, float* gwv, float* gbv) {
-  APPO_LAUNCH(c, head_grad_scatter_kernel, (A * kHidden + 255) / 256, 256, 0, A, headw,
-              bias_sums, gwpi, gbpi, gwv, gbv);
-  return APPO_OK;
-}
-int k_lag(Ctx* c, int B, const int64_t* ver, int64_t cur, double* stats) {
-  APPO_LAUNCH(c, lag_kernel, 1, 1024, 0, B, ver, cur, stats);
-  return APPO_OK;
-}
-
 }  // namespace appo_b200

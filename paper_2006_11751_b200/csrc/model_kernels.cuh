@@ -33,22 +33,12 @@ struct LossHP {
 int k_im2col_u8(Ctx* c, const ObsSrc& src, int64_t R, const Dims& d, uint16_t* col);
 int k_im2col_nhwc(Ctx* c, const uint16_t* act, int64_t R, int Hi, int Wi, int Cin, int k, int s,
                   int Ho, int Wo, uint16_t* col);
-int k_col2im_delu(Ctx* c, const float* dcol, const uint16_t* aprev, int64_t R, int Hi, int Wi,
-                  int Cin, int k, int s, int Ho, int Wo, uint16_t* dz);
-// Rearranges W[co][k][k][ci] (bf16) into the sub-pixel dgrad operand
-// wt[class (py,px)][ci][(2a + b)*Co + co] = W[co][py+2a][px+2b][ci] (0 outside the kernel).
-int k_dgrad_weights(Ctx* c, const uint16_t* w, int Co, int k, int Ci, uint16_t* wt);
-// bias.out != null: also writes the bias gradient (column sums of dz)
-int k_col2im_delu_bf16(Ctx* c, const uint16_t* dcol, const uint16_t* aprev, int64_t R, int Hi,
-                       int Wi, int Cin, int k, int s, int Ho, int Wo, uint16_t* dz,
-                       const BiasOut& bias = BiasOut());
-// Column sums of contiguous bf16 [M][bias.N] into bias.out
-int k_colsum_v(Ctx* c, int64_t M, const uint16_t* src, const BiasOut& bias);
-// All operands derived from a published copy (conv1 fp16 + bias', dgrad weights), one launch
+// All operands derived from a published copy, one launch: conv1 fp16 weights +
+// offset-corrected bias (gemm.cu u8 path) and the sub-pixel dgrad operands
+// wt[class (py,px)][ci][(2a + b)*Co + co] = W[co][py+2a][px+2b][ci] (0 outside
+// the kernel) of conv2 / conv3
 int k_publish_derived(Ctx* c, const uint16_t* wb, const float* pf, const Dims& d, uint16_t* c1h,
                       float* c1b, uint16_t* wt2, uint16_t* wt3);
-// fp16 conv1 weights + offset-corrected bias of a published copy (gemm.cu u8 path)
-int k_conv1_half(Ctx* c, const float* w, const float* b, int K, uint16_t* wh, float* bh);
 int k_f32_to_bf16(Ctx* c, int64_t rows, const float* src, int64_t src_ld, uint16_t* dst,
                   int64_t dst_ld, int cols);
 int k_gru_infer(Ctx* c, int B, int A, const float* gi, const float* gh, const float* h_in,
@@ -70,8 +60,6 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
                const int32_t* act, const float* blogp, const float* adv, const float* vt,
                const LossHP& hp, float* dlog, uint16_t* dhead, double* stats, const int64_t* ver,
                int64_t cur);
-int k_heads_bwd(Ctx* c, int B, int A, const float* dlog, const float* wpi, const float* wv,
-                float* dcore);
 // dcore + head weight / bias gradients (fp32, deterministic) in one launch;
 // part: >= 148 * (A+1) * 513 floats of workspace
 int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core,
@@ -81,9 +69,6 @@ int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_
               const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh);
 int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, float* part,
              float* out, bool accumulate);
-int k_head_grad_scatter(Ctx* c, int A, const float* headw, const float* bias_sums, float* gwpi,
-                        float* gbpi, float* gwv, float* gbv);
-int k_lag(Ctx* c, int B, const int64_t* ver, int64_t cur, double* stats);
 
 // persistent GRU recurrence (gru_seq.cu)
 int gru_seq_supported(int n_traj);

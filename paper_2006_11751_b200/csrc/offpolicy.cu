@@ -2,8 +2,8 @@
 //
 // V-trace / n-step / GAE are the same backward linear recurrence
 //   a_t = delta_t + k_t * a_{t+1},   a_T = terminal
-// (offpolicy.hpp:161-176 for V-trace with a = v - V, k = disc*c;
-//  offpolicy.hpp:185-190 for n-step with a = ret, k = disc, terminal = boot;
+// (offpolicy.hpp:83-98 for V-trace with a = v - V, k = disc*c;
+//  offpolicy.hpp:107-113 for n-step with a = ret, k = disc, terminal = boot;
 //  GAE with k = disc*lambda).  One warp owns one trajectory: each lane composes
 // the affine maps of its ceil(T/32) consecutive steps, a 5-step shuffle scan
 // composes the lanes right-to-left, and a second pass over the lane's chunk
@@ -41,7 +41,7 @@ __device__ __forceinline__ void step_coeffs(const ReturnsArgs& a, const float* r
   disc = d[t] ? 0.0f : a.gamma;
   if (MODE == kVTrace) {
     float lr = tl[t] - bl[t];
-    lr = fminf(fmaxf(lr, -20.0f), 20.0f);  // importance_ratio clamp, offpolicy.hpp:126-132
+    lr = fminf(fmaxf(lr, -20.0f), 20.0f);  // importance_ratio clamp, offpolicy.hpp:50-54
     const float ratio = expf(lr);
     rho = fminf(a.rho_bar, ratio);
     c = fminf(a.c_bar, ratio);
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) returns_kernel(ReturnsArgs a) {
   const int t0 = min(lane * per, T);
   const int t1 = min(t0 + per, T);
 
-  // validation (offpolicy.hpp:148-153): non-finite inputs -> NumericError
+  // validation (offpolicy.hpp:70-75): non-finite inputs -> NumericError
   if (MODE == kVTrace) {
     bool bad = !finitef(boot);
     for (int t = t0; t < t1; ++t)
@@ -188,7 +188,7 @@ __device__ __forceinline__ bool block_reduce_last(double (&acc)[NV], double* par
   return threadIdx.x == 0;
 }
 
-// total_loss (offpolicy.hpp:224-246): out = {policy, value, entropy, total}
+// total_loss (offpolicy.hpp:146-168): out = {policy, value, entropy, total}
 __global__ void __launch_bounds__(256)
     total_loss_kernel(int n, const float* __restrict__ ratios, const float* __restrict__ adv,
                       const float* __restrict__ values, const float* __restrict__ vt,

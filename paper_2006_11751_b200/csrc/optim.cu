@@ -15,8 +15,11 @@ namespace {
 
 __global__ void __launch_bounds__(256)
     sumsq_kernel(int64_t n, const float* __restrict__ g, double* partials, unsigned* counter,
-                 double* norm_out, float clip, int* flags) {
+                 double* norm_out, float clip, int* flags, const int* peer_flags) {
   APPO_PDL_ENTRY();
+  // data-parallel: adopt the other ranks' rejection flags (read by adam_kernel)
+  if (peer_flags && blockIdx.x == 0 && threadIdx.x < kNumFlags && peer_flags[threadIdx.x])
+    atomicOr(flags + threadIdx.x, peer_flags[threadIdx.x]);
   double acc = 0.0;
   bool bad = false;
   const int64_t n4 = (reinterpret_cast<uintptr_t>(g) & 15) ? 0 : (n >> 2);
@@ -122,12 +125,12 @@ const void* kanchor_optim() { return reinterpret_cast<const void*>(&sumsq_kernel
 
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
-                uint16_t* bf16_copy, float* f32_copy, unsigned* applied) {
+                uint16_t* bf16_copy, float* f32_copy, unsigned* applied, const int* peer_flags) {
   if (n == 0) return APPO_OK;
   const int grid = 148 * 4;  // partials fit kRedSlots; enough loads in flight for HBM
   c->next_bytes = (double)n * 4;
   APPO_LAUNCH(c, sumsq_kernel, grid, 256, 0, n, g, c->d_red, c->d_counter + 1, d_norm_out, clip,
-              c->d_flags);
+              c->d_flags, peer_flags);
   const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
   const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
   const int grid2 = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);

@@ -128,7 +128,10 @@ int pbt_step_impl(appo_pbt* s, const double* scores, const uint8_t* has, int64_t
     }
     const uint32_t src_rank = (uint32_t)(s->rng() % n_top);
     const appo_agent_meta src = s->agents[ranked[src_rank]];
-    if (cb.fn) {
+    // replace_fraction > 0.5 lets the top cohort overlap the replaced one, so
+    // src may be dst: the reference's copy_weights is then a harmless
+    // self-copy and the exchange is still logged -- no callback here
+    if (cb.fn && src.policy_id != a.policy_id) {
       const int st = cb.fn(cb.user, a.policy_id, src.policy_id);
       if (st != APPO_OK) return st;
     }
@@ -284,6 +287,7 @@ int appo_pbt_format_events(const appo_pbt_event* ev, int n, int header, char* bu
 // copy_weights over an array of learner contexts: user = appo_ctx*[P]
 int appo_pbt_copy_contexts(void* user, uint32_t dst, uint32_t src) {
   appo_ctx** learners = static_cast<appo_ctx**>(user);
+  if (dst == src || learners[dst] == learners[src]) return APPO_OK;  // self-copy: no-op
   return appo_params_copy(learners[dst], learners[src]);
 }
 

@@ -91,7 +91,7 @@ def main():
         RET[i] = ref.nstep_returns(x["rewards"], x["bootstrap"], x["dones"], 0.99)
     np.savez(os.path.join(HERE, "vtrace_c1.npz"), **pk, v=V, pg_adv=PG, nstep=RET)
 
-    # 4. PPO clip + total loss (offpolicy.hpp:195-246), numpy inputs seed 41
+    # 4. PPO clip + total loss (offpolicy.hpp:117-168), numpy inputs seed 41
     rs = np.random.default_rng(41)
     ratio = rs.uniform(0.01, 5.0, 10000)
     A = rs.uniform(-3.0, 3.0, 10000)
@@ -149,7 +149,7 @@ def main():
     #    compute_gradients with injected logits and values (policy.hpp:302-428,
     #    ref_shim.cpp ref_ppo_grads_injected): fp32-representable inputs, 6
     #    actions, a few samples beyond the +-20 log-ratio clamp
-    #    (offpolicy.hpp:48-54) and several right at the clip bounds.
+    #    (offpolicy.hpp:48-54).
     rs = np.random.default_rng(77)
     n, A = 1024, 6
     lg = rs.normal(scale=1.5, size=(n, A)).astype(np.float32).astype(np.float64)

@@ -1,12 +1,15 @@
 """Multi-process (gloo, world_size 2, CPU) checks of the data-parallel learner's
 host logic, with the fp64 oracle standing in for the device gradient:
 
-  * parity mode: two ranks each take half of the trajectories, average their
-    per-shard gradients with an all-reduce (what appo_learner_step does with
-    ncclAllReduce(avg) before clip + Adam) and apply the same Adam step; both
-    replicas must end bit-identical and equal to the single-process full-batch
-    step (the reference's 1/B mean, policy.hpp:318, makes the average of equal
-    shard means the full mean);
+  * parity mode: two ranks each take half of the trajectories and average
+    their per-shard gradients bucket by bucket in the order the product
+    library plans them (appo_dp_bucket_plan, host code of libappo_b200.so --
+    what appo_learner_step does with ncclAllReduce(avg) on its side stream
+    before clip + Adam), together with the max-reduction of the rejection
+    flags, then apply the same Adam step; both replicas must end bit-identical
+    and equal to the single-process full-batch step (the reference's 1/B mean,
+    policy.hpp:318, makes the average of equal shard means the full mean);
+  * a step rejected on one rank is rejected on both (flag consensus);
   * the NCCL unique-id broadcast helper used by paper_2006_11751_b200.dp_init;
   * bench.py's max-over-ranks timing reduction.
 """
@@ -62,9 +65,17 @@ def worker(rank, world, port, q):
         orc, theta, obs, h0, act, blogp, rew, dn = make_batch()
         per = N_TRAJ // world
         g = shard_grad(orc, theta, obs, h0, act, blogp, rew, dn, rank * per, (rank + 1) * per)
+        import paper_2006_11751_b200 as appo
+        plan = appo.dp_bucket_plan(appo.ModelDesc(*SHAPE, T))
         gt = torch.from_numpy(g)
-        dist.all_reduce(gt, op=dist.ReduceOp.SUM)
-        gt /= world
+        for off, n in plan:  # reverse layer order, as the learner launches them
+            b = gt[off:off + n]
+            dist.all_reduce(b, op=dist.ReduceOp.SUM)
+            b /= world
+        # rejection consensus: rank 1 flags a contract error on its shard
+        flags = torch.tensor([0, 1 if rank == 1 else 0, 0, 0], dtype=torch.int32)
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+        assert flags.tolist() == [0, 1, 0, 0]
         th = theta.copy()
         m = np.zeros_like(th)
         v = np.zeros_like(th)

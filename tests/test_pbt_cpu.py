@@ -111,3 +111,23 @@ def test_hparams_and_config_validation():
         appo.PbtController(appo.PbtConfig.defaults(mutation_factor=1.0), 2, 1)
     with pytest.raises(appo.ConfigError):
         appo.PbtController(appo.PbtConfig.defaults(replace_fraction=1.5), 2, 1)
+
+
+def test_overlapping_cohorts_self_exchange_is_logged_not_copied():
+    # replace_fraction > 0.5: the top cohort overlaps the replaced one, so a
+    # policy can draw itself as the source; the reference's copy_weights is
+    # then a harmless self-copy and the exchange is still logged
+    calls = []
+
+    def copy(d, s):
+        assert d != s, "self-copy must not reach copy_weights"
+        calls.append((d, s))
+
+    cfg = appo.PbtConfig.defaults(replace_fraction=0.8)
+    pbt = appo.PbtController(cfg, 4, 11, copy_weights=copy)
+    events = []
+    for period in range(60):
+        events += pbt.step(synthetic_scores(4, period), period)
+    ex = [(e.agent, int(e.old_value)) for e in events if e.as_tuple()[2] == "exchange"]
+    assert any(d == s for d, s in ex)
+    assert calls == [(d, s) for d, s in ex if d != s] and calls
