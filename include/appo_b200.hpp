@@ -1,27 +1,44 @@
 // appo_b200.hpp -- header-only C++ host mirror of the reference's hot-path API
 // over the C ABI (appo_capi.h).  A host that used
-//   appo::vtrace / appo::nstep_returns / appo::total_loss   (offpolicy.hpp)
-//   appo::log_prob_and_entropy / appo::optimizer_step        (policy.hpp)
-//   PolicyWorkerUnit::run_once / LearnerUnit::step            (orchestrator.hpp)
-// switches to the same names in namespace appo_b200, with std::span arguments,
-// the same output structs and the same exception taxonomy (ContractError /
-// ConfigError / NumericError, common.hpp:20-45).  Host-span overloads stage
-// through device memory (the reference-facing e2e path); device-pointer
-// overloads are the zero-copy path.
+//   appo::vtrace / appo::nstep_returns / appo::total_loss          (offpolicy.hpp)
+//   appo::sample_action / appo::log_prob_and_entropy /
+//   appo::optimizer_step                                           (policy.hpp)
+//   PolicyWorkerUnit::run_once / LearnerUnit::step                 (orchestrator.hpp)
+// switches to the same names in namespace appo_b200, with the same std::span
+// arguments and output structs, and the same exceptions: when the reference's
+// <appo/common.hpp> is on the include path (the drop-in case) the mirror
+// throws ::appo::ContractError / ConfigError / NumericError themselves
+// (common.hpp:20-40), so the reference's own catch sites -- e.g. the CLI's
+// exit-code mapping, tools/appo_cli.cpp:151-163 -- keep working unchanged;
+// otherwise it defines look-alike types (define APPO_B200_OWN_ERRORS to force
+// them).  Host-span overloads stage through device memory (the
+// reference-facing e2e path); device-pointer overloads are the zero-copy path.
 #pragma once
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
+#include <random>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "appo_capi.h"
 
+#if !defined(APPO_B200_OWN_ERRORS) && __has_include(<appo/common.hpp>)
+#include <appo/common.hpp>
+#define APPO_B200_REFERENCE_ERRORS 1
 namespace appo_b200 {
-
+using ContractError = ::appo::ContractError;  // common.hpp:23-26
+using ConfigError = ::appo::ConfigError;      // common.hpp:30-33
+using NumericError = ::appo::NumericError;    // common.hpp:37-40
+}  // namespace appo_b200
+#else
+#define APPO_B200_REFERENCE_ERRORS 0
+namespace appo_b200 {
 class ContractError : public std::logic_error {
  public:
   explicit ContractError(const std::string& w) : std::logic_error(w) {}
@@ -34,6 +51,14 @@ class NumericError : public std::runtime_error {
  public:
   explicit NumericError(const std::string& w) : std::runtime_error(w) {}
 };
+}  // namespace appo_b200
+#endif
+
+namespace appo_b200 {
+
+// CUDA / allocation failures.  The reference has no type of its own for these
+// (std::bad_alloc / std::runtime_error); the CLI's catch-all maps them to
+// kExitResource (appo_cli.cpp:157-163, runner.hpp:28-33).
 class ResourceError : public std::runtime_error {
  public:
   explicit ResourceError(const std::string& w) : std::runtime_error(w) {}
@@ -49,6 +74,36 @@ inline void check(int st) {
     default: throw ResourceError(m);
   }
 }
+
+// ActionHeadsSpec / FactoredAction (policy.hpp:25-37)
+struct ActionHeadsSpec {
+  std::vector<int> sizes;
+  int n_heads() const { return static_cast<int>(sizes.size()); }
+  int logits_dim() const {
+    int d = 0;
+    for (int s : sizes) d += s;
+    return d;
+  }
+};
+using FactoredAction = std::vector<std::int32_t>;
+
+// AdamConfig / AdamState / PolicyParams' optimizer fields (policy.hpp:88-105)
+struct AdamConfig {
+  double lr = 1e-4;
+  double beta1 = 0.9;
+  double beta2 = 0.999;
+  double eps = 1e-6;
+  double grad_clip = 4.0;  // global-norm threshold, 0 disables
+};
+struct AdamState {
+  std::vector<double> m, v;
+  std::int64_t t = 0;
+};
+struct PolicyParams {
+  std::vector<double> theta;  // flat parameter vector
+  std::int64_t version = 0;   // SGD-step counter
+  AdamState adam;
+};
 
 // offpolicy.hpp:18-45 defaults
 struct VTraceConfig {
@@ -127,6 +182,103 @@ class Context {
     out.rho.assign(c.begin(), c.end());
     out.c.assign(d.begin(), d.end());
     return out;
+  }
+
+  // nstep_returns (offpolicy.hpp:104-114): one trajectory, host spans.
+  std::vector<double> nstep_returns(std::span<const double> rewards, double bootstrap_value,
+                                    std::span<const uint8_t> dones, double gamma) const {
+    const size_t T = rewards.size();
+    if (dones.size() != T) throw ContractError("nstep_returns inputs must share length T");
+    const std::vector<float> r(rewards.begin(), rewards.end());
+    const float boot = static_cast<float>(bootstrap_value);
+    DeviceBuffer<float> dr(T), dboot(1), dret(T);
+    DeviceBuffer<uint8_t> dd(T);
+    dr.upload(r.data()); dboot.upload(&boot); dd.upload(dones.data());
+    check(appo_nstep_returns(h_, 1, static_cast<int>(T), dr.get(), dboot.get(), dd.get(),
+                             static_cast<float>(gamma), dret.get()));
+    sync();
+    std::vector<float> o(T);
+    dret.download(o.data());
+    return std::vector<double>(o.begin(), o.end());
+  }
+
+  // sample_action (policy.hpp:232-258): one row of concatenated head logits.
+  // The device draws counter-based uniforms; one draw of the caller's
+  // mt19937_64 keys them, so a seeded rng gives a reproducible stream
+  // (test_policy.cpp:226-239) with the reference's distribution, though not
+  // the reference's individual draws.
+  std::pair<FactoredAction, double> sample_action(const ActionHeadsSpec& heads,
+                                                  std::span<const double> logits,
+                                                  std::mt19937_64& rng) const {
+    if (static_cast<int>(logits.size()) != heads.logits_dim())
+      throw ContractError("sample_action: logits size != heads.logits_dim()");
+    const std::vector<float> lg(logits.begin(), logits.end());
+    DeviceBuffer<float> dl(lg.size()), dlp(1);
+    DeviceBuffer<int32_t> da(heads.sizes.size());
+    dl.upload(lg.data());
+    sample_actions(heads, 1, dl.get(), rng(), 0, da.get(), dlp.get());
+    sync();
+    FactoredAction a(heads.sizes.size());
+    float lp = 0;
+    da.download(a.data());
+    dlp.download(&lp);
+    return {std::move(a), static_cast<double>(lp)};
+  }
+  // Batched device form: B rows, actions [B][n_heads], u = U(key, counter0 + b*n_heads + j).
+  void sample_actions(const ActionHeadsSpec& heads, int B, const float* d_logits, uint64_t key,
+                      uint64_t counter0, int32_t* d_actions, float* d_logp) const {
+    check(appo_sample_actions_heads(h_, B, heads.n_heads(), heads.sizes.data(), d_logits, key,
+                                    counter0, d_actions, d_logp));
+  }
+
+  // log_prob_and_entropy (policy.hpp:262-281): joint logp of `action`, summed
+  // per-head entropy; out-of-range actions throw ContractError.
+  std::pair<double, double> log_prob_and_entropy(const ActionHeadsSpec& heads,
+                                                 std::span<const double> logits,
+                                                 const FactoredAction& action) const {
+    if (static_cast<int>(action.size()) != heads.n_heads())
+      throw ContractError("action arity mismatch");
+    if (static_cast<int>(logits.size()) != heads.logits_dim())
+      throw ContractError("log_prob_and_entropy: logits size != heads.logits_dim()");
+    const std::vector<float> lg(logits.begin(), logits.end());
+    DeviceBuffer<float> dl(lg.size()), dlp(1), den(1);
+    DeviceBuffer<int32_t> da(action.size());
+    dl.upload(lg.data());
+    da.upload(action.data());
+    check(appo_logp_entropy_heads(h_, 1, heads.n_heads(), heads.sizes.data(), dl.get(), da.get(),
+                                  dlp.get(), den.get()));
+    sync();
+    float lp = 0, en = 0;
+    dlp.download(&lp);
+    den.download(&en);
+    return {static_cast<double>(lp), static_cast<double>(en)};
+  }
+
+  // optimizer_step (policy.hpp:431-455): global-norm clip + Adam on p (fp32 on
+  // the device), t += 1, version += 1.  A non-finite gradient throws
+  // NumericError and leaves p untouched, as the reference does.
+  void optimizer_step(PolicyParams& p, std::span<const double> grads,
+                      const AdamConfig& cfg) const {
+    const size_t n = p.theta.size();
+    if (grads.size() != n) throw ContractError("gradient size mismatch");
+    if (p.adam.m.size() != n) p.adam.m.assign(n, 0.0);
+    if (p.adam.v.size() != n) p.adam.v.assign(n, 0.0);
+    auto f = [](const std::vector<double>& x) { return std::vector<float>(x.begin(), x.end()); };
+    std::vector<float> th = f(p.theta), m = f(p.adam.m), v = f(p.adam.v);
+    const std::vector<float> g(grads.begin(), grads.end());
+    DeviceBuffer<float> dth(n), dm(n), dv(n), dg(n);
+    dth.upload(th.data()); dm.upload(m.data()); dv.upload(v.data()); dg.upload(g.data());
+    double norm = 0;
+    check(appo_adam_step(h_, static_cast<int64_t>(n), dth.get(), dm.get(), dv.get(), dg.get(),
+                         p.adam.t + 1, static_cast<float>(cfg.lr), static_cast<float>(cfg.beta1),
+                         static_cast<float>(cfg.beta2), static_cast<float>(cfg.eps),
+                         static_cast<float>(cfg.grad_clip), &norm));
+    dth.download(th.data()); dm.download(m.data()); dv.download(v.data());
+    p.theta.assign(th.begin(), th.end());
+    p.adam.m.assign(m.begin(), m.end());
+    p.adam.v.assign(v.begin(), v.end());
+    p.adam.t += 1;
+    p.version += 1;
   }
 
   // Batched device form: [n_traj x T] row-major, the learner gather order.

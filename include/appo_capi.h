@@ -151,6 +151,19 @@ APPO_API int appo_logp_entropy(appo_ctx* ctx, int B, int n_actions, const float*
  * u_b = U(key, counter0 + b).  Writes action and joint log-prob. */
 APPO_API int appo_sample_actions(appo_ctx* ctx, int B, int n_actions, const float* d_logits, uint64_t key,
                         uint64_t counter0, int32_t* d_actions, float* d_logp);
+/* Factored action spaces (ActionHeadsSpec{sizes}, policy.hpp:25-35): n_heads
+ * (1..8) independent categorical heads of h_sizes[j] (1..64) actions; a
+ * logits row is the heads concatenated (logits_dim = sum of sizes), actions
+ * are [B][n_heads].  log_prob_and_entropy (policy.hpp:262-281): joint logp =
+ * sum over heads, entropy = sum of per-head entropies.  sample_action
+ * (policy.hpp:232-258): one uniform per (row b, head j), U(key, counter0 +
+ * b*n_heads + j), so n_heads = 1 equals the single-head calls above. */
+APPO_API int appo_logp_entropy_heads(appo_ctx* ctx, int B, int n_heads, const int32_t* h_sizes,
+                                     const float* d_logits, const int32_t* d_actions,
+                                     float* d_logp_out, float* d_entropy_out);
+APPO_API int appo_sample_actions_heads(appo_ctx* ctx, int B, int n_heads, const int32_t* h_sizes,
+                                       const float* d_logits, uint64_t key, uint64_t counter0,
+                                       int32_t* d_actions, float* d_logp);
 
 /* ---- optimizer (policy.hpp:431-455) -------------------------------------- */
 /* Global-norm clip + Adam over flat fp32 vectors, step t (1-based, after the
@@ -261,6 +274,31 @@ APPO_API int appo_sampler_destroy(appo_sampler* s);
 APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_bytes,
                                int32_t slot_base, int t, const uint8_t* h_obs,
                                int32_t* h_actions);
+
+/* CPU actors (the paper's setting): RolloutWorker::submit_group + step_group
+ * (orchestrator.hpp:435-552) in two calls per env step t of the rollout into
+ * slots [slot_base, slot_base + n_envs), strictly in the order act(0),
+ * feedback(0), act(1), ... feedback(T-1) (write_step's ordering contract,
+ * trajstore.hpp:172-174: anything else is a contract error).
+ *   act: h_obs [n_envs][obs_dim] (pinned host memory for an asynchronous
+ *     copy; it must stay unchanged until appo_rollout_wait returns) becomes
+ *     slot row t's obs; batched inference on it with the sampler's per-env
+ *     hidden state writes row t's input hidden, action, behaviour logp and
+ *     policy version (the exchange-row reply, :512-521); the actions are
+ *     copied to h_actions (optional), valid once appo_rollout_wait returns.
+ *   feedback: the env transition's h_rewards f32 [n_envs] and h_dones u8
+ *     [n_envs] (copied before the call returns) become row t's reward / done;
+ *     hidden <- h' (zero after done, reset_env :402); at t == T-1 h_next_obs
+ *     [n_envs][obs_dim] is REQUIRED -- the bootstrap obs (set_bootstrap,
+ *     :529-534; valid until the next appo_rollout_wait) with bootstrap hidden
+ *     h', the header is sealed and the slots go to the ready queue (if set).
+ * Asynchronous on the ctx stream. */
+APPO_API int appo_rollout_act(appo_sampler* s, void* d_region, uint64_t slot_bytes,
+                              int32_t slot_base, int t, const uint8_t* h_obs, int32_t* h_actions);
+APPO_API int appo_rollout_wait(appo_sampler* s);
+APPO_API int appo_rollout_feedback(appo_sampler* s, void* d_region, uint64_t slot_bytes,
+                                   int32_t slot_base, int t, const float* h_rewards,
+                                   const uint8_t* h_dones, const uint8_t* h_next_obs);
 
 /* ---- device slot queues: ready queue + free list ------------------------- */
 /* Replaces the host BoundedFifo ready_q drained by assemble_minibatch

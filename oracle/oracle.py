@@ -315,6 +315,40 @@ class Reference:
                                       C.byref(mr))
         return st, dict(dlogits=dl, dv=dv, loss=loss, mean_ratio=mr.value)
 
+    def logp_entropy_heads(self, sizes, logits, actions):
+        """log_prob_and_entropy (policy.hpp:262-281) over factored heads."""
+        sz = _c(sizes, np.int32)
+        lg = _c(logits, np.float64)
+        B = lg.shape[0]
+        act = _c(actions, np.int32)
+        lp = np.zeros(B); en = np.zeros(B)
+        L = self.L
+        L.ref_log_prob_entropy_heads.restype = C.c_int
+        L.ref_log_prob_entropy_heads.argtypes = [C.c_int, _i32p, C.c_int, _dp, _i32p, _dp, _dp]
+        st = L.ref_log_prob_entropy_heads(len(sz), sz, B, lg, act, lp, en)
+        return st, lp, en
+
+    def dump_trajectory(self, path, obs, hidden, actions, rewards, logp, dones, versions,
+                        boot_obs, boot_hidden, env=0, worker=0, policy=0):
+        """dump_trajectory (trajstore.hpp:335-359) of a slot the reference itself
+        filled with begin / write_step / set_bootstrap (ref_shim.cpp); returns
+        the guarded status (0 ok, 1 contract, 3 numeric)."""
+        obs = _c(obs, np.float64)
+        T, od = obs.shape
+        hid = _c(hidden, np.float64)
+        L = self.L
+        L.ref_dump_trajectory.restype = C.c_int
+        L.ref_dump_trajectory.argtypes = [C.c_uint32] * 3 + [_dp, _dp, _i32p, _dp, _dp, _u8p,
+                                          C.POINTER(C.c_int64), _dp, _dp] + \
+            [C.c_uint32] * 3 + [C.c_char_p]
+        ver = _c(versions, np.int64)
+        return int(L.ref_dump_trajectory(T, od, hid.shape[1], obs, hid, _c(actions, np.int32),
+                                         _c(rewards, np.float64), _c(logp, np.float64),
+                                         _c(dones, np.uint8),
+                                         ver.ctypes.data_as(C.POINTER(C.c_int64)),
+                                         _c(boot_obs, np.float64), _c(boot_hidden, np.float64),
+                                         env, worker, policy, os.fsencode(path)))
+
     @staticmethod
     def available(path: str = REF_LIB) -> bool:
         return os.path.exists(path)

@@ -124,6 +124,23 @@ int ref_log_prob_entropy(int n, const double* logits, int action, double* logp, 
   });
 }
 
+// policy.hpp:262 log_prob_and_entropy over factored heads {sizes[0..n_heads)}:
+// B rows of logits [B][logits_dim] and actions [B][n_heads]
+int ref_log_prob_entropy_heads(int n_heads, const int* sizes, int B, const double* logits,
+                               const int* actions, double* logp, double* ent) {
+  return guarded([&] {
+    ActionHeadsSpec h;
+    h.sizes.assign(sizes, sizes + n_heads);
+    const int ld = h.logits_dim();
+    for (int b = 0; b < B; ++b) {
+      FactoredAction a(actions + (size_t)b * n_heads, actions + (size_t)(b + 1) * n_heads);
+      auto [lp, e] = log_prob_and_entropy(h, {logits + (size_t)b * ld, (size_t)ld}, a);
+      logp[b] = lp;
+      ent[b] = e;
+    }
+  });
+}
+
 // policy.hpp:232 sample_action, `count` draws from one mt19937_64(seed)
 void ref_sample_actions(int n, const double* logits, std::uint64_t seed, int count, int* actions,
                         double* logps) {
@@ -320,6 +337,38 @@ long ref_pbt_log(int P, std::uint64_t seed, int periods, double threshold, char*
   if (t.size() + 1 > cap) return -1;
   std::memcpy(buf, t.c_str(), t.size() + 1);
   return static_cast<long>(t.size());
+}
+
+// dump_trajectory (trajstore.hpp:335-359) of one slot filled through the
+// reference's own TrajectorySlotView::begin / write_step / set_bootstrap
+// (trajstore.hpp:100-215) from the given arrays; n_heads = 1.  Returns the
+// guarded status (the write_step contracts apply).
+int ref_dump_trajectory(std::uint32_t T, std::uint32_t obs_dim, std::uint32_t hidden_dim,
+                        const double* obs, const double* hidden, const std::int32_t* actions,
+                        const double* rewards, const double* logp, const std::uint8_t* dones,
+                        const std::int64_t* versions, const double* boot_obs,
+                        const double* boot_hidden, std::uint32_t env, std::uint32_t worker,
+                        std::uint32_t policy, const char* path) {
+  return guarded([&] {
+    TrajectoryStore store(TrajectoryShape{T, obs_dim, hidden_dim, 1}, 1);
+    auto v = store.view(0);
+    v.begin(env, worker, policy, 0);
+    for (std::uint32_t t = 0; t < T; ++t) {
+      StepRecord rec;
+      rec.obs.assign(obs + std::size_t{t} * obs_dim, obs + std::size_t{t + 1} * obs_dim);
+      rec.hidden.assign(hidden + std::size_t{t} * hidden_dim,
+                        hidden + std::size_t{t + 1} * hidden_dim);
+      rec.action = {actions[t]};
+      rec.reward = rewards[t];
+      rec.behavior_logp = logp[t];
+      rec.done = dones[t] != 0;
+      rec.policy_version = versions[t];
+      v.write_step(t, rec);
+    }
+    v.set_bootstrap(std::span<const double>(boot_obs, obs_dim),
+                    std::span<const double>(boot_hidden, hidden_dim));
+    dump_trajectory(v, path);
+  });
 }
 
 }  // extern "C"

@@ -168,6 +168,8 @@ _sig("appo_total_loss", _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _f,
      C.POINTER(C.c_double))
 _sig("appo_logp_entropy", _i, _vp, _i, _i, _vp, _vp, _vp, _vp)
 _sig("appo_sample_actions", _i, _vp, _i, _i, _vp, _u64, _u64, _vp, _vp)
+_sig("appo_logp_entropy_heads", _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp)
+_sig("appo_sample_actions_heads", _i, _vp, _i, _i, _vp, _vp, _u64, _u64, _vp, _vp)
 _sig("appo_adam_step", _i, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _f, _f, _f, _f, _f,
      C.POINTER(C.c_double))
 _sig("appo_param_count", _i64, C.POINTER(ModelDesc))
@@ -195,6 +197,9 @@ _sig("appo_sampler_create", _i, _vp, _i, _i, _u64, C.POINTER(_vp))
 _sig("appo_sampler_destroy", _i, _vp)
 _sig("appo_sampler_step", _i, _vp, _vp, _u64, C.c_int32, _i, _vp, _vp)
 _sig("appo_sampler_set_ready_queue", _i, _vp, _vp)
+_sig("appo_rollout_act", _i, _vp, _vp, _u64, C.c_int32, _i, _vp, _vp)
+_sig("appo_rollout_wait", _i, _vp)
+_sig("appo_rollout_feedback", _i, _vp, _vp, _u64, C.c_int32, _i, _vp, _vp, _vp)
 _sig("appo_slotq_create", _i, _i, C.c_int32, C.c_int32, C.c_double, C.POINTER(_vp))
 _sig("appo_slotq_destroy", _i, _vp)
 _sig("appo_slotq_push", _i, _vp, _vp, _vp, _i)
@@ -378,6 +383,34 @@ class Context:
         if sync:
             self.sync()
         return lp, en
+
+    def log_prob_and_entropy_heads(self, sizes, logits, actions, sync=True):
+        """log_prob_and_entropy (policy.hpp:262-281) over factored heads
+        ``sizes``: logits [B][sum(sizes)], actions int32 [B][n_heads]."""
+        _need_cuda(logits, actions)
+        sz = (C.c_int32 * len(sizes))(*sizes)
+        B = logits.shape[0]
+        lp = self.torch.empty(B, device=logits.device, dtype=self.torch.float32)
+        en = self.torch.empty_like(lp)
+        check(_L.appo_logp_entropy_heads(self.h, B, len(sizes), sz, _ptr(logits), _ptr(actions),
+                                         _ptr(lp), _ptr(en)))
+        if sync:
+            self.sync()
+        return lp, en
+
+    def sample_actions_heads(self, sizes, logits, key, counter0=0, sync=True):
+        """sample_action (policy.hpp:232-258) over factored heads: actions
+        [B][n_heads], joint log-prob [B]; u(b, j) = U(key, counter0 + b*n + j)."""
+        _need_cuda(logits)
+        sz = (C.c_int32 * len(sizes))(*sizes)
+        B = logits.shape[0]
+        a = self.torch.empty((B, len(sizes)), device=logits.device, dtype=self.torch.int32)
+        lp = self.torch.empty(B, device=logits.device, dtype=self.torch.float32)
+        check(_L.appo_sample_actions_heads(self.h, B, len(sizes), sz, _ptr(logits), key, counter0,
+                                           _ptr(a), _ptr(lp)))
+        if sync:
+            self.sync()
+        return a, lp
 
     def sample_actions(self, logits, key, counter0=0, sync=True):
         _need_cuda(logits)
@@ -615,6 +648,30 @@ class Sampler:
         """h_obs / h_actions: optional pinned host tensors (CPU-actor path)."""
         check(_L.appo_sampler_step(self.h, _ptr(store.region), store.slot_bytes, slot_base, t,
                                    _ptr(h_obs), _ptr(h_actions)))
+
+    # ---- CPU actors: RolloutWorker::submit_group / step_group (two phases) ----
+    def act(self, store, slot_base: int, t: int, h_obs, h_actions=None):
+        """Step t's observations (host tensor [n_envs][obs_dim], pinned for an
+        asynchronous copy) -> slot row t + batched inference; sampled actions
+        into ``h_actions`` (host int32 [n_envs]), valid after ``wait()``."""
+        if h_obs is None or h_obs.is_cuda:
+            raise ContractError("rollout act: host observations required")
+        check(_L.appo_rollout_act(self.h, _ptr(store.region), store.slot_bytes, slot_base, t,
+                                  _ptr(h_obs), _ptr(h_actions)))
+
+    def wait(self):
+        """Blocks until the last act's actions are on the host and the caller's
+        observation buffers are no longer read."""
+        check(_L.appo_rollout_wait(self.h))
+
+    def feedback(self, store, slot_base: int, t: int, h_rewards, h_dones, h_next_obs=None):
+        """The env transition of step t: rewards (f32) and dones (u8) [n_envs]
+        from host memory; at t == T-1 also the next observations (bootstrap)."""
+        for x in (h_rewards, h_dones, h_next_obs):
+            if x is not None and x.is_cuda:
+                raise ContractError("rollout feedback: host tensors required")
+        check(_L.appo_rollout_feedback(self.h, _ptr(store.region), store.slot_bytes, slot_base, t,
+                                       _ptr(h_rewards), _ptr(h_dones), _ptr(h_next_obs)))
 
     def set_ready_queue(self, q: "SlotQueue | None"):
         """After step T-1 of a rollout the written slots are pushed to ``q``."""

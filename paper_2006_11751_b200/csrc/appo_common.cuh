@@ -219,10 +219,17 @@ int launch_gae(Ctx* c, int n_traj, int T, const float* r, const float* v, const 
 int launch_total_loss(Ctx* c, int n, const float* ratios, const float* adv, const float* values,
                       const float* vt, const float* ent, float lo, float hi, float vc, float ec,
                       double* d_out4);
-int launch_logp_entropy(Ctx* c, int B, int A, const float* logits, const int32_t* actions,
-                        float* logp, float* ent);
-int launch_sample(Ctx* c, int B, int A, const float* logits, uint64_t key, uint64_t counter0,
-                  int32_t* actions, float* logp);
+// Factored action heads (ActionHeadsSpec, policy.hpp:25-35): head j's logits
+// are columns [off[j], off[j+1]) of a row; off[n] = logits_dim.
+constexpr int kMaxHeads = 8;
+struct HeadsSpec {
+  int n;
+  int off[kMaxHeads + 1];
+};
+int launch_logp_entropy(Ctx* c, int B, const HeadsSpec& hs, const float* logits,
+                        const int32_t* actions, float* logp, float* ent);
+int launch_sample(Ctx* c, int B, const HeadsSpec& hs, const float* logits, uint64_t key,
+                  uint64_t counter0, int32_t* actions, float* logp);
 // peer_flags (data-parallel): the ranks' max-reduced rejection flags, folded
 // into c's flags before the update so every rank accepts or rejects together
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,

@@ -292,18 +292,50 @@ int appo_total_loss(appo_ctx* ctx, int n, const float* ratios, const float* adv,
   return st;
 }
 
+namespace {
+// ActionHeadsSpec validation: 1..kMaxHeads heads of 1..64 actions each
+int make_heads(int n_heads, const int32_t* sizes, HeadsSpec* hs) {
+  APPO_REQUIRE(n_heads >= 1 && n_heads <= kMaxHeads && sizes != nullptr, APPO_ERR_CONTRACT,
+               "action heads: need 1..8 heads");
+  hs->n = n_heads;
+  hs->off[0] = 0;
+  for (int j = 0; j < n_heads; ++j) {
+    APPO_REQUIRE(sizes[j] >= 1 && sizes[j] <= 64, APPO_ERR_CONTRACT,
+                 "action heads: head size must be in [1, 64]");
+    hs->off[j + 1] = hs->off[j] + sizes[j];
+  }
+  return APPO_OK;
+}
+}  // namespace
+
 int appo_logp_entropy(appo_ctx* ctx, int B, int A, const float* logits, const int32_t* actions,
                       float* logp, float* ent) {
-  CTX_OR_RETURN(ctx);
-  APPO_REQUIRE(B >= 0 && A >= 1 && A <= 64, APPO_ERR_CONTRACT, "logp_entropy: bad shape");
-  return launch_logp_entropy(ctx, B, A, logits, actions, logp, ent);
+  return appo_logp_entropy_heads(ctx, B, 1, &A, logits, actions, logp, ent);
 }
 
 int appo_sample_actions(appo_ctx* ctx, int B, int A, const float* logits, uint64_t key,
                         uint64_t counter0, int32_t* actions, float* logp) {
+  return appo_sample_actions_heads(ctx, B, 1, &A, logits, key, counter0, actions, logp);
+}
+
+int appo_logp_entropy_heads(appo_ctx* ctx, int B, int n_heads, const int32_t* h_sizes,
+                            const float* logits, const int32_t* actions, float* logp,
+                            float* ent) {
   CTX_OR_RETURN(ctx);
-  APPO_REQUIRE(B >= 0 && A >= 1 && A <= 64, APPO_ERR_CONTRACT, "sample: bad shape");
-  return launch_sample(ctx, B, A, logits, key, counter0, actions, logp);
+  APPO_REQUIRE(B >= 0, APPO_ERR_CONTRACT, "logp_entropy: bad shape");
+  HeadsSpec hs;
+  if (int st = make_heads(n_heads, h_sizes, &hs)) return st;
+  return launch_logp_entropy(ctx, B, hs, logits, actions, logp, ent);
+}
+
+int appo_sample_actions_heads(appo_ctx* ctx, int B, int n_heads, const int32_t* h_sizes,
+                              const float* logits, uint64_t key, uint64_t counter0,
+                              int32_t* actions, float* logp) {
+  CTX_OR_RETURN(ctx);
+  APPO_REQUIRE(B >= 0, APPO_ERR_CONTRACT, "sample: bad shape");
+  HeadsSpec hs;
+  if (int st = make_heads(n_heads, h_sizes, &hs)) return st;
+  return launch_sample(ctx, B, hs, logits, key, counter0, actions, logp);
 }
 
 int appo_adam_step(appo_ctx* ctx, int64_t n, float* theta, float* m, float* v, const float* g,

@@ -215,57 +215,75 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// log_prob_and_entropy (policy.hpp:262-281), single head of A actions.
-__global__ void logp_entropy_kernel(int B, int A, const float* __restrict__ logits,
+// Stable softmax statistics of one head's logits [n]: max and partition sum
+// (softmax_heads, policy.hpp:210-228).
+__device__ __forceinline__ void head_softmax(const float* lg, int n, double& mx, double& z) {
+  mx = lg[0];
+  for (int i = 1; i < n; ++i) mx = fmax(mx, (double)lg[i]);
+  z = 0;
+  for (int i = 0; i < n; ++i) z += exp((double)lg[i] - mx);
+}
+
+// log_prob_and_entropy (policy.hpp:262-281) over factored heads: joint logp of
+// the stored action [B][n_heads] = sum of per-head log max(p, 1e-300); entropy =
+// sum of per-head entropies.  Logits row = concatenated heads.
+__global__ void logp_entropy_kernel(int B, HeadsSpec hs, const float* __restrict__ logits,
                                     const int32_t* __restrict__ actions, float* logp, float* ent,
                                     int* flags) {
   APPO_PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const float* lg = logits + (size_t)b * A;
-  const int act = actions[b];
-  if (act < 0 || act >= A) {
-    atomicOr(flags + kFlagContract, 1);
-    return;
+  const int ld = hs.off[hs.n];
+  double lp = 0, h = 0;
+  for (int j = 0; j < hs.n; ++j) {
+    const int n = hs.off[j + 1] - hs.off[j];
+    const float* lg = logits + (size_t)b * ld + hs.off[j];
+    const int act = actions[(size_t)b * hs.n + j];
+    if (act < 0 || act >= n) {  // APPO_CHECK "action index out of range for head"
+      atomicOr(flags + kFlagContract, 1);
+      return;
+    }
+    double mx, z;
+    head_softmax(lg, n, mx, z);
+    for (int i = 0; i < n; ++i) {
+      const double p = exp((double)lg[i] - mx) / z;
+      if (p > 0) h -= p * log(p);
+    }
+    lp += log(fmax(exp((double)lg[act] - mx) / z, 1e-300));
   }
-  double mx = lg[0];
-  for (int i = 1; i < A; ++i) mx = fmax(mx, (double)lg[i]);
-  double z = 0;
-  for (int i = 0; i < A; ++i) z += exp((double)lg[i] - mx);
-  double h = 0;
-  for (int i = 0; i < A; ++i) {
-    const double p = exp((double)lg[i] - mx) / z;
-    if (p > 0) h -= p * log(p);
-  }
-  const double pa = exp((double)lg[act] - mx) / z;
-  logp[b] = (float)log(fmax(pa, 1e-300));
+  logp[b] = (float)lp;
   ent[b] = (float)h;
 }
 
-// sample_action (policy.hpp:232-258): inverse CDF with first i where u < cum,
-// fallback A-1, joint logp = log(max(p, 1e-300)); u is counter-based.
-__global__ void sample_kernel(int B, int A, const float* __restrict__ logits, uint64_t key,
+// sample_action (policy.hpp:232-258): per head, inverse CDF with the first i
+// where u < cum (fallback n-1); joint logp = sum of log max(p, 1e-300).  The
+// uniform of (row b, head j) is counter-based: U(key, counter0 + b*n_heads + j).
+__global__ void sample_kernel(int B, HeadsSpec hs, const float* __restrict__ logits, uint64_t key,
                               uint64_t counter0, int32_t* actions, float* logp) {
   APPO_PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const float* lg = logits + (size_t)b * A;
-  double mx = lg[0];
-  for (int i = 1; i < A; ++i) mx = fmax(mx, (double)lg[i]);
-  double z = 0;
-  for (int i = 0; i < A; ++i) z += exp((double)lg[i] - mx);
-  const double u = uniform01(key, counter0 + (uint64_t)b);
-  double cum = 0;
-  int chosen = A - 1;
-  for (int i = 0; i < A; ++i) {
-    cum += exp((double)lg[i] - mx) / z;
-    if (u < cum) {
-      chosen = i;
-      break;
+  const int ld = hs.off[hs.n];
+  double lp = 0;
+  for (int j = 0; j < hs.n; ++j) {
+    const int n = hs.off[j + 1] - hs.off[j];
+    const float* lg = logits + (size_t)b * ld + hs.off[j];
+    double mx, z;
+    head_softmax(lg, n, mx, z);
+    const double u = uniform01(key, counter0 + (uint64_t)b * hs.n + j);
+    double cum = 0;
+    int chosen = n - 1;
+    for (int i = 0; i < n; ++i) {
+      cum += exp((double)lg[i] - mx) / z;
+      if (u < cum) {
+        chosen = i;
+        break;
+      }
     }
+    actions[(size_t)b * hs.n + j] = chosen;
+    lp += log(fmax(exp((double)lg[chosen] - mx) / z, 1e-300));
   }
-  actions[b] = chosen;
-  logp[b] = (float)log(fmax(exp((double)lg[chosen] - mx) / z, 1e-300));
+  logp[b] = (float)lp;
 }
 
 }  // namespace
@@ -303,18 +321,18 @@ int launch_total_loss(Ctx* c, int n, const float* ratios, const float* adv, cons
   return APPO_OK;
 }
 
-int launch_logp_entropy(Ctx* c, int B, int A, const float* logits, const int32_t* actions,
-                        float* logp, float* ent) {
+int launch_logp_entropy(Ctx* c, int B, const HeadsSpec& hs, const float* logits,
+                        const int32_t* actions, float* logp, float* ent) {
   if (B == 0) return APPO_OK;
-  APPO_LAUNCH(c, logp_entropy_kernel, (B + 127) / 128, 128, 0, B, A, logits, actions, logp, ent,
+  APPO_LAUNCH(c, logp_entropy_kernel, (B + 127) / 128, 128, 0, B, hs, logits, actions, logp, ent,
               c->d_flags);
   return APPO_OK;
 }
 
-int launch_sample(Ctx* c, int B, int A, const float* logits, uint64_t key, uint64_t counter0,
-                  int32_t* actions, float* logp) {
+int launch_sample(Ctx* c, int B, const HeadsSpec& hs, const float* logits, uint64_t key,
+                  uint64_t counter0, int32_t* actions, float* logp) {
   if (B == 0) return APPO_OK;
-  APPO_LAUNCH(c, sample_kernel, (B + 127) / 128, 128, 0, B, A, logits, key, counter0, actions,
+  APPO_LAUNCH(c, sample_kernel, (B + 127) / 128, 128, 0, B, hs, logits, key, counter0, actions,
               logp);
   return APPO_OK;
 }

@@ -57,6 +57,18 @@ struct appo_sampler {
   cudaEvent_t copied[2] = {nullptr, nullptr};
   cudaEvent_t consumed[2] = {nullptr, nullptr};
   int stage_next = 0;
+  // CPU-actor rollout (appo_rollout_act / _feedback): per-step rewards and
+  // dones staged through a pinned double buffer (the caller's arrays are free
+  // to reuse when the call returns), the next expected (t, phase) as
+  // write_step's ordering contract, and the event the host waits on for the
+  // actions / the end of the caller-buffer reads
+  uint8_t* fb_host = nullptr;     // pinned [2][n_envs * 5]
+  uint8_t* fb_dev = nullptr;      // [2][n_envs * 5]: rewards f32 then dones u8
+  cudaEvent_t fb_ev[2] = {nullptr, nullptr};
+  int fb_next = 0;
+  cudaEvent_t host_ev = nullptr;  // after the last D2H of actions / read of caller obs
+  int next_t = 0;
+  bool acted = false;             // act(t) done, feedback(t) pending
 };
 
 namespace {
@@ -160,6 +172,62 @@ __global__ void record_kernel(int n_envs, int T, int t, int episode_len, uint32_
   }
 }
 
+// CPU-actor step records (RolloutWorker::step_group, orchestrator.hpp:486-552);
+// one block (128 threads) per env.
+//   act phase (feedback == nullptr): the step's INPUT hidden, action, behaviour
+//     logp and policy version into row t (StepRecord fields, :512-521);
+//   feedback phase: the env transition's reward and done into row t, hidden <-
+//     h' or 0 after done (:524, reset_env :402); at t == T-1 the bootstrap
+//     hidden h' (set_bootstrap before the reset, :531-534); the in-slot header.
+__global__ void host_record_kernel(int n_envs, int T, int t, uint32_t obs_dim, int64_t version,
+                                   float* __restrict__ hidden, const float* __restrict__ h_out,
+                                   const int32_t* __restrict__ act,
+                                   const float* __restrict__ logp,
+                                   const uint8_t* __restrict__ feedback, uint8_t* region,
+                                   uint64_t slot_bytes, int64_t slot_base, SlotOffsets off) {
+  APPO_PDL_ENTRY();
+  const int e = blockIdx.x;
+  if (e >= n_envs) return;
+  uint8_t* slot = region + (uint64_t)(slot_base + e) * slot_bytes;
+  float2* hs = reinterpret_cast<float2*>(hidden + (int64_t)e * kHidden);
+  if (feedback == nullptr) {
+    float2* dst = reinterpret_cast<float2*>(slot + off.hidden + (uint64_t)t * kHidden * 4);
+    for (int j = threadIdx.x; j < kHidden / 2; j += blockDim.x) dst[j] = hs[j];
+    if (threadIdx.x == 0) {
+      reinterpret_cast<int32_t*>(slot + off.actions)[t] = act[e];
+      reinterpret_cast<float*>(slot + off.logp)[t] = logp[e];
+      reinterpret_cast<int64_t*>(slot + off.versions)[t] = version;
+    }
+    return;
+  }
+  const float reward = reinterpret_cast<const float*>(feedback)[e];
+  const bool done = feedback[(size_t)n_envs * 4 + e] != 0;
+  const float2* ho = reinterpret_cast<const float2*>(h_out + (int64_t)e * kHidden);
+  float2* boot = reinterpret_cast<float2*>(slot + off.boot_hidden);
+  for (int j = threadIdx.x; j < kHidden / 2; j += blockDim.x) {
+    const float2 n = ho[j];
+    if (t == T - 1) boot[j] = n;
+    hs[j] = done ? make_float2(0.f, 0.f) : n;
+  }
+  if (threadIdx.x == 0) {
+    reinterpret_cast<float*>(slot + off.rewards)[t] = reward;
+    slot[off.dones + t] = done ? 1 : 0;
+    if (t == T - 1 || t == 0) {
+      uint32_t* h = reinterpret_cast<uint32_t*>(slot);
+      h[0] = T;
+      h[1] = obs_dim;
+      h[2] = kHidden;
+      h[3] = 1;
+      h[4] = t + 1;
+      h[5] = e;
+      h[6] = 0;
+      h[7] = 0;
+      h[8] = 0;
+      h[9] = (t == T - 1) ? 1u : 0u;  // bit0: bootstrap written
+    }
+  }
+}
+
 __global__ void init_env_kernel(int n_envs, int episode_len, uint32_t* step, uint32_t* episode) {
   APPO_PDL_ENTRY();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -175,6 +243,54 @@ __global__ void init_env_kernel(int n_envs, int episode_len, uint32_t* step, uin
 namespace appo_b200 {
 const void* kanchor_sampler() { return reinterpret_cast<const void*>(&init_env_kernel); }
 }  // namespace appo_b200
+
+namespace {
+// Host observations [n_envs][obs_dim] into field offset `off` of slots
+// [slot_base, slot_base + n_envs): a contiguous pinned -> device copy on the
+// sampler's copy stream into one of two staging buffers (so the next copy
+// overlaps this step's inference), then a scatter kernel on the ctx stream;
+// when the rows are not 16-byte aligned, one strided 2-D copy on the ctx
+// stream instead.
+int stage_host_obs(appo_sampler* s, const uint8_t* h_obs, uint8_t* region, uint64_t slot_bytes,
+                   int32_t slot_base, uint64_t off) {
+  appo_ctx* c = s->ctx;
+  const Dims& d = c->model->d;
+  const bool staged = d.obs_dim % 16 == 0 && slot_bytes % 16 == 0 &&
+                      ((reinterpret_cast<uintptr_t>(region) + off) & 15) == 0;
+  if (!staged) {
+    APPO_CUDA_TRY(cudaMemcpy2DAsync(region + (uint64_t)slot_base * slot_bytes + off, slot_bytes,
+                                    h_obs, d.obs_dim, d.obs_dim, s->n_envs,
+                                    cudaMemcpyHostToDevice, c->stream));
+    return APPO_OK;
+  }
+  const size_t bytes = (size_t)s->n_envs * d.obs_dim;
+  if (!s->copy_stream) {
+    APPO_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      APPO_CUDA_TRY(cudaMalloc(&s->staging[k], bytes));
+      APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->copied[k], cudaEventDisableTiming));
+      APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->consumed[k], cudaEventDisableTiming));
+      APPO_CUDA_TRY(cudaEventRecord(s->consumed[k], c->stream));
+    }
+  }
+  const int k = s->stage_next;
+  s->stage_next ^= 1;
+  // the buffer's previous contents were scattered (ctx stream) before it is refilled
+  APPO_CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->consumed[k], 0));
+  APPO_CUDA_TRY(cudaMemcpyAsync(s->staging[k], h_obs, bytes, cudaMemcpyHostToDevice,
+                                s->copy_stream));
+  APPO_CUDA_TRY(cudaEventRecord(s->copied[k], s->copy_stream));
+  APPO_CUDA_TRY(cudaStreamWaitEvent(c->stream, s->copied[k], 0));
+  const dim3 grid((unsigned)std::min<int64_t>(((d.obs_dim >> 4) + 255) / 256, 8),
+                  (unsigned)s->n_envs);
+  c->next_bytes = 2.0 * (double)bytes;
+  APPO_LAUNCH(c, scatter_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim,
+              reinterpret_cast<const uint4*>(s->staging[k]), region, slot_bytes,
+              (int64_t)slot_base, off);
+  APPO_CUDA_TRY(cudaEventRecord(s->consumed[k], c->stream));
+  return APPO_OK;
+}
+}  // namespace
 
 #define SMP_OR_RETURN(s)                                                            \
   do {                                                                              \
@@ -236,6 +352,11 @@ APPO_API int appo_sampler_destroy(appo_sampler* s) {
     cudaStreamSynchronize(s->copy_stream);
     cudaStreamDestroy(s->copy_stream);
   }
+  if (s->fb_host) cudaFreeHost(s->fb_host);
+  if (s->fb_dev) cudaFree(s->fb_dev);
+  for (int k = 0; k < 2; ++k)
+    if (s->fb_ev[k]) cudaEventDestroy(s->fb_ev[k]);
+  if (s->host_ev) cudaEventDestroy(s->host_ev);
   delete s;
   return APPO_OK;
 }
@@ -256,38 +377,9 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
                "sampler_step: bad slot region");
   uint8_t* region = static_cast<uint8_t*>(d_region);
   const uint64_t obs_off = d.slot[0] + (uint64_t)t * d.obs_dim;
-  const bool staged = h_obs && d.obs_dim % 16 == 0 && slot_bytes % 16 == 0 &&
-                      ((reinterpret_cast<uintptr_t>(region) + obs_off) & 15) == 0;
-  if (h_obs && staged) {
-    const size_t bytes = (size_t)s->n_envs * d.obs_dim;
-    if (!s->copy_stream) {
-      APPO_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
-      for (int k = 0; k < 2; ++k) {
-        APPO_CUDA_TRY(cudaMalloc(&s->staging[k], bytes));
-        APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->copied[k], cudaEventDisableTiming));
-        APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->consumed[k], cudaEventDisableTiming));
-        APPO_CUDA_TRY(cudaEventRecord(s->consumed[k], c->stream));
-      }
-    }
-    const int k = s->stage_next;
-    s->stage_next ^= 1;
-    // the buffer's previous contents were scattered (ctx stream) before it is refilled
-    APPO_CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->consumed[k], 0));
-    APPO_CUDA_TRY(cudaMemcpyAsync(s->staging[k], h_obs, bytes, cudaMemcpyHostToDevice,
-                                  s->copy_stream));
-    APPO_CUDA_TRY(cudaEventRecord(s->copied[k], s->copy_stream));
-    APPO_CUDA_TRY(cudaStreamWaitEvent(c->stream, s->copied[k], 0));
-    const dim3 grid((unsigned)std::min<int64_t>(((d.obs_dim >> 4) + 255) / 256, 8),
-                    (unsigned)s->n_envs);
-    c->next_bytes = 2.0 * (double)bytes;
-    APPO_LAUNCH(c, scatter_obs_kernel, grid, 256, 0, s->n_envs, d.obs_dim,
-                reinterpret_cast<const uint4*>(s->staging[k]), region, slot_bytes,
-                (int64_t)slot_base, obs_off);
-    APPO_CUDA_TRY(cudaEventRecord(s->consumed[k], c->stream));
-  } else if (h_obs) {
-    APPO_CUDA_TRY(cudaMemcpy2DAsync(region + (uint64_t)slot_base * slot_bytes + obs_off,
-                                    slot_bytes, h_obs, d.obs_dim, d.obs_dim, s->n_envs,
-                                    cudaMemcpyHostToDevice, c->stream));
+  if (h_obs) {
+    const int st = stage_host_obs(s, h_obs, region, slot_bytes, slot_base, obs_off);
+    if (st) return st;
   } else {
     const dim3 grid((unsigned)(((d.obs_dim >> 3) + 256 * kObsWordsPerThread - 1) /
                              (256 * kObsWordsPerThread)),
@@ -326,6 +418,100 @@ APPO_API int appo_sampler_step(appo_sampler* s, void* d_region, uint64_t slot_by
     APPO_CUDA_TRY(cudaMemcpyAsync(h_actions, s->actions, sizeof(int32_t) * s->n_envs,
                                   cudaMemcpyDeviceToHost, c->stream));
   s->steps_done++;
+  return APPO_OK;
+}
+
+APPO_API int appo_rollout_act(appo_sampler* s, void* d_region, uint64_t slot_bytes,
+                              int32_t slot_base, int t, const uint8_t* h_obs,
+                              int32_t* h_actions) {
+  SMP_OR_RETURN(s);
+  appo_ctx* c = s->ctx;
+  const Dims& d = c->model->d;
+  APPO_REQUIRE(h_obs && d_region && slot_bytes >= d.slot[9], APPO_ERR_CONTRACT,
+               "rollout_act: bad arguments");
+  APPO_REQUIRE(t >= 0 && t < d.T, APPO_ERR_CONTRACT, "write_step: index beyond rollout length");
+  APPO_REQUIRE(!s->acted && t == s->next_t, APPO_ERR_CONTRACT,
+               "write_step: out-of-order step write");
+  if (!s->host_ev) APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->host_ev, cudaEventDisableTiming));
+  uint8_t* region = static_cast<uint8_t*>(d_region);
+  const uint64_t obs_off = d.slot[0] + (uint64_t)t * d.obs_dim;
+  int st = stage_host_obs(s, h_obs, region, slot_bytes, slot_base, obs_off);
+  if (st) return st;
+  int64_t version = 0;
+  st = sampler_infer(c, region + (uint64_t)slot_base * slot_bytes + obs_off, slot_bytes,
+                     s->n_envs, s->hidden, s->steps_done * (uint64_t)s->n_envs, s->actions,
+                     s->logp, s->h_out, s->values, nullptr, &version);
+  if (st) return st;
+  SlotOffsets off;
+  std::memcpy(&off, d.slot, sizeof(off));
+  APPO_LAUNCH(c, host_record_kernel, s->n_envs, 128, 0, s->n_envs, d.T, t, (uint32_t)d.obs_dim,
+              version, s->hidden, s->h_out, s->actions, s->logp,
+              static_cast<const uint8_t*>(nullptr), region, slot_bytes, (int64_t)slot_base, off);
+  if (h_actions)
+    APPO_CUDA_TRY(cudaMemcpyAsync(h_actions, s->actions, sizeof(int32_t) * s->n_envs,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  APPO_CUDA_TRY(cudaEventRecord(s->host_ev, c->stream));
+  s->acted = true;
+  s->steps_done++;
+  return APPO_OK;
+}
+
+APPO_API int appo_rollout_wait(appo_sampler* s) {
+  SMP_OR_RETURN(s);
+  if (s->host_ev) APPO_CUDA_TRY(cudaEventSynchronize(s->host_ev));
+  return APPO_OK;
+}
+
+APPO_API int appo_rollout_feedback(appo_sampler* s, void* d_region, uint64_t slot_bytes,
+                                   int32_t slot_base, int t, const float* h_rewards,
+                                   const uint8_t* h_dones, const uint8_t* h_next_obs) {
+  SMP_OR_RETURN(s);
+  appo_ctx* c = s->ctx;
+  const Dims& d = c->model->d;
+  APPO_REQUIRE(h_rewards && h_dones && d_region && slot_bytes >= d.slot[9], APPO_ERR_CONTRACT,
+               "rollout_feedback: bad arguments");
+  APPO_REQUIRE(s->acted && t == s->next_t, APPO_ERR_CONTRACT,
+               "write_step: out-of-order step write");
+  APPO_REQUIRE(t < d.T - 1 || h_next_obs, APPO_ERR_CONTRACT,
+               "seal: trajectory incomplete (missing steps or bootstrap)");
+  const size_t fb = (size_t)s->n_envs * 5;
+  if (!s->fb_host) {
+    APPO_CUDA_TRY(cudaMallocHost(&s->fb_host, 2 * fb));
+    APPO_CUDA_TRY(cudaMalloc(&s->fb_dev, 2 * fb));
+    for (int k = 0; k < 2; ++k)
+      APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->fb_ev[k], cudaEventDisableTiming));
+  }
+  const int k = s->fb_next;
+  s->fb_next ^= 1;
+  // the half's previous upload has left the host buffer before it is refilled
+  APPO_CUDA_TRY(cudaEventSynchronize(s->fb_ev[k]));
+  uint8_t* hb = s->fb_host + k * fb;
+  std::memcpy(hb, h_rewards, sizeof(float) * s->n_envs);
+  std::memcpy(hb + (size_t)s->n_envs * 4, h_dones, s->n_envs);
+  uint8_t* db = s->fb_dev + k * fb;
+  APPO_CUDA_TRY(cudaMemcpyAsync(db, hb, fb, cudaMemcpyHostToDevice, c->stream));
+  APPO_CUDA_TRY(cudaEventRecord(s->fb_ev[k], c->stream));
+  uint8_t* region = static_cast<uint8_t*>(d_region);
+  SlotOffsets off;
+  std::memcpy(&off, d.slot, sizeof(off));
+  APPO_LAUNCH(c, host_record_kernel, s->n_envs, 128, 0, s->n_envs, d.T, t, (uint32_t)d.obs_dim,
+              (int64_t)0, s->hidden, s->h_out, s->actions, s->logp,
+              static_cast<const uint8_t*>(db), region, slot_bytes, (int64_t)slot_base, off);
+  if (t == d.T - 1) {
+    // set_bootstrap: the step's next observation (orchestrator.hpp:529-534)
+    const int st = stage_host_obs(s, h_next_obs, region, slot_bytes, slot_base, d.slot[7]);
+    if (st) return st;
+    if (!s->host_ev) APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->host_ev, cudaEventDisableTiming));
+    APPO_CUDA_TRY(cudaEventRecord(s->host_ev, c->stream));
+    if (s->ready_q) {
+      APPO_REQUIRE((int64_t)slot_base + s->n_envs <= s->ready_q->n_slots, APPO_ERR_CONTRACT,
+                   "rollout_feedback: slots outside the ready queue's range");
+      const int pst = slotq_push_launch(c, s->ready_q, nullptr, slot_base, s->n_envs, nullptr);
+      if (pst != APPO_OK) return pst;
+    }
+  }
+  s->acted = false;
+  s->next_t = (t + 1) % d.T;
   return APPO_OK;
 }
 

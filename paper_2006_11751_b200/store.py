@@ -31,11 +31,14 @@ class TrajectoryStore:
         self.n_slots = n_slots
         self.T = desc.T
         self.obs_dim = desc.obs_dim
-        self.region = torch.zeros(n_slots * self.slot_bytes, dtype=torch.uint8,
-                                  device=f"cuda:{device}")
+        # device = "cpu": a host region (layout / dump tests without a GPU; the
+        # library's kernels only ever see device regions)
+        dev = "cpu" if device == "cpu" else f"cuda:{device}"
+        self.region = torch.zeros(n_slots * self.slot_bytes, dtype=torch.uint8, device=dev)
         # the region is written by library streams other than torch's: make the
         # zero fill visible to them before first use
-        torch.cuda.synchronize(device)
+        if dev != "cpu":
+            torch.cuda.synchronize(device)
 
     # ---- typed views of one slot (device tensors aliasing the region) ----
     def _view(self, slot: int, field: str, dtype, count: int):

@@ -3,6 +3,7 @@
 // exception taxonomy, and one batched inference + learner step.
 #include <cmath>
 #include <cstdio>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -38,6 +39,66 @@ int main() {
   std::vector<double> r3{1.0, 1.0, 1.0};
   try { ctx.vtrace(r3, v, 0.0, tl, bl, d, VTraceConfig{}); } catch (const ContractError&) { got = true; }
   REQUIRE(got);
+
+  // nstep_returns KAT (test_offpolicy.cpp:254-261)
+  {
+    std::vector<double> rw{1.0, 1.0, 1.0};
+    std::vector<uint8_t> dn{0, 1, 0};
+    auto ret = ctx.nstep_returns(rw, 10.0, dn, 0.5);
+    REQUIRE(std::fabs(ret[2] - 6.0) < 1e-6 && std::fabs(ret[1] - 1.0) < 1e-6 &&
+            std::fabs(ret[0] - 1.5) < 1e-6);
+  }
+  // heads: uniform entropies (test_policy.cpp:241-252), degenerate logits
+  // (:195-203), reproducible sampling under a fixed seed over the full
+  // factored space (:226-239), out-of-range action (:292-297)
+  {
+    ActionHeadsSpec h22{{2, 2}};
+    auto [lp, ent] = ctx.log_prob_and_entropy(h22, std::vector<double>{0, 0, 0, 0}, {0, 1});
+    REQUIRE(std::fabs(ent - 2.0 * std::log(2.0)) < 1e-6 && std::fabs(lp - 2.0 * std::log(0.5)) < 1e-6);
+    ActionHeadsSpec h3{{3}};
+    std::mt19937_64 rng(11);
+    auto [a, lpa] = ctx.sample_action(h3, std::vector<double>{1e9, 0.0, 0.0}, rng);
+    REQUIRE(a.size() == 1 && a[0] == 0 && std::fabs(lpa) < 1e-6);
+    ActionHeadsSpec full{{3, 3, 2, 2, 2, 8, 21}};
+    std::vector<double> lg(full.logits_dim());
+    std::mt19937_64 lrng(5);
+    for (auto& l : lg) l = std::uniform_real_distribution<double>(-1, 1)(lrng);
+    std::mt19937_64 ra(99), rb(99);
+    for (int i = 0; i < 5; ++i) {
+      auto [a1, l1] = ctx.sample_action(full, lg, ra);
+      auto [a2, l2] = ctx.sample_action(full, lg, rb);
+      REQUIRE(a1 == a2 && l1 == l2 && a1.size() == 7);
+      for (int j = 0; j < 7; ++j) REQUIRE(a1[j] >= 0 && a1[j] < full.sizes[j]);
+    }
+    bool thrown = false;
+    try { ctx.log_prob_and_entropy(h3, std::vector<double>{0, 0, 0}, {3}); } catch (const ContractError&) { thrown = true; }
+    REQUIRE(thrown);
+  }
+  // optimizer_step: zero gradient leaves theta, bumps version
+  // (test_policy.cpp:382-390); norm 8 under clip 4 equals norm 4 unclipped
+  // (:392-413); non-finite gradient throws NumericError, p untouched
+  {
+    PolicyParams p;
+    p.theta.assign(1000, 0.0);
+    // fp32-representable values: the device keeps theta in fp32
+    for (size_t i = 0; i < p.theta.size(); ++i) p.theta[i] = static_cast<double>(i) / 1024.0;
+    const auto before = p.theta;
+    ctx.optimizer_step(p, std::vector<double>(1000, 0.0), AdamConfig{});
+    REQUIRE(p.theta == before && p.version == 1 && p.adam.t == 1);
+    PolicyParams pa = p, pb = p;
+    std::vector<double> g(1000, 0.0), half(1000, 0.0);
+    g[0] = 8.0; half[0] = 4.0;
+    AdamConfig clip4, noclip;
+    clip4.grad_clip = 4.0; noclip.grad_clip = 0.0;
+    ctx.optimizer_step(pa, g, clip4);
+    ctx.optimizer_step(pb, half, noclip);
+    REQUIRE(pa.theta == pb.theta && pa.theta != p.theta);
+    g[3] = NAN;
+    PolicyParams pc = p;
+    bool thrown = false;
+    try { ctx.optimizer_step(pc, g, clip4); } catch (const NumericError&) { thrown = true; }
+    REQUIRE(thrown && pc.theta == p.theta && pc.version == p.version);
+  }
 
   // model: one inference batch and one learner step through the C ABI
   appo_model_desc desc{3, 72, 128, 6, 8, {0, 0, 0}};

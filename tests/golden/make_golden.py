@@ -168,6 +168,24 @@ def main():
     np.savez(os.path.join(HERE, "ppo_grad.npz"), logits=lg, values=vals, actions=acts,
              blogp=blogp, adv=advs, vt=vt, dlogits=g["dlogits"], dv=g["dv"], loss=g["loss"],
              mean_ratio=g["mean_ratio"])
+    # 9. factored action heads (ActionHeadsSpec, policy.hpp:25-35,262-281): the
+    #    full Doom factored space {3,3,2,2,2,8,21} (test_policy.cpp:188-193),
+    #    {3,4} (:254-290) and the two-binary-head uniform KAT (:241-252).
+    rs = np.random.default_rng(91)
+    fact = {}
+    for name, sizes in (("doom", [3, 3, 2, 2, 2, 8, 21]), ("h34", [3, 4]), ("h22", [2, 2])):
+        B = 256
+        lg = rs.uniform(-2, 2, (B, sum(sizes))).astype(np.float32).astype(np.float64)
+        if name == "h22":
+            lg[0] = 0.0
+        acts = np.stack([rs.integers(0, n, B) for n in sizes], 1).astype(np.int32)
+        if name == "h22":
+            acts[0] = [0, 1]
+        st, lp, en = ref.logp_entropy_heads(sizes, lg, acts)
+        assert st == 0
+        fact.update({f"{name}_sizes": np.array(sizes, np.int32), f"{name}_logits": lg,
+                     f"{name}_actions": acts, f"{name}_logp": lp, f"{name}_entropy": en})
+    np.savez(os.path.join(HERE, "heads_factored.npz"), **fact)
     print("golden vectors written to", HERE)
 
 

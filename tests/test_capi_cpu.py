@@ -81,3 +81,26 @@ def test_ctx_without_gpu_fails_loudly():
     h = C.c_void_p()
     st = appo.LIB.appo_ctx_create(None, 0, 1, C.byref(h))
     assert st in (1, 4)
+
+
+REF_INC = "/root/reference/proj/include"
+
+
+@pytest.mark.parametrize("src,ref_inc", [("capi_host_test.cpp", False),
+                                         ("cli_exit_test.cpp", True)])
+def test_cpp_mirror_compiles(tmp_path, src, ref_inc):
+    """include/appo_b200.hpp compiles standalone (own exception types) and,
+    with the reference's include path, aliases ::appo::ContractError /
+    ConfigError / NumericError (cli_exit_test.cpp static_asserts it)."""
+    import paper_2006_11751_b200 as appo
+    if ref_inc and not os.path.isdir(os.path.join(REF_INC, "appo")):
+        pytest.skip("reference headers absent")
+    cmd = ["g++", "-std=c++20", "-O0", "-I", os.path.join(ROOT, "include"),
+           "-I", "/usr/local/cuda/include"]
+    if ref_inc:
+        cmd += ["-I", REF_INC]
+    cmd += [os.path.join(ROOT, "tests", "cpp", src), "-o", str(tmp_path / "a.out"),
+            "-L", os.path.dirname(appo.LIB_PATH), "-lappo_b200", "-L", "/usr/local/cuda/lib64",
+            "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

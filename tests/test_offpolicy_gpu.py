@@ -182,3 +182,49 @@ def test_large_sweep_vs_oracle(ctx, oracle):
                                               b[idx].astype(np.float64), tl[idx].astype(np.float64),
                                               bl[idx].astype(np.float64), d[idx], 1.0, 1.0, 0.99)
     assert close(v.cpu().numpy()[idx], ov) <= TOL and close(pg.cpu().numpy()[idx], opg) <= TOL
+
+
+@pytest.mark.parametrize("name", ["doom", "h34", "h22"])
+def test_factored_heads_logp_entropy(ctx, name):
+    """log_prob_and_entropy over factored heads vs the reference
+    (heads_factored.npz: {3,3,2,2,2,8,21}, {3,4}, and the 2 ln 2 KAT)."""
+    g = golden("heads_factored")
+    sizes = [int(x) for x in g[f"{name}_sizes"]]
+    lp, en = ctx.log_prob_and_entropy_heads(sizes, dev(g[f"{name}_logits"]),
+                                            dev(g[f"{name}_actions"], torch.int32))
+    assert close(lp.cpu(), g[f"{name}_logp"]) <= TOL
+    assert close(en.cpu(), g[f"{name}_entropy"]) <= TOL
+    bad = g[f"{name}_actions"][:2].copy()
+    bad[1, -1] = sizes[-1]  # out of range for the last head: ContractError
+    with pytest.raises(appo.ContractError):
+        ctx.log_prob_and_entropy_heads(sizes, dev(g[f"{name}_logits"][:2]), dev(bad, torch.int32))
+
+
+def test_factored_heads_sampling(ctx, oracle):
+    """sample_action over factored heads: per head the oracle's inverse CDF on
+    the same counter-based uniform, joint logp = sum; and per-head marginal
+    frequencies within 3 sigma over 2e5 rows."""
+    g = golden("heads_factored")
+    sizes = [int(x) for x in g["doom_sizes"]]
+    lg = g["doom_logits"]
+    key = 4321
+    a, lpa = ctx.sample_actions_heads(sizes, dev(lg), key, 5)
+    a = a.cpu().numpy()
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    n = len(sizes)
+    for b in range(len(lg)):
+        tot = 0.0
+        for j in range(n):
+            u = oracle.L.orc_uniform(key, 5 + b * n + j)
+            ea, elp = oracle.sample(lg[b, off[j]:off[j + 1]].astype(np.float32).astype(np.float64), u)
+            assert a[b, j] == ea
+            tot += elp
+        assert abs(lpa[b].item() - tot) <= 1e-5 * max(abs(tot), 1)
+    N = 200000
+    a, _ = ctx.sample_actions_heads(sizes, dev(np.tile(lg[0], (N, 1))), 9, 0)
+    a = a.cpu().numpy()
+    for j in range(n):
+        x = lg[0, off[j]:off[j + 1]]
+        p = np.exp(x - x.max()); p /= p.sum()
+        c = np.bincount(a[:, j], minlength=sizes[j])
+        assert np.all(np.abs(c - N * p) < 3.5 * np.sqrt(N * p * (1 - p)) + 1)

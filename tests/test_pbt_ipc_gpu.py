@@ -46,8 +46,9 @@ def worker(rank, port, q):
         states = [None, None]
         dist.all_gather_object(states, (th, m, v, t, ver))
         # the controller on both ranks: policy 0 has the better score, so the
-        # exchange copies 0 -> 1 (P = 2, replace 30 % -> one replaced agent)
-        cfg = appo.PbtConfig.defaults()
+        # exchange copies 0 -> 1 (P = 2, replace 50 %: n_replace = floor(1.0) =
+        # 1, n_top = 1, population.hpp:151-152; the default 30 % floors to 0)
+        cfg = appo.PbtConfig.defaults(replace_fraction=0.5)
         calls = []
         pbt = appo.PbtController(cfg, 2, 7, copy_weights=lambda d, s: calls.append((d, s)))
         pbt.step([1.0, 0.0], 0)
