@@ -126,13 +126,64 @@ def dist_setup(args):
 
 
 # --------------------------------------------------------------------- CPU baseline
+def host_cpu():
+    """lscpu model name and the usable core count of this host."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:  # noqa: BLE001
+        pass
+    return model, len(os.sched_getaffinity(0))
+
+
+_NATIVE_ORACLE = {}
+
+
+def native_oracle():
+    """The oracle port compiled for THIS host (-O3 -march=native, SURVEY §8(d)
+    CPU plan) into a temporary directory; the prebuilt portable -O3 build
+    (oracle/liboracle.so) if the compiler is unavailable."""
+    from oracle.oracle import Oracle
+    if "o" not in _NATIVE_ORACLE:
+        d = tempfile.mkdtemp(prefix="appo_oracle_")
+        so = os.path.join(d, "liboracle_native.so")
+        r = subprocess.run(["gcc", "-O3", "-march=native", "-std=c99", "-fPIC", "-shared", "-o", so,
+                            os.path.join(ROOT, "oracle", "appo_oracle.c"), "-lm"],
+                           capture_output=True)
+        _NATIVE_ORACLE["o"] = (Oracle(so), "gcc -O3 -march=native") if r.returncode == 0 else \
+            (Oracle(), "prebuilt -O3 (native build failed)")
+    return _NATIVE_ORACLE["o"]
+
+
+def reference_mlp_timing():
+    """The reference's own learner math (its MLP stand-in 27,648 -> 512 -> 512
+    -> 6 at the Doom input, oracle/_ref) on one thread: the CPU cost the
+    reference would pay per sample with its own model."""
+    try:
+        from oracle.oracle import Reference
+        if not Reference.available():
+            return None
+        st, r = Reference().mlp_stand_in_time(B=8, reps=2)
+        if st != 0:
+            return {"error": f"status {st}"}
+        per = r["forward_s_per_sample"] + r["gradient_s_per_sample"]
+        return dict(r, threads=1, frames_per_s_per_thread=4.0 / per,
+                    note="forward_batch (inference) + compute_gradients (learner) per sample, "
+                         "optimizer_step per call excluded; fp64, 1 thread, best of 2, B=8")
+    except Exception as ex:  # noqa: BLE001
+        return {"error": repr(ex)}
+
+
 def cpu_baseline_sample(args, n_traj=None, seed=0):
     """Oracle port (oracle/appo_oracle.c, fp64) on the host cores: every thread
     runs one trajectory through T+1 inference steps and one learner step over
-    it -- the same per-sample work as the GPU step, bounded in size."""
-    from oracle.oracle import Oracle
-    orc = Oracle()
-    cores = os.cpu_count() or 1
+    it -- the same per-sample work as the GPU step (the learner's cost is
+    linear in the trajectories of a minibatch), bounded in size."""
+    orc, build = native_oracle()
+    model, cores = host_cpu()
     n = n_traj or 8 * cores  # ~8-10 s of CPU work on the GPU box's host
     shape = (3, 72, 128, 6)
     T = args.T
@@ -164,6 +215,7 @@ def cpu_baseline_sample(args, n_traj=None, seed=0):
     dt = time.perf_counter() - t0
     frames = n * T * args.frameskip
     return {"value": frames / dt, "unit": "frames/s", "cores": min(cores, n), "kind": "port",
+            "cpu_model": model, "nproc": cores, "build": build,
             "sample": f"{n} trajectories x T={T} (inference of T+1 steps + one learner step each), "
                       f"fp64 C oracle, {min(cores, n)} threads, {dt:.1f} s"}
 
@@ -173,7 +225,7 @@ def run_reference(args, ws, rank):
         return
     K, W = args.steps, args.warmup
     for _ in range(min(W, 1)):
-        cpu_baseline_sample(args, n_traj=max(1, (os.cpu_count() or 1) // 4))
+        cpu_baseline_sample(args, n_traj=max(1, host_cpu()[1] // 4))
     vals = []
     t0 = time.perf_counter()
     res = None
@@ -188,7 +240,7 @@ def run_reference(args, ws, rank):
             "impl": "reference",
             "config": {"workload": "C4 per-sample work (inference + learner), Doom shape",
                        "obs": "u8 3x72x128", "T": args.T, "frameskip": args.frameskip},
-            "cpu_baseline": dict(res, value=v),
+            "cpu_baseline": dict(res, value=v, reference_mlp_stand_in=reference_mlp_timing()),
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -242,7 +294,27 @@ def run_ours(args, ws, rank, local):
     lstream, sstream = lctx.stream, sctx.stream
     state = {"k": 0}
 
-    def iteration(h_obs=None, h_act=None):
+    def host_step(h, base, t):
+        """CPU actors (appo_rollout_act / _feedback, orchestrator.hpp:435-552):
+        every env step's observations, rewards and dones -- and at T-1 the
+        bootstrap observations -- come from pinned host memory, and the actions
+        reach the host before the step's feedback (an actor needs them to step
+        its envs).  Two env groups, as the reference's double-buffered rollout
+        workers (orchestrator.hpp:434, exchange slot id*2+g): a group's next
+        act is issued right after its feedback, so its observation transfer
+        overlaps the other group's wait and inference."""
+        T = args.T
+        for g, smp in enumerate(h["samplers"]):
+            if t == 0:
+                smp.act(store, base + g * h["gn"], 0, h["obs"][g][0], h["act"][g])
+        for g, smp in enumerate(h["samplers"]):
+            smp.wait()
+            smp.feedback(store, base + g * h["gn"], t, h["rew"][g][t], h["dn"][g][t],
+                         h["obs"][g][(t + 1) % 2] if t == T - 1 else None)
+            if t + 1 < T:
+                smp.act(store, base + g * h["gn"], t + 1, h["obs"][g][(t + 1) % 2], h["act"][g])
+
+    def iteration(h=None):
         k = state["k"]
         base = (k % 2) * n
         # interleave submission (one sampler step per len(ids)/T learner steps)
@@ -250,9 +322,10 @@ def run_ours(args, ws, rank, local):
         per = (len(ids) + args.T - 1) // args.T
         prev = ((k - 1) % 2) * n
         for t in range(args.T):
-            sampler.step(store, base, t,
-                         h_obs=h_obs[t % h_obs.shape[0]] if h_obs is not None else None,
-                         h_actions=h_act)
+            if h is None:
+                sampler.step(store, base, t)
+            else:
+                host_step(h, base, t)
             if k > 0:
                 for mb in ids[t * per:(t + 1) * per]:  # asynchronous learner steps
                     lctx.learner_submit(store.region, store.slot_bytes, mb + prev, hp)
@@ -317,32 +390,48 @@ def run_ours(args, ws, rank, local):
     frames_step = n * args.T * args.frameskip
     value = frames_step * args.steps * ws / (ms / 1000.0)
 
-    # e2e: observations from pinned host memory (CPU actors) every env step,
-    # sampled actions back to the host, learner stats back to the host
+    # e2e: every env step's observations, rewards and dones (and the bootstrap
+    # observations) from pinned host memory (CPU actors), actions back to the
+    # host each step, learner stats back to the host
     e2e = None
     if not args.no_e2e:
-        h_obs = torch.from_numpy(np.random.default_rng(rank).integers(
-            0, 256, (2, n, desc.obs_dim), dtype=np.uint8)).pin_memory()
-        h_act = torch.empty(n, dtype=torch.int32).pin_memory()
-        iteration(h_obs, h_act)
+        gn = n // 2
+        rs = np.random.default_rng(rank)
+        T = args.T
+        h = {"gn": gn, "samplers": [appo.Sampler(sctx, gn, args.episode_len, seed=2000 + rank + g)
+                                    for g in range(2)],
+             "obs": [[torch.from_numpy(rs.integers(0, 256, (gn, desc.obs_dim), dtype=np.uint8))
+                      .pin_memory() for _ in range(2)] for _ in range(2)],
+             "act": [torch.empty(gn, dtype=torch.int32).pin_memory() for _ in range(2)],
+             # SyntheticLatencyEnv's reward schedule / episode ends (envs.hpp:127-128)
+             "rew": [[torch.from_numpy((0.1 * ((np.arange(gn) + t + 1 + g) % 11) - 0.5)
+                                       .astype(np.float32)).pin_memory() for t in range(T)]
+                     for g in range(2)],
+             "dn": [[torch.from_numpy(((np.arange(gn) * 7 + t + g) % args.episode_len == 0)
+                                      .astype(np.uint8)).pin_memory() for t in range(T)]
+                    for g in range(2)]}
+        iteration(h)
         barrier()
         e0.record(lstream)
         for k in range(args.steps):
-            iteration(h_obs, h_act)
+            iteration(h)
         e1.record(lstream)
         barrier()
         ems = e0.elapsed_time(e1)
         if dist is not None:
-            t = torch.tensor([ems], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = t.item()
+            t_ = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            ems = t_.item()
         n_mb = ids.shape[0]
         e2e = {"value": frames_step * args.steps * ws / (ems / 1000.0), "unit": "frames/s",
-               "h2d_bytes_per_step": n * desc.obs_dim * args.T + n_mb * tpb * 4,
-               "d2h_bytes_per_step": n * 4 * args.T + n_mb * (8 * 10 + 16),
-               "path": "appo_sampler_step(h_obs pinned) + appo_learner_submit/collect"}
+               "h2d_bytes_per_step": n * desc.obs_dim * (T + 1) + n * 5 * T + n_mb * tpb * 4,
+               "d2h_bytes_per_step": n * 4 * T + n_mb * (8 * 10 + 16),
+               "path": "appo_rollout_act(h_obs) + wait + appo_rollout_feedback(h_rewards, "
+                       "h_dones, h_next_obs at T-1), 2 env groups; appo_learner_submit/collect"}
         # the host link is the e2e bound: H2D rate achieved over the timed region
         e2e["h2d_gbps"] = e2e["h2d_bytes_per_step"] * args.steps / (ems / 1000.0) / 1e9
+        for smp in h["samplers"]:
+            smp.close()
 
     peaks, peak_src = load_peaks()
     roof = None
@@ -380,6 +469,7 @@ def run_ours(args, ws, rank, local):
     if ws == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline_sample(args, n_traj=args.cpu_traj or None)
+            cpu["reference_mlp_stand_in"] = reference_mlp_timing()
         except Exception as ex:  # noqa: BLE001
             cpu = {"error": repr(ex)}
     line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws,

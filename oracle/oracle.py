@@ -328,6 +328,18 @@ class Reference:
         st = L.ref_log_prob_entropy_heads(len(sz), sz, B, lg, act, lp, en)
         return st, lp, en
 
+    def mlp_stand_in_time(self, obs_dim=27648, trunk=512, A=6, B=8, reps=2):
+        """The reference's MLP stand-in at the Doom input through its own
+        forward_batch / compute_gradients / optimizer_step on one thread
+        (ref_shim.cpp): seconds per sample (forward, gradient), per Adam call."""
+        L = self.L
+        L.ref_mlp_stand_in_time.restype = C.c_int
+        L.ref_mlp_stand_in_time.argtypes = [C.c_int] * 5 + [_dp]
+        out = np.zeros(4)
+        st = L.ref_mlp_stand_in_time(obs_dim, trunk, A, B, reps, out)
+        return st, dict(forward_s_per_sample=out[0], gradient_s_per_sample=out[1],
+                        optimizer_s=out[2], n_params=int(out[3]))
+
     def dump_trajectory(self, path, obs, hidden, actions, rewards, logp, dones, versions,
                         boot_obs, boot_hidden, env=0, worker=0, policy=0):
         """dump_trajectory (trajstore.hpp:335-359) of a slot the reference itself

@@ -9,6 +9,7 @@
 // bench.py --impl reference also times these functions as the reference CPU
 // path.  No reference source is copied into this repository; this file only
 // includes the headers and forwards arguments.
+#include <chrono>
 #include <cstring>
 #include <sstream>
 #include <random>
@@ -298,6 +299,54 @@ int ref_ppo_grads_injected(int n, int A, const double* logits, const double* val
     loss4[2] = acc[2] / n;
     loss4[3] = loss4[0] + loss4[1] - entropy_coef * loss4[2];
     *mean_ratio = acc[4] / n;
+  });
+}
+
+// The reference's own learner math at the Doom input (SURVEY §8(d) CPU plan):
+// its MLP stand-in (ModelShape{obs_dim, 0, trunk, {A}}, policy.hpp:39-59) timed
+// through forward_batch (policy.hpp:165-200), compute_gradients (:302-428) and
+// optimizer_step (:431-455) on one thread, steady_clock, best of `reps`.
+// out[0] = forward s/sample, out[1] = compute_gradients s/sample,
+// out[2] = optimizer_step s/call, out[3] = n_params.
+int ref_mlp_stand_in_time(int obs_dim, int trunk, int A, int B, int reps, double* out) {
+  return guarded([&] {
+    ModelShape s;
+    s.obs_dim = obs_dim;
+    s.trunk_hidden = trunk;
+    s.heads.sizes = {A};
+    PolicyParams p = init_params(s, 1);
+    std::mt19937_64 rng(3);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    SampleBatch b;
+    b.batch = B;
+    b.obs.resize(static_cast<std::size_t>(B) * obs_dim);
+    for (auto& x : b.obs) x = u(rng);
+    for (int i = 0; i < B; ++i) {
+      b.actions.push_back(static_cast<std::int32_t>(rng() % A));
+      b.behavior_logp.push_back(-std::log(static_cast<double>(A)));
+      b.advantages.push_back(u(rng) - 0.5);
+      b.v_targets.push_back(u(rng) - 0.5);
+    }
+    LossConfig cfg;
+    AdamConfig adam;
+    double best[3] = {1e30, 1e30, 1e30};
+    for (int r = 0; r < reps; ++r) {
+      ForwardCache cache;
+      auto t0 = std::chrono::steady_clock::now();
+      forward_batch(p, b.obs, B, cache);
+      auto t1 = std::chrono::steady_clock::now();
+      GradientResult g = compute_gradients(p, b, cfg);
+      auto t2 = std::chrono::steady_clock::now();
+      optimizer_step(p, g.grad, adam);
+      auto t3 = std::chrono::steady_clock::now();
+      best[0] = std::min(best[0], std::chrono::duration<double>(t1 - t0).count() / B);
+      best[1] = std::min(best[1], std::chrono::duration<double>(t2 - t1).count() / B);
+      best[2] = std::min(best[2], std::chrono::duration<double>(t3 - t2).count());
+    }
+    out[0] = best[0];
+    out[1] = best[1];
+    out[2] = best[2];
+    out[3] = static_cast<double>(p.theta.size());
   });
 }
 

@@ -1309,18 +1309,18 @@ __global__ void __launch_bounds__(256)
   const int64_t i = (int64_t)blockIdx.x * 32 + lane;
   float s = 0.0f;
   if (i < total) {
+    // every load of the thread's group in flight at once (<= 160 splits: one
+    // memory round trip), then the adds in split order
     int z = g;
-    for (; z + 24 < splits; z += 32) {
-      const float a0 = __ldg(partial + (size_t)z * total + i);
-      const float a1 = __ldg(partial + (size_t)(z + 8) * total + i);
-      const float a2 = __ldg(partial + (size_t)(z + 16) * total + i);
-      const float a3 = __ldg(partial + (size_t)(z + 24) * total + i);
-      s += a0;
-      s += a1;
-      s += a2;
-      s += a3;
+    for (; z < splits; z += 8 * 20) {
+      float a[20];
+#pragma unroll
+      for (int k = 0; k < 20; ++k)
+        a[k] = z + 8 * k < splits ? __ldg(partial + (size_t)(z + 8 * k) * total + i) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 20; ++k)
+        if (z + 8 * k < splits) s += a[k];
     }
-    for (; z < splits; z += 8) s += __ldg(partial + (size_t)z * total + i);
   }
   __shared__ float sh[8][33];
   sh[g][lane] = s;

@@ -492,14 +492,32 @@ __global__ void __launch_bounds__(256)
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
+    // whole last block: thread b loads block b's partials (b, b + blockDim, ..
+    // summed in that order), then a fixed-order tree over the threads
+    // (deterministic; one memory round trip instead of a serial walk)
     __threadfence();
     double t[6] = {0, 0, 0, 0, 0, -1e300};
-    for (unsigned b = 0; b < gridDim.x; ++b)
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+#pragma unroll
       for (int k = 0; k < 6; ++k) {
-        const double x = ((volatile double*)partials)[b * 6 + k];
+        const double x = __ldcg(partials + b * 6 + k);
         t[k] = k == 5 ? fmax(t[k], x) : t[k] + x;
       }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) t[k] = warp_sum(t[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t[5] = fmax(t[5], __shfl_xor_sync(0xffffffffu, t[5], o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sh[threadIdx.x >> 5][k] = t[k];
+    __syncthreads();
+  }
+  if (last && threadIdx.x == 0) {
+    double t[6] = {0, 0, 0, 0, 0, -1e300};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      for (int k = 0; k < 6; ++k) t[k] = k == 5 ? fmax(t[k], sh[w][k]) : t[k] + sh[w][k];
     const double invB = 1.0 / B;
     stats[0] = t[0] * invB;
     stats[1] = hp.value_coef * t[1] * invB;
@@ -516,9 +534,12 @@ __global__ void __launch_bounds__(256)
 // Heads backward in one kernel (policy.hpp:377-383 analogue for the heads):
 // dcore[s][j] = sum_a dlog[s][a] * Wh[a][j] (Wh = policy rows then the value
 // row) and the head gradients dWh[a][j] = sum_s dlog[s][a] * core[s][j],
-// dbh[a] = sum_s dlog[s][a] in fp32.  Block = a chunk of rows x 512 columns
-// (thread j); per-block partials, the last block sums them in block order
-// (deterministic) straight into the flat gradient.
+// dbh[a] = sum_s dlog[s][a] in fp32.  Block = a range of rows x 512 columns
+// (thread j), walked in chunks of kHbRows: the chunk's dlog rows are staged in
+// shared memory and its core values loaded into registers up front (one
+// memory round trip per chunk instead of one per row); per-block partials are
+// summed in block order by heads_grad_reduce_kernel (deterministic).
+constexpr int kHbRows = 16;
 __global__ void __launch_bounds__(512)
     heads_bwd_fused_kernel(int B, int A, const float* __restrict__ dlog,
                            const float* __restrict__ core, const float* __restrict__ wpi,
@@ -526,6 +547,7 @@ __global__ void __launch_bounds__(512)
                            float* __restrict__ part, unsigned* counter, float* gwpi, float* gbpi,
                            float* gwv, float* gbv) {
   APPO_PDL_ENTRY();
+  __shared__ float sdl[kHbRows][kMaxActions + 1];
   const int j = threadIdx.x;
   const int A1 = A + 1;
   const int rows = (B + gridDim.x - 1) / gridDim.x;
@@ -536,20 +558,33 @@ __global__ void __launch_bounds__(512)
     w[a] = a < A ? wpi[a * kHidden + j] : (a == A ? wv[j] : 0.0f);
     sw[a] = 0.0f;
   }
-  for (int s = r0; s < r1; ++s) {
-    const float* dl = dlog + (int64_t)s * A1;
-    const float c = core[(int64_t)s * kHidden + j];
-    float dc = 0.0f;
+  for (int c0 = r0; c0 < r1; c0 += kHbRows) {
+    const int nr = min(kHbRows, r1 - c0);
+    __syncthreads();  // previous chunk's sdl reads done
+    if (j < kHbRows * A1) {
+      const int r = j / A1, a = j - r * A1;
+      sdl[r][a] = r < nr ? dlog[(int64_t)(c0 + r) * A1 + a] : 0.0f;
+    }
+    float cv[kHbRows];
 #pragma unroll
-    for (int a = 0; a <= kMaxActions; ++a) {
-      if (a < A1) {
-        const float g = dl[a];
-        dc += g * w[a];
-        sw[a] += g * c;
+    for (int r = 0; r < kHbRows; ++r) cv[r] = r < nr ? core[(int64_t)(c0 + r) * kHidden + j] : 0.0f;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kHbRows; ++r) {
+      if (r < nr) {
+        float dc = 0.0f;
+#pragma unroll
+        for (int a = 0; a <= kMaxActions; ++a) {
+          if (a < A1) {
+            const float g = sdl[r][a];
+            dc += g * w[a];
+            sw[a] += g * cv[r];
+          }
+        }
+        dcore[(int64_t)(c0 + r) * kHidden + j] = dc;
+        if (j < A1) sb += sdl[r][j];
       }
     }
-    dcore[(int64_t)s * kHidden + j] = dc;
-    if (j < A1) sb += dl[j];
   }
   float* pb = part + (size_t)blockIdx.x * (A1 * kHidden + A1);
 #pragma unroll
@@ -558,7 +593,8 @@ __global__ void __launch_bounds__(512)
   if (j < A1) pb[A1 * kHidden + j] = sb;
 }
 
-// Sums the per-block head-gradient partials in block order (thread per output).
+// Sums the per-block head-gradient partials in block order (thread per
+// output); loads are issued 16 at a time ahead of the in-order adds.
 __global__ void __launch_bounds__(256)
     heads_grad_reduce_kernel(int A, int nb, const float* __restrict__ part, float* gwpi,
                              float* gbpi, float* gwv, float* gbv) {
@@ -568,7 +604,14 @@ __global__ void __launch_bounds__(256)
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= stride) return;
   float t = 0.0f;
-  for (int b = 0; b < nb; ++b) t += part[(size_t)b * stride + o];
+  for (int b0 = 0; b0 < nb; b0 += 16) {
+    float x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = b0 + k < nb ? __ldg(part + (size_t)(b0 + k) * stride + o) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (b0 + k < nb) t += x[k];
+  }
   if (o < A * kHidden) gwpi[o] = t;
   else if (o < A1 * kHidden) gwv[o - A * kHidden] = t;
   else if (o - A1 * kHidden < A) gbpi[o - A1 * kHidden] = t;
@@ -739,6 +782,9 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
   // 64-thread blocks: the per-row fp64 softmax is latency-bound, spread it over SMs
   const int grid = (B + 63) / 64;
   APPO_REQUIRE(grid * 6 <= kRedSlots, APPO_ERR_CONTRACT, "ppo_loss: batch too large");
+  // in: logits, value, action, behaviour logp, advantage, v-target, version;
+  // out: dlogits + dV (fp32) and the bf16 head-gradient row (16 wide)
+  c->next_bytes = (double)B * (A * 4 + 28 + (A + 1) * 4 + 32);
   APPO_LAUNCH(c, ppo_loss_kernel, grid, 64, 0, B, A, logits, values, act, blogp, adv, vt, hp,
               dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
   return APPO_OK;
