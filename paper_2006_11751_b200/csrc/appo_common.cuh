@@ -65,8 +65,12 @@ struct Ctx {
   appo_model_desc desc{};
   Model* model = nullptr;
   Reader* reader = nullptr;  // inference state of this context (model.cu)
+  // host -> device observation copies of every sampler on this context, in
+  // issue order on one stream: groups' transfers queue back to back instead
+  // of splitting the link (sampler.cu)
+  cudaStream_t copy_stream = nullptr;
 };
-constexpr int kRedSlots = 148 * 8 * 8;
+constexpr int kRedSlots = 148 * 8 * 16;
 
 }  // namespace appo_b200
 

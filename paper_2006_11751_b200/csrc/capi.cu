@@ -144,6 +144,10 @@ int appo_ctx_destroy(appo_ctx* ctx) {
   if (ctx->model) appo_b200::reader_release(ctx);
   if (ctx->model && ctx->owns_model) model_destroy(ctx);
   appo_b200::dp_destroy(ctx);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_red);

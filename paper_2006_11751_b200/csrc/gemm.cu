@@ -1304,33 +1304,45 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
 __global__ void __launch_bounds__(256)
     splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
   APPO_PDL_ENTRY();
+  // lane = 4 consecutive outputs (16-byte loads, 512 B per warp and split),
+  // warp g = splits g, g+8, ... with 4 loads in flight; the 8 warp sums are
+  // then added in warp order (deterministic)
   const int64_t total = (int64_t)M * N;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
-  float s = 0.0f;
+  const int64_t i = ((int64_t)blockIdx.x * 32 + lane) * 4;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (i < total) {
-    // every load of the thread's group in flight at once (<= 160 splits: one
-    // memory round trip), then the adds in split order
+    const float4* p = reinterpret_cast<const float4*>(partial + (size_t)g * total + i);
+    const size_t step = (size_t)2 * total;  // 8 splits, in float4 units
     int z = g;
-    for (; z < splits; z += 8 * 20) {
-      float a[20];
-#pragma unroll
-      for (int k = 0; k < 20; ++k)
-        a[k] = z + 8 * k < splits ? __ldg(partial + (size_t)(z + 8 * k) * total + i) : 0.0f;
-#pragma unroll
-      for (int k = 0; k < 20; ++k)
-        if (z + 8 * k < splits) s += a[k];
+    for (; z + 24 < splits; z += 32, p += 4 * step) {
+      const float4 a0 = __ldg(p), a1 = __ldg(p + step), a2 = __ldg(p + 2 * step),
+                   a3 = __ldg(p + 3 * step);
+      s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
+      s.x += a1.x; s.y += a1.y; s.z += a1.z; s.w += a1.w;
+      s.x += a2.x; s.y += a2.y; s.z += a2.z; s.w += a2.w;
+      s.x += a3.x; s.y += a3.y; s.z += a3.z; s.w += a3.w;
+    }
+    for (; z < splits; z += 8, p += step) {
+      const float4 a0 = __ldg(p);
+      s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
     }
   }
-  __shared__ float sh[8][33];
+  __shared__ float4 sh[8][32];
   sh[g][lane] = s;
   __syncthreads();
-  if (g == 0 && i < total) {
-    float t = 0.0f;
+  if (g != 0 || i >= total) return;
+  float4 t = sh[0][lane];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][lane];
-    const int m = (int)(i / N), n = (int)(i % N);
-    float x = t * e.scale;
+  for (int k = 1; k < 8; ++k) {
+    const float4 u = sh[k][lane];
+    t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+  }
+  const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int m = (int)((i + q) / N), n = (int)((i + q) % N);
+    float x = tv[q] * e.scale;
     if (e.flags & EPI_BIAS) x += e.bias[n];
     const size_t o = (e.flags & EPI_TRANS) ? (size_t)n * e.ldo + m : (size_t)m * e.ldo + n;
     float* dst = reinterpret_cast<float*>(e.out) + o;
@@ -1366,16 +1378,36 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Any shape (M*N not a multiple of 4): one thread per output, splits in order.
+__global__ void __launch_bounds__(256)
+    splitk_reduce1_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
+  APPO_PDL_ENTRY();
+  const int64_t total = (int64_t)M * N;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  float t = 0.0f;
+  for (int z = 0; z < splits; ++z) t += __ldg(partial + (size_t)z * total + i);
+  const int m = (int)(i / N), n = (int)(i % N);
+  float x = t * e.scale;
+  if (e.flags & EPI_BIAS) x += e.bias[n];
+  const size_t o = (e.flags & EPI_TRANS) ? (size_t)n * e.ldo + m : (size_t)m * e.ldo + n;
+  float* dst = reinterpret_cast<float*>(e.out) + o;
+  *dst = (e.flags & EPI_ACCUM) ? *dst + x : x;
+}
+
 int launch_splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial,
                          const Epilogue& epi) {
   const int64_t total = (int64_t)M * N;
   c->next_bytes = (double)splits * total * 4 + (double)total * 4;
-  if (splits <= 16 && total % 4 == 0) {
+  if (total % 4 != 0) {
+    APPO_LAUNCH(c, splitk_reduce1_kernel, (int)((total + 255) / 256), 256, 0, M, N, splits,
+                partial, epi);
+  } else if (splits <= 16) {
     APPO_LAUNCH(c, splitk_reduce4_kernel, (int)((total / 4 + 255) / 256), 256, 0, M, N, splits,
                 partial, epi);
   } else {
-    APPO_LAUNCH(c, splitk_reduce_kernel, (int)((total + 31) / 32), 256, 0, M, N, splits, partial,
-                epi);
+    APPO_LAUNCH(c, splitk_reduce_kernel, (int)((total / 4 + 31) / 32), 256, 0, M, N, splits,
+                partial, epi);
   }
   return APPO_OK;
 }

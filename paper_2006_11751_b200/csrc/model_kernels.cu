@@ -280,10 +280,12 @@ __global__ void gru_train_kernel(int n_traj, int T, int t, const float* __restri
   if (t < T) hcur[g] = done[(int64_t)i * T + t] ? 0.0f : h;
 }
 
-// Heads forward: one warp per row.
 // Heads forward, warp per row; rows < B also get the target log-probability of
 // the stored action and the policy entropy (log_prob_and_entropy,
 // policy.hpp:262-281, learner use orchestrator.hpp:803-814) in fp64.
+// AMAX: compile-time bound on the action count (8 covers the Doom head's 6;
+// the loops over actions are unrolled to it, predicated by the runtime A).
+template <int AMAX>
 __global__ void __launch_bounds__(256)
     heads_fwd_kernel(int64_t R, int A, const float* __restrict__ core,
                      const float* __restrict__ wpi, const float* __restrict__ bpi,
@@ -295,9 +297,9 @@ __global__ void __launch_bounds__(256)
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= R) return;
-  float acc[kMaxActions + 1];
+  float acc[AMAX + 1];
 #pragma unroll
-  for (int a = 0; a <= kMaxActions; ++a) acc[a] = 0.0f;
+  for (int a = 0; a <= AMAX; ++a) acc[a] = 0.0f;
   // lane owns units 4 j4 .. 4 j4 + 3, j4 = lane + 32 q (float4 rows; wv sits at
   // an odd parameter offset: scalar loads)
   const float4* crow = reinterpret_cast<const float4*>(core + row * kHidden);
@@ -306,26 +308,26 @@ __global__ void __launch_bounds__(256)
     const int j4 = lane + 32 * q;
     const float4 h = __ldg(crow + j4);
 #pragma unroll
-    for (int a = 0; a < kMaxActions; ++a)
+    for (int a = 0; a < AMAX; ++a)
       if (a < A) {
         const float4 w = __ldg(reinterpret_cast<const float4*>(wpi + a * kHidden) + j4);
         acc[a] += w.x * h.x + w.y * h.y + w.z * h.z + w.w * h.w;
       }
-    acc[kMaxActions] += __ldg(wv + 4 * j4) * h.x + __ldg(wv + 4 * j4 + 1) * h.y +
+    acc[AMAX] += __ldg(wv + 4 * j4) * h.x + __ldg(wv + 4 * j4 + 1) * h.y +
                         __ldg(wv + 4 * j4 + 2) * h.z + __ldg(wv + 4 * j4 + 3) * h.w;
   }
 #pragma unroll
-  for (int a = 0; a < kMaxActions; ++a)
+  for (int a = 0; a < AMAX; ++a)
     if (a < A) acc[a] = warp_sum(acc[a]);
-  acc[kMaxActions] = warp_sum(acc[kMaxActions]);
+  acc[AMAX] = warp_sum(acc[AMAX]);
   // lane a < A holds logit a (all lanes hold the sums after warp_sum)
   float my = 0.0f;
 #pragma unroll
-  for (int a = 0; a < kMaxActions; ++a)
+  for (int a = 0; a < AMAX; ++a)
     if (a == lane) my = acc[a];
   const float lgf = lane < A ? my + bpi[lane] : -INFINITY;
   if (lane < A) logits[row * A + lane] = lgf;
-  if (lane == 0) values[row] = acc[kMaxActions] + bv[0];
+  if (lane == 0) values[row] = acc[AMAX] + bv[0];
   if (act && row < B) {
     const int ac = act[row];
     if (ac < 0 || ac >= A) {
@@ -409,8 +411,11 @@ __global__ void normalize_kernel(int n, float* __restrict__ adv) {
 }
 
 // Fused PPO / value / entropy loss and its gradient wrt logits and value
-// (policy.hpp:323-375).  One thread per sample; partial sums (policy, value,
-// entropy, ratio) -> deterministic last-block reduce into stats[0..4].
+// (policy.hpp:323-375).  LPS lanes per sample (lane a owns action a, lane A the
+// value gradient): the fp64 log-softmax / entropy run across the lane group
+// instead of serially in one thread; partial sums (policy, value, entropy,
+// ratio, lag) -> deterministic last-block reduce into stats[0..7].
+template <int LPS>
 __global__ void __launch_bounds__(256)
     ppo_loss_kernel(int B, int A, const float* __restrict__ logits,
                     const float* __restrict__ values, const int32_t* __restrict__ act,
@@ -419,30 +424,33 @@ __global__ void __launch_bounds__(256)
                     uint16_t* __restrict__ dhead, double* partials, unsigned* counter,
                     double* stats, int* flags, const int64_t* __restrict__ ver, int64_t cur) {
   APPO_PDL_ENTRY();
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x & (LPS - 1);
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) / LPS;
   // policy, value, entropy, ratio sums; version-lag sum and max (orchestrator.hpp:790,862-863)
   double acc[6] = {0, 0, 0, 0, 0, -1e300};
-  if (s < B) {
-    const float* lg = logits + (int64_t)s * A;
+  if (s < B) {  // whole lane groups: every lane of a group takes this branch together
+    const unsigned gm = (LPS == 32 ? 0xffffffffu : ((1u << LPS) - 1u) << (threadIdx.x & 31 & ~(LPS - 1)));
     const int a_s = act[s];
-    if (a_s < 0 || a_s >= A) atomicOr(flags + kFlagContract, 1);
-    // fp64 log-softmax: one exp per action and a single log
-    double mx = lg[0];
-    for (int a = 1; a < A; ++a) mx = fmax(mx, (double)lg[a]);
-    double ex[kMaxActions], z = 0;
-    for (int a = 0; a < A; ++a) {
-      ex[a] = exp((double)lg[a] - mx);
-      z += ex[a];
-    }
-    const double lz = log(z);
-    double p[kMaxActions], lp[kMaxActions], H = 0;
-    for (int a = 0; a < A; ++a) {
-      p[a] = ex[a] / z;
-      lp[a] = ((double)lg[a] - mx) - lz;
-      if (p[a] > 0) H -= p[a] * lp[a];
-    }
+    if (sub == 0 && (a_s < 0 || a_s >= A)) atomicOr(flags + kFlagContract, 1);
     const int ac = min(max(a_s, 0), A - 1);
-    const double logp = fmax(lp[ac], -690.7755278982137);  // log(1e-300) floor
+    const bool mine = sub < A;
+    const double l = mine ? (double)logits[(int64_t)s * A + sub] : -1e300;
+    // fp64 log-softmax over the lane group: one exp per action, a single log
+    double mx = l;
+#pragma unroll
+    for (int o = LPS / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(gm, mx, o, LPS));
+    const double ex = mine ? exp(l - mx) : 0.0;
+    double z = ex;
+#pragma unroll
+    for (int o = LPS / 2; o > 0; o >>= 1) z += __shfl_xor_sync(gm, z, o, LPS);
+    const double lz = log(z);
+    const double p = ex / z;
+    const double lp = (l - mx) - lz;
+    double H = (mine && p > 0) ? -p * lp : 0.0;
+#pragma unroll
+    for (int o = LPS / 2; o > 0; o >>= 1) H += __shfl_xor_sync(gm, H, o, LPS);
+    const double lpa = __shfl_sync(gm, lp, ac, LPS);
+    const double logp = fmax(lpa, -690.7755278982137);  // log(1e-300) floor
     double d = logp - (double)blogp[s];
     d = fmin(fmax(d, -20.0), 20.0);
     const double ratio = exp(d);
@@ -454,22 +462,27 @@ __global__ void __launch_bounds__(256)
     const double dL_dlogp = -invB * dsur * ratio;
     const double verr = (double)values[s] - (double)vt[s];
     const double dV = hp.value_coef * invB * 2.0 * verr;
-    for (int a = 0; a < A; ++a) {
-      const double dlp = (a == ac ? 1.0 : 0.0) - p[a];
-      const double dH = p[a] > 0 ? -p[a] * (lp[a] + H) : 0.0;
-      const float g = (float)(dL_dlogp * dlp - hp.entropy_coef * invB * dH);
-      dlog[(int64_t)s * (A + 1) + a] = g;
-      dhead[(int64_t)s * 16 + a] = f2bf(g);
+    float gsub = 0.0f;
+    if (mine) {
+      const double dlp = (sub == ac ? 1.0 : 0.0) - p;
+      const double dH = p > 0 ? -p * (lp + H) : 0.0;
+      gsub = (float)(dL_dlogp * dlp - hp.entropy_coef * invB * dH);
+      dlog[(int64_t)s * (A + 1) + sub] = gsub;
+    } else if (sub == A) {
+      gsub = (float)dV;
+      dlog[(int64_t)s * (A + 1) + A] = gsub;
     }
-    dlog[(int64_t)s * (A + 1) + A] = (float)dV;
-    dhead[(int64_t)s * 16 + A] = f2bf((float)dV);
-    for (int a = A + 1; a < 16; ++a) dhead[(int64_t)s * 16 + a] = 0;
-    acc[0] = -sur;
-    acc[1] = verr * verr;
-    acc[2] = H;
-    acc[3] = ratio;
-    acc[4] = (double)(cur - ver[s]);
-    acc[5] = (double)(cur - ver[s]);
+    // bf16 head-gradient row, 16 wide: dlogits, dV, zeros
+#pragma unroll
+    for (int col = sub; col < 16; col += LPS) dhead[(int64_t)s * 16 + col] = col <= A ? f2bf(gsub) : 0;
+    if (sub == 0) {
+      acc[0] = -sur;
+      acc[1] = verr * verr;
+      acc[2] = H;
+      acc[3] = ratio;
+      acc[4] = (double)(cur - ver[s]);
+      acc[5] = (double)(cur - ver[s]);
+    }
   }
   // block reduce + last block
   __shared__ double sh[8][6];
@@ -540,6 +553,7 @@ __global__ void __launch_bounds__(256)
 // memory round trip per chunk instead of one per row); per-block partials are
 // summed in block order by heads_grad_reduce_kernel (deterministic).
 constexpr int kHbRows = 16;
+template <int AMAX>
 __global__ void __launch_bounds__(512)
     heads_bwd_fused_kernel(int B, int A, const float* __restrict__ dlog,
                            const float* __restrict__ core, const float* __restrict__ wpi,
@@ -547,14 +561,14 @@ __global__ void __launch_bounds__(512)
                            float* __restrict__ part, unsigned* counter, float* gwpi, float* gbpi,
                            float* gwv, float* gbv) {
   APPO_PDL_ENTRY();
-  __shared__ float sdl[kHbRows][kMaxActions + 1];
+  __shared__ float sdl[kHbRows][AMAX + 1];
   const int j = threadIdx.x;
   const int A1 = A + 1;
   const int rows = (B + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * rows, r1 = min(B, r0 + rows);
-  float w[kMaxActions + 1], sw[kMaxActions + 1], sb = 0.0f;
+  float w[AMAX + 1], sw[AMAX + 1], sb = 0.0f;
 #pragma unroll
-  for (int a = 0; a <= kMaxActions; ++a) {
+  for (int a = 0; a <= AMAX; ++a) {
     w[a] = a < A ? wpi[a * kHidden + j] : (a == A ? wv[j] : 0.0f);
     sw[a] = 0.0f;
   }
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(512)
       if (r < nr) {
         float dc = 0.0f;
 #pragma unroll
-        for (int a = 0; a <= kMaxActions; ++a) {
+        for (int a = 0; a <= AMAX; ++a) {
           if (a < A1) {
             const float g = sdl[r][a];
             dc += g * w[a];
@@ -588,30 +602,41 @@ __global__ void __launch_bounds__(512)
   }
   float* pb = part + (size_t)blockIdx.x * (A1 * kHidden + A1);
 #pragma unroll
-  for (int a = 0; a <= kMaxActions; ++a)
+  for (int a = 0; a <= AMAX; ++a)
     if (a < A1) pb[a * kHidden + j] = sw[a];
   if (j < A1) pb[A1 * kHidden + j] = sb;
 }
 
-// Sums the per-block head-gradient partials in block order (thread per
-// output); loads are issued 16 at a time ahead of the in-order adds.
+// Sums the per-block head-gradient partials in a fixed order: block = 32
+// outputs x 8 warps, warp g sums blocks g, g+8, ... (loads issued 8 ahead),
+// then the 8 warp sums are added in warp order (deterministic).
 __global__ void __launch_bounds__(256)
     heads_grad_reduce_kernel(int A, int nb, const float* __restrict__ part, float* gwpi,
                              float* gbpi, float* gwv, float* gbv) {
   APPO_PDL_ENTRY();
+  __shared__ float sh[8][33];
   const int A1 = A + 1;
   const int stride = A1 * kHidden + A1;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= stride) return;
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + lane;
   float t = 0.0f;
-  for (int b0 = 0; b0 < nb; b0 += 16) {
-    float x[16];
+  if (o < stride) {
+    for (int b0 = g; b0 < nb; b0 += 64) {
+      float x[8];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) x[k] = b0 + k < nb ? __ldg(part + (size_t)(b0 + k) * stride + o) : 0.0f;
+      for (int k = 0; k < 8; ++k)
+        x[k] = b0 + 8 * k < nb ? __ldg(part + (size_t)(b0 + 8 * k) * stride + o) : 0.0f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (b0 + k < nb) t += x[k];
+      for (int k = 0; k < 8; ++k)
+        if (b0 + 8 * k < nb) t += x[k];
+    }
   }
+  sh[g][lane] = t;
+  __syncthreads();
+  if (g != 0 || o >= stride) return;
+  t = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t += sh[k][lane];
   if (o < A * kHidden) gwpi[o] = t;
   else if (o < A1 * kHidden) gwv[o - A * kHidden] = t;
   else if (o - A1 * kHidden < A) gbpi[o - A1 * kHidden] = t;
@@ -760,8 +785,14 @@ int k_heads_fwd(Ctx* c, int64_t R, int A, const float* core, const float* wpi, c
                 const int32_t* act, float* tlogp, float* ent) {
   APPO_REQUIRE(((reinterpret_cast<uintptr_t>(core) | reinterpret_cast<uintptr_t>(wpi)) & 15) == 0,
                APPO_ERR_CONTRACT, "heads: core / policy head must be 16-byte aligned");
-  APPO_LAUNCH(c, heads_fwd_kernel, (int)((R + 7) / 8), 256, 0, R, A, core, wpi, bpi, wv, bv,
-              logits, values, B, act, tlogp, ent, c->d_flags);
+  c->next_name = "heads_fwd_kernel";
+  if (A <= 8)
+    APPO_LAUNCH(c, heads_fwd_kernel<8>, (int)((R + 7) / 8), 256, 0, R, A, core, wpi, bpi, wv, bv,
+                logits, values, B, act, tlogp, ent, c->d_flags);
+  else
+    APPO_LAUNCH(c, heads_fwd_kernel<kMaxActions>, (int)((R + 7) / 8), 256, 0, R, A, core, wpi, bpi,
+                wv, bv, logits, values, B, act, tlogp, ent, c->d_flags);
+  c->next_name = nullptr;
   return APPO_OK;
 }
 int k_gather_slots(Ctx* c, int n_traj, int T, const uint8_t* region, uint64_t slot_bytes,
@@ -779,14 +810,21 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
                const int32_t* act, const float* blogp, const float* adv, const float* vt,
                const LossHP& hp, float* dlog, uint16_t* dhead, double* stats, const int64_t* ver,
                int64_t cur) {
-  // 64-thread blocks: the per-row fp64 softmax is latency-bound, spread it over SMs
-  const int grid = (B + 63) / 64;
+  // lane groups of 8 (A <= 7) or 16 per sample, 256-thread blocks
+  const int lps = A < 8 ? 8 : 16;
+  const int grid = (B + 256 / lps - 1) / (256 / lps);
   APPO_REQUIRE(grid * 6 <= kRedSlots, APPO_ERR_CONTRACT, "ppo_loss: batch too large");
   // in: logits, value, action, behaviour logp, advantage, v-target, version;
   // out: dlogits + dV (fp32) and the bf16 head-gradient row (16 wide)
   c->next_bytes = (double)B * (A * 4 + 28 + (A + 1) * 4 + 32);
-  APPO_LAUNCH(c, ppo_loss_kernel, grid, 64, 0, B, A, logits, values, act, blogp, adv, vt, hp,
-              dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
+  c->next_name = "ppo_loss_kernel";
+  if (lps == 8)
+    APPO_LAUNCH(c, ppo_loss_kernel<8>, grid, 256, 0, B, A, logits, values, act, blogp, adv, vt, hp,
+                dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
+  else
+    APPO_LAUNCH(c, ppo_loss_kernel<16>, grid, 256, 0, B, A, logits, values, act, blogp, adv, vt,
+                hp, dlog, dhead, c->d_red, c->d_counter + 2, stats, c->d_flags, ver, cur);
+  c->next_name = nullptr;
   return APPO_OK;
 }
 int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core,
@@ -795,10 +833,16 @@ int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core
   int grid = (B + 15) / 16;  // 16 rows per block
   if (grid > 160) grid = 160;
   if (grid < 1) grid = 1;
-  APPO_LAUNCH(c, heads_bwd_fused_kernel, grid, 512, 0, B, A, dlog, core, wpi, wv, dcore, part,
-              c->d_counter + 7, gwpi, gbpi, gwv, gbv);
+  c->next_name = "heads_bwd_fused_kernel";
+  if (A < 8)
+    APPO_LAUNCH(c, heads_bwd_fused_kernel<7>, grid, 512, 0, B, A, dlog, core, wpi, wv, dcore,
+                part, c->d_counter + 7, gwpi, gbpi, gwv, gbv);
+  else
+    APPO_LAUNCH(c, heads_bwd_fused_kernel<kMaxActions>, grid, 512, 0, B, A, dlog, core, wpi, wv,
+                dcore, part, c->d_counter + 7, gwpi, gbpi, gwv, gbv);
+  c->next_name = nullptr;
   const int outs = (A + 1) * (kHidden + 1);
-  APPO_LAUNCH(c, heads_grad_reduce_kernel, (outs + 255) / 256, 256, 0, A, grid, part, gwpi, gbpi,
+  APPO_LAUNCH(c, heads_grad_reduce_kernel, (outs + 31) / 32, 256, 0, A, grid, part, gwpi, gbpi,
               gwv, gbv);
   return APPO_OK;
 }

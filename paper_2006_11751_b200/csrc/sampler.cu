@@ -48,11 +48,10 @@ struct appo_sampler {
   float* values = nullptr;
   uint64_t steps_done = 0;
   appo_slotq* ready_q = nullptr;  // sealed slots are pushed here at t == T-1
-  // host observations (CPU actors): contiguous pinned -> device copies on an
-  // internal copy stream into two staging buffers, so step t+1's transfer
+  // host observations (CPU actors): contiguous pinned -> device copies on the
+  // context's copy stream into two staging buffers, so step t+1's transfer
   // overlaps step t's inference; a scatter kernel on the ctx stream moves them
   // into the slots (region writes stay ordered on the ctx stream)
-  cudaStream_t copy_stream = nullptr;
   uint8_t* staging[2] = {nullptr, nullptr};
   cudaEvent_t copied[2] = {nullptr, nullptr};
   cudaEvent_t consumed[2] = {nullptr, nullptr};
@@ -264,8 +263,9 @@ int stage_host_obs(appo_sampler* s, const uint8_t* h_obs, uint8_t* region, uint6
     return APPO_OK;
   }
   const size_t bytes = (size_t)s->n_envs * d.obs_dim;
-  if (!s->copy_stream) {
-    APPO_CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+  if (!c->copy_stream)
+    APPO_CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!s->staging[0]) {
     for (int k = 0; k < 2; ++k) {
       APPO_CUDA_TRY(cudaMalloc(&s->staging[k], bytes));
       APPO_CUDA_TRY(cudaEventCreateWithFlags(&s->copied[k], cudaEventDisableTiming));
@@ -276,10 +276,10 @@ int stage_host_obs(appo_sampler* s, const uint8_t* h_obs, uint8_t* region, uint6
   const int k = s->stage_next;
   s->stage_next ^= 1;
   // the buffer's previous contents were scattered (ctx stream) before it is refilled
-  APPO_CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->consumed[k], 0));
+  APPO_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, s->consumed[k], 0));
   APPO_CUDA_TRY(cudaMemcpyAsync(s->staging[k], h_obs, bytes, cudaMemcpyHostToDevice,
-                                s->copy_stream));
-  APPO_CUDA_TRY(cudaEventRecord(s->copied[k], s->copy_stream));
+                                c->copy_stream));
+  APPO_CUDA_TRY(cudaEventRecord(s->copied[k], c->copy_stream));
   APPO_CUDA_TRY(cudaStreamWaitEvent(c->stream, s->copied[k], 0));
   const dim3 grid((unsigned)std::min<int64_t>(((d.obs_dim >> 4) + 255) / 256, 8),
                   (unsigned)s->n_envs);
@@ -348,10 +348,7 @@ APPO_API int appo_sampler_destroy(appo_sampler* s) {
     if (s->copied[k]) cudaEventDestroy(s->copied[k]);
     if (s->consumed[k]) cudaEventDestroy(s->consumed[k]);
   }
-  if (s->copy_stream) {
-    cudaStreamSynchronize(s->copy_stream);
-    cudaStreamDestroy(s->copy_stream);
-  }
+  if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
   if (s->fb_host) cudaFreeHost(s->fb_host);
   if (s->fb_dev) cudaFree(s->fb_dev);
   for (int k = 0; k < 2; ++k)
