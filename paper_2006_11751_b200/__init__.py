@@ -51,6 +51,11 @@ _ERRS = {1: ContractError, 2: ConfigError, 3: NumericError, 4: ResourceError}
 
 
 def _load():
+    global LIB_PATH
+    alt = os.environ.get("APPO_LIB")  # A/B diagnostics: another in-tree build of this library
+    if alt:
+        LIB_PATH = os.path.abspath(alt)
+        return C.CDLL(LIB_PATH)
     from . import _build
     if _build.needs_build():  # missing or older than its sources: rebuild in-tree
         _build.build()

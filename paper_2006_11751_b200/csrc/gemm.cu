@@ -721,6 +721,8 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
                      const __grid_constant__ CUtensorMap mapB, const __grid_constant__ KParams p) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
+  // 1024-B aligned base (generic addressing of the staged epilogue values;
+  // the LDS/STS form measured slower for conv1: 133 -> 138 us, scripts/gpu_ab.sh)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   // stage ring (AG_TAPS: A only, the whole B operand stays resident after it)

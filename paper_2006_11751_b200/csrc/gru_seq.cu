@@ -145,9 +145,17 @@ struct FwdArgs {
   long long* prof;       // optional phase timestamps (APPO_GRU_PROF): [steps][4]
 };
 
+// per-step phase stamps of block 0 (APPO_GRU_PROF=1 diagnostics), 8 per step
+#define FSTAMP(k)                                                     \
+  do {                                                                \
+    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 8 + (k)] = clock64(); \
+  } while (0)
 __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_constant__ FwdArgs a) {
   APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
+  // 1024-B aligned base.  Generic (integer round trip) addressing is kept on
+  // purpose: the LDS/STS form measured slower (GRU forward 138 -> 163 us, same
+  // box A/B, scripts/gpu_ab.sh)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* tA = sm;
@@ -225,7 +233,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
   uint32_t phase = 0;
 
   for (int t = 0; t <= a.T; ++t) {
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 0] = clock64();
+    FSTAMP(0);
     const size_t nxt = (size_t)((t + 1) & 1) * a.n_traj * kHidden;
     // h_t (written by every CTA before the barrier) -> smem by TMA, one K block
     // per mbarrier so the MMAs start on the first block while the rest land
@@ -239,7 +247,6 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
                                 0, t & 1);
       }
     }
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 1] = clock64();
     if (warp == 0) {  // whole warp: elect.sync inside (no per-MMA waterfall)
       const uint32_t a0 = sm100::smem_u32(tA), b0 = sm100::smem_u32(tB);
 #pragma unroll
@@ -255,37 +262,52 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
         }
       }
       sm100::umma_commit_warp(mbar);
+      FSTAMP(1);
     }
     sm100::mbar_wait(mbar, phase);
     phase ^= 1;
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
+    FSTAMP(2);
     sm100::tc_fence_after();
     if (warp < 4) {  // M=128 accumulator: TMEM lane = row = trajectory + 64 * half
-      uint32_t r[16];
+      uint32_t r[NG];
       const int row = 32 * warp + lane;
       float* dst = warp < 2 ? gh + row * NG : gh2 + (row - MAXTRAJ) * NG;
       const int c0 = warp < 2 ? 0 : NG;  // diagonal block of the row's K half
+      // all three column blocks in flight, one wait
 #pragma unroll
-      for (int cb = 0; cb < NG; cb += 16) {
-        sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0 + cb, r);
-        sm100::tmem_ld_wait();
+      for (int cb = 0; cb < NG; cb += 16)
+        sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c0 + cb,
+                         *reinterpret_cast<uint32_t(*)[16]>(r + cb));
+      sm100::tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 16; ++q) dst[cb + q] = __uint_as_float(r[q]);
-      }
+      for (int q = 0; q < NG; ++q) dst[q] = __uint_as_float(r[q]);
     }
     sm100::tc_fence_before();
     __syncthreads();
+    FSTAMP(3);
     // the cell; only the exchange (next h, bf16) is stored before the barrier
     // arrive -- the rest of the step's outputs are stored while it completes
     float cv[CPT][6];  // r, z, n, ghn, h_prev, h
+    // every cell's gate pre-activations first: the exchange stores below may
+    // not be reordered above these (generic addressing), so loading them per
+    // cell would serialise the cells
+    float ghv[CPT][3];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = tid + c * THR;
+      const int i = (e < n_cells ? e : 0) / UPC_F, u = e % UPC_F;
+#pragma unroll
+      for (int g = 0; g < 3; ++g)
+        ghv[c][g] = (gh[i * NG + g * UPC_F + u] + gh2[i * NG + g * UPC_F + u]) + b3[c][g];
+    }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int e = tid + c * THR;
       if (e >= n_cells) continue;
       const int i = e / UPC_F, u = e % UPC_F, j = j0 + u;
-      const float ghr = (gh[i * NG + u] + gh2[i * NG + u]) + b3[c][0];
-      const float ghz = (gh[i * NG + UPC_F + u] + gh2[i * NG + UPC_F + u]) + b3[c][1];
-      const float ghn = (gh[i * NG + 2 * UPC_F + u] + gh2[i * NG + 2 * UPC_F + u]) + b3[c][2];
+      const float ghr = ghv[c][0];
+      const float ghz = ghv[c][1];
+      const float ghn = ghv[c][2];
       const float rr = sig_(g3[c][0] + ghr);
       const float z = sig_(g3[c][1] + ghz);
       const float n = tanh_(g3[c][2] + rr * ghn);
@@ -303,10 +325,13 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
         a.hbuf_bf[nxt + (int64_t)i * kHidden + j] = f2bf_(hn);
       }
     }
+    FSTAMP(4);
     if (t < a.T) {
       fence_proxy_async_global();
+      FSTAMP(5);
       grid_arrive(a.bar);
     }
+    FSTAMP(6);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int e = tid + c * THR;
@@ -323,7 +348,7 @@ __global__ void __launch_bounds__(THR, 1) gru_seq_fwd_kernel(const __grid_consta
       a.hin[row * kHidden + j] = cv[c][4];
       a.hbf[row * kHidden + j] = f2bf_(cv[c][4]);
     }
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 3] = clock64();
+    FSTAMP(7);
     if (t < a.T) {
       prefetch(t + 1);  // independent of the exchange: overlaps the barrier
       grid_wait(a.bar, ++epoch * gridDim.x);
@@ -364,6 +389,9 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __global__ void __launch_bounds__(THR, 1) gru_seq_bwd_kernel(const __grid_constant__ BwdArgs a) {
   APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
+  // 1024-B aligned base.  Generic (integer round trip) addressing is kept on
+  // purpose: the LDS/STS form measured slower (GRU forward 138 -> 163 us, same
+  // box A/B, scripts/gpu_ab.sh)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* tA = sm;                                      // 3 x 64 KB: all of dgh_t
@@ -650,6 +678,9 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THR, 1)
     gru_cl_fwd_kernel(const __grid_constant__ ClFwdArgs a) {
   APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
+  // 1024-B aligned base.  Generic (integer round trip) addressing is kept on
+  // purpose: the LDS/STS form measured slower (GRU forward 138 -> 163 us, same
+  // box A/B, scripts/gpu_ab.sh)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* tB = sm;                 // W slice (SW128 K-major)
@@ -831,9 +862,27 @@ static_assert(BWD_SMEM <= 227 * 1024, "backward GRU smem");
 long long* prof_buffer(Ctx* c) {
   static long long* buf = nullptr;
   if (!getenv("APPO_GRU_PROF")) return nullptr;
-  if (!buf && cudaMalloc(&buf, sizeof(long long) * 4 * 64) != cudaSuccess) return nullptr;
-  cudaMemsetAsync(buf, 0, sizeof(long long) * 4 * 64, c->stream);
+  if (!buf && cudaMalloc(&buf, sizeof(long long) * 8 * 64) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(buf, 0, sizeof(long long) * 8 * 64, c->stream);
   return buf;
+}
+// forward stamps: 8 per step; prints the mean cycles of each phase
+void prof_report8(Ctx* c, long long* d, int steps, const char* what) {
+  long long h[8 * 64];
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(h, d, sizeof(long long) * 8 * steps, cudaMemcpyDeviceToHost);
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int n = 0;
+  for (int t = 0; t + 1 < steps; ++t) {
+    const long long* a = h + 8 * t;
+    if (!a[0] || !a[7] || !h[8 * (t + 1)]) continue;
+    for (int k = 0; k < 7; ++k) acc[k] += a[k + 1] - a[k];
+    acc[7] += h[8 * (t + 1)] - a[7];
+    ++n;
+  }
+  fprintf(stderr, "[gru prof] %s (cycles/step, %d steps):", what, n);
+  for (int k = 0; k < 8; ++k) fprintf(stderr, " %.0f", acc[k] / (n ? n : 1));
+  fprintf(stderr, "\n");
 }
 void prof_report(Ctx* c, long long* d, int steps, const char* what) {
   long long h[4 * 64];
@@ -937,7 +986,10 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T + 1);
   timing_end(c, "gru_seq_fwd_kernel", ev);
   c->launches++;
-  if (prof) prof_report(c, prof, T + 1, "fwd: stage | mma | epilogue+barrier");
+  if (prof)
+    prof_report8(c, prof, T + 1,
+                 "fwd: tma+mma issue | mma wait | tmem->smem | cell+xchg store | proxy fence | "
+                 "arrive | outputs | prefetch+barrier wait");
   return APPO_OK;
 }
 
