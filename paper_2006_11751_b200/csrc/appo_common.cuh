@@ -69,6 +69,11 @@ struct Ctx {
   // issue order on one stream: groups' transfers queue back to back instead
   // of splitting the link (sampler.cu)
   cudaStream_t copy_stream = nullptr;
+  // GRU recurrence kernels (gru_seq.cu): per-group step counters (fwd [0, 4),
+  // bwd [4, 8)), bias-gradient combine counters [32, 64), per-group bias
+  // partial sums [4][512][4]; allocated zeroed on first use
+  unsigned* d_gru_sync = nullptr;
+  float* d_gru_part = nullptr;
 };
 constexpr int kRedSlots = 148 * 8 * 16;
 

@@ -148,6 +148,8 @@ int appo_ctx_destroy(appo_ctx* ctx) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
   }
+  cudaFree(ctx->d_gru_sync);
+  cudaFree(ctx->d_gru_part);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_red);
