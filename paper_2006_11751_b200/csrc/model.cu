@@ -872,7 +872,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   g.ldo = kGates;
   if (seq)
     TRY(k_gru_seq_fwd(ctx, n_traj, T, s.gi, wb + d.off_whh, th + d.off_bhh, s.done, s.hcur,
-                      s.hcur_bf, s.core, s.core_bf, s.gates, s.hin, s.hbf, ctx->d_counter + 4));
+                      s.hcur_bf, s.core, s.core_bf, s.gates, s.hin, s.hbf));
   for (int t = 0; !seq && t <= T; ++t) {
     TRY(k_stage_h(ctx, n_traj, T, t, s.hcur, s.hin, s.hbf));
     const uint16_t* a = (t < T) ? s.hbf + (size_t)t * kHidden : s.hbf + (size_t)B * kHidden;
@@ -925,7 +925,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   // ---- BPTT through the GRU ----
   if (seq)
     TRY(k_gru_seq_bwd(ctx, n_traj, T, s.dcore, s.done, s.gates, s.hin, wb + d.off_whh, s.dghx,
-                      s.dgi, s.dgh, G + d.off_bih, G + d.off_bhh, ctx->d_counter + 5));
+                      s.dgi, s.dgh, G + d.off_bih, G + d.off_bhh));
   else
     APPO_CUDA_TRY(cudaMemsetAsync(s.dnext, 0, sizeof(float) * n_traj * kHidden, st));
   if (!seq) {

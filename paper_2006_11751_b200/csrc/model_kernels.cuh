@@ -74,11 +74,10 @@ int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, f
 int gru_seq_supported(int n_traj);
 int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* whh,
                   const float* bhh, const uint8_t* done, float* hbuf, uint16_t* hbuf_bf,
-                  float* core, uint16_t* core_bf, float* gates, float* hin, uint16_t* hbf,
-                  unsigned* bar);
+                  float* core, uint16_t* core_bf, float* gates, float* hin, uint16_t* hbf);
 // also writes the bias gradients gb_ih / gb_hh (sums of the gate gradients)
 int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* done,
                   const float* gates, const float* hin, const uint16_t* whh, uint16_t* dghx,
-                  uint16_t* dgi, uint16_t* dgh, float* gbih, float* gbhh, unsigned* bar);
+                  uint16_t* dgi, uint16_t* dgh, float* gbih, float* gbhh);
 
 }  // namespace appo_b200
