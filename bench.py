@@ -363,13 +363,18 @@ def run_ours(args, ws, rank, local):
     rep = report()
     timing(False)
     total_ms = sum(r["ms"] for r in rep)
-    dom = max(rep, key=lambda r: r["ms"])
+    # the top kernel classes of the warm-up are timed live (the dominant one is
+    # `roofline`, the others `roofline_kernels`); conv1 forward is always among them
+    top = sorted(rep, key=lambda r: -r["ms"])[:4]
+    if not any(r["name"].startswith("conv1_s2d") for r in top):
+        top += [r for r in rep if r["name"].startswith("conv1_s2d")][:1]
+    live_names = "|".join(r["name"] for r in top)
 
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
     l0 = launches()
-    timing(True, dom["name"])
+    timing(True, live_names)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(lstream)
@@ -434,34 +439,41 @@ def run_ours(args, ws, rank, local):
             smp.close()
 
     peaks, peak_src = load_peaks()
-    roof = None
-    if live:
-        d = live[0]
+    ridge = peaks["bf16_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+
+    def roofline(d):
         avg_ms = d["ms"] / d["launches"]
         # bound by arithmetic intensity against the machine balance (measured
-        # peaks): FLOP-heavy GEMMs against the tensor peak, the rest against HBM
-        ridge = peaks["bf16_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+        # peaks): FLOP-heavy kernels against the tensor peak, the rest against HBM
         intensity = d["flops"] / d["bytes"] if d["bytes"] > 0 else float("inf")
         if d["flops"] > 0 and intensity >= ridge:
             achieved = d["flops"] / d["launches"] / (avg_ms * 1e-3) / 1e12
             peak = peaks["bf16_tflops_sustained"]
-            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak}
+            r = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                 "frac": achieved / peak}
         else:
             achieved = d["bytes"] / d["launches"] / (avg_ms * 1e-3) / 1e9
             peak = peaks["hbm_gbs"]
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak}
-        roof.update({"kernel": d["name"], "launches": d["launches"], "avg_us": avg_ms * 1e3,
-                     "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
-                     "algorithmic_flops_per_launch": d["flops"] / d["launches"],
-                     "intensity_flop_per_byte": intensity, "ridge_flop_per_byte": ridge,
-                     "share_of_step": d["ms"] / ms, "peak_source": peak_src,
-                     "note": "sampler and learner overlap on two streams; shares are per-stream "
-                             "busy time over the wall step"})
-        roof["traffic"] = load_traffic(d["name"])
+            r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                 "frac": achieved / peak}
+        r.update({"kernel": d["name"], "launches": d["launches"], "avg_us": avg_ms * 1e3,
+                  "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
+                  "algorithmic_flops_per_launch": d["flops"] / d["launches"],
+                  "intensity_flop_per_byte": intensity, "ridge_flop_per_byte": ridge,
+                  "share_of_step": d["ms"] / ms, "peak_source": peak_src,
+                  "traffic": load_traffic(d["name"])})
+        return r
+
+    roof = None
+    others = []
+    if live:
+        live_sorted = sorted(live, key=lambda r: -r["ms"])
+        roof = roofline(live_sorted[0])
+        roof["note"] = ("sampler and learner overlap on two streams; shares are per-stream "
+                        "busy time over the wall step")
         roof["kernel_shares_warmup"] = {r["name"]: round(r["ms"] / total_ms, 4) for r in
                                         sorted(rep, key=lambda r: -r["ms"])[:8]}
+        others = [roofline(d) for d in live_sorted[1:]]
 
     if rank != 0:
         return
@@ -487,6 +499,7 @@ def run_ours(args, ws, rank, local):
             "samples_per_s": value / args.frameskip,
             "gpu_launches": n_launch,
             "roofline": roof,
+            "roofline_kernels": others,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,

@@ -112,7 +112,8 @@ APPO_API int appo_ctx_sync(appo_ctx* ctx);
 /* Number of launches of this library's kernels enqueued on ctx so far. */
 APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);
 /* Per-launch CUDA-event timing of this library's kernels on the ctx stream
- * (name_filter: only kernels of that name; NULL = all).  The report is JSON
+ * (name_filter: only kernels of that name, or of any of several names
+ * separated by '|'; NULL = all).  The report is JSON
  * lines {"name", "launches", "ms", "flops", "bytes"} (algorithmic work per
  * launch as recorded by the launcher); it synchronizes and resets. */
 APPO_API int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter);

@@ -167,8 +167,9 @@ cudaEvent_t timing_event(Ctx* c);
 int ensure_smem_attr(const void* kernel, int bytes, int device);
 inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
   if (!c->timing) return nullptr;
+  // filter: one kernel class name, or several separated by '|'
   if (!c->timing_filter.empty() && c->timing_filter != "gemm_shapes" &&
-      c->timing_filter.compare(name) != 0)
+      ("|" + c->timing_filter + "|").find("|" + std::string(name) + "|") == std::string::npos)
     return nullptr;
   cudaEvent_t e = timing_event(c);
   cudaEventRecord(e, c->stream);

@@ -1,0 +1,501 @@
+// conv1 forward (k8 s4, u8 CHW observations -> 32 channels, ELU, bf16 NHWC)
+// as a space-to-depth "taps" GEMM on tcgen05 (sm_100a).
+//
+// A k8 s4 convolution is, after space-to-depth by 4 (Z[py][px][c,i,j] =
+// X[c][4py+i][4px+j], C*16 values per s2d pixel), a k2 s1 convolution:
+//   out[y][x] = sum_{a,b in {0,1}} Z[y+a][x+b] . W_ab        (W_ab: [32][C*16])
+// With the s2d rows of a tile stored ONCE in shared memory as a K-major
+// SWIZZLE_128B matrix (one 128-byte row per s2d pixel: its C*16 values, zero
+// padded to 64), the operand "Z shifted by (a, b)" is the same smem matrix with
+// its descriptor start moved by (32a + b) rows.  The two row taps (a) are two
+// MMA chains into ONE TMEM accumulator; the two column taps (b) are the two
+// 32-column halves of an N = 64 B operand [W_a0; W_a1], added in the epilogue
+// with a one-lane shuffle (lane x takes lane x+1's b = 1 half).  Every
+// observation byte is converted to fp16 once (the im2col form of gemm.cu's
+// AG_U8 path builds every byte 4 times), and each K16 step reads its A rows
+// for 64 output columns (an N = 32 MMA is bound by its 4 KB A read: measured
+// 64 cycles per M128 K16 step either way).  Pipeline (warp-specialised,
+// persistent, one CTA per SM):
+//   warp 0        TMA: whole image {W, 4*Hs rows, C} per box into a staging ring
+//   warp 1        TMEM owner + MMA issuer (2 row taps x C K-steps of M128 N64 K16)
+//   warps 2..5    converters: staged u8 -> fp16 (1024 + v, exact) s2d windows
+//   warps 6..21   epilogue: TMEM -> scale/bias/ELU -> bf16 rows of a1 (4 warps
+//                 per TMEM lane quarter, 8 output channels each)
+// The 1024 offset is removed through the corrected bias of the published copy
+// (k_conv1_half_weights), so A is exact and B is the fp16 weights.
+//
+// Replaces: the reference has no convolutional encoder (SURVEY.md §8 a2,
+// SPEC.md:273-274); this is convnet_simple's conv1 of the model contract
+// (DESIGN.md §2), parity-checked against the fp64 oracle (tests/test_model_gpu.py,
+// tests/test_parity_prod_gpu.py) exactly like the engine path it replaces.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "appo_common.cuh"
+#include "gemm.cuh"
+#include "sm100.cuh"
+
+namespace appo_b200 {
+namespace {
+
+#ifndef C1_CONV_WARPS_DEF
+#define C1_CONV_WARPS_DEF 4
+#endif
+#ifndef C1_EPI_PARTS_DEF
+#define C1_EPI_PARTS_DEF 4
+#endif
+constexpr int C1_CONV_WARPS = C1_CONV_WARPS_DEF;
+constexpr int C1_TMA = 0, C1_MMA = 1;  // warp roles (MMA on warp 0 measured no faster)
+constexpr int C1_EPI_PARTS = C1_EPI_PARTS_DEF;  // epilogue warps per TMEM lane quarter
+constexpr int C1_EPI_WARPS = 4 * C1_EPI_PARTS;
+constexpr int C1_EPI_CO = 32 / C1_EPI_PARTS;    // output channels per epilogue warp
+constexpr int C1_THREADS = 32 * (2 + C1_CONV_WARPS + C1_EPI_WARPS);
+#ifndef C1_NSTG_DEF
+#define C1_NSTG_DEF 3
+#endif
+#ifndef C1_NA_DEF
+#define C1_NA_DEF 4
+#endif
+constexpr int C1_NSTG = C1_NSTG_DEF;  // staged images in flight
+constexpr int C1_NA = C1_NA_DEF;      // s2d A windows (one per 128-row tile)
+constexpr int C1_NACC = 4;    // TMEM accumulators of 64 columns
+constexpr int C1_WROWS = 168; // window rows: 5 s2d rows x 32 px + 1 (x-tap overrun), to 8
+constexpr int C1_WBYTES = C1_WROWS * 128;  // one window (SW128 rows, 1024-aligned)
+
+struct C1Params {
+  int n_img, C, H, W, Ho, Wo, Hs;  // Hs = Ho + 1 s2d rows are read
+  int tiles;                       // 128-row tiles per image = ceil(Ho / 4)
+  int box_rows;                    // 4 * Hs input rows staged per image
+  int stg_bytes;                   // staging slot bytes (C * box_rows * W, 128-aligned)
+  int slack;                       // bytes after the ring read by the last tile's padding rows
+  // trajectory-slot images: r < n_traj*T is step r % T of slot slot_ids[r / T],
+  // later ones the bootstrap observation of slot slot_ids[r - n_traj*T]
+  const int32_t* slot_ids;
+  int T, n_traj;
+  const uint16_t* w;  // fp16 [32][C*64], k = c*64 + kh*8 + kw (published copy)
+  const float* bias;  // corrected bias (offset 1024 * sum(W) * scale removed)
+  float scale;
+  uint16_t* out;      // bf16 [n_img * Ho * Wo][ldo]
+  int64_t ldo;
+  long long* prof;    // diagnostics (APPO_C1_PROF): CTA 0 per-tile timestamps [64][16]
+};
+#ifdef C1_PROF_ON  // per-tile timeline of CTA 0 (build with -DC1_PROF_ON, run with APPO_C1_PROF=1)
+#define C1_PROF(tile, k)                                                   \
+  do {                                                                     \
+    if (p.prof && blockIdx.x == 0 && (tile) < 64) p.prof[(tile) * 16 + (k)] = clock64(); \
+  } while (0)
+#else
+#define C1_PROF(tile, k) \
+  do {                   \
+  } while (0)
+#endif
+
+constexpr int C1_BBYTES = 2 * 64 * 128;     // 2 row taps x (2 column taps x 32 channels), SW128 rows
+int c1_smem_bytes(int stg_bytes, int slack) {
+  return 1024 + C1_NA * C1_WBYTES + C1_BBYTES + C1_NSTG * stg_bytes + slack + 256;
+}
+// Converters read input rows up to 16 * tiles + 3 of every channel (the last
+// tile's rows past the image): slack after the ring so the last slot's reads
+// stay inside the allocation (a W-wide row per row past 4 * Hs, + 128)
+int c1_slack(int tiles, int box_rows, int W) {
+  const int over = 16 * tiles + 4 - box_rows;
+  return ((over > 0 ? over : 0) * W + 128 + 127) & ~127;
+}
+
+// A K-major SWIZZLE_128B descriptor may start at any 128-byte row of the
+// 1024-byte swizzle pattern with base offset 0: the XOR pattern follows the
+// absolute shared-memory address (measured: setting the row phase in the
+// base-offset field, bits 49-51, gives wrong products), so a row shift of the
+// operand is only a start-address change.
+
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// packed fp32 pairs (sm_100 FFMA2 / FADD2): half the epilogue's FP instructions
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+// 32 lanes x 32-bit, 32 consecutive TMEM columns per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+template <int C>
+__global__ void __launch_bounds__(C1_THREADS, 1)
+    conv1_s2d_kernel(const __grid_constant__ CUtensorMap map_obs,
+                     const __grid_constant__ CUtensorMap map_boot, const __grid_constant__ C1Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte aligned base derived by pointer arithmetic from smem_raw, so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* awin = smem;                                  // C1_NA s2d windows (SW128 rows)
+  uint8_t* bsm = awin + C1_NA * C1_WBYTES;               // 4 taps x 32 rows (SW128)
+  uint8_t* stg = bsm + C1_BBYTES;                        // C1_NSTG staged images
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + C1_NSTG * p.stg_bytes + p.slack);
+  uint64_t* stg_full = bars;
+  uint64_t* stg_empty = stg_full + C1_NSTG;
+  uint64_t* a_full = stg_empty + C1_NSTG;
+  uint64_t* a_empty = a_full + C1_NA;
+  uint64_t* acc_full = a_empty + C1_NA;
+  uint64_t* acc_empty = acc_full + C1_NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C1_NACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch(&map_obs);
+    if (p.slot_ids) sm100::tma_prefetch(&map_boot);
+    for (int s = 0; s < C1_NSTG; ++s) {
+      sm100::mbar_init(&stg_full[s], 1);
+      sm100::mbar_init(&stg_empty[s], C1_CONV_WARPS);
+    }
+    for (int s = 0; s < C1_NA; ++s) {
+      sm100::mbar_init(&a_full[s], C1_CONV_WARPS);
+      sm100::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < C1_NACC; ++s) {
+      sm100::mbar_init(&acc_full[s], 1);
+      sm100::mbar_init(&acc_empty[s], C1_EPI_WARPS);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == C1_MMA) {
+    sm100::tmem_alloc(tmem_slot, C1_NACC * 64);
+    sm100::tmem_relinquish();
+  }
+  // K padding of every A / B row (chunks 2C..7) is zero once; the converters
+  // only ever write chunks < 2C
+  for (int e = threadIdx.x; e < (C1_NA * C1_WROWS + 2 * 64) * (8 - 2 * C); e += C1_THREADS) {
+    const int row = e / (8 - 2 * C), kc = 2 * C + e % (8 - 2 * C);
+    *reinterpret_cast<uint4*>(awin + row * 128 + ((kc ^ (row & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+  }
+  APPO_PDL_ENTRY();  // the weights / images come from earlier kernels
+
+  // B operand of row tap a: row n = (output channel co = n >> 1, column tap
+  // b = n & 1), chunk kc = 2c + h holds 8 fp16 W[co][c][4a + 2h + ii][4b + j]
+  // (ii = 0, 1; j = 0..3), the same (ii, j) order as the A chunks
+  for (int e = threadIdx.x; e < 2 * 2 * C * 64; e += C1_THREADS) {
+    const int n = e & 63, kc = (e >> 6) % (2 * C), a = (e >> 6) / (2 * C);
+    const int c = kc >> 1, h = kc & 1, b = n & 1, co = n >> 1;
+    const uint16_t* src = p.w + (size_t)co * (C * 64) + c * 64 + (4 * a + 2 * h) * 8 + 4 * b;
+    const uint2 lo = *reinterpret_cast<const uint2*>(src);
+    const uint2 hi = *reinterpret_cast<const uint2*>(src + 8);
+    *reinterpret_cast<uint4*>(bsm + a * 8192 + n * 128 + ((kc ^ (n & 7)) << 4)) =
+        make_uint4(lo.x, lo.y, hi.x, hi.y);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int B = p.n_traj * p.T;
+
+  if (warp == C1_TMA) {
+    // ---- TMA producer: one box per image ----
+    int j = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % C1_NSTG;
+      sm100::mbar_wait(&stg_empty[s], ((j / C1_NSTG) & 1) ^ 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sm100::mbar_arrive_expect_tx_warp(&stg_full[s], (uint32_t)(C * p.box_rows * p.W));
+      uint8_t* dst = stg + s * p.stg_bytes;
+      if (lane == 0) C1_PROF(j * p.tiles, 0);
+      if (!p.slot_ids) {
+        sm100::tma_load_4d_warp(dst, &map_obs, &stg_full[s], 0, 0, 0, img);
+      } else if (img < B) {
+        sm100::tma_load_5d_warp(dst, &map_obs, &stg_full[s], 0, 0, 0, img % p.T,
+                                __ldg(p.slot_ids + img / p.T));
+      } else {
+        sm100::tma_load_4d_warp(dst, &map_boot, &stg_full[s], 0, 0, 0, __ldg(p.slot_ids + img - B));
+      }
+    }
+  } else if (warp == C1_MMA) {
+    // ---- MMA issuer: per tile, 2 row taps x C K16 steps into one accumulator ----
+    constexpr uint32_t idesc = sm100::make_idesc_f16(128, 64, 0, 0);
+    const uint32_t a0 = sm100::smem_u32(awin), b0 = sm100::smem_u32(bsm);
+    int a = 0, acc = 0, tile_i = 0;
+    uint32_t aph = 0, accph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x) {
+      for (int t = 0; t < p.tiles; ++t) {
+        sm100::mbar_wait(&a_full[a], aph);
+        if (lane == 0) C1_PROF(tile_i, 8);
+        sm100::mbar_wait(&acc_empty[acc], accph ^ 1);
+        sm100::tc_fence_after();
+        if (lane == 0) C1_PROF(tile_i, 3);
+        const uint32_t d = tmem_base + acc * 64;
+        const uint32_t abase = a0 + a * C1_WBYTES;
+#pragma unroll
+        for (int ta = 0; ta < 2; ++ta) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const uint64_t ad = sm100::make_sdesc(abase + ta * 32 * 128 + c * 32, 16, 1024);
+            const uint64_t bd = sm100::make_sdesc(b0 + ta * 8192 + c * 32, 16, 1024);
+            sm100::umma_f16_warp(d, ad, bd, idesc, (ta | c) ? 1u : 0u);
+          }
+        }
+        sm100::umma_commit_warp(&a_empty[a]);
+        sm100::umma_commit_warp(&acc_full[acc]);
+        if (lane == 0) C1_PROF(tile_i, 4);
+        ++tile_i;
+        if (++a == C1_NA) { a = 0; aph ^= 1; }
+        if (++acc == C1_NACC) { acc = 0; accph ^= 1; }
+      }
+    }
+  } else if (warp < 2 + C1_CONV_WARPS) {
+    // ---- converters: lane = s2d column px (window row pyl*32 + px); unit = (pyl, chunk) ----
+    // plain C++ shared-memory accesses (not asm volatile) so the fully unrolled
+    // units' loads are issued together: the loop is LDS-latency bound otherwise
+    const int cw = warp - 2;
+    constexpr int kUnits = 5 * 2 * C;
+    constexpr int kPerWarp = (kUnits + C1_CONV_WARPS - 1) / C1_CONV_WARPS;
+    // per unit k of this warp: staging offset of its two input rows (tile 0) and
+    // its window offset; every unit is converted for every tile (rows past the
+    // image read the staging slack and only feed output rows that are dropped)
+    uint32_t soff[kPerWarp], doff[kPerWarp];
+#pragma unroll
+    for (int k = 0; k < kPerWarp; ++k) {
+      const int u = min(cw + k * C1_CONV_WARPS, kUnits - 1);
+      const int pyl = u / (2 * C), kc = u - pyl * 2 * C;
+      soff[k] = (uint32_t)(((kc >> 1) * p.box_rows + 4 * pyl + 2 * (kc & 1)) * p.W + 4 * lane);
+      doff[k] = (uint32_t)(lane * 128 + pyl * 4096 + ((kc ^ (lane & 7)) << 4));
+    }
+    const uint32_t tstep = 16u * p.W;  // staging bytes per tile (4 s2d rows x 4 input rows)
+    int j = 0, a = 0;
+    uint32_t aph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % C1_NSTG;
+      sm100::mbar_wait(&stg_full[s], (j / C1_NSTG) & 1);
+      const uint8_t* src0 = stg + s * p.stg_bytes;
+      for (int t = 0; t < p.tiles; ++t, src0 += tstep) {
+        sm100::mbar_wait(&a_empty[a], aph ^ 1);
+        if (cw == 0 && lane == 0) C1_PROF(j * p.tiles + t, 1);
+        uint8_t* dst0 = awin + a * C1_WBYTES;
+        uint32_t lo[kPerWarp], hi[kPerWarp];
+#pragma unroll
+        for (int k = 0; k < kPerWarp; ++k) {
+          lo[k] = *reinterpret_cast<const uint32_t*>(src0 + soff[k]);
+          hi[k] = *reinterpret_cast<const uint32_t*>(src0 + soff[k] + p.W);
+        }
+#pragma unroll
+        for (int k = 0; k < kPerWarp; ++k)  // SW128 row: chunk kc at (kc ^ (row & 7))
+          *reinterpret_cast<uint4*>(dst0 + doff[k]) =
+              make_uint4(__byte_perm(lo[k], 0x64646464u, 0x4140),
+                         __byte_perm(lo[k], 0x64646464u, 0x4342),
+                         __byte_perm(hi[k], 0x64646464u, 0x4140),
+                         __byte_perm(hi[k], 0x64646464u, 0x4342));
+        if (cw == 0 && lane == 0) C1_PROF(j * p.tiles + t, 7);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> UMMA
+        __syncwarp();
+        if (cw == 0 && lane == 0) C1_PROF(j * p.tiles + t, 2);
+        if (cw == C1_CONV_WARPS - 1 && lane == 0) C1_PROF(j * p.tiles + t, 9);
+        if (lane == 0) sm100::mbar_arrive(&a_full[a]);
+        if (++a == C1_NA) { a = 0; aph ^= 1; }
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
+    }
+  } else {
+    // ---- epilogue: warp quarter q = TMEM lanes (output row 4t + q), 16 output
+    // channels = 32 TMEM columns (co, b) ----
+    const int ew = warp - (2 + C1_CONV_WARPS);
+    const int q = warp & 3, part = ew >> 2;
+    constexpr float kLog2e = 1.4426950408889634f;
+    uint64_t bias2[C1_EPI_CO / 2], bias2l[C1_EPI_CO / 2];  // bias, bias*log2(e) pairs
+#pragma unroll
+    for (int k = 0; k < C1_EPI_CO / 2; ++k) {
+      const float b0 = __ldg(p.bias + part * C1_EPI_CO + 2 * k);
+      const float b1 = __ldg(p.bias + part * C1_EPI_CO + 2 * k + 1);
+      bias2[k] = f2pack(b0, b1);
+      bias2l[k] = f2pack(b0 * kLog2e, b1 * kLog2e);
+    }
+    const uint64_t scale2 = f2pack(p.scale, p.scale);
+    const uint64_t scale2l = f2pack(p.scale * kLog2e, p.scale * kLog2e);
+    const uint64_t mone2 = f2pack(-1.0f, -1.0f);
+    int acc = 0, tile_i = 0;
+    uint32_t accph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x) {
+      // this lane's output pixel (row 4t + q, column lane) of the image, 8 channels
+      uint16_t* obase = p.out + ((int64_t)img * p.Ho * p.Wo + (int64_t)q * p.Wo + lane) * p.ldo +
+                        part * C1_EPI_CO;
+      const int64_t tstride = 4 * (int64_t)p.Wo * p.ldo;
+      for (int t = 0; t < p.tiles; ++t, ++tile_i, obase += tstride) {
+        sm100::mbar_wait(&acc_full[acc], accph);
+        sm100::tc_fence_after();
+        if (ew == 0 && lane == 0) C1_PROF(tile_i, 5);
+        const int y = 4 * t + q;
+        if (y < p.Ho) {  // warp-uniform
+          uint32_t r[2 * C1_EPI_CO];
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 64 + part * 2 * C1_EPI_CO;
+          if constexpr (C1_EPI_CO == 16) tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+          else sm100::tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+          sm100::tmem_ld_wait();
+          if (ew == 0 && lane == 0) C1_PROF(tile_i, 11);
+          uint32_t w[C1_EPI_CO / 2];
+#pragma unroll
+          for (int k = 0; k < C1_EPI_CO / 2; ++k) {
+            // column tap b = 0 at pixel x plus b = 1 taken from pixel x + 1
+            const uint64_t v = fadd2(
+                f2pack(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 2])),
+                f2pack(__shfl_down_sync(0xffffffffu, __uint_as_float(r[4 * k + 1]), 1),
+                       __shfl_down_sync(0xffffffffu, __uint_as_float(r[4 * k + 3]), 1)));
+            const float2 x = f2unpack(ffma2(v, scale2, bias2[k]));
+            const float2 tl = f2unpack(ffma2(v, scale2l, bias2l[k]));  // x * log2(e)
+            const float2 e = f2unpack(fadd2(f2pack(ex2_ftz(fminf(tl.x, 0.0f)), ex2_ftz(fminf(tl.y, 0.0f))), mone2));
+            // ELU = max(x, exp(min(x, 0)) - 1)
+            w[k] = pack_bf16x2(fmaxf(x.x, e.x), fmaxf(x.y, e.y));
+          }
+          if (ew == 0 && lane == 0) C1_PROF(tile_i, 12);
+          if (lane < p.Wo) {
+            uint4* dst = reinterpret_cast<uint4*>(obase);
+#pragma unroll
+            for (int k = 0; k < C1_EPI_CO / 8; ++k)
+              dst[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+          }
+        }
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (ew == 0 && lane == 0) C1_PROF(tile_i, 6);
+        if (ew == C1_EPI_WARPS - 1 && lane == 0) C1_PROF(tile_i, 10);
+        if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
+        if (++acc == C1_NACC) { acc = 0; accph ^= 1; }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == C1_MMA) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, C1_NACC * 64);
+  }
+}
+
+template <int C>
+int c1_launch(Ctx* c, const CUtensorMap& mo, const CUtensorMap& mbt, const C1Params& p) {
+  auto kern = conv1_s2d_kernel<C>;
+  const int smem = c1_smem_bytes(p.stg_bytes, p.slack);
+  static int attr_bytes[64] = {};
+  const int dev = c->device & 63;
+  if (attr_bytes[dev] < smem) {
+    APPO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_bytes[dev] = smem;
+  }
+  const int grid = c->num_sms < p.n_img ? c->num_sms : p.n_img;
+  C1Params q = p;
+#ifdef C1_PROF_ON
+  static long long* prof = nullptr;
+  const char* pe = getenv("APPO_C1_PROF");
+  if (pe && pe[0] == '1' && p.n_img > 4096) {
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 1024);
+    cudaMemsetAsync(prof, 0, sizeof(long long) * 1024, c->stream);
+    q.prof = prof;
+  }
+#endif
+  c->next_name = "conv1_s2d_tcgen05";
+  const double M = (double)p.n_img * p.Ho * p.Wo;
+  c->next_flops = 2.0 * M * 32 * C * 64;
+  c->next_bytes = (double)p.n_img * C * p.H * p.W + 2.0 * M * 32 + 2.0 * 32 * C * 64;
+  APPO_LAUNCH(c, kern, grid, C1_THREADS, smem, mo, mbt, q);
+#ifdef C1_PROF_ON
+  if (q.prof) {
+    long long h[1024];
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[conv1 prof] CTA0 tile: tma_issue conv_start conv_done | mma_start mma_issued | epi_start epi_done | conv_stores_issued mma_afull conv7_done epi7_done (cycles from first TMA)\n");
+    for (int i = 0; i < 64; ++i) {
+      fprintf(stderr, "  t%-2d", i);
+      for (int k = 0; k < 13; ++k) fprintf(stderr, " %8lld", h[i * 16 + k] ? h[i * 16 + k] - h[0] : -1);
+      fprintf(stderr, "\n");
+    }
+  }
+#endif
+  return APPO_OK;
+}
+
+}  // namespace
+
+const void* kanchor_conv1() { return reinterpret_cast<const void*>(&conv1_s2d_kernel<3>); }
+
+// Host side: contract of the s2d path (else the caller keeps the engine path).
+bool conv1_s2d_supported(const ConvIn& in, int N, const Epilogue& e) {
+  if (!in.u8 || in.ksz != 8 || in.s != 4 || N != 32) return false;
+  if (e.flags != (EPI_BIAS | EPI_ELU | EPI_BF16) || (e.ldo & 7) || !e.bias) return false;
+  if ((reinterpret_cast<uintptr_t>(e.out) & 15)) return false;
+  const int Hs = in.Ho + 1, Ws = in.Wo + 1;
+  if (Ws > 32 || in.Wi % 16 || 4 * Hs > in.Hi || 4 * Hs > 256 || in.Cin < 1 || in.Cin > 4)
+    return false;
+  const int tiles = (in.Ho + 3) / 4;
+  return c1_smem_bytes((in.Cin * 4 * Hs * in.Wi + 127) & ~127, c1_slack(tiles, 4 * Hs, in.Wi)) <=
+         227 * 1024;
+}
+
+int conv1_s2d_forward(Ctx* c, const ConvIn& in, const uint16_t* w1h, const Epilogue& e) {
+  if (in.n_img <= 0) return APPO_OK;
+  APPO_REQUIRE(conv1_s2d_supported(in, 32, e), APPO_ERR_CONTRACT, "conv1_s2d: unsupported shape");
+  C1Params p{};
+  p.n_img = in.n_img;
+  p.C = in.Cin;
+  p.H = in.Hi;
+  p.W = in.Wi;
+  p.Ho = in.Ho;
+  p.Wo = in.Wo;
+  p.Hs = in.Ho + 1;
+  p.tiles = (in.Ho + 3) / 4;
+  p.box_rows = 4 * p.Hs;
+  p.stg_bytes = (p.C * p.box_rows * p.W + 127) & ~127;
+  p.slack = c1_slack(p.tiles, p.box_rows, p.W);
+  p.slot_ids = in.slot_ids;
+  p.T = in.T;
+  p.n_traj = in.n_traj;
+  p.w = w1h;
+  p.bias = e.bias;
+  p.scale = e.scale;
+  p.out = reinterpret_cast<uint16_t*>(e.out);
+  p.ldo = e.ldo;
+  CUtensorMap mo, mbt;
+  APPO_REQUIRE(make_u8_image_maps(&mo, &mbt, in, p.box_rows), APPO_ERR_CONTRACT,
+               "conv1_s2d: images must be 16-byte aligned for TMA staging");
+  switch (p.C) {
+    case 1: return c1_launch<1>(c, mo, mbt, p);
+    case 2: return c1_launch<2>(c, mo, mbt, p);
+    case 3: return c1_launch<3>(c, mo, mbt, p);
+    default: return c1_launch<4>(c, mo, mbt, p);
+  }
+}
+
+}  // namespace appo_b200

@@ -1712,6 +1712,14 @@ bool make_image_maps(KParams& p, const ConvIn& in, int box_rows) {
          make_tmap_u8(&p.map3, in.src + in.boot_off, 4, bdims, bstr, box) == APPO_OK;
 }
 
+bool make_u8_image_maps(CUtensorMap* obs, CUtensorMap* boot, const ConvIn& in, int box_rows) {
+  KParams p{};
+  if (!make_image_maps(p, in, box_rows)) return false;
+  *obs = p.map2;
+  *boot = p.map3;
+  return true;
+}
+
 int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
                        int bn) {
   const int K = in.u8 ? in.Cin * 64 : in.ksz * in.ksz * in.Cin;

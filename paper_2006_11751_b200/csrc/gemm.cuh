@@ -67,6 +67,16 @@ struct ConvIn {
 int conv_implicit_bf16(Ctx* c, const ConvIn& in, int N, const Operand& W, const Epilogue& epi,
                        int bn);
 
+// u8 image staging tensor maps (observations; bootstrap observations in slot
+// mode) with boxes {W, box_rows, C}; false when the images are not 16-byte aligned.
+bool make_u8_image_maps(CUtensorMap* obs, CUtensorMap* boot, const ConvIn& in, int box_rows);
+
+// conv1 forward as a space-to-depth taps GEMM (conv1.cu): out = ELU(scale *
+// (1024 + obs) . W1h^T + bias') as bf16 NHWC rows; w1h = fp16 [32][C*64].
+// conv1_s2d_supported tells whether the shape / epilogue fits the kernel.
+bool conv1_s2d_supported(const ConvIn& in, int N, const Epilogue& e);
+int conv1_s2d_forward(Ctx* c, const ConvIn& in, const uint16_t* w1h, const Epilogue& e);
+
 // Bias-gradient output of a fused column sum: deterministic int64 fixed-point
 // accumulation (acc[16][N], zero between calls) + last-block conversion to out[N].
 struct BiasOut {

@@ -320,8 +320,18 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
   e.ldo = 32;
   // conv1 gathers its input from the u8 images (smem-staged implicit GEMM);
   // so does its weight gradient in the learner (conv1_wgrad_implicit)
-  TRY(conv_implicit_bf16(c, conv1_in(src, R, d), 32, Operand{M->pub_c1h[pub], d.K1, false}, e,
-                         32));
+  // conv1 as a space-to-depth taps GEMM (conv1.cu: each image byte converted
+  // once); the im2col engine path remains for shapes outside its envelope
+  // (unaligned images) and as the A/B reference (APPO_CONV1=engine)
+  static const bool conv1_engine = [] {
+    const char* v = getenv("APPO_CONV1");
+    return v && v[0] == 'e';
+  }();
+  const ConvIn c1in = conv1_in(src, R, d);
+  if (!conv1_engine && conv1_s2d_supported(c1in, 32, e) && conv1_s2d_forward(c, c1in, M->pub_c1h[pub], e) == APPO_OK) {
+  } else {
+    TRY(conv_implicit_bf16(c, c1in, 32, Operand{M->pub_c1h[pub], d.K1, false}, e, 32));
+  }
   e.scale = 1.0f;
   e.bias = pf + d.off_c2b;
   e.out = s.a2;
