@@ -199,12 +199,6 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
     sm100::tmem_alloc(tmem_slot, C1_NACC * 64);
     sm100::tmem_relinquish();
   }
-  // K padding of every A / B row (chunks 2C..7) is zero once; the converters
-  // only ever write chunks < 2C
-  for (int e = threadIdx.x; e < (C1_NA * C1_WROWS + 2 * 64) * (8 - 2 * C); e += C1_THREADS) {
-    const int row = e / (8 - 2 * C), kc = 2 * C + e % (8 - 2 * C);
-    *reinterpret_cast<uint4*>(awin + row * 128 + ((kc ^ (row & 7)) << 4)) = make_uint4(0, 0, 0, 0);
-  }
   APPO_PDL_ENTRY();  // the weights / images come from earlier kernels
 
   // B operand of row tap a: row n = (output channel co = n >> 1, column tap
@@ -447,6 +441,258 @@ int c1_launch(Ctx* c, const CUtensorMap& mo, const CUtensorMap& mbt, const C1Par
   return APPO_OK;
 }
 
+// ---- conv1 weight gradient in the same space-to-depth form ----------------
+// dW[co][c][4a+i][4b+j] = sum_{Y,x} Z[Y][x+b][(c,i,j)] * dz1[Y-a][x][co]: per
+// tile of 4 s2d rows Y (128 pixels), ONE MMA chain of 8 K16 pixel steps with
+// A = the s2d window as an MN-major SW128 operand whose two 64-row M atoms are
+// the column taps b = 0, 1 (atom stride LBO = 128 B = one pixel row: the
+// shifted view again) and B = dz1 rows 4t-1 .. 4t+3 (TMA box {64 channels (32
+// real, OOB zero), 32 x, 5 rows}, MN-major) whose two 64-wide N atoms are the
+// row taps a = 1, 0 (atom stride 4 KB = one dz1 row).  The accumulator
+// [128 x 128] lives in TMEM for the CTA's whole share of images (split-K over
+// the CTAs), is written once at the end and reduced deterministically.  Pixels
+// outside the image (x = Wo, rows -1 and >= Ho) have dz1 = 0 from the TMA zero
+// fill, so window rows past the image contribute nothing.  Operands are bf16 here (dz1 is bf16;
+// u8 -> bf16 is exact), so the converters build exact bf16 values.
+constexpr int W1_CONV_WARPS = 8;
+constexpr int W1_THREADS = 32 * (3 + W1_CONV_WARPS);  // image TMA, MMA, dz1 TMA, converters
+constexpr int W1_NSTG = 3, W1_NA = 3, W1_ND = 3;
+constexpr int W1_DROWS = 5;                           // dz1 rows per tile (4t-1 .. 4t+3)
+constexpr int W1_DBYTES = 64 * 2 * 32 * W1_DROWS;     // dz1 tile {64 ch, 32 x, 5 rows} bf16
+
+struct W1Params {
+  int n_img, C, H, W, Ho, Wo, Hs, tiles, box_rows, stg_bytes, slack;
+  const int32_t* slot_ids;
+  int T, n_traj;
+  float* partial;  // [gridDim.x][32][C*64] per-CTA partial sums
+};
+
+int w1_smem_bytes(int stg_bytes, int slack) {
+  return 1024 + W1_NA * C1_WBYTES + W1_ND * W1_DBYTES + W1_NSTG * stg_bytes + slack + 256;
+}
+
+template <int C>
+__global__ void __launch_bounds__(W1_THREADS, 1)
+    conv1_s2d_wgrad_kernel(const __grid_constant__ CUtensorMap map_obs,
+                           const __grid_constant__ CUtensorMap map_boot,
+                           const __grid_constant__ CUtensorMap map_dz, const __grid_constant__ W1Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* awin = smem;                          // W1_NA s2d windows (SW128 rows)
+  uint8_t* dtl = awin + W1_NA * C1_WBYTES;       // W1_ND dz1 tiles
+  uint8_t* stg = dtl + W1_ND * W1_DBYTES;        // W1_NSTG staged images
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + W1_NSTG * p.stg_bytes + p.slack);
+  uint64_t* stg_full = bars;
+  uint64_t* stg_empty = stg_full + W1_NSTG;
+  uint64_t* a_full = stg_empty + W1_NSTG;
+  uint64_t* a_empty = a_full + W1_NA;
+  uint64_t* d_full = a_empty + W1_NA;
+  uint64_t* d_empty = d_full + W1_ND;
+  uint64_t* acc_done = d_empty + W1_ND;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch(&map_obs);
+    sm100::tma_prefetch(&map_dz);
+    if (p.slot_ids) sm100::tma_prefetch(&map_boot);
+    for (int s = 0; s < W1_NSTG; ++s) {
+      sm100::mbar_init(&stg_full[s], 1);
+      sm100::mbar_init(&stg_empty[s], W1_CONV_WARPS);
+    }
+    for (int s = 0; s < W1_NA; ++s) {
+      sm100::mbar_init(&a_full[s], W1_CONV_WARPS);
+      sm100::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < W1_ND; ++s) {
+      sm100::mbar_init(&d_full[s], 1);
+      sm100::mbar_init(&d_empty[s], 1);
+    }
+    sm100::mbar_init(acc_done, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) {
+    sm100::tmem_alloc(tmem_slot, 128);
+    sm100::tmem_relinquish();
+  }
+  // windows fully zeroed once: rows the converters never write (the x-tap
+  // overrun row, K padding) must hold finite values, they meet dz1 = 0
+  for (int e = threadIdx.x; e < W1_NA * C1_WBYTES / 16; e += W1_THREADS)
+    reinterpret_cast<uint4*>(awin)[e] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  APPO_PDL_ENTRY();  // dz1 comes from the previous kernel
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int B = p.n_traj * p.T;
+
+  if (warp == 0) {
+    // ---- image TMA: one box per image ----
+    int j = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % W1_NSTG;
+      sm100::mbar_wait(&stg_empty[s], ((j / W1_NSTG) & 1) ^ 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sm100::mbar_arrive_expect_tx_warp(&stg_full[s], (uint32_t)(C * p.box_rows * p.W));
+      uint8_t* dst = stg + s * p.stg_bytes;
+      if (!p.slot_ids) {
+        sm100::tma_load_4d_warp(dst, &map_obs, &stg_full[s], 0, 0, 0, img);
+      } else if (img < B) {
+        sm100::tma_load_5d_warp(dst, &map_obs, &stg_full[s], 0, 0, 0, img % p.T,
+                                __ldg(p.slot_ids + img / p.T));
+      } else {
+        sm100::tma_load_4d_warp(dst, &map_boot, &stg_full[s], 0, 0, 0, __ldg(p.slot_ids + img - B));
+      }
+    }
+  } else if (warp == 2) {
+    // ---- dz1 TMA: rows 4t-1 .. 4t+3 of the tile's image (outside the image -> 0) ----
+    int d = 0;
+    uint32_t dph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x) {
+      for (int t = 0; t < p.tiles; ++t) {
+        sm100::mbar_wait(&d_empty[d], dph ^ 1);
+        sm100::mbar_arrive_expect_tx_warp(&d_full[d], (uint32_t)W1_DBYTES);
+        sm100::tma_load_4d_warp(dtl + d * W1_DBYTES, &map_dz, &d_full[d], 0, 0, 4 * t - 1, img);
+        if (++d == W1_ND) { d = 0; dph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA: per tile, 8 K16 pixel steps; M = (b, feature), N = (a = 1, 0; channel) ----
+    constexpr uint32_t idesc = sm100::make_idesc_bf16(128, 128, 1, 1);
+    const uint32_t a0 = sm100::smem_u32(awin), d0 = sm100::smem_u32(dtl);
+    int a = 0, d = 0;
+    uint32_t aph = 0, dph = 0, acc = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x) {
+      for (int t = 0; t < p.tiles; ++t) {
+        sm100::mbar_wait(&a_full[a], aph);
+        sm100::mbar_wait(&d_full[d], dph);
+        sm100::tc_fence_after();
+        const uint32_t wb = a0 + a * C1_WBYTES, db = d0 + d * W1_DBYTES;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          // A: pixels 16ks.. of the tile, M atoms b = 0, 1 one pixel row apart
+          // (LBO = 128 B); B: dz1 of the same pixels one row up (a = 1, N atom 0)
+          // and of the same row (a = 0, N atom 1, LBO = 4 KB)
+          const uint64_t ad = sm100::make_sdesc(wb + 16 * ks * 128, 128, 1024);
+          const uint64_t bd = sm100::make_sdesc(db + 16 * ks * 128, 4096, 1024);
+          sm100::umma_f16_warp(tmem_base, ad, bd, idesc, (acc | ks) ? 1u : 0u);
+        }
+        acc = 1;
+        sm100::umma_commit_warp(&a_empty[a]);
+        sm100::umma_commit_warp(&d_empty[d]);
+        if (++a == W1_NA) { a = 0; aph ^= 1; }
+        if (++d == W1_ND) { d = 0; dph ^= 1; }
+      }
+    }
+    sm100::umma_commit_warp(acc_done);
+  } else {
+    // ---- converters: staged u8 -> exact bf16 s2d windows (as conv1_s2d_kernel) ----
+    // (4 s2d rows per window: the row taps are in B; window row 128 (read by
+    // the b = 1 atom of the tile's last pixel, whose dz1 is 0) stays zero)
+    const int cw = warp - 3;
+    constexpr int kUnits = 4 * 2 * C;
+    constexpr int kPerWarp = (kUnits + W1_CONV_WARPS - 1) / W1_CONV_WARPS;
+    uint32_t soff[kPerWarp], doff[kPerWarp];
+#pragma unroll
+    for (int k = 0; k < kPerWarp; ++k) {
+      const int u = min(cw + k * W1_CONV_WARPS, kUnits - 1);
+      const int pyl = u / (2 * C), kc = u - pyl * 2 * C;
+      soff[k] = (uint32_t)(((kc >> 1) * p.box_rows + 4 * pyl + 2 * (kc & 1)) * p.W + 4 * lane);
+      doff[k] = (uint32_t)(lane * 128 + pyl * 4096 + ((kc ^ (lane & 7)) << 4));
+    }
+    const uint32_t tstep = 16u * p.W;
+    const uint64_t big2 = f2pack(8388608.0f, 8388608.0f);
+    // exact bf16 of 4 u8 values: 2^23 + v as float, minus 2^23, upper halves
+    auto cvt4 = [&](uint32_t w, uint32_t& x0, uint32_t& x1) {
+      const float2 v01 = f2unpack(fadd2(
+          f2pack(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650)),
+                 __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7651))), big2 ^ 0x8000000080000000ull));
+      const float2 v23 = f2unpack(fadd2(
+          f2pack(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7652)),
+                 __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7653))), big2 ^ 0x8000000080000000ull));
+      x0 = __byte_perm(__float_as_uint(v01.x), __float_as_uint(v01.y), 0x7632);
+      x1 = __byte_perm(__float_as_uint(v23.x), __float_as_uint(v23.y), 0x7632);
+    };
+    int j = 0, a = 0;
+    uint32_t aph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % W1_NSTG;
+      sm100::mbar_wait(&stg_full[s], (j / W1_NSTG) & 1);
+      const uint8_t* src0 = stg + s * p.stg_bytes;
+      for (int t = 0; t < p.tiles; ++t, src0 += tstep) {
+        sm100::mbar_wait(&a_empty[a], aph ^ 1);
+        uint8_t* dst0 = awin + a * C1_WBYTES;
+        uint32_t lo[kPerWarp], hi[kPerWarp];
+#pragma unroll
+        for (int k = 0; k < kPerWarp; ++k) {
+          lo[k] = *reinterpret_cast<const uint32_t*>(src0 + soff[k]);
+          hi[k] = *reinterpret_cast<const uint32_t*>(src0 + soff[k] + p.W);
+        }
+#pragma unroll
+        for (int k = 0; k < kPerWarp; ++k) {
+          uint4 v;
+          cvt4(lo[k], v.x, v.y);
+          cvt4(hi[k], v.z, v.w);
+          *reinterpret_cast<uint4*>(dst0 + doff[k]) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&a_full[a]);
+        if (++a == W1_NA) { a = 0; aph ^= 1; }
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
+    }
+    // ---- final epilogue (converter warps 0..3 = lane quarters 3, 0, 1, 2):
+    //      TMEM row m = (b = m / 64, feature f = m % 64 = c*16 + i*4 + j) ----
+    if (cw < 4) {
+      sm100::mbar_wait(acc_done, 0);
+      sm100::tc_fence_after();
+      const int q = warp & 3, m = 32 * q + lane;
+      const int b = m >> 6, f = m & 63;
+      const int c = f >> 4, i = (f >> 2) & 3, jj = f & 3;
+      float* out = p.partial + (size_t)blockIdx.x * 32 * (C * 64);
+#pragma unroll
+      for (int ta = 0; ta < 2; ++ta) {  // TMEM columns 64 * (1 - ta): row tap ta
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (1 - ta) * 64, r);
+        sm100::tmem_ld_wait();
+        if (f < 16 * C) {
+          const int k = c * 64 + (4 * ta + i) * 8 + 4 * b + jj;
+#pragma unroll
+          for (int co = 0; co < 32; ++co) out[co * (C * 64) + k] = __uint_as_float(r[co]);
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, 128);
+  }
+}
+
+template <int C>
+int w1_launch(Ctx* c, const CUtensorMap& mo, const CUtensorMap& mbt, const CUtensorMap& mdz,
+              const W1Params& p, int grid) {
+  auto kern = conv1_s2d_wgrad_kernel<C>;
+  const int smem = w1_smem_bytes(p.stg_bytes, p.slack);
+  static int attr_bytes[64] = {};
+  const int dev = c->device & 63;
+  if (attr_bytes[dev] < smem) {
+    APPO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_bytes[dev] = smem;
+  }
+  c->next_name = "conv1_s2d_wgrad_tcgen05";
+  const double M = (double)p.n_img * p.Ho * p.Wo;
+  c->next_flops = 2.0 * M * 32 * C * 64;
+  c->next_bytes = (double)p.n_img * C * p.H * p.W + 2.0 * M * 32 + 4.0 * grid * 32 * C * 64;
+  APPO_LAUNCH(c, kern, grid, W1_THREADS, smem, mo, mbt, mdz, p);
+  return APPO_OK;
+}
+
 }  // namespace
 
 const void* kanchor_conv1() { return reinterpret_cast<const void*>(&conv1_s2d_kernel<3>); }
@@ -496,6 +742,54 @@ int conv1_s2d_forward(Ctx* c, const ConvIn& in, const uint16_t* w1h, const Epilo
     case 3: return c1_launch<3>(c, mo, mbt, p);
     default: return c1_launch<4>(c, mo, mbt, p);
   }
+}
+
+int conv1_s2d_wgrad(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* dw, float scale) {
+  if (in.n_img <= 0) return APPO_OK;
+  const int Hs = in.Ho + 1, Ws = in.Wo + 1;
+  if (!in.u8 || in.ksz != 8 || in.s != 4 || Ws > 32 || in.Wi % 16 || 4 * Hs > in.Hi ||
+      4 * Hs > 256 || in.Cin < 1 || in.Cin > 3 || (reinterpret_cast<uintptr_t>(dz1) & 15))
+    return APPO_ERR_CONTRACT;
+  W1Params p{};
+  p.n_img = in.n_img;
+  p.C = in.Cin;
+  p.H = in.Hi;
+  p.W = in.Wi;
+  p.Ho = in.Ho;
+  p.Wo = in.Wo;
+  p.Hs = Hs;
+  p.tiles = (in.Ho + 3) / 4;
+  p.box_rows = 4 * Hs;
+  p.stg_bytes = (p.C * p.box_rows * p.W + 127) & ~127;
+  p.slack = c1_slack(p.tiles, p.box_rows, p.W);
+  p.slot_ids = in.slot_ids;
+  p.T = in.T;
+  p.n_traj = in.n_traj;
+  if (w1_smem_bytes(p.stg_bytes, p.slack) > 227 * 1024) return APPO_ERR_CONTRACT;
+  CUtensorMap mo, mbt, mdz;
+  if (!make_u8_image_maps(&mo, &mbt, in, p.box_rows)) return APPO_ERR_CONTRACT;
+  // dz1 [img][Ho][Wo][32] bf16, box {64 (32 real), 32, 5, 1}: out-of-range -> 0
+  const int st = make_tmap_bf16_4d(&mdz, dz1, 32, (uint64_t)in.Wo, (uint64_t)in.Ho,
+                                   (uint64_t)in.n_img, 64, 32, W1_DROWS, 1);
+  if (st) return st;
+  const int grid = c->num_sms < p.n_img ? c->num_sms : p.n_img;
+  const int K1 = p.C * 64;
+  float* part = nullptr;
+  const int wst = gemm_workspace(c, (size_t)grid * 32 * K1 * sizeof(float), &part);
+  if (wst) return wst;
+  p.partial = part;
+  int r;
+  switch (p.C) {
+    case 1: r = w1_launch<1>(c, mo, mbt, mdz, p, grid); break;
+    case 2: r = w1_launch<2>(c, mo, mbt, mdz, p, grid); break;
+    default: r = w1_launch<3>(c, mo, mbt, mdz, p, grid); break;
+  }
+  if (r) return r;
+  Epilogue e;
+  e.scale = scale;
+  e.out = dw;
+  e.ldo = K1;
+  return splitk_reduce(c, 32, K1, grid, part, e);
 }
 
 }  // namespace appo_b200

@@ -1712,6 +1712,10 @@ bool make_image_maps(KParams& p, const ConvIn& in, int box_rows) {
          make_tmap_u8(&p.map3, in.src + in.boot_off, 4, bdims, bstr, box) == APPO_OK;
 }
 
+int splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial, const Epilogue& epi) {
+  return launch_splitk_reduce(c, M, N, splits, partial, epi);
+}
+
 bool make_u8_image_maps(CUtensorMap* obs, CUtensorMap* boot, const ConvIn& in, int box_rows) {
   KParams p{};
   if (!make_image_maps(p, in, box_rows)) return false;
@@ -1981,6 +1985,27 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (3d) failed: " + std::to_string((int)r));
+    return APPO_ERR_CONTRACT;
+  }
+  return APPO_OK;
+}
+
+int make_tmap_bf16_4d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t d3, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return APPO_ERR_RESOURCE;
+  }
+  cuuint64_t dims[4] = {d0, d1, d2, d3};
+  cuuint64_t strides[3] = {d0 * 2, d0 * d1 * 2, d0 * d1 * d2 * 2};
+  cuuint32_t box[4] = {b0, b1, b2, b3};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (4d) failed: " + std::to_string((int)r));
     return APPO_ERR_CONTRACT;
   }
   return APPO_OK;

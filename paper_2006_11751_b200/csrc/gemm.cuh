@@ -76,6 +76,11 @@ bool make_u8_image_maps(CUtensorMap* obs, CUtensorMap* boot, const ConvIn& in, i
 // conv1_s2d_supported tells whether the shape / epilogue fits the kernel.
 bool conv1_s2d_supported(const ConvIn& in, int N, const Epilogue& e);
 int conv1_s2d_forward(Ctx* c, const ConvIn& in, const uint16_t* w1h, const Epilogue& e);
+// conv1 weight gradient in the same space-to-depth form (conv1.cu):
+// dw[co][(c,kh,kw)] = scale * sum_pixels dz1[pixel][co] * obs window, per-CTA
+// partial sums + deterministic split-K reduce.  APPO_ERR_CONTRACT when the
+// shape or the image alignment is outside the kernel's envelope.
+int conv1_s2d_wgrad(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* dw, float scale);
 
 // Bias-gradient output of a fused column sum: deterministic int64 fixed-point
 // accumulation (acc[16][N], zero between calls) + last-block conversion to out[N].
@@ -107,6 +112,10 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
                       uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
                       uint32_t b2, int swizzle_bytes = 128);
 
+// 4-D bf16 tensor map over a dense [d3][d2][d1][d0] array, 128B swizzle, zero OOB fill.
+int make_tmap_bf16_4d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t d3, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3);
+
 // conv1 weight gradient straight from the u8 images (no im2col):
 // dw[co][(c,kh,kw)] = scale * sum_pixels dz1[pixel][co] * obs window; in
 // describes the images exactly as for the forward.  APPO_ERR_CONTRACT when the
@@ -121,5 +130,7 @@ int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, int Ci
 
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);
+// Deterministic split-K reduction: out = epi(sum over `splits` fp32 partials [splits][M][N]).
+int splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial, const Epilogue& epi);
 
 }  // namespace appo_b200

@@ -1044,8 +1044,16 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   // ---- conv1 weight gradient (input is data): straight from the u8 images;
   //      im2col + GEMM only when the images cannot be TMA-staged ----
   {
-    const int wst = conv1_wgrad_implicit(ctx, conv1_in(src, B, d), s.dz1, G + d.off_c1w,
-                                         1.0f / 255.0f);
+    // space-to-depth form (conv1.cu), else the im2col-staging engine path
+    static const bool conv1_engine = [] {
+      const char* v = getenv("APPO_CONV1");
+      return v && v[0] == 'e';
+    }();
+    int wst = conv1_engine ? APPO_ERR_CONTRACT
+                           : conv1_s2d_wgrad(ctx, conv1_in(src, B, d), s.dz1, G + d.off_c1w,
+                                             1.0f / 255.0f);
+    if (wst == APPO_ERR_CONTRACT)
+      wst = conv1_wgrad_implicit(ctx, conv1_in(src, B, d), s.dz1, G + d.off_c1w, 1.0f / 255.0f);
     if (wst == APPO_ERR_CONTRACT) {
       const int M1 = B * d.P1;
       TRY(k_im2col_u8(ctx, src, B, d, s.col1));
