@@ -1712,6 +1712,8 @@ bool make_image_maps(KParams& p, const ConvIn& in, int box_rows) {
          make_tmap_u8(&p.map3, in.src + in.boot_off, 4, bdims, bstr, box) == APPO_OK;
 }
 
+EncodeTiledFnPublic tensor_map_encoder() { return get_encode(); }
+
 int splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial, const Epilogue& epi) {
   return launch_splitk_reduce(c, M, N, splits, partial, epi);
 }

@@ -130,6 +130,17 @@ int conv_taps_wgrad(Ctx* c, const uint16_t* x, int n_img, int Hi, int Wi, int Ci
 
 // Workspace management for split-K partials (grown on demand).
 int gemm_workspace(Ctx* c, size_t bytes, float** out);
+// cuTensorMapEncodeTiled from the driver (nullptr if unavailable)
+typedef CUresult (*EncodeTiledFnPublic)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                        const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                        const cuuint32_t*, CUtensorMapInterleave,
+                                        CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                        CUtensorMapFloatOOBfill);
+EncodeTiledFnPublic tensor_map_encoder();
+// conv2 forward (k4 s2, 32 -> 64, bf16 NHWC, bias + ELU) as a space-to-depth
+// taps GEMM (conv2.cu); APPO_ERR_CONTRACT outside its envelope.
+int conv2_s2d_forward(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, int Ho, int Wo,
+                      const uint16_t* w2, const Epilogue& e);
 // Deterministic split-K reduction: out = epi(sum over `splits` fp32 partials [splits][M][N]).
 int splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial, const Epilogue& epi);
 

@@ -341,7 +341,18 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
     in.src = reinterpret_cast<const uint8_t*>(s.a1);
     in.n_img = R;
     in.Hi = d.H1; in.Wi = d.W1; in.Cin = 32; in.ksz = 4; in.s = 2; in.Ho = d.H2; in.Wo = d.W2;
-    TRY(conv_implicit_bf16(c, in, 64, Operand{wb + d.off_c2w, 512, false}, e, 64));
+    // space-to-depth taps GEMM (conv2.cu), else the per-tap strided-box engine path
+    static const bool conv2_engine = [] {
+      const char* v = getenv("APPO_CONV2");
+      return v && v[0] == 'e';
+    }();
+    const int st2 = conv2_engine ? APPO_ERR_CONTRACT
+                                 : conv2_s2d_forward(c, s.a1, R, d.H1, d.W1, d.H2, d.W2,
+                                                     wb + d.off_c2w, e);
+    if (st2 == APPO_ERR_CONTRACT)
+      TRY(conv_implicit_bf16(c, in, 64, Operand{wb + d.off_c2w, 512, false}, e, 64));
+    else if (st2 != APPO_OK)
+      return st2;
   } else {
     TRY(k_im2col_nhwc(c, s.a1, R, d.H1, d.W1, 32, 4, 2, d.H2, d.W2, s.col2));
     TRY(gemm_bf16(c, R * d.P2, 64, 512, Operand{s.col2, 512, false},
