@@ -141,6 +141,15 @@ EncodeTiledFnPublic tensor_map_encoder();
 // taps GEMM (conv2.cu); APPO_ERR_CONTRACT outside its envelope.
 int conv2_s2d_forward(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, int Ho, int Wo,
                       const uint16_t* w2, const Epilogue& e);
+// Inference GRU step fused into its gate GEMMs + heads + sampling (gru_infer.cu):
+// x, hbf bf16 [B][512]; partials scratch >= 16*B*8 floats; A <= 7.
+bool gru_infer_fused_supported(int B, int A);
+int gru_infer_fused(Ctx* c, int B, int A, const uint16_t* x, const uint16_t* hbf,
+                    const uint16_t* w_ih, const uint16_t* w_hh, const float* b_ih,
+                    const float* b_hh, const float* h_in, const float* wpi, const float* bpi,
+                    const float* wv, const float* bv, uint64_t key, uint64_t counter0,
+                    float* part, float* h_out, int32_t* actions, float* logp, float* values,
+                    float* logits);
 // Deterministic split-K reduction: out = epi(sum over `splits` fp32 partials [splits][M][N]).
 int splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial, const Epilogue& epi);
 
