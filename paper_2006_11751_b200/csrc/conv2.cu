@@ -96,7 +96,8 @@ __device__ __forceinline__ void c2_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 __global__ void __launch_bounds__(C2_THREADS, 1)
-    conv2_s2d_kernel(const __grid_constant__ CUtensorMap map_a1, const __grid_constant__ C2Params p) {
+    conv2_s2d_kernel(const __grid_constant__ CUtensorMap map_a1,
+                     const __grid_constant__ CUtensorMap map_w, const __grid_constant__ C2Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stg = smem;                              // C2_NSTG x (even plane, odd plane)
@@ -106,11 +107,14 @@ __global__ void __launch_bounds__(C2_THREADS, 1)
   uint64_t* empty = full + C2_NSTG;
   uint64_t* acc_full = empty + C2_NSTG;
   uint64_t* acc_empty = acc_full + C2_NACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C2_NACC);
+  uint64_t* bfull = acc_empty + C2_NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     sm100::tma_prefetch(&map_a1);
+    sm100::tma_prefetch(&map_w);
+    sm100::mbar_init(bfull, 1);
     for (int s = 0; s < C2_NSTG; ++s) {
       sm100::mbar_init(&full[s], 1);
       sm100::mbar_init(&empty[s], 1);
@@ -131,21 +135,18 @@ __global__ void __launch_bounds__(C2_THREADS, 1)
     reinterpret_cast<uint4*>(stg + pl * C2_PLANE + p.plane_rows * 128)[rest] = make_uint4(0, 0, 0, 0);
   }
   APPO_PDL_ENTRY();  // a1 and the published weights come from earlier kernels
-  // B block (a, e): row n = 2co + b holds W2[co][2a+e][2b .. 2b+1][0..31] (128 B)
-  for (int i = threadIdx.x; i < 4 * 128 * 8; i += C2_THREADS) {
-    const int blk = i >> 10, n = (i >> 3) & 127, c = i & 7;
-    const int a = blk >> 1, e = blk & 1, co = n >> 1, b = n & 1;
-    const uint4 v = reinterpret_cast<const uint4*>(
-        p.w + ((size_t)(co * 4 + 2 * a + e) * 4 + 2 * b) * 32)[c];
-    *reinterpret_cast<uint4*>(bsm + blk * 16384 + n * 128 + ((c ^ (n & 7)) << 4)) = v;
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // B block (a, e): row n = 2co + b holds W2[co][2a+e][2b .. 2b+1][0..31]
+    // (128 B): one box {64, 2 (b), 1 (kh), 64 (co)} of the weights per block
+    sm100::mbar_arrive_expect_tx_warp(bfull, C2_BBYTES);
+#pragma unroll
+    for (int blk = 0; blk < 4; ++blk)
+      sm100::tma_load_4d_warp(bsm + blk * 16384, &map_w, bfull, 0, 0, blk, 0);
     // ---- TMA: even rows (coordinate 0) and odd rows (1), element stride 2 ----
     int j = 0;
     for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(C2_THREADS, 1)
     // ---- MMA: row taps a (plane offset 16a rows) x atoms e x 4 K16 steps ----
     constexpr uint32_t idesc = sm100::make_idesc_bf16(128, 128, 0, 0);
     const uint32_t s0 = sm100::smem_u32(stg), b0 = sm100::smem_u32(bsm);
+    sm100::mbar_wait(bfull, 0);
     int j = 0, acc = 0;
     uint32_t accph = 0;
     for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
@@ -243,6 +245,256 @@ __global__ void __launch_bounds__(C2_THREADS, 1)
   }
 }
 
+// ---- conv2 input gradient (sub-pixel classes) with the shifted-view trick --
+// dz1[2py+e][2px+pj][ci] = ELU'(a1) * sum_{a,b} dz2[py-a][px-b] . W2[:, 2a+e, 2b+pj, ci]:
+// rows m = py*16 + px (py < 8: the coarse row py = 8 only meets dz2 rows >= Ho,
+// its outputs are zero), N = (class 2e+pj, ci) = 128, K = (tap 2a+b, co) = 256.
+// dz2 is staged ONCE per image with a zero border (TMA box from (-1, -1): 9 x 16
+// rows of 128 B), tap (a, b) = plane rows from 17 - 16a - b on (a column wrap
+// lands on the next row's x = -1 border, which is zero); the ELU' operand a1 is
+// staged as four class planes (element stride 2 in x and y) whose row m is the
+// output pixel of TMEM row m; the bias gradient is summed from the stored bf16
+// values into 2^-32 fixed-point atomics (deterministic), as the engine path.
+constexpr int D2_EPI_WARPS = 8;
+constexpr int D2_THREADS = 32 * (2 + D2_EPI_WARPS);
+constexpr int D2_NSTG = 2;                        // images in flight (3 measured no faster)
+constexpr int D2_ZROWS = 152;                      // dz2 plane rows (144 + zero overrun)
+constexpr int D2_ZBYTES = D2_ZROWS * 128;
+constexpr int D2_ABYTES = 4 * 128 * 64;            // a1 class planes: 4 x 128 rows x 64 B
+constexpr int D2_STAGE = D2_ZBYTES + D2_ABYTES;
+constexpr int D2_BBYTES = 4 * 128 * 128;           // taps x 128 rows (class, ci)
+constexpr int D2_OBYTES = D2_EPI_WARPS * 2 * 2048;  // output staging: warp x class x 32 px x 64 B
+constexpr int D2_SMEM = 1024 + D2_NSTG * D2_STAGE + D2_BBYTES + D2_OBYTES + 256;
+
+struct D2Params {
+  int n_img, Hi, Wi;              // a1 / dz1 geometry (17 x 31)
+  const uint16_t* wt;             // [4 cls][32 ci][4 taps][64 co] (publish_derived)
+  uint16_t* dz;                   // dz1 [n_img][Hi][Wi][32]
+  unsigned long long* bacc;       // [16][32] fixed-point bias accumulators
+  unsigned* bcnt;
+  float* bout;
+};
+
+// two stores in flight per warp (one per class buffer): before refilling class
+// pj's buffer, at most one group (the other class's latest) may still read smem
+__device__ __forceinline__ void tma_store_wait_read_warp(int) {
+  sm100::tma_store_wait_read<1>();
+  __syncwarp();
+}
+
+__device__ __forceinline__ float d2_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int k = 8; k >= 1; k >>= 1) {
+    const bool up = (lane & k) != 0;
+#pragma unroll
+    for (int j = 0; j < k; ++j) {
+      const float send = up ? v[j] : v[j + k];
+      const float keep = up ? v[j + k] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+__global__ void __launch_bounds__(D2_THREADS, 1)
+    conv2_dgrad_kernel(const __grid_constant__ CUtensorMap map_dz2,
+                       const __grid_constant__ CUtensorMap map_a1,
+                       const __grid_constant__ CUtensorMap map_out,
+                       const __grid_constant__ CUtensorMap map_wt, const __grid_constant__ D2Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stg = smem;
+  uint8_t* bsm = stg + D2_NSTG * D2_STAGE;
+  uint8_t* osm = bsm + D2_BBYTES;                    // per-warp output staging (TMA stores)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(osm + D2_OBYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = full + D2_NSTG;
+  uint64_t* acc_full = empty + D2_NSTG;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bfull = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  __shared__ unsigned last_cta;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch(&map_dz2);
+    sm100::tma_prefetch(&map_a1);
+    sm100::tma_prefetch(&map_out);
+    sm100::tma_prefetch(&map_wt);
+    for (int s = 0; s < D2_NSTG; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1 + D2_EPI_WARPS);  // MMA commit + epilogue (a1 planes)
+    }
+    sm100::mbar_init(bfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&acc_full[s], 1);
+      sm100::mbar_init(&acc_empty[s], D2_EPI_WARPS);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) {
+    sm100::tmem_alloc(tmem_slot, 256);
+    sm100::tmem_relinquish();
+  }
+  for (int e = threadIdx.x; e < D2_NSTG * (D2_ZROWS - 144) * 8; e += D2_THREADS) {
+    const int st = e / ((D2_ZROWS - 144) * 8), r = e % ((D2_ZROWS - 144) * 8);
+    reinterpret_cast<uint4*>(stg + st * D2_STAGE + 144 * 128)[r] = make_uint4(0, 0, 0, 0);
+  }
+  APPO_PDL_ENTRY();  // dz2 and the derived weights come from earlier kernels
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // resident B by TMA: wt rows (class, ci) x K (tap, co), one SW128 box per tap
+    sm100::mbar_arrive_expect_tx_warp(bfull, D2_BBYTES);
+#pragma unroll
+    for (int tap = 0; tap < 4; ++tap)
+      sm100::tma_load_3d_warp(bsm + tap * 16384, &map_wt, bfull, tap * 64, 0, 0);
+    int j = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % D2_NSTG;
+      sm100::mbar_wait(&empty[s], ((j / D2_NSTG) & 1) ^ 1);
+      uint8_t* base = stg + s * D2_STAGE;
+      sm100::mbar_arrive_expect_tx_warp(&full[s], 144 * 128 + D2_ABYTES);
+      sm100::tma_load_4d_warp(base, &map_dz2, &full[s], 0, -1, -1, img);
+#pragma unroll
+      for (int cls = 0; cls < 4; ++cls)
+        sm100::tma_load_4d_warp(base + D2_ZBYTES + cls * 8192, &map_a1, &full[s], 0, cls & 1,
+                                cls >> 1, img);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = sm100::make_idesc_bf16(128, 128, 0, 0);
+    const uint32_t s0 = sm100::smem_u32(stg), b0 = sm100::smem_u32(bsm);
+    sm100::mbar_wait(bfull, 0);
+    int j = 0, acc = 0;
+    uint32_t accph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % D2_NSTG;
+      sm100::mbar_wait(&full[s], (j / D2_NSTG) & 1);
+      sm100::mbar_wait(&acc_empty[acc], accph ^ 1);
+      sm100::tc_fence_after();
+      const uint32_t d = tmem_base + acc * 128;
+#pragma unroll
+      for (int tap = 0; tap < 4; ++tap) {
+        const int a = tap >> 1, b = tap & 1;
+        const uint32_t arow = (uint32_t)(17 - 16 * a - b);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t ad = sm100::make_sdesc(s0 + s * D2_STAGE + arow * 128 + ks * 32, 16, 1024);
+          const uint64_t bd = sm100::make_sdesc(b0 + tap * 16384 + ks * 32, 16, 1024);
+          sm100::umma_f16_warp(d, ad, bd, idesc, (tap | ks) ? 1u : 0u);
+        }
+      }
+      sm100::umma_commit_warp(&empty[s]);
+      sm100::umma_commit_warp(&acc_full[acc]);
+      if (++acc == 2) { acc = 0; accph ^= 1; }
+    }
+  } else {
+    // epilogue: quarter q (rows m = 32q + lane), row parity e = part: classes 2e, 2e+1
+    const int ew = warp - 2, q = warp & 3, e = ew >> 2;
+    const int m = 32 * q + lane, py = m >> 4, px = m & 15;
+    float bs[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) bs[k] = 0.0f;
+    int j = 0, acc = 0;
+    uint32_t accph = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % D2_NSTG;
+      sm100::mbar_wait(&full[s], (j / D2_NSTG) & 1);  // a1 planes of this image
+      sm100::mbar_wait(&acc_full[acc], accph);
+      sm100::tc_fence_after();
+      const int Y = 2 * py + e;
+#pragma unroll
+      for (int pj = 0; pj < 2; ++pj) {
+        const int cls = 2 * e + pj, X = 2 * px + pj;
+        uint32_t r[32];
+        c2_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * 128 + cls * 32, r);
+        // ELU' operand: a1 class plane row m (64 B)
+        const uint4* ap = reinterpret_cast<const uint4*>(stg + s * D2_STAGE + D2_ZBYTES + cls * 8192 + m * 64);
+        uint4 av[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) av[c] = ap[c];
+        sm100::tmem_ld_wait();
+        const bool ok = Y < p.Hi && X < p.Wi;
+        uint32_t o[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t ww[4] = {av[c].x, av[c].y, av[c].z, av[c].w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float a0 = __uint_as_float(ww[t] << 16), a1v = __uint_as_float(ww[t] & 0xFFFF0000u);
+            const float v0 = __uint_as_float(r[8 * c + 2 * t]) * (a0 > 0.0f ? 1.0f : a0 + 1.0f);
+            const float v1 = __uint_as_float(r[8 * c + 2 * t + 1]) * (a1v > 0.0f ? 1.0f : a1v + 1.0f);
+            o[4 * c + t] = c2_bf16x2(v0, v1);
+          }
+        }
+        // stage the warp's 32 output pixels (box order: coarse row, px; 64 B each)
+        // and write them with one TMA store (the strided pixels of a class; X = Wi
+        // is clipped): per-lane stores at a 128-byte stride were LSU-bound
+        uint8_t* ob = osm + (ew * 2 + pj) * 2048;
+        tma_store_wait_read_warp(pj);  // this buffer's previous store has read it
+        uint4* sdst = reinterpret_cast<uint4*>(ob + lane * 64);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sdst[c] = make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        sm100::tma_store_4d_warp(&map_out, ob, 0, pj, 4 * q + e, img);
+        if (ok) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {  // the stored (rounded) values feed the bias gradient
+            bs[2 * k] += __uint_as_float(o[k] << 16);
+            bs[2 * k + 1] += __uint_as_float(o[k] & 0xFFFF0000u);
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        sm100::mbar_arrive(&acc_empty[acc]);
+        sm100::mbar_arrive(&empty[s]);
+      }
+      if (++acc == 2) { acc = 0; accph ^= 1; }
+    }
+    sm100::tma_store_wait_all();  // stores read their smem before the CTA exits
+    // bias gradient: lanes -> 32 column sums per warp -> fixed-point atomics
+    float lo[16], hi[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      lo[k] = bs[k];
+      hi[k] = bs[16 + k];
+    }
+    const float s_lo = d2_reduce16(lo, lane), s_hi = d2_reduce16(hi, lane);  // lane l < 16: column l (+16)
+    if (lane < 16) {
+      atomicAdd(p.bacc + (size_t)(blockIdx.x % 16) * 32 + lane,
+                (unsigned long long)llrint((double)s_lo * 4294967296.0));
+      atomicAdd(p.bacc + (size_t)(blockIdx.x % 16) * 32 + 16 + lane,
+                (unsigned long long)llrint((double)s_hi * 4294967296.0));
+    }
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * D2_EPI_WARPS) : "memory");  // epilogue warps only
+    if (ew == 0 && lane == 0) last_cta = atomicAdd(p.bcnt, 1u) == gridDim.x - 1;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * D2_EPI_WARPS) : "memory");
+    if (last_cta) {
+      __threadfence();
+      const int et = threadIdx.x - 64;
+      if (et < 32) {
+        unsigned long long v = 0;
+        for (int k = 0; k < 16; ++k) v += atomicExch(p.bacc + (size_t)k * 32 + et, 0ull);
+        p.bout[et] = (float)((double)(long long)v * (1.0 / 4294967296.0));
+      }
+      if (et == 0) *p.bcnt = 0;
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, 256);
+  }
+}
+
 }  // namespace
 
 const void* kanchor_conv2() { return reinterpret_cast<const void*>(&conv2_s2d_kernel); }
@@ -254,7 +506,7 @@ int conv2_s2d_forward(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, int
   if (Ho != (Hi - 4) / 2 + 1 || Wo != (Wi - 4) / 2 + 1 || Ho * 16 > 128 || Wo + 1 > 16 ||
       e.flags != (EPI_BIAS | EPI_ELU | EPI_BF16) || e.ldo != 64 || !e.bias ||
       (reinterpret_cast<uintptr_t>(a1) & 15) || (reinterpret_cast<uintptr_t>(e.out) & 15) ||
-      (Wi * 64) % 16)
+      (Wi * 64) % 16 || (reinterpret_cast<uintptr_t>(w2) & 15))
     return APPO_ERR_CONTRACT;
   // pixel-pair view of a1 [img][Hi][Wi][32] bf16: {64, Wi/2 pairs, Hi rows, n_img};
   // box {64, 16 pairs, Ho+1 rows at stride 2, 1} (pairs / rows outside -> 0)
@@ -269,6 +521,17 @@ int conv2_s2d_forward(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, int
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return APPO_ERR_CONTRACT;
+  CUtensorMap wmap;  // W2 [64 co][4 kh][4 kw][32 ci] as {64 (kw pair x ci), 2, 4, 64}
+  {
+    cuuint64_t dims[4] = {64, 2, 4, 64};
+    cuuint64_t str[3] = {128, 256, 1024};
+    cuuint32_t box[4] = {64, 2, 1, 64};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(w2), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return APPO_ERR_CONTRACT;
+  }
   C2Params p{};
   p.n_img = n_img;
   p.Ho = Ho;
@@ -288,7 +551,79 @@ int conv2_s2d_forward(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, int
   c->next_name = "conv2_s2d_tcgen05";
   c->next_flops = 2.0 * n_img * Ho * Wo * 64 * 512;
   c->next_bytes = 2.0 * n_img * ((double)Hi * Wi * 32 + (double)Ho * Wo * 64) + 2.0 * 64 * 512;
-  APPO_LAUNCH(c, conv2_s2d_kernel, grid, C2_THREADS, C2_SMEM, map, p);
+  APPO_LAUNCH(c, conv2_s2d_kernel, grid, C2_THREADS, C2_SMEM, map, wmap, p);
+  return APPO_OK;
+}
+
+int conv2_dgrad(Ctx* c, const DgradIn& in) {
+  if (!(in.N == 32 && in.Co == 64 && in.k == 4 && in.Hi == 17 && in.Wi == 31 && in.Ho == 7 &&
+        in.Wo == 14 && in.bias.out && in.bias.acc && in.bias.counter && in.n_img > 0 &&
+        !((reinterpret_cast<uintptr_t>(in.dz_next) | reinterpret_cast<uintptr_t>(in.dz) |
+           reinterpret_cast<uintptr_t>(in.aprev)) & 15)))
+    return APPO_ERR_CONTRACT;
+  EncodeTiledFnPublic enc = tensor_map_encoder();
+  if (!enc) return APPO_ERR_RESOURCE;
+  CUtensorMap mz, ma;
+  {  // dz2 [img][7][14][64], box {64, 16, 9, 1} from (-1, -1): zero border, SW128
+    cuuint64_t dims[4] = {64, (cuuint64_t)in.Wo, (cuuint64_t)in.Ho, (cuuint64_t)in.n_img};
+    cuuint64_t str[3] = {128, (cuuint64_t)in.Wo * 128, (cuuint64_t)in.Ho * in.Wo * 128};
+    cuuint32_t box[4] = {64, 16, 9, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&mz, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(in.dz_next), dims, str,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return APPO_ERR_CONTRACT;
+  }
+  {  // a1 [img][17][31][32] class planes: box {32, 32 (x stride 2), 16 (y stride 2), 1}
+    cuuint64_t dims[4] = {32, (cuuint64_t)in.Wi, (cuuint64_t)in.Hi, (cuuint64_t)in.n_img};
+    cuuint64_t str[3] = {64, (cuuint64_t)in.Wi * 64, (cuuint64_t)in.Hi * in.Wi * 64};
+    cuuint32_t box[4] = {32, 32, 16, 1};
+    cuuint32_t es[4] = {1, 2, 2, 1};
+    if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(in.aprev), dims, str,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return APPO_ERR_CONTRACT;
+  }
+  CUtensorMap mo;
+  {  // dz1 class boxes (TMA stores): box {32, 32 (x stride 2), 4 (y stride 2), 1}, X = Wi clipped
+    cuuint64_t dims[4] = {32, (cuuint64_t)in.Wi, (cuuint64_t)in.Hi, (cuuint64_t)in.n_img};
+    cuuint64_t str[3] = {64, (cuuint64_t)in.Wi * 64, (cuuint64_t)in.Hi * in.Wi * 64};
+    cuuint32_t box[4] = {32, 32, 4, 1};
+    cuuint32_t es[4] = {1, 2, 2, 1};
+    if (enc(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, in.dz, dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return APPO_ERR_CONTRACT;
+  }
+  CUtensorMap mw;  // wt [128 rows (class, ci)][256 (tap, co)], box {64, 128, 1}
+  {
+    const int st = make_tmap_bf16_3d(&mw, in.wt, 256, 128, 1, 512, 128 * 512, 64, 128, 1);
+    if (st) return st;
+  }
+  // input row 16 (coarse row 8) meets only dz2 rows >= Ho: zero
+  APPO_CUDA_TRY(cudaMemset2DAsync(in.dz + (size_t)16 * in.Wi * 32, (size_t)in.Hi * in.Wi * 32 * 2, 0,
+                                  (size_t)in.Wi * 32 * 2, in.n_img, c->stream));
+  D2Params p{};
+  p.n_img = in.n_img;
+  p.Hi = in.Hi;
+  p.Wi = in.Wi;
+  p.wt = in.wt;
+  p.dz = in.dz;
+  p.bacc = in.bias.acc;
+  p.bcnt = in.bias.counter;
+  p.bout = in.bias.out;
+  static int attr_bytes[64] = {};
+  const int dev = c->device & 63;
+  if (attr_bytes[dev] < D2_SMEM) {
+    APPO_CUDA_TRY(cudaFuncSetAttribute(conv2_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       D2_SMEM));
+    attr_bytes[dev] = D2_SMEM;
+  }
+  const int grid = c->num_sms < in.n_img ? c->num_sms : in.n_img;
+  c->next_name = "conv2_dgrad_s2d_tcgen05";
+  c->next_flops = 2.0 * in.n_img * in.Hi * in.Wi * 32.0 * 64 * 4;
+  c->next_bytes = 2.0 * in.n_img * ((double)in.Ho * in.Wo * 64 + 2.0 * in.Hi * in.Wi * 32);
+  APPO_LAUNCH(c, conv2_dgrad_kernel, grid, D2_THREADS, D2_SMEM, mz, ma, mo, mw, p);
   return APPO_OK;
 }
 

@@ -105,6 +105,9 @@ struct DgradIn {
   BiasOut bias;
 };
 int conv_dgrad_s2_bf16(Ctx* c, const DgradIn& in);
+// conv2's input gradient (N 32, Co 64, k 4, 17x31 <- 7x14) with the shifted-view
+// trick (conv2.cu); APPO_ERR_CONTRACT for any other geometry.
+int conv2_dgrad(Ctx* c, const DgradIn& in);
 
 // 3-D bf16 tensor map (dims innermost first, byte strides of dims 1 and 2),
 // 128B swizzle, zero OOB fill.

@@ -1069,7 +1069,16 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     in.n_img = B;
     in.Ho = d.H2; in.Wo = d.W2; in.Co = 64; in.Hi = d.H1; in.Wi = d.W1; in.N = 32; in.k = 4;
     in.bias = bias_out(3, G + d.off_c1b, 32);
-    TRY(conv_dgrad_s2_bf16(ctx, in));
+    // shifted-view kernel (conv2.cu) at the Doom shape, else the engine path
+    static const bool dgrad_engine = [] {
+      const char* v = getenv("APPO_CONV2");
+      return v && v[0] == 'e';
+    }();
+    const int dst = dgrad_engine ? APPO_ERR_CONTRACT : conv2_dgrad(ctx, in);
+    if (dst == APPO_ERR_CONTRACT)
+      TRY(conv_dgrad_s2_bf16(ctx, in));
+    else if (dst != APPO_OK)
+      return dst;
   }
   // ---- conv1 weight gradient (input is data): straight from the u8 images;
   //      im2col + GEMM only when the images cannot be TMA-staged ----

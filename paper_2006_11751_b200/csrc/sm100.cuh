@@ -48,6 +48,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---- TMA store (shared -> global, bulk groups) ------------------------------
+// Whole warp calls; the elected lane issues the store of a 4-D box and commits
+// it as one bulk group.  The smem source must have been written by the warp
+// and made visible to the async proxy (fence.proxy.async.shared::cta).
+__device__ __forceinline__ void tma_store_4d_warp(const CUtensorMap* map, const void* src,
+                                                  int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n\t"
+      "@e cp.async.bulk.commit_group;\n\t}" ::"l"(reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// Wait until at most n of this thread's bulk store groups still read their smem
+// source (the elected lane issued them: call from the whole warp, then __syncwarp).
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// Wait for the stores to be complete (global writes performed).
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---- TMA ---------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

@@ -1,10 +1,9 @@
 #!/bin/bash
-# bench throughput vs the sampler's SM budget (persistent grids of the sampler context)
+# bench value vs the sampler context's SM budget (--sampler-sms)
 cd $GRAFT_REPO_ROOT
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
-for n in ${SMS:-24 32 40 48 64}; do
-  timeout -s KILL 600 python bench.py --no-cpu-baseline --no-e2e --sampler-sms $n > gpurun_out/bench_sms_$n.log 2>&1
-  python -c "
-import json; d=json.loads(open('gpurun_out/bench_sms_$n.log').read().strip().splitlines()[-1]); print('sms $n value', round(d['value']), 'ms', round(d['ms_per_step'],2))"
+for s in ${SMS:-40 48 56 64 80}; do
+  timeout -s KILL 300 python bench.py --sampler-sms $s --no-cpu-baseline --no-e2e > gpurun_out/sms_$s.log 2>&1
+  echo "sms=$s $(tail -1 gpurun_out/sms_$s.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]/1e6,3))')"
 done
