@@ -16,6 +16,16 @@ AG_NAMES = {0: "gemm_bf16_tcgen05", 1: "gemm_conv_nhwc_gather_tcgen05",
             6: "gemm_conv_taps_wgrad_tcgen05"}
 
 
+# dedicated kernels: symbol -> the class name the library times them under
+SYMBOL_CLASSES = {"conv1_s2d_kernel": "conv1_s2d_tcgen05",
+                  "conv1_s2d_wgrad_kernel": "conv1_s2d_wgrad_tcgen05",
+                  "conv2_s2d_kernel": "conv2_s2d_tcgen05",
+                  "conv2_dgrad_kernel": "conv2_dgrad_s2d_tcgen05",
+                  "gru_infer_fused_kernel": "gru_infer_fused_tcgen05",
+                  "gru_g_fwd_kernel": "gru_seq_fwd_kernel",
+                  "gru_g_bwd_kernel": "gru_seq_bwd_kernel"}
+
+
 def kname(full: str) -> str:
     """Kernel class; GEMM engine instantiations by gather mode (the same names
     bench.py / the timing report use)."""
@@ -30,7 +40,8 @@ def kname(full: str) -> str:
     s = s.replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
     s = s.replace("appo_b200::", "")
     s = s.split("(")[0]
-    return re.sub(r"<.*", "", s)
+    s = re.sub(r"<.*", "", s)
+    return SYMBOL_CLASSES.get(s, s)
 
 
 def main():

@@ -12,6 +12,16 @@ AG_NAMES = {0: "gemm_bf16_tcgen05", 1: "gemm_conv_nhwc_gather_tcgen05",
             6: "gemm_conv_taps_wgrad_tcgen05"}
 
 
+# dedicated kernels: symbol -> the class name the library times them under
+SYMBOL_CLASSES = {"conv1_s2d_kernel": "conv1_s2d_tcgen05",
+                  "conv1_s2d_wgrad_kernel": "conv1_s2d_wgrad_tcgen05",
+                  "conv2_s2d_kernel": "conv2_s2d_tcgen05",
+                  "conv2_dgrad_kernel": "conv2_dgrad_s2d_tcgen05",
+                  "gru_infer_fused_kernel": "gru_infer_fused_tcgen05",
+                  "gru_g_fwd_kernel": "gru_seq_fwd_kernel",
+                  "gru_g_bwd_kernel": "gru_seq_bwd_kernel"}
+
+
 def klass(name):
     m = re.search(r"gemm_bf16_kernel<[^>]*?(\d+)\s*>", name.replace("(int)", "").replace("(bool)", ""))
     if "gemm_bf16_kernel" in name and m:
@@ -20,7 +30,7 @@ def klass(name):
     base = base.split("(")[0] if not base.startswith("(") else base
     base = base.replace("<unnamed>::", "").replace("(anonymous namespace)::", "")
     base = re.sub(r"<.*", "", base).split("::")[-1]
-    return base
+    return SYMBOL_CLASSES.get(base, base)
 
 
 def main(path):
