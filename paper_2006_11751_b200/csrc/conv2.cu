@@ -495,6 +495,127 @@ __global__ void __launch_bounds__(D2_THREADS, 1)
   }
 }
 
+// ---- conv2 weight gradient with the same planes ----------------------------
+// dW2[co][2a+e][2b+pj][ci] = sum over pixels k = y*16 + x of P_e[k + 16a + b][(pj, ci)]
+// * dz2[k][co], P_e = the even / odd-row pixel-pair planes of conv2_s2d_kernel.
+// Per image and (a, e): one chain of 7 K16 pixel steps with A = plane e from row
+// 16a on as an MN-major operand whose two M atoms are the column taps b = 0, 1
+// (LBO 128 B: one pixel row) and B = the dz2 rows (TMA box {64, 16, 7}: columns
+// x >= Wo are zero, so padding pixels add nothing); the four accumulators live in
+// TMEM for the CTA's share of images, are written once (per-CTA partials) and
+// reduced deterministically by splitk_reduce.
+constexpr int W2_NSTG = 3;
+constexpr int W2_DBYTES = 16 * 1024;                 // dz2 rows (112 used) x 128 B
+constexpr int W2_STAGE = 2 * C2_PLANE + W2_DBYTES;
+constexpr int W2_THREADS = 32 * 6;                   // TMA, MMA, 4 epilogue warps
+constexpr int W2_SMEM = 1024 + W2_NSTG * W2_STAGE + 256;
+
+struct W2Params {
+  int n_img, Ho;
+  float* partial;  // [gridDim.x][64 co][512 = (kh, kw, ci)]
+};
+
+__global__ void __launch_bounds__(W2_THREADS, 1)
+    conv2_wgrad_kernel(const __grid_constant__ CUtensorMap map_a1,
+                       const __grid_constant__ CUtensorMap map_dz2, const __grid_constant__ W2Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + W2_NSTG * W2_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = full + W2_NSTG;
+  uint64_t* done = empty + W2_NSTG;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int plane_rows = (p.Ho + 1) * 16;
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch(&map_a1);
+    sm100::tma_prefetch(&map_dz2);
+    for (int s = 0; s < W2_NSTG; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(done, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) {
+    sm100::tmem_alloc(tmem_slot, 256);
+    sm100::tmem_relinquish();
+  }
+  // plane rows past the TMA box meet dz2 zeros only: finite zeros
+  for (int e = threadIdx.x; e < W2_NSTG * 2 * (C2_PROWS - plane_rows) * 8; e += W2_THREADS) {
+    const int pl = e / ((C2_PROWS - plane_rows) * 8), r = e % ((C2_PROWS - plane_rows) * 8);
+    reinterpret_cast<uint4*>(smem + (pl >> 1) * W2_STAGE + (pl & 1) * C2_PLANE + plane_rows * 128)[r] =
+        make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  APPO_PDL_ENTRY();  // a1 / dz2 come from earlier kernels
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    int j = 0;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % W2_NSTG;
+      sm100::mbar_wait(&empty[s], ((j / W2_NSTG) & 1) ^ 1);
+      uint8_t* base = smem + s * W2_STAGE;
+      sm100::mbar_arrive_expect_tx_warp(&full[s], 2u * plane_rows * 128 + (uint32_t)p.Ho * 16 * 128);
+      sm100::tma_load_4d_warp(base, &map_a1, &full[s], 0, 0, 0, img);
+      sm100::tma_load_4d_warp(base + C2_PLANE, &map_a1, &full[s], 0, 0, 1, img);
+      sm100::tma_load_4d_warp(base + 2 * C2_PLANE, &map_dz2, &full[s], 0, 0, 0, img);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = sm100::make_idesc_bf16(128, 64, 1, 1);
+    const uint32_t s0 = sm100::smem_u32(smem);
+    int j = 0;
+    const int ksteps = p.Ho;  // 16-pixel K steps: Ho rows x 16 columns
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
+      const int s = j % W2_NSTG;
+      sm100::mbar_wait(&full[s], (j / W2_NSTG) & 1);
+      sm100::tc_fence_after();
+      const uint32_t st = s0 + s * W2_STAGE;
+#pragma unroll
+      for (int blk = 0; blk < 4; ++blk) {  // (a, e) = (blk >> 1, blk & 1)
+        const int a = blk >> 1, e = blk & 1;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const uint64_t ad = sm100::make_sdesc(st + e * C2_PLANE + (16 * a + 16 * ks) * 128, 128, 1024);
+          const uint64_t bd = sm100::make_sdesc(st + 2 * C2_PLANE + ks * 2048, 8192, 1024);
+          sm100::umma_f16_warp(tmem_base + blk * 64, ad, bd, idesc, (j | ks) ? 1u : 0u);
+        }
+      }
+      sm100::umma_commit_warp(&empty[s]);
+    }
+    sm100::umma_commit_warp(done);
+  } else {
+    // ---- final epilogue: TMEM row m = (b = m >> 6, pj = (m >> 5) & 1, ci = m & 31) ----
+    sm100::mbar_wait(done, 0);
+    sm100::tc_fence_after();
+    const int q = warp & 3, m = 32 * q + lane;
+    const int b = m >> 6, pj = (m >> 5) & 1, ci = m & 31;
+    float* out = p.partial + (size_t)blockIdx.x * 64 * 512;
+#pragma unroll
+    for (int blk = 0; blk < 4; ++blk) {
+      const int kh = 2 * (blk >> 1) + (blk & 1), kw = 2 * b + pj;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[32];
+        c2_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + blk * 64 + h * 32, r);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          out[(size_t)(h * 32 + c) * 512 + (kh * 4 + kw) * 32 + ci] = __uint_as_float(r[c]);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem_base, 256);
+  }
+}
+
 }  // namespace
 
 const void* kanchor_conv2() { return reinterpret_cast<const void*>(&conv2_s2d_kernel); }
@@ -625,6 +746,60 @@ int conv2_dgrad(Ctx* c, const DgradIn& in) {
   c->next_bytes = 2.0 * in.n_img * ((double)in.Ho * in.Wo * 64 + 2.0 * in.Hi * in.Wi * 32);
   APPO_LAUNCH(c, conv2_dgrad_kernel, grid, D2_THREADS, D2_SMEM, mz, ma, mo, mw, p);
   return APPO_OK;
+}
+
+int conv2_wgrad(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, const uint16_t* dz2, int Ho,
+                int Wo, float* dw) {
+  if (n_img <= 0) return APPO_OK;
+  if (Ho != (Hi - 4) / 2 + 1 || Wo != (Wi - 4) / 2 + 1 || Ho * 16 > 128 || Wo + 1 > 16 ||
+      ((reinterpret_cast<uintptr_t>(a1) | reinterpret_cast<uintptr_t>(dz2)) & 15) || (Wi * 64) % 16)
+    return APPO_ERR_CONTRACT;
+  EncodeTiledFnPublic enc = tensor_map_encoder();
+  if (!enc) return APPO_ERR_RESOURCE;
+  CUtensorMap ma, mz;
+  {  // the conv2_s2d_kernel planes: pixel pairs, rows at stride 2
+    cuuint64_t dims[4] = {64, (cuuint64_t)(Wi / 2), (cuuint64_t)Hi, (cuuint64_t)n_img};
+    cuuint64_t str[3] = {128, (cuuint64_t)Wi * 64, (cuuint64_t)Hi * Wi * 64};
+    cuuint32_t box[4] = {64, 16, (cuuint32_t)(2 * (Ho + 1)), 1};
+    cuuint32_t es[4] = {1, 1, 2, 1};
+    if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(a1), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return APPO_ERR_CONTRACT;
+  }
+  {  // dz2 [img][Ho][Wo][64]: box {64, 16, Ho, 1} (x >= Wo -> 0)
+    cuuint64_t dims[4] = {64, (cuuint64_t)Wo, (cuuint64_t)Ho, (cuuint64_t)n_img};
+    cuuint64_t str[3] = {128, (cuuint64_t)Wo * 128, (cuuint64_t)Ho * Wo * 128};
+    cuuint32_t box[4] = {64, 16, (cuuint32_t)Ho, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&mz, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(dz2), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return APPO_ERR_CONTRACT;
+  }
+  const int grid = c->num_sms < n_img ? c->num_sms : n_img;
+  float* part = nullptr;
+  const int wst = gemm_workspace(c, (size_t)grid * 64 * 512 * sizeof(float), &part);
+  if (wst) return wst;
+  W2Params p{};
+  p.n_img = n_img;
+  p.Ho = Ho;
+  p.partial = part;
+  static int attr_bytes[64] = {};
+  const int dev = c->device & 63;
+  if (attr_bytes[dev] < W2_SMEM) {
+    APPO_CUDA_TRY(cudaFuncSetAttribute(conv2_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       W2_SMEM));
+    attr_bytes[dev] = W2_SMEM;
+  }
+  c->next_name = "conv2_wgrad_s2d_tcgen05";
+  c->next_flops = 2.0 * n_img * Ho * Wo * 64.0 * 512;
+  c->next_bytes = 2.0 * n_img * ((double)Hi * Wi * 32 + (double)Ho * Wo * 64) + 4.0 * grid * 64 * 512;
+  APPO_LAUNCH(c, conv2_wgrad_kernel, grid, W2_THREADS, W2_SMEM, ma, mz, p);
+  Epilogue e;
+  e.out = dw;
+  e.ldo = 512;
+  return splitk_reduce(c, 64, 512, grid, part, e);
 }
 
 }  // namespace appo_b200

@@ -108,6 +108,10 @@ int conv_dgrad_s2_bf16(Ctx* c, const DgradIn& in);
 // conv2's input gradient (N 32, Co 64, k 4, 17x31 <- 7x14) with the shifted-view
 // trick (conv2.cu); APPO_ERR_CONTRACT for any other geometry.
 int conv2_dgrad(Ctx* c, const DgradIn& in);
+// conv2's weight gradient dw[co][(kh, kw, ci)] from a1 / dz2 with the same planes
+// (conv2.cu), per-CTA partials + deterministic reduce; APPO_ERR_CONTRACT outside.
+int conv2_wgrad(Ctx* c, const uint16_t* a1, int n_img, int Hi, int Wi, const uint16_t* dz2, int Ho,
+                int Wo, float* dw);
 
 // 3-D bf16 tensor map (dims innermost first, byte strides of dims 1 and 2),
 // 128B swizzle, zero OOB fill.

@@ -1059,7 +1059,17 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   // ---- conv2 backward ----
   {
     // weight gradient straight from a1 / dz2 (strided TMA windows, no col2)
-    TRY(conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, 32, s.dz2, d.H2, d.W2, 64, 4, G + d.off_c2w));
+    static const bool wgrad2_engine = [] {
+      const char* v = getenv("APPO_CONV2");
+      return v && v[0] == 'e';
+    }();
+    const int w2st = wgrad2_engine ? APPO_ERR_CONTRACT
+                                   : conv2_wgrad(ctx, s.a1, B, d.H1, d.W1, s.dz2, d.H2, d.W2,
+                                                 G + d.off_c2w);
+    if (w2st == APPO_ERR_CONTRACT)
+      TRY(conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, 32, s.dz2, d.H2, d.W2, 64, 4, G + d.off_c2w));
+    else if (w2st != APPO_OK)
+      return w2st;
     // dz1 = ELU'(a1) * conv2^T(dz2) (+ conv1 bias grad)
     DgradIn in;
     in.dz_next = s.dz2;
