@@ -7,20 +7,19 @@
 // With the s2d rows of a tile stored ONCE in shared memory as a K-major
 // SWIZZLE_128B matrix (one 128-byte row per s2d pixel: its C*16 values, zero
 // padded to 64), the operand "Z shifted by (a, b)" is the same smem matrix with
-// its descriptor start moved by (32a + b) rows.  The two row taps (a) are two
-// MMA chains into ONE TMEM accumulator; the two column taps (b) are the two
-// 32-column halves of an N = 64 B operand [W_a0; W_a1], added in the epilogue
-// with a one-lane shuffle (lane x takes lane x+1's b = 1 half).  Every
+// its descriptor start moved by (32a + b) rows: the four taps are four MMA
+// chains (N = 32, C K16 steps each) into ONE TMEM accumulator, and every
 // observation byte is converted to fp16 once (the im2col form of gemm.cu's
-// AG_U8 path builds every byte 4 times), and each K16 step reads its A rows
-// for 64 output columns (an N = 32 MMA is bound by its 4 KB A read: measured
-// 64 cycles per M128 K16 step either way).  Pipeline (warp-specialised,
-// persistent, one CTA per SM):
+// AG_U8 path builds every byte 4 times).  (Measured alternative: the column
+// taps as the two halves of an N = 64 B operand summed by a lane shuffle in the
+// epilogue -- half the MMAs, but the shuffles and the wider TMEM reads made the
+// issue-bound epilogue slower: 312 vs 281 us per 16 K images.)  Pipeline
+// (warp-specialised, persistent, one CTA per SM):
 //   warp 0        TMA: whole image {W, 4*Hs rows, C} per box into a staging ring
-//   warp 1        TMEM owner + MMA issuer (2 row taps x C K-steps of M128 N64 K16)
-//   warps 2..5    converters: staged u8 -> fp16 (1024 + v, exact) s2d windows
-//   warps 6..21   epilogue: TMEM -> scale/bias/ELU -> bf16 rows of a1 (4 warps
-//                 per TMEM lane quarter, 8 output channels each)
+//   warp 1        TMEM owner + MMA issuer (4 taps x C K-steps of M128 N32 K16)
+//   warps 2..9    converters: staged u8 -> fp16 (1024 + v, exact) s2d windows
+//   warps 10..17  epilogue: TMEM -> scale/bias/ELU -> bf16 rows of a1 (2 warps
+//                 per TMEM lane quarter, 16 output channels each)
 // The 1024 offset is removed through the corrected bias of the published copy
 // (k_conv1_half_weights), so A is exact and B is the fp16 weights.
 //
@@ -42,10 +41,10 @@ namespace appo_b200 {
 namespace {
 
 #ifndef C1_CONV_WARPS_DEF
-#define C1_CONV_WARPS_DEF 4
+#define C1_CONV_WARPS_DEF 8
 #endif
 #ifndef C1_EPI_PARTS_DEF
-#define C1_EPI_PARTS_DEF 4
+#define C1_EPI_PARTS_DEF 2
 #endif
 constexpr int C1_CONV_WARPS = C1_CONV_WARPS_DEF;
 constexpr int C1_TMA = 0, C1_MMA = 1;  // warp roles (MMA on warp 0 measured no faster)
@@ -61,7 +60,7 @@ constexpr int C1_THREADS = 32 * (2 + C1_CONV_WARPS + C1_EPI_WARPS);
 #endif
 constexpr int C1_NSTG = C1_NSTG_DEF;  // staged images in flight
 constexpr int C1_NA = C1_NA_DEF;      // s2d A windows (one per 128-row tile)
-constexpr int C1_NACC = 4;    // TMEM accumulators of 64 columns
+constexpr int C1_NACC = 4;    // TMEM accumulators (64 columns apart; 32 used)
 constexpr int C1_WROWS = 168; // window rows: 5 s2d rows x 32 px + 1 (x-tap overrun), to 8
 constexpr int C1_WBYTES = C1_WROWS * 128;  // one window (SW128 rows, 1024-aligned)
 
@@ -204,13 +203,14 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
   // B operand of row tap a: row n = (output channel co = n >> 1, column tap
   // b = n & 1), chunk kc = 2c + h holds 8 fp16 W[co][c][4a + 2h + ii][4b + j]
   // (ii = 0, 1; j = 0..3), the same (ii, j) order as the A chunks
-  for (int e = threadIdx.x; e < 2 * 2 * C * 64; e += C1_THREADS) {
-    const int n = e & 63, kc = (e >> 6) % (2 * C), a = (e >> 6) / (2 * C);
-    const int c = kc >> 1, h = kc & 1, b = n & 1, co = n >> 1;
+  // (A/B variant) B of tap tau = 2a + b: row co, 32 rows per tap
+  for (int e = threadIdx.x; e < 4 * 2 * C * 32; e += C1_THREADS) {
+    const int co = e & 31, kc = (e >> 5) % (2 * C), tau = (e >> 5) / (2 * C);
+    const int c = kc >> 1, h = kc & 1, a = tau >> 1, b = tau & 1;
     const uint16_t* src = p.w + (size_t)co * (C * 64) + c * 64 + (4 * a + 2 * h) * 8 + 4 * b;
     const uint2 lo = *reinterpret_cast<const uint2*>(src);
     const uint2 hi = *reinterpret_cast<const uint2*>(src + 8);
-    *reinterpret_cast<uint4*>(bsm + a * 8192 + n * 128 + ((kc ^ (n & 7)) << 4)) =
+    *reinterpret_cast<uint4*>(bsm + tau * 4096 + co * 128 + ((kc ^ (co & 7)) << 4)) =
         make_uint4(lo.x, lo.y, hi.x, hi.y);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
     }
   } else if (warp == C1_MMA) {
     // ---- MMA issuer: per tile, 2 row taps x C K16 steps into one accumulator ----
-    constexpr uint32_t idesc = sm100::make_idesc_f16(128, 64, 0, 0);
+    constexpr uint32_t idesc = sm100::make_idesc_f16(128, 32, 0, 0);
     const uint32_t a0 = sm100::smem_u32(awin), b0 = sm100::smem_u32(bsm);
     int a = 0, acc = 0, tile_i = 0;
     uint32_t aph = 0, accph = 0;
@@ -255,12 +255,13 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
         const uint32_t d = tmem_base + acc * 64;
         const uint32_t abase = a0 + a * C1_WBYTES;
 #pragma unroll
-        for (int ta = 0; ta < 2; ++ta) {
+        for (int tau = 0; tau < 4; ++tau) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const uint64_t ad = sm100::make_sdesc(abase + ta * 32 * 128 + c * 32, 16, 1024);
-            const uint64_t bd = sm100::make_sdesc(b0 + ta * 8192 + c * 32, 16, 1024);
-            sm100::umma_f16_warp(d, ad, bd, idesc, (ta | c) ? 1u : 0u);
+            const uint64_t ad = sm100::make_sdesc(
+                abase + (32 * (tau >> 1) + (tau & 1)) * 128 + c * 32, 16, 1024);
+            const uint64_t bd = sm100::make_sdesc(b0 + tau * 4096 + c * 32, 16, 1024);
+            sm100::umma_f16_warp(d, ad, bd, idesc, (tau | c) ? 1u : 0u);
           }
         }
         sm100::umma_commit_warp(&a_empty[a]);
@@ -354,20 +355,15 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
         if (ew == 0 && lane == 0) C1_PROF(tile_i, 5);
         const int y = 4 * t + q;
         if (y < p.Ho) {  // warp-uniform
-          uint32_t r[2 * C1_EPI_CO];
-          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 64 + part * 2 * C1_EPI_CO;
-          if constexpr (C1_EPI_CO == 16) tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
-          else sm100::tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+          static_assert(C1_EPI_CO == 16, "4-tap variant: 16 channels per epilogue warp");
+          uint32_t r[16];
+          sm100::tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * 64 + part * 16, r);
           sm100::tmem_ld_wait();
           if (ew == 0 && lane == 0) C1_PROF(tile_i, 11);
           uint32_t w[C1_EPI_CO / 2];
 #pragma unroll
           for (int k = 0; k < C1_EPI_CO / 2; ++k) {
-            // column tap b = 0 at pixel x plus b = 1 taken from pixel x + 1
-            const uint64_t v = fadd2(
-                f2pack(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 2])),
-                f2pack(__shfl_down_sync(0xffffffffu, __uint_as_float(r[4 * k + 1]), 1),
-                       __shfl_down_sync(0xffffffffu, __uint_as_float(r[4 * k + 3]), 1)));
+            const uint64_t v = f2pack(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]));
             const float2 x = f2unpack(ffma2(v, scale2, bias2[k]));
             const float2 tl = f2unpack(ffma2(v, scale2l, bias2l[k]));  // x * log2(e)
             const float2 e = f2unpack(fadd2(f2pack(ex2_ftz(fminf(tl.x, 0.0f)), ex2_ftz(fminf(tl.y, 0.0f))), mone2));
