@@ -124,7 +124,11 @@ constexpr int G_KB = 128 * 128;             // one 64-wide K block of the 128-ro
 constexpr int G_A = 2 * G_KB;               // A tile: 32 KB
 constexpr int G_NB = GQ * NG;               // 192 B rows
 constexpr int G_B = 2 * G_NB * 128;         // 48 KB
-constexpr int G_FWD_SMEM = 1024 + G_A + G_B + GQ * GT * NG * 4 + 64;
+// partial-sum rows padded to 52 floats: the lane-per-row float4 stores of the
+// TMEM readout hit 8 distinct bank groups (a 48-float pitch put 16 lanes on
+// one bank: 16-way conflicts on every store)
+constexpr int GQS = NG + 4;
+constexpr int G_FWD_SMEM = 1024 + G_A + G_B + GQ * GT * GQS * 4 + 64;
 
 struct GFwdArgs {
   CUtensorMap hmap;      // 3-D map over hbuf_bf {512, n_traj, 2}, box {64, 32, 1}, SW128
@@ -151,8 +155,8 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
                                            ~uintptr_t(1023));
   uint8_t* tA = sm;
   uint8_t* tB = sm + G_A;
-  float* gq = reinterpret_cast<float*>(tB + G_B);                 // [GQ][GT][NG] partial sums
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(gq + GQ * GT * NG);
+  float* gq = reinterpret_cast<float*>(tB + G_B);                 // [GQ][GT][GQS] partial sums
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(gq + GQ * GT * GQS);
   uint64_t* kbar = mbar + 1;  // [2] one per K block (all four quarters of it)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kbar + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -263,9 +267,11 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
         sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + NG * warp + cb,
                          *reinterpret_cast<uint32_t(*)[16]>(r + cb));
       sm100::tmem_ld_wait();
-      float* dst = gq + (warp * GT + lane) * NG;
+      float4* dst = reinterpret_cast<float4*>(gq + (warp * GT + lane) * GQS);
 #pragma unroll
-      for (int q = 0; q < NG; ++q) dst[q] = __uint_as_float(r[q]);
+      for (int q = 0; q < NG / 4; ++q)
+        dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                             __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
     }
     sm100::tc_fence_before();
     __syncthreads();
@@ -277,8 +283,8 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
 #pragma unroll
       for (int g = 0; g < 3; ++g) {
         const int n = g * UPC_F + u;
-        ghv[c][g] = ((gq[(0 * GT + cl[c]) * NG + n] + gq[(1 * GT + cl[c]) * NG + n]) +
-                     (gq[(2 * GT + cl[c]) * NG + n] + gq[(3 * GT + cl[c]) * NG + n])) +
+        ghv[c][g] = ((gq[(0 * GT + cl[c]) * GQS + n] + gq[(1 * GT + cl[c]) * GQS + n]) +
+                     (gq[(2 * GT + cl[c]) * GQS + n] + gq[(3 * GT + cl[c]) * GQS + n])) +
                     b3[c][g];
       }
     }
@@ -350,7 +356,8 @@ constexpr int GKB_Q = kGates / GQ;                // 384 gates per K quarter = 6
 constexpr int G_BA = 6 * G_KB;                    // A: 96 KB
 constexpr int G_BN = GQ * UPC_GB;                 // 64 B rows
 constexpr int G_BB = 6 * G_BN * 128;              // B: 48 KB
-constexpr int G_BWD_SMEM = 1024 + G_BA + G_BB + GQ * GT * UPC_GB * 4 + 64;
+constexpr int MMS = UPC_GB + 4;  // padded partial-sum rows (conflict-free float4 stores)
+constexpr int G_BWD_SMEM = 1024 + G_BA + G_BB + GQ * GT * MMS * 4 + 64;
 
 struct GBwdArgs {
   CUtensorMap xmap;     // 3-D map over dghx {1536, n_traj, 2}, box {64, 32, 1}, SW128
@@ -379,7 +386,7 @@ __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant
   uint8_t* tA = sm;
   uint8_t* tB = sm + G_BA;
   float* mm = reinterpret_cast<float*>(tB + G_BB);          // [GQ][GT][16] partial sums
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(mm + GQ * GT * UPC_GB);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(mm + GQ * GT * MMS);
   uint64_t* kbar = mbar + 1;  // [3] one per two K blocks (32 KB)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(kbar + 3);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -467,8 +474,8 @@ __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant
       const float dnext =
           (t == a.T - 1)
               ? 0.0f
-              : ddr[c] + ((mm[(0 * GT + cl[c]) * UPC_GB + u] + mm[(1 * GT + cl[c]) * UPC_GB + u]) +
-                          (mm[(2 * GT + cl[c]) * UPC_GB + u] + mm[(3 * GT + cl[c]) * UPC_GB + u]));
+              : ddr[c] + ((mm[(0 * GT + cl[c]) * MMS + u] + mm[(1 * GT + cl[c]) * MMS + u]) +
+                          (mm[(2 * GT + cl[c]) * MMS + u] + mm[(3 * GT + cl[c]) * MMS + u]));
       const float dh = pf[c][0] + pf[c][6] * dnext;
       const float r = pf[c][1], z = pf[c][2], n = pf[c][3], ghn = pf[c][4], hp = pf[c][5];
       const float dnn = dh * (1.0f - z);
@@ -559,9 +566,11 @@ __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant
       uint32_t r[16];
       sm100::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + UPC_GB * warp, r);
       sm100::tmem_ld_wait();
-      float* dst = mm + (warp * GT + lane) * UPC_GB;
+      float4* dst = reinterpret_cast<float4*>(mm + (warp * GT + lane) * MMS);
 #pragma unroll
-      for (int u = 0; u < UPC_GB; ++u) dst[u] = __uint_as_float(r[u]);
+      for (int u = 0; u < UPC_GB / 4; ++u)
+        dst[u] = make_float4(__uint_as_float(r[4 * u]), __uint_as_float(r[4 * u + 1]),
+                             __uint_as_float(r[4 * u + 2]), __uint_as_float(r[4 * u + 3]));
     }
     sm100::tc_fence_before();
     __syncthreads();
