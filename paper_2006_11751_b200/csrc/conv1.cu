@@ -111,6 +111,18 @@ int c1_slack(int tiles, int box_rows, int W) {
 // operand is only a start-address change.
 
 
+// MN-major SWIZZLE_64B descriptor (atoms of 32 bf16 MN elements x 8 K rows of
+// 64 B): lbo = stride between MN atoms, sbo = between 8-row K groups
+__device__ __forceinline__ uint64_t sdesc_mn_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -442,19 +454,29 @@ int c1_launch(Ctx* c, const CUtensorMap& mo, const CUtensorMap& mbt, const C1Par
 // tile of 4 s2d rows Y (128 pixels), ONE MMA chain of 8 K16 pixel steps with
 // A = the s2d window as an MN-major SW128 operand whose two 64-row M atoms are
 // the column taps b = 0, 1 (atom stride LBO = 128 B = one pixel row: the
-// shifted view again) and B = dz1 rows 4t-1 .. 4t+3 (TMA box {64 channels (32
-// real, OOB zero), 32 x, 5 rows}, MN-major) whose two 64-wide N atoms are the
-// row taps a = 1, 0 (atom stride 4 KB = one dz1 row).  The accumulator
-// [128 x 128] lives in TMEM for the CTA's whole share of images (split-K over
+// shifted view again) and B = dz1 rows 4t-1 .. 4t+3 (TMA box {32 channels, 32
+// x, 5 rows}, MN-major SWIZZLE_64B) whose two 32-wide N atoms are the row taps
+// a = 1, 0 (atom stride 2 KB = one dz1 row; N = 64 with no zero padding: the
+// MMA time is proportional to N, measured 16 cycles per M128 N32 K16 step).  The accumulator
+// [128 x 64] lives in TMEM for the CTA's whole share of images (split-K over
 // the CTAs), is written once at the end and reduced deterministically.  Pixels
 // outside the image (x = Wo, rows -1 and >= Ho) have dz1 = 0 from the TMA zero
 // fill, so window rows past the image contribute nothing.  Operands are bf16 here (dz1 is bf16;
 // u8 -> bf16 is exact), so the converters build exact bf16 values.
 constexpr int W1_CONV_WARPS = 8;
 constexpr int W1_THREADS = 32 * (3 + W1_CONV_WARPS);  // image TMA, MMA, dz1 TMA, converters
-constexpr int W1_NSTG = 3, W1_NA = 3, W1_ND = 3;
+#ifndef W1_NSTG_DEF
+#define W1_NSTG_DEF 3
+#endif
+#ifndef W1_NA_DEF
+#define W1_NA_DEF 3
+#endif
+#ifndef W1_ND_DEF
+#define W1_ND_DEF 6  // dz1 tiles in flight (3 -> 6: 44 -> 39 us, measured)
+#endif
+constexpr int W1_NSTG = W1_NSTG_DEF, W1_NA = W1_NA_DEF, W1_ND = W1_ND_DEF;
 constexpr int W1_DROWS = 5;                           // dz1 rows per tile (4t-1 .. 4t+3)
-constexpr int W1_DBYTES = 64 * 2 * 32 * W1_DROWS;     // dz1 tile {64 ch, 32 x, 5 rows} bf16
+constexpr int W1_DBYTES = 32 * 2 * 32 * W1_DROWS;     // dz1 tile {32 ch, 32 x, 5 rows} bf16, SW64
 
 struct W1Params {
   int n_img, C, H, W, Ho, Wo, Hs, tiles, box_rows, stg_bytes, slack;
@@ -554,8 +576,8 @@ __global__ void __launch_bounds__(W1_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ---- MMA: per tile, 8 K16 pixel steps; M = (b, feature), N = (a = 1, 0; channel) ----
-    constexpr uint32_t idesc = sm100::make_idesc_bf16(128, 128, 1, 1);
+    // ---- MMA: per tile, 8 K16 pixel steps; M = (b, feature), N = (a = 1, 0; channel) = 64 ----
+    constexpr uint32_t idesc = sm100::make_idesc_bf16(128, 64, 1, 1);
     const uint32_t a0 = sm100::smem_u32(awin), d0 = sm100::smem_u32(dtl);
     int a = 0, d = 0;
     uint32_t aph = 0, dph = 0, acc = 0;
@@ -569,9 +591,9 @@ __global__ void __launch_bounds__(W1_THREADS, 1)
         for (int ks = 0; ks < 8; ++ks) {
           // A: pixels 16ks.. of the tile, M atoms b = 0, 1 one pixel row apart
           // (LBO = 128 B); B: dz1 of the same pixels one row up (a = 1, N atom 0)
-          // and of the same row (a = 0, N atom 1, LBO = 4 KB)
+          // and of the same row (a = 0, N atom 1, LBO = 2 KB)
           const uint64_t ad = sm100::make_sdesc(wb + 16 * ks * 128, 128, 1024);
-          const uint64_t bd = sm100::make_sdesc(db + 16 * ks * 128, 4096, 1024);
+          const uint64_t bd = sdesc_mn_sw64(db + 16 * ks * 64, 2048, 512);
           sm100::umma_f16_warp(tmem_base, ad, bd, idesc, (acc | ks) ? 1u : 0u);
         }
         acc = 1;
@@ -650,9 +672,9 @@ __global__ void __launch_bounds__(W1_THREADS, 1)
       const int c = f >> 4, i = (f >> 2) & 3, jj = f & 3;
       float* out = p.partial + (size_t)blockIdx.x * 32 * (C * 64);
 #pragma unroll
-      for (int ta = 0; ta < 2; ++ta) {  // TMEM columns 64 * (1 - ta): row tap ta
+      for (int ta = 0; ta < 2; ++ta) {  // TMEM columns 32 * (1 - ta): row tap ta
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (1 - ta) * 64, r);
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (1 - ta) * 32, r);
         sm100::tmem_ld_wait();
         if (f < 16 * C) {
           const int k = c * 64 + (4 * ta + i) * 8 + 4 * b + jj;
@@ -766,7 +788,7 @@ int conv1_s2d_wgrad(Ctx* c, const ConvIn& in, const uint16_t* dz1, float* dw, fl
   if (!make_u8_image_maps(&mo, &mbt, in, p.box_rows)) return APPO_ERR_CONTRACT;
   // dz1 [img][Ho][Wo][32] bf16, box {64 (32 real), 32, 5, 1}: out-of-range -> 0
   const int st = make_tmap_bf16_4d(&mdz, dz1, 32, (uint64_t)in.Wo, (uint64_t)in.Ho,
-                                   (uint64_t)in.n_img, 64, 32, W1_DROWS, 1);
+                                   (uint64_t)in.n_img, 32, 32, W1_DROWS, 1, 64);
   if (st) return st;
   const int grid = c->num_sms < p.n_img ? c->num_sms : p.n_img;
   const int K1 = p.C * 64;

@@ -1993,7 +1993,8 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
 }
 
 int make_tmap_bf16_4d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
-                      uint64_t d3, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+                      uint64_t d3, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
+                      int swizzle_bytes) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -2004,7 +2005,8 @@ int make_tmap_bf16_4d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
   cuuint32_t box[4] = {b0, b1, b2, b3};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (4d) failed: " + std::to_string((int)r));

@@ -119,9 +119,10 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
                       uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
                       uint32_t b2, int swizzle_bytes = 128);
 
-// 4-D bf16 tensor map over a dense [d3][d2][d1][d0] array, 128B swizzle, zero OOB fill.
+// 4-D bf16 tensor map over a dense [d3][d2][d1][d0] array, 128B (or 64B) swizzle, zero OOB fill.
 int make_tmap_bf16_4d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
-                      uint64_t d3, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3);
+                      uint64_t d3, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
+                      int swizzle_bytes = 128);
 
 // conv1 weight gradient straight from the u8 images (no im2col):
 // dw[co][(c,kh,kw)] = scale * sum_pixels dz1[pixel][co] * obs window; in
