@@ -15,7 +15,10 @@ from test_model_gpu import (GNORM_TOL, GRAD_TOL, H_TOL, LOGPI_TOL, LOSS_ATOL, LO
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(1, 40, 64, 4, 8), (2, 48, 64, 3, 16), (4, 72, 128, 5, 16), (3, 56, 128, 6, 8)]
+# the last shape has 12 actions: above the fused GRU step's 7, so inference
+# takes the unfused gate GEMMs + gru_infer_kernel
+SHAPES = [(1, 40, 64, 4, 8), (2, 48, 64, 3, 16), (4, 72, 128, 5, 16), (3, 56, 128, 6, 8),
+          (3, 72, 128, 12, 8)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -34,7 +37,8 @@ def test_policy_forward_other_shapes(oracle, shape):
     launched = {r["name"] for r in ctx.timing_report()}
     ctx.set_timing(False)
     # the dedicated kernels ran (not an engine fallback)
-    assert {"conv1_s2d_tcgen05", "conv2_s2d_tcgen05", "gru_infer_fused_tcgen05"} <= launched, launched
+    gru = "gru_infer_fused_tcgen05" if A <= 7 else "gru_infer_kernel"
+    assert {"conv1_s2d_tcgen05", "conv2_s2d_tcgen05", gru} <= launched, launched
     ref = oracle.policy_forward((C_, H, W, A), th.astype(np.float64), obs, h.astype(np.float64))
     lg = out["logits"].cpu().numpy().astype(np.float64)
     assert np.abs(log_softmax(lg) - log_softmax(ref["logits"])).max() <= LOGPI_TOL
