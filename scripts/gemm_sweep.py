@@ -37,6 +37,15 @@ def main():
             run(ctx, 16384, 1536, 512, bn=bn, reps=20)
             run(ctx, 16384, 512, 2304, bn=bn, reps=20)
         return
+    if os.environ.get("SWEEP") == "wgrad2":
+        # round 2: split-K choices that fill 148 SMs in one wave (per-SM L2 intake bound)
+        for bn, sp in ((64, 1), (128, 3), (64, 2), (256, 6), (128, 2)):
+            run(ctx, 1536, 512, 2048, a_mn=True, b_mn=True, bn=bn, splits=sp)
+        for bn, sp in ((64, 1), (128, 2), (256, 4), (192, 3)):
+            run(ctx, 512, 2304, 2048, a_mn=True, b_mn=True, bn=bn, splits=sp)
+        for bn, sp in ((64, 1), (128, 2), (256, 4)):
+            run(ctx, 2112, 512, 2304, bn=bn, splits=sp)
+        return
     if os.environ.get("SWEEP") == "wgrad":
         for bn, sp in ((256, 1), (256, 2), (256, 3), (128, 1), (128, 2), (128, 4), (64, 1)):
             run(ctx, 1536, 512, 2048, a_mn=True, b_mn=True, bn=bn, splits=sp)
