@@ -113,7 +113,9 @@ APPO_API int appo_ctx_sync(appo_ctx* ctx);
 APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);
 /* Per-launch CUDA-event timing of this library's kernels on the ctx stream
  * (name_filter: only kernels of that name, or of any of several names
- * separated by '|'; NULL = all).  The report is JSON
+ * separated by '|'; NULL = all; a prefix "@N:" brackets only every N-th
+ * matching launch, since the events end the programmatic-dependent-launch
+ * overlap of the launches they separate).  The report is JSON
  * lines {"name", "launches", "ms", "flops", "bytes"} (algorithmic work per
  * launch as recorded by the launcher); it synchronizes and resets. */
 APPO_API int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter);

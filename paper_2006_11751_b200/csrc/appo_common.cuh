@@ -46,6 +46,8 @@ struct Ctx {
   // timing
   bool timing = false;
   std::string timing_filter;
+  int timing_stride = 1;      // time every N-th matching launch ("@N:" filter prefix)
+  uint64_t timing_seq = 0;
   std::vector<TimedLaunch> timed;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -171,6 +173,9 @@ inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
   if (!c->timing_filter.empty() && c->timing_filter != "gemm_shapes" &&
       ("|" + c->timing_filter + "|").find("|" + std::string(name) + "|") == std::string::npos)
     return nullptr;
+  // sampling: only every timing_stride-th matching launch is bracketed (an
+  // event between two kernels ends their programmatic-dependent-launch overlap)
+  if (c->timing_stride > 1 && (c->timing_seq++ % (uint64_t)c->timing_stride) != 0) return nullptr;
   cudaEvent_t e = timing_event(c);
   cudaEventRecord(e, c->stream);
   return e;

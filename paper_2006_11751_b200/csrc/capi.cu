@@ -203,7 +203,16 @@ int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter) {
   CTX_OR_RETURN(ctx);
   APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   ctx->timing = enable != 0;
-  ctx->timing_filter = name_filter ? name_filter : "";
+  std::string f = name_filter ? name_filter : "";
+  ctx->timing_stride = 1;
+  ctx->timing_seq = 0;
+  if (f.size() > 1 && f[0] == '@') {  // "@N:names": sample every N-th matching launch
+    const size_t colon = f.find(':');
+    ctx->timing_stride = atoi(f.substr(1, colon == std::string::npos ? std::string::npos : colon - 1).c_str());
+    if (ctx->timing_stride < 1) ctx->timing_stride = 1;
+    f = colon == std::string::npos ? std::string() : f.substr(colon + 1);
+  }
+  ctx->timing_filter = f;
   ctx->timed.clear();
   ctx->ev_used = 0;
   return APPO_OK;
