@@ -920,35 +920,47 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
                   Operand{wb + d.off_whh, kHidden, false}, g, 128));
     TRY(k_gru_train(ctx, n_traj, T, t, s.gi, s.gh, s.done, s.hcur, s.core, s.core_bf, s.gates));
   }
-  TRY(k_heads_fwd(ctx, R, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
-                  th + d.off_bv, s.logits, s.values, B, s.act, s.tlogp, s.ent));
-
-  // ---- targets: logp/entropy, V-trace, advantages ----
-  TRY(launch_vtrace(ctx, n_traj, T, s.rew, s.values, s.values + B, s.tlogp, s.blogp, s.done,
-                    hp->gamma, hp->rho_bar, hp->c_bar, s.vt, s.pg, nullptr, nullptr));
-  const float* adv = s.pg;
-  if (hp->adv_source == 1 || hp->adv_source == 2) {
-    const float lam = hp->adv_source == 1 ? 1.0f : hp->gae_lambda;
-    TRY(launch_gae(ctx, n_traj, T, s.rew, s.values, s.values + B, s.done, hp->gamma, lam, s.adv,
-                   nullptr));
-    adv = s.adv;
-  } else if (hp->normalize_adv) {
-    APPO_CUDA_TRY(cudaMemcpyAsync(s.adv, s.pg, sizeof(float) * B, cudaMemcpyDeviceToDevice, st));
-    adv = s.adv;
-  }
-  if (hp->normalize_adv) TRY(k_normalize(ctx, B, s.adv));
-
-  // ---- loss and its gradient wrt logits / value ----
   LossHP lh{hp->clip_low, hp->clip_high, hp->value_coef, hp->entropy_coef};
-  TRY(k_ppo_loss(ctx, B, d.A, s.logits, s.values, s.act, s.blogp, adv, s.vt, lh, s.dlog,
-                 s.dhead, s.stats, s.ver, M->version));
-
   float* G = M->grad;
-  APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
+  if (traj_loss_supported(n_traj, T, d.A, hp->normalize_adv != 0)) {
+    // heads, targets, loss and heads backward fused per trajectory (traj_loss.cu)
+    APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
+    const bool gae = hp->adv_source == 1 || hp->adv_source == 2;
+    const float lam = hp->adv_source == 1 ? 1.0f : hp->gae_lambda;
+    TRY(k_traj_loss(ctx, n_traj, T, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
+                    th + d.off_bv, s.act, s.rew, s.blogp, s.done, s.ver, M->version, hp->gamma,
+                    hp->rho_bar, hp->c_bar, gae, lam, lh, s.logits, s.values, s.vt, s.pg, s.adv,
+                    s.dcore, s.colsum_part, s.stats, G + d.off_wpi, G + d.off_bpi, G + d.off_wv,
+                    G + d.off_bv));
+  } else {
+    TRY(k_heads_fwd(ctx, R, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
+                    th + d.off_bv, s.logits, s.values, B, s.act, s.tlogp, s.ent));
 
-  // ---- heads backward: dcore + head weight / bias gradients, one launch ----
-  TRY(k_heads_bwd_fused(ctx, B, d.A, s.dlog, s.core, th + d.off_wpi, th + d.off_wv, s.dcore,
-                        s.colsum_part, G + d.off_wpi, G + d.off_bpi, G + d.off_wv, G + d.off_bv));
+    // ---- targets: logp/entropy, V-trace, advantages ----
+    TRY(launch_vtrace(ctx, n_traj, T, s.rew, s.values, s.values + B, s.tlogp, s.blogp, s.done,
+                      hp->gamma, hp->rho_bar, hp->c_bar, s.vt, s.pg, nullptr, nullptr));
+    const float* adv = s.pg;
+    if (hp->adv_source == 1 || hp->adv_source == 2) {
+      const float lam = hp->adv_source == 1 ? 1.0f : hp->gae_lambda;
+      TRY(launch_gae(ctx, n_traj, T, s.rew, s.values, s.values + B, s.done, hp->gamma, lam, s.adv,
+                     nullptr));
+      adv = s.adv;
+    } else if (hp->normalize_adv) {
+      APPO_CUDA_TRY(cudaMemcpyAsync(s.adv, s.pg, sizeof(float) * B, cudaMemcpyDeviceToDevice, st));
+      adv = s.adv;
+    }
+    if (hp->normalize_adv) TRY(k_normalize(ctx, B, s.adv));
+
+    // ---- loss and its gradient wrt logits / value ----
+    TRY(k_ppo_loss(ctx, B, d.A, s.logits, s.values, s.act, s.blogp, adv, s.vt, lh, s.dlog,
+                   s.dhead, s.stats, s.ver, M->version));
+
+    APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
+
+    // ---- heads backward: dcore + head weight / bias gradients, one launch ----
+    TRY(k_heads_bwd_fused(ctx, B, d.A, s.dlog, s.core, th + d.off_wpi, th + d.off_wv, s.dcore,
+                          s.colsum_part, G + d.off_wpi, G + d.off_bpi, G + d.off_wv, G + d.off_bv));
+  }
 
   // bias gradients of fc / conv layers, fused into the kernels producing /
   // reading their dz (deterministic fixed-point sums, model_kernels.cu)

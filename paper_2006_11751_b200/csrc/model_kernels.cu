@@ -841,8 +841,12 @@ int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core
     APPO_LAUNCH(c, heads_bwd_fused_kernel<kMaxActions>, grid, 512, 0, B, A, dlog, core, wpi, wv,
                 dcore, part, c->d_counter + 7, gwpi, gbpi, gwv, gbv);
   c->next_name = nullptr;
+  return k_heads_grad_reduce(c, A, grid, part, gwpi, gbpi, gwv, gbv);
+}
+int k_heads_grad_reduce(Ctx* c, int A, int nb, const float* part, float* gwpi, float* gbpi,
+                        float* gwv, float* gbv) {
   const int outs = (A + 1) * (kHidden + 1);
-  APPO_LAUNCH(c, heads_grad_reduce_kernel, (outs + 31) / 32, 256, 0, A, grid, part, gwpi, gbpi,
+  APPO_LAUNCH(c, heads_grad_reduce_kernel, (outs + 31) / 32, 256, 0, A, nb, part, gwpi, gbpi,
               gwv, gbv);
   return APPO_OK;
 }

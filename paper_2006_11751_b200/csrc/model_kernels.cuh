@@ -65,6 +65,20 @@ int k_ppo_loss(Ctx* c, int B, int A, const float* logits, const float* values,
 int k_heads_bwd_fused(Ctx* c, int B, int A, const float* dlog, const float* core,
                       const float* wpi, const float* wv, float* dcore, float* part, float* gwpi,
                       float* gbpi, float* gwv, float* gbv);
+// sums nb per-block head-gradient partials (layout of k_heads_bwd_fused) in block order
+int k_heads_grad_reduce(Ctx* c, int A, int nb, const float* part, float* gwpi, float* gbpi,
+                        float* gwv, float* gbv);
+// The loss block fused per trajectory (traj_loss.cu): heads, target logp,
+// V-trace (+ GAE when gae), PPO loss gradient, dcore and the head gradients
+// (+ heads_grad_reduce); stats as k_ppo_loss.  part: n_traj * (A+1) * 513 floats.
+bool traj_loss_supported(int n_traj, int T, int A, bool normalize_adv);
+int k_traj_loss(Ctx* c, int n_traj, int T, int A, const float* core, const float* wpi,
+                const float* bpi, const float* wv, const float* bv, const int32_t* act,
+                const float* rew, const float* blogp, const uint8_t* done, const int64_t* ver,
+                int64_t cur_version, float gamma, float rho_bar, float c_bar, bool gae,
+                float lambda, const LossHP& hp, float* logits, float* values, float* vt, float* pg,
+                float* adv, float* dcore, float* part, double* stats, float* gwpi, float* gbpi,
+                float* gwv, float* gbv);
 int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,
               const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh);
 int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, float* part,

@@ -10,12 +10,11 @@
 // writes the outputs.  HBM-bound: V-trace moves 17 B in + 8 B out per element
 // (16 B more with rho/c outputs).
 #include "appo_common.cuh"
+#include "returns.cuh"
 
 namespace appo_b200 {
 
 namespace {
-
-enum ReturnsMode { kVTrace = 0, kNStep = 1, kGAE = 2 };
 
 struct ReturnsArgs {
   int n_traj, T;
@@ -135,97 +134,59 @@ __global__ void __launch_bounds__(256) returns_kernel(ReturnsArgs a) {
 
 // T <= 32 (the configs' T = 32): lane t owns step t, every input of a
 // trajectory is loaded once into registers (V_{t+1} by shuffle), so a
-// trajectory costs one memory round trip; warps are persistent and load the
-// next trajectory before computing the current one (two round trips in
-// flight per warp).
+// trajectory costs one memory round trip.  Warps are persistent and take
+// kRetU consecutive trajectories per pass, all loaded before any is scanned
+// (kRetU round trips in flight per warp: at 65,536 x 32 two loads per warp
+// left the kernel latency-bound at 0.37 of HBM).
+constexpr int kRetU = 4;
 template <int MODE>
-__global__ void __launch_bounds__(256) returns32_kernel(ReturnsArgs a) {
+__global__ void __launch_bounds__(256, 4) returns32_kernel(ReturnsArgs a) {
   APPO_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int T = a.T;
   const bool on = lane < T;
-  struct In {
-    float r, v, tl, bl, boot;
-    uint8_t d;
-  };
-  auto load = [&](int i, In& x) {
-    const size_t o = (size_t)i * T + lane;
-    x.r = on ? __ldcs(a.r + o) : 0.0f;
-    x.v = (MODE != kNStep && on) ? __ldcs(a.v + o) : 0.0f;
-    x.tl = (MODE == kVTrace && on) ? __ldcs(a.tl + o) : 0.0f;
-    x.bl = (MODE == kVTrace && on) ? __ldcs(a.bl + o) : 0.0f;
-    x.d = on ? a.d[o] : 1;
-    x.boot = __ldg(a.boot + i);
-  };
-  int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  In cur{}, nxt{};
-  if (i < a.n_traj) load(i, cur);
-  for (; i < a.n_traj; i += nw) {
-    if (i + nw < a.n_traj) load(i + nw, nxt);
-    // validation (offpolicy.hpp:70-75): non-finite inputs -> NumericError
-    if (MODE == kVTrace) {
-      const bool bad = __any_sync(0xffffffffu, (lane == 0 && !finitef(cur.boot)) ||
-                                                   (on && (!finitef(cur.r) || !finitef(cur.v) ||
-                                                           !finitef(cur.tl) || !finitef(cur.bl))));
-      if (bad && lane == 0) atomicOr(a.flags + kFlagNumeric, 1);
-    }
-    float vnext = __shfl_down_sync(0xffffffffu, cur.v, 1);
-    if (lane == T - 1) vnext = cur.boot;
-    const float disc = cur.d ? 0.0f : a.gamma;
-    float k = 1.0f, delta = 0.0f, rho = 0.0f, c = 0.0f;
-    if (on) {
-      if (MODE == kVTrace) {
-        const float lr = fminf(fmaxf(cur.tl - cur.bl, -20.0f), 20.0f);  // offpolicy.hpp:50-54
-        const float ratio = expf(lr);
-        rho = fminf(a.rho_bar, ratio);
-        c = fminf(a.c_bar, ratio);
-        delta = rho * (cur.r + disc * vnext - cur.v);
-        k = disc * c;
-      } else if (MODE == kNStep) {
-        delta = cur.r;
-        k = disc;
-      } else {
-        delta = cur.r + disc * vnext - cur.v;
-        k = disc * a.lambda;
-      }
-    }
-    // inclusive right-to-left scan of the affine maps (K, D): a_t = D + K a_T
-    float K = k, D = delta;
+  for (int i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRetU; i0 < a.n_traj;
+       i0 += nw * kRetU) {
+    ReturnsStepIn x[kRetU];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const float Kn = __shfl_down_sync(0xffffffffu, K, off);
-      const float Dn = __shfl_down_sync(0xffffffffu, D, off);
-      if (lane + off < 32) {
-        D = D + K * Dn;
-        K = K * Kn;
-      }
-    }
-    float Kx = __shfl_down_sync(0xffffffffu, K, 1);
-    float Dx = __shfl_down_sync(0xffffffffu, D, 1);
-    if (lane == 31) {
-      Kx = 1.0f;
-      Dx = 0.0f;
-    }
-    const float terminal = (MODE == kNStep) ? cur.boot : 0.0f;
-    const float a_next = Dx + Kx * terminal;  // a_{t+1}
-    const float at = delta + k * a_next;
-    if (on) {
+    for (int u = 0; u < kRetU; ++u) {
+      const int i = i0 + u;
+      const bool ok = on && i < a.n_traj;
       const size_t o = (size_t)i * T + lane;
+      x[u].r = ok ? __ldcs(a.r + o) : 0.0f;
+      x[u].v = (MODE != kNStep && ok) ? __ldcs(a.v + o) : 0.0f;
+      x[u].tl = (MODE == kVTrace && ok) ? __ldcs(a.tl + o) : 0.0f;
+      x[u].bl = (MODE == kVTrace && ok) ? __ldcs(a.bl + o) : 0.0f;
+      x[u].d = ok ? a.d[o] : 1;
+      x[u].boot = i < a.n_traj ? __ldg(a.boot + i) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kRetU; ++u) {
+      const int i = i0 + u;
+      if (i >= a.n_traj) break;  // warp-uniform
+      // validation (offpolicy.hpp:70-75): non-finite inputs -> NumericError
       if (MODE == kVTrace) {
-        const float vnext_corr = (lane + 1 < T) ? (vnext + a_next) : cur.boot;  // v_{t+1}
-        __stcs(a.out0 + o, cur.v + at);
-        __stcs(a.out1 + o, rho * (cur.r + disc * vnext_corr - cur.v));
-        if (a.out2) __stcs(a.out2 + o, rho);
-        if (a.out3) __stcs(a.out3 + o, c);
-      } else if (MODE == kNStep) {
-        __stcs(a.out0 + o, at);
-      } else {
-        __stcs(a.out0 + o, at);
-        if (a.out1) __stcs(a.out1 + o, at + cur.v);
+        const bool bad =
+            __any_sync(0xffffffffu, (lane == 0 && !finitef(x[u].boot)) ||
+                                        (on && (!finitef(x[u].r) || !finitef(x[u].v) ||
+                                                !finitef(x[u].tl) || !finitef(x[u].bl))));
+        if (bad && lane == 0) atomicOr(a.flags + kFlagNumeric, 1);
+      }
+      const ReturnsStepOut y =
+          returns_warp32<MODE>(x[u], lane, T, a.gamma, a.rho_bar, a.c_bar, a.lambda);
+      if (on) {
+        const size_t o = (size_t)i * T + lane;
+        __stcs(a.out0 + o, y.o0);
+        if (MODE == kVTrace) {
+          __stcs(a.out1 + o, y.o1);
+          if (a.out2) __stcs(a.out2 + o, y.rho);
+          if (a.out3) __stcs(a.out3 + o, y.c);
+        } else if (MODE == kGAE) {
+          if (a.out1) __stcs(a.out1 + o, y.o1);
+        }
       }
     }
-    cur = nxt;
   }
 }
 
@@ -239,8 +200,10 @@ int launch_returns(Ctx* c, const ReturnsArgs& a) {
                   : MODE == kNStep ? n * 9 + a.n_traj * 4.0
                                    : n * (13 + (a.out1 ? 8 : 4)) + a.n_traj * 4.0;
   if (a.T <= 32) {
-    // persistent: up to 8 resident blocks of 8 warps per SM
-    const int g32 = grid < c->num_sms * 8 ? grid : c->num_sms * 8;
+    // persistent, kRetU trajectories per warp pass: 4 resident blocks of 8
+    // warps per SM (__launch_bounds__(256, 4): <= 64 registers)
+    const int gu = (a.n_traj + warps_per_block * kRetU - 1) / (warps_per_block * kRetU);
+    const int g32 = gu < c->num_sms * 4 ? gu : c->num_sms * 4;
     APPO_LAUNCH(c, returns32_kernel<MODE>, g32, warps_per_block * 32, 0, a);
     return APPO_OK;
   }

@@ -147,6 +147,7 @@ const void* kanchor_sampler();
 const void* kanchor_conv1();
 const void* kanchor_conv2();
 const void* kanchor_gru_infer();
+const void* kanchor_traj_loss();
 
 // CUDA lazy loading loads a kernel on its first launch, and that load may
 // need a context-wide synchronisation; a consumer spinning on the device for
@@ -177,7 +178,9 @@ int preload_library_kernels() {
     }
   }
   const void* anchors[] = {kanchor_gemm(),      kanchor_gru(),   kanchor_model(),
-                           kanchor_offpolicy(), kanchor_optim(), kanchor_sampler(), kanchor_conv1(), kanchor_conv2(), kanchor_gru_infer(),
+                           kanchor_offpolicy(), kanchor_optim(), kanchor_sampler(),
+                           kanchor_conv1(),     kanchor_conv2(), kanchor_gru_infer(),
+                           kanchor_traj_loss(),
                            reinterpret_cast<const void*>(&slotq_push_kernel)};
   for (const void* a : anchors) {
     cudaFunction_t f = nullptr;

@@ -48,6 +48,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---- 1-D bulk copy global -> shared (no tensor map) --------------------------
+// dst, src 16-byte aligned, bytes a multiple of 16; completes on bar (tx bytes)
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---- TMA store (shared -> global, bulk groups) ------------------------------
 // Whole warp calls; the elected lane issues the store of a 4-D box and commits
 // it as one bulk group.  The smem source must have been written by the warp

@@ -82,7 +82,8 @@ def test_learner_step_other_shapes(oracle, shape):
 
 def test_doom_learner_runs_the_dedicated_kernels():
     """At the bench shape every convolution of the learner step except conv3's
-    runs in the space-to-depth kernels (no silent engine fallback)."""
+    runs in the space-to-depth kernels (no silent engine fallback), and the
+    loss block runs fused per trajectory (traj_loss.cu)."""
     desc = appo.ModelDesc.doom(T=32)
     ctx = appo.Context(0, seed=2, model=desc)
     store = appo.TrajectoryStore(desc, 4)
@@ -94,4 +95,6 @@ def test_doom_learner_runs_the_dedicated_kernels():
     ctx.set_timing(False)
     assert {"conv1_s2d_tcgen05", "conv1_s2d_wgrad_tcgen05", "conv2_s2d_tcgen05",
             "conv2_dgrad_s2d_tcgen05", "conv2_wgrad_s2d_tcgen05", "gru_seq_fwd_kernel",
-            "gru_seq_bwd_kernel"} <= launched, launched
+            "gru_seq_bwd_kernel", "traj_loss_kernel"} <= launched, launched
+    # the fused loss block replaces the four unfused launches
+    assert not {"heads_fwd_kernel", "ppo_loss_kernel", "heads_bwd_fused_kernel"} & launched
