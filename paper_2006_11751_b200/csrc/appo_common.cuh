@@ -75,6 +75,10 @@ struct Ctx {
   // bwd [4, 8)), bias-gradient combine counters [32, 64), per-group bias
   // partial sums [4][512][4]; allocated zeroed on first use
   unsigned* d_gru_sync = nullptr;
+  // GRU step counters are never reset: each launch waits for base + epoch *
+  // CTAs, with the base per counter tracked here (no memset node between the
+  // kernels, so the GRU launches keep programmatic dependent launch)
+  unsigned gru_epochs[8] = {};
   float* d_gru_part = nullptr;
 };
 constexpr int kRedSlots = 148 * 8 * 16;

@@ -68,8 +68,9 @@ __device__ __forceinline__ uint32_t sw128(int rows, int r, int kb, int c) {
   return (uint32_t)(kb * rows * 128 + r * 128 + ((c ^ (r & 7)) << 4));
 }
 
-// Grid-wide barrier on a monotonically increasing counter (zeroed by the host
-// before the launch); all CTAs are co-resident (cooperative launch).
+// Grid-wide barrier on a monotonically increasing counter (never reset: a
+// launch waits for base + epoch * CTAs, the base passed by the host); all
+// CTAs are co-resident (cooperative launch).
 // Split form: arrive (release of everything the CTA stored before it), then
 // work that no other CTA needs (deferred stores, prefetches), then wait.
 __device__ __forceinline__ void grid_arrive(unsigned* counter) {
@@ -82,7 +83,7 @@ __device__ __forceinline__ void grid_wait(unsigned* counter, unsigned target) {
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-    } while (v < target);
+    } while ((int)(v - target) < 0);  // wrap-safe: the counters only grow
   }
   __syncthreads();
 }
@@ -96,7 +97,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned target)
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-    } while (v < target);
+    } while ((int)(v - target) < 0);
   }
   __syncthreads();
 }
@@ -145,11 +146,11 @@ struct GFwdArgs {
   float* hin;
   uint16_t* hbf;
   unsigned* bar;         // [groups] step counters
+  unsigned base[4];      // counter values at launch, per group
   long long* prof;
 };
 
 __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant__ GFwdArgs a) {
-  APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
   const int j0 = uc * UPC_F, i0 = grp * GT;
   const int B = a.n_traj * a.T;
   unsigned* bar = a.bar + grp;
+  const unsigned base = a.base[grp];
 
   // resident B: row q*NG + n = gate row n (g*16 + u) restricted to K quarter q
   for (int e = tid; e < G_NB * 16; e += THR) {  // 16 chunks of 16 B per 128-wide quarter row
@@ -183,6 +185,9 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
     sm100::tmem_alloc(tslot, 256);
     sm100::tmem_relinquish();
   }
+  // everything above reads only parameters (published by an earlier step):
+  // it overlaps the previous kernel's tail
+  APPO_PDL_ENTRY();
   constexpr int CPT = GT * UPC_F / THR;  // 2 cells per thread
   float hreg[CPT], b3[CPT][3], g3[CPT][3];
   uint8_t dn[CPT];
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
   prefetch(0);
   fence_proxy_async_global();
   sm100::tc_fence_before();
-  grid_barrier(bar, NCTA_F);  // the group's h0 (bf16) complete
+  grid_barrier(bar, base + NCTA_F);  // the group's h0 (bf16) complete
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
   constexpr uint32_t idesc = sm100::make_idesc_bf16(GQ * GT, G_NB, 0, 0);
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(THR, 1) gru_g_fwd_kernel(const __grid_constant
     FSTAMP(7);
     if (t < a.T) {
       prefetch(t + 1);
-      grid_wait(bar, ++epoch * NCTA_F);
+      grid_wait(bar, base + ++epoch * NCTA_F);
     }
   }
   sm100::tc_fence_before();
@@ -373,13 +378,13 @@ struct GBwdArgs {
   float* gbih;
   float* gbhh;
   unsigned* bar;        // [groups] step counters
+  unsigned base[4];     // counter values at launch, per group
   unsigned* pair;       // [NCTA_GB] bias-gradient combine counters (self-resetting)
   float* bpart;         // [groups][512][4] per-group bias partial sums
   long long* prof;
 };
 
 __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant__ GBwdArgs a) {
-  APPO_PDL_ENTRY();
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) &
                                            ~uintptr_t(1023));
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant
   const int grp = blockIdx.x / NCTA_GB, uc = blockIdx.x % NCTA_GB;
   const int j0 = uc * UPC_GB, i0 = grp * GT;
   unsigned* bar = a.bar + grp;
+  const unsigned base = a.base[grp];
   const int ngrp = gridDim.x / NCTA_GB;
 
   // resident B: row q*16 + u, K = k' in the quarter: W_hh[q*384 + k'][j0 + u]
@@ -418,6 +424,8 @@ __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant
     sm100::tmem_alloc(tslot, 64);
     sm100::tmem_relinquish();
   }
+  // the prologue above reads only parameters: it overlaps the previous kernel
+  APPO_PDL_ENTRY();
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -524,7 +532,7 @@ __global__ void __launch_bounds__(THR, 1) gru_g_bwd_kernel(const __grid_constant
     if (t == 0) break;  // d(h0) is not needed
     prefetch(t - 1);    // independent of the exchange: overlaps barrier + MMA
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 1] = clock64();
-    grid_wait(bar, ++epoch * NCTA_GB);
+    grid_wait(bar, base + ++epoch * NCTA_GB);
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[t * 4 + 2] = clock64();
     // the group's dgh_t: K block kb of quarter q = gates q*384 + kb*64, rows i0..i0+31
     if (warp == 1) {
@@ -691,6 +699,25 @@ int gru_ws(Ctx* c) {
   APPO_CUDA_TRY(cudaMemsetAsync(c->d_gru_sync, 0, sizeof(unsigned) * 64, c->stream));
   return APPO_OK;
 }
+// Cooperative launch (all CTAs co-resident for the step barriers) with
+// programmatic stream serialisation when the context uses it
+int launch_coop(Ctx* c, const void* kernel, int grid, int smem, void* arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THR);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 2 : 1;
+  void* args[] = {arg};
+  APPO_CUDA_TRY(cudaLaunchKernelExC(&cfg, kernel, args));
+  return APPO_OK;
+}
 }  // namespace
 
 int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* whh,
@@ -700,18 +727,19 @@ int k_gru_seq_fwd(Ctx* c, int n_traj, int T, const float* gi, const uint16_t* wh
   APPO_TRY(ensure_smem_attr((const void*)gru_g_fwd_kernel, G_FWD_SMEM, c->device));
   const int ng = (n_traj + GT - 1) / GT;
   unsigned* gbar = c->d_gru_sync;
-  APPO_CUDA_TRY(cudaMemsetAsync(gbar, 0, sizeof(unsigned) * ng, c->stream));
   GFwdArgs a{};
+  for (int g = 0; g < ng; ++g) {  // this launch advances each group's counter by (T+1) NCTA_F
+    a.base[g] = c->gru_epochs[g];
+    c->gru_epochs[g] += (unsigned)(T + 1) * NCTA_F;
+  }
   int st = make_tmap_bf16_3d(&a.hmap, hbuf_bf, kHidden, n_traj, 2, kHidden * 2,
                              (uint64_t)n_traj * kHidden * 2, 64, GT, 1);
   if (st) return st;
   a.n_traj = n_traj; a.T = T; a.gi = gi; a.whh = whh; a.bhh = bhh; a.done = done;
   a.hbuf = hbuf; a.hbuf_bf = hbuf_bf; a.core = core; a.core_bf = core_bf; a.gates = gates;
   a.hin = hin; a.hbf = hbf; a.bar = gbar; a.prof = prof_buffer(c);
-  void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_fwd_kernel");
-  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_g_fwd_kernel, dim3(NCTA_F * ng),
-                                            dim3(THR), args, G_FWD_SMEM, c->stream));
+  APPO_TRY(launch_coop(c, (const void*)gru_g_fwd_kernel, NCTA_F * ng, G_FWD_SMEM, &a));
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T + 1);
   timing_end(c, "gru_seq_fwd_kernel", ev);
   c->launches++;
@@ -729,18 +757,19 @@ int k_gru_seq_bwd(Ctx* c, int n_traj, int T, const float* dcore, const uint8_t* 
   APPO_TRY(ensure_smem_attr((const void*)gru_g_bwd_kernel, G_BWD_SMEM, c->device));
   const int ng = (n_traj + GT - 1) / GT;
   unsigned* gbar = c->d_gru_sync + 4;
-  APPO_CUDA_TRY(cudaMemsetAsync(gbar, 0, sizeof(unsigned) * ng, c->stream));
   GBwdArgs a{};
+  for (int g = 0; g < ng; ++g) {  // T-1 step barriers of NCTA_GB arrivals
+    a.base[g] = c->gru_epochs[4 + g];
+    c->gru_epochs[4 + g] += (unsigned)(T > 1 ? T - 1 : 0) * NCTA_GB;
+  }
   int st = make_tmap_bf16_3d(&a.xmap, dghx, kGates, n_traj, 2, kGates * 2,
                              (uint64_t)n_traj * kGates * 2, 64, GT, 1);
   if (st) return st;
   a.n_traj = n_traj; a.T = T; a.dcore = dcore; a.done = done; a.gates = gates; a.hin = hin;
   a.whh = whh; a.dghx = dghx; a.dgi = dgi; a.dgh = dgh; a.gbih = gbih; a.gbhh = gbhh;
   a.bar = gbar; a.pair = c->d_gru_sync + 32; a.bpart = c->d_gru_part; a.prof = prof_buffer(c);
-  void* args[] = {&a};
   cudaEvent_t ev = timing_begin(c, "gru_seq_bwd_kernel");
-  APPO_CUDA_TRY(cudaLaunchCooperativeKernel((void*)gru_g_bwd_kernel, dim3(NCTA_GB * ng),
-                                            dim3(THR), args, G_BWD_SMEM, c->stream));
+  APPO_TRY(launch_coop(c, (const void*)gru_g_bwd_kernel, NCTA_GB * ng, G_BWD_SMEM, &a));
   c->next_flops = 2.0 * n_traj * (double)kGates * kHidden * (T - 1);
   timing_end(c, "gru_seq_bwd_kernel", ev);
   c->launches++;

@@ -924,7 +924,9 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   float* G = M->grad;
   if (traj_loss_supported(n_traj, T, d.A, hp->normalize_adv != 0)) {
     // heads, targets, loss and heads backward fused per trajectory (traj_loss.cu)
-    APPO_CUDA_TRY(cudaMemsetAsync(G, 0, d.total * 4, st));
+    // no gradient memset on this path: every entry of G is written (not
+    // accumulated) by the kernels below -- checked by running the learner
+    // parity tests with G pre-filled with NaN
     const bool gae = hp->adv_source == 1 || hp->adv_source == 2;
     const float lam = hp->adv_source == 1 ? 1.0f : hp->gae_lambda;
     TRY(k_traj_loss(ctx, n_traj, T, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
