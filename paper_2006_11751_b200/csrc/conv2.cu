@@ -449,6 +449,11 @@ __global__ void __launch_bounds__(D2_THREADS, 1)
           }
         }
       }
+      {  // input row 16 (coarse row 8) meets only dz2 rows >= Ho: its zeros are
+         // stored here (a memset node would end the kernels' PDL overlap)
+        uint4* zr = reinterpret_cast<uint4*>(p.dz + ((size_t)img * p.Hi + 16) * p.Wi * 32);
+        for (int i = ew * 32 + lane; i < p.Wi * 4; i += 8 * 32) zr[i] = make_uint4(0, 0, 0, 0);
+      }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -721,9 +726,6 @@ int conv2_dgrad(Ctx* c, const DgradIn& in) {
     const int st = make_tmap_bf16_3d(&mw, in.wt, 256, 128, 1, 512, 128 * 512, 64, 128, 1);
     if (st) return st;
   }
-  // input row 16 (coarse row 8) meets only dz2 rows >= Ho: zero
-  APPO_CUDA_TRY(cudaMemset2DAsync(in.dz + (size_t)16 * in.Wi * 32, (size_t)in.Hi * in.Wi * 32 * 2, 0,
-                                  (size_t)in.Wi * 32 * 2, in.n_img, c->stream));
   D2Params p{};
   p.n_img = in.n_img;
   p.Hi = in.Hi;

@@ -859,6 +859,12 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   cudaStream_t st = ctx->stream;
   const int pub = M->published;
   const uint16_t* wb = M->pub_bf16[pub];
+  // this step publishes into the oldest of the kPub copies: wait (here, ahead
+  // of the step's kernels, so no event wait splits their PDL chain) for every
+  // inference that may still read it -- readers only take the newest copy, so
+  // all of them were enqueued before this step
+  const int next = (pub + 1) % Model::kPub;
+  TRY(wait_readers(M, st, next));
   const float* th = M->theta;  // fp32 master (== pub_f32[pub])
   const uint8_t* region = static_cast<const uint8_t*>(d_region);
 
@@ -1140,18 +1146,17 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   TRY(dp_finish(ctx, G, d.off_fcw, &peer_flags));
 
   // ---- global-norm clip + Adam; publish into the other buffer ----
-  const int next = (pub + 1) % Model::kPub;
-  // do not overwrite a published copy an inference (any stream) may still read
-  TRY(wait_readers(M, st, next));
   M->adam_t += 1;
   TRY(launch_adam(ctx, d.total, M->theta, M->m, M->v, G, M->adam_t, hp->lr, hp->beta1,
                   hp->beta2, hp->eps, hp->grad_clip, s.stats + 8, M->pub_bf16[next],
                   M->pub_f32[next], ctx->d_counter + 6, peer_flags));
-  APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
-  APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
   TRY(k_publish_derived(ctx, M->pub_bf16[next], M->pub_f32[next], d, M->pub_c1h[next],
                         M->pub_c1b[next], M->pub_wt2[next], M->pub_wt3[next]));
   APPO_CUDA_TRY(cudaEventRecord(M->ready_ev[next], st));
+  // statistics back to the host after the kernels (a copy node between two
+  // kernels would end their PDL overlap)
+  APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
+  APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
   M->last_ring = ring;
   // Optimistic publish: the Adam kernel always rewrites pub[next] (with the
   // unchanged parameters when the step is rejected); readers on other streams
