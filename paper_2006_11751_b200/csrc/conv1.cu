@@ -210,8 +210,6 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
     sm100::tmem_alloc(tmem_slot, C1_NACC * 64);
     sm100::tmem_relinquish();
   }
-  APPO_PDL_ENTRY();  // the weights / images come from earlier kernels
-
   // B operand of row tap a: row n = (output channel co = n >> 1, column tap
   // b = n & 1), chunk kc = 2c + h holds 8 fp16 W[co][c][4a + 2h + ii][4b + j]
   // (ii = 0, 1; j = 0..3), the same (ii, j) order as the A chunks
@@ -225,6 +223,9 @@ __global__ void __launch_bounds__(C1_THREADS, 1)
     *reinterpret_cast<uint4*>(bsm + tau * 4096 + co * 128 + ((kc ^ (co & 7)) << 4)) =
         make_uint4(lo.x, lo.y, hi.x, hi.y);
   }
+  // the weights are a published copy (an earlier step): staged before the wait,
+  // overlapping the previous kernel; the images come from earlier kernels
+  APPO_PDL_ENTRY();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   sm100::tc_fence_before();
   __syncthreads();

@@ -125,6 +125,16 @@ __global__ void __launch_bounds__(C2_THREADS, 1)
     }
     sm100::fence_barrier_init();
   }
+  if (warp == 0) {
+    // B block (a, e): row n = 2co + b holds W2[co][2a+e][2b .. 2b+1][0..31]
+    // (128 B): one box {64, 2 (b), 1 (kh), 64 (co)} of the weights per block.
+    // A published copy (an earlier step): loaded before the PDL wait.
+    __syncwarp();
+    sm100::mbar_arrive_expect_tx_warp(bfull, C2_BBYTES);
+#pragma unroll
+    for (int blk = 0; blk < 4; ++blk)
+      sm100::tma_load_4d_warp(bsm + blk * 16384, &map_w, bfull, 0, 0, blk, 0);
+  }
   if (warp == 1) {
     sm100::tmem_alloc(tmem_slot, C2_NACC * 128);
     sm100::tmem_relinquish();
@@ -141,12 +151,6 @@ __global__ void __launch_bounds__(C2_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // B block (a, e): row n = 2co + b holds W2[co][2a+e][2b .. 2b+1][0..31]
-    // (128 B): one box {64, 2 (b), 1 (kh), 64 (co)} of the weights per block
-    sm100::mbar_arrive_expect_tx_warp(bfull, C2_BBYTES);
-#pragma unroll
-    for (int blk = 0; blk < 4; ++blk)
-      sm100::tma_load_4d_warp(bsm + blk * 16384, &map_w, bfull, 0, 0, blk, 0);
     // ---- TMA: even rows (coordinate 0) and odd rows (1), element stride 2 ----
     int j = 0;
     for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
@@ -332,6 +336,15 @@ __global__ void __launch_bounds__(D2_THREADS, 1)
     }
     sm100::fence_barrier_init();
   }
+  if (warp == 0) {
+    // resident B by TMA: wt rows (class, ci) x K (tap, co), one SW128 box per
+    // tap; derived from a published copy (an earlier step): before the PDL wait
+    __syncwarp();
+    sm100::mbar_arrive_expect_tx_warp(bfull, D2_BBYTES);
+#pragma unroll
+    for (int tap = 0; tap < 4; ++tap)
+      sm100::tma_load_3d_warp(bsm + tap * 16384, &map_wt, bfull, tap * 64, 0, 0);
+  }
   if (warp == 1) {
     sm100::tmem_alloc(tmem_slot, 256);
     sm100::tmem_relinquish();
@@ -347,11 +360,6 @@ __global__ void __launch_bounds__(D2_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // resident B by TMA: wt rows (class, ci) x K (tap, co), one SW128 box per tap
-    sm100::mbar_arrive_expect_tx_warp(bfull, D2_BBYTES);
-#pragma unroll
-    for (int tap = 0; tap < 4; ++tap)
-      sm100::tma_load_3d_warp(bsm + tap * 16384, &map_wt, bfull, tap * 64, 0, 0);
     int j = 0;
     for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, ++j) {
       const int s = j % D2_NSTG;
