@@ -104,14 +104,47 @@ __global__ void __launch_bounds__(256)
   }
   if (applied && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(applied, 1u);
   const float scale = (float)norm_in[1];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+  auto upd = [&](float th, float& mi, float& vi, float gr) {
+    const float gi = gr * scale;
+    mi = b1 * mi + (1.0f - b1) * gi;
+    vi = b2 * vi + (1.0f - b2) * gi * gi;
+    return th - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  };
+  // float4 body (16-byte aligned vectors, 8-byte aligned bf16 copy), scalar tail
+  const bool vec = ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(theta) |
+                     reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v) |
+                     reinterpret_cast<uintptr_t>(f32)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(bf16) & 7) == 0;
+  const int64_t n4 = vec ? (n >> 2) : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i] * scale;
-    const float mi = b1 * m[i] + (1.0f - b1) * gi;
-    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 th = reinterpret_cast<float4*>(theta)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    th.x = upd(th.x, mm.x, vv.x, gg.x);
+    th.y = upd(th.y, mm.y, vv.y, gg.y);
+    th.z = upd(th.z, mm.z, vv.z, gg.z);
+    th.w = upd(th.w, mm.w, vv.w, gg.w);
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    reinterpret_cast<float4*>(theta)[i] = th;
+    if (bf16) {
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(th.x, th.y);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(th.z, th.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(bf16)[i] = pk;
+    }
+    if (f32) reinterpret_cast<float4*>(f32)[i] = th;
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float mi = m[i], vi = v[i];
+    const float th = upd(theta[i], mi, vi, g[i]);
     m[i] = mi;
     v[i] = vi;
-    const float th = theta[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
     theta[i] = th;
     if (bf16) bf16[i] = __float2bfloat16_rn(th);
     if (f32) f32[i] = th;
@@ -133,7 +166,8 @@ int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float
               c->d_flags, peer_flags);
   const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
   const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
-  const int grid2 = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  const int64_t nv = (n + 3) / 4;  // float4 groups (the kernel falls back to scalars if unaligned)
+  const int grid2 = (int)((nv + 255) / 256 < 148 * 16 ? (nv + 255) / 256 : 148 * 16);
   c->next_bytes = (double)n * (4 + 24 + (bf16_copy ? 2 : 0) + (f32_copy ? 4 : 0));
   APPO_LAUNCH(c, adam_kernel, grid2, 256, 0, n, theta, m, v, g, d_norm_out, lr, b1, b2, eps, bc1,
               bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags, applied);
