@@ -17,4 +17,6 @@ timeout -s KILL 900 ncu --profile-from-start off --metrics sm__pipe_tensor_cycle
 KREGEX="conv1_s2d_kernel" NAME=final_conv1 SKIP=2 COUNT=1 bash scripts/gpu_ncu_kernel.sh
 ENVS=2048 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:gru_g_ -s 4 -c 2 -o gpurun_out/final_gru python scripts/profile_step.py > gpurun_out/final_ncu_gru.log 2>&1; echo "ncu gru rc=$?"
 APPO_GRU_PROF=1 timeout -s KILL 120 python scripts/_prof_gru.py 2>&1 | grep "gru prof" > gpurun_out/final_gru_phases.txt
+KREGEX="traj_loss_kernel" NAME=final_traj_loss SKIP=2 COUNT=1 bash scripts/gpu_ncu_kernel.sh
+timeout -s KILL 300 python scripts/hbm_sweep.py > gpurun_out/final_hbm_sweep.jsonl 2>&1; echo "hbm sweep rc=$?"
 ls -la gpurun_out | head -40

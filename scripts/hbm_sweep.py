@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 import paper_2006_11751_b200 as appo  # noqa: E402
 
 L2 = 126 << 20
-RET = "returns32_kernel<MODE>"  # T <= 32 path (offpolicy.cu)
+RET = "returns32v_kernel<MODE>|returns32_kernel<MODE>"  # T = 32 paths (offpolicy.cu)
 QUICK = "--quick" in sys.argv
 REPS = 3 if QUICK else 20
 
