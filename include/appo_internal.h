@@ -34,6 +34,23 @@ APPO_API int appo_dbg_ppo_loss(appo_ctx* ctx, int B, int A, const float* d_logit
                                float clip_low, float clip_high, float value_coef,
                                float entropy_coef, float* d_dlog, double* h_stats8);
 
+/* The learner's fused per-trajectory loss block (traj_loss_kernel) on injected
+ * core rows d_core [B + n_traj][512] (steps s = i*T + t, then the bootstrap
+ * rows) and head weights: logits [B + n_traj][A], values [B + n_traj], V-trace
+ * targets / pg advantages [B], GAE advantages [B] (adv_source 1, 2), dcore
+ * [B][512], head gradients d_ghead = {W_pi [A][512], b_pi [A], w_v [512],
+ * b_v} (the parameter layout), h_stats8 as appo_dbg_ppo_loss; versions 0,
+ * current version 0.  T <= 32, A <= 7, n_traj <= 320. */
+APPO_API int appo_dbg_traj_loss(appo_ctx* ctx, int n_traj, int T, int A, const float* d_core,
+                                const float* d_wpi, const float* d_bpi, const float* d_wv,
+                                const float* d_bv, const int32_t* d_actions,
+                                const float* d_rewards, const float* d_blogp,
+                                const uint8_t* d_dones, float gamma, float rho_bar,
+                                float c_bar, int adv_source, float gae_lambda, float clip_low,
+                                float clip_high, float value_coef, float entropy_coef,
+                                float* d_logits, float* d_values, float* d_vt, float* d_pg,
+                                float* d_adv, float* d_dcore, float* d_ghead, double* h_stats8);
+
 /* Synchronous device->host copy on the ctx stream (test plumbing). */
 APPO_API int appo_dbg_copy_d2h(appo_ctx* ctx, void* h_dst, const void* d_src, uint64_t bytes);
 

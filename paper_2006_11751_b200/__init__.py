@@ -193,6 +193,8 @@ _sig("appo_dbg_model_ptrs", _i, _vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_
 _sig("appo_dbg_copy_d2h", _i, _vp, _vp, _vp, _u64)
 _sig("appo_dbg_ppo_loss", _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _f, _f, _f, _f, _vp,
      _vp)
+_sig("appo_dbg_traj_loss", _i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f,
+     _f, _f, _i, _f, _f, _f, _f, _f, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp)
 _sig("appo_learner_submit", _i, _vp, _vp, _u64, _vp, _i, C.POINTER(HParams))
 _sig("appo_learner_collect", _i, _vp, C.POINTER(StepOut))
 _sig("appo_dp_unique_id", _i, C.c_char_p)
@@ -575,6 +577,31 @@ class Context:
                                    value_coef, entropy_coef, _ptr(dlog),
                                    stats.ctypes.data_as(C.c_void_p)))
         return dlog, stats
+
+    def traj_loss_injected(self, T, core, wpi, bpi, wv, bv, actions, rewards, blogp, dones,
+                           gamma=0.99, rho_bar=1.0, c_bar=1.0, adv_source=0, gae_lambda=0.95,
+                           clip_low=1 / 1.1, clip_high=1.1, value_coef=0.5, entropy_coef=0.003):
+        """The learner's fused per-trajectory loss block (traj_loss_kernel) on injected
+        core rows [B + n_traj][512] and head weights (include/appo_internal.h)."""
+        _need_cuda(core, wpi, bpi, wv, bv, actions, rewards, blogp, dones)
+        import torch
+        R = core.shape[0]
+        n = R // (T + 1)
+        B = n * T
+        A = wpi.shape[0]
+        f = lambda *shape: torch.empty(*shape, dtype=torch.float32, device=core.device)
+        out = dict(logits=f(R, A), values=f(R), vt=f(B), pg=f(B), adv=f(B), dcore=f(B, 512),
+                   ghead=f(A * 512 + A + 512 + 1))
+        stats = np.zeros(8)
+        check(_L.appo_dbg_traj_loss(self.h, n, T, A, _ptr(core), _ptr(wpi), _ptr(bpi), _ptr(wv),
+                                    _ptr(bv), _ptr(actions), _ptr(rewards), _ptr(blogp),
+                                    _ptr(dones), gamma, rho_bar, c_bar, adv_source, gae_lambda,
+                                    clip_low, clip_high, value_coef, entropy_coef,
+                                    _ptr(out["logits"]), _ptr(out["values"]), _ptr(out["vt"]),
+                                    _ptr(out["pg"]), _ptr(out["adv"]), _ptr(out["dcore"]),
+                                    _ptr(out["ghead"]), stats.ctypes.data_as(C.c_void_p)))
+        out["stats"] = stats
+        return out
 
     def gemm(self, M, N, K, a, lda, a_mn, b, ldb, b_mn, out, ldo, flags=0, scale=1.0, bias=None,
              aux=None, ld_aux=0, bn=128, splits=1):

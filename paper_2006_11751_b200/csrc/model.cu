@@ -1248,6 +1248,45 @@ extern "C" int appo_dbg_copy_d2h(appo_ctx* ctx, void* h_dst, const void* d_src, 
 // The learner's fused loss kernel (ppo_loss_kernel) on caller-supplied logits /
 // values: parity of the loss and its logit / value gradient against the
 // reference's compute_gradients (policy.hpp:323-375) with injected inputs.
+extern "C" int appo_dbg_traj_loss(appo_ctx* ctx, int n_traj, int T, int A, const float* d_core,
+                                  const float* d_wpi, const float* d_bpi, const float* d_wv,
+                                  const float* d_bv, const int32_t* d_actions,
+                                  const float* d_rewards, const float* d_blogp,
+                                  const uint8_t* d_dones, float gamma, float rho_bar,
+                                  float c_bar, int adv_source, float gae_lambda, float clip_low,
+                                  float clip_high, float value_coef, float entropy_coef,
+                                  float* d_logits, float* d_values, float* d_vt, float* d_pg,
+                                  float* d_adv, float* d_dcore, float* d_ghead, double* h_stats8) {
+  APPO_REQUIRE(ctx != nullptr && traj_loss_supported(n_traj, T, A, false), APPO_ERR_CONTRACT,
+               "dbg_traj_loss: outside the fused kernel's envelope");
+  APPO_CUDA_TRY(cudaSetDevice(ctx->device));
+  const int B = n_traj * T;
+  double* stats = nullptr;
+  int64_t* ver = nullptr;
+  float* part = nullptr;
+  APPO_CUDA_TRY(cudaMalloc(&stats, sizeof(double) * 16));
+  APPO_CUDA_TRY(cudaMalloc(&ver, sizeof(int64_t) * B));
+  APPO_CUDA_TRY(cudaMalloc(&part, sizeof(float) * n_traj * (A + 1) * (kHidden + 1)));
+  APPO_CUDA_TRY(cudaMemsetAsync(ver, 0, sizeof(int64_t) * B, ctx->stream));
+  LossHP lh{clip_low, clip_high, value_coef, entropy_coef};
+  const bool gae = adv_source == 1 || adv_source == 2;
+  const float lam = adv_source == 1 ? 1.0f : gae_lambda;
+  float* g = d_ghead;  // W_pi [A][512], b_pi [A], w_v [512], b_v
+  int st = k_traj_loss(ctx, n_traj, T, A, d_core, d_wpi, d_bpi, d_wv, d_bv, d_actions, d_rewards,
+                       d_blogp, d_dones, ver, 0, gamma, rho_bar, c_bar, gae, lam, lh, d_logits,
+                       d_values, d_vt, d_pg, d_adv, d_dcore, part, stats, g, g + A * kHidden,
+                       g + A * kHidden + A, g + A * kHidden + A + kHidden);
+  if (st == APPO_OK) {
+    APPO_CUDA_TRY(cudaMemcpyAsync(h_stats8, stats, sizeof(double) * 8, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(stats);
+  cudaFree(ver);
+  cudaFree(part);
+  return st;
+}
+
 extern "C" int appo_dbg_ppo_loss(appo_ctx* ctx, int B, int A, const float* d_logits,
                                  const float* d_values, const int32_t* d_actions,
                                  const float* d_blogp, const float* d_adv, const float* d_vt,
