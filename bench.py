@@ -37,7 +37,8 @@ sys.path.insert(0, ROOT)
 METRIC = "env frames/sec (inference + V-trace/PPO learn) per GPU and at 2/4/8 B200"
 
 
-TIMING_STRIDE = 13  # prime: no aliasing with the 29-launch learner step / 9-launch sampler step
+# prime: no aliasing with the 26-launch learner step / 9-launch sampler step
+TIMING_STRIDE = int(os.environ.get("APPO_BENCH_TIMING_STRIDE", "13"))
 
 
 def parse():
