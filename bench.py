@@ -275,7 +275,7 @@ def run_ours(args, ws, rank, local):
     seed = 1 if args.mode == "dp" else 1 + rank
     # learner on a high-priority stream (its GRU phases are latency-bound and
     # use few SMs); the sampler fills the rest of the GPU at low priority
-    hi = torch.cuda.Stream(local, priority=-1)
+    hi = torch.cuda.Stream(local, priority=int(os.environ.get("APPO_BENCH_LEARNER_PRIO", "-1")))
     torch.cuda.set_stream(hi)
     lctx = appo.Context(local, seed=seed, model=desc, stream=hi)    # learner
     if args.no_overlap:

@@ -108,6 +108,11 @@ APPO_API int appo_ctx_set_sm_budget(appo_ctx* ctx, int n_sms);
  * (samplers running next to a learner); env APPO_PDL=0/1/B/S overrides
  * (none / all / owners only / shared only). */
 APPO_API int appo_ctx_set_pdl(appo_ctx* ctx, int enable);
+/* Learner backward on two streams: the weight-gradient kernels run on a side
+ * stream beside the input-gradient chain (bit-identical results, joined
+ * before the optimizer).  Default on; env APPO_LEARNER_FORK=0 turns the
+ * default off. */
+APPO_API int appo_ctx_set_learner_fork(appo_ctx* ctx, int enable);
 APPO_API int appo_ctx_sync(appo_ctx* ctx);
 /* Number of launches of this library's kernels enqueued on ctx so far. */
 APPO_API int64_t appo_ctx_launch_count(appo_ctx* ctx);

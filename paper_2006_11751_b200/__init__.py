@@ -160,6 +160,7 @@ _sig("appo_ctx_destroy", _i, _vp)
 _sig("appo_ctx_create_shared", _i, _vp, C.POINTER(_vp))
 _sig("appo_ctx_set_sm_budget", _i, _vp, _i)
 _sig("appo_ctx_set_pdl", _i, _vp, _i)
+_sig("appo_ctx_set_learner_fork", _i, _vp, _i)
 _sig("appo_ctx_set_stream", _i, _vp, _vp)
 _sig("appo_ctx_sync", _i, _vp)
 _sig("appo_ctx_launch_count", _i64, _vp)
@@ -302,6 +303,10 @@ class Context:
     def set_pdl(self, enable: bool):
         """Programmatic dependent launch of this context's kernels."""
         check(_L.appo_ctx_set_pdl(self.h, int(enable)))
+
+    def set_learner_fork(self, enable: bool):
+        """Learner backward on two streams (weight gradients on a side stream)."""
+        check(_L.appo_ctx_set_learner_fork(self.h, int(enable)))
 
     def close(self):
         if getattr(self, "h", None):

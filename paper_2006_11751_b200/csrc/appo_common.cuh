@@ -80,6 +80,16 @@ struct Ctx {
   // kernels, so the GRU launches keep programmatic dependent launch)
   unsigned gru_epochs[8] = {};
   float* d_gru_part = nullptr;
+  // learner side stream (model.cu): weight-gradient kernels of the backward
+  // run here beside the input-gradient chain on `stream`, with their own
+  // split-K workspace; fork/join by events
+  bool fork = true;  // appo_ctx_set_learner_fork
+  cudaStream_t side_stream = nullptr;
+  static constexpr int kSideEvents = 16;
+  cudaEvent_t side_ev[kSideEvents] = {};
+  unsigned side_ev_next = 0;
+  float* side_ws = nullptr;
+  size_t side_ws_bytes = 0;
 };
 constexpr int kRedSlots = 148 * 8 * 16;
 
@@ -127,6 +137,12 @@ inline bool pdl_default(bool shared) {
   if (e[0] == 'B') return !shared;
   if (e[0] == 'S') return shared;
   return false;
+}
+// learner backward on two streams (model.cu); APPO_LEARNER_FORK=0 turns the
+// default off
+inline bool learner_fork_default() {
+  const char* v = getenv("APPO_LEARNER_FORK");
+  return !(v && v[0] == '0');
 }
 }  // namespace appo_b200
 #define APPO_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")

@@ -91,6 +91,7 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (c->num_sms <= 0) c->num_sms = 148;
   c->pdl = pdl_default(false);
+  c->fork = learner_fork_default();
   if (cudaMalloc(&c->d_flags, sizeof(int) * kNumFlags) != cudaSuccess ||
       cudaMalloc(&c->d_red, sizeof(double) * kRedSlots) != cudaSuccess ||
       cudaMalloc(&c->d_counter, sizeof(unsigned) * 16) != cudaSuccess ||
@@ -112,6 +113,12 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
     }
   }
   *out = c;
+  return APPO_OK;
+}
+
+int appo_ctx_set_learner_fork(appo_ctx* ctx, int enable) {
+  CTX_OR_RETURN(ctx);
+  ctx->fork = enable != 0;
   return APPO_OK;
 }
 
@@ -148,6 +155,13 @@ int appo_ctx_destroy(appo_ctx* ctx) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
   }
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+  }
+  for (auto e : ctx->side_ev)
+    if (e) cudaEventDestroy(e);
+  cudaFree(ctx->side_ws);
   cudaFree(ctx->d_gru_sync);
   cudaFree(ctx->d_gru_part);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);

@@ -1300,24 +1300,25 @@ __global__ void __launch_bounds__(kernel_threads<EV, AG>(), 1)
 }
 
 // Split-K reduction + epilogue (fp32 outputs only).  Block = 32 consecutive
-// outputs x 8 split groups: group g sums splits z = g, g+8, ... in order, then
-// the 8 group sums are added in order -- deterministic, and enough threads in
-// flight for the partial stream even when M*N is small and splits is large.
-__global__ void __launch_bounds__(256)
+// outputs x G split groups (G = 8 or 32 warps): group g sums splits z = g,
+// g+G, ... in order, then the G group sums are added in order --
+// deterministic, and enough loads in flight for the partial stream even when
+// M*N is small and splits is large (G = 32 when the grid fits one wave: the
+// conv1 weight gradient's 6,144 outputs x 148 splits take 2 load rounds per
+// warp instead of 5).
+template <int G>
+__global__ void __launch_bounds__(G * 32)
     splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ partial, Epilogue e) {
   APPO_PDL_ENTRY();
-  // lane = 4 consecutive outputs (16-byte loads, 512 B per warp and split),
-  // warp g = splits g, g+8, ... with 4 loads in flight; the 8 warp sums are
-  // then added in warp order (deterministic)
   const int64_t total = (int64_t)M * N;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t i = ((int64_t)blockIdx.x * 32 + lane) * 4;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (i < total) {
     const float4* p = reinterpret_cast<const float4*>(partial + (size_t)g * total + i);
-    const size_t step = (size_t)2 * total;  // 8 splits, in float4 units
+    const size_t step = (size_t)G * total / 4;  // G splits, in float4 units
     int z = g;
-    for (; z + 24 < splits; z += 32, p += 4 * step) {
+    for (; z + 3 * G < splits; z += 4 * G, p += 4 * step) {
       const float4 a0 = __ldg(p), a1 = __ldg(p + step), a2 = __ldg(p + 2 * step),
                    a3 = __ldg(p + 3 * step);
       s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
@@ -1325,18 +1326,18 @@ __global__ void __launch_bounds__(256)
       s.x += a2.x; s.y += a2.y; s.z += a2.z; s.w += a2.w;
       s.x += a3.x; s.y += a3.y; s.z += a3.z; s.w += a3.w;
     }
-    for (; z < splits; z += 8, p += step) {
+    for (; z < splits; z += G, p += step) {
       const float4 a0 = __ldg(p);
       s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
     }
   }
-  __shared__ float4 sh[8][32];
+  __shared__ float4 sh[G][32];
   sh[g][lane] = s;
   __syncthreads();
   if (g != 0 || i >= total) return;
   float4 t = sh[0][lane];
-#pragma unroll
-  for (int k = 1; k < 8; ++k) {
+#pragma unroll 8
+  for (int k = 1; k < G; ++k) {
     const float4 u = sh[k][lane];
     t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
   }
@@ -1408,8 +1409,11 @@ int launch_splitk_reduce(Ctx* c, int M, int N, int splits, const float* partial,
     APPO_LAUNCH(c, splitk_reduce4_kernel, (int)((total / 4 + 255) / 256), 256, 0, M, N, splits,
                 partial, epi);
   } else {
-    APPO_LAUNCH(c, splitk_reduce_kernel, (int)((total / 4 + 31) / 32), 256, 0, M, N, splits,
-                partial, epi);
+    const int grid = (int)((total / 4 + 31) / 32);
+    if ((int64_t)grid * 1024 <= (int64_t)c->num_sms * 2048)
+      APPO_LAUNCH(c, splitk_reduce_kernel<32>, grid, 1024, 0, M, N, splits, partial, epi);
+    else
+      APPO_LAUNCH(c, splitk_reduce_kernel<8>, grid, 256, 0, M, N, splits, partial, epi);
   }
   return APPO_OK;
 }
@@ -1625,7 +1629,7 @@ int dispatch_major(Ctx* c, bool amn, bool bmn, const CUtensorMap& ma, const CUte
 }  // namespace
 
 // module anchor for preload_library_kernels (slotq.cu)
-const void* kanchor_gemm() { return reinterpret_cast<const void*>(&splitk_reduce_kernel); }
+const void* kanchor_gemm() { return reinterpret_cast<const void*>(&splitk_reduce_kernel<8>); }
 
 int gemm_workspace(Ctx* c, size_t bytes, float** out) {
   if (bytes > c->ws_bytes) {

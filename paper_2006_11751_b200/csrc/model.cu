@@ -829,6 +829,62 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
 // h_slot_ids != null: ids from the host (FIFO order given by the caller);
 // else ids popped on the device from rq (FIFO arrival order) and, when fq is
 // set, returned to fq after the last kernel reading the slots.
+// ---- learner side stream ----
+// The backward's weight-gradient kernels (dW_ih, dW_hh, FC, conv3, conv2)
+// depend on the input-gradient chain (dx -> FC dgrad -> conv3 dgrad -> conv2
+// dgrad -> conv1 wgrad) but nothing in the chain depends on them, so they run
+// on a side stream as soon as their inputs exist and fill the SMs the chain's
+// kernels leave idle; the main stream joins before the optimizer.  Every
+// kernel writes disjoint outputs (bias sums have their own counters), the side
+// stream has its own split-K workspace, so the results are bit-identical to
+// the serial order.  appo_ctx_set_learner_fork(ctx, 0) (or the env default
+// APPO_LEARNER_FORK=0) keeps everything on one stream.
+
+static int side_init(Ctx* c) {
+  if (c->side_stream) return APPO_OK;
+  // the main stream's priority (measured: one step below it lets the
+  // concurrently running sampler delay the weight gradients the join waits
+  // for, 12.26 -> 11.98 M frames/s); APPO_SIDE_PRIO=+/- one step below/above
+  int prio = 0, least = 0, greatest = 0;
+  APPO_CUDA_TRY(cudaStreamGetPriority(c->stream, &prio));
+  APPO_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  const char* sp = getenv("APPO_SIDE_PRIO");
+  if (sp && sp[0] == '+' && prio < least) prio += 1;
+  if (sp && sp[0] == '-' && prio > greatest) prio -= 1;
+  APPO_CUDA_TRY(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio));
+  for (auto& e : c->side_ev) APPO_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return APPO_OK;
+}
+
+// record on `from`, wait on `to`
+static int side_edge(Ctx* c, cudaStream_t from, cudaStream_t to) {
+  cudaEvent_t e = c->side_ev[c->side_ev_next++ % Ctx::kSideEvents];
+  APPO_CUDA_TRY(cudaEventRecord(e, from));
+  APPO_CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
+  return APPO_OK;
+}
+
+// launches inside the scope go to the side stream with the side workspace
+struct OnSide {
+  Ctx* c;
+  cudaStream_t main_stream;
+  float* main_ws;
+  size_t main_ws_bytes;
+  explicit OnSide(Ctx* ctx) : c(ctx), main_stream(ctx->stream), main_ws(ctx->d_ws),
+                              main_ws_bytes(ctx->ws_bytes) {
+    c->stream = c->side_stream;
+    c->d_ws = c->side_ws;
+    c->ws_bytes = c->side_ws_bytes;
+  }
+  ~OnSide() {
+    c->side_ws = c->d_ws;
+    c->side_ws_bytes = c->ws_bytes;
+    c->stream = main_stream;
+    c->d_ws = main_ws;
+    c->ws_bytes = main_ws_bytes;
+  }
+};
+
 static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slot_bytes,
                                const int32_t* h_slot_ids, appo_slotq* rq, appo_slotq* fq,
                                int n_traj, const appo_hparams* hp) {
@@ -928,6 +984,18 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   }
   LossHP lh{hp->clip_low, hp->clip_high, hp->value_coef, hp->entropy_coef};
   float* G = M->grad;
+  // weight gradients on the side stream (ctx->fork), the
+  // input-gradient chain (and BPTT) on the main stream
+  const bool fork = seq && ctx->fork;
+  if (fork) TRY(side_init(ctx));
+  auto to_side = [&]() -> int {
+    return fork ? side_edge(ctx, ctx->stream, ctx->side_stream) : APPO_OK;
+  };
+  auto run_side = [&](auto&& f) -> int {
+    if (!fork) return f();
+    OnSide on(ctx);
+    return f();
+  };
   if (traj_loss_supported(n_traj, T, d.A, hp->normalize_adv != 0)) {
     // heads, targets, loss and heads backward fused per trajectory (traj_loss.cu)
     // no gradient memset on this path: every entry of G is written (not
@@ -939,7 +1007,15 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
                     th + d.off_bv, s.act, s.rew, s.blogp, s.done, s.ver, M->version, hp->gamma,
                     hp->rho_bar, hp->c_bar, gae, lam, lh, s.logits, s.values, s.vt, s.pg, s.adv,
                     s.dcore, s.colsum_part, s.stats, G + d.off_wpi, G + d.off_bpi, G + d.off_wv,
-                    G + d.off_bv));
+                    G + d.off_bv, !fork));
+    if (fork) {
+      // the head gradients' partial sums are reduced beside BPTT
+      TRY(to_side());
+      TRY(run_side([&]() -> int {
+        return k_heads_grad_reduce(ctx, d.A, n_traj, s.colsum_part, G + d.off_wpi,
+                                   G + d.off_bpi, G + d.off_wv, G + d.off_bv);
+      }));
+    }
   } else {
     TRY(k_heads_fwd(ctx, R, d.A, s.core, th + d.off_wpi, th + d.off_bpi, th + d.off_wv,
                     th + d.off_bv, s.logits, s.values, B, s.act, s.tlogp, s.ent));
@@ -1000,7 +1076,8 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
                     Operand{wb + d.off_whh, kHidden, true}, e, 64, 4));
     }
   }
-  {
+  TRY(to_side());  // dgi, dgh, GRU bias and head gradients are final
+  TRY(run_side([&]() -> int {
     // dW_ih = dgi^T x, dW_hh = dgh^T h_in, biases = column sums (64-wide N
     // tiles, no split-K: measured fastest at these shapes, scripts/gemm_sweep.py)
     Epilogue e;
@@ -1017,7 +1094,9 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     }
     // data-parallel bucket 1 (GRU + heads) is final: reduce it while the
     // encoder backward runs
-    TRY(dp_bucket(ctx, G + d.off_wih, d.total - d.off_wih));
+    return dp_bucket(ctx, G + d.off_wih, d.total - d.off_wih);
+  }));
+  {
     // dx = dgi . W_ih, times ELU'(fc) -> dz_fc
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
@@ -1037,12 +1116,17 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
                   Operand{wb + d.off_wih, kHidden, true}, x, 64));
   }
   // ---- FC backward ----
-  {
+  TRY(to_side());  // dz_fc and the fc bias gradient are final
+  TRY(run_side([&]() -> int {
     Epilogue e;
     e.out = G + d.off_fcw;
     e.ldo = d.F;
     TRY(gemm_bf16(ctx, kHidden, d.F, B, Operand{s.dzfc, kHidden, true},
                   Operand{s.a3, d.F, true}, e, 64, 1));
+    // bucket 2 (FC weight + bias) is final
+    return dp_bucket(ctx, G + d.off_fcw, d.off_wih - d.off_fcw);
+  }));
+  {
     Epilogue x;
     x.flags = EPI_DELU | EPI_BF16;
     x.aux = s.a3;
@@ -1059,12 +1143,13 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     TRY(gemm_bf16(ctx, B, d.F, kHidden, Operand{s.dzfc, kHidden, false},
                   Operand{wb + d.off_fcw, d.F, true}, x, 128));
   }
-  // bucket 2 (FC weight + bias) is final
-  TRY(dp_bucket(ctx, G + d.off_fcw, d.off_wih - d.off_fcw));
   // ---- conv3 backward ----
+  TRY(to_side());  // dz3 is final
+  TRY(run_side([&]() -> int {
+    return conv_taps_wgrad(ctx, s.a2, B, d.H2, d.W2, 64, s.dz3, d.H3, d.W3, 128, 3,
+                           G + d.off_c3w);
+  }));
   {
-    const int M3 = B * d.P3;
-    TRY(conv_taps_wgrad(ctx, s.a2, B, d.H2, d.W2, 64, s.dz3, d.H3, d.W3, 128, 3, G + d.off_c3w));
     // dz2 = ELU'(a2) * conv3^T(dz3): sub-pixel implicit GEMM (+ conv2 bias grad)
     DgradIn in;
     in.dz_next = s.dz3;
@@ -1077,19 +1162,22 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     TRY(conv_dgrad_s2_bf16(ctx, in));
   }
   // ---- conv2 backward ----
-  {
+  static const bool conv2_engine = [] {
+    const char* v = getenv("APPO_CONV2");
+    return v && v[0] == 'e';
+  }();
+  TRY(to_side());  // dz2 is final
+  TRY(run_side([&]() -> int {
     // weight gradient straight from a1 / dz2 (strided TMA windows, no col2)
-    static const bool wgrad2_engine = [] {
-      const char* v = getenv("APPO_CONV2");
-      return v && v[0] == 'e';
-    }();
-    const int w2st = wgrad2_engine ? APPO_ERR_CONTRACT
-                                   : conv2_wgrad(ctx, s.a1, B, d.H1, d.W1, s.dz2, d.H2, d.W2,
-                                                 G + d.off_c2w);
+    const int w2st = conv2_engine ? APPO_ERR_CONTRACT
+                                  : conv2_wgrad(ctx, s.a1, B, d.H1, d.W1, s.dz2, d.H2, d.W2,
+                                                G + d.off_c2w);
     if (w2st == APPO_ERR_CONTRACT)
-      TRY(conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, 32, s.dz2, d.H2, d.W2, 64, 4, G + d.off_c2w));
-    else if (w2st != APPO_OK)
-      return w2st;
+      return conv_taps_wgrad(ctx, s.a1, B, d.H1, d.W1, 32, s.dz2, d.H2, d.W2, 64, 4,
+                             G + d.off_c2w);
+    return w2st;
+  }));
+  {
     // dz1 = ELU'(a1) * conv2^T(dz2) (+ conv1 bias grad)
     DgradIn in;
     in.dz_next = s.dz2;
@@ -1100,11 +1188,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     in.Ho = d.H2; in.Wo = d.W2; in.Co = 64; in.Hi = d.H1; in.Wi = d.W1; in.N = 32; in.k = 4;
     in.bias = bias_out(3, G + d.off_c1b, 32);
     // shifted-view kernel (conv2.cu) at the Doom shape, else the engine path
-    static const bool dgrad_engine = [] {
-      const char* v = getenv("APPO_CONV2");
-      return v && v[0] == 'e';
-    }();
-    const int dst = dgrad_engine ? APPO_ERR_CONTRACT : conv2_dgrad(ctx, in);
+    const int dst = conv2_engine ? APPO_ERR_CONTRACT : conv2_dgrad(ctx, in);
     if (dst == APPO_ERR_CONTRACT)
       TRY(conv_dgrad_s2_bf16(ctx, in));
     else if (dst != APPO_OK)
@@ -1139,6 +1223,9 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   }
   // the slots are no longer read: hand them back (free list, orchestrator.hpp:870)
   if (fq) TRY(slotq_push_launch(ctx, fq, s.slot_ids, 0, n_traj, q_ok));
+
+  // join: every weight gradient is final before the reduction / optimizer
+  if (fork) TRY(side_edge(ctx, ctx->side_stream, ctx->stream));
 
   // ---- data-parallel: last bucket (convolutions) + rejection consensus;
   //      the averaged gradient is complete before clip + Adam ----

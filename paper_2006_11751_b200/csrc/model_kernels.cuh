@@ -78,7 +78,7 @@ int k_traj_loss(Ctx* c, int n_traj, int T, int A, const float* core, const float
                 int64_t cur_version, float gamma, float rho_bar, float c_bar, bool gae,
                 float lambda, const LossHP& hp, float* logits, float* values, float* vt, float* pg,
                 float* adv, float* dcore, float* part, double* stats, float* gwpi, float* gbpi,
-                float* gwv, float* gbv);
+                float* gwv, float* gbv, bool reduce_heads = true);
 int k_gru_bwd(Ctx* c, int n_traj, int T, int t, const float* dcore, const uint8_t* done,
               const float* gates, const float* hin, float* dnext, uint16_t* dgi, uint16_t* dgh);
 int k_colsum(Ctx* c, int64_t M, int N, const void* src, int64_t ld, bool bf16, float* part,

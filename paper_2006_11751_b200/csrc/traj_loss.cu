@@ -430,7 +430,7 @@ int k_traj_loss(Ctx* c, int n_traj, int T, int A, const float* core, const float
                 int64_t cur_version, float gamma, float rho_bar, float c_bar, bool gae,
                 float lambda, const LossHP& hp, float* logits, float* values, float* vt, float* pg,
                 float* adv, float* dcore, float* part, double* stats, float* gwpi, float* gbpi,
-                float* gwv, float* gbv) {
+                float* gwv, float* gbv, bool reduce_heads) {
   APPO_REQUIRE(traj_loss_supported(n_traj, T, A, false), APPO_ERR_CONTRACT,
                "traj_loss: outside the fused kernel's envelope");
   APPO_REQUIRE(((reinterpret_cast<uintptr_t>(core) | reinterpret_cast<uintptr_t>(wpi)) & 15) == 0,
@@ -488,6 +488,7 @@ int k_traj_loss(Ctx* c, int n_traj, int T, int A, const float* core, const float
   else
     APPO_LAUNCH(c, traj_loss_kernel<false>, n_traj, kTlThreads, kTlSmem, a);
   c->next_name = nullptr;
+  if (!reduce_heads) return APPO_OK;  // the caller launches it (learner side stream)
   return k_heads_grad_reduce(c, A, n_traj, part, gwpi, gbpi, gwv, gbv);
 }
 

@@ -275,6 +275,26 @@ def test_async_submit_collect_determinism_and_rejected_steps():
     assert torch.equal(a["logits"], b["logits"])
 
 
+@pytest.mark.parametrize("n_traj", [3, 64])
+def test_learner_fork_is_bitwise_neutral(n_traj):
+    # the weight gradients on the side stream write disjoint outputs with
+    # their own split-K workspace: same bits as the one-stream order
+    desc = appo.ModelDesc.doom()
+    store = appo.TrajectoryStore(desc, n_traj)
+    fill_store(store, n_traj, np.random.default_rng(14), 6)
+    hp = appo.HParams.defaults(lr=3e-4)
+    ref = appo.Context(0, seed=33, model=desc)
+    ref.set_learner_fork(False)
+    ctx = appo.Context(0, seed=33, model=desc)
+    ctx.set_learner_fork(True)
+    ids = list(range(n_traj))[::-1]
+    for _ in range(3):
+        a = ref.learner_step(store.region, store.slot_bytes, ids, hp)
+        b = ctx.learner_step(store.region, store.slot_bytes, ids, hp)
+        assert a["total_loss"] == b["total_loss"] and a["grad_norm"] == b["grad_norm"]
+    assert np.array_equal(ref.get_params()[0], ctx.get_params()[0])
+
+
 @pytest.mark.parametrize("pdl", [False, True])
 def test_programmatic_dependent_launch_is_bitwise_neutral(pdl):
     # every kernel waits on griddepcontrol before touching its predecessor's
