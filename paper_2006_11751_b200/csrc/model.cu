@@ -829,6 +829,15 @@ int appo_policy_forward(appo_ctx* ctx, int B, const uint8_t* d_obs, const float*
 // h_slot_ids != null: ids from the host (FIFO order given by the caller);
 // else ids popped on the device from rq (FIFO arrival order) and, when fq is
 // set, returned to fq after the last kernel reading the slots.
+// GEMM tile width override for A/B sweeps of the learner backward
+// (APPO_BN_<name>=32/64/128/192/256; unset = the measured default)
+static int bn_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !v[0]) return dflt;
+  const int b = atoi(v);
+  return (b == 32 || b == 64 || b == 128 || b == 192 || b == 256) ? b : dflt;
+}
+
 // ---- learner side stream ----
 // The backward's weight-gradient kernels (dW_ih, dW_hh, FC, conv3, conv2)
 // depend on the input-gradient chain (dx -> FC dgrad -> conv3 dgrad -> conv2
@@ -987,6 +996,8 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   // weight gradients on the side stream (ctx->fork), the
   // input-gradient chain (and BPTT) on the main stream
   const bool fork = seq && ctx->fork;
+  static const int bn_dw = bn_env("APPO_BN_DW", 64), bn_dx = bn_env("APPO_BN_DX", 64),
+                   bn_fcw = bn_env("APPO_BN_FCW", 64), bn_fcd = bn_env("APPO_BN_FCD", 128);
   if (fork) TRY(side_init(ctx));
   auto to_side = [&]() -> int {
     return fork ? side_edge(ctx, ctx->stream, ctx->side_stream) : APPO_OK;
@@ -1084,10 +1095,10 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     e.out = G + d.off_wih;
     e.ldo = kHidden;
     TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgi, kGates, true},
-                  Operand{s.x, kHidden, true}, e, 64, 1));
+                  Operand{s.x, kHidden, true}, e, bn_dw, 1));
     e.out = G + d.off_whh;
     TRY(gemm_bf16(ctx, kGates, kHidden, B, Operand{s.dgh, kGates, true},
-                  Operand{s.hbf, kHidden, true}, e, 64, 1));
+                  Operand{s.hbf, kHidden, true}, e, bn_dw, 1));
     if (!seq) {
       TRY(k_colsum(ctx, B, kGates, s.dgi, kGates, true, s.colsum_part, G + d.off_bih, false));
       TRY(k_colsum(ctx, B, kGates, s.dgh, kGates, true, s.colsum_part, G + d.off_bhh, false));
@@ -1113,7 +1124,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     }
     // 64-wide N tiles: 128 tiles instead of 64 on 148 SMs (22.8 -> 18.9 us measured)
     TRY(gemm_bf16(ctx, B, kHidden, kGates, Operand{s.dgi, kGates, false},
-                  Operand{wb + d.off_wih, kHidden, true}, x, 64));
+                  Operand{wb + d.off_wih, kHidden, true}, x, bn_dx));
   }
   // ---- FC backward ----
   TRY(to_side());  // dz_fc and the fc bias gradient are final
@@ -1122,7 +1133,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
     e.out = G + d.off_fcw;
     e.ldo = d.F;
     TRY(gemm_bf16(ctx, kHidden, d.F, B, Operand{s.dzfc, kHidden, true},
-                  Operand{s.a3, d.F, true}, e, 64, 1));
+                  Operand{s.a3, d.F, true}, e, bn_fcw, 1));
     // bucket 2 (FC weight + bias) is final
     return dp_bucket(ctx, G + d.off_fcw, d.off_wih - d.off_fcw);
   }));
@@ -1141,7 +1152,7 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
       x.bsum_mod = 128;
     }
     TRY(gemm_bf16(ctx, B, d.F, kHidden, Operand{s.dzfc, kHidden, false},
-                  Operand{wb + d.off_fcw, d.F, true}, x, 128));
+                  Operand{wb + d.off_fcw, d.F, true}, x, bn_fcd));
   }
   // ---- conv3 backward ----
   TRY(to_side());  // dz3 is final

@@ -19,4 +19,5 @@ ENVS=2048 timeout -s KILL 600 ncu --set full --clock-control none --import-sourc
 APPO_GRU_PROF=1 timeout -s KILL 120 python scripts/_prof_gru.py 2>&1 | grep "gru prof" > gpurun_out/final_gru_phases.txt
 KREGEX="traj_loss_kernel" NAME=final_traj_loss SKIP=2 COUNT=1 bash scripts/gpu_ncu_kernel.sh
 timeout -s KILL 300 python scripts/hbm_sweep.py > gpurun_out/final_hbm_sweep.jsonl 2>&1; echo "hbm sweep rc=$?"
+# (learner --set full capture: scripts/gpu_ncu_learner.sh, separate call: 64 MB report)
 ls -la gpurun_out | head -40
