@@ -522,7 +522,7 @@ def load_traffic(name):
     (profiles/traffic.json, scripts/traffic_summary.py); None if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f)["traffic_bytes_per_launch"].get(name)
+            return json.load(f)["traffic_bytes_per_launch"].get(name.split("@")[0])
     except Exception:
         return None
 

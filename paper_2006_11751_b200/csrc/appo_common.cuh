@@ -84,6 +84,7 @@ struct Ctx {
   // run here beside the input-gradient chain on `stream`, with their own
   // split-K workspace; fork/join by events
   bool fork = true;  // appo_ctx_set_learner_fork
+  bool on_side = false;  // launches go to side_stream (timing class name gets "@side")
   cudaStream_t side_stream = nullptr;
   static constexpr int kSideEvents = 16;
   cudaEvent_t side_ev[kSideEvents] = {};
@@ -187,8 +188,12 @@ cudaEvent_t timing_event(Ctx* c);
 // current device, once per (kernel, device): the attribute is per device, so a
 // process driving learners on several GPUs must set it on each.
 int ensure_smem_attr(const void* kernel, int bytes, int device);
+// interned "<name>@side": kernels on the learner side stream run beside the
+// main chain, so their event-timed durations are a separate timing class
+const char* side_class_name(const char* name);
 inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
   if (!c->timing) return nullptr;
+  if (c->on_side) name = side_class_name(name);
   // filter: one kernel class name, or several separated by '|'
   if (!c->timing_filter.empty() && c->timing_filter != "gemm_shapes" &&
       ("|" + c->timing_filter + "|").find("|" + std::string(name) + "|") == std::string::npos)
@@ -202,6 +207,7 @@ inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
 }
 inline void timing_end(Ctx* c, const char* name, cudaEvent_t a) {
   if (a) {
+    if (c->on_side) name = side_class_name(name);
     cudaEvent_t b = timing_event(c);
     cudaEventRecord(b, c->stream);
     c->timed.push_back(TimedLaunch{name, a, b, c->next_flops, c->next_bytes});

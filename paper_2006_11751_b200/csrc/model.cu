@@ -16,6 +16,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
+#include <string>
 #include <vector>
 
 #include "gemm.cuh"
@@ -505,6 +507,13 @@ int wait_readers(Model* M, cudaStream_t st, int k) {
   return APPO_OK;
 }
 
+const char* side_class_name(const char* name) {
+  static std::mutex mu;
+  static std::set<std::string> names;
+  std::lock_guard<std::mutex> lock(mu);
+  return names.insert(std::string(name) + "@side").first->c_str();
+}
+
 }  // namespace appo_b200
 
 using namespace appo_b200;
@@ -884,10 +893,12 @@ struct OnSide {
     c->stream = c->side_stream;
     c->d_ws = c->side_ws;
     c->ws_bytes = c->side_ws_bytes;
+    c->on_side = true;
   }
   ~OnSide() {
     c->side_ws = c->d_ws;
     c->side_ws_bytes = c->ws_bytes;
+    c->on_side = false;
     c->stream = main_stream;
     c->d_ws = main_ws;
     c->ws_bytes = main_ws_bytes;
