@@ -295,6 +295,26 @@ def test_learner_fork_is_bitwise_neutral(n_traj):
     assert np.array_equal(ref.get_params()[0], ctx.get_params()[0])
 
 
+def test_learner_fork_mixed_minibatch_sizes():
+    # steps alternating between the two-stream backward (64 trajectories,
+    # persistent GRU) and the one-stream path (65: non-persistent GRU) on the
+    # same context, queued asynchronously, match a one-stream context bit for bit
+    desc = appo.ModelDesc.doom()
+    store = appo.TrajectoryStore(desc, 65)
+    fill_store(store, 65, np.random.default_rng(15), 6)
+    hp = appo.HParams.defaults(lr=3e-4)
+    ref = appo.Context(0, seed=35, model=desc)
+    ref.set_learner_fork(False)
+    ctx = appo.Context(0, seed=35, model=desc)
+    ctx.set_learner_fork(True)
+    plans = [list(range(64)), list(range(65)), list(range(63, -1, -1)), list(range(1, 65))]
+    for c in (ref, ctx):
+        for ids in plans:
+            c.learner_submit(store.region, store.slot_bytes, ids, hp)
+        c.learner_collect()
+    assert np.array_equal(ref.get_params()[0], ctx.get_params()[0])
+
+
 @pytest.mark.parametrize("pdl", [False, True])
 def test_programmatic_dependent_launch_is_bitwise_neutral(pdl):
     # every kernel waits on griddepcontrol before touching its predecessor's
