@@ -34,7 +34,7 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint64_t seed = 0;
-  int* d_flags = nullptr;        // [kNumFlags]
+  int* d_flags = nullptr;        // [kNumFlags] live + [kNumFlags] frozen by the global norm
   double* d_red = nullptr;       // reduction workspace (partials), kRedSlots doubles
   unsigned* d_counter = nullptr; // last-block counters
   double* h_pinned = nullptr;    // small pinned readback buffer
@@ -91,6 +91,11 @@ struct Ctx {
   unsigned side_ev_next = 0;
   float* side_ws = nullptr;
   size_t side_ws_bytes = 0;
+  // the rest of a learner step's Adam (past the convolution parameters) runs
+  // on the side stream beside the next step's convolutions; that step joins
+  // adam_tail_ev before its FC forward
+  cudaEvent_t adam_tail_ev = nullptr;
+  bool adam_tail_pending = false;
 };
 constexpr int kRedSlots = 148 * 8 * 16;
 
@@ -191,6 +196,14 @@ int ensure_smem_attr(const void* kernel, int bytes, int device);
 // interned "<name>@side": kernels on the learner side stream run beside the
 // main chain, so their event-timed durations are a separate timing class
 const char* side_class_name(const char* name);
+// host-side wait for everything this context enqueued (main + side stream)
+inline cudaError_t ctx_streams_sync(Ctx* c) {
+  if (c->side_stream) {
+    const cudaError_t e = cudaStreamSynchronize(c->side_stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaStreamSynchronize(c->stream);
+}
 inline cudaEvent_t timing_begin(Ctx* c, const char* name) {
   if (!c->timing) return nullptr;
   if (c->on_side) name = side_class_name(name);
@@ -276,6 +289,11 @@ int launch_sample(Ctx* c, int B, const HeadsSpec& hs, const float* logits, uint6
 int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
                 float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
                 uint16_t* bf16_copy, float* f32_copy, unsigned* applied,
-                const int* peer_flags = nullptr);
+                const int* peer_flags = nullptr, int64_t n_head = -1);
+// n_head >= 0 above: Adam ran over [0, n_head) only; this runs it over
+// [lo, n) with the same norm and frozen accept/reject decision
+int launch_adam_rest(Ctx* c, int64_t n, int64_t lo, float* theta, float* m, float* v,
+                     const float* g, int64_t t, float lr, float b1, float b2, float eps,
+                     double* d_norm_out, uint16_t* bf16_copy, float* f32_copy);
 
 }  // namespace appo_b200

@@ -92,7 +92,7 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
   if (c->num_sms <= 0) c->num_sms = 148;
   c->pdl = pdl_default(false);
   c->fork = learner_fork_default();
-  if (cudaMalloc(&c->d_flags, sizeof(int) * kNumFlags) != cudaSuccess ||
+  if (cudaMalloc(&c->d_flags, sizeof(int) * 2 * kNumFlags) != cudaSuccess ||
       cudaMalloc(&c->d_red, sizeof(double) * kRedSlots) != cudaSuccess ||
       cudaMalloc(&c->d_counter, sizeof(unsigned) * 16) != cudaSuccess ||
       cudaMallocHost(&c->h_pinned, sizeof(double) * 64) != cudaSuccess) {
@@ -100,7 +100,7 @@ int appo_ctx_create(const appo_model_desc* desc, int device, uint64_t seed, appo
     delete c;
     return APPO_ERR_RESOURCE;
   }
-  cudaMemset(c->d_flags, 0, sizeof(int) * kNumFlags);
+  cudaMemset(c->d_flags, 0, sizeof(int) * 2 * kNumFlags);
   cudaMemset(c->d_counter, 0, sizeof(unsigned) * 16);
   cudaDeviceSynchronize();
   if (desc) {
@@ -159,6 +159,7 @@ int appo_ctx_destroy(appo_ctx* ctx) {
     cudaStreamSynchronize(ctx->side_stream);
     cudaStreamDestroy(ctx->side_stream);
   }
+  if (ctx->adam_tail_ev) cudaEventDestroy(ctx->adam_tail_ev);
   for (auto e : ctx->side_ev)
     if (e) cudaEventDestroy(e);
   cudaFree(ctx->side_ws);
@@ -193,10 +194,10 @@ int appo_ctx_sync(appo_ctx* ctx) {
   int flags[kNumFlags];
   APPO_CUDA_TRY(cudaMemcpyAsync(flags, ctx->d_flags, sizeof(flags), cudaMemcpyDeviceToHost,
                                 ctx->stream));
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   if (flags[kFlagNumeric] || flags[kFlagContract] || flags[kFlagQueue]) {
     APPO_CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(flags), ctx->stream));
-    APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    APPO_CUDA_TRY(ctx_streams_sync(ctx));
     if (flags[kFlagQueue]) {
       set_error("slot queue: timed out waiting on the device for published slot ids");
       return APPO_ERR_RESOURCE;
@@ -215,7 +216,7 @@ int64_t appo_ctx_launch_count(appo_ctx* ctx) { return ctx ? ctx->launches : -1; 
 
 int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter) {
   CTX_OR_RETURN(ctx);
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   ctx->timing = enable != 0;
   std::string f = name_filter ? name_filter : "";
   ctx->timing_stride = 1;
@@ -236,7 +237,7 @@ int appo_ctx_set_timing(appo_ctx* ctx, int enable, const char* name_filter) {
 // {"name":..,"launches":..,"ms":..,"flops":..,"bytes":..}.  Synchronizes.
 int appo_ctx_timing_report(appo_ctx* ctx, char* buf, int buflen) {
   CTX_OR_RETURN(ctx);
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   struct Agg {
     std::string name;
     long n = 0;

@@ -311,7 +311,7 @@ ConvIn conv1_in(const ObsSrc& src, int R, const Dims& d) {
 
 int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, const uint16_t* wb,
                     const float* pf, int pub, bool implicit, bool conv2_implicit,
-                    bool gate_proj = true) {
+                    bool gate_proj = true, cudaEvent_t join_before_fc = nullptr) {
   const Dims& d = M->d;
   Epilogue e;
   // conv1: [R*P1, 32] = (1024 + obs) . W1h^T / 255 + bias' (fp16 operands,
@@ -375,6 +375,9 @@ int encoder_forward(Ctx* c, Model* M, Scratch& s, const ObsSrc& src, int R, cons
     TRY(gemm_bf16(c, R * d.P3, 128, 576, Operand{s.col3, 576, false},
                   Operand{wb + d.off_c3w, 576, false}, e, 128));
   }
+  // the previous learner step's Adam over the FC / GRU / head parameters
+  // (side stream) is complete before anything reads them
+  if (join_before_fc) APPO_CUDA_TRY(cudaStreamWaitEvent(c->stream, join_before_fc, 0));
   e.bias = pf + d.off_fcb;
   e.out = s.x;
   e.ldo = kHidden;
@@ -627,7 +630,7 @@ int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version) {
   for (int k = 0; k < Model::kPub; ++k)
     TRY(k_publish_derived(ctx, M->pub_bf16[k], M->pub_f32[k], M->d, M->pub_c1h[k], M->pub_c1b[k],
                           M->pub_wt2[k], M->pub_wt3[k]));
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   M->version = version;
   M->adam_t = 0;
   M->published = 0;
@@ -639,7 +642,7 @@ int appo_params_set(appo_ctx* ctx, const float* h_src, int64_t version) {
 int appo_params_get(appo_ctx* ctx, float* h_dst, int64_t* version_out) {
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   if (h_dst)
     APPO_CUDA_TRY(cudaMemcpy(h_dst, M->theta, M->d.total * 4, cudaMemcpyDeviceToHost));
   if (version_out) *version_out = M->version;
@@ -649,7 +652,7 @@ int appo_params_get(appo_ctx* ctx, float* h_dst, int64_t* version_out) {
 int appo_adam_get(appo_ctx* ctx, float* h_m, float* h_v, int64_t* t_out) {
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   if (h_m) APPO_CUDA_TRY(cudaMemcpy(h_m, M->m, M->d.total * 4, cudaMemcpyDeviceToHost));
   if (h_v) APPO_CUDA_TRY(cudaMemcpy(h_v, M->v, M->d.total * 4, cudaMemcpyDeviceToHost));
   if (t_out) *t_out = M->adam_t;
@@ -659,7 +662,7 @@ int appo_adam_get(appo_ctx* ctx, float* h_m, float* h_v, int64_t* t_out) {
 int appo_adam_set(appo_ctx* ctx, const float* h_m, const float* h_v, int64_t t) {
   MODEL_OR_RETURN(ctx);
   Model* M = ctx->model;
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   if (h_m) APPO_CUDA_TRY(cudaMemcpy(M->m, h_m, M->d.total * 4, cudaMemcpyHostToDevice));
   if (h_v) APPO_CUDA_TRY(cudaMemcpy(M->v, h_v, M->d.total * 4, cudaMemcpyHostToDevice));
   M->adam_t = t;
@@ -709,7 +712,7 @@ int appo_params_copy(appo_ctx* dst, appo_ctx* src) {
   // src's published state is final once its stream drained (its version and
   // adam_t are host values advanced at submit)
   APPO_CUDA_TRY(cudaSetDevice(src->device));
-  APPO_CUDA_TRY(cudaStreamSynchronize(src->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(src));
   APPO_CUDA_TRY(cudaSetDevice(dst->device));
   cudaStream_t st = dst->stream;
   const int next = (D->published + 1) % Model::kPub;
@@ -745,7 +748,7 @@ int appo_params_export(appo_ctx* ctx, void* handle_out) {
   Model* M = ctx->model;
   APPO_REQUIRE(M->pending == 0, APPO_ERR_CONTRACT,
                "params_export: collect the learner steps first");
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the exported state is final
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));  // the exported state is final
   StateHandle h{};
   h.magic = kStateMagic;
   h.pid = (int64_t)getpid();
@@ -871,6 +874,7 @@ static int side_init(Ctx* c) {
   if (sp && sp[0] == '-' && prio > greatest) prio -= 1;
   APPO_CUDA_TRY(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio));
   for (auto& e : c->side_ev) APPO_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  APPO_CUDA_TRY(cudaEventCreateWithFlags(&c->adam_tail_ev, cudaEventDisableTiming));
   return APPO_OK;
 }
 
@@ -982,7 +986,10 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   src.obs_dim = d.obs_dim;
   // learner: every convolution gathers its input by TMA (so do the weight
   // gradients: conv1_wgrad_implicit, conv_taps_wgrad) -- no im2col matrices
-  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false, /*learner=*/true));
+  cudaEvent_t tail = ctx->adam_tail_pending ? ctx->adam_tail_ev : nullptr;
+  ctx->adam_tail_pending = false;
+  TRY(encoder_forward(ctx, M, s, src, R, wb, th, pub, /*implicit=*/false, /*learner=*/true,
+                      /*gate_proj=*/true, tail));
 
   // ---- GRU unrolled over T steps (+ bootstrap step) ----
   const bool seq = gru_seq_supported(n_traj);
@@ -1258,14 +1265,36 @@ static int learner_submit_impl(appo_ctx* ctx, const void* d_region, uint64_t slo
   M->adam_t += 1;
   TRY(launch_adam(ctx, d.total, M->theta, M->m, M->v, G, M->adam_t, hp->lr, hp->beta1,
                   hp->beta2, hp->eps, hp->grad_clip, s.stats + 8, M->pub_bf16[next],
-                  M->pub_f32[next], ctx->d_counter + 6, peer_flags));
+                  M->pub_f32[next], ctx->d_counter + 6, peer_flags,
+                  fork ? d.off_fcw : -1));
   TRY(k_publish_derived(ctx, M->pub_bf16[next], M->pub_f32[next], d, M->pub_c1h[next],
                         M->pub_c1b[next], M->pub_wt2[next], M->pub_wt3[next]));
-  APPO_CUDA_TRY(cudaEventRecord(M->ready_ev[next], st));
+  // two-stream tail: the next step's convolutions need only the convolution
+  // parameters (updated above with their derived operands); Adam over the rest
+  // runs on the side stream beside them and the next step joins before its FC
+  // forward.  The published copy, the statistics and the step's ring event
+  // follow the side stream.
+  cudaStream_t tail_st = st;
+  if (fork) {
+    TRY(side_edge(ctx, ctx->stream, ctx->side_stream));
+    {
+      OnSide on(ctx);
+      TRY(launch_adam_rest(ctx, d.total, d.off_fcw, M->theta, M->m, M->v, G, M->adam_t, hp->lr,
+                           hp->beta1, hp->beta2, hp->eps, s.stats + 8, M->pub_bf16[next],
+                           M->pub_f32[next]));
+    }
+    tail_st = ctx->side_stream;
+  }
+  APPO_CUDA_TRY(cudaEventRecord(M->ready_ev[next], tail_st));
   // statistics back to the host after the kernels (a copy node between two
   // kernels would end their PDL overlap)
-  APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost, st));
-  APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], st));
+  APPO_CUDA_TRY(cudaMemcpyAsync(h_st, s.stats, sizeof(double) * 10, cudaMemcpyDeviceToHost,
+                                tail_st));
+  APPO_CUDA_TRY(cudaEventRecord(M->ring_ev[ring], tail_st));
+  if (fork) {  // after the statistics copy: the next step rewrites them
+    APPO_CUDA_TRY(cudaEventRecord(ctx->adam_tail_ev, ctx->side_stream));
+    ctx->adam_tail_pending = true;
+  }
   M->last_ring = ring;
   // Optimistic publish: the Adam kernel always rewrites pub[next] (with the
   // unchanged parameters when the step is rejected); readers on other streams
@@ -1350,7 +1379,7 @@ extern "C" int appo_dbg_copy_d2h(appo_ctx* ctx, void* h_dst, const void* d_src, 
   APPO_REQUIRE(ctx != nullptr, APPO_ERR_CONTRACT, "null ctx");
   APPO_CUDA_TRY(cudaSetDevice(ctx->device));
   APPO_CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  APPO_CUDA_TRY(ctx_streams_sync(ctx));
   return APPO_OK;
 }
 
@@ -1388,7 +1417,7 @@ extern "C" int appo_dbg_traj_loss(appo_ctx* ctx, int n_traj, int T, int A, const
   if (st == APPO_OK) {
     APPO_CUDA_TRY(cudaMemcpyAsync(h_stats8, stats, sizeof(double) * 8, cudaMemcpyDeviceToHost,
                                   ctx->stream));
-    APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    APPO_CUDA_TRY(ctx_streams_sync(ctx));
   }
   cudaFree(stats);
   cudaFree(ver);
@@ -1417,7 +1446,7 @@ extern "C" int appo_dbg_ppo_loss(appo_ctx* ctx, int B, int A, const float* d_log
   if (st == APPO_OK) {
     APPO_CUDA_TRY(cudaMemcpyAsync(h_stats8, stats, sizeof(double) * 8, cudaMemcpyDeviceToHost,
                                   ctx->stream));
-    APPO_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    APPO_CUDA_TRY(ctx_streams_sync(ctx));
   }
   cudaFree(dhead);
   cudaFree(stats);

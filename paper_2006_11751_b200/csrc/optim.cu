@@ -72,6 +72,11 @@ __global__ void __launch_bounds__(256)
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
     __syncthreads();
   }
+  // the step's accept/reject decision, frozen here for both Adam launches
+  // (the rest of Adam may run on the learner side stream after the next
+  // step's first kernels have raised flags of their own)
+  if (last && threadIdx.x < kNumFlags)
+    flags[kNumFlags + threadIdx.x] = ((volatile int*)flags)[threadIdx.x];
   if (last && threadIdx.x == 0) {
     double s = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
@@ -156,22 +161,40 @@ __global__ void __launch_bounds__(256)
 // module anchor for preload_library_kernels (slotq.cu)
 const void* kanchor_optim() { return reinterpret_cast<const void*>(&sumsq_kernel); }
 
-int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
-                float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
-                uint16_t* bf16_copy, float* f32_copy, unsigned* applied, const int* peer_flags) {
-  if (n == 0) return APPO_OK;
-  const int grid = 148 * 4;  // partials fit kRedSlots; enough loads in flight for HBM
-  c->next_bytes = (double)n * 4;
-  APPO_LAUNCH(c, sumsq_kernel, grid, 256, 0, n, g, c->d_red, c->d_counter + 1, d_norm_out, clip,
-              c->d_flags, peer_flags);
+static int adam_range(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g,
+                      int64_t t, float lr, float b1, float b2, float eps, double* d_norm_out,
+                      uint16_t* bf16_copy, float* f32_copy, unsigned* applied) {
+  if (n <= 0) return APPO_OK;
   const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
   const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
   const int64_t nv = (n + 3) / 4;  // float4 groups (the kernel falls back to scalars if unaligned)
   const int grid2 = (int)((nv + 255) / 256 < 148 * 16 ? (nv + 255) / 256 : 148 * 16);
   c->next_bytes = (double)n * (4 + 24 + (bf16_copy ? 2 : 0) + (f32_copy ? 4 : 0));
   APPO_LAUNCH(c, adam_kernel, grid2, 256, 0, n, theta, m, v, g, d_norm_out, lr, b1, b2, eps, bc1,
-              bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags, applied);
+              bc2, reinterpret_cast<__nv_bfloat16*>(bf16_copy), f32_copy, c->d_flags + kNumFlags,
+              applied);
   return APPO_OK;
+}
+
+int launch_adam_rest(Ctx* c, int64_t n, int64_t lo, float* theta, float* m, float* v,
+                     const float* g, int64_t t, float lr, float b1, float b2, float eps,
+                     double* d_norm_out, uint16_t* bf16_copy, float* f32_copy) {
+  return adam_range(c, n - lo, theta + lo, m + lo, v + lo, g + lo, t, lr, b1, b2, eps, d_norm_out,
+                    bf16_copy ? bf16_copy + lo : nullptr, f32_copy ? f32_copy + lo : nullptr,
+                    nullptr);
+}
+
+int launch_adam(Ctx* c, int64_t n, float* theta, float* m, float* v, const float* g, int64_t t,
+                float lr, float b1, float b2, float eps, float clip, double* d_norm_out,
+                uint16_t* bf16_copy, float* f32_copy, unsigned* applied, const int* peer_flags,
+                int64_t n_head) {
+  if (n == 0) return APPO_OK;
+  const int grid = 148 * 4;  // partials fit kRedSlots; enough loads in flight for HBM
+  c->next_bytes = (double)n * 4;
+  APPO_LAUNCH(c, sumsq_kernel, grid, 256, 0, n, g, c->d_red, c->d_counter + 1, d_norm_out, clip,
+              c->d_flags, peer_flags);
+  return adam_range(c, n_head >= 0 && n_head < n ? n_head : n, theta, m, v, g, t, lr, b1, b2, eps,
+                    d_norm_out, bf16_copy, f32_copy, applied);
 }
 
 }  // namespace appo_b200
